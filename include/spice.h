@@ -1,0 +1,222 @@
+/*
+ * spice.h — C ABI of the B200-native Spice hot path (arXiv 2102.04681).
+ *
+ * One network slice per process and GPU ("each GPU is responsible for delivering all
+ * spikes to its neurons via its synapses", §III-D).  The calls below are
+ * the four north-star entry points (create / step / read_spikes / free) plus parity
+ * and debug hooks used by the tests.  Plain C types only; no torch types.
+ *
+ * Conventions (all functions):
+ *   - Return a spice_status; never throw, exit or abort.  On failure
+ *     spice_last_error() (thread-local) holds a message naming the rank and step.
+ *   - After SPICE_ECUDA or SPICE_ENCCL the handle is poisoned: every call except
+ *     spice_free returns SPICE_ESTATE.
+ *   - The library owns every device allocation it makes; callers own host buffers.
+ *   - "global ID" = neuron index in [0, n_neurons); "local index" = position of an
+ *     owned neuron in Listing 1 order: j = (i/S*G + g)*S + i%S.
+ *   - All calls on one handle must come from one host thread.
+ */
+#ifndef SPICE_H
+#define SPICE_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPICE_ABI_VERSION 1u
+
+#if defined(__GNUC__)
+#define SPICE_API __attribute__((visibility("default")))
+#else
+#define SPICE_API
+#endif
+
+typedef struct spice_net spice_net;   /* opaque; owned by the library */
+
+typedef enum {
+    SPICE_OK = 0,
+    SPICE_EINVAL = 1,   /* invalid configuration or argument */
+    SPICE_ENOMEM = 2,   /* device or host allocation failed (message names the buffer) */
+    SPICE_ECUDA = 3,    /* CUDA runtime error; handle poisoned */
+    SPICE_ENCCL = 4,    /* NCCL error; handle poisoned */
+    SPICE_ERANGE = 5,   /* requested steps are outside the spike record ring */
+    SPICE_ETRUNC = 6,   /* output buffer too small; *total holds the size needed */
+    SPICE_ESTATE = 7    /* handle poisoned or call not valid in the current state */
+} spice_status;
+
+/* Neuron models (§IV: Vogels, Brunel, Brunel+, Synth). */
+enum { SPICE_VOGELS = 1, SPICE_BRUNEL = 2, SPICE_BRUNEL_PLUS = 3, SPICE_SYNTH = 4 };
+
+/* Connectivity rule kinds.  FIXED_PROB is the paper's descriptor entry
+ * {range1, range2, p} (§III-B): edge s->j iff
+ * Philox4x32-10(ctr = (s, j>>2, rule index, 1), key = seed)[j&3] < floor(p 2^32).
+ * FIXED_INDEGREE (the BASELINE synth rule): target j draws k sources
+ * src_begin + floor(r64 |src| / 2^64), r64 from Philox(ctr = (j, k>>1, rule, 2)). */
+enum { SPICE_FIXED_PROB = 0, SPICE_FIXED_INDEGREE = 1 };
+
+/* Flags */
+#define SPICE_FLAG_EXTERNAL_EXCHANGE 0x1u  /* G > 1 without NCCL: the caller moves bitmaps
+                                              between spice_exchange_begin / _end */
+#define SPICE_FLAG_GLOBAL_ATOMICS    0x2u  /* deliver with the paper-style column-wise
+                                              warps and global atomics (A/B baseline) */
+
+typedef struct {
+    uint32_t src_begin, src_end;   /* range1, half-open global IDs */
+    uint32_t dst_begin, dst_end;   /* range2, half-open global IDs */
+    uint32_t kind;                 /* SPICE_FIXED_PROB | SPICE_FIXED_INDEGREE */
+    uint32_t k;                    /* in-degree for FIXED_INDEGREE */
+    uint32_t plastic;              /* 1: STDP synapses (Brunel+ E->E only) */
+    uint32_t reserved;
+    double   p;                    /* probability for FIXED_PROB */
+} spice_rule;
+
+/* Model constant vectors (model_params), in order:
+ *  VOGELS     [tau_m, E_L, V_t, V_r, t_ref, E_e, E_i, tau_e, tau_i, dg_e, dg_i,
+ *              v_lo, v_hi, ge_lo, ge_hi, gi_lo, gi_hi]                   (17)
+ *  BRUNEL     [tau_m, V_L, theta, V_r, t_ref, J_E, g, lambda_ext, v_lo, v_hi]  (10)
+ *  BRUNEL_PLUS BRUNEL + [tau_plus, tau_minus, A_plus, A_minus, w_max, w0]    (16)
+ *  SYNTH      []  (uses `activity`)
+ * Times in ms, potentials in mV, conductances in units of g_L. */
+typedef struct {
+    uint32_t abi_version;          /* SPICE_ABI_VERSION */
+    uint32_t model;
+    uint32_t n_neurons;            /* N */
+    uint32_t n_exc;                /* [0, n_exc) excitatory; n_exc == N: one population */
+    const spice_rule *rules;       /* copied during create */
+    uint32_t n_rules;
+    uint32_t delay_steps;          /* uniform synaptic delay >= 1 */
+    double   dt_ms;
+    uint64_t seed;                 /* Philox key = (seed lo, seed hi) */
+    double   activity;             /* SYNTH per-step firing probability */
+    const double *model_params;    /* copied during create */
+    uint32_t n_model_params;
+    uint32_t rank, world_size;     /* this slice g and the GPU count G */
+    uint32_t slice_width;          /* S, multiple of 32; 0 = spice_default_slice_width */
+    int32_t  device;               /* CUDA device ordinal */
+    const void *nccl_unique_id;    /* 128-byte ncclUniqueId from rank 0; required when
+                                      world_size > 1 unless EXTERNAL_EXCHANGE */
+    uint32_t record_steps;         /* spike record ring length in steps (>= 1) */
+    uint32_t flags;                /* SPICE_FLAG_* */
+    uint32_t tile_width;           /* targets per delivery tile (multiple of 32,
+                                      <= 49152); 0 = auto */
+    uint32_t ctas_per_tile;        /* CTAs sharing one tile (>= 1); 0 = auto */
+} spice_config;
+
+/* Create this rank's slice: expand the descriptor restricted to owned targets on the
+ * GPU, allocate state, input ring, spike lists and the record
+ * ring.  Collective over the world when world_size > 1 (NCCL communicator init).
+ * Errors: EINVAL (N = 0, p outside [0,1], ranges outside [0,N), delay 0, rules of one
+ * source with overlapping destination ranges, a fixed-in-degree segment too long to
+ * sort, ...), ENOMEM, ECUDA, ENCCL.  *out is NULL on failure. */
+SPICE_API spice_status spice_create_network(const spice_config *cfg, spice_net **out);
+
+/* Enqueue n_steps lock-step simulation steps on the library stream (CUDA-graph replay;
+ * update -> [all-gather] -> deliver per step).  Returns after enqueueing. */
+SPICE_API spice_status spice_step(spice_net *net, uint64_t n_steps);
+
+/* Copy the spikes of steps [t_begin, t_end) to the host (synchronises the stream).
+ * ids receives global IDs, ascending within each step, the same list on every rank;
+ * offsets (t_end - t_begin + 1 entries) receives per-step starts.  ERANGE if a step is
+ * not in the record ring (older than record_steps or not yet simulated); ETRUNC if cap
+ * is too small (then *total = spikes needed, nothing else written). */
+SPICE_API spice_status spice_read_spikes(spice_net *net, uint64_t t_begin, uint64_t t_end,
+                               uint32_t *ids, uint64_t cap, uint64_t *offsets,
+                               uint64_t *total);
+
+/* Release everything.  NULL-safe.  Collective when an NCCL communicator exists. */
+SPICE_API spice_status spice_free(spice_net *net);
+
+/* ---------------------------- parity / debug hooks --------------------------- */
+
+/* Rows [row_begin, row_end) (global source IDs) of this rank's synapses, as global
+ * target IDs ascending within each row.  row_offsets has row_end - row_begin + 1
+ * entries.  ETRUNC semantics as in spice_read_spikes. */
+SPICE_API spice_status spice_read_connectivity(spice_net *net, uint32_t row_begin, uint32_t row_end,
+                                     uint32_t *tgt_global, uint64_t cap,
+                                     uint64_t *row_offsets, uint64_t *total);
+
+/* Fields of the owned neurons in local order (n = owned count):
+ * 0 v (f32), 1 ge (f32), 2 gi (f32), 3 refractory counter (u32), 4 synth accumulator
+ * (u32), 5 pre trace x (f32), 6 post trace y (f32). EINVAL for a field the model lacks. */
+enum { SPICE_FIELD_V = 0, SPICE_FIELD_GE = 1, SPICE_FIELD_GI = 2, SPICE_FIELD_REF = 3,
+       SPICE_FIELD_ACC = 4, SPICE_FIELD_XTR = 5, SPICE_FIELD_YTR = 6 };
+SPICE_API spice_status spice_read_state(spice_net *net, uint32_t field, void *host_out, uint64_t n);
+SPICE_API spice_status spice_write_state(spice_net *net, uint32_t field, const void *host_in, uint64_t n);
+
+/* Input slot that the update of step (t_now + rel) reads, rel in [0, delay]: packed
+ * receptor counts (exc in bits 0-15, inh in bits 16-31; one population: all 32 bits)
+ * and, for Brunel+, plastic fixed-point sums rint(w 2^32) (plastic may be NULL). */
+SPICE_API spice_status spice_read_input(spice_net *net, uint32_t rel, uint32_t *counts,
+                              int64_t *plastic, uint64_t n);
+
+/* Plastic weights of this rank's synapses in the order of spice_read_connectivity for
+ * rows [row_begin, row_end); non-plastic synapses read as 0.  ETRUNC as above. */
+SPICE_API spice_status spice_read_weights(spice_net *net, uint32_t row_begin, uint32_t row_end,
+                                float *w, uint64_t cap, uint64_t *total);
+
+/* Teacher forcing of the next step: mode 1 replaces its spike set by the owned
+ * neurons among ids (global IDs), mode 2 adds them to the natural set. */
+SPICE_API spice_status spice_force_spikes(spice_net *net, const uint32_t *ids, uint64_t n, int mode);
+
+/* Counters since create (synchronises): steps done, spikes emitted by owned neurons,
+ * synaptic events delivered to owned neurons. */
+SPICE_API spice_status spice_stats(spice_net *net, uint64_t *steps, uint64_t *fired,
+                         uint64_t *delivered);
+
+/* The cudaStream_t the library enqueues on (for CUDA-event timing by the caller). */
+SPICE_API void *spice_stream(spice_net *net);
+
+/* Synchronise the library stream. */
+SPICE_API spice_status spice_sync(spice_net *net);
+
+/* Sizes of this slice: owned neurons, synapses, delivery tiles, device bytes held. */
+SPICE_API spice_status spice_info(spice_net *net, uint64_t *n_owned, uint64_t *n_synapses,
+                        uint32_t *n_tiles, uint32_t *tile_width, uint32_t *ctas_per_tile,
+                        uint64_t *device_bytes);
+
+/* Run n_steps steps with each kernel launched individually and bracketed by CUDA events
+ * on the library stream; writes the average device time per launch in ms:
+ * [0] neuron update, [1] spike delivery, [2] bitmap->list (G > 1), [3] NCCL all-gather
+ * (G > 1).  *n_kernels = entries written (cap >= 4).  Synchronises. */
+SPICE_API spice_status spice_profile(spice_net *net, uint64_t n_steps, double *ms_per_kernel,
+                                     uint32_t cap, uint32_t *n_kernels);
+
+/* Number of kernels the library launches per simulated step (evidence for benches). */
+SPICE_API uint32_t spice_kernels_per_step(spice_net *net);
+
+/* Thread-local message of the last failing call ("" if none). */
+SPICE_API const char *spice_last_error(void);
+
+/* ------------------------- multi-GPU plumbing -------------------------------- */
+
+/* Fill 128 bytes with a fresh ncclUniqueId (rank 0 only; broadcast it yourself). */
+SPICE_API spice_status spice_nccl_unique_id(void *out128);
+
+/* External exchange (SPICE_FLAG_EXTERNAL_EXCHANGE; used for single-GPU "virtual rank"
+ * tests): begin enqueues the neuron update of the next step, leaving this rank's spike
+ * bitmap (words_per_rank u32 words) in the send buffer; the caller must fill the receive
+ * buffer (world_size * words_per_rank words, rank r at offset r * words_per_rank) and
+ * then call end, which enqueues bitmap->list conversion and delivery. */
+SPICE_API spice_status spice_exchange_begin(spice_net *net);
+SPICE_API spice_status spice_exchange_end(spice_net *net);
+/* Device-to-device copy of src's send buffer into dst's receive segment for src's rank
+ * (both handles on the same device; ordered after src's update; returns when done). */
+SPICE_API spice_status spice_exchange_put(spice_net *dst, spice_net *src);
+
+/* ------------------- static partition (host-only, no GPU needed) -------------- */
+/* PAPER.md §III-F P:376 strided slices, Listing 1 P:496 (reading R1). */
+SPICE_API uint32_t spice_partition_owner(uint64_t j, uint32_t world_size, uint32_t slice_width);
+SPICE_API uint64_t spice_partition_local_to_global(uint64_t i, uint32_t rank, uint32_t world_size,
+                                         uint32_t slice_width);
+SPICE_API uint64_t spice_partition_owned_count(uint64_t n, uint32_t rank, uint32_t world_size,
+                                     uint32_t slice_width);
+/* Default S: a multiple of 32 giving each rank >= ~100 slices when N allows. */
+SPICE_API uint32_t spice_default_slice_width(uint64_t n, uint32_t world_size);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPICE_H */

@@ -1,0 +1,788 @@
+// abi.cu — network object, memory plan, CUDA-graph step loop and the C ABI of
+// include/spice.h.  Host-side runtime of the B200 Spice hot path.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "spice.h"
+#include "spice_internal.cuh"
+#include "spice_launch.h"
+
+using namespace spice;
+
+namespace {
+
+thread_local std::string g_err;
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi &nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void *h = nullptr;
+    const char *env = getenv("SPICE_NCCL_LIB");
+    if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+    api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.AllReduce &&
+             api.CommDestroy && api.GetErrorString;
+    return api;
+}
+
+uint64_t owned_count(uint64_t n, uint32_t g, uint32_t G, uint32_t S) {
+    const uint64_t full = n / ((uint64_t)S * G);           // complete rounds of G slices
+    uint64_t c = full * S;
+    const uint64_t rem = n - full * S * G;                 // neurons in the last round
+    const uint64_t start = (uint64_t)g * S;
+    if (rem > start) c += std::min<uint64_t>(S, rem - start);
+    return c;
+}
+
+uint64_t prob_threshold(double p) {
+    if (p <= 0.0) return 0;
+    if (p >= 1.0) return 1ull << 32;
+    return (uint64_t)std::floor(p * 4294967296.0);
+}
+
+// Poisson inversion table T_k = floor(2^32 F(k)) (reading R12; same formula as the
+// oracle, written independently): p0 = exp(-lambda), p_k = p_{k-1} lambda / k.
+std::vector<uint64_t> poisson_table(double lambda) {
+    std::vector<uint64_t> t;
+    double pk = std::exp(-lambda), F = pk;
+    for (uint32_t k = 0; k < 4096; ++k) {
+        const double T = std::floor(F * 4294967296.0);
+        if (T >= 4294967295.0) { t.push_back(1ull << 32); return t; }
+        t.push_back((uint64_t)T);
+        pk = pk * lambda / (double)(k + 1);
+        F = F + pk;
+    }
+    return {};
+}
+
+}  // namespace
+
+struct spice_net {
+    // configuration
+    uint32_t model = 0, N = 0, n_exc = 0, delay = 0, D = 0, rank = 0, G = 1, S = 32, flags = 0;
+    uint32_t R = 1;   // record steps
+    double dt = 0.1, activity = 0;
+    uint64_t seed = 0;
+    std::vector<double> prm;
+    std::vector<spice_rule> rules;
+    int device = 0, n_sm = 148;
+    cudaStream_t stream = nullptr;
+    bool poisoned = false;
+    bool external = false;
+    // geometry
+    uint64_t n_own = 0, n_own_max = 0;
+    uint32_t W = 0, TW = 32, NT = 1, C = 1;
+    uint64_t ring_stride = 0;
+    uint64_t nnz = 0;
+    double mean_seg = 0;
+    // device memory
+    std::vector<void *> allocs;
+    uint64_t device_bytes = 0;
+    uint64_t *row_ptr = nullptr;
+    uint32_t *bnd = nullptr;
+    uint16_t *ent_alloc = nullptr, *ent = nullptr;
+    float *v = nullptr, *ge = nullptr, *gi = nullptr;
+    uint32_t *ref = nullptr, *acc = nullptr, *ring = nullptr;
+    uint32_t *splist = nullptr, *spcount = nullptr, *record = nullptr, *sendbuf = nullptr, *gather = nullptr;
+    unsigned long long *stats = nullptr;
+    uint64_t *t0 = nullptr;
+    uint32_t *force_bits = nullptr;
+    uint64_t *force_ctl = nullptr;
+    uint64_t *ptab = nullptr;
+    ModelConst mc{};
+    SimArgs args{};
+    // host progress
+    uint64_t t_host = 0;
+    // graphs
+    static constexpr uint32_t kGraphSteps = 32;
+    cudaGraphExec_t g_big = nullptr, g_one = nullptr;
+    // nccl
+    ncclComm_t comm = nullptr;
+    cudaEvent_t ev = nullptr;
+};
+
+namespace {
+
+spice_status fail(spice_net *n, spice_status st, const char *fmt, ...) {
+    char buf[768];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    char head[96];
+    snprintf(head, sizeof head, "spice rank %u step %llu: ", n ? n->rank : 0u,
+             (unsigned long long)(n ? n->t_host : 0ull));
+    g_err = std::string(head) + buf;
+    if (n && (st == SPICE_ECUDA || st == SPICE_ENCCL)) n->poisoned = true;
+    return st;
+}
+
+#define CU(net, x)                                                                           \
+    do {                                                                                     \
+        cudaError_t e_ = (x);                                                                \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(net, SPICE_ECUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                 \
+    } while (0)
+
+#define CHECK_NET(net)                                                                       \
+    do {                                                                                     \
+        if (!(net)) return fail(nullptr, SPICE_EINVAL, "null handle");                       \
+        if ((net)->poisoned) return fail(net, SPICE_ESTATE, "handle poisoned by an earlier error"); \
+    } while (0)
+
+spice_status dalloc(spice_net *n, void **p, size_t bytes, const char *what) {
+    *p = nullptr;
+    cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(n, SPICE_ENOMEM, "cudaMalloc of %zu bytes for %s failed: %s", bytes, what,
+                    cudaGetErrorString(e));
+    }
+    n->allocs.push_back(*p);
+    n->device_bytes += bytes;
+    return SPICE_OK;
+}
+template <typename T>
+spice_status dalloc_t(spice_net *n, T **p, size_t count, const char *what) {
+    return dalloc(n, reinterpret_cast<void **>(p), count * sizeof(T), what);
+}
+void dfree(spice_net *n, void *p) {
+    if (!p) return;
+    auto it = std::find(n->allocs.begin(), n->allocs.end(), p);
+    if (it != n->allocs.end()) n->allocs.erase(it);
+    cudaFree(p);
+}
+
+spice_status validate(const spice_config *c) {
+    if (!c) return fail(nullptr, SPICE_EINVAL, "null config");
+    if (c->abi_version != SPICE_ABI_VERSION) return fail(nullptr, SPICE_EINVAL, "abi_version %u != %u", c->abi_version, SPICE_ABI_VERSION);
+    if (c->model != SPICE_VOGELS && c->model != SPICE_BRUNEL && c->model != SPICE_SYNTH)
+        return fail(nullptr, SPICE_EINVAL, "model %u not supported by this build", c->model);
+    if (c->n_neurons == 0) return fail(nullptr, SPICE_EINVAL, "n_neurons must be > 0");
+    if (c->n_exc > c->n_neurons) return fail(nullptr, SPICE_EINVAL, "n_exc > n_neurons");
+    if (c->delay_steps == 0) return fail(nullptr, SPICE_EINVAL, "delay_steps must be >= 1");
+    if (!(c->dt_ms > 0)) return fail(nullptr, SPICE_EINVAL, "dt_ms must be > 0");
+    if (c->world_size == 0 || c->rank >= c->world_size) return fail(nullptr, SPICE_EINVAL, "rank %u / world_size %u", c->rank, c->world_size);
+    if (c->slice_width % 32) return fail(nullptr, SPICE_EINVAL, "slice_width must be a multiple of 32");
+    if (c->record_steps == 0) return fail(nullptr, SPICE_EINVAL, "record_steps must be >= 1");
+    if (c->tile_width && (c->tile_width % 32 || c->tile_width > kMaxTileWidth))
+        return fail(nullptr, SPICE_EINVAL, "tile_width must be a multiple of 32 and <= %u", kMaxTileWidth);
+    const uint32_t need = c->model == SPICE_VOGELS ? 17 : c->model == SPICE_BRUNEL ? 10 : 0;
+    if (c->n_model_params < need || (need && !c->model_params))
+        return fail(nullptr, SPICE_EINVAL, "model %u needs %u parameters, got %u", c->model, need, c->n_model_params);
+    if (c->model == SPICE_SYNTH && !(c->activity >= 0 && c->activity <= 1))
+        return fail(nullptr, SPICE_EINVAL, "activity outside [0,1]");
+    if (c->n_rules && !c->rules) return fail(nullptr, SPICE_EINVAL, "rules is NULL");
+    for (uint32_t r = 0; r < c->n_rules; ++r) {
+        const spice_rule &R = c->rules[r];
+        if (R.src_begin > R.src_end || R.src_end > c->n_neurons || R.dst_begin > R.dst_end || R.dst_end > c->n_neurons)
+            return fail(nullptr, SPICE_EINVAL, "rule %u: ranges outside [0, N)", r);
+        if (R.kind == SPICE_FIXED_PROB && !(R.p >= 0 && R.p <= 1)) return fail(nullptr, SPICE_EINVAL, "rule %u: p outside [0,1]", r);
+        if (R.kind != SPICE_FIXED_PROB && R.kind != SPICE_FIXED_INDEGREE) return fail(nullptr, SPICE_EINVAL, "rule %u: unknown kind", r);
+        if (R.plastic) return fail(nullptr, SPICE_EINVAL, "rule %u: plastic synapses need model BRUNEL_PLUS", r);
+        for (uint32_t q = 0; q < r; ++q) {
+            const spice_rule &Q = c->rules[q];
+            const bool src_overlap = R.src_begin < Q.src_end && Q.src_begin < R.src_end;
+            const bool dst_overlap = R.dst_begin < Q.dst_end && Q.dst_begin < R.dst_end;
+            if (src_overlap && dst_overlap && R.src_begin < R.src_end && R.dst_begin < R.dst_end &&
+                Q.src_begin < Q.src_end && Q.dst_begin < Q.dst_end)
+                return fail(nullptr, SPICE_EINVAL, "rules %u and %u overlap in both ranges", q, r);
+        }
+    }
+    return SPICE_OK;
+}
+
+void build_model_const(spice_net *n) {
+    ModelConst &m = n->mc;
+    const double *P = n->prm.data();
+    const double dt = n->dt;
+    if (n->model == SPICE_VOGELS) {
+        m.h = (float)(dt / P[0]); m.EL = (float)P[1]; m.Vt = (float)P[2]; m.Vr = (float)P[3];
+        m.R = (uint32_t)std::llround(P[4] / dt); m.Ee = (float)P[5]; m.Ei = (float)P[6];
+        m.ke = (float)(dt / P[7]); m.ki = (float)(dt / P[8]); m.dge = (float)P[9]; m.dgi = (float)P[10];
+    } else if (n->model == SPICE_BRUNEL) {
+        m.h = (float)(dt / P[0]); m.EL = (float)P[1]; m.theta = (float)P[2]; m.Vr = (float)P[3];
+        m.R = (uint32_t)std::llround(P[4] / dt);
+        m.JE = (float)P[5]; m.JI = (float)(-P[6] * P[5]);
+    } else {
+        m.thr_fire = prob_threshold(n->activity);
+    }
+}
+
+spice_status capture_graph(spice_net *n, uint32_t steps, cudaGraphExec_t *out) {
+    cudaGraph_t g = nullptr;
+    CU(n, cudaStreamBeginCapture(n->stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t err = cudaSuccess;
+    spice_status st = SPICE_OK;
+    for (uint32_t k = 0; k < steps && err == cudaSuccess && st == SPICE_OK; ++k) {
+        if (n->G == 1) {
+            err = launch_update(n->args, k, true, n->stream);
+        } else {
+            err = launch_update(n->args, k, false, n->stream);
+            if (err == cudaSuccess) {
+                ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, n->stream);
+                if (r != ncclSuccess) st = fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
+            }
+            if (err == cudaSuccess && st == SPICE_OK) err = launch_bitmap_to_list(n->args, k, n->stream);
+        }
+        if (err == cudaSuccess && st == SPICE_OK) err = launch_deliver(n->args, k, n->mean_seg, n->n_sm, n->stream);
+    }
+    if (err == cudaSuccess && st == SPICE_OK) err = launch_advance(n->t0, steps, n->stream);
+    cudaError_t e2 = cudaStreamEndCapture(n->stream, &g);
+    if (st != SPICE_OK) { if (g) cudaGraphDestroy(g); return st; }
+    if (err != cudaSuccess) { if (g) cudaGraphDestroy(g); return fail(n, SPICE_ECUDA, "graph capture: %s", cudaGetErrorString(err)); }
+    if (e2 != cudaSuccess) return fail(n, SPICE_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(e2));
+    err = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    if (err != cudaSuccess) return fail(n, SPICE_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(err));
+    return SPICE_OK;
+}
+
+void destroy(spice_net *n) {
+    if (!n) return;
+    if (n->stream) cudaStreamSynchronize(n->stream);
+    if (n->g_big) cudaGraphExecDestroy(n->g_big);
+    if (n->g_one) cudaGraphExecDestroy(n->g_one);
+    if (n->comm) nccl().CommDestroy(n->comm);
+    for (void *p : n->allocs) cudaFree(p);
+    n->allocs.clear();
+    if (n->ev) cudaEventDestroy(n->ev);
+    if (n->stream) cudaStreamDestroy(n->stream);
+    delete n;
+}
+
+// Exact post-generation check that packed 16-bit receptor counts cannot overflow:
+// the number of excitatory (inhibitory) in-synapses of any owned target is < 65536.
+__global__ void indegree_kernel(const uint64_t *row_ptr, const uint32_t *bnd, const uint16_t *ent,
+                                uint32_t N, uint32_t NT, uint32_t TW, uint32_t n_exc, uint32_t *deg) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    for (uint64_t w = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); w < (uint64_t)N * NT; w += nwarps) {
+        const uint32_t s = (uint32_t)(w / NT), b = (uint32_t)(w % NT);
+        const uint32_t *bp = bnd + (uint64_t)s * (NT + 1) + b;
+        const uint64_t st = row_ptr[s] + bp[0];
+        const uint32_t len = bp[1] - bp[0];
+        const uint32_t q = s >= n_exc ? 65536u : 1u;
+        for (uint32_t e = lane; e < len; e += 32) atomicAdd(&deg[(uint64_t)b * TW + ent[st + e]], q);
+    }
+}
+__global__ void max_halves_kernel(const uint32_t *deg, uint64_t n, uint32_t *out) {
+    uint32_t me = 0, mi = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        me = max(me, deg[i] & 0xFFFFu); mi = max(mi, deg[i] >> 16);
+    }
+    atomicMax(&out[0], me); atomicMax(&out[1], mi);
+}
+
+spice_status generate(spice_net *n) {
+    GenGeom g{};
+    g.N = n->N; g.n_own = (uint32_t)n->n_own; g.rank = n->rank; g.G = n->G; g.S = n->S;
+    g.TW = n->TW; g.NT = n->NT; g.key0 = (uint32_t)n->seed; g.key1 = (uint32_t)(n->seed >> 32);
+    const uint64_t nb = (uint64_t)n->N * (n->NT + 1);
+    uint32_t *cursor = nullptr;
+    spice_status st;
+    if ((st = dalloc_t(n, &n->row_ptr, (size_t)n->N + 1, "row_ptr"))) return st;
+    if ((st = dalloc_t(n, &n->bnd, nb, "segment bounds"))) return st;
+    CU(n, cudaMemsetAsync(n->bnd, 0, nb * 4, n->stream));
+    // rules in ascending destination order so that per-segment appends stay sorted
+    std::vector<uint32_t> order(n->rules.size());
+    for (uint32_t r = 0; r < order.size(); ++r) order[r] = r;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+        return n->rules[a].dst_begin < n->rules[b].dst_begin;
+    });
+    std::vector<GenRule> gr;
+    bool any_indeg = false;
+    for (uint32_t r : order) {
+        const spice_rule &R = n->rules[r];
+        GenRule x{R.src_begin, R.src_end, R.dst_begin, R.dst_end, R.kind, R.k, r, prob_threshold(R.p)};
+        gr.push_back(x);
+        any_indeg |= R.kind == SPICE_FIXED_INDEGREE && R.k > 0;
+    }
+    for (const GenRule &x : gr) CU(n, gen_count(g, x, n->bnd, n->stream));
+    uint64_t nnz = 0;
+    CU(n, gen_scan(g, n->bnd, n->row_ptr, &nnz, n->stream));
+    n->nnz = nnz;
+    if ((st = dalloc_t(n, &n->ent_alloc, (size_t)nnz + 2 * kEntPad, "synapse entries"))) return st;
+    n->ent = n->ent_alloc + kEntPad;
+    CU(n, cudaMemsetAsync(n->ent_alloc, 0, ((size_t)nnz + 2 * kEntPad) * 2, n->stream));
+    if ((st = dalloc_t(n, &cursor, nb, "fill cursors"))) return st;
+    CU(n, cudaMemsetAsync(cursor, 0, nb * 4, n->stream));
+    for (const GenRule &x : gr) CU(n, gen_fill(g, x, n->row_ptr, n->bnd, cursor, n->ent, n->stream));
+    if (any_indeg) CU(n, gen_sort_segments(g, n->row_ptr, n->bnd, n->ent, n->stream));
+    CU(n, cudaStreamSynchronize(n->stream));
+    dfree(n, cursor);
+    n->device_bytes -= nb * 4;
+    n->mean_seg = n->N ? (double)nnz / ((double)n->N * n->NT) : 0;
+    // receptor packing check (two populations only)
+    if (n->n_exc < n->N && n->n_own) {
+        uint32_t *deg = nullptr, *mx = nullptr;
+        if ((st = dalloc_t(n, &deg, n->ring_stride, "in-degree check"))) return st;
+        if ((st = dalloc_t(n, &mx, 2, "in-degree max"))) return st;
+        CU(n, cudaMemsetAsync(deg, 0, n->ring_stride * 4, n->stream));
+        CU(n, cudaMemsetAsync(mx, 0, 8, n->stream));
+        indegree_kernel<<<n->n_sm * 8, 256, 0, n->stream>>>(n->row_ptr, n->bnd, n->ent, n->N, n->NT, n->TW, n->n_exc, deg);
+        max_halves_kernel<<<n->n_sm * 4, 256, 0, n->stream>>>(deg, n->ring_stride, mx);
+        uint32_t h[2] = {0, 0};
+        CU(n, cudaMemcpyAsync(h, mx, 8, cudaMemcpyDeviceToHost, n->stream));
+        CU(n, cudaStreamSynchronize(n->stream));
+        dfree(n, deg); dfree(n, mx);
+        n->device_bytes -= n->ring_stride * 4 + 8;
+        // a 16-bit field saturates only if one target has >= 65535 in-synapses of a type
+        if (h[0] >= 65535u || h[1] >= 65535u)
+            return fail(n, SPICE_EINVAL, "a target has >= 65535 in-synapses of one receptor type; packed counts could overflow");
+    }
+    return SPICE_OK;
+}
+
+}  // namespace
+
+// =========================================================================== ABI
+extern "C" {
+
+const char *spice_last_error(void) { return g_err.c_str(); }
+
+uint32_t spice_partition_owner(uint64_t j, uint32_t G, uint32_t S) {
+    return (G && S) ? (uint32_t)((j / S) % G) : 0u;
+}
+uint64_t spice_partition_local_to_global(uint64_t i, uint32_t g, uint32_t G, uint32_t S) {
+    return local_to_global(i, g, G, S);
+}
+uint64_t spice_partition_owned_count(uint64_t n, uint32_t g, uint32_t G, uint32_t S) {
+    if (!G || !S || g >= G) return 0;
+    return owned_count(n, g, G, S);
+}
+uint32_t spice_default_slice_width(uint64_t n, uint32_t G) {
+    if (G <= 1) return 32;
+    const uint64_t s = n / (256ull * G);      // ~256 slices per rank ("hundreds")
+    const uint64_t r = (s / 32) * 32;
+    return (uint32_t)std::max<uint64_t>(32, std::min<uint64_t>(r, 1u << 20));
+}
+
+spice_status spice_nccl_unique_id(void *out128) {
+    if (!out128) return fail(nullptr, SPICE_EINVAL, "null output");
+    if (!nccl().ok) return fail(nullptr, SPICE_ENCCL, "libnccl.so.2 not found (set SPICE_NCCL_LIB)");
+    ncclUniqueId id;
+    ncclResult_t r = nccl().GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, SPICE_ENCCL, "ncclGetUniqueId: %s", nccl().GetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(out128, &id, 128);
+    return SPICE_OK;
+}
+
+spice_status spice_create_network(const spice_config *c, spice_net **out) {
+    if (!out) return fail(nullptr, SPICE_EINVAL, "null output handle");
+    *out = nullptr;
+    spice_status st = validate(c);
+    if (st) return st;
+    spice_net *n = new spice_net();
+    n->model = c->model; n->N = c->n_neurons; n->n_exc = c->n_exc; n->delay = c->delay_steps;
+    n->D = c->delay_steps + 1; n->rank = c->rank; n->G = c->world_size;
+    n->S = c->slice_width ? c->slice_width : spice_default_slice_width(c->n_neurons, c->world_size);
+    n->flags = c->flags; n->R = c->record_steps; n->dt = c->dt_ms; n->activity = c->activity;
+    n->seed = c->seed; n->device = c->device;
+    n->external = (c->flags & SPICE_FLAG_EXTERNAL_EXCHANGE) != 0;
+    n->prm.assign(c->model_params, c->model_params + c->n_model_params);
+    n->rules.assign(c->rules, c->rules + c->n_rules);
+    auto bail = [&](spice_status s) { destroy(n); return s; };
+    if (n->G > 1 && !n->external && !c->nccl_unique_id)
+        return bail(fail(n, SPICE_EINVAL, "world_size > 1 needs nccl_unique_id or EXTERNAL_EXCHANGE"));
+    {
+        cudaError_t e = cudaSetDevice(n->device);
+        if (e) return bail(fail(n, SPICE_ECUDA, "cudaSetDevice(%d): %s", n->device, cudaGetErrorString(e)));
+        cudaDeviceGetAttribute(&n->n_sm, cudaDevAttrMultiProcessorCount, n->device);
+        e = cudaStreamCreateWithFlags(&n->stream, cudaStreamNonBlocking);
+        if (e) return bail(fail(n, SPICE_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)));
+        cudaEventCreateWithFlags(&n->ev, cudaEventDisableTiming);
+    }
+    // ---- partition (a0) ----
+    n->n_own = owned_count(n->N, n->rank, n->G, n->S);
+    n->n_own_max = owned_count(n->N, 0, n->G, n->S);
+    n->W = (uint32_t)((n->n_own_max + 31) / 32);
+    // ---- delivery tiles ----
+    if (c->tile_width) {
+        n->TW = c->tile_width;
+    } else {
+        const uint64_t want_tiles = 2ull * n->n_sm;
+        uint64_t tw = (n->n_own + want_tiles - 1) / want_tiles;
+        tw = (tw + 31) / 32 * 32;
+        n->TW = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(tw, 32), kMaxTileWidth);
+    }
+    n->NT = (uint32_t)std::max<uint64_t>(1, (n->n_own + n->TW - 1) / n->TW);
+    n->C = c->ctas_per_tile ? c->ctas_per_tile : 1;
+    n->ring_stride = (uint64_t)n->NT * n->TW;
+    // ---- NCCL communicator ----
+    if (n->G > 1 && !n->external) {
+        if (!nccl().ok) return bail(fail(n, SPICE_ENCCL, "libnccl.so.2 not found (set SPICE_NCCL_LIB)"));
+        ncclUniqueId id;
+        memcpy(&id, c->nccl_unique_id, sizeof id);
+        ncclResult_t r = nccl().CommInitRank(&n->comm, (int)n->G, id, (int)n->rank);
+        if (r != ncclSuccess) return bail(fail(n, SPICE_ENCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r)));
+    }
+    // ---- connectivity (a0') ----
+    if ((st = generate(n))) return bail(st);
+    // ---- state, ring, spike buffers ----
+    const uint64_t no = std::max<uint64_t>(n->n_own, 1);
+    if ((st = dalloc_t(n, &n->ring, (size_t)n->D * n->ring_stride, "input ring"))) return bail(st);
+    if ((st = dalloc_t(n, &n->splist, std::max<uint32_t>(n->N, 1), "spike list"))) return bail(st);
+    if ((st = dalloc_t(n, &n->spcount, 4, "spike counts"))) return bail(st);
+    if ((st = dalloc_t(n, &n->record, (size_t)n->R * n->G * n->W, "spike record"))) return bail(st);
+    if ((st = dalloc_t(n, &n->sendbuf, std::max<uint32_t>(n->W, 1), "send bitmap"))) return bail(st);
+    if ((st = dalloc_t(n, &n->gather, (size_t)n->G * std::max<uint32_t>(n->W, 1), "gathered bitmaps"))) return bail(st);
+    if ((st = dalloc_t(n, &n->stats, 2, "stats"))) return bail(st);
+    if ((st = dalloc_t(n, &n->t0, 1, "step counter"))) return bail(st);
+    if ((st = dalloc_t(n, &n->force_bits, std::max<uint32_t>(n->W, 1), "force bits"))) return bail(st);
+    if ((st = dalloc_t(n, &n->force_ctl, 2, "force control"))) return bail(st);
+    if ((st = dalloc_t(n, &n->v, no, "v"))) return bail(st);
+    if ((st = dalloc_t(n, &n->ref, no, "ref"))) return bail(st);
+    if (n->model == SPICE_VOGELS) {
+        if ((st = dalloc_t(n, &n->ge, no, "ge"))) return bail(st);
+        if ((st = dalloc_t(n, &n->gi, no, "gi"))) return bail(st);
+    }
+    if (n->model == SPICE_SYNTH && (st = dalloc_t(n, &n->acc, no, "acc"))) return bail(st);
+    cudaStream_t s = n->stream;
+    CU(n, cudaMemsetAsync(n->ring, 0, (size_t)n->D * n->ring_stride * 4, s));
+    CU(n, cudaMemsetAsync(n->spcount, 0, 16, s));
+    CU(n, cudaMemsetAsync(n->record, 0, (size_t)n->R * n->G * n->W * 4, s));
+    CU(n, cudaMemsetAsync(n->stats, 0, 16, s));
+    CU(n, cudaMemsetAsync(n->t0, 0, 8, s));
+    CU(n, cudaMemsetAsync(n->force_bits, 0, std::max<uint32_t>(n->W, 1) * 4, s));
+    CU(n, cudaMemsetAsync(n->force_ctl, 0xFF, 16, s));
+    CU(n, cudaMemsetAsync(n->v, 0, no * 4, s));
+    CU(n, cudaMemsetAsync(n->ref, 0, no * 4, s));
+    if (n->acc) CU(n, cudaMemsetAsync(n->acc, 0, no * 4, s));
+    build_model_const(n);
+    GenGeom g{};
+    g.N = n->N; g.n_own = (uint32_t)n->n_own; g.rank = n->rank; g.G = n->G; g.S = n->S;
+    g.TW = n->TW; g.NT = n->NT; g.key0 = (uint32_t)n->seed; g.key1 = (uint32_t)(n->seed >> 32);
+    const double *P = n->prm.data();
+    if (n->model == SPICE_VOGELS) {
+        CU(n, gen_init_uniform(g, 0, (float)P[11], (float)P[12], n->v, s));
+        CU(n, gen_init_uniform(g, 1, (float)P[13], (float)P[14], n->ge, s));
+        CU(n, gen_init_uniform(g, 2, (float)P[15], (float)P[16], n->gi, s));
+    } else if (n->model == SPICE_BRUNEL) {
+        CU(n, gen_init_uniform(g, 0, (float)P[8], (float)P[9], n->v, s));
+        std::vector<uint64_t> tab = poisson_table(P[7]);
+        if (tab.empty()) return bail(fail(n, SPICE_EINVAL, "lambda_ext %g too large for the Poisson table", P[7]));
+        if ((st = dalloc_t(n, &n->ptab, tab.size(), "Poisson table"))) return bail(st);
+        CU(n, cudaMemcpyAsync(n->ptab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, s));
+        n->mc.ptab = n->ptab;
+        n->mc.ptab_len = (uint32_t)tab.size();
+    }
+    CU(n, cudaStreamSynchronize(s));
+    // ---- kernel arguments ----
+    SimArgs &a = n->args;
+    a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D;
+    a.rank = n->rank; a.G = n->G; a.S = n->S; a.n_own = (uint32_t)n->n_own; a.W = n->W;
+    a.TW = n->TW; a.NT = n->NT; a.C = n->C; a.ring_stride = n->ring_stride; a.record_steps = n->R;
+    a.key0 = (uint32_t)n->seed; a.key1 = (uint32_t)(n->seed >> 32);
+    a.global_atomics = (n->flags & SPICE_FLAG_GLOBAL_ATOMICS) ? 1u : 0u;
+    a.mc = n->mc;
+    a.row_ptr = n->row_ptr; a.bnd = n->bnd; a.ent = n->ent;
+    a.v = n->v; a.ge = n->ge; a.gi = n->gi; a.ref = n->ref; a.acc = n->acc; a.ring = n->ring;
+    a.splist = n->splist; a.spcount = n->spcount; a.record = n->record; a.sendbuf = n->sendbuf;
+    a.gather = n->gather; a.stats = n->stats; a.t0 = n->t0; a.force_bits = n->force_bits;
+    a.force_ctl = n->force_ctl;
+    CU(n, prepare_deliver(n->TW));
+    if (deliver_smem_bytes(n->TW) > 227 * 1024) return bail(fail(n, SPICE_EINVAL, "tile too wide"));
+    if (!n->external) {
+        if ((st = capture_graph(n, spice_net::kGraphSteps, &n->g_big))) return bail(st);
+        if ((st = capture_graph(n, 1, &n->g_one))) return bail(st);
+    }
+    *out = n;
+    return SPICE_OK;
+}
+
+spice_status spice_step(spice_net *n, uint64_t steps) {
+    CHECK_NET(n);
+    if (n->external) return fail(n, SPICE_ESTATE, "external-exchange networks step via spice_exchange_begin/end");
+    while (steps >= spice_net::kGraphSteps) {
+        CU(n, cudaGraphLaunch(n->g_big, n->stream));
+        steps -= spice_net::kGraphSteps;
+        n->t_host += spice_net::kGraphSteps;
+    }
+    while (steps--) {
+        CU(n, cudaGraphLaunch(n->g_one, n->stream));
+        n->t_host += 1;
+    }
+    return SPICE_OK;
+}
+
+spice_status spice_exchange_begin(spice_net *n) {
+    CHECK_NET(n);
+    if (!n->external) return fail(n, SPICE_ESTATE, "not an external-exchange network");
+    CU(n, launch_update(n->args, 0, n->G == 1, n->stream));
+    CU(n, cudaEventRecord(n->ev, n->stream));
+    return SPICE_OK;
+}
+
+spice_status spice_exchange_put(spice_net *dst, spice_net *src) {
+    CHECK_NET(dst);
+    CHECK_NET(src);
+    if (dst->W != src->W || src->rank >= dst->G) return fail(dst, SPICE_EINVAL, "incompatible exchange peers");
+    CU(dst, cudaStreamWaitEvent(dst->stream, src->ev, 0));
+    CU(dst, cudaMemcpyAsync(dst->gather + (uint64_t)src->rank * src->W, src->sendbuf, (size_t)src->W * 4,
+                            cudaMemcpyDeviceToDevice, dst->stream));
+    // test hook: complete the copy so src may overwrite its send buffer next step
+    CU(dst, cudaStreamSynchronize(dst->stream));
+    return SPICE_OK;
+}
+
+spice_status spice_exchange_end(spice_net *n) {
+    CHECK_NET(n);
+    if (!n->external) return fail(n, SPICE_ESTATE, "not an external-exchange network");
+    if (n->G > 1) CU(n, launch_bitmap_to_list(n->args, 0, n->stream));
+    CU(n, launch_deliver(n->args, 0, n->mean_seg, n->n_sm, n->stream));
+    CU(n, launch_advance(n->t0, 1, n->stream));
+    // the next begin on another handle must not overwrite our gather buffer early
+    CU(n, cudaEventRecord(n->ev, n->stream));
+    n->t_host += 1;
+    return SPICE_OK;
+}
+
+spice_status spice_read_spikes(spice_net *n, uint64_t t_begin, uint64_t t_end, uint32_t *ids,
+                               uint64_t cap, uint64_t *offsets, uint64_t *total) {
+    CHECK_NET(n);
+    if (t_begin > t_end || t_end > n->t_host || (n->t_host > n->R && t_begin < n->t_host - n->R))
+        return fail(n, SPICE_ERANGE, "steps [%llu, %llu) not in the record ring (have [%llu, %llu))",
+                    (unsigned long long)t_begin, (unsigned long long)t_end,
+                    (unsigned long long)(n->t_host > n->R ? n->t_host - n->R : 0), (unsigned long long)n->t_host);
+    CU(n, cudaStreamSynchronize(n->stream));
+    const uint64_t words = (uint64_t)n->G * n->W;
+    std::vector<uint32_t> bm(words);
+    std::vector<std::vector<uint32_t>> per(t_end - t_begin);
+    uint64_t tot = 0;
+    for (uint64_t t = t_begin; t < t_end; ++t) {
+        CU(n, cudaMemcpy(bm.data(), n->record + (t % n->R) * words, words * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> &L = per[t - t_begin];
+        for (uint32_t r = 0; r < n->G; ++r)
+            for (uint32_t w = 0; w < n->W; ++w) {
+                uint32_t bits = bm[(uint64_t)r * n->W + w];
+                while (bits) {
+                    const uint32_t b = __builtin_ctz(bits);
+                    bits &= bits - 1;
+                    L.push_back((uint32_t)local_to_global((uint64_t)w * 32 + b, r, n->G, n->S));
+                }
+            }
+        if (n->G > 1) std::sort(L.begin(), L.end());
+        tot += L.size();
+    }
+    if (total) *total = tot;
+    if (tot > cap || (!ids && tot)) return fail(n, SPICE_ETRUNC, "need %llu ids", (unsigned long long)tot);
+    uint64_t o = 0;
+    for (uint64_t q = 0; q < per.size(); ++q) {
+        if (offsets) offsets[q] = o;
+        memcpy(ids + o, per[q].data(), per[q].size() * 4);
+        o += per[q].size();
+    }
+    if (offsets) offsets[per.size()] = o;
+    return SPICE_OK;
+}
+
+spice_status spice_read_connectivity(spice_net *n, uint32_t row_begin, uint32_t row_end, uint32_t *tgt,
+                                     uint64_t cap, uint64_t *row_offsets, uint64_t *total) {
+    CHECK_NET(n);
+    if (row_begin > row_end || row_end > n->N) return fail(n, SPICE_EINVAL, "rows outside [0, N)");
+    CU(n, cudaStreamSynchronize(n->stream));
+    const uint32_t nr = row_end - row_begin;
+    std::vector<uint64_t> rp(nr + 1);
+    CU(n, cudaMemcpy(rp.data(), n->row_ptr + row_begin, (nr + 1) * 8ull, cudaMemcpyDeviceToHost));
+    const uint64_t tot = rp[nr] - rp[0];
+    if (total) *total = tot;
+    if (tot > cap || (!tgt && tot)) return fail(n, SPICE_ETRUNC, "need %llu targets", (unsigned long long)tot);
+    std::vector<uint32_t> bd((uint64_t)nr * (n->NT + 1));
+    std::vector<uint16_t> en(tot ? tot : 1);
+    if (nr) CU(n, cudaMemcpy(bd.data(), n->bnd + (uint64_t)row_begin * (n->NT + 1), bd.size() * 4, cudaMemcpyDeviceToHost));
+    if (tot) CU(n, cudaMemcpy(en.data(), n->ent + rp[0], tot * 2, cudaMemcpyDeviceToHost));
+    for (uint32_t q = 0; q < nr; ++q) {
+        if (row_offsets) row_offsets[q] = rp[q] - rp[0];
+        const uint32_t *B = bd.data() + (uint64_t)q * (n->NT + 1);
+        for (uint32_t b = 0; b < n->NT; ++b)
+            for (uint32_t e = B[b]; e < B[b + 1]; ++e) {
+                const uint64_t i = (uint64_t)b * n->TW + en[rp[q] - rp[0] + e];
+                tgt[rp[q] - rp[0] + e] = (uint32_t)local_to_global(i, n->rank, n->G, n->S);
+            }
+    }
+    if (row_offsets) row_offsets[nr] = tot;
+    return SPICE_OK;
+}
+
+static spice_status field_ptr(spice_net *n, uint32_t field, void **p) {
+    *p = nullptr;
+    switch (field) {
+    case SPICE_FIELD_V: *p = n->model != SPICE_SYNTH ? n->v : nullptr; break;
+    case SPICE_FIELD_GE: *p = n->ge; break;
+    case SPICE_FIELD_GI: *p = n->gi; break;
+    case SPICE_FIELD_REF: *p = n->model != SPICE_SYNTH ? n->ref : nullptr; break;
+    case SPICE_FIELD_ACC: *p = n->acc; break;
+    default: break;
+    }
+    if (!*p) return fail(n, SPICE_EINVAL, "field %u not present for model %u", field, n->model);
+    return SPICE_OK;
+}
+
+spice_status spice_read_state(spice_net *n, uint32_t field, void *out, uint64_t count) {
+    CHECK_NET(n);
+    void *p;
+    spice_status st = field_ptr(n, field, &p);
+    if (st) return st;
+    if (count != n->n_own) return fail(n, SPICE_EINVAL, "n = %llu, owned = %llu", (unsigned long long)count, (unsigned long long)n->n_own);
+    CU(n, cudaStreamSynchronize(n->stream));
+    if (count) CU(n, cudaMemcpy(out, p, count * 4, cudaMemcpyDeviceToHost));
+    return SPICE_OK;
+}
+
+spice_status spice_write_state(spice_net *n, uint32_t field, const void *in, uint64_t count) {
+    CHECK_NET(n);
+    void *p;
+    spice_status st = field_ptr(n, field, &p);
+    if (st) return st;
+    if (count != n->n_own) return fail(n, SPICE_EINVAL, "n = %llu, owned = %llu", (unsigned long long)count, (unsigned long long)n->n_own);
+    CU(n, cudaStreamSynchronize(n->stream));
+    if (count) CU(n, cudaMemcpy(p, in, count * 4, cudaMemcpyHostToDevice));
+    return SPICE_OK;
+}
+
+spice_status spice_read_input(spice_net *n, uint32_t rel, uint32_t *counts, int64_t *plastic, uint64_t count) {
+    CHECK_NET(n);
+    if (rel >= n->D) return fail(n, SPICE_EINVAL, "rel %u >= D %u", rel, n->D);
+    if (count != n->n_own) return fail(n, SPICE_EINVAL, "n must equal the owned count");
+    CU(n, cudaStreamSynchronize(n->stream));
+    const uint64_t slot = (n->t_host + rel) % n->D;
+    if (counts && count) CU(n, cudaMemcpy(counts, n->ring + slot * n->ring_stride, count * 4, cudaMemcpyDeviceToHost));
+    if (plastic) memset(plastic, 0, count * 8);
+    return SPICE_OK;
+}
+
+spice_status spice_read_weights(spice_net *n, uint32_t, uint32_t, float *, uint64_t, uint64_t *) {
+    CHECK_NET(n);
+    return fail(n, SPICE_EINVAL, "model %u has no plastic weights", n->model);
+}
+
+spice_status spice_force_spikes(spice_net *n, const uint32_t *ids, uint64_t count, int mode) {
+    CHECK_NET(n);
+    if (mode != 1 && mode != 2) return fail(n, SPICE_EINVAL, "mode must be 1 (replace) or 2 (add)");
+    std::vector<uint32_t> bits(std::max<uint32_t>(n->W, 1), 0u);
+    for (uint64_t q = 0; q < count; ++q) {
+        const uint32_t j = ids[q];
+        if (j >= n->N) return fail(n, SPICE_EINVAL, "id %u >= N", j);
+        if ((j / n->S) % n->G != n->rank) continue;
+        const uint64_t i = (uint64_t)(j / n->S / n->G) * n->S + j % n->S;   // inverse of Listing 1
+        bits[i >> 5] |= 1u << (i & 31);
+    }
+    const uint64_t ctl[2] = {n->t_host, (uint64_t)mode};
+    CU(n, cudaMemcpyAsync(n->force_bits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, n->stream));
+    CU(n, cudaMemcpyAsync(n->force_ctl, ctl, 16, cudaMemcpyHostToDevice, n->stream));
+    CU(n, cudaStreamSynchronize(n->stream));
+    return SPICE_OK;
+}
+
+spice_status spice_stats(spice_net *n, uint64_t *steps, uint64_t *fired, uint64_t *delivered) {
+    CHECK_NET(n);
+    CU(n, cudaStreamSynchronize(n->stream));
+    unsigned long long h[2];
+    CU(n, cudaMemcpy(h, n->stats, 16, cudaMemcpyDeviceToHost));
+    if (steps) *steps = n->t_host;
+    if (fired) *fired = h[0];
+    if (delivered) *delivered = h[1];
+    return SPICE_OK;
+}
+
+void *spice_stream(spice_net *n) { return n ? (void *)n->stream : nullptr; }
+
+spice_status spice_sync(spice_net *n) {
+    CHECK_NET(n);
+    CU(n, cudaStreamSynchronize(n->stream));
+    return SPICE_OK;
+}
+
+spice_status spice_info(spice_net *n, uint64_t *n_owned, uint64_t *n_syn, uint32_t *n_tiles,
+                        uint32_t *tile_width, uint32_t *ctas, uint64_t *bytes) {
+    CHECK_NET(n);
+    if (n_owned) *n_owned = n->n_own;
+    if (n_syn) *n_syn = n->nnz;
+    if (n_tiles) *n_tiles = n->NT;
+    if (tile_width) *tile_width = n->TW;
+    if (ctas) *ctas = n->C;
+    if (bytes) *bytes = n->device_bytes;
+    return SPICE_OK;
+}
+
+spice_status spice_profile(spice_net *n, uint64_t steps, double *ms, uint32_t cap, uint32_t *nk) {
+    CHECK_NET(n);
+    if (n->external) return fail(n, SPICE_ESTATE, "profiling needs an NCCL or single-GPU network");
+    if (!ms || cap < 4) return fail(n, SPICE_EINVAL, "need room for 4 timings");
+    cudaEvent_t ev[5];
+    for (auto &e : ev) CU(n, cudaEventCreate(&e));
+    double acc[4] = {0, 0, 0, 0};
+    for (uint64_t q = 0; q < steps; ++q) {
+        CU(n, cudaEventRecord(ev[0], n->stream));
+        CU(n, launch_update(n->args, 0, n->G == 1, n->stream));
+        CU(n, cudaEventRecord(ev[1], n->stream));
+        if (n->G > 1) {
+            ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, n->stream);
+            if (r != ncclSuccess) return fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
+            CU(n, cudaEventRecord(ev[2], n->stream));
+            CU(n, launch_bitmap_to_list(n->args, 0, n->stream));
+        } else {
+            CU(n, cudaEventRecord(ev[2], n->stream));
+        }
+        CU(n, cudaEventRecord(ev[3], n->stream));
+        CU(n, launch_deliver(n->args, 0, n->mean_seg, n->n_sm, n->stream));
+        CU(n, cudaEventRecord(ev[4], n->stream));
+        CU(n, launch_advance(n->t0, 1, n->stream));
+        CU(n, cudaEventSynchronize(ev[4]));
+        float a = 0, b = 0, c = 0, d = 0;
+        CU(n, cudaEventElapsedTime(&a, ev[0], ev[1]));
+        CU(n, cudaEventElapsedTime(&b, ev[3], ev[4]));
+        CU(n, cudaEventElapsedTime(&c, ev[2], ev[3]));
+        CU(n, cudaEventElapsedTime(&d, ev[1], ev[2]));
+        acc[0] += a; acc[1] += b; acc[2] += c; acc[3] += d;
+        n->t_host += 1;
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    for (int k = 0; k < 4; ++k) ms[k] = steps ? acc[k] / (double)steps : 0.0;
+    if (nk) *nk = 4;
+    return SPICE_OK;
+}
+
+uint32_t spice_kernels_per_step(spice_net *n) {
+    if (!n) return 0;
+    return n->G == 1 ? 2u : 3u;   // update, [bitmap_to_list], deliver (+ NCCL's own kernel)
+}
+
+spice_status spice_free(spice_net *n) {
+    if (!n) return SPICE_OK;
+    destroy(n);
+    return SPICE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,304 @@
+// gen.cu — on-device network generator (SURVEY §8(a) a0'; §III-B,
+// "the layout description is then uploaded to the GPU where it is expanded").
+//
+// Each rank expands only the edges whose target it owns (the descriptor split of
+// {range1, range2 ∩ owned, p}), directly into the destination-tiled
+// CSR used by delivery:
+//   row_ptr[s]            start of source s's row (global source IDs, all N rows)
+//   bnd[s*(NT+1) + b]     start of tile b's segment within row s (bnd[..NT] = row length)
+//   ent[row_ptr[s] + e]   tile-local target offset (u16), ascending within each segment
+// Pipeline: count per (row, tile) -> scan -> fill -> (fixed in-degree only) sort segments.
+// Fixed probability rows come out sorted because every warp appends its row segment in
+// ascending target order (ballot/prefix ordered append).
+#include "spice_internal.cuh"
+#include "spice_launch.h"
+
+namespace spice {
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, uint32_t lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    return x;
+}
+
+// Bits of the 4 targets of local 4-block q of tile b that receive an edge from s.
+__device__ __forceinline__ uint32_t prob_bits4(const GenGeom &g, const GenRule &r, uint32_t s,
+                                               uint32_t i0) {
+    if (i0 >= g.n_own) return 0u;
+    const uint32_t j0 = (uint32_t)local_to_global(i0, g.rank, g.G, g.S);   // multiple of 4
+    const uint4 x = philox4x32_10(make_uint4(s, j0 >> 2, r.index, kTagConn), g.key0, g.key1);
+    uint32_t m = 0;
+#pragma unroll
+    for (uint32_t e = 0; e < 4; ++e) {
+        const uint32_t j = j0 + e;
+        const bool ok = (i0 + e < g.n_own) && j >= r.dst_begin && j < r.dst_end &&
+                        (uint64_t)word_of(x, e) < r.thr;
+        m |= (ok ? 1u : 0u) << e;
+    }
+    return m;
+}
+
+__device__ __forceinline__ bool tile_hits_dst(const GenGeom &g, const GenRule &r, uint32_t b) {
+    const uint32_t lo = b * g.TW;
+    if (lo >= g.n_own) return false;
+    const uint32_t hi = min(lo + g.TW, g.n_own) - 1u;
+    const uint64_t jlo = local_to_global(lo, g.rank, g.G, g.S);
+    const uint64_t jhi = local_to_global(hi, g.rank, g.G, g.S);
+    return !(jhi < r.dst_begin || jlo >= r.dst_end);
+}
+
+__global__ void __launch_bounds__(256) count_prob_kernel(GenGeom g, GenRule r, uint32_t *cnt) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * 8;
+    const uint64_t npairs = (uint64_t)(r.src_end - r.src_begin) * g.NT;
+    for (uint64_t w = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); w < npairs; w += nwarps) {
+        const uint32_t s = r.src_begin + (uint32_t)(w / g.NT), b = (uint32_t)(w % g.NT);
+        if (!tile_hits_dst(g, r, b)) continue;
+        const uint32_t len = min(g.TW, g.n_own - b * g.TW);
+        const uint32_t nblk = (len + 3u) / 4u;
+        uint32_t c = 0;
+        for (uint32_t q = lane; q < nblk; q += 32) c += __popc(prob_bits4(g, r, s, b * g.TW + 4u * q));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+        if (lane == 0) cnt[(uint64_t)s * (g.NT + 1) + b] += c;
+    }
+}
+
+__global__ void __launch_bounds__(256) fill_prob_kernel(GenGeom g, GenRule r, const uint64_t *row_ptr,
+                                                        const uint32_t *bnd, uint32_t *cursor,
+                                                        uint16_t *ent) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * 8;
+    const uint64_t npairs = (uint64_t)(r.src_end - r.src_begin) * g.NT;
+    for (uint64_t w = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); w < npairs; w += nwarps) {
+        const uint32_t s = r.src_begin + (uint32_t)(w / g.NT), b = (uint32_t)(w % g.NT);
+        if (!tile_hits_dst(g, r, b)) continue;
+        const uint64_t seg = (uint64_t)s * (g.NT + 1) + b;
+        uint64_t pos = row_ptr[s] + bnd[seg] + cursor[seg];
+        const uint32_t len = min(g.TW, g.n_own - b * g.TW);
+        const uint32_t nblk = (len + 3u) / 4u;
+        uint32_t written = 0;
+        for (uint32_t q0 = 0; q0 < nblk; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            const uint32_t m = q < nblk ? prob_bits4(g, r, s, b * g.TW + 4u * q) : 0u;
+            const uint32_t c = __popc(m);
+            const uint32_t incl = warp_incl_scan(c, lane);
+            uint64_t p = pos + incl - c;
+            for (uint32_t e = 0; e < 4; ++e)
+                if (m >> e & 1u) ent[p++] = (uint16_t)(4u * q + e);
+            const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            pos += tot;
+            written += tot;
+        }
+        if (lane == 0) cursor[seg] += written;
+    }
+}
+
+// Fixed in-degree: target j (owned, in range2) draws k sources; r64 from
+// Philox(ctr = (j, k>>1, rule, TAG_INDEG)) words 2(k&1), 2(k&1)+1; source =
+// src_begin + floor(r64 |src| / 2^64) (reading R9).
+template <bool FILL>
+__global__ void __launch_bounds__(256) indeg_kernel(GenGeom g, GenRule r, const uint64_t *row_ptr,
+                                                    const uint32_t *bnd, uint32_t *cnt_or_cursor,
+                                                    uint16_t *ent) {
+    const uint32_t kp = (r.k + 1u) / 2u;
+    const uint64_t total = (uint64_t)g.n_own * kp;
+    const uint64_t nsrc = (uint64_t)r.src_end - r.src_begin;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = (uint32_t)(w / kp), pr = (uint32_t)(w % kp);
+        const uint32_t j = (uint32_t)local_to_global(i, g.rank, g.G, g.S);
+        if (j < r.dst_begin || j >= r.dst_end) continue;
+        const uint4 x = philox4x32_10(make_uint4(j, pr, r.index, kTagIndeg), g.key0, g.key1);
+        const uint32_t b = i / g.TW;
+#pragma unroll
+        for (uint32_t h = 0; h < 2; ++h) {
+            const uint32_t kk = 2u * pr + h;
+            if (kk >= r.k) break;
+            const uint64_t r64 = h ? (((uint64_t)x.w << 32) | x.z) : (((uint64_t)x.y << 32) | x.x);
+            const uint32_t s = r.src_begin + (uint32_t)__umul64hi(r64, nsrc);
+            const uint64_t seg = (uint64_t)s * (g.NT + 1) + b;
+            const uint32_t slot = atomicAdd(&cnt_or_cursor[seg], 1u);
+            if (FILL) ent[row_ptr[s] + bnd[seg] + slot] = (uint16_t)(i - b * g.TW);
+        }
+    }
+}
+
+// Per row: exclusive prefix of the NT segment counts (in place), row length into rowlen.
+__global__ void __launch_bounds__(256) row_prefix_kernel(GenGeom g, uint32_t *cnt, uint64_t *rowlen) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * 8;
+    for (uint64_t s = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); s < g.N; s += nwarps) {
+        uint32_t *row = cnt + s * (g.NT + 1);
+        uint32_t carry = 0;
+        for (uint32_t b0 = 0; b0 < g.NT; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            const uint32_t c = b < g.NT ? row[b] : 0u;
+            const uint32_t incl = warp_incl_scan(c, lane);
+            if (b < g.NT) row[b] = carry + incl - c;
+            carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+        if (lane == 0) { row[g.NT] = carry; rowlen[s] = carry; }
+    }
+}
+
+// Exclusive scan of n u64 values (in place, out[n] = total); 3 kernels.
+constexpr int kScanBlock = 1024;
+__global__ void scan_block_sums(const uint64_t *in, uint64_t n, uint64_t *sums) {
+    __shared__ uint64_t red[32];
+    const uint64_t i = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
+    uint64_t v = i < n ? in[i] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t t = 0;
+        for (int w = 0; w < kScanBlock / 32; ++w) t += red[w];
+        sums[blockIdx.x] = t;
+    }
+}
+__global__ void scan_sums_serial(uint64_t *sums, uint64_t nb) {
+    // single block: chunked exclusive scan of the block sums
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint64_t base = 0; base < nb; base += kScanBlock) {
+        __shared__ uint64_t buf[kScanBlock];
+        const uint64_t i = base + threadIdx.x;
+        buf[threadIdx.x] = i < nb ? sums[i] : 0;
+        __syncthreads();
+        for (int o = 1; o < kScanBlock; o <<= 1) {
+            const uint64_t y = threadIdx.x >= (unsigned)o ? buf[threadIdx.x - o] : 0;
+            __syncthreads();
+            buf[threadIdx.x] += y;
+            __syncthreads();
+        }
+        const uint64_t incl = buf[threadIdx.x];
+        const uint64_t excl = incl - (i < nb ? sums[i] : 0);
+        __syncthreads();
+        if (i < nb) sums[i] = carry + excl;
+        __syncthreads();
+        if (threadIdx.x == kScanBlock - 1) carry += incl;
+        __syncthreads();
+    }
+}
+__global__ void scan_apply(const uint64_t *in, uint64_t n, const uint64_t *sums, uint64_t *out) {
+    __shared__ uint64_t buf[kScanBlock];
+    const uint64_t i = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
+    const uint64_t v = i < n ? in[i] : 0;
+    buf[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < kScanBlock; o <<= 1) {
+        const uint64_t y = threadIdx.x >= (unsigned)o ? buf[threadIdx.x - o] : 0;
+        __syncthreads();
+        buf[threadIdx.x] += y;
+        __syncthreads();
+    }
+    if (i < n) out[i] = sums[blockIdx.x] + buf[threadIdx.x] - v;
+    if (i == n - 1) out[n] = sums[blockIdx.x] + buf[threadIdx.x];
+}
+
+// Insertion sort of each (row, tile) segment (fixed in-degree fills out of order).
+__global__ void __launch_bounds__(256) sort_segments_kernel(GenGeom g, const uint64_t *row_ptr,
+                                                            const uint32_t *bnd, uint16_t *ent) {
+    const uint64_t total = (uint64_t)g.N * g.NT;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = (uint32_t)(w / g.NT), b = (uint32_t)(w % g.NT);
+        const uint64_t seg = (uint64_t)s * (g.NT + 1) + b;
+        const uint32_t b0 = bnd[seg], b1 = bnd[seg + 1];
+        if (b1 - b0 < 2) continue;
+        uint16_t *p = ent + row_ptr[s] + b0;
+        const uint32_t len = b1 - b0;
+        for (uint32_t x = 1; x < len; ++x) {
+            const uint16_t key = p[x];
+            uint32_t y = x;
+            while (y > 0 && p[y - 1] > key) { p[y] = p[y - 1]; --y; }
+            p[y] = key;
+        }
+    }
+}
+
+__global__ void init_uniform_kernel(GenGeom g, uint32_t field, float lo, float hi, float *out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n_own) return;
+    const uint32_t j = (uint32_t)local_to_global(i, g.rank, g.G, g.S);
+    const uint4 x = philox4x32_10(make_uint4(j >> 2, field, 0u, kTagInit), g.key0, g.key1);
+    // u = (x >> 8) 2^-24 exactly; value = lo + u (hi - lo) (reading R15)
+    const float u = __fmul_rn(__uint2float_rn(word_of(x, j & 3) >> 8), 5.9604644775390625e-08f);
+    out[i] = __fadd_rn(lo, __fmul_rn(u, __fsub_rn(hi, lo)));
+}
+
+static int grid_for(uint64_t work, int per_block) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (work + per_block - 1) / per_block;
+    const uint64_t cap = (uint64_t)nsm * 16;
+    return (int)(want < cap ? (want ? want : 1) : cap);
+}
+
+cudaError_t gen_count(const GenGeom &g, const GenRule &r, uint32_t *cnt, cudaStream_t s) {
+    if (r.src_end <= r.src_begin || r.dst_end <= r.dst_begin) return cudaSuccess;
+    if (r.kind == 0) {
+        if (r.thr == 0) return cudaSuccess;
+        count_prob_kernel<<<grid_for((uint64_t)(r.src_end - r.src_begin) * g.NT, 8), 256, 0, s>>>(g, r, cnt);
+    } else {
+        if (r.k == 0) return cudaSuccess;
+        indeg_kernel<false><<<grid_for((uint64_t)g.n_own * ((r.k + 1) / 2), 256), 256, 0, s>>>(
+            g, r, nullptr, nullptr, cnt, nullptr);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t gen_scan(const GenGeom &g, uint32_t *cnt_bnd, uint64_t *row_ptr, uint64_t *nnz,
+                     cudaStream_t s) {
+    cudaError_t e;
+    row_prefix_kernel<<<grid_for(g.N, 8), 256, 0, s>>>(g, cnt_bnd, row_ptr);
+    if ((e = cudaGetLastError())) return e;
+    const uint64_t n = g.N;
+    const uint64_t nb = (n + kScanBlock - 1) / kScanBlock;
+    uint64_t *sums = nullptr;
+    if ((e = cudaMallocAsync(&sums, nb * sizeof(uint64_t), s))) return e;
+    scan_block_sums<<<(unsigned)nb, kScanBlock, 0, s>>>(row_ptr, n, sums);
+    scan_sums_serial<<<1, kScanBlock, 0, s>>>(sums, nb);
+    scan_apply<<<(unsigned)nb, kScanBlock, 0, s>>>(row_ptr, n, sums, row_ptr);
+    if ((e = cudaGetLastError())) return e;
+    if ((e = cudaFreeAsync(sums, s))) return e;
+    if ((e = cudaMemcpyAsync(nnz, row_ptr + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s))) return e;
+    return cudaStreamSynchronize(s);
+}
+
+cudaError_t gen_fill(const GenGeom &g, const GenRule &r, const uint64_t *row_ptr,
+                     const uint32_t *bnd, uint32_t *cursor, uint16_t *ent, cudaStream_t s) {
+    if (r.src_end <= r.src_begin || r.dst_end <= r.dst_begin) return cudaSuccess;
+    if (r.kind == 0) {
+        if (r.thr == 0) return cudaSuccess;
+        fill_prob_kernel<<<grid_for((uint64_t)(r.src_end - r.src_begin) * g.NT, 8), 256, 0, s>>>(
+            g, r, row_ptr, bnd, cursor, ent);
+    } else {
+        if (r.k == 0) return cudaSuccess;
+        indeg_kernel<true><<<grid_for((uint64_t)g.n_own * ((r.k + 1) / 2), 256), 256, 0, s>>>(
+            g, r, row_ptr, bnd, cursor, ent);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t gen_sort_segments(const GenGeom &g, const uint64_t *row_ptr, const uint32_t *bnd,
+                              uint16_t *ent, cudaStream_t s) {
+    sort_segments_kernel<<<grid_for((uint64_t)g.N * g.NT, 256), 256, 0, s>>>(g, row_ptr, bnd, ent);
+    return cudaGetLastError();
+}
+
+cudaError_t gen_init_uniform(const GenGeom &g, uint32_t field, float lo, float hi, float *out,
+                             cudaStream_t s) {
+    if (g.n_own == 0) return cudaSuccess;
+    init_uniform_kernel<<<(g.n_own + 255) / 256, 256, 0, s>>>(g, field, lo, hi, out);
+    return cudaGetLastError();
+}
+
+}  // namespace spice

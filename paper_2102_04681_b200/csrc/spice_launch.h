@@ -1,0 +1,43 @@
+// spice_launch.h — host launchers shared by the library's translation units.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "spice_internal.cuh"
+
+namespace spice {
+
+// ---- step kernels (sim.cu) ----
+cudaError_t launch_update(const SimArgs &a, uint32_t k, bool produce_list, cudaStream_t s);
+cudaError_t prepare_deliver(uint32_t tile_width);
+size_t deliver_smem_bytes(uint32_t tile_width);
+cudaError_t launch_deliver(const SimArgs &a, uint32_t k, double mean_segment, int n_sm, cudaStream_t s);
+cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s);
+cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s);
+
+// ---- generator (gen.cu) ----
+struct GenRule {
+    uint32_t src_begin, src_end, dst_begin, dst_end, kind, k, index;
+    uint64_t thr;   // floor(p 2^32), 2^32 = always
+};
+struct GenGeom {
+    uint32_t N, n_own, rank, G, S, TW, NT;
+    uint32_t key0, key1;
+};
+// Count segment lengths cnt[s*(NT+1)+b] (+=) for one rule.
+cudaError_t gen_count(const GenGeom &g, const GenRule &r, uint32_t *cnt, cudaStream_t s);
+// cnt -> bnd (exclusive prefix within each row, in place; element NT = row length) and
+// row_ptr (exclusive prefix over rows).  Returns nnz through *nnz (synchronises).
+cudaError_t gen_scan(const GenGeom &g, uint32_t *cnt_bnd, uint64_t *row_ptr, uint64_t *nnz,
+                     cudaStream_t s);
+// Fill the entries of one rule; cursor[s*(NT+1)+b] counts entries already written.
+cudaError_t gen_fill(const GenGeom &g, const GenRule &r, const uint64_t *row_ptr,
+                     const uint32_t *bnd, uint32_t *cursor, uint16_t *ent, cudaStream_t s);
+// Sort every (row, tile) segment ascending.
+cudaError_t gen_sort_segments(const GenGeom &g, const uint64_t *row_ptr, const uint32_t *bnd,
+                              uint16_t *ent, cudaStream_t s);
+// Initial state (reading R15).
+cudaError_t gen_init_uniform(const GenGeom &g, uint32_t field, float lo, float hi, float *out,
+                             cudaStream_t s);
+
+}  // namespace spice

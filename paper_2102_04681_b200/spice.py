@@ -1,0 +1,271 @@
+"""Thin ctypes binding of libspice.so (include/spice.h).  Argument marshalling only:
+every step of the hot path runs in the library's CUDA kernels.  There is no CPU
+fallback: if the library is missing or no GPU is visible, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libspice.so")
+
+OK, EINVAL, ENOMEM, ECUDA, ENCCL, ERANGE, ETRUNC, ESTATE = range(8)
+VOGELS, BRUNEL, BRUNEL_PLUS, SYNTH = 1, 2, 3, 4
+FLAG_EXTERNAL_EXCHANGE, FLAG_GLOBAL_ATOMICS = 0x1, 0x2
+FIELD_V, FIELD_GE, FIELD_GI, FIELD_REF, FIELD_ACC, FIELD_XTR, FIELD_YTR = range(7)
+ABI_VERSION = 1
+
+
+class SpiceError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[status {status}] {msg}")
+        self.status = status
+
+
+class Rule(C.Structure):
+    _fields_ = [("src_begin", C.c_uint32), ("src_end", C.c_uint32),
+                ("dst_begin", C.c_uint32), ("dst_end", C.c_uint32),
+                ("kind", C.c_uint32), ("k", C.c_uint32), ("plastic", C.c_uint32),
+                ("reserved", C.c_uint32), ("p", C.c_double)]
+
+
+class Config(C.Structure):
+    _fields_ = [("abi_version", C.c_uint32), ("model", C.c_uint32),
+                ("n_neurons", C.c_uint32), ("n_exc", C.c_uint32),
+                ("rules", C.POINTER(Rule)), ("n_rules", C.c_uint32),
+                ("delay_steps", C.c_uint32), ("dt_ms", C.c_double), ("seed", C.c_uint64),
+                ("activity", C.c_double), ("model_params", C.POINTER(C.c_double)),
+                ("n_model_params", C.c_uint32), ("rank", C.c_uint32), ("world_size", C.c_uint32),
+                ("slice_width", C.c_uint32), ("device", C.c_int32), ("nccl_unique_id", C.c_void_p),
+                ("record_steps", C.c_uint32), ("flags", C.c_uint32), ("tile_width", C.c_uint32),
+                ("ctas_per_tile", C.c_uint32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libspice.so (fails loudly when it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2102_04681_b200.build`")
+    L = C.CDLL(LIB_PATH)
+    vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+    st = C.c_int
+    sigs = {
+        "spice_create_network": (st, [C.POINTER(Config), C.POINTER(vp)]),
+        "spice_step": (st, [vp, u64]),
+        "spice_read_spikes": (st, [vp, u64, u64, vp, u64, vp, C.POINTER(u64)]),
+        "spice_free": (st, [vp]),
+        "spice_read_connectivity": (st, [vp, u32, u32, vp, u64, vp, C.POINTER(u64)]),
+        "spice_read_state": (st, [vp, u32, vp, u64]),
+        "spice_write_state": (st, [vp, u32, vp, u64]),
+        "spice_read_input": (st, [vp, u32, vp, vp, u64]),
+        "spice_read_weights": (st, [vp, u32, u32, vp, u64, C.POINTER(u64)]),
+        "spice_force_spikes": (st, [vp, vp, u64, i32]),
+        "spice_stats": (st, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
+        "spice_stream": (vp, [vp]),
+        "spice_sync": (st, [vp]),
+        "spice_info": (st, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32), C.POINTER(u32),
+                            C.POINTER(u32), C.POINTER(u64)]),
+        "spice_kernels_per_step": (u32, [vp]),
+        "spice_profile": (st, [vp, u64, vp, u32, C.POINTER(u32)]),
+        "spice_last_error": (C.c_char_p, []),
+        "spice_nccl_unique_id": (st, [vp]),
+        "spice_exchange_begin": (st, [vp]),
+        "spice_exchange_end": (st, [vp]),
+        "spice_exchange_put": (st, [vp, vp]),
+        "spice_partition_owner": (u32, [u64, u32, u32]),
+        "spice_partition_local_to_global": (u64, [u64, u32, u32, u32]),
+        "spice_partition_owned_count": (u64, [u64, u32, u32, u32]),
+        "spice_default_slice_width": (u32, [u64, u32]),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    _lib = L
+    return L
+
+
+def _check(status: int) -> None:
+    if status != OK:
+        raise SpiceError(status, lib().spice_last_error().decode())
+
+
+# ------------------------------------------------------------- host-only helpers
+def partition_owner(j: int, world_size: int, slice_width: int) -> int:
+    return lib().spice_partition_owner(j, world_size, slice_width)
+
+
+def partition_local_to_global(i: int, rank: int, world_size: int, slice_width: int) -> int:
+    return lib().spice_partition_local_to_global(i, rank, world_size, slice_width)
+
+
+def partition_owned_count(n: int, rank: int, world_size: int, slice_width: int) -> int:
+    return lib().spice_partition_owned_count(n, rank, world_size, slice_width)
+
+
+def default_slice_width(n: int, world_size: int) -> int:
+    return lib().spice_default_slice_width(n, world_size)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().spice_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Network:
+    """One rank's slice of a network (``spice_net``).
+
+    ``cfg`` is any object with the fields of ``workloads.NetConfig`` (model, n, n_exc,
+    rules, dt_ms, delay, seed, activity, params)."""
+
+    def __init__(self, cfg, rank: int = 0, world_size: int = 1, slice_width: int = 0,
+                 device: int = 0, record_steps: int = 1024, nccl_id: Optional[bytes] = None,
+                 external_exchange: bool = False, global_atomics: bool = False,
+                 tile_width: int = 0, ctas_per_tile: int = 0):
+        L = lib()
+        self._rules = (Rule * max(1, len(cfg.rules)))()
+        for q, r in enumerate(cfg.rules):
+            self._rules[q] = Rule(r.src[0], r.src[1], r.dst[0], r.dst[1], r.kind, r.k,
+                                  1 if r.plastic else 0, 0, float(r.p))
+        self._params = (C.c_double * max(1, len(cfg.params)))(*cfg.params)
+        self._nccl = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        flags = (FLAG_EXTERNAL_EXCHANGE if external_exchange else 0) | \
+                (FLAG_GLOBAL_ATOMICS if global_atomics else 0)
+        c = Config(ABI_VERSION, cfg.model, cfg.n, cfg.n_exc, self._rules, len(cfg.rules),
+                   cfg.delay, cfg.dt_ms, cfg.seed, cfg.activity, self._params, len(cfg.params),
+                   rank, world_size, slice_width, device,
+                   C.cast(self._nccl, C.c_void_p) if self._nccl else None,
+                   record_steps, flags, tile_width, ctas_per_tile)
+        h = C.c_void_p()
+        _check(L.spice_create_network(C.byref(c), C.byref(h)))
+        self.h = h
+        self.cfg, self.rank, self.world_size = cfg, rank, world_size
+        self.n = cfg.n
+        info = self.info()
+        self.n_owned = info["n_owned"]
+        self.slice_width = slice_width or default_slice_width(cfg.n, world_size)
+
+    # lifecycle ---------------------------------------------------------------
+    def free(self) -> None:
+        if getattr(self, "h", None):
+            lib().spice_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.free()
+
+    # hot path ----------------------------------------------------------------
+    def step(self, n_steps: int = 1) -> None:
+        _check(lib().spice_step(self.h, n_steps))
+
+    def read_spikes(self, t_begin: int, t_end: int):
+        """List (per step) of ascending global spike IDs for steps [t_begin, t_end)."""
+        L = lib()
+        total = C.c_uint64(0)
+        offs = np.zeros(t_end - t_begin + 1, dtype=np.uint64)
+        st = L.spice_read_spikes(self.h, t_begin, t_end, None, 0, offs.ctypes.data, C.byref(total))
+        if st not in (OK, ETRUNC):
+            _check(st)
+        ids = np.zeros(max(1, total.value), dtype=np.uint32)
+        _check(L.spice_read_spikes(self.h, t_begin, t_end, ids.ctypes.data, ids.size,
+                                   offs.ctypes.data, C.byref(total)))
+        return [ids[int(offs[q]):int(offs[q + 1])].copy() for q in range(t_end - t_begin)]
+
+    def read_spikes_into(self, t_begin: int, t_end: int, ids: np.ndarray, offs: np.ndarray) -> int:
+        """Zero-allocation variant for timing loops; returns the spike count."""
+        total = C.c_uint64(0)
+        _check(lib().spice_read_spikes(self.h, t_begin, t_end, ids.ctypes.data, ids.size,
+                                       offs.ctypes.data, C.byref(total)))
+        return total.value
+
+    # parity hooks --------------------------------------------------------------
+    def connectivity(self, row_begin: int = 0, row_end: Optional[int] = None):
+        L = lib()
+        row_end = self.n if row_end is None else row_end
+        total = C.c_uint64(0)
+        offs = np.zeros(row_end - row_begin + 1, dtype=np.uint64)
+        st = L.spice_read_connectivity(self.h, row_begin, row_end, None, 0, offs.ctypes.data, C.byref(total))
+        if st not in (OK, ETRUNC):
+            _check(st)
+        tg = np.zeros(max(1, total.value), dtype=np.uint32)
+        _check(L.spice_read_connectivity(self.h, row_begin, row_end, tg.ctypes.data, tg.size,
+                                         offs.ctypes.data, C.byref(total)))
+        return offs, tg[: total.value]
+
+    def state(self, field: int) -> np.ndarray:
+        dt = np.uint32 if field in (FIELD_REF, FIELD_ACC) else np.float32
+        out = np.zeros(self.n_owned, dtype=dt)
+        _check(lib().spice_read_state(self.h, field, out.ctypes.data, self.n_owned))
+        return out
+
+    def write_state(self, field: int, values) -> None:
+        dt = np.uint32 if field in (FIELD_REF, FIELD_ACC) else np.float32
+        a = np.ascontiguousarray(values, dtype=dt)
+        _check(lib().spice_write_state(self.h, field, a.ctypes.data, a.size))
+
+    def input(self, rel: int = 0):
+        c = np.zeros(self.n_owned, dtype=np.uint32)
+        p = np.zeros(self.n_owned, dtype=np.int64)
+        _check(lib().spice_read_input(self.h, rel, c.ctypes.data, p.ctypes.data, self.n_owned))
+        return c, p
+
+    def force_next(self, ids: Sequence[int], mode: str = "replace") -> None:
+        a = np.ascontiguousarray(ids, dtype=np.uint32)
+        _check(lib().spice_force_spikes(self.h, a.ctypes.data, a.size, {"replace": 1, "add": 2}[mode]))
+
+    def stats(self):
+        s, f, d = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().spice_stats(self.h, C.byref(s), C.byref(f), C.byref(d)))
+        return {"steps": s.value, "fired": f.value, "delivered": d.value}
+
+    def info(self):
+        o, s, nt, tw, c, b = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint64()
+        _check(lib().spice_info(self.h, C.byref(o), C.byref(s), C.byref(nt), C.byref(tw), C.byref(c), C.byref(b)))
+        return {"n_owned": o.value, "n_synapses": s.value, "n_tiles": nt.value, "tile_width": tw.value,
+                "ctas_per_tile": c.value, "device_bytes": b.value}
+
+    def profile(self, n_steps: int):
+        """Average device ms per launch, each kernel bracketed by CUDA events on the
+        library stream: update, deliver, bitmap_to_list, allgather."""
+        out = np.zeros(4, dtype=np.float64)
+        nk = C.c_uint32()
+        _check(lib().spice_profile(self.h, n_steps, out.ctypes.data, 4, C.byref(nk)))
+        return {"update": out[0], "deliver": out[1], "bitmap_to_list": out[2], "allgather": out[3]}
+
+    def kernels_per_step(self) -> int:
+        return lib().spice_kernels_per_step(self.h)
+
+    @property
+    def stream(self) -> int:
+        return lib().spice_stream(self.h) or 0
+
+    def sync(self) -> None:
+        _check(lib().spice_sync(self.h))
+
+    # external exchange (virtual ranks on one GPU) -------------------------------
+    def exchange_begin(self) -> None:
+        _check(lib().spice_exchange_begin(self.h))
+
+    def exchange_end(self) -> None:
+        _check(lib().spice_exchange_end(self.h))
+
+    def exchange_put_from(self, src: "Network") -> None:
+        _check(lib().spice_exchange_put(self.h, src.h))
