@@ -232,16 +232,17 @@ def main_spice(args):
     value = events / (ms_max / 1e3)
 
     # ---- per-kernel live timing for the roofline (CUDA events around each launch) ----
-    p0 = net.stats()
     prof = net.profile(args.profile_steps)
-    p1 = net.stats()
-    ev_launch = (p1["delivered"] - p0["delivered"]) / args.profile_steps
-    sp_launch = allreduce(p1["fired"] - p0["fired"], dist.ReduceOp.SUM if world > 1 else None) / args.profile_steps
+    ev_step = events / args.steps              # per launch of the step's delivery kernel
+    sp_step = fired / args.steps
     # 4 B target record per event + 12 B per spike (row pointer + list entry)
-    bytes_launch = 4.0 * ev_launch + 12.0 * sp_launch
+    bytes_launch = 4.0 * ev_step + 12.0 * sp_step
     peak, peak_src = hbm_peak()
-    achieved = bytes_launch / (prof["deliver"] * 1e-3) / 1e9
-    step_ms_prof = prof["update"] + prof["deliver"] + prof["bitmap_to_list"] + prof["allgather"]
+    fused = prof["fused"] > 0
+    kern = "k_fused (deliver t + update t+1)" if fused else ("k_global_atomics" if args.global_atomics else "k_deliver")
+    launch_ms = prof["fused"] if fused else prof["deliver"]
+    achieved = bytes_launch / (launch_ms * 1e-3) / 1e9
+    step_ms_prof = prof["fused"] if fused else prof["update"] + prof["deliver"] + prof["exchange"]
 
     # ---- end to end through the public API: step + read that step's spikes to host ----
     G, Sw = world, net.slice_width
@@ -286,11 +287,12 @@ def main_spice(args):
                                f"tiled smem, {info['n_tiles']} tiles x {info['tile_width']} targets, {info['ctas_per_tile']} CTA/tile",
                    "l2": "no flush: synapse stream per step >> 126 MB L2 is read from 12 GB/GPU",
                    "setup_s": setup_s},
-        "roofline": {"bound": "hbm", "kernel": "deliver", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                     "bytes_per_launch": bytes_launch, "launch_ms": prof["deliver"],
-                     "bytes_model": "SURVEY §8(d): 4 B/event + 12 B/spike", "peak_source": peak_src,
-                     "deliver_share_of_step": prof["deliver"] / step_ms_prof if step_ms_prof else None,
+                     "bytes_per_launch": bytes_launch, "launch_ms": launch_ms,
+                     "bytes_model": "SURVEY §8(d): 4 B/event + 12 B/spike (delivery bytes only)",
+                     "peak_source": peak_src,
+                     "kernel_share_of_step": launch_ms / step_ms_prof if step_ms_prof else None,
                      "kernel_ms": prof},
         "e2e": {"value": e2e_value, "unit": "events/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,

@@ -62,6 +62,8 @@ enum { SPICE_FIXED_PROB = 0, SPICE_FIXED_INDEGREE = 1 };
                                               between spice_exchange_begin / _end */
 #define SPICE_FLAG_GLOBAL_ATOMICS    0x2u  /* deliver with the paper-style column-wise
                                               warps and global atomics (A/B baseline) */
+#define SPICE_FLAG_UNFUSED           0x4u  /* G = 1: separate update and delivery kernels
+                                              instead of the fused deliver(t)+update(t+1) */
 
 typedef struct {
     uint32_t src_begin, src_end;   /* range1, half-open global IDs */
@@ -179,8 +181,9 @@ SPICE_API spice_status spice_info(spice_net *net, uint64_t *n_owned, uint64_t *n
 
 /* Run n_steps steps with each kernel launched individually and bracketed by CUDA events
  * on the library stream; writes the average device time per launch in ms:
- * [0] neuron update, [1] spike delivery, [2] bitmap->list (G > 1), [3] NCCL all-gather
- * (G > 1).  *n_kernels = entries written (cap >= 4).  Synchronises. */
+ * [0] neuron update kernel, [1] delivery kernel, [2] fused deliver(t)+update(t+1) kernel
+ * (G = 1; 0 otherwise), [3] exchange (NCCL all-gather + bitmap->list; G > 1).
+ * *n_kernels = entries written (cap >= 4).  Synchronises. */
 SPICE_API spice_status spice_profile(spice_net *net, uint64_t n_steps, double *ms_per_kernel,
                                      uint32_t cap, uint32_t *n_kernels);
 
@@ -213,6 +216,12 @@ SPICE_API uint64_t spice_partition_local_to_global(uint64_t i, uint32_t rank, ui
                                          uint32_t slice_width);
 SPICE_API uint64_t spice_partition_owned_count(uint64_t n, uint32_t rank, uint32_t world_size,
                                      uint32_t slice_width);
+/* Decode one step's gathered bitmaps (G segments of W words; bit i of segment r =
+ * local index i of rank r) into ascending global IDs (the union of all ranks' spikes,
+ * Fig. 2).  ETRUNC with *total when cap is too small. */
+SPICE_API spice_status spice_decode_bitmaps(const uint32_t *words, uint32_t world_size, uint32_t W,
+                                            uint32_t slice_width, uint32_t *ids, uint64_t cap,
+                                            uint64_t *total);
 /* Default S: a multiple of 32 giving each rank >= ~100 slices when N allows. */
 SPICE_API uint32_t spice_default_slice_width(uint64_t n, uint32_t world_size);
 

@@ -75,6 +75,12 @@ def lib(precision: str = "mirror32"):
     L.orc_owner.restype = u32; L.orc_owner.argtypes = [u64, u32, u32]
     L.orc_local_to_global.restype = u64; L.orc_local_to_global.argtypes = [u64, u32, u32, u32]
     L.orc_sizeof_real.restype = u32
+    L.orc_row.restype = u64
+    L.orc_row.argtypes = [C.POINTER(_Rule), u32, u64, u32, u32, u32, u32, vp, u64]
+    L.orc_col.restype = u64
+    L.orc_col.argtypes = [C.POINTER(_Rule), u32, u64, u32, vp, u64]
+    L.orc_set_input.argtypes = [vp, u32, vp]
+    L.orc_set_time.argtypes = [vp, u64]
     _LIBS[tag] = L
     return L
 
@@ -91,6 +97,36 @@ def poisson_table(lam: float) -> np.ndarray:
     out = np.zeros(1024, dtype=np.uint64)
     n = lib().orc_poisson_table(lam, out.ctypes.data, 1024)
     return out[:n]
+
+
+def _rules(cfg):
+    rules = (_Rule * max(1, len(cfg.rules)))()
+    for i, r in enumerate(cfg.rules):
+        rules[i] = _Rule(r.src[0], r.src[1], r.dst[0], r.dst[1], r.kind, r.k, 1 if r.plastic else 0, 0, float(r.p))
+    return rules
+
+
+def row(cfg, s: int, part: Optional[tuple] = None) -> np.ndarray:
+    """Sorted targets of source s (brute force, no network built)."""
+    g, G, S = part if part else (0, 1, 1)
+    cap = 1 << 16
+    while True:
+        out = np.zeros(cap, dtype=np.uint32)
+        n = lib().orc_row(_rules(cfg), len(cfg.rules), cfg.seed, s, g, G, S, out.ctypes.data, cap)
+        if n <= cap:
+            return out[:n]
+        cap = int(n)
+
+
+def col(cfg, j: int) -> np.ndarray:
+    """Sorted sources (with multiplicity) of all edges into target j."""
+    cap = 1 << 16
+    while True:
+        out = np.zeros(cap, dtype=np.uint32)
+        n = lib().orc_col(_rules(cfg), len(cfg.rules), cfg.seed, j, out.ctypes.data, cap)
+        if n <= cap:
+            return out[:n]
+        cap = int(n)
 
 
 def owner(j: int, G: int, S: int) -> int:
@@ -194,6 +230,15 @@ class OracleNet:
         if self.L.orc_get_input(self.h, rel, c.ctypes.data, p.ctypes.data) != 0:
             raise ValueError(rel)
         return c, p
+
+    def set_input(self, rel: int, counts) -> None:
+        a = np.ascontiguousarray(counts, dtype=np.uint32)
+        assert a.shape == (self.n,)
+        if self.L.orc_set_input(self.h, rel, a.ctypes.data) != 0:
+            raise ValueError(rel)
+
+    def set_time(self, t: int) -> None:
+        self.L.orc_set_time(self.h, t)
 
     def force_next(self, ids, mode: str = "replace") -> None:
         a = np.ascontiguousarray(ids, dtype=np.uint32)

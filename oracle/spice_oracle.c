@@ -184,41 +184,111 @@ static int cmp_tp(const void *a, const void *b)
 
 static int owned(const orc_net *N, uint64_t j) { return N->pG <= 1 || orc_owner(j, N->pG, N->pS) == N->pg; }
 
+/* The two edge rules (reading R9), written once and used by the build and by the
+ * sampled-row / sampled-column queries below. */
+static int prob_edge(uint32_t key0, uint32_t key1, uint32_t r, uint64_t thr, uint64_t s, uint64_t j)
+{
+    /* edge s -> j iff Philox(ctr=(s, j>>2, r, TAG_CONN))[j & 3] < floor(p 2^32) */
+    uint32_t x = philox_word((uint32_t)s, (uint32_t)(j >> 2), r, TAG_CONN, key0, key1, (unsigned)(j & 3));
+    return (uint64_t)x < thr;
+}
+static uint64_t indeg_source(uint32_t key0, uint32_t key1, uint32_t r, const orc_rule *R, uint64_t j, uint32_t k)
+{
+    /* target j's k-th draw: r64 from Philox(ctr=(j, k>>1, r, TAG_INDEG)) words 2(k&1),
+     * 2(k&1)+1; source = src_begin + floor(r64 |src| / 2^64). */
+    uint64_t nsrc = (uint64_t)R->src_end - R->src_begin;
+    uint32_t ctr[4] = { (uint32_t)j, k >> 1, r, TAG_INDEG }, key[2] = { key0, key1 }, o[4];
+    orc_philox(ctr, key, o);
+    uint64_t r64 = ((uint64_t)o[2 * (k & 1) + 1] << 32) | o[2 * (k & 1)];
+    return R->src_begin + (uint64_t)(((unsigned __int128)r64 * nsrc) >> 64);
+}
+
 /* Edge enumeration by brute force.  pass 0 counts per source, pass 1 fills.  */
 static void enumerate_edges(orc_net *N, int pass, uint64_t *cursor)
 {
     for (uint32_t r = 0; r < N->n_rules; r++) {
         const orc_rule *R = &N->rules[r];
         if (R->kind == ORC_FIXED_PROB) {
-            /* edge s -> j iff Philox(ctr=(s, j>>2, r, TAG_CONN))[j & 3] < floor(p 2^32) */
             uint64_t thr = prob_threshold(R->p);
             for (uint64_t s = R->src_begin; s < R->src_end; s++)
                 for (uint64_t j = R->dst_begin; j < R->dst_end; j++) {
                     if (!owned(N, j)) continue;
-                    uint32_t x = philox_word((uint32_t)s, (uint32_t)(j >> 2), r, TAG_CONN,
-                                             N->key0, N->key1, (unsigned)(j & 3));
-                    if ((uint64_t)x < thr) {
+                    if (prob_edge(N->key0, N->key1, r, thr, s, j)) {
                         if (pass == 0) N->row_ptr[s + 1]++;
                         else { uint64_t e = cursor[s]++; N->tgt[e] = (uint32_t)j; N->plastic[e] = (uint8_t)R->plastic; }
                     }
                 }
         } else {
-            /* target j draws k sources: r64 from Philox(ctr=(j, k>>1, r, TAG_INDEG))
-             * words 2(k&1), 2(k&1)+1; source = src_begin + floor(r64 |src| / 2^64). */
-            uint64_t nsrc = (uint64_t)R->src_end - R->src_begin;
             for (uint64_t j = R->dst_begin; j < R->dst_end; j++) {
                 if (!owned(N, j)) continue;
                 for (uint32_t k = 0; k < R->k; k++) {
-                    uint32_t ctr[4] = { (uint32_t)j, k >> 1, r, TAG_INDEG }, key[2] = { N->key0, N->key1 }, o[4];
-                    orc_philox(ctr, key, o);
-                    uint64_t r64 = ((uint64_t)o[2 * (k & 1) + 1] << 32) | o[2 * (k & 1)];
-                    uint64_t s = R->src_begin + (uint64_t)(((unsigned __int128)r64 * nsrc) >> 64);
+                    uint64_t s = indeg_source(N->key0, N->key1, r, R, j, k);
                     if (pass == 0) N->row_ptr[s + 1]++;
                     else { uint64_t e = cursor[s]++; N->tgt[e] = (uint32_t)j; N->plastic[e] = (uint8_t)R->plastic; }
                 }
             }
         }
     }
+}
+
+static int cmp_u32v(const void *a, const void *b)
+{
+    uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* Sampled row: the sorted targets of source s under all rules (brute force over all
+ * targets; fixed in-degree rules scan every target's draws), restricted to targets
+ * owned by rank pg of pG with slice width pS.  Returns the row length (writes at most cap). */
+EXPORT uint64_t orc_row(const orc_rule *rules, uint32_t n_rules, uint64_t seed, uint32_t s,
+                        uint32_t pg, uint32_t pG, uint32_t pS, uint32_t *out, uint64_t cap)
+{
+    uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
+    uint64_t n = 0;
+    for (uint32_t r = 0; r < n_rules; r++) {
+        const orc_rule *R = &rules[r];
+        if (R->kind == ORC_FIXED_PROB) {
+            if (s < R->src_begin || s >= R->src_end) continue;
+            uint64_t thr = prob_threshold(R->p);
+            for (uint64_t j = R->dst_begin; j < R->dst_end; j++) {
+                if (pG > 1 && orc_owner(j, pG, pS) != pg) continue;
+                if (prob_edge(key0, key1, r, thr, s, j)) { if (n < cap) out[n] = (uint32_t)j; n++; }
+            }
+        } else {
+            for (uint64_t j = R->dst_begin; j < R->dst_end; j++) {
+                if (pG > 1 && orc_owner(j, pG, pS) != pg) continue;
+                for (uint32_t k = 0; k < R->k; k++)
+                    if (indeg_source(key0, key1, r, R, j, k) == s) { if (n < cap) out[n] = (uint32_t)j; n++; }
+            }
+        }
+    }
+    if (n <= cap) qsort(out, n, sizeof(uint32_t), cmp_u32v);
+    return n;
+}
+
+/* Sampled column: the sources (with multiplicity, sorted) of all edges into target j. */
+EXPORT uint64_t orc_col(const orc_rule *rules, uint32_t n_rules, uint64_t seed, uint32_t j,
+                        uint32_t *out, uint64_t cap)
+{
+    uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
+    uint64_t n = 0;
+    for (uint32_t r = 0; r < n_rules; r++) {
+        const orc_rule *R = &rules[r];
+        if (j < R->dst_begin || j >= R->dst_end) continue;
+        if (R->kind == ORC_FIXED_PROB) {
+            uint64_t thr = prob_threshold(R->p);
+            for (uint64_t s = R->src_begin; s < R->src_end; s++)
+                if (prob_edge(key0, key1, r, thr, s, j)) { if (n < cap) out[n] = (uint32_t)s; n++; }
+        } else {
+            for (uint32_t k = 0; k < R->k; k++) {
+                uint64_t s = indeg_source(key0, key1, r, R, j, k);
+                if (n < cap) out[n] = (uint32_t)s;
+                n++;
+            }
+        }
+    }
+    if (n <= cap) qsort(out, n, sizeof(uint32_t), cmp_u32v);
+    return n;
 }
 
 static real init_uniform(const orc_net *N, uint32_t j, uint32_t field, double lo, double hi)
@@ -560,6 +630,18 @@ EXPORT int orc_get_input(const orc_net *N, uint32_t rel, uint32_t *counts, int64
     if (plastic_fx) memcpy(plastic_fx, N->pring + s, N->n * sizeof(int64_t));
     return 0;
 }
+
+/* Overwrite the input slot that the update of step (t_now + rel) will read. */
+EXPORT int orc_set_input(orc_net *N, uint32_t rel, const uint32_t *counts)
+{
+    if (rel >= N->D) return -1;
+    memcpy(N->ring + (size_t)((N->t + rel) % N->D) * N->n, counts, N->n * sizeof(uint32_t));
+    return 0;
+}
+
+/* Jump the step counter (the oracle's state is then treated as the state at step t);
+ * used to replay one step of a GPU run at full size. */
+EXPORT void orc_set_time(orc_net *N, uint64_t t) { N->t = t; if (N->t + 1 >= N->off_cap) { N->off_cap = N->t + 1024; N->sp_off = realloc(N->sp_off, (N->off_cap + 1) * sizeof(uint64_t)); N->delivered = realloc(N->delivered, N->off_cap * sizeof(uint64_t)); } for (uint64_t q = 0; q <= t; q++) N->sp_off[q] = N->sp_len; for (uint64_t q = 0; q < t; q++) N->delivered[q] = 0; }
 
 /* Teacher forcing of the NEXT step (t_now): mode 1 replaces its spike set by ids,
  * mode 2 adds ids to the naturally emitted set.  A forced spike resets the neuron

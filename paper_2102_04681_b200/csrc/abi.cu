@@ -53,6 +53,21 @@ NcclApi &nccl() {
     return api;
 }
 
+// gathered bitmaps -> ascending global IDs (host side of the exchange, Fig. 2 union)
+void decode_into(const uint32_t *bm, uint32_t G, uint32_t W, uint32_t S, std::vector<uint32_t> &L) {
+    L.clear();
+    for (uint32_t r = 0; r < G; ++r)
+        for (uint32_t w = 0; w < W; ++w) {
+            uint32_t bits = bm[(uint64_t)r * W + w];
+            while (bits) {
+                const uint32_t b = __builtin_ctz(bits);
+                bits &= bits - 1;
+                L.push_back((uint32_t)local_to_global((uint64_t)w * 32 + b, r, G, S));
+            }
+        }
+    if (G > 1) std::sort(L.begin(), L.end());
+}
+
 uint64_t owned_count(uint64_t n, uint32_t g, uint32_t G, uint32_t S) {
     const uint64_t full = n / ((uint64_t)S * G);           // complete rounds of G slices
     uint64_t c = full * S;
@@ -103,6 +118,8 @@ struct spice_net {
     uint64_t ring_stride = 0;
     uint64_t nnz = 0;
     double mean_seg = 0;
+    uint32_t NR = 1, RS = 32;    // spike-list regions
+    bool fused = true, global_atomics = false;
     // device memory
     std::vector<void *> allocs;
     uint64_t device_bytes = 0;
@@ -111,12 +128,20 @@ struct spice_net {
     uint16_t *ent_alloc = nullptr, *ent = nullptr;
     float *v = nullptr, *ge = nullptr, *gi = nullptr;
     uint32_t *ref = nullptr, *acc = nullptr, *ring = nullptr;
-    uint32_t *splist = nullptr, *spcount = nullptr, *record = nullptr, *sendbuf = nullptr, *gather = nullptr;
-    unsigned long long *stats = nullptr;
+    uint32_t *sl_ids = nullptr, *sl_counts = nullptr;
+    uint64_t *sl_rows = nullptr;
+    uint32_t *record = nullptr, *sendbuf = nullptr, *gather = nullptr;
+    unsigned long long *fired_cta = nullptr, *delivered_cta = nullptr;
     uint64_t *t0 = nullptr;
     uint32_t *force_bits = nullptr;
     uint64_t *force_ctl = nullptr;
     uint64_t *ptab = nullptr;
+    // Brunel+
+    float *w = nullptr, *xtr = nullptr, *ytr = nullptr;
+    long long *pring = nullptr;
+    uint64_t *in_ptr = nullptr, *in_pos = nullptr;
+    uint32_t *in_src = nullptr;
+    uint64_t n_plastic = 0;
     ModelConst mc{};
     SimArgs args{};
     // host progress
@@ -185,7 +210,7 @@ void dfree(spice_net *n, void *p) {
 spice_status validate(const spice_config *c) {
     if (!c) return fail(nullptr, SPICE_EINVAL, "null config");
     if (c->abi_version != SPICE_ABI_VERSION) return fail(nullptr, SPICE_EINVAL, "abi_version %u != %u", c->abi_version, SPICE_ABI_VERSION);
-    if (c->model != SPICE_VOGELS && c->model != SPICE_BRUNEL && c->model != SPICE_SYNTH)
+    if (c->model < SPICE_VOGELS || c->model > SPICE_SYNTH)
         return fail(nullptr, SPICE_EINVAL, "model %u not supported by this build", c->model);
     if (c->n_neurons == 0) return fail(nullptr, SPICE_EINVAL, "n_neurons must be > 0");
     if (c->n_exc > c->n_neurons) return fail(nullptr, SPICE_EINVAL, "n_exc > n_neurons");
@@ -196,7 +221,11 @@ spice_status validate(const spice_config *c) {
     if (c->record_steps == 0) return fail(nullptr, SPICE_EINVAL, "record_steps must be >= 1");
     if (c->tile_width && (c->tile_width % 32 || c->tile_width > kMaxTileWidth))
         return fail(nullptr, SPICE_EINVAL, "tile_width must be a multiple of 32 and <= %u", kMaxTileWidth);
-    const uint32_t need = c->model == SPICE_VOGELS ? 17 : c->model == SPICE_BRUNEL ? 10 : 0;
+    const uint32_t need = c->model == SPICE_VOGELS ? 17 : c->model == SPICE_BRUNEL ? 10
+                        : c->model == SPICE_BRUNEL_PLUS ? 16 : 0;
+    if (c->model == SPICE_BRUNEL_PLUS && c->ctas_per_tile > 1)
+        return fail(nullptr, SPICE_EINVAL, "Brunel+ needs one CTA per tile (ctas_per_tile = 1)");
+    uint32_t nplastic = 0;
     if (c->n_model_params < need || (need && !c->model_params))
         return fail(nullptr, SPICE_EINVAL, "model %u needs %u parameters, got %u", c->model, need, c->n_model_params);
     if (c->model == SPICE_SYNTH && !(c->activity >= 0 && c->activity <= 1))
@@ -208,7 +237,8 @@ spice_status validate(const spice_config *c) {
             return fail(nullptr, SPICE_EINVAL, "rule %u: ranges outside [0, N)", r);
         if (R.kind == SPICE_FIXED_PROB && !(R.p >= 0 && R.p <= 1)) return fail(nullptr, SPICE_EINVAL, "rule %u: p outside [0,1]", r);
         if (R.kind != SPICE_FIXED_PROB && R.kind != SPICE_FIXED_INDEGREE) return fail(nullptr, SPICE_EINVAL, "rule %u: unknown kind", r);
-        if (R.plastic) return fail(nullptr, SPICE_EINVAL, "rule %u: plastic synapses need model BRUNEL_PLUS", r);
+        if (R.plastic && c->model != SPICE_BRUNEL_PLUS) return fail(nullptr, SPICE_EINVAL, "rule %u: plastic synapses need model BRUNEL_PLUS", r);
+        if (R.plastic && ++nplastic > kMaxPlasticRules) return fail(nullptr, SPICE_EINVAL, "at most %d plastic rules", kMaxPlasticRules);
         for (uint32_t q = 0; q < r; ++q) {
             const spice_rule &Q = c->rules[q];
             const bool src_overlap = R.src_begin < Q.src_end && Q.src_begin < R.src_end;
@@ -229,39 +259,50 @@ void build_model_const(spice_net *n) {
         m.h = (float)(dt / P[0]); m.EL = (float)P[1]; m.Vt = (float)P[2]; m.Vr = (float)P[3];
         m.R = (uint32_t)std::llround(P[4] / dt); m.Ee = (float)P[5]; m.Ei = (float)P[6];
         m.ke = (float)(dt / P[7]); m.ki = (float)(dt / P[8]); m.dge = (float)P[9]; m.dgi = (float)P[10];
-    } else if (n->model == SPICE_BRUNEL) {
+    } else if (n->model == SPICE_BRUNEL || n->model == SPICE_BRUNEL_PLUS) {
         m.h = (float)(dt / P[0]); m.EL = (float)P[1]; m.theta = (float)P[2]; m.Vr = (float)P[3];
         m.R = (uint32_t)std::llround(P[4] / dt);
         m.JE = (float)P[5]; m.JI = (float)(-P[6] * P[5]);
+        if (n->model == SPICE_BRUNEL_PLUS) {
+            m.ap = (float)std::exp(-dt / P[10]); m.am = (float)std::exp(-dt / P[11]);
+            m.Ap = (float)P[12]; m.Am = (float)P[13]; m.wmax = (float)P[14];
+        }
     } else {
         m.thr_fire = prob_threshold(n->activity);
     }
 }
 
+// Enqueue steps k = 0..steps-1 of one replay (each kernel reads t = *t0 + k).
+spice_status enqueue_steps(spice_net *n, uint32_t steps) {
+    cudaStream_t s = n->stream;
+    const SimArgs &a = n->args;
+    if (n->G == 1 && n->fused && !n->global_atomics) {
+        CU(n, launch_update(a, 0, s));
+        for (uint32_t k = 0; k + 1 < steps; ++k) CU(n, launch_fused(a, k, s));   // deliver(k)+update(k+1)
+        CU(n, launch_deliver(a, steps - 1, false, n->n_sm, s));
+    } else {
+        for (uint32_t k = 0; k < steps; ++k) {
+            CU(n, launch_update(a, k, s));
+            if (n->G > 1) {
+                ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, s);
+                if (r != ncclSuccess) return fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
+                CU(n, launch_bitmap_to_list(a, k, s));
+            }
+            CU(n, launch_deliver(a, k, n->global_atomics, n->n_sm, s));
+        }
+    }
+    CU(n, launch_advance(n->t0, steps, s));
+    return SPICE_OK;
+}
+
 spice_status capture_graph(spice_net *n, uint32_t steps, cudaGraphExec_t *out) {
     cudaGraph_t g = nullptr;
     CU(n, cudaStreamBeginCapture(n->stream, cudaStreamCaptureModeThreadLocal));
-    cudaError_t err = cudaSuccess;
-    spice_status st = SPICE_OK;
-    for (uint32_t k = 0; k < steps && err == cudaSuccess && st == SPICE_OK; ++k) {
-        if (n->G == 1) {
-            err = launch_update(n->args, k, true, n->stream);
-        } else {
-            err = launch_update(n->args, k, false, n->stream);
-            if (err == cudaSuccess) {
-                ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, n->stream);
-                if (r != ncclSuccess) st = fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
-            }
-            if (err == cudaSuccess && st == SPICE_OK) err = launch_bitmap_to_list(n->args, k, n->stream);
-        }
-        if (err == cudaSuccess && st == SPICE_OK) err = launch_deliver(n->args, k, n->mean_seg, n->n_sm, n->stream);
-    }
-    if (err == cudaSuccess && st == SPICE_OK) err = launch_advance(n->t0, steps, n->stream);
+    spice_status st = enqueue_steps(n, steps);
     cudaError_t e2 = cudaStreamEndCapture(n->stream, &g);
     if (st != SPICE_OK) { if (g) cudaGraphDestroy(g); return st; }
-    if (err != cudaSuccess) { if (g) cudaGraphDestroy(g); return fail(n, SPICE_ECUDA, "graph capture: %s", cudaGetErrorString(err)); }
     if (e2 != cudaSuccess) return fail(n, SPICE_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(e2));
-    err = cudaGraphInstantiate(out, g, 0);
+    cudaError_t err = cudaGraphInstantiate(out, g, 0);
     cudaGraphDestroy(g);
     if (err != cudaSuccess) return fail(n, SPICE_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(err));
     return SPICE_OK;
@@ -281,7 +322,7 @@ void destroy(spice_net *n) {
 }
 
 // Exact post-generation check that packed 16-bit receptor counts cannot overflow:
-// the number of excitatory (inhibitory) in-synapses of any owned target is < 65536.
+// the number of excitatory (inhibitory) in-synapses of any owned target is < 65535.
 __global__ void indegree_kernel(const uint64_t *row_ptr, const uint32_t *bnd, const uint16_t *ent,
                                 uint32_t N, uint32_t NT, uint32_t TW, uint32_t n_exc, uint32_t *deg) {
     const uint32_t lane = threadIdx.x & 31;
@@ -356,7 +397,6 @@ spice_status generate(spice_net *n) {
         CU(n, cudaStreamSynchronize(n->stream));
         dfree(n, deg); dfree(n, mx);
         n->device_bytes -= n->ring_stride * 4 + 8;
-        // a 16-bit field saturates only if one target has >= 65535 in-synapses of a type
         if (h[0] >= 65535u || h[1] >= 65535u)
             return fail(n, SPICE_EINVAL, "a target has >= 65535 in-synapses of one receptor type; packed counts could overflow");
     }
@@ -385,6 +425,17 @@ uint32_t spice_default_slice_width(uint64_t n, uint32_t G) {
     const uint64_t s = n / (256ull * G);      // ~256 slices per rank ("hundreds")
     const uint64_t r = (s / 32) * 32;
     return (uint32_t)std::max<uint64_t>(32, std::min<uint64_t>(r, 1u << 20));
+}
+
+spice_status spice_decode_bitmaps(const uint32_t *words, uint32_t G, uint32_t W, uint32_t S,
+                                  uint32_t *ids, uint64_t cap, uint64_t *total) {
+    if (!words || !G || !S || S % 32) return fail(nullptr, SPICE_EINVAL, "bad bitmap geometry");
+    std::vector<uint32_t> L;
+    decode_into(words, G, W, S, L);
+    if (total) *total = L.size();
+    if (L.size() > cap || (!ids && !L.empty())) return fail(nullptr, SPICE_ETRUNC, "need %zu ids", L.size());
+    if (!L.empty()) memcpy(ids, L.data(), L.size() * 4);
+    return SPICE_OK;
 }
 
 spice_status spice_nccl_unique_id(void *out128) {
@@ -431,7 +482,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (c->tile_width) {
         n->TW = c->tile_width;
     } else {
-        const uint64_t want_tiles = 2ull * n->n_sm;
+        const uint64_t want_tiles = (uint64_t)n->n_sm;     // one tile CTA per SM
         uint64_t tw = (n->n_own + want_tiles - 1) / want_tiles;
         tw = (tw + 31) / 32 * 32;
         n->TW = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(tw, 32), kMaxTileWidth);
@@ -439,6 +490,14 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     n->NT = (uint32_t)std::max<uint64_t>(1, (n->n_own + n->TW - 1) / n->TW);
     n->C = c->ctas_per_tile ? c->ctas_per_tile : 1;
     n->ring_stride = (uint64_t)n->NT * n->TW;
+    n->global_atomics = (n->flags & SPICE_FLAG_GLOBAL_ATOMICS) != 0;
+    n->fused = !(n->flags & SPICE_FLAG_UNFUSED) && n->C == 1;
+    // spike-list regions: one per tile (G = 1, written by the tile's update) or one per
+    // kB2LWords gathered bitmap words (G > 1, written by bitmap->list)
+    if (n->G == 1) { n->NR = n->NT; n->RS = n->TW; }
+    else { n->NR = (uint32_t)(((uint64_t)n->G * n->W + kB2LWords - 1) / kB2LWords); n->RS = kB2LWords * 32; }
+    if (n->NR > kMaxRegions) return bail(fail(n, SPICE_EINVAL, "%u spike-list regions > %u: use a wider tile_width", n->NR, kMaxRegions));
+    if (tile_smem_bytes(n->TW, n->NR) > 227 * 1024) return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for shared memory", n->TW));
     // ---- NCCL communicator ----
     if (n->G > 1 && !n->external) {
         if (!nccl().ok) return bail(fail(n, SPICE_ENCCL, "libnccl.so.2 not found (set SPICE_NCCL_LIB)"));
@@ -449,15 +508,18 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     }
     // ---- connectivity (a0') ----
     if ((st = generate(n))) return bail(st);
-    // ---- state, ring, spike buffers ----
-    const uint64_t no = std::max<uint64_t>(n->n_own, 1);
+    // ---- state, ring, spike buffers (state padded to NT*TW for 16-byte vector access) ----
+    const uint64_t no = n->ring_stride;
+    const uint64_t nctas = (uint64_t)n->NT * n->C;
     if ((st = dalloc_t(n, &n->ring, (size_t)n->D * n->ring_stride, "input ring"))) return bail(st);
-    if ((st = dalloc_t(n, &n->splist, std::max<uint32_t>(n->N, 1), "spike list"))) return bail(st);
-    if ((st = dalloc_t(n, &n->spcount, 4, "spike counts"))) return bail(st);
+    if ((st = dalloc_t(n, &n->sl_ids, 2ull * n->NR * n->RS, "spike lists"))) return bail(st);
+    if ((st = dalloc_t(n, &n->sl_rows, 2ull * n->NR * n->RS, "spike list rows"))) return bail(st);
+    if ((st = dalloc_t(n, &n->sl_counts, 2ull * n->NR, "spike list counts"))) return bail(st);
     if ((st = dalloc_t(n, &n->record, (size_t)n->R * n->G * n->W, "spike record"))) return bail(st);
     if ((st = dalloc_t(n, &n->sendbuf, std::max<uint32_t>(n->W, 1), "send bitmap"))) return bail(st);
     if ((st = dalloc_t(n, &n->gather, (size_t)n->G * std::max<uint32_t>(n->W, 1), "gathered bitmaps"))) return bail(st);
-    if ((st = dalloc_t(n, &n->stats, 2, "stats"))) return bail(st);
+    if ((st = dalloc_t(n, &n->fired_cta, n->NT, "fired counters"))) return bail(st);
+    if ((st = dalloc_t(n, &n->delivered_cta, nctas, "delivered counters"))) return bail(st);
     if ((st = dalloc_t(n, &n->t0, 1, "step counter"))) return bail(st);
     if ((st = dalloc_t(n, &n->force_bits, std::max<uint32_t>(n->W, 1), "force bits"))) return bail(st);
     if ((st = dalloc_t(n, &n->force_ctl, 2, "force control"))) return bail(st);
@@ -470,15 +532,45 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (n->model == SPICE_SYNTH && (st = dalloc_t(n, &n->acc, no, "acc"))) return bail(st);
     cudaStream_t s = n->stream;
     CU(n, cudaMemsetAsync(n->ring, 0, (size_t)n->D * n->ring_stride * 4, s));
-    CU(n, cudaMemsetAsync(n->spcount, 0, 16, s));
+    CU(n, cudaMemsetAsync(n->sl_counts, 0, 2ull * n->NR * 4, s));
+    CU(n, cudaMemsetAsync(n->sendbuf, 0, std::max<uint32_t>(n->W, 1) * 4, s));   // words past the last tile stay 0
+    CU(n, cudaMemsetAsync(n->gather, 0, (size_t)n->G * std::max<uint32_t>(n->W, 1) * 4, s));
     CU(n, cudaMemsetAsync(n->record, 0, (size_t)n->R * n->G * n->W * 4, s));
-    CU(n, cudaMemsetAsync(n->stats, 0, 16, s));
+    CU(n, cudaMemsetAsync(n->fired_cta, 0, n->NT * 8ull, s));
+    CU(n, cudaMemsetAsync(n->delivered_cta, 0, nctas * 8, s));
     CU(n, cudaMemsetAsync(n->t0, 0, 8, s));
     CU(n, cudaMemsetAsync(n->force_bits, 0, std::max<uint32_t>(n->W, 1) * 4, s));
     CU(n, cudaMemsetAsync(n->force_ctl, 0xFF, 16, s));
     CU(n, cudaMemsetAsync(n->v, 0, no * 4, s));
     CU(n, cudaMemsetAsync(n->ref, 0, no * 4, s));
+    if (n->ge) CU(n, cudaMemsetAsync(n->ge, 0, no * 4, s));
+    if (n->gi) CU(n, cudaMemsetAsync(n->gi, 0, no * 4, s));
     if (n->acc) CU(n, cudaMemsetAsync(n->acc, 0, no * 4, s));
+    PlasticBoxes pbx{};
+    for (const spice_rule &R : n->rules)
+        if (R.plastic) { uint32_t *bx = pbx.box[pbx.n++]; bx[0] = R.src_begin; bx[1] = R.src_end; bx[2] = R.dst_begin; bx[3] = R.dst_end; }
+    if (n->model == SPICE_BRUNEL_PLUS) {
+        GenGeom g2{};
+        g2.N = n->N; g2.n_own = (uint32_t)n->n_own; g2.rank = n->rank; g2.G = n->G; g2.S = n->S;
+        g2.TW = n->TW; g2.NT = n->NT; g2.key0 = (uint32_t)n->seed; g2.key1 = (uint32_t)(n->seed >> 32);
+        uint32_t *tmp = nullptr;
+        if ((st = dalloc_t(n, &n->w, n->nnz + 8, "plastic weights"))) return bail(st);
+        if ((st = dalloc_t(n, &n->pring, (size_t)n->D * n->ring_stride, "plastic input ring"))) return bail(st);
+        if ((st = dalloc_t(n, &n->xtr, 2ull * n->N, "pre traces"))) return bail(st);
+        if ((st = dalloc_t(n, &n->ytr, no, "post traces"))) return bail(st);
+        if ((st = dalloc_t(n, &n->in_ptr, n->n_own + 1, "in-synapse index"))) return bail(st);
+        if ((st = dalloc_t(n, &tmp, std::max<uint64_t>(n->n_own, 1), "in-degree counts"))) return bail(st);
+        CU(n, cudaMemsetAsync(n->pring, 0, (size_t)n->D * n->ring_stride * 8, s));
+        CU(n, cudaMemsetAsync(n->xtr, 0, 2ull * n->N * 4, s));
+        CU(n, cudaMemsetAsync(n->ytr, 0, no * 4, s));
+        CU(n, gen_plastic(g2, pbx, n->row_ptr, n->bnd, n->ent, n->w, (float)n->prm[15], tmp, n->in_ptr,
+                          &n->in_pos, &n->in_src, &n->n_plastic, s));
+        n->allocs.push_back(n->in_pos);
+        n->allocs.push_back(n->in_src);
+        n->device_bytes += n->n_plastic * 12;
+        CU(n, cudaStreamSynchronize(s));
+        dfree(n, tmp);
+    }
     build_model_const(n);
     GenGeom g{};
     g.N = n->N; g.n_own = (uint32_t)n->n_own; g.rank = n->rank; g.G = n->G; g.S = n->S;
@@ -488,7 +580,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         CU(n, gen_init_uniform(g, 0, (float)P[11], (float)P[12], n->v, s));
         CU(n, gen_init_uniform(g, 1, (float)P[13], (float)P[14], n->ge, s));
         CU(n, gen_init_uniform(g, 2, (float)P[15], (float)P[16], n->gi, s));
-    } else if (n->model == SPICE_BRUNEL) {
+    } else if (n->model == SPICE_BRUNEL || n->model == SPICE_BRUNEL_PLUS) {
         CU(n, gen_init_uniform(g, 0, (float)P[8], (float)P[9], n->v, s));
         std::vector<uint64_t> tab = poisson_table(P[7]);
         if (tab.empty()) return bail(fail(n, SPICE_EINVAL, "lambda_ext %g too large for the Poisson table", P[7]));
@@ -503,16 +595,21 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D;
     a.rank = n->rank; a.G = n->G; a.S = n->S; a.n_own = (uint32_t)n->n_own; a.W = n->W;
     a.TW = n->TW; a.NT = n->NT; a.C = n->C; a.ring_stride = n->ring_stride; a.record_steps = n->R;
+    a.GS = pick_group_lanes(n->mean_seg);
+    if (const char *gs = getenv("SPICE_GROUP_LANES")) a.GS = (uint32_t)atoi(gs);
     a.key0 = (uint32_t)n->seed; a.key1 = (uint32_t)(n->seed >> 32);
-    a.global_atomics = (n->flags & SPICE_FLAG_GLOBAL_ATOMICS) ? 1u : 0u;
+    a.NR = n->NR; a.RS = n->RS;
     a.mc = n->mc;
     a.row_ptr = n->row_ptr; a.bnd = n->bnd; a.ent = n->ent;
     a.v = n->v; a.ge = n->ge; a.gi = n->gi; a.ref = n->ref; a.acc = n->acc; a.ring = n->ring;
-    a.splist = n->splist; a.spcount = n->spcount; a.record = n->record; a.sendbuf = n->sendbuf;
-    a.gather = n->gather; a.stats = n->stats; a.t0 = n->t0; a.force_bits = n->force_bits;
-    a.force_ctl = n->force_ctl;
-    CU(n, prepare_deliver(n->TW));
-    if (deliver_smem_bytes(n->TW) > 227 * 1024) return bail(fail(n, SPICE_EINVAL, "tile too wide"));
+    a.sl_ids = n->sl_ids; a.sl_rows = n->sl_rows; a.sl_counts = n->sl_counts; a.record = n->record; a.sendbuf = n->sendbuf;
+    a.gather = n->gather; a.fired_cta = n->fired_cta; a.delivered_cta = n->delivered_cta;
+    a.t0 = n->t0; a.force_bits = n->force_bits; a.force_ctl = n->force_ctl;
+    a.w = n->w; a.pring = n->pring; a.xtr = n->xtr; a.ytr = n->ytr;
+    a.in_ptr = n->in_ptr; a.in_pos = n->in_pos; a.in_src = n->in_src;
+    a.npl = pbx.n;
+    memcpy(a.pl, pbx.box, sizeof a.pl);
+    CU(n, prepare_kernels(a));
     if (!n->external) {
         if ((st = capture_graph(n, spice_net::kGraphSteps, &n->g_big))) return bail(st);
         if ((st = capture_graph(n, 1, &n->g_one))) return bail(st);
@@ -539,7 +636,7 @@ spice_status spice_step(spice_net *n, uint64_t steps) {
 spice_status spice_exchange_begin(spice_net *n) {
     CHECK_NET(n);
     if (!n->external) return fail(n, SPICE_ESTATE, "not an external-exchange network");
-    CU(n, launch_update(n->args, 0, n->G == 1, n->stream));
+    CU(n, launch_update(n->args, 0, n->stream));
     CU(n, cudaEventRecord(n->ev, n->stream));
     return SPICE_OK;
 }
@@ -560,9 +657,8 @@ spice_status spice_exchange_end(spice_net *n) {
     CHECK_NET(n);
     if (!n->external) return fail(n, SPICE_ESTATE, "not an external-exchange network");
     if (n->G > 1) CU(n, launch_bitmap_to_list(n->args, 0, n->stream));
-    CU(n, launch_deliver(n->args, 0, n->mean_seg, n->n_sm, n->stream));
+    CU(n, launch_deliver(n->args, 0, n->global_atomics, n->n_sm, n->stream));
     CU(n, launch_advance(n->t0, 1, n->stream));
-    // the next begin on another handle must not overwrite our gather buffer early
     CU(n, cudaEventRecord(n->ev, n->stream));
     n->t_host += 1;
     return SPICE_OK;
@@ -583,16 +679,7 @@ spice_status spice_read_spikes(spice_net *n, uint64_t t_begin, uint64_t t_end, u
     for (uint64_t t = t_begin; t < t_end; ++t) {
         CU(n, cudaMemcpy(bm.data(), n->record + (t % n->R) * words, words * 4, cudaMemcpyDeviceToHost));
         std::vector<uint32_t> &L = per[t - t_begin];
-        for (uint32_t r = 0; r < n->G; ++r)
-            for (uint32_t w = 0; w < n->W; ++w) {
-                uint32_t bits = bm[(uint64_t)r * n->W + w];
-                while (bits) {
-                    const uint32_t b = __builtin_ctz(bits);
-                    bits &= bits - 1;
-                    L.push_back((uint32_t)local_to_global((uint64_t)w * 32 + b, r, n->G, n->S));
-                }
-            }
-        if (n->G > 1) std::sort(L.begin(), L.end());
+        decode_into(bm.data(), n->G, n->W, n->S, L);
         tot += L.size();
     }
     if (total) *total = tot;
@@ -643,6 +730,8 @@ static spice_status field_ptr(spice_net *n, uint32_t field, void **p) {
     case SPICE_FIELD_GI: *p = n->gi; break;
     case SPICE_FIELD_REF: *p = n->model != SPICE_SYNTH ? n->ref : nullptr; break;
     case SPICE_FIELD_ACC: *p = n->acc; break;
+    case SPICE_FIELD_XTR: *p = n->xtr; break;
+    case SPICE_FIELD_YTR: *p = n->ytr; break;
     default: break;
     }
     if (!*p) return fail(n, SPICE_EINVAL, "field %u not present for model %u", field, n->model);
@@ -656,6 +745,12 @@ spice_status spice_read_state(spice_net *n, uint32_t field, void *out, uint64_t 
     if (st) return st;
     if (count != n->n_own) return fail(n, SPICE_EINVAL, "n = %llu, owned = %llu", (unsigned long long)count, (unsigned long long)n->n_own);
     CU(n, cudaStreamSynchronize(n->stream));
+    if (field == SPICE_FIELD_XTR) {           // global pre traces of the current parity
+        std::vector<float> x(n->N);
+        CU(n, cudaMemcpy(x.data(), n->xtr + (n->t_host & 1) * (uint64_t)n->N, n->N * 4ull, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < count; ++i) ((float *)out)[i] = x[local_to_global(i, n->rank, n->G, n->S)];
+        return SPICE_OK;
+    }
     if (count) CU(n, cudaMemcpy(out, p, count * 4, cudaMemcpyDeviceToHost));
     return SPICE_OK;
 }
@@ -678,13 +773,27 @@ spice_status spice_read_input(spice_net *n, uint32_t rel, uint32_t *counts, int6
     CU(n, cudaStreamSynchronize(n->stream));
     const uint64_t slot = (n->t_host + rel) % n->D;
     if (counts && count) CU(n, cudaMemcpy(counts, n->ring + slot * n->ring_stride, count * 4, cudaMemcpyDeviceToHost));
-    if (plastic) memset(plastic, 0, count * 8);
+    if (plastic) {
+        if (n->pring && count) CU(n, cudaMemcpy(plastic, n->pring + slot * n->ring_stride, count * 8, cudaMemcpyDeviceToHost));
+        else memset(plastic, 0, count * 8);
+    }
     return SPICE_OK;
 }
 
-spice_status spice_read_weights(spice_net *n, uint32_t, uint32_t, float *, uint64_t, uint64_t *) {
+spice_status spice_read_weights(spice_net *n, uint32_t row_begin, uint32_t row_end, float *w,
+                                uint64_t cap, uint64_t *total) {
     CHECK_NET(n);
-    return fail(n, SPICE_EINVAL, "model %u has no plastic weights", n->model);
+    if (!n->w) return fail(n, SPICE_EINVAL, "model %u has no plastic weights", n->model);
+    if (row_begin > row_end || row_end > n->N) return fail(n, SPICE_EINVAL, "rows outside [0, N)");
+    CU(n, cudaStreamSynchronize(n->stream));
+    uint64_t rp[2];
+    CU(n, cudaMemcpy(&rp[0], n->row_ptr + row_begin, 8, cudaMemcpyDeviceToHost));
+    CU(n, cudaMemcpy(&rp[1], n->row_ptr + row_end, 8, cudaMemcpyDeviceToHost));
+    const uint64_t tot = rp[1] - rp[0];
+    if (total) *total = tot;
+    if (tot > cap || (!w && tot)) return fail(n, SPICE_ETRUNC, "need %llu weights", (unsigned long long)tot);
+    if (tot) CU(n, cudaMemcpy(w, n->w + rp[0], tot * 4, cudaMemcpyDeviceToHost));
+    return SPICE_OK;
 }
 
 spice_status spice_force_spikes(spice_net *n, const uint32_t *ids, uint64_t count, int mode) {
@@ -708,11 +817,15 @@ spice_status spice_force_spikes(spice_net *n, const uint32_t *ids, uint64_t coun
 spice_status spice_stats(spice_net *n, uint64_t *steps, uint64_t *fired, uint64_t *delivered) {
     CHECK_NET(n);
     CU(n, cudaStreamSynchronize(n->stream));
-    unsigned long long h[2];
-    CU(n, cudaMemcpy(h, n->stats, 16, cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> f(n->NT), d((size_t)n->NT * n->C);
+    CU(n, cudaMemcpy(f.data(), n->fired_cta, f.size() * 8, cudaMemcpyDeviceToHost));
+    CU(n, cudaMemcpy(d.data(), n->delivered_cta, d.size() * 8, cudaMemcpyDeviceToHost));
+    unsigned long long sf = 0, sd = 0;
+    for (auto x : f) sf += x;
+    for (auto x : d) sd += x;
     if (steps) *steps = n->t_host;
-    if (fired) *fired = h[0];
-    if (delivered) *delivered = h[1];
+    if (fired) *fired = sf;
+    if (delivered) *delivered = sd;
     return SPICE_OK;
 }
 
@@ -740,42 +853,67 @@ spice_status spice_profile(spice_net *n, uint64_t steps, double *ms, uint32_t ca
     CHECK_NET(n);
     if (n->external) return fail(n, SPICE_ESTATE, "profiling needs an NCCL or single-GPU network");
     if (!ms || cap < 4) return fail(n, SPICE_EINVAL, "need room for 4 timings");
-    cudaEvent_t ev[5];
-    for (auto &e : ev) CU(n, cudaEventCreate(&e));
+    cudaStream_t s = n->stream;
+    const SimArgs &a = n->args;
+    cudaEvent_t e0, e1;
+    CU(n, cudaEventCreate(&e0));
+    CU(n, cudaEventCreate(&e1));
     double acc[4] = {0, 0, 0, 0};
+    uint64_t cnt[4] = {0, 0, 0, 0};
+    auto timed = [&](int slot, auto &&fn) -> spice_status {
+        CU(n, cudaEventRecord(e0, s));
+        spice_status st = fn();
+        if (st) return st;
+        CU(n, cudaEventRecord(e1, s));
+        CU(n, cudaEventSynchronize(e1));
+        float x = 0;
+        CU(n, cudaEventElapsedTime(&x, e0, e1));
+        acc[slot] += x;
+        cnt[slot] += 1;
+        return SPICE_OK;
+    };
+    // (1) unfused steps: update, [exchange], deliver
     for (uint64_t q = 0; q < steps; ++q) {
-        CU(n, cudaEventRecord(ev[0], n->stream));
-        CU(n, launch_update(n->args, 0, n->G == 1, n->stream));
-        CU(n, cudaEventRecord(ev[1], n->stream));
+        spice_status st = timed(0, [&]() -> spice_status { CU(n, launch_update(a, 0, s)); return SPICE_OK; });
+        if (st) return st;
         if (n->G > 1) {
-            ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, n->stream);
-            if (r != ncclSuccess) return fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
-            CU(n, cudaEventRecord(ev[2], n->stream));
-            CU(n, launch_bitmap_to_list(n->args, 0, n->stream));
-        } else {
-            CU(n, cudaEventRecord(ev[2], n->stream));
+            st = timed(3, [&]() -> spice_status {
+                ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, s);
+                if (r != ncclSuccess) return fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
+                CU(n, launch_bitmap_to_list(a, 0, s));
+                return SPICE_OK;
+            });
+            if (st) return st;
         }
-        CU(n, cudaEventRecord(ev[3], n->stream));
-        CU(n, launch_deliver(n->args, 0, n->mean_seg, n->n_sm, n->stream));
-        CU(n, cudaEventRecord(ev[4], n->stream));
-        CU(n, launch_advance(n->t0, 1, n->stream));
-        CU(n, cudaEventSynchronize(ev[4]));
-        float a = 0, b = 0, c = 0, d = 0;
-        CU(n, cudaEventElapsedTime(&a, ev[0], ev[1]));
-        CU(n, cudaEventElapsedTime(&b, ev[3], ev[4]));
-        CU(n, cudaEventElapsedTime(&c, ev[2], ev[3]));
-        CU(n, cudaEventElapsedTime(&d, ev[1], ev[2]));
-        acc[0] += a; acc[1] += b; acc[2] += c; acc[3] += d;
+        st = timed(1, [&]() -> spice_status { CU(n, launch_deliver(a, 0, n->global_atomics, n->n_sm, s)); return SPICE_OK; });
+        if (st) return st;
+        CU(n, launch_advance(n->t0, 1, s));
         n->t_host += 1;
     }
-    for (auto &e : ev) cudaEventDestroy(e);
-    for (int k = 0; k < 4; ++k) ms[k] = steps ? acc[k] / (double)steps : 0.0;
+    // (2) the fused kernel (G = 1): update(t), then fused launches deliver(t)+update(t+1)
+    if (n->G == 1 && n->fused && !n->global_atomics && steps > 0) {
+        CU(n, launch_update(a, 0, s));
+        for (uint64_t q = 0; q < steps; ++q) {
+            spice_status st = timed(2, [&]() -> spice_status { CU(n, launch_fused(a, 0, s)); return SPICE_OK; });
+            if (st) return st;
+            CU(n, launch_advance(n->t0, 1, s));
+            n->t_host += 1;
+        }
+        CU(n, launch_deliver(a, 0, false, n->n_sm, s));
+        CU(n, launch_advance(n->t0, 1, s));
+        n->t_host += 1;
+    }
+    CU(n, cudaStreamSynchronize(s));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (int k = 0; k < 4; ++k) ms[k] = cnt[k] ? acc[k] / (double)cnt[k] : 0.0;
     if (nk) *nk = 4;
     return SPICE_OK;
 }
 
 uint32_t spice_kernels_per_step(spice_net *n) {
     if (!n) return 0;
+    if (n->G == 1 && n->fused && !n->global_atomics) return 1u;   // fused deliver(t)+update(t+1)
     return n->G == 1 ? 2u : 3u;   // update, [bitmap_to_list], deliver (+ NCCL's own kernel)
 }
 

@@ -2,8 +2,9 @@
 // "the layout description is then uploaded to the GPU where it is expanded").
 //
 // Each rank expands only the edges whose target it owns (the descriptor split of
-// {range1, range2 ∩ owned, p}), directly into the destination-tiled
-// CSR used by delivery:
+// {range1, range2 ∩ owned, p}), directly into the destination-tiled,
+// source-major CSR used by delivery (rows stay contiguous so that the segments of
+// neighbouring tiles share DRAM sectors through L2 — the Fig. 1 column-wise idea):
 //   row_ptr[s]            start of source s's row (global source IDs, all N rows)
 //   bnd[s*(NT+1) + b]     start of tile b's segment within row s (bnd[..NT] = row length)
 //   ent[row_ptr[s] + e]   tile-local target offset (u16), ascending within each segment
@@ -15,7 +16,7 @@
 
 namespace spice {
 
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, uint32_t lane) {
+__device__ __forceinline__ uint32_t warp_incl_scan_g(uint32_t x, uint32_t lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(256) fill_prob_kernel(GenGeom g, GenRule r, co
             const uint32_t q = q0 + lane;
             const uint32_t m = q < nblk ? prob_bits4(g, r, s, b * g.TW + 4u * q) : 0u;
             const uint32_t c = __popc(m);
-            const uint32_t incl = warp_incl_scan(c, lane);
+            const uint32_t incl = warp_incl_scan_g(c, lane);
             uint64_t p = pos + incl - c;
             for (uint32_t e = 0; e < 4; ++e)
                 if (m >> e & 1u) ent[p++] = (uint16_t)(4u * q + e);
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(256) row_prefix_kernel(GenGeom g, uint32_t *cn
         for (uint32_t b0 = 0; b0 < g.NT; b0 += 32) {
             const uint32_t b = b0 + lane;
             const uint32_t c = b < g.NT ? row[b] : 0u;
-            const uint32_t incl = warp_incl_scan(c, lane);
+            const uint32_t incl = warp_incl_scan_g(c, lane);
             if (b < g.NT) row[b] = carry + incl - c;
             carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
@@ -273,6 +274,19 @@ cudaError_t gen_scan(const GenGeom &g, uint32_t *cnt_bnd, uint64_t *row_ptr, uin
     return cudaStreamSynchronize(s);
 }
 
+cudaError_t gen_scan_u64(uint64_t *data, uint64_t n, cudaStream_t s) {
+    cudaError_t e;
+    const uint64_t nb = (n + kScanBlock - 1) / kScanBlock;
+    uint64_t *sums = nullptr;
+    if (n == 0) return cudaMemsetAsync(data, 0, 8, s);
+    if ((e = cudaMallocAsync(&sums, nb * sizeof(uint64_t), s))) return e;
+    scan_block_sums<<<(unsigned)nb, kScanBlock, 0, s>>>(data, n, sums);
+    scan_sums_serial<<<1, kScanBlock, 0, s>>>(sums, nb);
+    scan_apply<<<(unsigned)nb, kScanBlock, 0, s>>>(data, n, sums, data);
+    if ((e = cudaGetLastError())) return e;
+    return cudaFreeAsync(sums, s);
+}
+
 cudaError_t gen_fill(const GenGeom &g, const GenRule &r, const uint64_t *row_ptr,
                      const uint32_t *bnd, uint32_t *cursor, uint16_t *ent, cudaStream_t s) {
     if (r.src_end <= r.src_begin || r.dst_end <= r.dst_begin) return cudaSuccess;
@@ -291,6 +305,66 @@ cudaError_t gen_fill(const GenGeom &g, const GenRule &r, const uint64_t *row_ptr
 cudaError_t gen_sort_segments(const GenGeom &g, const uint64_t *row_ptr, const uint32_t *bnd,
                               uint16_t *ent, cudaStream_t s) {
     sort_segments_kernel<<<grid_for((uint64_t)g.N * g.NT, 256), 256, 0, s>>>(g, row_ptr, bnd, ent);
+    return cudaGetLastError();
+}
+
+// ---- Brunel+ plastic synapses: weights and the per-target in-synapse index ----
+__device__ __forceinline__ bool is_plastic(const PlasticBoxes &pb, uint32_t s, uint32_t j) {
+    for (uint32_t q = 0; q < pb.n; ++q)
+        if (s >= pb.box[q][0] && s < pb.box[q][1] && j >= pb.box[q][2] && j < pb.box[q][3]) return true;
+    return false;
+}
+// MODE 0: weights (w0 on plastic synapses, 0 elsewhere) and in-degree counts;
+// MODE 1: fill the in-synapse index (absolute entry, source) through per-target cursors.
+template <int MODE>
+__global__ void __launch_bounds__(256) plastic_kernel(GenGeom g, PlasticBoxes pb, const uint64_t *row_ptr,
+                                                      const uint32_t *bnd, const uint16_t *ent, float *w,
+                                                      float w0, uint32_t *cnt_or_cursor,
+                                                      const uint64_t *in_ptr, uint64_t *in_pos,
+                                                      uint32_t *in_src) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * 8;
+    for (uint64_t q = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); q < (uint64_t)g.N * g.NT; q += nwarps) {
+        const uint32_t s = (uint32_t)(q / g.NT), b = (uint32_t)(q % g.NT);
+        const uint32_t *bp = bnd + (uint64_t)s * (g.NT + 1) + b;
+        const uint64_t st = row_ptr[s] + bp[0];
+        const uint32_t len = bp[1] - bp[0];
+        for (uint32_t e = lane; e < len; e += 32) {
+            const uint32_t il = b * g.TW + ent[st + e];
+            const bool pl = is_plastic(pb, s, (uint32_t)local_to_global(il, g.rank, g.G, g.S));
+            if (MODE == 0) {
+                w[st + e] = pl ? w0 : 0.0f;
+                if (pl) atomicAdd(&cnt_or_cursor[il], 1u);
+            } else if (pl) {
+                const uint64_t k = in_ptr[il] + atomicAdd(&cnt_or_cursor[il], 1u);
+                in_pos[k] = st + e;
+                in_src[k] = s;
+            }
+        }
+    }
+}
+__global__ void u32_to_u64(const uint32_t *in, uint64_t n, uint64_t *out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+
+cudaError_t gen_plastic(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
+                        const uint32_t *bnd, const uint16_t *ent, float *w, float w0,
+                        uint32_t *tmp_cnt, uint64_t *in_ptr, uint64_t **in_pos, uint32_t **in_src,
+                        uint64_t *n_plastic, cudaStream_t s) {
+    cudaError_t e;
+    const uint64_t pairs = (uint64_t)g.N * g.NT;
+    if ((e = cudaMemsetAsync(tmp_cnt, 0, (size_t)g.n_own * 4, s))) return e;
+    plastic_kernel<0><<<grid_for(pairs, 8), 256, 0, s>>>(g, pb, row_ptr, bnd, ent, w, w0, tmp_cnt, nullptr, nullptr, nullptr);
+    u32_to_u64<<<grid_for(g.n_own, 256), 256, 0, s>>>(tmp_cnt, g.n_own, in_ptr);
+    if ((e = cudaGetLastError())) return e;
+    if ((e = gen_scan_u64(in_ptr, g.n_own, s))) return e;
+    if ((e = cudaMemcpyAsync(n_plastic, in_ptr + g.n_own, 8, cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    if ((e = cudaMalloc(in_pos, (*n_plastic ? *n_plastic : 1) * 8))) return e;
+    if ((e = cudaMalloc(in_src, (*n_plastic ? *n_plastic : 1) * 4))) return e;
+    if ((e = cudaMemsetAsync(tmp_cnt, 0, (size_t)g.n_own * 4, s))) return e;
+    plastic_kernel<1><<<grid_for(pairs, 8), 256, 0, s>>>(g, pb, row_ptr, bnd, ent, w, w0, tmp_cnt, in_ptr, *in_pos, *in_src);
     return cudaGetLastError();
 }
 

@@ -1,16 +1,23 @@
 // sim.cu — per-step kernels of the Spice hot path on sm_100a.
 //
-//   update_kernel<MODEL>   neuron update + warp-ballot spike bitmap + block-prefix spike
-//                          compaction (Listing 1)
-//   deliver_tiled<GS>      destination-tiled spike delivery: every CTA owns a tile of
-//                          targets, walks the tile's segment of each spiking row (rows
-//                          pre-split at tile pivots, the split of P:273-275) and
-//                          accumulates receptor counts with shared-memory atomics; the
-//                          tile is then added to the L2-resident input ring slot
-//                          (a3; "delivered to all neighbors in said row")
-//   deliver_global_atomics paper-style column-wise warps with global atomics (P:200,
-//                          P:436 "bottlenecked by atomic operations"): the A/B baseline
-//   bitmap_to_list         gathered per-rank bitmaps -> global spike list (a2, G > 1)
+// One CTA owns one destination tile of TW consecutive local targets (SURVEY §8(a) a3,
+// PAPER.md:198-200 "cache-aware": concurrent writes stay inside one narrow destination
+// band — here the band is a shared-memory tile).
+//
+//   k_update<M>      neuron update of a tile for step t (a1; Listing 1):
+//                    4 neurons per thread (one Philox call covers 4 consecutive IDs),
+//                    4-bit nibbles OR-reduced into 32-bit bitmap words, spikes appended
+//                    to the tile's own list region (no global atomics)
+//   k_deliver<GS>    destination-tiled delivery of step t (a3): segment descriptors of the
+//                    spiking rows staged in smem, GS lanes per segment load 16-byte windows
+//                    of u16 offsets, shared-memory atomicAdd of packed receptor counts,
+//                    then the tile is added to the input ring slot of step t + delay
+//   k_fused<M,GS>    deliver(t) + update(t+1) of the same tile in one CTA (G = 1): with
+//                    delay 1 the tile's inputs never leave shared memory; one launch per
+//                    step, the kernel boundary is the step barrier
+//   k_global_atomics paper-style column-wise warps with global atomics:
+//                    the A/B baseline
+//   k_b2l            gathered per-rank bitmaps -> global spike list (a2, G > 1)
 //
 // Floating point: every operation of the neuron update is an explicit round-to-nearest
 // intrinsic in the order fixed by DESIGN.md readings R3-R5 (no contraction), so results
@@ -20,41 +27,91 @@
 
 namespace spice {
 
-__device__ __forceinline__ uint32_t philox_pick(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
-                                                uint32_t k0, uint32_t k1, uint32_t which) {
-    return word_of(philox4x32_10(make_uint4(w0, w1, w2, w3), k0, k1), which);
+// --------------------------------------------------------------------- helpers
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    return x;
 }
 
+// Exclusive scan of arr[0..n) in shared memory (n <= kBlock * 8); arr[n] = total.
+__device__ void block_exclusive_scan(uint32_t *arr, uint32_t n, uint32_t *s_tmp) {
+    const uint32_t tid = threadIdx.x, per = (n + kBlock - 1) / kBlock;
+    const uint32_t lo = min(n, tid * per), hi = min(n, lo + per);
+    uint32_t sum = 0;
+    for (uint32_t x = lo; x < hi; ++x) sum += arr[x];
+    const uint32_t incl = warp_incl_scan(sum);
+    if ((tid & 31) == 31) s_tmp[tid >> 5] = incl;
+    __syncthreads();
+    if (tid < 32) {
+        const uint32_t v = tid < kBlock / 32 ? s_tmp[tid] : 0u;
+        const uint32_t wi = warp_incl_scan(v);
+        if (tid < kBlock / 32) s_tmp[tid] = wi - v;
+    }
+    __syncthreads();
+    uint32_t run = s_tmp[tid >> 5] + incl - sum;
+    for (uint32_t x = lo; x < hi; ++x) { const uint32_t c = arr[x]; arr[x] = run; run += c; }
+    if (tid == kBlock - 1) arr[n] = run;
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint4 ld_stream_v4(const uint16_t *p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t philox_word(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                                const SimArgs &a, uint32_t which) {
+    return word_of(philox4x32_10(make_uint4(w0, w1, w2, w3), a.key0, a.key1), which);
+}
+
+// ------------------------------------------------------------------ neuron update
+// Update the 4 consecutive owned neurons i0..i0+3 (i0 % 4 == 0) for step t with packed
+// input counts c[4]; returns the spike nibble.  State arrays are padded to NT*TW.
 template <int MODEL>
-__global__ void __launch_bounds__(kUpdateBlock) update_kernel(SimArgs a, uint32_t k, int produce_list) {
-    const uint64_t t = *a.t0 + k;
-    const uint32_t i = blockIdx.x * kUpdateBlock + threadIdx.x;   // local index
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool valid = i < a.n_own;
-    const uint32_t j = valid ? (uint32_t)local_to_global(i, a.rank, a.G, a.S) : 0u;
-    bool spiked = false;
-    if (valid) {
-        uint32_t *slot = a.ring + (t % a.D) * a.ring_stride + i;
-        const uint32_t c = *slot;
-        *slot = 0u;
-        const ModelConst &m = a.mc;
-        int forced = 0;
-        bool fbit = false;
-        if (a.force_ctl[0] == t) {
-            forced = (int)a.force_ctl[1];
-            fbit = (a.force_bits[i >> 5] >> (i & 31)) & 1u;
-        }
-        if (MODEL == 4) {                           // Synth (reading R12)
-            a.acc[i] = a.acc[i] + c;
-            const uint32_t x = philox_pick(j >> 2, (uint32_t)t, 0u, kTagFire, a.key0, a.key1, j & 3);
-            spiked = (uint64_t)x < m.thr_fire;
-            if (forced == 1) spiked = fbit; else if (forced == 2) spiked = spiked || fbit;
-        } else if (MODEL == 1) {                    // Vogels-Abbott COBA (readings R3-R5)
-            const uint32_t ne = c & 0xFFFFu, ni = c >> 16;
-            float ge = a.ge[i], gi = a.gi[i], v = a.v[i];
-            uint32_t ref = a.ref[i];
-            ge = __fadd_rn(ge, __fmul_rn(m.dge, __uint2float_rn(ne)));
-            gi = __fadd_rn(gi, __fmul_rn(m.dgi, __uint2float_rn(ni)));
+__device__ __forceinline__ uint32_t update4(const SimArgs &a, uint64_t t, uint32_t i0, const uint32_t c[4],
+                                            const long long pin[4]) {
+    const ModelConst &m = a.mc;
+    const uint32_t j0 = (uint32_t)local_to_global(i0, a.rank, a.G, a.S);   // multiple of 4
+    uint32_t valid = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) valid |= (i0 + e < a.n_own ? 1u : 0u) << e;
+    int forced = 0;
+    uint32_t fbits = 0;
+    if (a.force_ctl[0] == t) {
+        forced = (int)a.force_ctl[1];
+        fbits = (a.force_bits[i0 >> 5] >> (i0 & 31)) & 0xFu;
+    }
+    uint32_t spk = 0;
+    if (MODEL == 4) {                                   // Synth (reading R12)
+        const uint4 x = philox4x32_10(make_uint4(j0 >> 2, (uint32_t)t, 0u, kTagFire), a.key0, a.key1);
+        uint4 acc = *reinterpret_cast<const uint4 *>(a.acc + i0);
+        acc.x += c[0]; acc.y += c[1]; acc.z += c[2]; acc.w += c[3];
+        *reinterpret_cast<uint4 *>(a.acc + i0) = acc;
+        spk = ((uint64_t)x.x < m.thr_fire ? 1u : 0u) | ((uint64_t)x.y < m.thr_fire ? 2u : 0u) |
+              ((uint64_t)x.z < m.thr_fire ? 4u : 0u) | ((uint64_t)x.w < m.thr_fire ? 8u : 0u);
+        if (forced == 1) spk = fbits; else if (forced == 2) spk |= fbits;
+    } else if (MODEL == 1) {                            // Vogels-Abbott COBA (readings R3-R5)
+        float4 v4 = *reinterpret_cast<const float4 *>(a.v + i0);
+        float4 ge4 = *reinterpret_cast<const float4 *>(a.ge + i0);
+        float4 gi4 = *reinterpret_cast<const float4 *>(a.gi + i0);
+        uint4 rf4 = *reinterpret_cast<const uint4 *>(a.ref + i0);
+        float *vv = &v4.x, *gev = &ge4.x, *giv = &gi4.x;
+        uint32_t *rfv = &rf4.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t ne = c[e] & 0xFFFFu, ni = c[e] >> 16;
+            float ge = __fadd_rn(gev[e], __fmul_rn(m.dge, __uint2float_rn(ne)));
+            float gi = __fadd_rn(giv[e], __fmul_rn(m.dgi, __uint2float_rn(ni)));
+            float v = vv[e];
+            uint32_t ref = rfv[e];
+            bool s = false;
             if (ref > 0u) {
                 ref -= 1u;
                 v = m.Vr;
@@ -62,277 +119,651 @@ __global__ void __launch_bounds__(kUpdateBlock) update_kernel(SimArgs a, uint32_
                 const float ta = __fsub_rn(m.EL, v);
                 const float tb = __fmul_rn(ge, __fsub_rn(m.Ee, v));
                 const float tc = __fmul_rn(gi, __fsub_rn(m.Ei, v));
-                const float sum = __fadd_rn(__fadd_rn(ta, tb), tc);
-                v = __fadd_rn(v, __fmul_rn(m.h, sum));
-                spiked = v >= m.Vt;
+                v = __fadd_rn(v, __fmul_rn(m.h, __fadd_rn(__fadd_rn(ta, tb), tc)));
+                s = v >= m.Vt;
             }
-            if (forced == 1) spiked = fbit; else if (forced == 2) spiked = spiked || fbit;
-            if (spiked) { v = m.Vr; ref = m.R; }
-            ge = __fsub_rn(ge, __fmul_rn(m.ke, ge));
-            gi = __fsub_rn(gi, __fmul_rn(m.ki, gi));
-            a.v[i] = v; a.ge[i] = ge; a.gi[i] = gi; a.ref[i] = ref;
-        } else {                                    // Brunel model A (readings R3-R5, R12)
-            float v = a.v[i];
-            uint32_t ref = a.ref[i];
+            const bool fb = (fbits >> e) & 1u;
+            if (forced == 1) s = fb; else if (forced == 2) s = s || fb;
+            if (s) { v = m.Vr; ref = m.R; }
+            gev[e] = __fsub_rn(ge, __fmul_rn(m.ke, ge));
+            giv[e] = __fsub_rn(gi, __fmul_rn(m.ki, gi));
+            vv[e] = v;
+            rfv[e] = ref;
+            spk |= (s ? 1u : 0u) << e;
+        }
+        *reinterpret_cast<float4 *>(a.v + i0) = v4;
+        *reinterpret_cast<float4 *>(a.ge + i0) = ge4;
+        *reinterpret_cast<float4 *>(a.gi + i0) = gi4;
+        *reinterpret_cast<uint4 *>(a.ref + i0) = rf4;
+    } else {                                            // Brunel model A (readings R3-R5, R12)
+        float4 v4 = *reinterpret_cast<const float4 *>(a.v + i0);
+        uint4 rf4 = *reinterpret_cast<const uint4 *>(a.ref + i0);
+        float *vv = &v4.x;
+        uint32_t *rfv = &rf4.x;
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (rfv[0] == 0u || rfv[1] == 0u || rfv[2] == 0u || rfv[3] == 0u)
+            x = philox4x32_10(make_uint4(j0 >> 2, (uint32_t)t, 0u, kTagExt), a.key0, a.key1);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float v = vv[e];
+            uint32_t ref = rfv[e];
+            bool s = false;
             if (ref > 0u) {
                 ref -= 1u;
-                v = m.Vr;                          // input and drive discarded
+                v = m.Vr;                              // input and drive discarded
             } else {
-                const uint32_t x = philox_pick(j >> 2, (uint32_t)t, 0u, kTagExt, a.key0, a.key1, j & 3);
+                const uint32_t xe = word_of(x, e);
                 uint32_t next = 0;
-                while ((uint64_t)x >= m.ptab[next]) ++next;   // min{k : x < T_k}
-                const uint32_t ne = c & 0xFFFFu, ni = c >> 16;
+                while ((uint64_t)xe >= m.ptab[next]) ++next;   // min{k : x < T_k}
+                const uint32_t ne = c[e] & 0xFFFFu, ni = c[e] >> 16;
                 v = __fadd_rn(v, __fmul_rn(m.h, __fsub_rn(m.EL, v)));
                 v = __fadd_rn(v, __fmul_rn(m.JE, __uint2float_rn(ne + next)));
                 v = __fadd_rn(v, __fmul_rn(m.JI, __uint2float_rn(ni)));
-                spiked = v >= m.theta;
+                if (MODEL == 3) v = __fadd_rn(v, __fmul_rn(__ll2float_rn(pin[e]), 2.3283064365386963e-10f));
+                s = v >= m.theta;
             }
-            if (forced == 1) spiked = fbit; else if (forced == 2) spiked = spiked || fbit;
-            if (spiked) { v = m.Vr; ref = m.R; }
-            a.v[i] = v; a.ref[i] = ref;
+            const bool fb = (fbits >> e) & 1u;
+            if (forced == 1) s = fb; else if (forced == 2) s = s || fb;
+            if (s) { v = m.Vr; ref = m.R; }
+            vv[e] = v;
+            rfv[e] = ref;
+            spk |= (s ? 1u : 0u) << e;
+        }
+        *reinterpret_cast<float4 *>(a.v + i0) = v4;
+        *reinterpret_cast<uint4 *>(a.ref + i0) = rf4;
+    }
+    return spk & valid;
+}
+
+// Update every neuron of tile b for step t.  Inputs come from `cnt` (shared memory, the
+// tile's counts) or, when cnt == nullptr, from input ring slot t mod D (read and cleared).
+template <int MODEL>
+__device__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, const uint32_t *cnt,
+                            bool write_list, uint32_t *s_count) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    const uint32_t lo = b * a.TW;
+    const uint32_t span = lo < a.W * 32u ? min(a.TW, a.W * 32u - lo) : 0u;   // bitmap coverage
+    const uint32_t par = (uint32_t)(t & 1);
+    uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
+    uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + b) * a.RS;
+    uint32_t *bm = a.G == 1 ? a.record + (t % a.record_steps) * (uint64_t)a.W : a.sendbuf;
+    uint32_t *ring_slot = a.ring + (t % a.D) * a.ring_stride + lo;
+    for (uint32_t x0 = 0; x0 < span; x0 += 4u * kBlock) {      // uniform trip count per CTA
+        const uint32_t x4 = x0 + 4u * tid;
+        uint32_t nib = 0;
+        const bool act = x4 < span && lo + x4 < a.n_own;
+        if (act) {
+            uint32_t c[4];
+            long long pin[4] = {0, 0, 0, 0};
+            if (MODEL == 3) {
+                long long *ps = a.pring + (t % a.D) * a.ring_stride + lo + x4;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) { pin[e] = ps[e]; ps[e] = 0; }
+            }
+            if (cnt) {
+                c[0] = cnt[x4]; c[1] = cnt[x4 + 1]; c[2] = cnt[x4 + 2]; c[3] = cnt[x4 + 3];
+            } else {
+                const uint4 cv = *reinterpret_cast<const uint4 *>(ring_slot + x4);
+                *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
+                c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
+            }
+            nib = update4<MODEL>(a, t, lo + x4, c, pin);
+        }
+        // 8 lanes x 4 bits -> one 32-neuron bitmap word
+        uint32_t w = nib << (4u * (lane & 7u));
+        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 1);
+        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 2);
+        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 4);
+        if ((lane & 7u) == 0 && x4 < span) bm[(lo + x4) >> 5] = w;
+        // append spikes to this tile's list region (warp-aggregated smem counter)
+        const uint32_t nsp = __popc(nib);
+        const uint32_t incl = warp_incl_scan(nsp);
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        if (tot) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(s_count, tot);
+            base = __shfl_sync(0xFFFFFFFFu, base, 0);
+            if (write_list && nib) {
+                uint32_t pos = base + incl - nsp;
+                const uint32_t j0 = (uint32_t)local_to_global(lo + x4, a.rank, a.G, a.S);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if ((nib >> e) & 1u) { region[pos] = j0 + e; region_rows[pos] = a.row_ptr[j0 + e]; ++pos; }
+            }
         }
     }
-    // --- warp ballot -> bitmap word (32 consecutive local indices; S % 32 == 0) ---
-    const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, spiked);
-    const uint32_t wi = i >> 5;
-    if (lane == 0 && wi < a.W) {
-        uint32_t *bm = a.G == 1 ? a.record + (t % a.record_steps) * (uint64_t)a.W : a.sendbuf;
-        bm[wi] = ballot;
-    }
-    // --- block prefix over warp popcounts -> one atomic per CTA -> ordered append ---
-    __shared__ uint32_t s_wcnt[kUpdateBlock / 32];
-    __shared__ uint32_t s_base;
-    if (lane == 0) s_wcnt[warp] = __popc(ballot);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t tot = 0;
-        for (int w = 0; w < kUpdateBlock / 32; ++w) { const uint32_t cw = s_wcnt[w]; s_wcnt[w] = tot; tot += cw; }
-        if (tot) atomicAdd(&a.stats[0], (unsigned long long)tot);
-        s_base = (produce_list && tot) ? atomicAdd(&a.spcount[t % 3], tot) : 0u;
-        if (produce_list && blockIdx.x == 0) a.spcount[(t + 1) % 3] = 0u;
-    }
-    __syncthreads();
-    if (produce_list && spiked) {
-        const uint32_t pos = s_base + s_wcnt[warp] + __popc(ballot & ((1u << lane) - 1u));
-        a.splist[pos] = j;
+    if (tid == 0) {
+        const uint32_t n = *s_count;
+        if (write_list) a.sl_counts[par * a.NR + b] = n;
+        a.fired_cta[b] += n;
+        *s_count = 0;
     }
 }
 
-__device__ __forceinline__ uint2 ld_stream_v2(const uint16_t *p) {
-    uint2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
-    return v;
+// ------------------------------------------------------------------ delivery
+struct DeliverSmem {
+    uint32_t *cnt;     // [TW] tile counters
+    uint32_t *pref;    // [NR + 1] region prefix
+    uint64_t *dstart;  // [kDescChunk] absolute segment start in ent
+    uint32_t *dlen;    // [kDescChunk] len | inh << 31
+    uint32_t *tmp;     // [32]
+};
+
+__device__ __forceinline__ uint32_t region_of(const uint32_t *pref, uint32_t nr, uint32_t p) {
+    uint32_t lo = 0, hi = nr;             // largest r with pref[r] <= p
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (pref[mid] <= p) lo = mid; else hi = mid;
+    }
+    return lo;
 }
 
-// Destination-tiled delivery.  CTA (b, c) owns tile b's counters in shared memory and
-// handles spikes p = c, c+C, c+2C, ... of the step's list.  GS lanes cooperate on one
-// segment, each loading 8 bytes (4 u16 offsets) per window.
+__device__ __forceinline__ void accumulate8(uint32_t *cnt, const uint4 v, uint64_t w, uint64_t st,
+                                            uint64_t en, uint32_t q) {
+    const uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
+                           v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        if (w + u >= st && w + u < en) atomicAdd(&cnt[e[u]], q);
+}
+
+// Deliver the spikes of step t with index p = c, c+C, ... into tile b's counters.
+// Returns this thread's share of the delivered-event count.
 template <int GS>
-__global__ void __launch_bounds__(kDeliverBlock) deliver_tiled(SimArgs a, uint32_t k,
-                                                               const uint32_t *__restrict__ list) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    const uint32_t tw_pad = (a.TW + 3u) & ~3u;
-    uint32_t *cnt = smem;
-    uint64_t *dstart = reinterpret_cast<uint64_t *>(smem + tw_pad + (tw_pad & 1u ? 1u : 0u));
-    uint32_t *dlen = reinterpret_cast<uint32_t *>(dstart + kDescChunk);
-    const uint64_t t = *a.t0 + k;
-    const uint32_t b = blockIdx.x / a.C, c = blockIdx.x % a.C;
+__device__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c, DeliverSmem sm) {
     const uint32_t tid = threadIdx.x;
-    for (uint32_t x = tid; x < a.TW; x += kDeliverBlock) cnt[x] = 0u;
-    const uint32_t n_sp = a.spcount[t % 3];
+    const uint32_t par = (uint32_t)(t & 1);
+    for (uint32_t r = tid; r < a.NR; r += kBlock) sm.pref[r] = a.sl_counts[par * a.NR + r];
+    __syncthreads();
+    block_exclusive_scan(sm.pref, a.NR, sm.tmp);
+    const uint32_t n_sp = sm.pref[a.NR];
     const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
+    const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
     uint32_t delivered = 0;
     const uint32_t grp = tid / GS, lig = tid % GS;
-    constexpr uint32_t ngrp = kDeliverBlock / GS;
+    constexpr uint32_t ngrp = kBlock / GS;
     for (uint32_t q0 = 0; q0 < my; q0 += kDescChunk) {
         const uint32_t nq = min((uint32_t)kDescChunk, my - q0);
-        __syncthreads();
-        for (uint32_t q = tid; q < nq; q += kDeliverBlock) {
-            const uint32_t s = list[c + (q0 + q) * a.C];
+        // ---- stage (segment start, length) of every spike of this chunk ----
+#pragma unroll 2
+        for (uint32_t q = tid; q < nq; q += kBlock) {
+            const uint32_t p = c + (q0 + q) * a.C;
+            const uint32_t r = region_of(sm.pref, a.NR, p);
+            const uint64_t slot = lbase + (uint64_t)r * a.RS + (p - sm.pref[r]);
+            const uint32_t s = a.sl_ids[slot];
+            const uint64_t rs = a.sl_rows[slot];
             const uint32_t *bp = a.bnd + (uint64_t)s * (a.NT + 1u) + b;
             const uint32_t b0 = bp[0], b1 = bp[1];
-            dstart[q] = a.row_ptr[s] + b0;
-            dlen[q] = (b1 - b0) | (s >= a.n_exc ? 0x80000000u : 0u);
+            sm.dstart[q] = rs + b0;
+            sm.dlen[q] = (b1 - b0) | (s >= a.n_exc ? 0x80000000u : 0u);
             delivered += b1 - b0;
         }
         __syncthreads();
-        for (uint32_t q = grp; q < nq; q += ngrp) {
-            const uint64_t st = dstart[q];
-            const uint32_t lw = dlen[q];
-            const uint64_t en = st + (lw & 0x7FFFFFFFu);
-            const uint32_t qv = (lw >> 31) ? 65536u : 1u;
-            for (uint64_t w = (st & ~3ull) + lig * 4u; w < en; w += GS * 4u) {
-                const uint2 v = ld_stream_v2(a.ent + w);
-                const uint32_t e[4] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16};
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (w + u >= st && w + u < en) atomicAdd(&cnt[e[u]], qv);
+        // ---- walk the segments: GS lanes per segment, two segments in flight ----
+        for (uint32_t q = grp; q < nq; q += 2 * ngrp) {
+            const bool hasB = q + ngrp < nq;
+            const uint64_t stA = sm.dstart[q], stB = hasB ? sm.dstart[q + ngrp] : 0ull;
+            const uint32_t lA = sm.dlen[q], lB = hasB ? sm.dlen[q + ngrp] : 0u;
+            const uint64_t enA = stA + (lA & 0x7FFFFFFFu), enB = stB + (lB & 0x7FFFFFFFu);
+            const uint32_t qA = (lA >> 31) ? 65536u : 1u, qB = (lB >> 31) ? 65536u : 1u;
+            uint64_t wA = (stA & ~7ull) + 8u * lig, wB = (stB & ~7ull) + 8u * lig;
+            uint4 vA = make_uint4(0, 0, 0, 0), vB = make_uint4(0, 0, 0, 0);
+            if (wA < enA) vA = ld_stream_v4(a.ent + wA);
+            if (wB < enB) vB = ld_stream_v4(a.ent + wB);
+            if (wA < enA) accumulate8(sm.cnt, vA, wA, stA, enA, qA);
+            if (wB < enB) accumulate8(sm.cnt, vB, wB, stB, enB, qB);
+            for (wA += 8u * GS; wA < enA; wA += 8u * GS) accumulate8(sm.cnt, ld_stream_v4(a.ent + wA), wA, stA, enA, qA);
+            for (wB += 8u * GS; wB < enB; wB += 8u * GS) accumulate8(sm.cnt, ld_stream_v4(a.ent + wB), wB, stB, enB, qB);
+        }
+        __syncthreads();
+    }
+    return delivered;
+}
+
+// ------------------------------------------------------------- Brunel+ STDP
+// Reading R13 (eager, in the oracle's order): (i) every post spike i of this tile at step
+// t potentiates its plastic in-synapses w += A+ x_pre(t) (clamped at w_max); (ii) the
+// delivery walk depresses every plastic synapse of a spiking pre w -= A- y_post(t)
+// (clamped at 0) and then delivers w as int64 fixed point rint(w 2^32) (reading R10);
+// (iii) traces advance x(t+1) = a+ (x(t) + s(t)), y likewise.  Every synapse touched by
+// CTA b has its target in tile b, so no two CTAs write the same weight.
+__device__ __forceinline__ const uint32_t *step_bitmap(const SimArgs &a, uint64_t t) {
+    return a.record + (t % a.record_steps) * (uint64_t)a.G * a.W + (uint64_t)a.rank * a.W;
+}
+
+__device__ __forceinline__ bool plastic_src(const SimArgs &a, uint32_t s) {
+    for (uint32_t q = 0; q < a.npl; ++q)
+        if (s >= a.pl[q][0] && s < a.pl[q][1]) return true;
+    return false;
+}
+__device__ __forceinline__ bool plastic_edge(const SimArgs &a, uint32_t s, uint32_t j) {
+    for (uint32_t q = 0; q < a.npl; ++q)
+        if (s >= a.pl[q][0] && s < a.pl[q][1] && j >= a.pl[q][2] && j < a.pl[q][3]) return true;
+    return false;
+}
+
+__device__ void potentiate_tile(const SimArgs &a, uint64_t t, uint32_t b) {
+    const uint32_t *bm = step_bitmap(a, t);
+    const float *x = a.xtr + (t & 1) * (uint64_t)a.N;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lo = b * a.TW, hi = min(lo + a.TW, a.n_own);
+    for (uint32_t wi = lo / 32 + warp; wi < (hi + 31) / 32; wi += kBlock / 32) {
+        uint32_t word = bm[wi];
+        while (word) {
+            const uint32_t i = wi * 32 + __ffs(word) - 1;
+            word &= word - 1;
+            for (uint64_t e = a.in_ptr[i] + lane; e < a.in_ptr[i + 1]; e += 32) {
+                const uint64_t pos = a.in_pos[e];
+                const float wv = __fadd_rn(a.w[pos], __fmul_rn(a.mc.Ap, x[a.in_src[e]]));
+                a.w[pos] = wv < a.mc.wmax ? wv : a.mc.wmax;
             }
         }
     }
+}
+
+__device__ void stdp_traces(const SimArgs &a, uint64_t t, uint32_t b) {
+    const uint32_t *bm = step_bitmap(a, t);
+    const uint32_t lo = b * a.TW, hi = min(lo + a.TW, a.n_own);
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += kBlock) {
+        const float sp = (bm[i >> 5] >> (i & 31)) & 1u ? 1.0f : 0.0f;
+        a.ytr[i] = __fmul_rn(a.mc.am, __fadd_rn(a.ytr[i], sp));
+    }
+    // pre traces of every global source: CTA b advances slice b of [0, N)
+    const float *xo = a.xtr + (t & 1) * (uint64_t)a.N;
+    float *xn = a.xtr + ((t + 1) & 1) * (uint64_t)a.N;
+    const uint32_t per = (a.N + a.NT * a.C - 1) / (a.NT * a.C);
+    const uint32_t j0 = blockIdx.x * per, j1 = min(a.N, j0 + per);
+    const uint32_t *gbm = a.record + (t % a.record_steps) * (uint64_t)a.G * a.W;
+    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kBlock) {
+        const uint32_t r = (j / a.S) % a.G;
+        const uint32_t il = (j / a.S / a.G) * a.S + j % a.S;
+        const float sp = (gbm[(uint64_t)r * a.W + (il >> 5)] >> (il & 31)) & 1u ? 1.0f : 0.0f;
+        xn[j] = __fmul_rn(a.mc.ap, __fadd_rn(xo[j], sp));
+    }
+}
+
+__device__ __forceinline__ void walk_plastic(const SimArgs &a, uint32_t b, uint32_t *cnt, long long *pin,
+                                             uint64_t w, uint64_t st, uint64_t en, uint32_t q,
+                                             uint32_t s, bool pls) {
+    const uint4 v = ld_stream_v4(a.ent + w);
+    const uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
+                           v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        if (w + u < st || w + u >= en) continue;
+        const uint32_t off = e[u];
+        const uint32_t il = b * a.TW + off;
+        if (pls && plastic_edge(a, s, (uint32_t)local_to_global(il, a.rank, a.G, a.S))) {
+            float wv = __fsub_rn(a.w[w + u], __fmul_rn(a.mc.Am, a.ytr[il]));
+            wv = wv > 0.0f ? wv : 0.0f;
+            a.w[w + u] = wv;
+            atomicAdd(reinterpret_cast<unsigned long long *>(&pin[off]),
+                      (unsigned long long)__double2ll_rn((double)wv * 4294967296.0));
+        } else {
+            atomicAdd(&cnt[off], q);
+        }
+    }
+}
+
+template <int GS>
+__device__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b, uint32_t *cnt,
+                                         long long *pin, uint32_t *pref, uint32_t *tmp) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t par = (uint32_t)(t & 1);
+    potentiate_tile(a, t, b);
+    for (uint32_t r = tid; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
     __syncthreads();
-    // Add the tile into the input ring slot of step t + delay (exclusive owner when C = 1).
+    block_exclusive_scan(pref, a.NR, tmp);       // also orders (i) before (ii)
+    const uint32_t n_sp = pref[a.NR];
+    const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
+    uint32_t delivered = 0;
+    const uint32_t grp = tid / GS, lig = tid % GS;
+    for (uint32_t p = grp; p < n_sp; p += kBlock / GS) {
+        const uint32_t r = region_of(pref, a.NR, p);
+        const uint64_t slot = lbase + (uint64_t)r * a.RS + (p - pref[r]);
+        const uint32_t s = a.sl_ids[slot];
+        const uint32_t *bp = a.bnd + (uint64_t)s * (a.NT + 1u) + b;
+        const uint64_t st = a.sl_rows[slot] + bp[0], en = a.sl_rows[slot] + bp[1];
+        const uint32_t q = s >= a.n_exc ? 65536u : 1u;
+        const bool pls = plastic_src(a, s);
+        if (lig == 0) delivered += (uint32_t)(en - st);
+        for (uint64_t w = (st & ~7ull) + 8u * lig; w < en; w += 8u * GS) walk_plastic(a, b, cnt, pin, w, st, en, q, s, pls);
+    }
+    __syncthreads();
+    stdp_traces(a, t, b);
+    return delivered;
+}
+
+__device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot, uint32_t d, uint32_t *s_tmp) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xFFFFFFFFu, d, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s_tmp[threadIdx.x >> 5] = d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < kBlock / 32; ++w) tot += s_tmp[w];
+        a.delivered_cta[slot] += tot;
+    }
+}
+
+__device__ __forceinline__ DeliverSmem carve(const SimArgs &a, uint32_t *smem) {
+    DeliverSmem sm;
+    const uint32_t tw4 = (a.TW + 3u) & ~3u;
+    sm.cnt = smem;
+    sm.dstart = reinterpret_cast<uint64_t *>(smem + tw4);
+    sm.dlen = smem + tw4 + 2 * kDescChunk;
+    sm.pref = sm.dlen + kDescChunk;
+    sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
+    return sm;
+}
+
+size_t tile_smem_bytes(uint32_t TW, uint32_t NR) {
+    const uint32_t tw4 = (TW + 3u) & ~3u;
+    return ((size_t)tw4 + 3 * kDescChunk + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
+}
+
+// Brunel+ tile kernels: counters [TW] u32, plastic sums [TW] i64, region prefix, scan tmp.
+size_t plastic_smem_bytes(uint32_t TW, uint32_t NR) {
+    const uint32_t tw4 = (TW + 3u) & ~3u;
+    return (size_t)tw4 * 4 + (size_t)tw4 * 8 + (((NR + 1 + 3) & ~3u) + 32) * 4 + 16;
+}
+struct PlasticSmem { uint32_t *cnt; long long *pin; uint32_t *pref; uint32_t *tmp; };
+__device__ __forceinline__ PlasticSmem carve_plastic(const SimArgs &a, uint32_t *smem) {
+    PlasticSmem sm;
+    const uint32_t tw4 = (a.TW + 3u) & ~3u;
+    sm.pin = reinterpret_cast<long long *>(smem);          // 8-byte aligned first
+    sm.cnt = smem + 2 * tw4;
+    sm.pref = sm.cnt + tw4;
+    sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
+    return sm;
+}
+
+// ------------------------------------------------------------------ kernels
+template <int MODEL>
+__global__ void __launch_bounds__(kBlock) k_update(SimArgs a, uint32_t k) {
+    __shared__ uint32_t s_count;
+    if (threadIdx.x == 0) s_count = 0;
+    __syncthreads();
+    update_tile<MODEL>(a, *a.t0 + k, blockIdx.x, nullptr, a.G == 1, &s_count);
+}
+
+template <int GS>
+__global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    DeliverSmem sm = carve(a, smem);
+    const uint64_t t = *a.t0 + k;
+    const uint32_t b = blockIdx.x / a.C, c = blockIdx.x % a.C;
+    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
+    const uint32_t d = deliver_tile<GS>(a, t, b, c, sm);
     uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
     if (a.C == 1u) {
-        for (uint32_t x = tid * 4u; x < a.TW; x += kDeliverBlock * 4u) {
+        for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u) {
             uint4 o = *reinterpret_cast<uint4 *>(dst + x);
-            o.x += cnt[x]; o.y += cnt[x + 1]; o.z += cnt[x + 2]; o.w += cnt[x + 3];
+            o.x += sm.cnt[x]; o.y += sm.cnt[x + 1]; o.z += sm.cnt[x + 2]; o.w += sm.cnt[x + 3];
             *reinterpret_cast<uint4 *>(dst + x) = o;
         }
     } else {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
-        if (tid == 0) {
+        if (threadIdx.x == 0) {
             const uint32_t bytes_total = a.TW * 4u;
             for (uint32_t off = 0; off < bytes_total; off += 32768u) {
                 const uint32_t nb = min(32768u, bytes_total - off);
-                const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(cnt) + off;
+                const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(sm.cnt) + off;
                 asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u32 [%0], [%1], %2;"
                              :: "l"(reinterpret_cast<char *>(dst) + off), "r"(saddr), "r"(nb) : "memory");
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
     }
-    // delivered-event statistics: one atomic per CTA
-    __shared__ uint32_t s_red[kDeliverBlock / 32];
-    uint32_t d = delivered;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xFFFFFFFFu, d, o);
-    if ((tid & 31) == 0) s_red[tid >> 5] = d;
-    __syncthreads();
-    if (tid == 0) {
-        unsigned long long tot = 0;
-        for (int w = 0; w < kDeliverBlock / 32; ++w) tot += s_red[w];
-        if (tot) atomicAdd(&a.stats[1], tot);
-    }
-    if (a.C != 1u && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    store_delivered(a, blockIdx.x, d, sm.tmp);
+    if (a.C != 1u && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// Paper-style baseline: warp i delivers spike (i mod |S|) to column block floor(i/|S|)
-// (column-wise; here a column block is one tile segment), with global atomics.
-__global__ void __launch_bounds__(256) deliver_global_atomics(SimArgs a, uint32_t k,
-                                                              const uint32_t *__restrict__ list) {
+template <int GS>
+__global__ void __launch_bounds__(kBlock) k_deliver_plastic(SimArgs a, uint32_t k) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    PlasticSmem sm = carve_plastic(a, smem);
     const uint64_t t = *a.t0 + k;
-    const uint32_t n_sp = a.spcount[t % 3];
+    const uint32_t b = blockIdx.x;
+    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.pin[x] = 0; }
+    const uint32_t d = deliver_tile_plastic<GS>(a, t, b, sm.cnt, sm.pin, sm.pref, sm.tmp);
+    const uint64_t base = ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
+    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
+        a.ring[base + x] += sm.cnt[x];
+        a.pring[base + x] += sm.pin[x];
+    }
+    store_delivered(a, b, d, sm.tmp);
+}
+
+template <int MODEL, int GS>
+__global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
+    if (MODEL == 3) {                                       // Brunel+ (delay >= 1 via the rings)
+        extern __shared__ __align__(16) uint32_t smem[];
+        PlasticSmem sm = carve_plastic(a, smem);
+        __shared__ uint32_t s_count3;
+        const uint64_t t = *a.t0 + k;
+        const uint32_t b = blockIdx.x;
+        if (threadIdx.x == 0) s_count3 = 0;
+        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.pin[x] = 0; }
+        const uint32_t d = deliver_tile_plastic<GS>(a, t, b, sm.cnt, sm.pin, sm.pref, sm.tmp);
+        const uint64_t base = ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
+        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
+            a.ring[base + x] += sm.cnt[x];
+            a.pring[base + x] += sm.pin[x];
+        }
+        store_delivered(a, b, d, sm.tmp);
+        __syncthreads();
+        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count3);
+        return;
+    }
+    extern __shared__ __align__(16) uint32_t smem[];
+    DeliverSmem sm = carve(a, smem);
+    __shared__ uint32_t s_count;
+    const uint64_t t = *a.t0 + k;
+    const uint32_t b = blockIdx.x;
+    if (threadIdx.x == 0) s_count = 0;
+    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
+    const uint32_t d = deliver_tile<GS>(a, t, b, 0, sm);
+    store_delivered(a, b, d, sm.tmp);
+    if (a.delay == 1) {
+        update_tile<MODEL>(a, t + 1, b, sm.cnt, true, &s_count);
+    } else {
+        uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
+        for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)
+            *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(sm.cnt + x);
+        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count);
+    }
+}
+
+// Paper-style baseline: warp w delivers spike (w mod |S|) to tile (w / |S|), column-wise
+// (P:200), with one global atomic per event.
+__global__ void __launch_bounds__(kBlock) k_global_atomics(SimArgs a, uint32_t k) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t *pref = smem, *tmp = smem + ((a.NR + 1 + 3) & ~3u);
+    const uint64_t t = *a.t0 + k;
+    const uint32_t par = (uint32_t)(t & 1);
+    for (uint32_t r = threadIdx.x; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
+    __syncthreads();
+    block_exclusive_scan(pref, a.NR, tmp);
+    const uint32_t n_sp = pref[a.NR];
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
     uint32_t *slot = a.ring + ((t + a.delay) % a.D) * a.ring_stride;
+    const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
     uint32_t delivered = 0;
-    for (uint64_t w = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-         w < (uint64_t)a.NT * n_sp; w += nwarps) {
+    for (uint64_t w = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); w < (uint64_t)a.NT * n_sp; w += nwarps) {
         const uint32_t b = (uint32_t)(w / n_sp), p = (uint32_t)(w % n_sp);
-        const uint32_t s = list[p];
+        const uint32_t r = region_of(pref, a.NR, p);
+        const uint64_t sl = lbase + (uint64_t)r * a.RS + (p - pref[r]);
+        const uint32_t s = a.sl_ids[sl];
         const uint32_t *bp = a.bnd + (uint64_t)s * (a.NT + 1u) + b;
-        const uint32_t b0 = bp[0], b1 = bp[1];
-        const uint64_t st = a.row_ptr[s] + b0;
+        const uint64_t st = a.sl_rows[sl] + bp[0];
+        const uint32_t len = bp[1] - bp[0];
         const uint32_t qv = s >= a.n_exc ? 65536u : 1u;
         uint32_t *tile = slot + (uint64_t)b * a.TW;
-        for (uint32_t e = lane; e < b1 - b0; e += 32) atomicAdd(tile + a.ent[st + e], qv);
-        if (lane == 0) delivered += b1 - b0;
+        for (uint32_t e = lane; e < len; e += 32) atomicAdd(tile + a.ent[st + e], qv);
+        if (lane == 0) delivered += len;
     }
-    if (lane == 0 && delivered) atomicAdd(&a.stats[1], (unsigned long long)delivered);
+    store_delivered(a, blockIdx.x % (a.NT * a.C), delivered, tmp);
 }
 
-// Gathered bitmaps of all ranks -> global spike list + record ring copy.
-__global__ void __launch_bounds__(256) bitmap_to_list(SimArgs a, uint32_t k) {
+// Gathered bitmaps of all ranks -> global spike list regions + record ring copy.
+__global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
+    __shared__ uint32_t s_count;
     const uint64_t t = *a.t0 + k;
-    const uint32_t idx = blockIdx.x * 256 + threadIdx.x;
-    const uint32_t nw = a.G * a.W;
-    const uint32_t word = idx < nw ? a.gather[idx] : 0u;
-    if (idx < nw) a.record[(t % a.record_steps) * (uint64_t)nw + idx] = word;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t cnt = __popc(word), incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= (uint32_t)o) incl += y;
-    }
-    __shared__ uint32_t s_w[8];
-    __shared__ uint32_t s_base;
-    if (lane == 31) s_w[warp] = incl;
+    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t nw = a.G * a.W, r = blockIdx.x;
+    if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t tot = 0;
-        for (int w = 0; w < 8; ++w) { const uint32_t cw = s_w[w]; s_w[w] = tot; tot += cw; }
-        s_base = tot ? atomicAdd(&a.spcount[t % 3], tot) : 0u;
-        if (blockIdx.x == 0) a.spcount[(t + 1) % 3] = 0u;
-    }
-    __syncthreads();
-    uint32_t pos = s_base + s_w[warp] + incl - cnt;
-    if (word) {
-        const uint32_t r = idx / a.W, wl = idx % a.W;
-        uint32_t bits = word;
-        while (bits) {
-            const uint32_t bit = __ffs(bits) - 1;
-            bits &= bits - 1;
-            a.splist[pos++] = (uint32_t)local_to_global((uint64_t)wl * 32 + bit, r, a.G, a.S);
+    uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + r) * a.RS;
+    uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + r) * a.RS;
+    for (uint32_t q0 = 0; q0 < kB2LWords; q0 += kBlock) {
+        const uint32_t idx = r * kB2LWords + q0 + threadIdx.x;
+        const bool in = q0 + threadIdx.x < kB2LWords && idx < nw;
+        const uint32_t word = in ? a.gather[idx] : 0u;
+        if (in) a.record[(t % a.record_steps) * (uint64_t)nw + idx] = word;
+        const uint32_t cnt = __popc(word), incl = warp_incl_scan(cnt);
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        uint32_t base = 0;
+        if ((threadIdx.x & 31) == 0 && tot) base = atomicAdd(&s_count, tot);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        uint32_t pos = base + incl - cnt;
+        if (word) {
+            const uint32_t rk = idx / a.W, wl = idx % a.W;
+            uint32_t bits = word;
+            while (bits) {
+                const uint32_t bit = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const uint32_t j = (uint32_t)local_to_global((uint64_t)wl * 32 + bit, rk, a.G, a.S);
+                region[pos] = j;
+                region_rows[pos] = a.row_ptr[j];
+                ++pos;
+            }
         }
     }
+    __syncthreads();
+    if (threadIdx.x == 0) a.sl_counts[par * a.NR + r] = s_count;
 }
 
-__global__ void advance_kernel(uint64_t *t0, uint32_t steps) { *t0 += steps; }
+__global__ void k_advance(uint64_t *t0, uint32_t steps) { *t0 += steps; }
 
 // ------------------------------------------------------------------ launchers
-cudaError_t launch_update(const SimArgs &a, uint32_t k, bool produce_list, cudaStream_t s) {
-    const uint32_t threads = a.W * 32u;
-    const uint32_t grid = (threads + kUpdateBlock - 1) / kUpdateBlock;
+static uint32_t group_lanes(double mean_seg) {
+    if (mean_seg <= 10) return 1;
+    if (mean_seg <= 22) return 2;
+    if (mean_seg <= 48) return 4;
+    if (mean_seg <= 100) return 8;
+    if (mean_seg <= 200) return 16;
+    return 32;
+}
+
+uint32_t pick_group_lanes(double mean_seg) { return group_lanes(mean_seg); }
+
+template <typename K>
+static cudaError_t allow_smem(K kern, size_t bytes) {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+cudaError_t prepare_kernels(const SimArgs &a) {
+    const size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    cudaError_t e = cudaSuccess;
+#define ALLOW(kern) if (!e) e = allow_smem(kern, bytes)
+    ALLOW(k_deliver<1>); ALLOW(k_deliver<2>); ALLOW(k_deliver<4>); ALLOW(k_deliver<8>);
+    ALLOW(k_deliver<16>); ALLOW(k_deliver<32>);
+#define ALLOW_M(M) ALLOW((k_fused<M, 1>)); ALLOW((k_fused<M, 2>)); ALLOW((k_fused<M, 4>)); \
+    ALLOW((k_fused<M, 8>)); ALLOW((k_fused<M, 16>)); ALLOW((k_fused<M, 32>))
+    ALLOW_M(1); ALLOW_M(2); ALLOW_M(4);
+    ALLOW(k_global_atomics);
+    if (a.model == 3) {
+        const size_t pb = plastic_smem_bytes(a.TW, a.NR);
+#define ALLOWP(kern) if (!e) e = allow_smem(kern, pb)
+        ALLOWP(k_deliver_plastic<1>); ALLOWP(k_deliver_plastic<2>); ALLOWP(k_deliver_plastic<4>);
+        ALLOWP(k_deliver_plastic<8>); ALLOWP(k_deliver_plastic<16>); ALLOWP(k_deliver_plastic<32>);
+        ALLOWP((k_fused<3, 1>)); ALLOWP((k_fused<3, 2>)); ALLOWP((k_fused<3, 4>));
+        ALLOWP((k_fused<3, 8>)); ALLOWP((k_fused<3, 16>)); ALLOWP((k_fused<3, 32>));
+#undef ALLOWP
+    }
+#undef ALLOW_M
+#undef ALLOW
+    return e;
+}
+
+cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s) {
     switch (a.model) {
-    case 1: update_kernel<1><<<grid, kUpdateBlock, 0, s>>>(a, k, produce_list); break;
-    case 2: update_kernel<2><<<grid, kUpdateBlock, 0, s>>>(a, k, produce_list); break;
-    case 4: update_kernel<4><<<grid, kUpdateBlock, 0, s>>>(a, k, produce_list); break;
+    case 1: k_update<1><<<a.NT, kBlock, 0, s>>>(a, k); break;
+    case 2: k_update<2><<<a.NT, kBlock, 0, s>>>(a, k); break;
+    case 3: k_update<3><<<a.NT, kBlock, 0, s>>>(a, k); break;
+    case 4: k_update<4><<<a.NT, kBlock, 0, s>>>(a, k); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
-size_t deliver_smem_bytes(uint32_t TW) {
-    const uint32_t tw_pad = (TW + 3u) & ~3u;
-    return (size_t)(tw_pad + 1) * 4 + (size_t)kDescChunk * 12 + 16;
-}
-
-static uint32_t pick_group(const SimArgs &a, double mean_seg) {
-    (void)a;
-    if (mean_seg <= 12) return 4;
-    if (mean_seg <= 28) return 8;
-    if (mean_seg <= 60) return 16;
-    return 32;
-}
-
-cudaError_t prepare_deliver(uint32_t TW) {
-    const int bytes = (int)deliver_smem_bytes(TW);
-    cudaError_t e;
-    if ((e = cudaFuncSetAttribute(deliver_tiled<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
-    if ((e = cudaFuncSetAttribute(deliver_tiled<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
-    if ((e = cudaFuncSetAttribute(deliver_tiled<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
-    return cudaFuncSetAttribute(deliver_tiled<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-}
-
-cudaError_t launch_deliver(const SimArgs &a, uint32_t k, double mean_seg, int n_sm, cudaStream_t s) {
-    const uint32_t *list = a.splist;
-    if (a.global_atomics) {
-        deliver_global_atomics<<<n_sm * 8, 256, 0, s>>>(a, k, list);
+cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, int n_sm, cudaStream_t s) {
+    if (global_atomics) {
+        const size_t bytes = tile_smem_bytes(0, a.NR);
+        k_global_atomics<<<min((uint32_t)(n_sm * 4), a.NT * a.C), kBlock, bytes, s>>>(a, k);
         return cudaGetLastError();
     }
-    const size_t smem = deliver_smem_bytes(a.TW);
+    if (a.model == 3) {
+        const size_t pb = plastic_smem_bytes(a.TW, a.NR);
+        switch (a.GS) {
+        case 1: k_deliver_plastic<1><<<a.NT, kBlock, pb, s>>>(a, k); break;
+        case 2: k_deliver_plastic<2><<<a.NT, kBlock, pb, s>>>(a, k); break;
+        case 4: k_deliver_plastic<4><<<a.NT, kBlock, pb, s>>>(a, k); break;
+        case 8: k_deliver_plastic<8><<<a.NT, kBlock, pb, s>>>(a, k); break;
+        case 16: k_deliver_plastic<16><<<a.NT, kBlock, pb, s>>>(a, k); break;
+        default: k_deliver_plastic<32><<<a.NT, kBlock, pb, s>>>(a, k); break;
+        }
+        return cudaGetLastError();
+    }
+    const size_t bytes = tile_smem_bytes(a.TW, a.NR);
     const uint32_t grid = a.NT * a.C;
-    switch (pick_group(a, mean_seg)) {
-    case 4: deliver_tiled<4><<<grid, kDeliverBlock, smem, s>>>(a, k, list); break;
-    case 8: deliver_tiled<8><<<grid, kDeliverBlock, smem, s>>>(a, k, list); break;
-    case 16: deliver_tiled<16><<<grid, kDeliverBlock, smem, s>>>(a, k, list); break;
-    default: deliver_tiled<32><<<grid, kDeliverBlock, smem, s>>>(a, k, list); break;
+    switch (a.GS) {
+    case 1: k_deliver<1><<<grid, kBlock, bytes, s>>>(a, k); break;
+    case 2: k_deliver<2><<<grid, kBlock, bytes, s>>>(a, k); break;
+    case 4: k_deliver<4><<<grid, kBlock, bytes, s>>>(a, k); break;
+    case 8: k_deliver<8><<<grid, kBlock, bytes, s>>>(a, k); break;
+    case 16: k_deliver<16><<<grid, kBlock, bytes, s>>>(a, k); break;
+    default: k_deliver<32><<<grid, kBlock, bytes, s>>>(a, k); break;
+    }
+    return cudaGetLastError();
+}
+
+template <int M>
+static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
+    switch (a.GS) {
+    case 1: k_fused<M, 1><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+    case 2: k_fused<M, 2><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+    case 4: k_fused<M, 4><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+    case 8: k_fused<M, 8><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+    case 16: k_fused<M, 16><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+    default: k_fused<M, 32><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+    }
+}
+
+cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
+    const size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    switch (a.model) {
+    case 1: fused_m<1>(a, k, bytes, s); break;
+    case 2: fused_m<2>(a, k, bytes, s); break;
+    case 3: fused_m<3>(a, k, plastic_smem_bytes(a.TW, a.NR), s); break;
+    case 4: fused_m<4>(a, k, bytes, s); break;
+    default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s) {
-    const uint32_t nw = a.G * a.W;
-    bitmap_to_list<<<(nw + 255) / 256, 256, 0, s>>>(a, k);
+    k_b2l<<<a.NR, kBlock, 0, s>>>(a, k);
     return cudaGetLastError();
 }
 
 cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s) {
-    advance_kernel<<<1, 1, 0, s>>>(t0, steps);
+    k_advance<<<1, 1, 0, s>>>(t0, steps);
     return cudaGetLastError();
 }
 

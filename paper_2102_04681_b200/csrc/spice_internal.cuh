@@ -11,10 +11,11 @@ namespace spice {
 // Philox counter word 3 stream tags (reading R9).
 enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFire = 5 };
 
-constexpr int kUpdateBlock = 256;     // threads per update CTA (8 warps -> 8 bitmap words)
-constexpr int kDeliverBlock = 512;    // threads per delivery CTA
-constexpr int kDescChunk = 1024;      // segment descriptors staged in smem per pass
+constexpr int kBlock = 1024;          // threads per tile CTA (update / deliver / fused)
+constexpr int kDescChunk = 2048;      // segment descriptors staged in smem per pass
 constexpr uint32_t kMaxTileWidth = 49152;   // u32 counters per tile <= 192 KiB smem
+constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
+constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list region
 constexpr int kEntPad = 64;           // u16 padding before/after the entry array
 
 // Philox4x32-10 (Salmon et al., SC'11).  Multipliers 0xD2511F53 / 0xCD9E8D57, Weyl
@@ -48,32 +49,63 @@ struct ModelConst {
     uint64_t thr_fire;                                // synth: floor(a 2^32) (2^32 = always)
     const uint64_t *ptab;                             // Brunel: Poisson inversion table
     uint32_t ptab_len;
+    float ap, am, Ap, Am, wmax;                       // Brunel+ STDP (reading R13)
 };
 
+constexpr int kMaxPlasticRules = 4;
+
 // Everything a step kernel needs, passed by value.
+//
+// Connectivity (destination-tiled, source-major CSR): owned targets (local indices) are
+// cut into NT tiles of TW; row s = ent[row_ptr[s] .. row_ptr[s+1]) is the concatenation of
+// its tile segments, segment (s, b) = row_ptr[s] + [bnd[s*(NT+1)+b], bnd[s*(NT+1)+b+1]);
+// entries are u16 offsets inside the tile, ascending within a segment.  Rows stay
+// contiguous so that neighbouring tiles' segments share DRAM sectors through L2.
+//
+// Spike lists: per step parity p, NR regions of RS slots; region r holds counts[p*NR+r]
+// spikes: global source IDs at ids[(p*NR + r)*RS ...] and their row starts at rows[...]
+// (order inside a step is irrelevant to the integer accumulation, reading R10; the
+// bitmap record is the canonical output).
 struct SimArgs {
     uint32_t model, N, n_exc, delay, D, rank, G, S;
     uint32_t n_own;          // owned neurons of this rank
     uint32_t W;              // bitmap words per rank
     uint32_t TW, NT, C;      // tile width, tile count, CTAs per tile
+    uint32_t GS;             // lanes per segment group in delivery
     uint64_t ring_stride;    // NT * TW
     uint32_t record_steps;
     uint32_t key0, key1;
-    uint32_t global_atomics; // delivery variant
+    uint32_t NR, RS;         // spike-list regions
     ModelConst mc;
-    // device buffers
-    const uint64_t *row_ptr; // [N+1] row starts (global source rows)
-    const uint32_t *bnd;     // [N * (NT+1)] segment starts within the row
-    const uint16_t *ent;     // tile-local target offsets
+    // connectivity
+    const uint64_t *row_ptr; // [N+1]
+    const uint32_t *bnd;     // [N * (NT+1)]
+    const uint16_t *ent;
+    // state
     float *v, *ge, *gi;
     uint32_t *ref, *acc;
     uint32_t *ring;          // D * ring_stride packed receptor counts
-    uint32_t *splist;        // spike list (global IDs), capacity N
-    uint32_t *spcount;       // [3] per-step list lengths (rotating)
+    // spikes
+    uint32_t *sl_ids;        // 2 * NR * RS
+    uint64_t *sl_rows;       // 2 * NR * RS row starts of the listed spikes
+    uint32_t *sl_counts;     // 2 * NR
     uint32_t *record;        // record_steps * G * W words
     uint32_t *sendbuf;       // W words (G > 1)
     uint32_t *gather;        // G * W words (G > 1)
-    unsigned long long *stats;   // [0] fired, [1] delivered
+    unsigned long long *fired_cta;      // [NT]   per-CTA counters (no shared atomics)
+    unsigned long long *delivered_cta;  // [NT*C]
+    // Brunel+ (model 3): per-synapse weights aligned with ent, fixed-point plastic input
+    // ring, pre traces x for all N sources (double-buffered by step parity), post traces
+    // y for owned neurons, and per-target in-synapse index (absolute entry, source).
+    float *w;
+    long long *pring;        // D * ring_stride, rint(w 2^32) sums
+    float *xtr;              // 2 * N
+    float *ytr;              // ring_stride
+    const uint64_t *in_ptr;  // [n_own + 1]
+    const uint64_t *in_pos;
+    const uint32_t *in_src;
+    uint32_t npl;                                  // plastic boxes (src x dst ranges)
+    uint32_t pl[kMaxPlasticRules][4];
     const uint64_t *t0;      // step index of the first step of this graph replay
     const uint32_t *force_bits;  // W words over local indices
     const uint64_t *force_ctl;   // [0] forced step (~0 = none), [1] mode

@@ -8,10 +8,13 @@
 namespace spice {
 
 // ---- step kernels (sim.cu) ----
-cudaError_t launch_update(const SimArgs &a, uint32_t k, bool produce_list, cudaStream_t s);
-cudaError_t prepare_deliver(uint32_t tile_width);
-size_t deliver_smem_bytes(uint32_t tile_width);
-cudaError_t launch_deliver(const SimArgs &a, uint32_t k, double mean_segment, int n_sm, cudaStream_t s);
+size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions);
+size_t plastic_smem_bytes(uint32_t tile_width, uint32_t n_regions);
+uint32_t pick_group_lanes(double mean_segment);
+cudaError_t prepare_kernels(const SimArgs &a);
+cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s);
+cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, int n_sm, cudaStream_t s);
+cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s);
 
@@ -36,6 +39,18 @@ cudaError_t gen_fill(const GenGeom &g, const GenRule &r, const uint64_t *row_ptr
 // Sort every (row, tile) segment ascending.
 cudaError_t gen_sort_segments(const GenGeom &g, const uint64_t *row_ptr, const uint32_t *bnd,
                               uint16_t *ent, cudaStream_t s);
+// In-place exclusive scan of n u64 values; data[n] receives the total.
+cudaError_t gen_scan_u64(uint64_t *data, uint64_t n, cudaStream_t s);
+// Brunel+: plastic boxes (src x dst ranges of plastic rules).
+struct PlasticBoxes {
+    uint32_t n;
+    uint32_t box[kMaxPlasticRules][4];
+};
+// Weights (w0 on plastic synapses) and the per-target in-synapse index.
+cudaError_t gen_plastic(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
+                        const uint32_t *bnd, const uint16_t *ent, float *w, float w0,
+                        uint32_t *tmp_cnt, uint64_t *in_ptr, uint64_t **in_pos, uint32_t **in_src,
+                        uint64_t *n_plastic, cudaStream_t s);
 // Initial state (reading R15).
 cudaError_t gen_init_uniform(const GenGeom &g, uint32_t field, float lo, float hi, float *out,
                              cudaStream_t s);

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_PKG, "libspice.so")
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ERANGE, ETRUNC, ESTATE = range(8)
 VOGELS, BRUNEL, BRUNEL_PLUS, SYNTH = 1, 2, 3, 4
-FLAG_EXTERNAL_EXCHANGE, FLAG_GLOBAL_ATOMICS = 0x1, 0x2
+FLAG_EXTERNAL_EXCHANGE, FLAG_GLOBAL_ATOMICS, FLAG_UNFUSED = 0x1, 0x2, 0x4
 FIELD_V, FIELD_GE, FIELD_GI, FIELD_REF, FIELD_ACC, FIELD_XTR, FIELD_YTR = range(7)
 ABI_VERSION = 1
 
@@ -85,6 +85,7 @@ def lib():
         "spice_partition_local_to_global": (u64, [u64, u32, u32, u32]),
         "spice_partition_owned_count": (u64, [u64, u32, u32, u32]),
         "spice_default_slice_width": (u32, [u64, u32]),
+        "spice_decode_bitmaps": (st, [vp, u32, u32, u32, vp, u64, C.POINTER(u64)]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -115,6 +116,16 @@ def default_slice_width(n: int, world_size: int) -> int:
     return lib().spice_default_slice_width(n, world_size)
 
 
+def decode_bitmaps(words: np.ndarray, world_size: int, words_per_rank: int, slice_width: int) -> np.ndarray:
+    """Gathered per-rank spike bitmaps of one step -> ascending global IDs (host only)."""
+    w = np.ascontiguousarray(words, dtype=np.uint32)
+    total = C.c_uint64(0)
+    out = np.zeros(max(1, int(sum(bin(int(x)).count("1") for x in w))), dtype=np.uint32)
+    _check(lib().spice_decode_bitmaps(w.ctypes.data, world_size, words_per_rank, slice_width,
+                                      out.ctypes.data, out.size, C.byref(total)))
+    return out[: total.value]
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().spice_nccl_unique_id(buf))
@@ -130,7 +141,7 @@ class Network:
     def __init__(self, cfg, rank: int = 0, world_size: int = 1, slice_width: int = 0,
                  device: int = 0, record_steps: int = 1024, nccl_id: Optional[bytes] = None,
                  external_exchange: bool = False, global_atomics: bool = False,
-                 tile_width: int = 0, ctas_per_tile: int = 0):
+                 tile_width: int = 0, ctas_per_tile: int = 0, unfused: bool = False):
         L = lib()
         self._rules = (Rule * max(1, len(cfg.rules)))()
         for q, r in enumerate(cfg.rules):
@@ -139,7 +150,7 @@ class Network:
         self._params = (C.c_double * max(1, len(cfg.params)))(*cfg.params)
         self._nccl = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         flags = (FLAG_EXTERNAL_EXCHANGE if external_exchange else 0) | \
-                (FLAG_GLOBAL_ATOMICS if global_atomics else 0)
+                (FLAG_GLOBAL_ATOMICS if global_atomics else 0) | (FLAG_UNFUSED if unfused else 0)
         c = Config(ABI_VERSION, cfg.model, cfg.n, cfg.n_exc, self._rules, len(cfg.rules),
                    cfg.delay, cfg.dt_ms, cfg.seed, cfg.activity, self._params, len(cfg.params),
                    rank, world_size, slice_width, device,
@@ -244,11 +255,13 @@ class Network:
 
     def profile(self, n_steps: int):
         """Average device ms per launch, each kernel bracketed by CUDA events on the
-        library stream: update, deliver, bitmap_to_list, allgather."""
+        library stream: update, deliver (unfused kernels), fused deliver(t)+update(t+1)
+        (G = 1), exchange (all-gather + bitmap->list, G > 1).  Advances the network by
+        2 * n_steps + 1 steps (G = 1) or n_steps steps."""
         out = np.zeros(4, dtype=np.float64)
         nk = C.c_uint32()
         _check(lib().spice_profile(self.h, n_steps, out.ctypes.data, 4, C.byref(nk)))
-        return {"update": out[0], "deliver": out[1], "bitmap_to_list": out[2], "allgather": out[3]}
+        return {"update": out[0], "deliver": out[1], "fused": out[2], "exchange": out[3]}
 
     def kernels_per_step(self) -> int:
         return lib().spice_kernels_per_step(self.h)

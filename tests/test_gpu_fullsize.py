@@ -1,0 +1,105 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times, on
+outputs the oracle can compute one by one (R17):
+
+* Brunel 100K (~1e9 synapses): sampled rows bit-exact against the oracle's brute-force
+  row; one full-size step replayed by the oracle from the GPU's state and inputs
+  (update bit-exact for all 100K neurons); the input ring after delivery equals the sum of
+  the oracle's rows of that step's spiking sources (every target).
+* Synth 3e9 synapses (one B200): every neuron's spike train bit-exact (the oracle
+  simulates the synth drive for all 1.39M neurons); the accumulators of sampled targets
+  equal the spike counts of the oracle's column (in-degree sources) of that target.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2102_04681_b200 import build as B
+    B.build()
+    from paper_2102_04681_b200 import spice
+    return spice
+
+
+@pytest.fixture(scope="module")
+def brunel(S):
+    cfg = W.brunel(100_000)
+    net = S.Network(cfg, record_steps=64)
+    yield cfg, net
+    net.free()
+
+
+def test_brunel100k_synapse_count_and_sampled_rows(S, brunel):
+    cfg, net = brunel
+    n = net.info()["n_synapses"]
+    mean = sum((r.src[1] - r.src[0]) * (r.dst[1] - r.dst[0]) * r.p for r in cfg.rules)
+    assert abs(n - mean) < 5 * np.sqrt(mean * 0.9)
+    rng = np.random.default_rng(1)
+    for s in list(rng.choice(cfg.n, 12, replace=False)) + [0, cfg.n_exc - 1, cfg.n_exc, cfg.n - 1]:
+        offs, tg = net.connectivity(int(s), int(s) + 1)
+        assert np.array_equal(tg, O.row(cfg, int(s))), s
+
+
+def test_brunel100k_one_step_update_and_delivery(S, brunel):
+    cfg, net = brunel
+    T0 = 40
+    net.step(T0 - net.stats()["steps"])
+    v0, ref0 = net.state(S.FIELD_V), net.state(S.FIELD_REF)
+    inp = [net.input(rel)[0] for rel in range(cfg.delay + 1)]
+    net.step(1)
+    sp = net.read_spikes(T0, T0 + 1)[0]
+    # (1) oracle replays step T0 for all neurons from the GPU's state and inputs
+    bare = dataclasses.replace(cfg, rules=())
+    o = O.OracleNet(bare)
+    o.set_state(O.F_V, v0)
+    o.set_state(O.F_REF, ref0)
+    o.set_time(T0)
+    for rel in range(cfg.delay + 1):
+        o.set_input(rel, inp[rel])
+    o.step(1)
+    assert np.array_equal(o.spikes()[T0], sp)
+    assert np.array_equal(o.state(O.F_V), net.state(S.FIELD_V))
+    assert np.array_equal(o.state(O.F_REF), net.state(S.FIELD_REF))
+    assert len(sp) > 0
+    # (2) the slot read at T0 + delay now holds exactly the deliveries of step T0:
+    #     packed counts of the oracle's rows of the spiking sources (every target)
+    want = inp[cfg.delay].astype(np.int64)     # earlier contents of that slot (zero)
+    assert not want.any()
+    for s in sp:
+        q = 1 if s < cfg.n_exc else 65536
+        np.add.at(want, O.row(cfg, int(s)).astype(np.int64), q)
+    got = net.input(cfg.delay - 1)[0]
+    assert np.array_equal(got.astype(np.int64), want)
+
+
+def test_synth3b_spikes_and_sampled_accumulators(S):
+    cfg = W.synth_weak(1)                      # 1,386,750 neurons, K = 2163, 3.0e9 synapses
+    T = 60
+    with S.Network(cfg, record_steps=T) as net:
+        assert net.info()["n_synapses"] == cfg.n * cfg.rules[0].k
+        net.step(T)
+        got = net.read_spikes(0, T)
+        acc = net.state(S.FIELD_ACC)
+        st = net.stats()
+    o = O.OracleNet(dataclasses.replace(cfg, rules=()))
+    o.step(T)
+    want = o.spikes()
+    assert all(np.array_equal(a, b) for a, b in zip(got, want))
+    counts = np.zeros(cfg.n, dtype=np.int64)
+    for s in want[:T - cfg.delay]:
+        counts[s] += 1
+    rng = np.random.default_rng(3)
+    for j in list(rng.choice(cfg.n, 24, replace=False)) + [0, cfg.n - 1]:
+        src = O.col(cfg, int(j))
+        assert len(src) == cfg.rules[0].k
+        assert acc[int(j)] == counts[src.astype(np.int64)].sum(), j
+    assert st["fired"] == sum(len(s) for s in want)
+    # every delivered event is one (spike, synapse) pair: K per target on average
+    assert abs(st["delivered"] / max(1, sum(len(s) for s in want)) - cfg.rules[0].k) < 0.02 * cfg.rules[0].k

@@ -166,7 +166,8 @@ def test_virtual_ranks_match_single_gpu(S, G, name):
 
 def test_edge_cases(S):
     # no synapses at all; tiny N below one warp; silent synth
-    cfg = dataclasses.replace(W.brunel(20, 0.0, seed=1, delay=2))
+    base = W.brunel(20, 0.1, seed=1, delay=2)
+    cfg = dataclasses.replace(base, rules=tuple(dataclasses.replace(r, p=0.0) for r in base.rules))
     o = O.OracleNet(cfg)
     with S.Network(cfg) as net:
         assert net.info()["n_synapses"] == 0
