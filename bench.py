@@ -42,7 +42,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10000)
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", default="spice", choices=["spice", "reference"])
-    ap.add_argument("--workload", default="synth", choices=["synth", "brunel100k", "vogels4000"])
+    ap.add_argument("--workload", default="synth", choices=["synth", "brunel100k", "brunelplus50k", "vogels4000"])
     ap.add_argument("--tile-width", type=int, default=0)
     ap.add_argument("--ctas-per-tile", type=int, default=0)
     ap.add_argument("--global-atomics", action="store_true", help="paper-style delivery (A/B)")
@@ -58,6 +58,8 @@ def workload(name: str, G: int):
         return W.synth_weak(G), "synth_3e9_synapses_per_gpu"
     if name == "brunel100k":
         return W.brunel(100_000), "brunel100k"
+    if name == "brunelplus50k":
+        return W.brunel_plus(50_000), "brunelplus50k"
     return W.vogels(4000), "vogels4000"
 
 
@@ -69,6 +71,8 @@ def cpu_sample(name: str, cfg):
             f"synth N={n} (1/32 of the GPU workload's neurons) with the same in-degree K={cfg.rules[0].k} and activity"
     if name == "brunel100k":
         return W.brunel(12_500), "brunel N=12,500 (base scale, p=0.1) instead of 100K"
+    if name == "brunelplus50k":
+        return W.brunel_plus(6_250), "brunel+ N=6,250 (p=0.1, same STDP) instead of 50K"
     return cfg, "vogels4000 (full workload)"
 
 

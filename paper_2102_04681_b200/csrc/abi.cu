@@ -130,6 +130,7 @@ struct spice_net {
     uint32_t *ref = nullptr, *acc = nullptr, *ring = nullptr;
     uint32_t *sl_ids = nullptr, *sl_counts = nullptr;
     uint64_t *sl_rows = nullptr;
+    uint64_t *desc = nullptr;
     uint32_t *record = nullptr, *sendbuf = nullptr, *gather = nullptr;
     unsigned long long *fired_cta = nullptr, *delivered_cta = nullptr;
     uint64_t *t0 = nullptr;
@@ -515,6 +516,8 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if ((st = dalloc_t(n, &n->sl_ids, 2ull * n->NR * n->RS, "spike lists"))) return bail(st);
     if ((st = dalloc_t(n, &n->sl_rows, 2ull * n->NR * n->RS, "spike list rows"))) return bail(st);
     if ((st = dalloc_t(n, &n->sl_counts, 2ull * n->NR, "spike list counts"))) return bail(st);
+    if (n->G == 1 && n->model != SPICE_BRUNEL_PLUS &&
+        (st = dalloc_t(n, &n->desc, 2ull * n->NT * n->NR * n->RS, "segment descriptors"))) return bail(st);
     if ((st = dalloc_t(n, &n->record, (size_t)n->R * n->G * n->W, "spike record"))) return bail(st);
     if ((st = dalloc_t(n, &n->sendbuf, std::max<uint32_t>(n->W, 1), "send bitmap"))) return bail(st);
     if ((st = dalloc_t(n, &n->gather, (size_t)n->G * std::max<uint32_t>(n->W, 1), "gathered bitmaps"))) return bail(st);
@@ -602,7 +605,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.mc = n->mc;
     a.row_ptr = n->row_ptr; a.bnd = n->bnd; a.ent = n->ent;
     a.v = n->v; a.ge = n->ge; a.gi = n->gi; a.ref = n->ref; a.acc = n->acc; a.ring = n->ring;
-    a.sl_ids = n->sl_ids; a.sl_rows = n->sl_rows; a.sl_counts = n->sl_counts; a.record = n->record; a.sendbuf = n->sendbuf;
+    a.sl_ids = n->sl_ids; a.sl_rows = n->sl_rows; a.sl_counts = n->sl_counts; a.desc = n->desc; a.record = n->record; a.sendbuf = n->sendbuf;
     a.gather = n->gather; a.fired_cta = n->fired_cta; a.delivered_cta = n->delivered_cta;
     a.t0 = n->t0; a.force_bits = n->force_bits; a.force_ctl = n->force_ctl;
     a.w = n->w; a.pring = n->pring; a.xtr = n->xtr; a.ytr = n->ytr;

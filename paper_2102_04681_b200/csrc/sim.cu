@@ -177,9 +177,42 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, uint64_t t, uint32
 
 // Update every neuron of tile b for step t.  Inputs come from `cnt` (shared memory, the
 // tile's counts) or, when cnt == nullptr, from input ring slot t mod D (read and cleared).
+// Descriptor transposition (G = 1): for the n spikes of region b (this tile's spikes), load
+// their bnd rows (coalesced, CH spikes at a time, staged in smem) and write, for every
+// destination tile bb, the CH descriptors desc[par][bb][b][q0 .. q0+CH) with one coalesced
+// store per tile.  Delivery CTAs then read their descriptors contiguously.
+__device__ void write_descriptors(const SimArgs &a, uint32_t par, uint32_t b, uint32_t n,
+                                  const uint32_t *region, const uint64_t *region_rows, uint32_t *stage) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t rowlen = a.NT + 1u;
+    const uint32_t CH = max(1u, min(32u, (uint32_t)kStageWords / rowlen));
+    for (uint32_t q0 = 0; q0 < n; q0 += CH) {
+        const uint32_t nq = min(CH, n - q0);
+        __syncthreads();
+        for (uint32_t ql = warp; ql < nq; ql += kBlock / 32) {            // one warp per spike row
+            const uint32_t *row = a.bnd + (uint64_t)region[q0 + ql] * rowlen;
+            for (uint32_t bb = lane; bb < rowlen; bb += 32) stage[ql * rowlen + bb] = row[bb];
+        }
+        __syncthreads();
+        // lane ql of warp w writes descriptor (tile bb, spike q0 + ql): coalesced per tile
+        const uint32_t ql = lane;
+        uint32_t s = 0;
+        uint64_t rs = 0;
+        if (ql < nq) { s = region[q0 + ql]; rs = region_rows[q0 + ql]; }
+        const uint64_t inh = s >= a.n_exc ? (1ull << 63) : 0ull;
+        for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
+            if (ql < nq) {
+                const uint32_t lo = stage[ql * rowlen + bb], hi = stage[ql * rowlen + bb + 1];
+                a.desc[(((uint64_t)par * a.NT + bb) * a.NR + b) * a.RS + q0 + ql] =
+                    (rs + lo) | ((uint64_t)(hi - lo) << 40) | inh;
+            }
+        }
+    }
+}
+
 template <int MODEL>
 __device__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, const uint32_t *cnt,
-                            bool write_list, uint32_t *s_count) {
+                            bool write_list, uint32_t *s_count, uint32_t *stage) {
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     const uint32_t lo = b * a.TW;
     const uint32_t span = lo < a.W * 32u ? min(a.TW, a.W * 32u - lo) : 0u;   // bitmap coverage
@@ -233,16 +266,20 @@ __device__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, const uint
         }
     }
     __syncthreads();
+    const uint32_t n_tile = *s_count;
     if (tid == 0) {
-        const uint32_t n = *s_count;
-        if (write_list) a.sl_counts[par * a.NR + b] = n;
-        a.fired_cta[b] += n;
-        *s_count = 0;
+        if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
+        a.fired_cta[b] += n_tile;
     }
+    if (write_list && a.desc) write_descriptors(a, par, b, n_tile, region, region_rows, stage);
+    __syncthreads();
+    if (tid == 0) *s_count = 0;
 }
 
 // ------------------------------------------------------------------ delivery
 struct DeliverSmem {
+    uint4 *wbuf;       // [32 warps * 4 stages * 32 lanes] cp.async window stages
+    uint32_t *stage;   // [kStageWords] descriptor-transposition staging (aliases dstart/dlen)
     uint32_t *cnt;     // [TW] tile counters
     uint32_t *pref;    // [NR + 1] region prefix
     uint64_t *dstart;  // [kDescChunk] absolute segment start in ent
@@ -259,6 +296,43 @@ __device__ __forceinline__ uint32_t region_of(const uint32_t *pref, uint32_t nr,
     return lo;
 }
 
+// Entries [lo, hi) of an 8-entry window are valid (lo, hi clamped to 0..8): one bitmask,
+// then predicated shared-memory atomics (no per-entry 64-bit compares or branches).
+__device__ __forceinline__ uint32_t window_mask(int lo, int hi) {
+    lo = max(lo, 0);
+    hi = min(hi, 8);
+    return hi > lo ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
+}
+// Predicated shared-memory reductions of one 8-entry window in a single asm block:
+// per slot one predicate test (bit u of m) and one predicated red.shared.add.u32.
+// cnt_s: shared-window address of the tile counters; entry e adds q to counter e.
+__device__ __forceinline__ void accumulate_masked(uint32_t cnt_s, const uint4 v, uint32_t m, uint32_t q) {
+    const uint32_t a0 = cnt_s + ((v.x & 0xFFFFu) << 2), a1 = cnt_s + ((v.x >> 14) & ~3u);
+    const uint32_t a2 = cnt_s + ((v.y & 0xFFFFu) << 2), a3 = cnt_s + ((v.y >> 14) & ~3u);
+    const uint32_t a4 = cnt_s + ((v.z & 0xFFFFu) << 2), a5 = cnt_s + ((v.z >> 14) & ~3u);
+    const uint32_t a6 = cnt_s + ((v.w & 0xFFFFu) << 2), a7 = cnt_s + ((v.w >> 14) & ~3u);
+    asm volatile(
+        "{\n\t.reg .pred p<8>;\n\t.reg .b32 t;\n\t"
+        "and.b32 t, %9, 1;   setp.ne.u32 p0, t, 0;\n\t"
+        "and.b32 t, %9, 2;   setp.ne.u32 p1, t, 0;\n\t"
+        "and.b32 t, %9, 4;   setp.ne.u32 p2, t, 0;\n\t"
+        "and.b32 t, %9, 8;   setp.ne.u32 p3, t, 0;\n\t"
+        "and.b32 t, %9, 16;  setp.ne.u32 p4, t, 0;\n\t"
+        "and.b32 t, %9, 32;  setp.ne.u32 p5, t, 0;\n\t"
+        "and.b32 t, %9, 64;  setp.ne.u32 p6, t, 0;\n\t"
+        "and.b32 t, %9, 128; setp.ne.u32 p7, t, 0;\n\t"
+        "@p0 red.shared.add.u32 [%0], %8;\n\t"
+        "@p1 red.shared.add.u32 [%1], %8;\n\t"
+        "@p2 red.shared.add.u32 [%2], %8;\n\t"
+        "@p3 red.shared.add.u32 [%3], %8;\n\t"
+        "@p4 red.shared.add.u32 [%4], %8;\n\t"
+        "@p5 red.shared.add.u32 [%5], %8;\n\t"
+        "@p6 red.shared.add.u32 [%6], %8;\n\t"
+        "@p7 red.shared.add.u32 [%7], %8;\n\t}"
+        :: "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7), "r"(q), "r"(m)
+        : "memory");
+}
+
 __device__ __forceinline__ void accumulate8(uint32_t *cnt, const uint4 v, uint64_t w, uint64_t st,
                                             uint64_t en, uint32_t q) {
     const uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
@@ -269,9 +343,13 @@ __device__ __forceinline__ void accumulate8(uint32_t *cnt, const uint4 v, uint64
 }
 
 // Deliver the spikes of step t with index p = c, c+C, ... into tile b's counters.
-// Returns this thread's share of the delivered-event count.
+// Every group of GS lanes walks its own segments with no block-wide barrier; each group
+// keeps U segments in flight (descriptor loads, then window loads, then the shared-memory
+// atomics) so that enough loads are outstanding per SM.  Returns this thread's share of
+// the delivered-event count.
 template <int GS>
 __device__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c, DeliverSmem sm) {
+    constexpr int U = 4;
     const uint32_t tid = threadIdx.x;
     const uint32_t par = (uint32_t)(t & 1);
     for (uint32_t r = tid; r < a.NR; r += kBlock) sm.pref[r] = a.sl_counts[par * a.NR + r];
@@ -283,41 +361,139 @@ __device__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, uint32_t b, uint3
     uint32_t delivered = 0;
     const uint32_t grp = tid / GS, lig = tid % GS;
     constexpr uint32_t ngrp = kBlock / GS;
-    for (uint32_t q0 = 0; q0 < my; q0 += kDescChunk) {
-        const uint32_t nq = min((uint32_t)kDescChunk, my - q0);
-        // ---- stage (segment start, length) of every spike of this chunk ----
-#pragma unroll 2
-        for (uint32_t q = tid; q < nq; q += kBlock) {
-            const uint32_t p = c + (q0 + q) * a.C;
-            const uint32_t r = region_of(sm.pref, a.NR, p);
-            const uint64_t slot = lbase + (uint64_t)r * a.RS + (p - sm.pref[r]);
-            const uint32_t s = a.sl_ids[slot];
-            const uint64_t rs = a.sl_rows[slot];
-            const uint32_t *bp = a.bnd + (uint64_t)s * (a.NT + 1u) + b;
-            const uint32_t b0 = bp[0], b1 = bp[1];
-            sm.dstart[q] = rs + b0;
-            sm.dlen[q] = (b1 - b0) | (s >= a.n_exc ? 0x80000000u : 0u);
-            delivered += b1 - b0;
+    for (uint32_t q0 = grp; q0 < my; q0 += ngrp * U) {
+        uint32_t s[U];
+        uint64_t rs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t q = q0 + u * ngrp;
+            s[u] = 0xFFFFFFFFu;
+            rs[u] = 0;
+            if (q < my) {
+                const uint32_t p = c + q * a.C;
+                const uint32_t r = region_of(sm.pref, a.NR, p);
+                const uint64_t slot = lbase + (uint64_t)r * a.RS + (p - sm.pref[r]);
+                s[u] = a.sl_ids[slot];
+                rs[u] = a.sl_rows[slot];
+            }
         }
-        __syncthreads();
-        // ---- walk the segments: GS lanes per segment, two segments in flight ----
-        for (uint32_t q = grp; q < nq; q += 2 * ngrp) {
-            const bool hasB = q + ngrp < nq;
-            const uint64_t stA = sm.dstart[q], stB = hasB ? sm.dstart[q + ngrp] : 0ull;
-            const uint32_t lA = sm.dlen[q], lB = hasB ? sm.dlen[q + ngrp] : 0u;
-            const uint64_t enA = stA + (lA & 0x7FFFFFFFu), enB = stB + (lB & 0x7FFFFFFFu);
-            const uint32_t qA = (lA >> 31) ? 65536u : 1u, qB = (lB >> 31) ? 65536u : 1u;
-            uint64_t wA = (stA & ~7ull) + 8u * lig, wB = (stB & ~7ull) + 8u * lig;
-            uint4 vA = make_uint4(0, 0, 0, 0), vB = make_uint4(0, 0, 0, 0);
-            if (wA < enA) vA = ld_stream_v4(a.ent + wA);
-            if (wB < enB) vB = ld_stream_v4(a.ent + wB);
-            if (wA < enA) accumulate8(sm.cnt, vA, wA, stA, enA, qA);
-            if (wB < enB) accumulate8(sm.cnt, vB, wB, stB, enB, qB);
-            for (wA += 8u * GS; wA < enA; wA += 8u * GS) accumulate8(sm.cnt, ld_stream_v4(a.ent + wA), wA, stA, enA, qA);
-            for (wB += 8u * GS; wB < enB; wB += 8u * GS) accumulate8(sm.cnt, ld_stream_v4(a.ent + wB), wB, stB, enB, qB);
+        uint64_t st[U], en[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            st[u] = en[u] = 0;
+            if (s[u] != 0xFFFFFFFFu) {
+                const uint32_t *bp = a.bnd + (uint64_t)s[u] * (a.NT + 1u) + b;
+                st[u] = rs[u] + bp[0];
+                en[u] = rs[u] + bp[1];
+            }
         }
-        __syncthreads();
+        uint4 v[U];
+        uint64_t w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            w[u] = (st[u] & ~7ull) + 8u * lig;
+            v[u] = w[u] < en[u] ? ld_stream_v4(a.ent + w[u]) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t qv = s[u] >= a.n_exc ? 65536u : 1u;
+            if (lig == 0) delivered += (uint32_t)(en[u] - st[u]);
+            if (w[u] < en[u]) accumulate8(sm.cnt, v[u], w[u], st[u], en[u], qv);
+            for (uint64_t x = w[u] + 8u * GS; x < en[u]; x += 8u * GS)
+                accumulate8(sm.cnt, ld_stream_v4(a.ent + x), x, st[u], en[u], qv);
+        }
     }
+    __syncthreads();
+    return delivered;
+}
+
+// Descriptor-driven delivery (G = 1), software-pipelined through shared memory.
+//  * The CTA's visits (spike x this tile, for spikes p with p % C == c) are split evenly
+//    across its warps (flat prefix over the spike-list regions), so no warp waits for a
+//    heavier one at the closing barrier.
+//  * A warp walks its visits in batches of GPW = 32/GS (one visit per GS-lane group).  For
+//    every batch each lane copies its 16-byte window of the segment (8 u16 offsets) into a
+//    per-warp shared-memory stage with cp.async (LDGSTS, L2 only); S stages are in flight,
+//    the descriptor of the next batch is prefetched one batch ahead.  Processing a batch
+//    (mask + shared-memory reductions) overlaps the loads of the following S-1 batches.
+template <int GS>
+__device__ uint32_t deliver_tile_desc(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+                                      uint32_t *cnt, uint32_t *pref, uint32_t *tmp, uint4 *wbuf) {
+    constexpr int S = 4;
+    constexpr uint32_t GPW = 32 / GS;
+    constexpr uint32_t NW = kBlock / 32;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t gw = lane / GS, lig = lane % GS;
+    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
+    // visits of this CTA: spikes p = c + C q; region counts -> prefix (in spike units)
+    for (uint32_t r = tid; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
+    __syncthreads();
+    block_exclusive_scan(pref, a.NR, tmp);
+    const uint32_t n_sp = pref[a.NR];
+    const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
+    const uint32_t v0 = (uint32_t)((uint64_t)my * warp / NW), v1 = (uint32_t)((uint64_t)my * (warp + 1) / NW);
+    const uint64_t dbase = ((uint64_t)par * a.NT + b) * a.NR;
+    uint4 *buf = wbuf + warp * (S * 32);
+    uint32_t delivered = 0;
+    uint32_t rc = 0;                                   // region cursor of this lane's group
+    auto dload = [&](uint32_t vb) -> uint64_t {        // descriptor of visit vb + gw (0 if none)
+        const uint32_t v = vb + gw;
+        if (v >= v1) return 0ull;
+        const uint32_t p = c + v * a.C;
+        while (pref[rc + 1] <= p) ++rc;
+        return a.desc[(dbase + rc) * a.RS + (p - pref[rc])];
+    };
+    {   // region of the first visit of this group (binary search once)
+        const uint32_t p = c + (v0 + gw) * a.C;
+        uint32_t lo = 0, hi = a.NR;
+        while (hi - lo > 1) { const uint32_t mid = (lo + hi) >> 1; if (pref[mid] <= p) lo = mid; else hi = mid; }
+        rc = lo;
+    }
+    uint32_t meta[S];                                   // tot | head << 24 | inh << 31
+    uint64_t al[S];
+    auto issue = [&](int s, uint64_t d) {
+        const uint64_t st = d & ((1ull << 40) - 1);
+        const uint32_t len = (uint32_t)(d >> 40) & ((1u << 23) - 1);
+        const uint32_t head = (uint32_t)st & 7u;
+        meta[s] = (head + len) | (head << 24) | ((uint32_t)(d >> 63) << 31);
+        al[s] = st & ~7ull;
+        if (lig == 0) delivered += len;
+        if (8u * lig < head + len && len) {
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf + s * 32 + lane);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(a.ent + al[s] + 8u * lig) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto process = [&](int s) {
+        const uint32_t tot = meta[s] & 0xFFFFFFu, head = (meta[s] >> 24) & 7u;
+        const uint32_t qv = (meta[s] >> 31) ? 65536u : 1u;
+        uint32_t off = 8u * lig;
+        if (off < tot && tot > head) {
+            const uint4 v = buf[s * 32 + lane];
+            accumulate_masked(cnt_s, v, window_mask((int)head - (int)off, (int)(tot - off)), qv);
+            for (off += 8u * GS; off < tot; off += 8u * GS)
+                accumulate_masked(cnt_s, ld_stream_v4(a.ent + al[s] + off),
+                                  window_mask((int)head - (int)off, (int)(tot - off)), qv);
+        }
+    };
+    uint32_t vb = v0;                                   // next batch to issue
+    uint64_t dn = dload(vb);
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) { const uint64_t d = dn; vb += GPW; dn = dload(vb); issue(s, d); }
+    for (uint32_t pb = v0; pb < v1; ) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            // issue batch (pb + (S-1) GPW) into stage (s + S - 1) % S, prefetch the next descriptor
+            { const uint64_t d = dn; vb += GPW; dn = dload(vb); issue((s + S - 1) % S, d); }
+            asm volatile("cp.async.wait_group %0;" :: "n"(S - 1) : "memory");
+            process(s);
+            pb += GPW;
+            if (pb >= v1) break;
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
     return delivered;
 }
 
@@ -451,9 +627,12 @@ __device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot,
 __device__ __forceinline__ DeliverSmem carve(const SimArgs &a, uint32_t *smem) {
     DeliverSmem sm;
     const uint32_t tw4 = (a.TW + 3u) & ~3u;
+    sm.wbuf = reinterpret_cast<uint4 *>(smem);          // kWbufWords words, 16-byte aligned
+    smem += kWbufWords;
     sm.cnt = smem;
     sm.dstart = reinterpret_cast<uint64_t *>(smem + tw4);
     sm.dlen = smem + tw4 + 2 * kDescChunk;
+    sm.stage = smem + tw4;
     sm.pref = sm.dlen + kDescChunk;
     sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
     return sm;
@@ -461,15 +640,15 @@ __device__ __forceinline__ DeliverSmem carve(const SimArgs &a, uint32_t *smem) {
 
 size_t tile_smem_bytes(uint32_t TW, uint32_t NR) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
-    return ((size_t)tw4 + 3 * kDescChunk + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
+    return ((size_t)kWbufWords + tw4 + 3 * kDescChunk + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
 }
 
 // Brunel+ tile kernels: counters [TW] u32, plastic sums [TW] i64, region prefix, scan tmp.
 size_t plastic_smem_bytes(uint32_t TW, uint32_t NR) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
-    return (size_t)tw4 * 4 + (size_t)tw4 * 8 + (((NR + 1 + 3) & ~3u) + 32) * 4 + 16;
+    return (size_t)tw4 * 4 + (size_t)tw4 * 8 + (((NR + 1 + 3) & ~3u) + 32 + kStageWords) * 4 + 16;
 }
-struct PlasticSmem { uint32_t *cnt; long long *pin; uint32_t *pref; uint32_t *tmp; };
+struct PlasticSmem { uint32_t *cnt; long long *pin; uint32_t *pref; uint32_t *tmp; uint32_t *stage; };
 __device__ __forceinline__ PlasticSmem carve_plastic(const SimArgs &a, uint32_t *smem) {
     PlasticSmem sm;
     const uint32_t tw4 = (a.TW + 3u) & ~3u;
@@ -477,16 +656,18 @@ __device__ __forceinline__ PlasticSmem carve_plastic(const SimArgs &a, uint32_t 
     sm.cnt = smem + 2 * tw4;
     sm.pref = sm.cnt + tw4;
     sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
+    sm.stage = sm.tmp + 32;
     return sm;
 }
 
 // ------------------------------------------------------------------ kernels
 template <int MODEL>
 __global__ void __launch_bounds__(kBlock) k_update(SimArgs a, uint32_t k) {
+    extern __shared__ __align__(16) uint32_t stage[];
     __shared__ uint32_t s_count;
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
-    update_tile<MODEL>(a, *a.t0 + k, blockIdx.x, nullptr, a.G == 1, &s_count);
+    update_tile<MODEL>(a, *a.t0 + k, blockIdx.x, nullptr, a.G == 1, &s_count, stage);
 }
 
 template <int GS>
@@ -496,7 +677,9 @@ __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
     const uint64_t t = *a.t0 + k;
     const uint32_t b = blockIdx.x / a.C, c = blockIdx.x % a.C;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
-    const uint32_t d = deliver_tile<GS>(a, t, b, c, sm);
+    uint32_t d;
+    if (a.desc) { __syncthreads(); d = deliver_tile_desc<GS>(a, t, b, c, sm.cnt, sm.pref, sm.tmp, sm.wbuf); }
+    else d = deliver_tile<GS>(a, t, b, c, sm);
     uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
     if (a.C == 1u) {
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u) {
@@ -556,7 +739,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         }
         store_delivered(a, b, d, sm.tmp);
         __syncthreads();
-        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count3);
+        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count3, sm.stage);
         return;
     }
     extern __shared__ __align__(16) uint32_t smem[];
@@ -566,15 +749,16 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
     const uint32_t b = blockIdx.x;
     if (threadIdx.x == 0) s_count = 0;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
-    const uint32_t d = deliver_tile<GS>(a, t, b, 0, sm);
+    __syncthreads();
+    const uint32_t d = deliver_tile_desc<GS>(a, t, b, 0, sm.cnt, sm.pref, sm.tmp, sm.wbuf);
     store_delivered(a, b, d, sm.tmp);
     if (a.delay == 1) {
-        update_tile<MODEL>(a, t + 1, b, sm.cnt, true, &s_count);
+        update_tile<MODEL>(a, t + 1, b, sm.cnt, true, &s_count, sm.stage);
     } else {
         uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)
             *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(sm.cnt + x);
-        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count);
+        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count, sm.stage);
     }
 }
 
@@ -651,12 +835,12 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
 __global__ void k_advance(uint64_t *t0, uint32_t steps) { *t0 += steps; }
 
 // ------------------------------------------------------------------ launchers
-static uint32_t group_lanes(double mean_seg) {
-    if (mean_seg <= 10) return 1;
-    if (mean_seg <= 22) return 2;
-    if (mean_seg <= 48) return 4;
-    if (mean_seg <= 100) return 8;
-    if (mean_seg <= 200) return 16;
+static uint32_t group_lanes(double mean_seg) {   // 8 entries (16 B) per lane
+    if (mean_seg <= 6) return 1;
+    if (mean_seg <= 12) return 2;
+    if (mean_seg <= 26) return 4;
+    if (mean_seg <= 56) return 8;
+    if (mean_seg <= 120) return 16;
     return 32;
 }
 
@@ -693,10 +877,10 @@ cudaError_t prepare_kernels(const SimArgs &a) {
 
 cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s) {
     switch (a.model) {
-    case 1: k_update<1><<<a.NT, kBlock, 0, s>>>(a, k); break;
-    case 2: k_update<2><<<a.NT, kBlock, 0, s>>>(a, k); break;
-    case 3: k_update<3><<<a.NT, kBlock, 0, s>>>(a, k); break;
-    case 4: k_update<4><<<a.NT, kBlock, 0, s>>>(a, k); break;
+    case 1: k_update<1><<<a.NT, kBlock, kStageWords * 4, s>>>(a, k); break;
+    case 2: k_update<2><<<a.NT, kBlock, kStageWords * 4, s>>>(a, k); break;
+    case 3: k_update<3><<<a.NT, kBlock, kStageWords * 4, s>>>(a, k); break;
+    case 4: k_update<4><<<a.NT, kBlock, kStageWords * 4, s>>>(a, k); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -13,6 +13,8 @@ enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFi
 
 constexpr int kBlock = 1024;          // threads per tile CTA (update / deliver / fused)
 constexpr int kDescChunk = 2048;      // segment descriptors staged in smem per pass
+constexpr int kStageWords = 6144;     // bnd rows staged per descriptor-transposition pass
+constexpr uint32_t kWbufWords = (kBlock / 32) * 4 * 32 * 4;   // cp.async window stages: warps x 4 stages x 32 lanes x 16 B
 constexpr uint32_t kMaxTileWidth = 49152;   // u32 counters per tile <= 192 KiB smem
 constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
 constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list region
@@ -89,6 +91,10 @@ struct SimArgs {
     uint32_t *sl_ids;        // 2 * NR * RS
     uint64_t *sl_rows;       // 2 * NR * RS row starts of the listed spikes
     uint32_t *sl_counts;     // 2 * NR
+    // G = 1: per-step segment descriptors written transposed by the updating CTA:
+    // desc[((par*NT + b)*NR + r)*RS + q] = start (bits 0-39) | len (40-62) | inh (63)
+    // of the q-th spike of region r restricted to tile b (coalesced reads in delivery)
+    uint64_t *desc;
     uint32_t *record;        // record_steps * G * W words
     uint32_t *sendbuf;       // W words (G > 1)
     uint32_t *gather;        // G * W words (G > 1)

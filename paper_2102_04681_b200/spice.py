@@ -221,6 +221,18 @@ class Network:
                                          offs.ctypes.data, C.byref(total)))
         return offs, tg[: total.value]
 
+    def weights(self, row_begin: int = 0, row_end: Optional[int] = None) -> np.ndarray:
+        """Plastic weights in the order of :meth:`connectivity` (static synapses read 0)."""
+        L = lib()
+        row_end = self.n if row_end is None else row_end
+        total = C.c_uint64(0)
+        st = L.spice_read_weights(self.h, row_begin, row_end, None, 0, C.byref(total))
+        if st not in (OK, ETRUNC):
+            _check(st)
+        w = np.zeros(max(1, total.value), dtype=np.float32)
+        _check(L.spice_read_weights(self.h, row_begin, row_end, w.ctypes.data, w.size, C.byref(total)))
+        return w[: total.value]
+
     def state(self, field: int) -> np.ndarray:
         dt = np.uint32 if field in (FIELD_REF, FIELD_ACC) else np.float32
         out = np.zeros(self.n_owned, dtype=dt)

@@ -1,0 +1,108 @@
+"""Brunel+ (STDP) on the GPU against the oracle's eager rule (reading
+R13): pair-STDP weights, traces, plastic fixed-point inputs and spike trains BIT-EXACT
+(every weight change is a single fp32 operation per synapse in a fixed order; plastic
+input is int64 fixed point, reading R10)."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2102_04681_b200 import build as B
+    B.build()
+    from paper_2102_04681_b200 import spice
+    return spice
+
+
+def _stronger_stdp(cfg, scale=20.0):
+    """Same network with A+/A- scaled up so that weights visibly move in a short run."""
+    import dataclasses
+    p = list(cfg.params)
+    p[12] *= scale
+    p[13] *= scale
+    return dataclasses.replace(cfg, params=tuple(p))
+
+
+CASES = {
+    "bplus3000": (W.brunel_plus(3000, 0.1, seed=5), {}, 300),
+    "bplus3000_strong_t64": (_stronger_stdp(W.brunel_plus(3000, 0.1, seed=6)), dict(tile_width=64), 300),
+    "bplus2001_ragged": (_stronger_stdp(W.brunel_plus(2001, 0.15, seed=7, delay=3)), dict(tile_width=96), 200),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_brunel_plus_free_run_bit_exact(S, name):
+    cfg, kw, T = CASES[name]
+    o = O.OracleNet(cfg)
+    rp, tg = o.csr()
+    with S.Network(cfg, record_steps=T, **kw) as net:
+        offs, g = net.connectivity()
+        assert np.array_equal(g, tg)
+        assert np.array_equal(net.weights(), o.weights())          # w0 on plastic, 0 elsewhere
+        net.step(T)
+        o.step(T)
+        want = o.spikes()
+        got = net.read_spikes(0, T)
+        bad = [t for t in range(T) if not np.array_equal(got[t], want[t])]
+        assert not bad, f"first mismatching step {bad[0]}"
+        w_gpu, w_orc = net.weights(), o.weights()
+        assert np.array_equal(w_gpu, w_orc), np.flatnonzero(w_gpu != w_orc)[:10]
+        assert np.any(w_orc[o.plastic_flags() == 1] != np.float32(cfg.params[15]))  # STDP acted
+        assert np.array_equal(net.state(S.FIELD_V), o.state(O.F_V))
+        assert np.array_equal(net.state(S.FIELD_YTR), o.state(O.F_YTR))
+        assert np.array_equal(net.state(S.FIELD_XTR), o.state(O.F_XTR))
+        for rel in range(cfg.delay + 1):
+            c1, p1 = net.input(rel)
+            c2, p2 = o.input(rel)
+            assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
+        assert net.stats()["delivered"] == int(o.delivered().sum())
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_brunel_plus_virtual_ranks(S, G):
+    cfg, _, T = CASES["bplus3000_strong_t64"]
+    T = 150
+    o = O.OracleNet(cfg)
+    o.step(T)
+    want = o.spikes()
+    Sw = 32
+    nets = [S.Network(cfg, rank=g, world_size=G, slice_width=Sw, external_exchange=True,
+                      record_steps=T) for g in range(G)]
+    try:
+        for _ in range(T):
+            for n in nets:
+                n.exchange_begin()
+            for d in nets:
+                for s in nets:
+                    d.exchange_put_from(s)
+            for n in nets:
+                n.exchange_end()
+        for n in nets:
+            assert all(np.array_equal(a, b) for a, b in zip(n.read_spikes(0, T), want))
+        # per-rank weights equal the oracle's weights of that rank's synapses
+        for g, n in enumerate(nets):
+            part = O.OracleNet(cfg, part=(g, G, Sw))
+            rp, tg = part.csr()
+            offs, gt = n.connectivity()
+            assert np.array_equal(gt, tg)
+        # weights: compare per synapse through (source, target) keys
+        full_rp, full_tg = o.csr()
+        wfull = o.weights()
+        key = {}
+        for s_ in range(cfg.n):
+            for e in range(int(full_rp[s_]), int(full_rp[s_ + 1])):
+                key[(s_, int(full_tg[e]))] = wfull[e]
+        for g, n in enumerate(nets):
+            offs, gt = n.connectivity()
+            wg = n.weights()
+            for s_ in range(0, cfg.n, 7):
+                for e in range(int(offs[s_]), int(offs[s_ + 1])):
+                    assert wg[e] == key[(s_, int(gt[e]))]
+    finally:
+        for n in nets:
+            n.free()
