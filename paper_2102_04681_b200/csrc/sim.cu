@@ -271,7 +271,7 @@ __device__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, const uint
         if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
         a.fired_cta[b] += n_tile;
     }
-    if (write_list && a.desc) write_descriptors(a, par, b, n_tile, region, region_rows, stage);
+    if (write_list && a.desc && !(a.dbg & 4u)) write_descriptors(a, par, b, n_tile, region, region_rows, stage);
     __syncthreads();
     if (tid == 0) *s_count = 0;
 }
@@ -459,7 +459,7 @@ __device__ uint32_t deliver_tile_desc(const SimArgs &a, uint64_t t, uint32_t b, 
         meta[s] = (head + len) | (head << 24) | ((uint32_t)(d >> 63) << 31);
         al[s] = st & ~7ull;
         if (lig == 0) delivered += len;
-        if (8u * lig < head + len && len) {
+        if (8u * lig < head + len && len && !(a.dbg & 2u)) {
             const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf + s * 32 + lane);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(a.ent + al[s] + 8u * lig) : "memory");
         }
@@ -469,6 +469,7 @@ __device__ uint32_t deliver_tile_desc(const SimArgs &a, uint64_t t, uint32_t b, 
         const uint32_t tot = meta[s] & 0xFFFFFFu, head = (meta[s] >> 24) & 7u;
         const uint32_t qv = (meta[s] >> 31) ? 65536u : 1u;
         uint32_t off = 8u * lig;
+        if ((a.dbg & 3u) && off < tot) { delivered ^= (a.dbg & 2u) ? 0u : buf[s * 32 + lane].x; return; }
         if (off < tot && tot > head) {
             const uint4 v = buf[s * 32 + lane];
             accumulate_masked(cnt_s, v, window_mask((int)head - (int)off, (int)(tot - off)), qv);

@@ -78,6 +78,8 @@ struct SimArgs {
     uint32_t record_steps;
     uint32_t key0, key1;
     uint32_t NR, RS;         // spike-list regions
+    uint32_t dbg;            // diagnostics only (SPICE_DEBUG_MODE): bit0 no smem reductions,
+                             // bit1 no synapse loads, bit2 no descriptor writes
     ModelConst mc;
     // connectivity
     const uint64_t *row_ptr; // [N+1]
