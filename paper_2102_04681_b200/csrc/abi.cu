@@ -131,6 +131,11 @@ struct spice_net {
     uint32_t *sl_ids = nullptr, *sl_counts = nullptr;
     uint64_t *sl_rows = nullptr;
     uint64_t *desc = nullptr;
+    // tile-pair exchange (G = 1)
+    uint16_t *xbuf = nullptr;
+    uint64_t *xoff = nullptr;
+    uint32_t *xcnt = nullptr;
+    uint64_t xtotal = 0;
     uint32_t *record = nullptr, *sendbuf = nullptr, *gather = nullptr;
     unsigned long long *fired_cta = nullptr, *delivered_cta = nullptr;
     uint64_t *t0 = nullptr;
@@ -516,8 +521,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if ((st = dalloc_t(n, &n->sl_ids, 2ull * n->NR * n->RS, "spike lists"))) return bail(st);
     if ((st = dalloc_t(n, &n->sl_rows, 2ull * n->NR * n->RS, "spike list rows"))) return bail(st);
     if ((st = dalloc_t(n, &n->sl_counts, 2ull * n->NR, "spike list counts"))) return bail(st);
-    if (n->G == 1 && n->model != SPICE_BRUNEL_PLUS &&
-        (st = dalloc_t(n, &n->desc, 2ull * n->NT * n->NR * n->RS, "segment descriptors"))) return bail(st);
+
     if ((st = dalloc_t(n, &n->record, (size_t)n->R * n->G * n->W, "spike record"))) return bail(st);
     if ((st = dalloc_t(n, &n->sendbuf, std::max<uint32_t>(n->W, 1), "send bitmap"))) return bail(st);
     if ((st = dalloc_t(n, &n->gather, (size_t)n->G * std::max<uint32_t>(n->W, 1), "gathered bitmaps"))) return bail(st);
@@ -593,6 +597,42 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         n->mc.ptab_len = (uint32_t)tab.size();
     }
     CU(n, cudaStreamSynchronize(s));
+    // ---- tile-pair exchange (G = 1): static chunk capacities from the connectivity ----
+    // experimental (opt-in, SPICE_XCHG=1): measured slower than descriptor transposition on
+    // synth 3e9 (producer segment copies dominate), see DESIGN.md "Delivery design log"
+    if (n->G == 1 && n->model != SPICE_BRUNEL_PLUS && n->C == 1 && !n->global_atomics && getenv("SPICE_XCHG") &&
+        xchg_kernel_smem_bytes(n->TW, n->NT) <= 227 * 1024) {
+        std::vector<uint64_t> rp(n->N + 1);
+        CU(n, cudaMemcpy(rp.data(), n->row_ptr, (n->N + 1) * 8ull, cudaMemcpyDeviceToHost));
+        uint64_t maxlen = 0;
+        for (uint32_t q = 0; q < n->N; ++q) maxlen = std::max<uint64_t>(maxlen, rp[q + 1] - rp[q]);
+        if (((maxlen + 7 + 7) / 8 * 8) * 2 <= kXRowsBytes) {
+            SimArgs ta{};
+            ta.N = n->N; ta.n_exc = n->n_exc; ta.TW = n->TW; ta.NT = n->NT; ta.bnd = n->bnd;
+            const uint64_t nc = (uint64_t)n->NT * n->NT * 2;
+            uint32_t *cap = nullptr;
+            if ((st = dalloc_t(n, &cap, nc, "exchange capacities"))) return bail(st);
+            CU(n, launch_xcap(ta, cap, s));
+            std::vector<uint32_t> hc(nc);
+            CU(n, cudaMemcpyAsync(hc.data(), cap, nc * 4, cudaMemcpyDeviceToHost, s));
+            CU(n, cudaStreamSynchronize(s));
+            dfree(n, cap);
+            n->device_bytes -= nc * 4;
+            std::vector<uint64_t> off(nc);
+            uint64_t tot = 0;
+            for (uint64_t q = 0; q < nc; ++q) { off[q] = tot; tot += (hc[q] + 7) / 8 * 8; }   // 16-byte aligned chunks
+            n->xtotal = tot + 8;
+            if ((st = dalloc_t(n, &n->xoff, nc, "exchange offsets"))) return bail(st);
+            if ((st = dalloc_t(n, &n->xcnt, 2 * nc, "exchange counts"))) return bail(st);
+            if ((st = dalloc_t(n, &n->xbuf, 2 * n->xtotal + 2 * kEntPad, "exchange chunks"))) return bail(st);
+            CU(n, cudaMemcpyAsync(n->xoff, off.data(), nc * 8, cudaMemcpyHostToDevice, s));
+            CU(n, cudaMemsetAsync(n->xcnt, 0, 2 * nc * 4, s));
+            CU(n, cudaStreamSynchronize(s));
+        }
+    }
+    // descriptor transposition path (G = 1 without the exchange)
+    if (n->G == 1 && n->model != SPICE_BRUNEL_PLUS && !n->xbuf &&
+        (st = dalloc_t(n, &n->desc, 2ull * n->NT * n->NR * n->RS, "segment descriptors"))) return bail(st);
     // ---- kernel arguments ----
     SimArgs &a = n->args;
     a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D;
@@ -606,7 +646,8 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.mc = n->mc;
     a.row_ptr = n->row_ptr; a.bnd = n->bnd; a.ent = n->ent;
     a.v = n->v; a.ge = n->ge; a.gi = n->gi; a.ref = n->ref; a.acc = n->acc; a.ring = n->ring;
-    a.sl_ids = n->sl_ids; a.sl_rows = n->sl_rows; a.sl_counts = n->sl_counts; a.desc = n->desc; a.record = n->record; a.sendbuf = n->sendbuf;
+    a.sl_ids = n->sl_ids; a.sl_rows = n->sl_rows; a.sl_counts = n->sl_counts; a.desc = n->desc;
+    a.xbuf = n->xbuf; a.xoff = n->xoff; a.xcnt = n->xcnt; a.xtotal = n->xtotal; a.xrows_bytes = kXRowsBytes; a.record = n->record; a.sendbuf = n->sendbuf;
     a.gather = n->gather; a.fired_cta = n->fired_cta; a.delivered_cta = n->delivered_cta;
     a.t0 = n->t0; a.force_bits = n->force_bits; a.force_ctl = n->force_ctl;
     a.w = n->w; a.pring = n->pring; a.xtr = n->xtr; a.ytr = n->ytr;

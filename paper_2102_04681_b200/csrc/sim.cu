@@ -39,7 +39,7 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
 }
 
 // Exclusive scan of arr[0..n) in shared memory (n <= kBlock * 8); arr[n] = total.
-__device__ void block_exclusive_scan(uint32_t *arr, uint32_t n, uint32_t *s_tmp) {
+__device__ __forceinline__ void block_exclusive_scan(uint32_t *arr, uint32_t n, uint32_t *s_tmp) {
     const uint32_t tid = threadIdx.x, per = (n + kBlock - 1) / kBlock;
     const uint32_t lo = min(n, tid * per), hi = min(n, lo + per);
     uint32_t sum = 0;
@@ -177,105 +177,6 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, uint64_t t, uint32
 
 // Update every neuron of tile b for step t.  Inputs come from `cnt` (shared memory, the
 // tile's counts) or, when cnt == nullptr, from input ring slot t mod D (read and cleared).
-// Descriptor transposition (G = 1): for the n spikes of region b (this tile's spikes), load
-// their bnd rows (coalesced, CH spikes at a time, staged in smem) and write, for every
-// destination tile bb, the CH descriptors desc[par][bb][b][q0 .. q0+CH) with one coalesced
-// store per tile.  Delivery CTAs then read their descriptors contiguously.
-__device__ void write_descriptors(const SimArgs &a, uint32_t par, uint32_t b, uint32_t n,
-                                  const uint32_t *region, const uint64_t *region_rows, uint32_t *stage) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t rowlen = a.NT + 1u;
-    const uint32_t CH = max(1u, min(32u, (uint32_t)kStageWords / rowlen));
-    for (uint32_t q0 = 0; q0 < n; q0 += CH) {
-        const uint32_t nq = min(CH, n - q0);
-        __syncthreads();
-        for (uint32_t ql = warp; ql < nq; ql += kBlock / 32) {            // one warp per spike row
-            const uint32_t *row = a.bnd + (uint64_t)region[q0 + ql] * rowlen;
-            for (uint32_t bb = lane; bb < rowlen; bb += 32) stage[ql * rowlen + bb] = row[bb];
-        }
-        __syncthreads();
-        // lane ql of warp w writes descriptor (tile bb, spike q0 + ql): coalesced per tile
-        const uint32_t ql = lane;
-        uint32_t s = 0;
-        uint64_t rs = 0;
-        if (ql < nq) { s = region[q0 + ql]; rs = region_rows[q0 + ql]; }
-        const uint64_t inh = s >= a.n_exc ? (1ull << 63) : 0ull;
-        for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
-            if (ql < nq) {
-                const uint32_t lo = stage[ql * rowlen + bb], hi = stage[ql * rowlen + bb + 1];
-                a.desc[(((uint64_t)par * a.NT + bb) * a.NR + b) * a.RS + q0 + ql] =
-                    (rs + lo) | ((uint64_t)(hi - lo) << 40) | inh;
-            }
-        }
-    }
-}
-
-template <int MODEL>
-__device__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, const uint32_t *cnt,
-                            bool write_list, uint32_t *s_count, uint32_t *stage) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31;
-    const uint32_t lo = b * a.TW;
-    const uint32_t span = lo < a.W * 32u ? min(a.TW, a.W * 32u - lo) : 0u;   // bitmap coverage
-    const uint32_t par = (uint32_t)(t & 1);
-    uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
-    uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + b) * a.RS;
-    uint32_t *bm = a.G == 1 ? a.record + (t % a.record_steps) * (uint64_t)a.W : a.sendbuf;
-    uint32_t *ring_slot = a.ring + (t % a.D) * a.ring_stride + lo;
-    for (uint32_t x0 = 0; x0 < span; x0 += 4u * kBlock) {      // uniform trip count per CTA
-        const uint32_t x4 = x0 + 4u * tid;
-        uint32_t nib = 0;
-        const bool act = x4 < span && lo + x4 < a.n_own;
-        if (act) {
-            uint32_t c[4];
-            long long pin[4] = {0, 0, 0, 0};
-            if (MODEL == 3) {
-                long long *ps = a.pring + (t % a.D) * a.ring_stride + lo + x4;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) { pin[e] = ps[e]; ps[e] = 0; }
-            }
-            if (cnt) {
-                c[0] = cnt[x4]; c[1] = cnt[x4 + 1]; c[2] = cnt[x4 + 2]; c[3] = cnt[x4 + 3];
-            } else {
-                const uint4 cv = *reinterpret_cast<const uint4 *>(ring_slot + x4);
-                *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
-                c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
-            }
-            nib = update4<MODEL>(a, t, lo + x4, c, pin);
-        }
-        // 8 lanes x 4 bits -> one 32-neuron bitmap word
-        uint32_t w = nib << (4u * (lane & 7u));
-        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 1);
-        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 2);
-        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 4);
-        if ((lane & 7u) == 0 && x4 < span) bm[(lo + x4) >> 5] = w;
-        // append spikes to this tile's list region (warp-aggregated smem counter)
-        const uint32_t nsp = __popc(nib);
-        const uint32_t incl = warp_incl_scan(nsp);
-        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        if (tot) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(s_count, tot);
-            base = __shfl_sync(0xFFFFFFFFu, base, 0);
-            if (write_list && nib) {
-                uint32_t pos = base + incl - nsp;
-                const uint32_t j0 = (uint32_t)local_to_global(lo + x4, a.rank, a.G, a.S);
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if ((nib >> e) & 1u) { region[pos] = j0 + e; region_rows[pos] = a.row_ptr[j0 + e]; ++pos; }
-            }
-        }
-    }
-    __syncthreads();
-    const uint32_t n_tile = *s_count;
-    if (tid == 0) {
-        if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
-        a.fired_cta[b] += n_tile;
-    }
-    if (write_list && a.desc && !(a.dbg & 4u)) write_descriptors(a, par, b, n_tile, region, region_rows, stage);
-    __syncthreads();
-    if (tid == 0) *s_count = 0;
-}
-
 // ------------------------------------------------------------------ delivery
 struct DeliverSmem {
     uint4 *wbuf;       // [32 warps * 4 stages * 32 lanes] cp.async window stages
@@ -347,8 +248,306 @@ __device__ __forceinline__ void accumulate8(uint32_t *cnt, const uint4 v, uint64
 // keeps U segments in flight (descriptor loads, then window loads, then the shared-memory
 // atomics) so that enough loads are outstanding per SM.  Returns this thread's share of
 // the delivered-event count.
+// ------------------------------------------------------------- tile-pair exchange (G = 1)
+// Delivery with every global access contiguous.  Producer (CTA g, right after it updated
+// source tile g): the rows of its spiking neurons are loaded whole into shared memory with
+// TMA bulk copies (one cp.async.bulk per row, completion on an mbarrier); for every target
+// tile bt the segments of those rows (the pivot split of PAPER.md:273-275) are written
+// back-to-back into chunk (bt, g, receptor).  Consumer (CTA bt, next launch): its chunks
+// are read with 16-byte coalesced loads and accumulated with shared-memory atomics.
+// Chunk capacities are the exact static synapse counts, so they never overflow.
+struct XSmem {
+    uint16_t *rows;      // [kXRowsBytes / 2] staged rows (16-byte aligned)
+    uint32_t *bstage;    // [32 * (NT+1)] segment bounds of the batch's rows
+    uint32_t *off;       // [2 * NT] running chunk offsets
+    uint32_t *binfo;     // [32 * 4]: source, row start lo, row start hi, staged offset (entries)
+    uint32_t *misc;      // [4]: batch size
+    unsigned long long *mbar;
+};
+
+__host__ __device__ inline size_t xchg_smem_bytes(uint32_t NT) {
+    return (size_t)kXRowsBytes + (size_t)32 * (NT + 1) * 4 + (size_t)2 * NT * 4 + 32 * 16 + 16 + 16;
+}
+
+__device__ __forceinline__ XSmem carve_x(const SimArgs &a, uint32_t *smem) {
+    XSmem x;
+    x.rows = reinterpret_cast<uint16_t *>(smem);
+    uint32_t *p = smem + kXRowsBytes / 4;
+    x.bstage = p; p += 32 * (a.NT + 1);
+    x.off = p; p += 2 * a.NT;
+    x.binfo = p; p += 32 * 4;
+    x.misc = p; p += 4;
+    p = reinterpret_cast<uint32_t *>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
+    x.mbar = reinterpret_cast<unsigned long long *>(p);
+    return x;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long *m) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(m)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long *m, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *m, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(smem_u32(m)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, unsigned long long *m) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
+}
+
+// Producer: spikes ids[0..n) (global IDs, row starts rows[]) of source tile g, parity pw.
+__device__ __forceinline__ void exchange_produce(const SimArgs &a, uint32_t pw, uint32_t g, const uint32_t *ids,
+                                 const uint64_t *rows, uint32_t n, XSmem x, uint32_t &phase) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t NT = a.NT, rl = NT + 1u;
+    for (uint32_t i = tid; i < 2 * NT; i += kBlock) x.off[i] = 0u;
+    if (tid == 0) mbar_init(x.mbar);
+    uint16_t *xb = a.xbuf + (uint64_t)pw * a.xtotal;
+    for (uint32_t q0 = 0; q0 < n; ) {
+        __syncthreads();                                  // previous batch fully consumed
+        if (warp == 0) {                                  // form the batch: rows that fit the stage
+            const uint32_t q = q0 + lane;
+            uint32_t s = 0, bytes = 0;
+            uint64_t rs = 0, al = 0;
+            if (q < n) {
+                s = ids[q];
+                rs = rows[q];
+                const uint32_t len = a.bnd[(uint64_t)s * rl + NT];
+                al = rs & ~7ull;
+                bytes = (uint32_t)(((rs + len + 7) & ~7ull) - al) * 2u;
+            }
+            const uint32_t incl = warp_incl_scan(bytes);
+            const bool fits = q < n && (incl <= a.xrows_bytes || lane == 0);
+            const uint32_t nb = __popc(__ballot_sync(0xFFFFFFFFu, fits));
+            if (fits) {
+                x.binfo[lane * 4 + 0] = s;
+                x.binfo[lane * 4 + 1] = (uint32_t)rs;
+                x.binfo[lane * 4 + 2] = (uint32_t)(rs >> 32);
+                x.binfo[lane * 4 + 3] = (incl - bytes) / 2u + (uint32_t)(rs - al);   // staged row start (entries)
+            }
+            const uint32_t tot_bytes = __shfl_sync(0xFFFFFFFFu, incl, nb - 1);
+            if (lane == 0) {
+                x.misc[0] = nb;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive_tx(x.mbar, tot_bytes);
+            }
+            __syncwarp();
+            if (fits && bytes)
+                tma_load_1d(x.rows + (incl - bytes) / 2u, a.ent + al, bytes, x.mbar);
+        }
+        __syncthreads();
+        const uint32_t nb = x.misc[0];
+        // segment bounds of the batch rows (coalesced, one warp per row)
+        for (uint32_t q = warp; q < nb; q += kBlock / 32) {
+            const uint32_t *src = a.bnd + (uint64_t)x.binfo[q * 4] * rl;
+            for (uint32_t bt = lane; bt < rl; bt += 32) x.bstage[q * rl + bt] = src[bt];
+        }
+        __syncthreads();
+        mbar_wait(x.mbar, phase);
+        phase ^= 1u;
+        // one warp per target tile: positions of the nb segments, then copy them back-to-back
+        for (uint32_t bt = warp; bt < NT; bt += kBlock / 32) {
+            uint32_t len = 0, rcp = 0, srcoff = 0;
+            if (lane < nb) {
+                const uint32_t lo = x.bstage[lane * rl + bt];
+                len = x.bstage[lane * rl + bt + 1] - lo;
+                rcp = x.binfo[lane * 4] >= a.n_exc ? 1u : 0u;
+                srcoff = x.binfo[lane * 4 + 3] + lo;
+            }
+            const uint32_t l0 = rcp ? 0u : len, l1 = rcp ? len : 0u;
+            const uint32_t i0 = warp_incl_scan(l0), i1 = warp_incl_scan(l1);
+            const uint32_t pos = rcp ? x.off[bt * 2 + 1] + i1 - l1 : x.off[bt * 2] + i0 - l0;
+            const uint64_t ch0 = a.xoff[((uint64_t)bt * NT + g) * 2];
+            const uint64_t ch1 = a.xoff[((uint64_t)bt * NT + g) * 2 + 1];
+            for (uint32_t q = 0; q < nb; ++q) {
+                const uint32_t lq = __shfl_sync(0xFFFFFFFFu, len, q);
+                const uint32_t pq = __shfl_sync(0xFFFFFFFFu, pos, q);
+                const uint32_t sq = __shfl_sync(0xFFFFFFFFu, srcoff, q);
+                const uint32_t rq = __shfl_sync(0xFFFFFFFFu, rcp, q);
+                uint16_t *dst = xb + (rq ? ch1 : ch0) + pq;
+                for (uint32_t e = lane; e < lq; e += 32) dst[e] = x.rows[sq + e];
+            }
+            if (lane == 31) { x.off[bt * 2] += i0; x.off[bt * 2 + 1] += i1; }
+        }
+        q0 += nb;
+    }
+    __syncthreads();
+    uint32_t *xc = a.xcnt + (uint64_t)pw * NT * NT * 2;
+    for (uint32_t i = tid; i < 2 * NT; i += kBlock) {
+        const uint32_t bt = i >> 1, r = i & 1;
+        xc[((uint64_t)bt * NT + g) * 2 + r] = x.off[i];
+    }
+}
+
+// Consumer: accumulate every chunk (bt, g, r) of parity par into the tile counters.
+__device__ __forceinline__ uint32_t exchange_consume(const SimArgs &a, uint32_t par, uint32_t bt, uint32_t *cnt) {
+    constexpr int U = 4;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t NT = a.NT;
+    const uint32_t cnt_s = smem_u32(cnt);
+    const uint16_t *xb = a.xbuf + (uint64_t)par * a.xtotal;
+    const uint32_t *xc = a.xcnt + (uint64_t)par * NT * NT * 2;
+    uint32_t delivered = 0;
+    for (uint32_t k = warp; k < 2 * NT; k += kBlock / 32) {          // k = r * NT + g
+        const uint32_t r = k / NT, g = k - r * NT;
+        const uint64_t ci = ((uint64_t)bt * NT + g) * 2 + r;
+        const uint32_t n = xc[ci];
+        if (!n) continue;
+        const uint16_t *base = xb + a.xoff[ci];
+        const uint32_t q = r ? 65536u : 1u;
+        if (lane == 0) delivered += n;
+        for (uint32_t i0 = 0; i0 < n; i0 += 256u * U) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + 256u * u + 8u * lane;
+                v[u] = i < n ? ld_stream_v4(base + i) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + 256u * u + 8u * lane;
+                if (i < n) accumulate_masked(cnt_s, v[u], window_mask(0, (int)(n - i)), q);
+            }
+        }
+    }
+    __syncthreads();
+    return delivered;
+}
+
+// Capacities: cap[(bt*NT + g)*2 + r] = synapses from source tile g (receptor r) into tile bt.
+__global__ void __launch_bounds__(kBlock) k_xcap(SimArgs a, uint32_t *cap) {
+    extern __shared__ uint32_t e[];
+    const uint32_t g = blockIdx.x, NT = a.NT, rl = NT + 1u;
+    for (uint32_t i = threadIdx.x; i < 2 * NT; i += kBlock) e[i] = 0u;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t s0 = g * a.TW, s1 = min(a.N, s0 + a.TW);
+    for (uint32_t s = s0 + warp; s < s1; s += kBlock / 32) {
+        const uint32_t r = s >= a.n_exc ? 1u : 0u;
+        const uint32_t *row = a.bnd + (uint64_t)s * rl;
+        for (uint32_t bt = lane; bt < NT; bt += 32) {
+            const uint32_t len = row[bt + 1] - row[bt];
+            if (len) atomicAdd(&e[bt * 2 + r], len);
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 2 * NT; i += kBlock) cap[((uint64_t)(i >> 1) * NT + g) * 2 + (i & 1)] = e[i];
+}
+
+// Descriptor transposition (G = 1): for the n spikes of region b (this tile's spikes), load
+// their bnd rows (coalesced, CH spikes at a time, staged in smem) and write, for every
+// destination tile bb, the CH descriptors desc[par][bb][b][q0 .. q0+CH) with one coalesced
+// store per tile.  Delivery CTAs then read their descriptors contiguously.
+__device__ __forceinline__ void write_descriptors(const SimArgs &a, uint32_t par, uint32_t b, uint32_t n,
+                                  const uint32_t *region, const uint64_t *region_rows, uint32_t *stage) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t rowlen = a.NT + 1u;
+    const uint32_t CH = max(1u, min(32u, (uint32_t)kStageWords / rowlen));
+    for (uint32_t q0 = 0; q0 < n; q0 += CH) {
+        const uint32_t nq = min(CH, n - q0);
+        __syncthreads();
+        for (uint32_t ql = warp; ql < nq; ql += kBlock / 32) {            // one warp per spike row
+            const uint32_t *row = a.bnd + (uint64_t)region[q0 + ql] * rowlen;
+            for (uint32_t bb = lane; bb < rowlen; bb += 32) stage[ql * rowlen + bb] = row[bb];
+        }
+        __syncthreads();
+        // lane ql of warp w writes descriptor (tile bb, spike q0 + ql): coalesced per tile
+        const uint32_t ql = lane;
+        uint32_t s = 0;
+        uint64_t rs = 0;
+        if (ql < nq) { s = region[q0 + ql]; rs = region_rows[q0 + ql]; }
+        const uint64_t inh = s >= a.n_exc ? (1ull << 63) : 0ull;
+        for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
+            if (ql < nq) {
+                const uint32_t lo = stage[ql * rowlen + bb], hi = stage[ql * rowlen + bb + 1];
+                a.desc[(((uint64_t)par * a.NT + bb) * a.NR + b) * a.RS + q0 + ql] =
+                    (rs + lo) | ((uint64_t)(hi - lo) << 40) | inh;
+            }
+        }
+    }
+}
+
+template <int MODEL>
+__device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, const uint32_t *cnt,
+                            bool write_list, uint32_t *s_count, uint32_t *stage, uint32_t *xsm = nullptr) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    const uint32_t lo = b * a.TW;
+    const uint32_t span = lo < a.W * 32u ? min(a.TW, a.W * 32u - lo) : 0u;   // bitmap coverage
+    const uint32_t par = (uint32_t)(t & 1);
+    uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
+    uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + b) * a.RS;
+    uint32_t *bm = a.G == 1 ? a.record + (t % a.record_steps) * (uint64_t)a.W : a.sendbuf;
+    uint32_t *ring_slot = a.ring + (t % a.D) * a.ring_stride + lo;
+    for (uint32_t x0 = 0; x0 < span; x0 += 4u * kBlock) {      // uniform trip count per CTA
+        const uint32_t x4 = x0 + 4u * tid;
+        uint32_t nib = 0;
+        const bool act = x4 < span && lo + x4 < a.n_own;
+        if (act) {
+            uint32_t c[4];
+            long long pin[4] = {0, 0, 0, 0};
+            if (MODEL == 3) {
+                long long *ps = a.pring + (t % a.D) * a.ring_stride + lo + x4;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) { pin[e] = ps[e]; ps[e] = 0; }
+            }
+            if (cnt) {
+                c[0] = cnt[x4]; c[1] = cnt[x4 + 1]; c[2] = cnt[x4 + 2]; c[3] = cnt[x4 + 3];
+            } else {
+                const uint4 cv = *reinterpret_cast<const uint4 *>(ring_slot + x4);
+                *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
+                c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
+            }
+            nib = update4<MODEL>(a, t, lo + x4, c, pin);
+        }
+        // 8 lanes x 4 bits -> one 32-neuron bitmap word
+        uint32_t w = nib << (4u * (lane & 7u));
+        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 1);
+        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 2);
+        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 4);
+        if ((lane & 7u) == 0 && x4 < span) bm[(lo + x4) >> 5] = w;
+        // append spikes to this tile's list region (warp-aggregated smem counter)
+        const uint32_t nsp = __popc(nib);
+        const uint32_t incl = warp_incl_scan(nsp);
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        if (tot) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(s_count, tot);
+            base = __shfl_sync(0xFFFFFFFFu, base, 0);
+            if (write_list && nib) {
+                uint32_t pos = base + incl - nsp;
+                const uint32_t j0 = (uint32_t)local_to_global(lo + x4, a.rank, a.G, a.S);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if ((nib >> e) & 1u) { region[pos] = j0 + e; region_rows[pos] = a.row_ptr[j0 + e]; ++pos; }
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t n_tile = *s_count;
+    if (tid == 0) {
+        if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
+        a.fired_cta[b] += n_tile;
+    }
+    if (write_list && a.desc && !(a.dbg & 4u)) write_descriptors(a, par, b, n_tile, region, region_rows, stage);
+    if constexpr (MODEL != 3) {
+        if (write_list && a.xbuf) {
+            uint32_t phase = 0;
+            exchange_produce(a, par, b, region, region_rows, n_tile, carve_x(a, xsm), phase);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) *s_count = 0;
+}
+
 template <int GS>
-__device__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c, DeliverSmem sm) {
+__device__ __forceinline__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c, DeliverSmem sm) {
     constexpr int U = 4;
     const uint32_t tid = threadIdx.x;
     const uint32_t par = (uint32_t)(t & 1);
@@ -417,7 +616,7 @@ __device__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, uint32_t b, uint3
 //    the descriptor of the next batch is prefetched one batch ahead.  Processing a batch
 //    (mask + shared-memory reductions) overlaps the loads of the following S-1 batches.
 template <int GS>
-__device__ uint32_t deliver_tile_desc(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+__device__ __forceinline__ uint32_t deliver_tile_desc(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
                                       uint32_t *cnt, uint32_t *pref, uint32_t *tmp, uint4 *wbuf) {
     constexpr int S = 4;
     constexpr uint32_t GPW = 32 / GS;
@@ -520,7 +719,7 @@ __device__ __forceinline__ bool plastic_edge(const SimArgs &a, uint32_t s, uint3
     return false;
 }
 
-__device__ void potentiate_tile(const SimArgs &a, uint64_t t, uint32_t b) {
+__device__ __forceinline__ void potentiate_tile(const SimArgs &a, uint64_t t, uint32_t b) {
     const uint32_t *bm = step_bitmap(a, t);
     const float *x = a.xtr + (t & 1) * (uint64_t)a.N;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -539,7 +738,7 @@ __device__ void potentiate_tile(const SimArgs &a, uint64_t t, uint32_t b) {
     }
 }
 
-__device__ void stdp_traces(const SimArgs &a, uint64_t t, uint32_t b) {
+__device__ __forceinline__ void stdp_traces(const SimArgs &a, uint64_t t, uint32_t b) {
     const uint32_t *bm = step_bitmap(a, t);
     const uint32_t lo = b * a.TW, hi = min(lo + a.TW, a.n_own);
     for (uint32_t i = lo + threadIdx.x; i < hi; i += kBlock) {
@@ -584,7 +783,7 @@ __device__ __forceinline__ void walk_plastic(const SimArgs &a, uint32_t b, uint3
 }
 
 template <int GS>
-__device__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b, uint32_t *cnt,
+__device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b, uint32_t *cnt,
                                          long long *pin, uint32_t *pref, uint32_t *tmp) {
     const uint32_t tid = threadIdx.x;
     const uint32_t par = (uint32_t)(t & 1);
@@ -643,6 +842,11 @@ size_t tile_smem_bytes(uint32_t TW, uint32_t NR) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
     return ((size_t)kWbufWords + tw4 + 3 * kDescChunk + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
 }
+size_t xchg_kernel_smem_bytes(uint32_t TW, uint32_t NT) {
+    const size_t c = ((size_t)((TW + 3u) & ~3u)) * 4;
+    const size_t x = xchg_smem_bytes(NT);
+    return c > x ? c : x;
+}
 
 // Brunel+ tile kernels: counters [TW] u32, plastic sums [TW] i64, region prefix, scan tmp.
 size_t plastic_smem_bytes(uint32_t TW, uint32_t NR) {
@@ -668,12 +872,28 @@ __global__ void __launch_bounds__(kBlock) k_update(SimArgs a, uint32_t k) {
     __shared__ uint32_t s_count;
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
-    update_tile<MODEL>(a, *a.t0 + k, blockIdx.x, nullptr, a.G == 1, &s_count, stage);
+    update_tile<MODEL>(a, *a.t0 + k, blockIdx.x, nullptr, a.G == 1, &s_count, stage, stage);
 }
 
 template <int GS>
 __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
     extern __shared__ __align__(16) uint32_t smem[];
+    if (a.xbuf) {                                        // tile-pair exchange (G = 1, C = 1)
+        __shared__ uint32_t s_tmp[32];
+        const uint64_t t = *a.t0 + k;
+        const uint32_t b = blockIdx.x;
+        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) smem[x] = 0u;
+        __syncthreads();
+        const uint32_t d = exchange_consume(a, (uint32_t)(t & 1), b, smem);
+        uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
+        for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u) {
+            uint4 o = *reinterpret_cast<uint4 *>(dst + x);
+            o.x += smem[x]; o.y += smem[x + 1]; o.z += smem[x + 2]; o.w += smem[x + 3];
+            *reinterpret_cast<uint4 *>(dst + x) = o;
+        }
+        store_delivered(a, b, d, s_tmp);
+        return;
+    }
     DeliverSmem sm = carve(a, smem);
     const uint64_t t = *a.t0 + k;
     const uint32_t b = blockIdx.x / a.C, c = blockIdx.x % a.C;
@@ -724,7 +944,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver_plastic(SimArgs a, uint32_t 
 
 template <int MODEL, int GS>
 __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
-    if (MODEL == 3) {                                       // Brunel+ (delay >= 1 via the rings)
+    if constexpr (MODEL == 3) {                             // Brunel+ (delay >= 1 via the rings)
         extern __shared__ __align__(16) uint32_t smem[];
         PlasticSmem sm = carve_plastic(a, smem);
         __shared__ uint32_t s_count3;
@@ -741,14 +961,31 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         store_delivered(a, b, d, sm.tmp);
         __syncthreads();
         update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count3, sm.stage);
-        return;
-    }
+    } else {
     extern __shared__ __align__(16) uint32_t smem[];
     DeliverSmem sm = carve(a, smem);
     __shared__ uint32_t s_count;
     const uint64_t t = *a.t0 + k;
     const uint32_t b = blockIdx.x;
     if (threadIdx.x == 0) s_count = 0;
+    if (a.xbuf) {                                        // tile-pair exchange
+        __shared__ uint32_t s_tmp[32];
+        uint32_t *cnt = smem;
+        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) cnt[x] = 0u;
+        __syncthreads();
+        const uint32_t d = exchange_consume(a, (uint32_t)(t & 1), b, cnt);
+        store_delivered(a, b, d, s_tmp);
+        if (a.delay == 1) {
+            update_tile<MODEL>(a, t + 1, b, cnt, true, &s_count, nullptr, smem);
+        } else {
+            uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
+            for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)
+                *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
+            __syncthreads();
+            update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count, nullptr, smem);
+        }
+        return;
+    }
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
     __syncthreads();
     const uint32_t d = deliver_tile_desc<GS>(a, t, b, 0, sm.cnt, sm.pref, sm.tmp, sm.wbuf);
@@ -760,6 +997,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)
             *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(sm.cnt + x);
         update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count, sm.stage);
+    }
     }
 }
 
@@ -853,7 +1091,15 @@ static cudaError_t allow_smem(K kern, size_t bytes) {
 }
 
 cudaError_t prepare_kernels(const SimArgs &a) {
-    const size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    if (a.xbuf) {
+        const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT);
+        if (xb > bytes) bytes = xb;
+        cudaError_t e0 = cudaSuccess;
+        if (!e0) e0 = allow_smem(k_update<1>, xb); if (!e0) e0 = allow_smem(k_update<2>, xb);
+        if (!e0) e0 = allow_smem(k_update<4>, xb);
+        if (e0) return e0;
+    }
     cudaError_t e = cudaSuccess;
 #define ALLOW(kern) if (!e) e = allow_smem(kern, bytes)
     ALLOW(k_deliver<1>); ALLOW(k_deliver<2>); ALLOW(k_deliver<4>); ALLOW(k_deliver<8>);
@@ -877,11 +1123,12 @@ cudaError_t prepare_kernels(const SimArgs &a) {
 }
 
 cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s) {
+    const size_t ub = a.xbuf ? xchg_kernel_smem_bytes(a.TW, a.NT) : (size_t)kStageWords * 4;
     switch (a.model) {
-    case 1: k_update<1><<<a.NT, kBlock, kStageWords * 4, s>>>(a, k); break;
-    case 2: k_update<2><<<a.NT, kBlock, kStageWords * 4, s>>>(a, k); break;
+    case 1: k_update<1><<<a.NT, kBlock, ub, s>>>(a, k); break;
+    case 2: k_update<2><<<a.NT, kBlock, ub, s>>>(a, k); break;
     case 3: k_update<3><<<a.NT, kBlock, kStageWords * 4, s>>>(a, k); break;
-    case 4: k_update<4><<<a.NT, kBlock, kStageWords * 4, s>>>(a, k); break;
+    case 4: k_update<4><<<a.NT, kBlock, ub, s>>>(a, k); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -905,7 +1152,8 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
         }
         return cudaGetLastError();
     }
-    const size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    if (a.xbuf) { const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT); if (xb > bytes) bytes = xb; }
     const uint32_t grid = a.NT * a.C;
     switch (a.GS) {
     case 1: k_deliver<1><<<grid, kBlock, bytes, s>>>(a, k); break;
@@ -931,7 +1179,8 @@ static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) 
 }
 
 cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
-    const size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    if (a.xbuf) { const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT); if (xb > bytes) bytes = xb; }
     switch (a.model) {
     case 1: fused_m<1>(a, k, bytes, s); break;
     case 2: fused_m<2>(a, k, bytes, s); break;
@@ -944,6 +1193,11 @@ cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
 
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s) {
     k_b2l<<<a.NR, kBlock, 0, s>>>(a, k);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xcap(const SimArgs &a, uint32_t *cap, cudaStream_t s) {
+    k_xcap<<<a.NT, kBlock, 2 * a.NT * 4, s>>>(a, cap);
     return cudaGetLastError();
 }
 

@@ -14,6 +14,7 @@ enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFi
 constexpr int kBlock = 1024;          // threads per tile CTA (update / deliver / fused)
 constexpr int kDescChunk = 2048;      // segment descriptors staged in smem per pass
 constexpr int kStageWords = 6144;     // bnd rows staged per descriptor-transposition pass
+constexpr uint32_t kXRowsBytes = 128 * 1024;   // exchange producer: staged rows per batch
 constexpr uint32_t kWbufWords = (kBlock / 32) * 4 * 32 * 4;   // cp.async window stages: warps x 4 stages x 32 lanes x 16 B
 constexpr uint32_t kMaxTileWidth = 49152;   // u32 counters per tile <= 192 KiB smem
 constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
@@ -97,6 +98,15 @@ struct SimArgs {
     // desc[((par*NT + b)*NR + r)*RS + q] = start (bits 0-39) | len (40-62) | inh (63)
     // of the q-th spike of region r restricted to tile b (coalesced reads in delivery)
     uint64_t *desc;
+    // G = 1 tile-pair exchange (SimArgs::xbuf != nullptr): chunk (bt, g, r) of parity p holds
+    // the concatenated segments, for target tile bt, of the step's spikes of source tile g
+    // with receptor r; xoff[(bt*NT + g)*2 + r] is its start (static capacity from the
+    // connectivity), xcnt[p][...] the entries written for the step.
+    uint16_t *xbuf;          // 2 * xtotal
+    const uint64_t *xoff;    // NT * NT * 2
+    uint32_t *xcnt;          // 2 * NT * NT * 2
+    uint64_t xtotal;
+    uint32_t xrows_bytes;    // TMA row-staging capacity in shared memory
     uint32_t *record;        // record_steps * G * W words
     uint32_t *sendbuf;       // W words (G > 1)
     uint32_t *gather;        // G * W words (G > 1)

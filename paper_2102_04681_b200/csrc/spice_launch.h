@@ -10,6 +10,8 @@ namespace spice {
 // ---- step kernels (sim.cu) ----
 size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions);
 size_t plastic_smem_bytes(uint32_t tile_width, uint32_t n_regions);
+size_t xchg_kernel_smem_bytes(uint32_t tile_width, uint32_t n_tiles);
+cudaError_t launch_xcap(const SimArgs &a, uint32_t *cap, cudaStream_t s);
 uint32_t pick_group_lanes(double mean_segment);
 cudaError_t prepare_kernels(const SimArgs &a);
 cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s);
