@@ -641,6 +641,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.GS = pick_group_lanes(n->mean_seg);
     if (const char *gs = getenv("SPICE_GROUP_LANES")) a.GS = (uint32_t)atoi(gs);
     if (const char *dm = getenv("SPICE_DEBUG_MODE")) a.dbg = (uint32_t)atoi(dm);   // diagnostics only
+    a.pf_rows = getenv("SPICE_PREFETCH_ROWS") ? (uint32_t)atoi(getenv("SPICE_PREFETCH_ROWS")) : 0u;   // measured: no gain
     a.key0 = (uint32_t)n->seed; a.key1 = (uint32_t)(n->seed >> 32);
     a.NR = n->NR; a.RS = n->RS;
     a.mc = n->mc;

@@ -449,7 +449,7 @@ __device__ __forceinline__ void write_descriptors(const SimArgs &a, uint32_t par
                                   const uint32_t *region, const uint64_t *region_rows, uint32_t *stage) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t rowlen = a.NT + 1u;
-    const uint32_t CH = max(1u, min(32u, (uint32_t)kStageWords / rowlen));
+    const uint32_t CH = max(1u, min(32u, (uint32_t)kStageWords / rowlen));   // one lane per spike
     for (uint32_t q0 = 0; q0 < n; q0 += CH) {
         const uint32_t nq = min(CH, n - q0);
         __syncthreads();
@@ -525,7 +525,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 const uint32_t j0 = (uint32_t)local_to_global(lo + x4, a.rank, a.G, a.S);
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    if ((nib >> e) & 1u) { region[pos] = j0 + e; region_rows[pos] = a.row_ptr[j0 + e]; ++pos; }
+                    if ((nib >> e) & 1u) region[pos++] = j0 + e;
             }
         }
     }
@@ -534,6 +534,23 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     if (tid == 0) {
         if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
         a.fired_cta[b] += n_tile;
+    }
+    if (write_list) {                                     // row starts of the spikes, all at once
+        for (uint32_t q = tid; q < n_tile; q += kBlock) region_rows[q] = a.row_ptr[region[q]];
+        __syncthreads();
+    }
+    if (write_list && (a.dbg & 8u) == 0 && a.pf_rows) {
+        // TMA L2 prefetch of every spiking row (contiguous, ~rowlen * 2 bytes): the next
+        // launch's delivery reads these rows as scattered 16-byte windows from ~all CTAs;
+        // pulling each row into L2 with one bulk request turns those into L2 hits.
+        for (uint32_t q = tid; q < n_tile; q += kBlock) {
+            const uint32_t s = region[q];
+            const uint64_t rs = region_rows[q];
+            const uint64_t re = a.row_ptr[s + 1];
+            const uint64_t lo = rs & ~7ull, hi = (re + 7) & ~7ull;
+            if (hi > lo)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a.ent + lo), "r"((uint32_t)(hi - lo) * 2u) : "memory");
+        }
     }
     if (write_list && a.desc && !(a.dbg & 4u)) write_descriptors(a, par, b, n_tile, region, region_rows, stage);
     if constexpr (MODEL != 3) {
@@ -618,7 +635,7 @@ __device__ __forceinline__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, u
 template <int GS>
 __device__ __forceinline__ uint32_t deliver_tile_desc(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
                                       uint32_t *cnt, uint32_t *pref, uint32_t *tmp, uint4 *wbuf) {
-    constexpr int S = 4;
+    constexpr int S = kStages;
     constexpr uint32_t GPW = 32 / GS;
     constexpr uint32_t NW = kBlock / 32;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -635,20 +652,31 @@ __device__ __forceinline__ uint32_t deliver_tile_desc(const SimArgs &a, uint64_t
     const uint64_t dbase = ((uint64_t)par * a.NT + b) * a.NR;
     uint4 *buf = wbuf + warp * (S * 32);
     uint32_t delivered = 0;
-    uint32_t rc = 0;                                   // region cursor of this lane's group
-    auto dload = [&](uint32_t vb) -> uint64_t {        // descriptor of visit vb + gw (0 if none)
-        const uint32_t v = vb + gw;
+    uint32_t rc = 0;                                   // region cursor of this lane
+    {   // region of visit v0 + lane (binary search once)
+        const uint32_t p = c + (v0 + lane) * a.C;
+        uint32_t lo = 0, hi = a.NR;
+        while (hi - lo > 1) { const uint32_t mid = (lo + hi) >> 1; if (pref[mid] <= p) lo = mid; else hi = mid; }
+        rc = lo;
+    }
+    // every lane loads the descriptor of one of the next 32 visits; batch j (GPW visits)
+    // hands descriptor j*GPW + gw to group gw with a shuffle
+    auto dload32 = [&](uint32_t vbase) -> uint64_t {
+        const uint32_t v = vbase + lane;
         if (v >= v1) return 0ull;
         const uint32_t p = c + v * a.C;
         while (pref[rc + 1] <= p) ++rc;
         return a.desc[(dbase + rc) * a.RS + (p - pref[rc])];
     };
-    {   // region of the first visit of this group (binary search once)
-        const uint32_t p = c + (v0 + gw) * a.C;
-        uint32_t lo = 0, hi = a.NR;
-        while (hi - lo > 1) { const uint32_t mid = (lo + hi) >> 1; if (pref[mid] <= p) lo = mid; else hi = mid; }
-        rc = lo;
-    }
+    uint64_t dcur = dload32(v0), dnxt = dload32(v0 + 32);
+    uint32_t vbase = v0;                               // first visit held in dcur
+    auto dload = [&](uint32_t vb) -> uint64_t {        // descriptor of visit vb + gw (0 if none)
+        while (vb >= vbase + 32) { vbase += 32; dcur = dnxt; dnxt = dload32(vbase + 32); }
+        const uint32_t src = vb - vbase + gw;          // < 32 because vb - vbase is a multiple of GPW
+        const uint32_t lo = __shfl_sync(0xFFFFFFFFu, (uint32_t)dcur, src);
+        const uint32_t hi = __shfl_sync(0xFFFFFFFFu, (uint32_t)(dcur >> 32), src);
+        return vb + gw < v1 ? (((uint64_t)hi << 32) | lo) : 0ull;
+    };
     uint32_t meta[S];                                   // tot | head << 24 | inh << 31
     uint64_t al[S];
     auto issue = [&](int s, uint64_t d) {
@@ -1092,6 +1120,14 @@ static cudaError_t allow_smem(K kern, size_t bytes) {
 
 cudaError_t prepare_kernels(const SimArgs &a) {
     size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    {
+        const size_t ub = (size_t)kStageWords * 4;
+        cudaError_t e1 = allow_smem(k_update<1>, ub);
+        if (!e1) e1 = allow_smem(k_update<2>, ub);
+        if (!e1) e1 = allow_smem(k_update<3>, ub);
+        if (!e1) e1 = allow_smem(k_update<4>, ub);
+        if (e1) return e1;
+    }
     if (a.xbuf) {
         const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT);
         if (xb > bytes) bytes = xb;

@@ -11,11 +11,18 @@ namespace spice {
 // Philox counter word 3 stream tags (reading R9).
 enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFire = 5 };
 
-constexpr int kBlock = 1024;          // threads per tile CTA (update / deliver / fused)
-constexpr int kDescChunk = 2048;      // segment descriptors staged in smem per pass
-constexpr int kStageWords = 6144;     // bnd rows staged per descriptor-transposition pass
+#ifndef SPICE_KBLOCK
+#define SPICE_KBLOCK 1024
+#endif
+#ifndef SPICE_STAGES
+#define SPICE_STAGES 2
+#endif
+constexpr int kBlock = SPICE_KBLOCK;  // threads per tile CTA (update / deliver / fused)
+constexpr int kStages = SPICE_STAGES; // cp.async window stages per warp in delivery
+constexpr int kDescChunk = 4096;      // segment descriptors staged in smem per pass
+constexpr int kStageWords = 12288;     // bnd rows staged per descriptor-transposition pass
 constexpr uint32_t kXRowsBytes = 128 * 1024;   // exchange producer: staged rows per batch
-constexpr uint32_t kWbufWords = (kBlock / 32) * 4 * 32 * 4;   // cp.async window stages: warps x 4 stages x 32 lanes x 16 B
+constexpr uint32_t kWbufWords = (kBlock / 32) * kStages * 32 * 4;   // cp.async window stages: warps x 4 stages x 32 lanes x 16 B
 constexpr uint32_t kMaxTileWidth = 49152;   // u32 counters per tile <= 192 KiB smem
 constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
 constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list region
@@ -79,6 +86,7 @@ struct SimArgs {
     uint32_t record_steps;
     uint32_t key0, key1;
     uint32_t NR, RS;         // spike-list regions
+    uint32_t pf_rows;        // 1: TMA-prefetch spiking rows into L2 at the end of the update
     uint32_t dbg;            // diagnostics only (SPICE_DEBUG_MODE): bit0 no smem reductions,
                              // bit1 no synapse loads, bit2 no descriptor writes
     ModelConst mc;

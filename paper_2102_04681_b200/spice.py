@@ -11,7 +11,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libspice.so")
+# SPICE_LIB: alternative build of the same library (used only for A/B experiments)
+LIB_PATH = os.environ.get("SPICE_LIB") or os.path.join(_PKG, "libspice.so")
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ERANGE, ETRUNC, ESTATE = range(8)
 VOGELS, BRUNEL, BRUNEL_PLUS, SYNTH = 1, 2, 3, 4
