@@ -187,6 +187,15 @@ SPICE_API spice_status spice_info(spice_net *net, uint64_t *n_owned, uint64_t *n
 SPICE_API spice_status spice_profile(spice_net *net, uint64_t n_steps, double *ms_per_kernel,
                                      uint32_t cap, uint32_t *n_kernels);
 
+/* Diagnostics.  With SPICE_PHASES=1 in the environment at create time, thread 0 of every
+ * fused-kernel CTA accumulates, per launch, the SM-clock offset of each phase boundary
+ * from the kernel start: out[cta*16 + slot] for slots 1..12 (1 counters zeroed, 2 region
+ * prefix, 3 descriptors staged, 4 warp 0 done delivering, 5 delivery barrier, 6 delivered
+ * stat, 7 update loop, 8 spike rows, 9 descriptors written, 12 end); slot 13 = launches,
+ * 14/15 = %globaltimer (ns) at start/end of the last launch.  *count = NT*C*16 (0 when
+ * disabled).  Synchronises. */
+SPICE_API spice_status spice_debug_phases(spice_net *net, uint64_t *out, uint64_t cap, uint64_t *count);
+
 /* Number of kernels the library launches per simulated step (evidence for benches). */
 SPICE_API uint32_t spice_kernels_per_step(spice_net *net);
 

@@ -116,9 +116,14 @@ struct spice_net {
     uint64_t n_own = 0, n_own_max = 0;
     uint32_t W = 0, TW = 32, NT = 1, C = 1;
     uint64_t ring_stride = 0;
-    uint64_t nnz = 0;
+    uint64_t nnz = 0;        // stored entries (incl. padding sentinels)
+    uint64_t n_syn = 0;      // synapses (owned targets)
+    bool pad8 = false;       // segments padded to 8-entry windows (window-stream delivery)
+    uint32_t *deg = nullptr; // pad8: true out-degree of every source on this rank
     double mean_seg = 0;
     uint32_t NR = 1, RS = 32;    // spike-list regions
+    uint32_t dcap = 0;           // descriptors staged in shared memory per delivering CTA
+    unsigned long long *ptimes = nullptr;   // SPICE_PHASES diagnostics
     bool fused = true, global_atomics = false;
     // device memory
     std::vector<void *> allocs;
@@ -131,6 +136,7 @@ struct spice_net {
     uint32_t *sl_ids = nullptr, *sl_counts = nullptr;
     uint64_t *sl_rows = nullptr;
     uint64_t *desc = nullptr;
+    uint32_t *dcount = nullptr;
     // tile-pair exchange (G = 1)
     uint16_t *xbuf = nullptr;
     uint64_t *xoff = nullptr;
@@ -339,7 +345,10 @@ __global__ void indegree_kernel(const uint64_t *row_ptr, const uint32_t *bnd, co
         const uint64_t st = row_ptr[s] + bp[0];
         const uint32_t len = bp[1] - bp[0];
         const uint32_t q = s >= n_exc ? 65536u : 1u;
-        for (uint32_t e = lane; e < len; e += 32) atomicAdd(&deg[(uint64_t)b * TW + ent[st + e]], q);
+        for (uint32_t e = lane; e < len; e += 32) {
+            const uint32_t x = ent[st + e];
+            if (x < TW) atomicAdd(&deg[(uint64_t)b * TW + x], q);     // skip padding sentinels
+        }
     }
 }
 __global__ void max_halves_kernel(const uint32_t *deg, uint64_t n, uint32_t *out) {
@@ -354,6 +363,7 @@ spice_status generate(spice_net *n) {
     GenGeom g{};
     g.N = n->N; g.n_own = (uint32_t)n->n_own; g.rank = n->rank; g.G = n->G; g.S = n->S;
     g.TW = n->TW; g.NT = n->NT; g.key0 = (uint32_t)n->seed; g.key1 = (uint32_t)(n->seed >> 32);
+    g.pad8 = n->pad8 ? 1u : 0u;
     const uint64_t nb = (uint64_t)n->N * (n->NT + 1);
     uint32_t *cursor = nullptr;
     spice_status st;
@@ -376,16 +386,22 @@ spice_status generate(spice_net *n) {
     }
     for (const GenRule &x : gr) CU(n, gen_count(g, x, n->bnd, n->stream));
     uint64_t nnz = 0;
-    CU(n, gen_scan(g, n->bnd, n->row_ptr, &nnz, n->stream));
+    if (n->pad8 && (st = dalloc_t(n, &n->deg, n->N, "out-degrees"))) return st;
+    CU(n, gen_scan(g, n->bnd, n->row_ptr, &nnz, n->deg, n->stream));
     n->nnz = nnz;
+    if (n->pad8 && nnz / 8 >= (1ull << 32))
+        return fail(n, SPICE_EINVAL, "%llu synapse windows per rank exceed the 32-bit window index", (unsigned long long)(nnz / 8));
     if ((st = dalloc_t(n, &n->ent_alloc, (size_t)nnz + 2 * kEntPad, "synapse entries"))) return st;
     n->ent = n->ent_alloc + kEntPad;
     CU(n, cudaMemsetAsync(n->ent_alloc, 0, ((size_t)nnz + 2 * kEntPad) * 2, n->stream));
     if ((st = dalloc_t(n, &cursor, nb, "fill cursors"))) return st;
     CU(n, cudaMemsetAsync(cursor, 0, nb * 4, n->stream));
     for (const GenRule &x : gr) CU(n, gen_fill(g, x, n->row_ptr, n->bnd, cursor, n->ent, n->stream));
-    if (any_indeg) CU(n, gen_sort_segments(g, n->row_ptr, n->bnd, n->ent, n->stream));
+    if (n->pad8) CU(n, gen_pad_segments(g, n->row_ptr, n->bnd, cursor, n->ent, n->stream));
+    if (any_indeg) CU(n, gen_sort_segments(g, n->row_ptr, n->bnd, n->ent, n->stream));   // sentinels (>= TW) sort last
     CU(n, cudaStreamSynchronize(n->stream));
+    if (n->pad8) CU(n, gen_sum_u32(n->deg, n->N, &n->n_syn, n->stream));
+    else n->n_syn = nnz;
     dfree(n, cursor);
     n->device_bytes -= nb * 4;
     n->mean_seg = n->N ? (double)nnz / ((double)n->N * n->NT) : 0;
@@ -495,6 +511,9 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     }
     n->NT = (uint32_t)std::max<uint64_t>(1, (n->n_own + n->TW - 1) / n->TW);
     n->C = c->ctas_per_tile ? c->ctas_per_tile : 1;
+    // padded segments + window-stream delivery: single rank, descriptor path (not Brunel+,
+    // not the tile-pair exchange experiment); SPICE_NOPAD=1 keeps the unpadded layout
+    n->pad8 = n->G == 1 && n->model != SPICE_BRUNEL_PLUS && !getenv("SPICE_XCHG") && !getenv("SPICE_NOPAD");
     n->ring_stride = (uint64_t)n->NT * n->TW;
     n->global_atomics = (n->flags & SPICE_FLAG_GLOBAL_ATOMICS) != 0;
     n->fused = !(n->flags & SPICE_FLAG_UNFUSED) && n->C == 1;
@@ -503,7 +522,11 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (n->G == 1) { n->NR = n->NT; n->RS = n->TW; }
     else { n->NR = (uint32_t)(((uint64_t)n->G * n->W + kB2LWords - 1) / kB2LWords); n->RS = kB2LWords * 32; }
     if (n->NR > kMaxRegions) return bail(fail(n, SPICE_EINVAL, "%u spike-list regions > %u: use a wider tile_width", n->NR, kMaxRegions));
-    if (tile_smem_bytes(n->TW, n->NR) > 227 * 1024) return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for shared memory", n->TW));
+    // descriptor staging capacity: kDescSmem, shrunk (not below the update's staging area)
+    // when wide tiles need the shared memory
+    n->dcap = kDescSmem;
+    while (n->dcap > (uint32_t)kStageWords / 2 && tile_smem_bytes(n->TW, n->NR, n->dcap) > 227 * 1024) n->dcap -= 512;
+    if (tile_smem_bytes(n->TW, n->NR, n->dcap) > 227 * 1024) return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for shared memory", n->TW));
     // ---- NCCL communicator ----
     if (n->G > 1 && !n->external) {
         if (!nccl().ok) return bail(fail(n, SPICE_ENCCL, "libnccl.so.2 not found (set SPICE_NCCL_LIB)"));
@@ -631,8 +654,12 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         }
     }
     // descriptor transposition path (G = 1 without the exchange)
-    if (n->G == 1 && n->model != SPICE_BRUNEL_PLUS && !n->xbuf &&
-        (st = dalloc_t(n, &n->desc, 2ull * n->NT * n->NR * n->RS, "segment descriptors"))) return bail(st);
+    if (n->pad8 && !n->xbuf &&
+        (st = dalloc_t(n, &n->desc, 2ull * n->NT * ((n->n_own + 1) & ~1ull), "segment descriptors"))) return bail(st);
+    if (n->desc) {
+        if ((st = dalloc_t(n, &n->dcount, 4, "descriptor counters"))) return bail(st);
+        CU(n, cudaMemset(n->dcount, 0, 16));
+    }
     // ---- kernel arguments ----
     SimArgs &a = n->args;
     a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D;
@@ -641,13 +668,20 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.GS = pick_group_lanes(n->mean_seg);
     if (const char *gs = getenv("SPICE_GROUP_LANES")) a.GS = (uint32_t)atoi(gs);
     if (const char *dm = getenv("SPICE_DEBUG_MODE")) a.dbg = (uint32_t)atoi(dm);   // diagnostics only
+    a.dcap = n->dcap;
+    if (getenv("SPICE_PHASES") && atoi(getenv("SPICE_PHASES"))) {     // diagnostics only
+        if ((st = dalloc_t(n, &n->ptimes, (size_t)n->NT * n->C * 16, "phase clocks"))) return bail(st);
+        CU(n, cudaMemset(n->ptimes, 0, (size_t)n->NT * n->C * 16 * 8));
+        a.ptimes = n->ptimes;
+    }
     a.pf_rows = getenv("SPICE_PREFETCH_ROWS") ? (uint32_t)atoi(getenv("SPICE_PREFETCH_ROWS")) : 0u;   // measured: no gain
     a.key0 = (uint32_t)n->seed; a.key1 = (uint32_t)(n->seed >> 32);
     a.NR = n->NR; a.RS = n->RS;
     a.mc = n->mc;
-    a.row_ptr = n->row_ptr; a.bnd = n->bnd; a.ent = n->ent;
+    a.row_ptr = n->row_ptr; a.bnd = n->bnd; a.ent = n->ent; a.deg = n->deg;
     a.v = n->v; a.ge = n->ge; a.gi = n->gi; a.ref = n->ref; a.acc = n->acc; a.ring = n->ring;
     a.sl_ids = n->sl_ids; a.sl_rows = n->sl_rows; a.sl_counts = n->sl_counts; a.desc = n->desc;
+    a.dstride = (n->n_own + 1) & ~1ull; a.dcount = n->dcount;
     a.xbuf = n->xbuf; a.xoff = n->xoff; a.xcnt = n->xcnt; a.xtotal = n->xtotal; a.xrows_bytes = kXRowsBytes; a.record = n->record; a.sendbuf = n->sendbuf;
     a.gather = n->gather; a.fired_cta = n->fired_cta; a.delivered_cta = n->delivered_cta;
     a.t0 = n->t0; a.force_bits = n->force_bits; a.force_ctl = n->force_ctl;
@@ -748,21 +782,34 @@ spice_status spice_read_connectivity(spice_net *n, uint32_t row_begin, uint32_t 
     const uint32_t nr = row_end - row_begin;
     std::vector<uint64_t> rp(nr + 1);
     CU(n, cudaMemcpy(rp.data(), n->row_ptr + row_begin, (nr + 1) * 8ull, cudaMemcpyDeviceToHost));
-    const uint64_t tot = rp[nr] - rp[0];
+    const uint64_t stored = rp[nr] - rp[0];
+    std::vector<uint64_t> off(nr + 1, 0);       // output offsets (padding sentinels excluded)
+    if (n->pad8) {
+        std::vector<uint32_t> dg(nr ? nr : 1);
+        if (nr) CU(n, cudaMemcpy(dg.data(), n->deg + row_begin, nr * 4ull, cudaMemcpyDeviceToHost));
+        for (uint32_t q = 0; q < nr; ++q) off[q + 1] = off[q] + dg[q];
+    } else {
+        for (uint32_t q = 0; q <= nr; ++q) off[q] = rp[q] - rp[0];
+    }
+    const uint64_t tot = off[nr];
     if (total) *total = tot;
     if (tot > cap || (!tgt && tot)) return fail(n, SPICE_ETRUNC, "need %llu targets", (unsigned long long)tot);
     std::vector<uint32_t> bd((uint64_t)nr * (n->NT + 1));
-    std::vector<uint16_t> en(tot ? tot : 1);
+    std::vector<uint16_t> en(stored ? stored : 1);
     if (nr) CU(n, cudaMemcpy(bd.data(), n->bnd + (uint64_t)row_begin * (n->NT + 1), bd.size() * 4, cudaMemcpyDeviceToHost));
-    if (tot) CU(n, cudaMemcpy(en.data(), n->ent + rp[0], tot * 2, cudaMemcpyDeviceToHost));
+    if (stored) CU(n, cudaMemcpy(en.data(), n->ent + rp[0], stored * 2, cudaMemcpyDeviceToHost));
     for (uint32_t q = 0; q < nr; ++q) {
-        if (row_offsets) row_offsets[q] = rp[q] - rp[0];
+        if (row_offsets) row_offsets[q] = off[q];
         const uint32_t *B = bd.data() + (uint64_t)q * (n->NT + 1);
+        uint64_t o = off[q];
         for (uint32_t b = 0; b < n->NT; ++b)
             for (uint32_t e = B[b]; e < B[b + 1]; ++e) {
-                const uint64_t i = (uint64_t)b * n->TW + en[rp[q] - rp[0] + e];
-                tgt[rp[q] - rp[0] + e] = (uint32_t)local_to_global(i, n->rank, n->G, n->S);
+                const uint32_t x = en[rp[q] - rp[0] + e];
+                if (x >= n->TW) continue;                       // padding sentinel
+                tgt[o++] = (uint32_t)local_to_global((uint64_t)b * n->TW + x, n->rank, n->G, n->S);
             }
+        if (o != off[q + 1]) return fail(n, SPICE_ECUDA, "row %u: %llu targets, out-degree %llu", row_begin + q,
+                                         (unsigned long long)(o - off[q]), (unsigned long long)(off[q + 1] - off[q]));
     }
     if (row_offsets) row_offsets[nr] = tot;
     return SPICE_OK;
@@ -887,7 +934,7 @@ spice_status spice_info(spice_net *n, uint64_t *n_owned, uint64_t *n_syn, uint32
                         uint32_t *tile_width, uint32_t *ctas, uint64_t *bytes) {
     CHECK_NET(n);
     if (n_owned) *n_owned = n->n_own;
-    if (n_syn) *n_syn = n->nnz;
+    if (n_syn) *n_syn = n->n_syn;
     if (n_tiles) *n_tiles = n->NT;
     if (tile_width) *tile_width = n->TW;
     if (ctas) *ctas = n->C;
@@ -954,6 +1001,17 @@ spice_status spice_profile(spice_net *n, uint64_t steps, double *ms, uint32_t ca
     cudaEventDestroy(e1);
     for (int k = 0; k < 4; ++k) ms[k] = cnt[k] ? acc[k] / (double)cnt[k] : 0.0;
     if (nk) *nk = 4;
+    return SPICE_OK;
+}
+
+spice_status spice_debug_phases(spice_net *n, uint64_t *out, uint64_t cap, uint64_t *count) {
+    CHECK_NET(n);
+    const uint64_t m = n->ptimes ? (uint64_t)n->NT * n->C * 16 : 0;
+    if (count) *count = m;
+    if (!m) return SPICE_OK;
+    if (!out || cap < m) return fail(n, SPICE_ETRUNC, "need %llu values", (unsigned long long)m);
+    CU(n, cudaStreamSynchronize(n->stream));
+    CU(n, cudaMemcpy(out, n->ptimes, m * 8, cudaMemcpyDeviceToHost));
     return SPICE_OK;
 }
 

@@ -129,21 +129,57 @@ __global__ void __launch_bounds__(256) indeg_kernel(GenGeom g, GenRule r, const 
 }
 
 // Per row: exclusive prefix of the NT segment counts (in place), row length into rowlen.
-__global__ void __launch_bounds__(256) row_prefix_kernel(GenGeom g, uint32_t *cnt, uint64_t *rowlen) {
+// Padded layout (g.pad8): every segment is padded to a multiple of 8 entries (one aligned
+// 16-byte window each), so the prefix runs over padded lengths and the true row length
+// (out-degree on this rank) goes to deg[s].
+__global__ void __launch_bounds__(256) row_prefix_kernel(GenGeom g, uint32_t *cnt, uint64_t *rowlen,
+                                                         uint32_t *deg) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t)gridDim.x * 8;
     for (uint64_t s = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); s < g.N; s += nwarps) {
         uint32_t *row = cnt + s * (g.NT + 1);
-        uint32_t carry = 0;
+        uint32_t carry = 0, ctrue = 0;
         for (uint32_t b0 = 0; b0 < g.NT; b0 += 32) {
             const uint32_t b = b0 + lane;
             const uint32_t c = b < g.NT ? row[b] : 0u;
-            const uint32_t incl = warp_incl_scan_g(c, lane);
-            if (b < g.NT) row[b] = carry + incl - c;
+            const uint32_t cp = g.pad8 ? (c + 7u) & ~7u : c;
+            const uint32_t incl = warp_incl_scan_g(cp, lane);
+            if (b < g.NT) row[b] = carry + incl - cp;
             carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+            uint32_t ct = c;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ct += __shfl_xor_sync(0xFFFFFFFFu, ct, o);
+            ctrue += ct;
         }
-        if (lane == 0) { row[g.NT] = carry; rowlen[s] = carry; }
+        if (lane == 0) { row[g.NT] = carry; rowlen[s] = carry; if (deg) deg[s] = ctrue; }
     }
+}
+
+// Padded layout: entries [cursor, padded length) of every segment get sentinel offsets
+// TW + (window index mod 64) -- dummy counters past the tile, one per window, so that the
+// sentinels of the 32 windows of one delivery round spread over distinct shared banks.
+__global__ void __launch_bounds__(256) pad_segments_kernel(GenGeom g, const uint64_t *row_ptr,
+                                                           const uint32_t *bnd, const uint32_t *cursor,
+                                                           uint16_t *ent) {
+    const uint64_t total = (uint64_t)g.N * g.NT;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = (uint32_t)(w / g.NT), b = (uint32_t)(w % g.NT);
+        const uint64_t seg = (uint64_t)s * (g.NT + 1) + b;
+        const uint64_t base = row_ptr[s] + bnd[seg];
+        const uint32_t padded = bnd[seg + 1] - bnd[seg];
+        for (uint32_t e = cursor[seg]; e < padded; ++e)
+            ent[base + e] = (uint16_t)(g.TW + (((base + e) >> 3) & 63u));
+    }
+}
+
+__global__ void sum_u32_kernel(const uint32_t *x, uint64_t n, unsigned long long *out) {
+    unsigned long long t = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        t += x[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, t);
 }
 
 // Exclusive scan of n u64 values (in place, out[n] = total); 3 kernels.
@@ -257,9 +293,9 @@ cudaError_t gen_count(const GenGeom &g, const GenRule &r, uint32_t *cnt, cudaStr
 }
 
 cudaError_t gen_scan(const GenGeom &g, uint32_t *cnt_bnd, uint64_t *row_ptr, uint64_t *nnz,
-                     cudaStream_t s) {
+                     uint32_t *deg, cudaStream_t s) {
     cudaError_t e;
-    row_prefix_kernel<<<grid_for(g.N, 8), 256, 0, s>>>(g, cnt_bnd, row_ptr);
+    row_prefix_kernel<<<grid_for(g.N, 8), 256, 0, s>>>(g, cnt_bnd, row_ptr, deg);
     if ((e = cudaGetLastError())) return e;
     const uint64_t n = g.N;
     const uint64_t nb = (n + kScanBlock - 1) / kScanBlock;
@@ -300,6 +336,23 @@ cudaError_t gen_fill(const GenGeom &g, const GenRule &r, const uint64_t *row_ptr
             g, r, row_ptr, bnd, cursor, ent);
     }
     return cudaGetLastError();
+}
+
+cudaError_t gen_pad_segments(const GenGeom &g, const uint64_t *row_ptr, const uint32_t *bnd,
+                             const uint32_t *cursor, uint16_t *ent, cudaStream_t s) {
+    pad_segments_kernel<<<grid_for((uint64_t)g.N * g.NT, 256), 256, 0, s>>>(g, row_ptr, bnd, cursor, ent);
+    return cudaGetLastError();
+}
+
+cudaError_t gen_sum_u32(const uint32_t *x, uint64_t n, uint64_t *out_host, cudaStream_t s) {
+    cudaError_t e;
+    unsigned long long *d = nullptr;
+    if ((e = cudaMallocAsync(&d, 8, s))) return e;
+    if ((e = cudaMemsetAsync(d, 0, 8, s))) return e;
+    if (n) sum_u32_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, d);
+    if ((e = cudaMemcpyAsync(out_host, d, 8, cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaFreeAsync(d, s))) return e;
+    return cudaStreamSynchronize(s);
 }
 
 cudaError_t gen_sort_segments(const GenGeom &g, const uint64_t *row_ptr, const uint32_t *bnd,

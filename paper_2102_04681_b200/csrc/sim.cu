@@ -72,11 +72,22 @@ __device__ __forceinline__ uint32_t philox_word(uint32_t w0, uint32_t w1, uint32
 }
 
 // ------------------------------------------------------------------ neuron update
+// Where a tile's neuron state lives during the update: the global SoA arrays (base 0) or
+// shared-memory copies of the tile slice [base, base + TW) staged by TMA bulk copies.
+struct StatePtrs {
+    float *v, *ge, *gi;
+    uint32_t *ref, *acc;
+    uint32_t base;
+};
+__device__ __forceinline__ StatePtrs global_state(const SimArgs &a) {
+    return StatePtrs{a.v, a.ge, a.gi, a.ref, a.acc, 0u};
+}
 // Update the 4 consecutive owned neurons i0..i0+3 (i0 % 4 == 0) for step t with packed
 // input counts c[4]; returns the spike nibble.  State arrays are padded to NT*TW.
 template <int MODEL>
-__device__ __forceinline__ uint32_t update4(const SimArgs &a, uint64_t t, uint32_t i0, const uint32_t c[4],
-                                            const long long pin[4]) {
+__device__ __forceinline__ uint32_t update4(const SimArgs &a, const StatePtrs &sp, uint64_t t, uint32_t i0,
+                                            const uint32_t c[4], const long long pin[4]) {
+    const uint32_t li = i0 - sp.base;                  // index into the state arrays
     const ModelConst &m = a.mc;
     const uint32_t j0 = (uint32_t)local_to_global(i0, a.rank, a.G, a.S);   // multiple of 4
     uint32_t valid = 0;
@@ -91,17 +102,17 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, uint64_t t, uint32
     uint32_t spk = 0;
     if (MODEL == 4) {                                   // Synth (reading R12)
         const uint4 x = philox4x32_10(make_uint4(j0 >> 2, (uint32_t)t, 0u, kTagFire), a.key0, a.key1);
-        uint4 acc = *reinterpret_cast<const uint4 *>(a.acc + i0);
+        uint4 acc = *reinterpret_cast<const uint4 *>(sp.acc + li);
         acc.x += c[0]; acc.y += c[1]; acc.z += c[2]; acc.w += c[3];
-        *reinterpret_cast<uint4 *>(a.acc + i0) = acc;
+        *reinterpret_cast<uint4 *>(sp.acc + li) = acc;
         spk = ((uint64_t)x.x < m.thr_fire ? 1u : 0u) | ((uint64_t)x.y < m.thr_fire ? 2u : 0u) |
               ((uint64_t)x.z < m.thr_fire ? 4u : 0u) | ((uint64_t)x.w < m.thr_fire ? 8u : 0u);
         if (forced == 1) spk = fbits; else if (forced == 2) spk |= fbits;
     } else if (MODEL == 1) {                            // Vogels-Abbott COBA (readings R3-R5)
-        float4 v4 = *reinterpret_cast<const float4 *>(a.v + i0);
-        float4 ge4 = *reinterpret_cast<const float4 *>(a.ge + i0);
-        float4 gi4 = *reinterpret_cast<const float4 *>(a.gi + i0);
-        uint4 rf4 = *reinterpret_cast<const uint4 *>(a.ref + i0);
+        float4 v4 = *reinterpret_cast<const float4 *>(sp.v + li);
+        float4 ge4 = *reinterpret_cast<const float4 *>(sp.ge + li);
+        float4 gi4 = *reinterpret_cast<const float4 *>(sp.gi + li);
+        uint4 rf4 = *reinterpret_cast<const uint4 *>(sp.ref + li);
         float *vv = &v4.x, *gev = &ge4.x, *giv = &gi4.x;
         uint32_t *rfv = &rf4.x;
 #pragma unroll
@@ -131,13 +142,13 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, uint64_t t, uint32
             rfv[e] = ref;
             spk |= (s ? 1u : 0u) << e;
         }
-        *reinterpret_cast<float4 *>(a.v + i0) = v4;
-        *reinterpret_cast<float4 *>(a.ge + i0) = ge4;
-        *reinterpret_cast<float4 *>(a.gi + i0) = gi4;
-        *reinterpret_cast<uint4 *>(a.ref + i0) = rf4;
+        *reinterpret_cast<float4 *>(sp.v + li) = v4;
+        *reinterpret_cast<float4 *>(sp.ge + li) = ge4;
+        *reinterpret_cast<float4 *>(sp.gi + li) = gi4;
+        *reinterpret_cast<uint4 *>(sp.ref + li) = rf4;
     } else {                                            // Brunel model A (readings R3-R5, R12)
-        float4 v4 = *reinterpret_cast<const float4 *>(a.v + i0);
-        uint4 rf4 = *reinterpret_cast<const uint4 *>(a.ref + i0);
+        float4 v4 = *reinterpret_cast<const float4 *>(sp.v + li);
+        uint4 rf4 = *reinterpret_cast<const uint4 *>(sp.ref + li);
         float *vv = &v4.x;
         uint32_t *rfv = &rf4.x;
         uint4 x = make_uint4(0, 0, 0, 0);
@@ -169,22 +180,39 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, uint64_t t, uint32
             rfv[e] = ref;
             spk |= (s ? 1u : 0u) << e;
         }
-        *reinterpret_cast<float4 *>(a.v + i0) = v4;
-        *reinterpret_cast<uint4 *>(a.ref + i0) = rf4;
+        *reinterpret_cast<float4 *>(sp.v + li) = v4;
+        *reinterpret_cast<uint4 *>(sp.ref + li) = rf4;
     }
     return spk & valid;
+}
+
+// Diagnostics (SPICE_PHASES=1): thread 0 of every fused-kernel CTA accumulates the SM
+// clock offset of phase boundary `slot` from the kernel start into ptimes[cta*16 + slot];
+// slot 13 counts launches, 14/15 hold %globaltimer at start/end of the last launch.
+__device__ __forceinline__ long long &phase_c0() { __shared__ long long c0; return c0; }
+__device__ __forceinline__ void phase_mark(const SimArgs &a, int slot) {
+    if (a.ptimes && threadIdx.x == 0) {
+        unsigned long long *p = a.ptimes + blockIdx.x * 16u;
+        if (slot == 0) {
+            phase_c0() = clock64();
+            unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            p[14] = g; p[13] += 1;
+        } else {
+            p[slot] += (unsigned long long)(clock64() - phase_c0());
+            if (slot == 12) { unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p[15] = g; }
+        }
+    }
 }
 
 // Update every neuron of tile b for step t.  Inputs come from `cnt` (shared memory, the
 // tile's counts) or, when cnt == nullptr, from input ring slot t mod D (read and cleared).
 // ------------------------------------------------------------------ delivery
 struct DeliverSmem {
-    uint4 *wbuf;       // [32 warps * 4 stages * 32 lanes] cp.async window stages
-    uint32_t *stage;   // [kStageWords] descriptor-transposition staging (aliases dstart/dlen)
-    uint32_t *cnt;     // [TW] tile counters
+    uint4 *wbuf;       // [warps * kStages * 32 lanes] cp.async window stages
+    uint32_t *cnt;     // [TW + kDummy] tile counters (+ padding-sentinel dummies)
+    uint64_t *dsm;     // [dcap] the CTA's segment descriptors (delivery phase)
+    uint32_t *stage;   // [kStageWords] bnd-row staging of the update phase (aliases dsm)
     uint32_t *pref;    // [NR + 1] region prefix
-    uint64_t *dstart;  // [kDescChunk] absolute segment start in ent
-    uint32_t *dlen;    // [kDescChunk] len | inh << 31
     uint32_t *tmp;     // [32]
 };
 
@@ -441,42 +469,63 @@ __global__ void __launch_bounds__(kBlock) k_xcap(SimArgs a, uint32_t *cap) {
     for (uint32_t i = threadIdx.x; i < 2 * NT; i += kBlock) cap[((uint64_t)(i >> 1) * NT + g) * 2 + (i & 1)] = e[i];
 }
 
-// Descriptor transposition (G = 1): for the n spikes of region b (this tile's spikes), load
-// their bnd rows (coalesced, CH spikes at a time, staged in smem) and write, for every
-// destination tile bb, the CH descriptors desc[par][bb][b][q0 .. q0+CH) with one coalesced
-// store per tile.  Delivery CTAs then read their descriptors contiguously.
-__device__ __forceinline__ void write_descriptors(const SimArgs &a, uint32_t par, uint32_t b, uint32_t n,
-                                  const uint32_t *region, const uint64_t *region_rows, uint32_t *stage) {
+// Descriptor transposition (G = 1, padded layout): for the n spikes of region b (this
+// tile's spikes), one pass loads every spike's bnd row (a warp per spike, coalesced),
+// row start and out-degree, staged in smem (CH spikes at a time; CH covers a whole step's
+// tile list in the common case), then writes, for every destination tile bb, the
+// descriptors desc[par][bb][b][q0 .. q0+CH) with coalesced stores.  Delivery CTAs then read
+// their descriptors contiguously.  Returns (to thread 0) the spikes' delivered-event count.
+__device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t t, uint32_t b, uint32_t n,
+                                  const uint32_t *region, uint64_t *region_rows, uint32_t *stage) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t par = (uint32_t)(t & 1);
+    // dense per-tile lists: this CTA's n descriptors go to [off, off + n) of every
+    // destination tile's list of step t (one atomic on the step's counter)
+    __shared__ uint32_t s_off;
+    if (threadIdx.x == 0 && n) s_off = atomicAdd(&a.dcount[t % 3], n);
     const uint32_t rowlen = a.NT + 1u;
-    const uint32_t CH = max(1u, min(32u, (uint32_t)kStageWords / rowlen));   // one lane per spike
+    const uint32_t CH = max(1u, (uint32_t)kStageWords / (rowlen + 3u));
+    uint64_t *srow = reinterpret_cast<uint64_t *>(stage + CH * rowlen + (CH * rowlen & 1u));
+    uint32_t *sdeg = reinterpret_cast<uint32_t *>(srow + CH);
+    uint64_t dsum = 0;
     for (uint32_t q0 = 0; q0 < n; q0 += CH) {
         const uint32_t nq = min(CH, n - q0);
         __syncthreads();
+        // every load of the pass in flight at once (cp.async, no register round trips)
         for (uint32_t ql = warp; ql < nq; ql += kBlock / 32) {            // one warp per spike row
-            const uint32_t *row = a.bnd + (uint64_t)region[q0 + ql] * rowlen;
-            for (uint32_t bb = lane; bb < rowlen; bb += 32) stage[ql * rowlen + bb] = row[bb];
+            const uint32_t s = region[q0 + ql];
+            const uint32_t *row = a.bnd + (uint64_t)s * rowlen;
+            for (uint32_t bb = lane; bb < rowlen; bb += 32)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(stage + ql * rowlen + bb)), "l"(row + bb) : "memory");
+            if (lane == 0) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(srow + ql)), "l"(a.row_ptr + s) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(sdeg + ql)), "l"(a.deg + s) : "memory");
+            }
         }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         __syncthreads();
-        // lane ql of warp w writes descriptor (tile bb, spike q0 + ql): coalesced per tile
-        const uint32_t ql = lane;
-        uint32_t s = 0;
-        uint64_t rs = 0;
-        if (ql < nq) { s = region[q0 + ql]; rs = region_rows[q0 + ql]; }
-        const uint64_t inh = s >= a.n_exc ? (1ull << 63) : 0ull;
+        if (warp == 0)
+            for (uint32_t ql = lane; ql < nq; ql += 32) { region_rows[q0 + ql] = srow[ql]; dsum += sdeg[ql]; }
         for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
-            if (ql < nq) {
+            uint64_t *dst = a.desc + ((uint64_t)par * a.NT + bb) * a.dstride + s_off + q0;
+            for (uint32_t ql = lane; ql < nq; ql += 32) {   // padded: rs, lo, hi are multiples of 8
                 const uint32_t lo = stage[ql * rowlen + bb], hi = stage[ql * rowlen + bb + 1];
-                a.desc[(((uint64_t)par * a.NT + bb) * a.NR + b) * a.RS + q0 + ql] =
-                    (rs + lo) | ((uint64_t)(hi - lo) << 40) | inh;
+                const uint64_t inh = region[q0 + ql] >= a.n_exc ? (1ull << 63) : 0ull;
+                dst[ql] = ((srow[ql] + lo) >> 3) | ((uint64_t)((hi - lo) >> 3) << 32) | inh;
             }
         }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xFFFFFFFFu, dsum, o);
+    __syncthreads();
+    return dsum;                                       // valid in warp 0
 }
 
 template <int MODEL>
 __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, const uint32_t *cnt,
-                            bool write_list, uint32_t *s_count, uint32_t *stage, uint32_t *xsm = nullptr) {
+                            bool write_list, uint32_t *s_count, uint32_t *stage, uint32_t *xsm = nullptr,
+                            const StatePtrs *staged = nullptr, bool marks = false) {
+    const StatePtrs sp = staged ? *staged : global_state(a);
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     const uint32_t lo = b * a.TW;
     const uint32_t span = lo < a.W * 32u ? min(a.TW, a.W * 32u - lo) : 0u;   // bitmap coverage
@@ -504,7 +553,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
                 c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
             }
-            nib = update4<MODEL>(a, t, lo + x4, c, pin);
+            nib = update4<MODEL>(a, sp, t, lo + x4, c, pin);
         }
         // 8 lanes x 4 bits -> one 32-neuron bitmap word
         uint32_t w = nib << (4u * (lane & 7u));
@@ -530,15 +579,39 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
         }
     }
     __syncthreads();
+    if (marks) phase_mark(a, 7);
+    if (staged) {                                          // staged state -> global (coalesced)
+        const uint32_t nw = a.TW / 4;
+        for (uint32_t x = tid; x < nw; x += kBlock) {
+            const uint32_t g = lo + 4 * x;
+            if (MODEL == 4) reinterpret_cast<uint4 *>(a.acc + g)[0] = reinterpret_cast<const uint4 *>(sp.acc)[x];
+            if (MODEL != 4) reinterpret_cast<float4 *>(a.v + g)[0] = reinterpret_cast<const float4 *>(sp.v)[x];
+            if (MODEL != 4) reinterpret_cast<uint4 *>(a.ref + g)[0] = reinterpret_cast<const uint4 *>(sp.ref)[x];
+            if (MODEL == 1) reinterpret_cast<float4 *>(a.ge + g)[0] = reinterpret_cast<const float4 *>(sp.ge)[x];
+            if (MODEL == 1) reinterpret_cast<float4 *>(a.gi + g)[0] = reinterpret_cast<const float4 *>(sp.gi)[x];
+        }
+        __syncthreads();
+    }
     const uint32_t n_tile = *s_count;
     if (tid == 0) {
         if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
         a.fired_cta[b] += n_tile;
     }
-    if (write_list) {                                     // row starts of the spikes, all at once
-        for (uint32_t q = tid; q < n_tile; q += kBlock) region_rows[q] = a.row_ptr[region[q]];
+    if (write_list && !a.desc) {                          // row starts of the spikes, all at once
+        uint32_t dsum = 0;                                // (the descriptor pass loads them itself)
+        for (uint32_t q = tid; q < n_tile; q += kBlock) {
+            const uint32_t s = region[q];
+            region_rows[q] = a.row_ptr[s];
+            if (a.deg) dsum += a.deg[s];
+        }
+        if (a.deg) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xFFFFFFFFu, dsum, o);
+            if (lane == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
+        }
         __syncthreads();
     }
+    if (marks) phase_mark(a, 8);
     if (write_list && (a.dbg & 8u) == 0 && a.pf_rows) {
         // TMA L2 prefetch of every spiking row (contiguous, ~rowlen * 2 bytes): the next
         // launch's delivery reads these rows as scattered 16-byte windows from ~all CTAs;
@@ -552,7 +625,11 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a.ent + lo), "r"((uint32_t)(hi - lo) * 2u) : "memory");
         }
     }
-    if (write_list && a.desc && !(a.dbg & 4u)) write_descriptors(a, par, b, n_tile, region, region_rows, stage);
+    if (write_list && a.desc && !(a.dbg & 4u)) {          // padded layout: delivered events are
+        const uint64_t dsum = write_descriptors(a, t, b, n_tile, region, region_rows, stage);
+        if (tid == 0 && dsum) a.delivered_cta[b] += dsum;   // counted here from the out-degrees
+    }
+    if (marks) phase_mark(a, 9);
     if constexpr (MODEL != 3) {
         if (write_list && a.xbuf) {
             uint32_t phase = 0;
@@ -623,106 +700,161 @@ __device__ __forceinline__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, u
     return delivered;
 }
 
-// Descriptor-driven delivery (G = 1), software-pipelined through shared memory.
+// Eight unconditional shared-memory reductions of one padded 16-byte window (sentinel
+// entries land in the dummy counters past the tile).
+__device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v, uint32_t q) {
+    const uint32_t a0 = cnt_s + ((v.x & 0xFFFFu) << 2), a1 = cnt_s + ((v.x >> 14) & ~3u);
+    const uint32_t a2 = cnt_s + ((v.y & 0xFFFFu) << 2), a3 = cnt_s + ((v.y >> 14) & ~3u);
+    const uint32_t a4 = cnt_s + ((v.z & 0xFFFFu) << 2), a5 = cnt_s + ((v.z >> 14) & ~3u);
+    const uint32_t a6 = cnt_s + ((v.w & 0xFFFFu) << 2), a7 = cnt_s + ((v.w >> 14) & ~3u);
+    asm volatile(
+        "red.shared.add.u32 [%0], %8;\n\t"
+        "red.shared.add.u32 [%1], %8;\n\t"
+        "red.shared.add.u32 [%2], %8;\n\t"
+        "red.shared.add.u32 [%3], %8;\n\t"
+        "red.shared.add.u32 [%4], %8;\n\t"
+        "red.shared.add.u32 [%5], %8;\n\t"
+        "red.shared.add.u32 [%6], %8;\n\t"
+        "red.shared.add.u32 [%7], %8;"
+        :: "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7), "r"(q)
+        : "memory");
+}
+
+// Window-stream delivery (G = 1, padded layout), software-pipelined through shared memory.
 //  * The CTA's visits (spike x this tile, for spikes p with p % C == c) are split evenly
-//    across its warps (flat prefix over the spike-list regions), so no warp waits for a
-//    heavier one at the closing barrier.
-//  * A warp walks its visits in batches of GPW = 32/GS (one visit per GS-lane group).  For
-//    every batch each lane copies its 16-byte window of the segment (8 u16 offsets) into a
-//    per-warp shared-memory stage with cp.async (LDGSTS, L2 only); S stages are in flight,
-//    the descriptor of the next batch is prefetched one batch ahead.  Processing a batch
-//    (mask + shared-memory reductions) overlaps the loads of the following S-1 batches.
-template <int GS>
-__device__ __forceinline__ uint32_t deliver_tile_desc(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
-                                      uint32_t *cnt, uint32_t *pref, uint32_t *tmp, uint4 *wbuf) {
+//    across its warps (flat prefix over the spike-list regions).
+//  * A warp takes its visits 32 at a time (a "group"): lane L loads the descriptor of visit
+//    L (coalesced, prefetched one group ahead); a warp scan of the segments' window counts
+//    concatenates their windows into one stream of T windows.
+//  * The stream is consumed 32 windows per round, one window per lane.  The owner of
+//    every (non-empty, compacted) segment starting inside the round sets bit (start - r0);
+//    one redux.sync.or gives the round's start mask, so lane L's segment is
+//    sprev + popc(mask & lanes <= L) (sprev: segment of window r0 - 1).  Lane L then
+//    copies its window into its slot of a per-warp shared-memory stage with cp.async
+//    (LDGSTS, L2 only).  S stages are in flight; processing a stage is one 16-byte shared
+//    load and eight unconditional red.shared.add (no masks: padding maps to dummies).
+// Segment length no longer sets the lane mapping: short and long segments fill the same
+// rounds, and the per-visit bookkeeping is one descriptor load and one scan step.
+__device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+                                     uint32_t *cnt, uint32_t *pref, uint32_t *tmp, uint4 *wbuf, uint64_t *dsm,
+                                     bool marks = false) {
     constexpr int S = kStages;
-    constexpr uint32_t GPW = 32 / GS;
     constexpr uint32_t NW = kBlock / 32;
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t gw = lane / GS, lig = lane % GS;
     const uint32_t par = (uint32_t)(t & 1);
     const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
-    // visits of this CTA: spikes p = c + C q; region counts -> prefix (in spike units)
-    for (uint32_t r = tid; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
+    // the step's dense descriptor list of this tile: total from the step counter (CTA 0
+    // also clears the counter step t + 2 will use; nobody touches it in this launch)
+    __shared__ uint32_t s_total;
+    if (tid == 0) {
+        s_total = a.dcount[t % 3];
+        if (b == 0 && c == 0) a.dcount[(t + 2) % 3] = 0u;
+    }
     __syncthreads();
-    block_exclusive_scan(pref, a.NR, tmp);
-    const uint32_t n_sp = pref[a.NR];
+    if (marks) phase_mark(a, 2);
+    const uint32_t n_sp = s_total;
     const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
     const uint32_t v0 = (uint32_t)((uint64_t)my * warp / NW), v1 = (uint32_t)((uint64_t)my * (warp + 1) / NW);
-    const uint64_t dbase = ((uint64_t)par * a.NT + b) * a.NR;
+    const uint64_t *dlist = a.desc + ((uint64_t)par * a.NT + b) * a.dstride + c;   // visit v -> dlist[v * C]
+    const uint4 *ent4 = reinterpret_cast<const uint4 *>(a.ent);
     uint4 *buf = wbuf + warp * (S * 32);
-    uint32_t delivered = 0;
-    uint32_t rc = 0;                                   // region cursor of this lane
-    {   // region of visit v0 + lane (binary search once)
-        const uint32_t p = c + (v0 + lane) * a.C;
-        uint32_t lo = 0, hi = a.NR;
-        while (hi - lo > 1) { const uint32_t mid = (lo + hi) >> 1; if (pref[mid] <= p) lo = mid; else hi = mid; }
-        rc = lo;
+    // The warp's descriptors [v0, v1) are copied into shared memory first (8-byte
+    // cp.async, one memory latency for the whole walk) when the CTA's visits fit.
+    const bool dsmem = my <= a.dcap;
+    if (dsmem) {
+        for (uint32_t v = v0 + lane; v < v1; v += 32) {
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dsm + v);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa), "l"(dlist + (uint64_t)v * a.C) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
     }
-    // every lane loads the descriptor of one of the next 32 visits; batch j (GPW visits)
-    // hands descriptor j*GPW + gw to group gw with a shuffle
-    auto dload32 = [&](uint32_t vbase) -> uint64_t {
+    if (marks) phase_mark(a, 3);
+    auto dload32 = [&](uint32_t vbase) -> uint64_t {   // descriptor of visit vbase + lane (0: none)
         const uint32_t v = vbase + lane;
         if (v >= v1) return 0ull;
-        const uint32_t p = c + v * a.C;
-        while (pref[rc + 1] <= p) ++rc;
-        return a.desc[(dbase + rc) * a.RS + (p - pref[rc])];
+        return dsmem ? dsm[v] : dlist[(uint64_t)v * a.C];
     };
-    uint64_t dcur = dload32(v0), dnxt = dload32(v0 + 32);
-    uint32_t vbase = v0;                               // first visit held in dcur
-    auto dload = [&](uint32_t vb) -> uint64_t {        // descriptor of visit vb + gw (0 if none)
-        while (vb >= vbase + 32) { vbase += 32; dcur = dnxt; dnxt = dload32(vbase + 32); }
-        const uint32_t src = vb - vbase + gw;          // < 32 because vb - vbase is a multiple of GPW
-        const uint32_t lo = __shfl_sync(0xFFFFFFFFu, (uint32_t)dcur, src);
-        const uint32_t hi = __shfl_sync(0xFFFFFFFFu, (uint32_t)(dcur >> 32), src);
-        return vb + gw < v1 ? (((uint64_t)hi << 32) | lo) : 0ull;
-    };
-    uint32_t meta[S];                                   // tot | head << 24 | inh << 31
-    uint64_t al[S];
-    auto issue = [&](int s, uint64_t d) {
-        const uint64_t st = d & ((1ull << 40) - 1);
-        const uint32_t len = (uint32_t)(d >> 40) & ((1u << 23) - 1);
-        const uint32_t head = (uint32_t)st & 7u;
-        meta[s] = (head + len) | (head << 24) | ((uint32_t)(d >> 63) << 31);
-        al[s] = st & ~7ull;
-        if (lig == 0) delivered += len;
-        if (8u * lig < head + len && len && !(a.dbg & 2u)) {
-            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf + s * 32 + lane);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(a.ent + al[s] + 8u * lig) : "memory");
+    uint32_t gnext = v0;                               // first visit of the next group
+    uint64_t dn = dload32(v0);                         // its descriptors (prefetched)
+    uint32_t cw = 0, pw = 0, nwl = 0, T = 0, inhm = 0, r0 = 0, sprev = 0;   // current group
+    bool done = false;
+    const uint32_t lmask_le = 0xFFFFFFFFu >> (31u - lane);
+    auto next_group = [&]() {
+        while (gnext < v1) {
+            uint64_t d = dn;
+            gnext += 32;
+            dn = dload32(gnext);
+            uint32_t nw = (uint32_t)(d >> 32) & 0x7FFFFFFFu;
+            const uint32_t nzm = __ballot_sync(FULL, nw != 0u);
+            if (nzm & (nzm + 1u)) {                    // empty segments before non-empty ones:
+                const uint32_t k = __popc(nzm);        // compact (lane j <- j-th non-empty)
+                const uint32_t src = lane < k ? __fns(nzm, 0u, (int)lane + 1) : lane;
+                const uint32_t lo32 = __shfl_sync(FULL, (uint32_t)d, src);
+                const uint32_t hi32 = __shfl_sync(FULL, (uint32_t)(d >> 32), src);
+                d = lane < k ? (((uint64_t)hi32 << 32) | lo32) : 0ull;
+                nw = (uint32_t)(d >> 32) & 0x7FFFFFFFu;
+            }
+            cw = (uint32_t)d;
+            nwl = nw;
+            const uint32_t incl = warp_incl_scan(nw);
+            pw = incl - nw;
+            T = __shfl_sync(FULL, incl, 31);
+            inhm = __ballot_sync(FULL, (uint32_t)(d >> 63));
+            r0 = 0;
+            sprev = 0xFFFFFFFFu;                       // segment 0 starts at window 0
+            if (T) return;
         }
+        done = true;
+    };
+    uint32_t qs[S];                                    // per stage: q of this lane's window (0: none)
+    uint32_t live = 0;                                 // warp-uniform: stages holding a round
+    auto issue = [&](int s) {
+        if (!done && r0 >= T) next_group();
+        uint32_t q = 0;
+        if (!done) {
+            const uint32_t w = r0 + lane;
+            const uint32_t dd = pw - r0;               // my segment's start, relative to the round
+            const uint32_t smask = __reduce_or_sync(FULL, (nwl != 0u && dd < 32u) ? 1u << dd : 0u);
+            const uint32_t lo = (sprev + __popc(smask & lmask_le)) & 31u;
+            sprev += __popc(smask);
+            const uint32_t wi = __shfl_sync(FULL, cw, lo);
+            const uint32_t plo = __shfl_sync(FULL, pw, lo);
+            if (w < T) {
+                q = (inhm >> lo) & 1u ? 65536u : 1u;
+                if (!(a.dbg & 2u)) {
+                    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf + s * 32 + lane);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(ent4 + (wi + (w - plo))) : "memory");
+                }
+            }
+            r0 += 32;
+            live |= 1u << s;
+        }
+        qs[s] = q;
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     auto process = [&](int s) {
-        const uint32_t tot = meta[s] & 0xFFFFFFu, head = (meta[s] >> 24) & 7u;
-        const uint32_t qv = (meta[s] >> 31) ? 65536u : 1u;
-        uint32_t off = 8u * lig;
-        if ((a.dbg & 3u) && off < tot) { delivered ^= (a.dbg & 2u) ? 0u : buf[s * 32 + lane].x; return; }
-        if (off < tot && tot > head) {
-            const uint4 v = buf[s * 32 + lane];
-            accumulate_masked(cnt_s, v, window_mask((int)head - (int)off, (int)(tot - off)), qv);
-            for (off += 8u * GS; off < tot; off += 8u * GS)
-                accumulate_masked(cnt_s, ld_stream_v4(a.ent + al[s] + off),
-                                  window_mask((int)head - (int)off, (int)(tot - off)), qv);
-        }
+        if (qs[s] && !(a.dbg & 3u)) accumulate_window(cnt_s, buf[s * 32 + lane], qs[s]);
+        live &= ~(1u << s);
     };
-    uint32_t vb = v0;                                   // next batch to issue
-    uint64_t dn = dload(vb);
 #pragma unroll
-    for (int s = 0; s < S - 1; ++s) { const uint64_t d = dn; vb += GPW; dn = dload(vb); issue(s, d); }
-    for (uint32_t pb = v0; pb < v1; ) {
+    for (int s = 0; s < S - 1; ++s) issue(s);
+    bool fin = false;
+    while (!fin) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
-            // issue batch (pb + (S-1) GPW) into stage (s + S - 1) % S, prefetch the next descriptor
-            { const uint64_t d = dn; vb += GPW; dn = dload(vb); issue((s + S - 1) % S, d); }
+            issue((s + S - 1) % S);
             asm volatile("cp.async.wait_group %0;" :: "n"(S - 1) : "memory");
             process(s);
-            pb += GPW;
-            if (pb >= v1) break;
+            if (done && live == 0) { fin = true; break; }
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (marks) phase_mark(a, 4);
     __syncthreads();
-    return delivered;
+    if (marks) phase_mark(a, 5);
+    return 0u;                                         // delivered events: counted at the source
 }
 
 // ------------------------------------------------------------- Brunel+ STDP
@@ -852,23 +984,28 @@ __device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot,
     }
 }
 
+// Delivery shared memory: wbuf | cnt [TW + kDummy] | big [max(kStageWords, 2 dcap)] | pref | tmp
+__host__ __device__ inline uint32_t big_words(uint32_t dcap) {
+    return (uint32_t)kStageWords > 2u * dcap ? (uint32_t)kStageWords : 2u * dcap;
+}
 __device__ __forceinline__ DeliverSmem carve(const SimArgs &a, uint32_t *smem) {
     DeliverSmem sm;
     const uint32_t tw4 = (a.TW + 3u) & ~3u;
     sm.wbuf = reinterpret_cast<uint4 *>(smem);          // kWbufWords words, 16-byte aligned
     smem += kWbufWords;
     sm.cnt = smem;
-    sm.dstart = reinterpret_cast<uint64_t *>(smem + tw4);
-    sm.dlen = smem + tw4 + 2 * kDescChunk;
-    sm.stage = smem + tw4;
-    sm.pref = sm.dlen + kDescChunk;
+    smem += tw4 + kDummy;
+    sm.dsm = reinterpret_cast<uint64_t *>(smem);
+    sm.stage = smem;
+    smem += big_words(a.dcap);
+    sm.pref = smem;
     sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
     return sm;
 }
 
-size_t tile_smem_bytes(uint32_t TW, uint32_t NR) {
+size_t tile_smem_bytes(uint32_t TW, uint32_t NR, uint32_t dcap) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
-    return ((size_t)kWbufWords + tw4 + 3 * kDescChunk + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
+    return ((size_t)kWbufWords + tw4 + kDummy + big_words(dcap) + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
 }
 size_t xchg_kernel_smem_bytes(uint32_t TW, uint32_t NT) {
     const size_t c = ((size_t)((TW + 3u) & ~3u)) * 4;
@@ -927,7 +1064,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
     const uint32_t b = blockIdx.x / a.C, c = blockIdx.x % a.C;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
     uint32_t d;
-    if (a.desc) { __syncthreads(); d = deliver_tile_desc<GS>(a, t, b, c, sm.cnt, sm.pref, sm.tmp, sm.wbuf); }
+    if (a.desc) { __syncthreads(); d = deliver_tile_win(a, t, b, c, sm.cnt, sm.pref, sm.tmp, sm.wbuf, sm.dsm); }
     else d = deliver_tile<GS>(a, t, b, c, sm);
     uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
     if (a.C == 1u) {
@@ -1014,18 +1151,21 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         }
         return;
     }
+    phase_mark(a, 0);
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
     __syncthreads();
-    const uint32_t d = deliver_tile_desc<GS>(a, t, b, 0, sm.cnt, sm.pref, sm.tmp, sm.wbuf);
-    store_delivered(a, b, d, sm.tmp);
+    phase_mark(a, 1);
+    deliver_tile_win(a, t, b, 0, sm.cnt, sm.pref, sm.tmp, sm.wbuf, sm.dsm, true);
+    phase_mark(a, 6);
     if (a.delay == 1) {
-        update_tile<MODEL>(a, t + 1, b, sm.cnt, true, &s_count, sm.stage);
+        update_tile<MODEL>(a, t + 1, b, sm.cnt, true, &s_count, sm.stage, nullptr, nullptr, true);
     } else {
         uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)
             *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(sm.cnt + x);
-        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count, sm.stage);
+        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count, sm.stage, nullptr, nullptr, true);
     }
+    phase_mark(a, 12);
     }
 }
 
@@ -1055,8 +1195,11 @@ __global__ void __launch_bounds__(kBlock) k_global_atomics(SimArgs a, uint32_t k
         const uint32_t len = bp[1] - bp[0];
         const uint32_t qv = s >= a.n_exc ? 65536u : 1u;
         uint32_t *tile = slot + (uint64_t)b * a.TW;
-        for (uint32_t e = lane; e < len; e += 32) atomicAdd(tile + a.ent[st + e], qv);
-        if (lane == 0) delivered += len;
+        for (uint32_t e = lane; e < len; e += 32) {
+            const uint32_t x = a.ent[st + e];
+            if (x < a.TW) atomicAdd(tile + x, qv);       // skip padding sentinels
+        }
+        if (lane == 0 && !a.deg) delivered += len;
     }
     store_delivered(a, blockIdx.x % (a.NT * a.C), delivered, tmp);
 }
@@ -1119,7 +1262,7 @@ static cudaError_t allow_smem(K kern, size_t bytes) {
 }
 
 cudaError_t prepare_kernels(const SimArgs &a) {
-    size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap);
     {
         const size_t ub = (size_t)kStageWords * 4;
         cudaError_t e1 = allow_smem(k_update<1>, ub);
@@ -1172,7 +1315,7 @@ cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s) {
 
 cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, int n_sm, cudaStream_t s) {
     if (global_atomics) {
-        const size_t bytes = tile_smem_bytes(0, a.NR);
+        const size_t bytes = tile_smem_bytes(0, a.NR, a.dcap);
         k_global_atomics<<<min((uint32_t)(n_sm * 4), a.NT * a.C), kBlock, bytes, s>>>(a, k);
         return cudaGetLastError();
     }
@@ -1188,7 +1331,7 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
         }
         return cudaGetLastError();
     }
-    size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap);
     if (a.xbuf) { const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT); if (xb > bytes) bytes = xb; }
     const uint32_t grid = a.NT * a.C;
     switch (a.GS) {
@@ -1215,7 +1358,7 @@ static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) 
 }
 
 cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
-    size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap);
     if (a.xbuf) { const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT); if (xb > bytes) bytes = xb; }
     switch (a.model) {
     case 1: fused_m<1>(a, k, bytes, s); break;

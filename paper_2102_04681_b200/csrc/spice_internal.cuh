@@ -19,7 +19,7 @@ enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFi
 #endif
 constexpr int kBlock = SPICE_KBLOCK;  // threads per tile CTA (update / deliver / fused)
 constexpr int kStages = SPICE_STAGES; // cp.async window stages per warp in delivery
-constexpr int kDescChunk = 4096;      // segment descriptors staged in smem per pass
+constexpr uint32_t kDescSmem = 8192;  // default descriptor staging capacity per CTA (64 KiB)
 constexpr int kStageWords = 12288;     // bnd rows staged per descriptor-transposition pass
 constexpr uint32_t kXRowsBytes = 128 * 1024;   // exchange producer: staged rows per batch
 constexpr uint32_t kWbufWords = (kBlock / 32) * kStages * 32 * 4;   // cp.async window stages: warps x 4 stages x 32 lanes x 16 B
@@ -27,6 +27,7 @@ constexpr uint32_t kMaxTileWidth = 49152;   // u32 counters per tile <= 192 KiB 
 constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
 constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list region
 constexpr int kEntPad = 64;           // u16 padding before/after the entry array
+constexpr uint32_t kDummy = 64;       // dummy counters past the tile (padding sentinels)
 
 // Philox4x32-10 (Salmon et al., SC'11).  Multipliers 0xD2511F53 / 0xCD9E8D57, Weyl
 // key increments 0x9E3779B9 / 0xBB67AE85; 10 rounds.
@@ -87,6 +88,8 @@ struct SimArgs {
     uint32_t key0, key1;
     uint32_t NR, RS;         // spike-list regions
     uint32_t pf_rows;        // 1: TMA-prefetch spiking rows into L2 at the end of the update
+    uint32_t dcap;           // descriptors a delivering CTA stages in shared memory
+    unsigned long long *ptimes;   // diagnostics (SPICE_PHASES=1): per CTA [16] phase clocks
     uint32_t dbg;            // diagnostics only (SPICE_DEBUG_MODE): bit0 no smem reductions,
                              // bit1 no synapse loads, bit2 no descriptor writes
     ModelConst mc;
@@ -94,6 +97,9 @@ struct SimArgs {
     const uint64_t *row_ptr; // [N+1]
     const uint32_t *bnd;     // [N * (NT+1)]
     const uint16_t *ent;
+    const uint32_t *deg;     // padded layout (G = 1, not Brunel+): every segment is padded to
+                             // a multiple of 8 entries with sentinels >= TW (dummy counters
+                             // TW .. TW+63); deg[s] = true out-degree (delivered-event count)
     // state
     float *v, *ge, *gi;
     uint32_t *ref, *acc;
@@ -102,10 +108,13 @@ struct SimArgs {
     uint32_t *sl_ids;        // 2 * NR * RS
     uint64_t *sl_rows;       // 2 * NR * RS row starts of the listed spikes
     uint32_t *sl_counts;     // 2 * NR
-    // G = 1: per-step segment descriptors written transposed by the updating CTA:
-    // desc[((par*NT + b)*NR + r)*RS + q] = start (bits 0-39) | len (40-62) | inh (63)
-    // of the q-th spike of region r restricted to tile b (coalesced reads in delivery)
+    // G = 1 (padded layout): per-step segment descriptors, written transposed by the
+    // updating CTAs into one dense list per destination tile: desc[(par*NT + b)*dstride + i]
+    // = first 16-byte window (bits 0-31) | window count (32-62) | inh (63) of the i-th
+    // spike of the step restricted to tile b (list order = producer arrival order)
     uint64_t *desc;
+    uint64_t dstride;        // descriptor slots per (parity, tile) list (>= owned neurons)
+    uint32_t *dcount;        // [3] descriptors per list of step t at dcount[t % 3]
     // G = 1 tile-pair exchange (SimArgs::xbuf != nullptr): chunk (bt, g, r) of parity p holds
     // the concatenated segments, for target tile bt, of the step's spikes of source tile g
     // with receptor r; xoff[(bt*NT + g)*2 + r] is its start (static capacity from the

@@ -8,7 +8,7 @@
 namespace spice {
 
 // ---- step kernels (sim.cu) ----
-size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions);
+size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions, uint32_t desc_cap);
 size_t plastic_smem_bytes(uint32_t tile_width, uint32_t n_regions);
 size_t xchg_kernel_smem_bytes(uint32_t tile_width, uint32_t n_tiles);
 cudaError_t launch_xcap(const SimArgs &a, uint32_t *cap, cudaStream_t s);
@@ -28,13 +28,20 @@ struct GenRule {
 struct GenGeom {
     uint32_t N, n_own, rank, G, S, TW, NT;
     uint32_t key0, key1;
+    uint32_t pad8;       // pad every (row, tile) segment to a multiple of 8 entries
 };
 // Count segment lengths cnt[s*(NT+1)+b] (+=) for one rule.
 cudaError_t gen_count(const GenGeom &g, const GenRule &r, uint32_t *cnt, cudaStream_t s);
 // cnt -> bnd (exclusive prefix within each row, in place; element NT = row length) and
 // row_ptr (exclusive prefix over rows).  Returns nnz through *nnz (synchronises).
+// Padded layout (g.pad8): bnd/row_ptr over padded lengths, true row lengths into deg[N].
 cudaError_t gen_scan(const GenGeom &g, uint32_t *cnt_bnd, uint64_t *row_ptr, uint64_t *nnz,
-                     cudaStream_t s);
+                     uint32_t *deg, cudaStream_t s);
+// Sentinel offsets in the padding of every segment (cursor = true segment lengths).
+cudaError_t gen_pad_segments(const GenGeom &g, const uint64_t *row_ptr, const uint32_t *bnd,
+                             const uint32_t *cursor, uint16_t *ent, cudaStream_t s);
+// Sum of n u32 values (synchronises).
+cudaError_t gen_sum_u32(const uint32_t *x, uint64_t n, uint64_t *out_host, cudaStream_t s);
 // Fill the entries of one rule; cursor[s*(NT+1)+b] counts entries already written.
 cudaError_t gen_fill(const GenGeom &g, const GenRule &r, const uint64_t *row_ptr,
                      const uint32_t *bnd, uint32_t *cursor, uint16_t *ent, cudaStream_t s);

@@ -76,6 +76,7 @@ def lib():
         "spice_info": (st, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32), C.POINTER(u32),
                             C.POINTER(u32), C.POINTER(u64)]),
         "spice_kernels_per_step": (u32, [vp]),
+        "spice_debug_phases": (st, [vp, vp, u64, C.POINTER(u64)]),
         "spice_profile": (st, [vp, u64, vp, u32, C.POINTER(u32)]),
         "spice_last_error": (C.c_char_p, []),
         "spice_nccl_unique_id": (st, [vp]),
@@ -275,6 +276,17 @@ class Network:
         nk = C.c_uint32()
         _check(lib().spice_profile(self.h, n_steps, out.ctypes.data, 4, C.byref(nk)))
         return {"update": out[0], "deliver": out[1], "fused": out[2], "exchange": out[3]}
+
+    def debug_phases(self) -> np.ndarray:
+        """SPICE_PHASES=1 diagnostics: (CTAs, 16) accumulated phase clocks (see spice.h)."""
+        n = C.c_uint64()
+        st = lib().spice_debug_phases(self.h, None, 0, C.byref(n))
+        if st not in (OK, ETRUNC):
+            _check(st)
+        out = np.zeros(max(1, n.value), dtype=np.uint64)
+        if n.value:
+            _check(lib().spice_debug_phases(self.h, out.ctypes.data, out.size, C.byref(n)))
+        return out[: n.value].reshape(-1, 16)
 
     def kernels_per_step(self) -> int:
         return lib().spice_kernels_per_step(self.h)
