@@ -137,6 +137,8 @@ struct spice_net {
     uint64_t *sl_rows = nullptr;
     uint64_t *desc = nullptr;
     uint32_t *dcount = nullptr;
+    uint32_t *wl = nullptr, *wcount = nullptr;   // window lists (default G = 1 delivery)
+    uint64_t wstride = 0;
     // tile-pair exchange (G = 1)
     uint16_t *xbuf = nullptr;
     uint64_t *xoff = nullptr;
@@ -351,6 +353,16 @@ __global__ void indegree_kernel(const uint64_t *row_ptr, const uint32_t *bnd, co
         }
     }
 }
+// Windows per destination tile summed over all rows (capacity of the tile's window list).
+__global__ void tile_windows_kernel(const uint32_t *bnd, uint32_t N, uint32_t NT, unsigned long long *tw) {
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < (uint64_t)N * NT;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = (uint32_t)(w / NT), b = (uint32_t)(w % NT);
+        const uint32_t *bp = bnd + (uint64_t)s * (NT + 1) + b;
+        const uint32_t nw = (bp[1] - bp[0]) >> 3;
+        if (nw) atomicAdd(&tw[b], (unsigned long long)nw);
+    }
+}
 __global__ void max_halves_kernel(const uint32_t *deg, uint64_t n, uint32_t *out) {
     uint32_t me = 0, mi = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -389,7 +401,7 @@ spice_status generate(spice_net *n) {
     if (n->pad8 && (st = dalloc_t(n, &n->deg, n->N, "out-degrees"))) return st;
     CU(n, gen_scan(g, n->bnd, n->row_ptr, &nnz, n->deg, n->stream));
     n->nnz = nnz;
-    if (n->pad8 && nnz / 8 >= (1ull << 32))
+    if (n->pad8 && nnz / 8 >= (1ull << 31) - 1)
         return fail(n, SPICE_EINVAL, "%llu synapse windows per rank exceed the 32-bit window index", (unsigned long long)(nnz / 8));
     if ((st = dalloc_t(n, &n->ent_alloc, (size_t)nnz + 2 * kEntPad, "synapse entries"))) return st;
     n->ent = n->ent_alloc + kEntPad;
@@ -654,12 +666,34 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         }
     }
     // descriptor transposition path (G = 1 without the exchange)
-    if (n->pad8 && !n->xbuf &&
-        (st = dalloc_t(n, &n->desc, 2ull * n->NT * ((n->n_own + 1) & ~1ull), "segment descriptors"))) return bail(st);
-    if (n->desc) {
+    // padded-layout delivery structures (G = 1): per-tile segment-descriptor lists consumed
+    // through per-warp window rings (default), or per-tile window lists written by the
+    // producers (SPICE_WLIST=1; measured slower: the window writes cost the producer more
+    // than the consumer saves, DESIGN.md delivery log)
+    const bool segdesc = !(getenv("SPICE_WLIST") && atoi(getenv("SPICE_WLIST")));
+    if (n->pad8 && !n->xbuf && segdesc) {
+        if ((st = dalloc_t(n, &n->desc, 2ull * n->NT * ((n->n_own + 1) & ~1ull), "segment descriptors"))) return bail(st);
         if ((st = dalloc_t(n, &n->dcount, 4, "descriptor counters"))) return bail(st);
         CU(n, cudaMemset(n->dcount, 0, 16));
+    } else if (n->pad8 && !n->xbuf) {
+        unsigned long long *tw = nullptr;
+        if ((st = dalloc_t(n, &tw, n->NT, "tile windows"))) return bail(st);
+        CU(n, cudaMemsetAsync(tw, 0, n->NT * 8ull, s));
+        tile_windows_kernel<<<n->n_sm * 8, 256, 0, s>>>(n->bnd, n->N, n->NT, tw);
+        std::vector<unsigned long long> h(n->NT);
+        CU(n, cudaMemcpyAsync(h.data(), tw, n->NT * 8ull, cudaMemcpyDeviceToHost, s));
+        CU(n, cudaStreamSynchronize(s));
+        dfree(n, tw);
+        n->device_bytes -= n->NT * 8ull;
+        uint64_t mx = 0;
+        for (unsigned long long x : h) mx = std::max<uint64_t>(mx, x);
+        if (mx >= 0xFFFFFFFFull) return bail(fail(n, SPICE_EINVAL, "%llu windows into one tile exceed the 32-bit list index", (unsigned long long)mx));
+        n->wstride = (mx + 3) & ~3ull;
+        if ((st = dalloc_t(n, &n->wl, std::max<uint64_t>(2ull * n->NT * n->wstride, 4), "window lists"))) return bail(st);
+        if ((st = dalloc_t(n, &n->wcount, 3ull * n->NT, "window counters"))) return bail(st);
+        CU(n, cudaMemset(n->wcount, 0, 3ull * n->NT * 4));
     }
+    if (n->G == 1 && !n->desc && !n->wl && !n->xbuf) n->fused = false;   // unpadded G = 1 (SPICE_NOPAD)
     // ---- kernel arguments ----
     SimArgs &a = n->args;
     a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D;
@@ -682,6 +716,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.v = n->v; a.ge = n->ge; a.gi = n->gi; a.ref = n->ref; a.acc = n->acc; a.ring = n->ring;
     a.sl_ids = n->sl_ids; a.sl_rows = n->sl_rows; a.sl_counts = n->sl_counts; a.desc = n->desc;
     a.dstride = (n->n_own + 1) & ~1ull; a.dcount = n->dcount;
+    a.wl = n->wl; a.wstride = n->wstride; a.wcount = n->wcount;
     a.xbuf = n->xbuf; a.xoff = n->xoff; a.xcnt = n->xcnt; a.xtotal = n->xtotal; a.xrows_bytes = kXRowsBytes; a.record = n->record; a.sendbuf = n->sendbuf;
     a.gather = n->gather; a.fired_cta = n->fired_cta; a.delivered_cta = n->delivered_cta;
     a.t0 = n->t0; a.force_bits = n->force_bits; a.force_ctl = n->force_ctl;

@@ -521,6 +521,80 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
     return dsum;                                       // valid in warp 0
 }
 
+// Window lists (G = 1, padded layout; the default delivery path).  For every destination
+// tile bb the step's spikes contribute one u32 per 16-byte window of their segment:
+// wl[(par*NT + bb)*wstride + i] = window index (bits 0-30) | inh (bit 31).  This CTA's n
+// spikes: one pass loads their bnd rows, row starts and out-degrees (cp.async, all in
+// flight at once); per tile a warp sums the windows, one thread per tile reserves a range
+// of the tile's list with an atomic on wcount[t % 3][bb] (all tiles at once), then every
+// warp writes its tiles' windows (lane = spike, exclusive scan of the window counts).
+__device__ __forceinline__ uint64_t write_windows(const SimArgs &a, uint64_t t, uint32_t b, uint32_t n,
+                                  const uint32_t *region, uint64_t *region_rows, uint32_t *stage,
+                                  bool marks = false) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t rowlen = a.NT + 1u;
+    const uint32_t CH = max(1u, ((uint32_t)kStageWords - 2u * a.NT - 2u) / (rowlen + 3u));
+    uint64_t *srow = reinterpret_cast<uint64_t *>(stage + CH * rowlen + (CH * rowlen & 1u));
+    uint32_t *sdeg = reinterpret_cast<uint32_t *>(srow + CH);
+    uint32_t *stot = sdeg + CH;                        // [NT] windows per tile, then offsets
+    uint32_t *wc = a.wcount + (t % 3) * a.NT;
+    uint64_t dsum = 0;
+    for (uint32_t q0 = 0; q0 < n; q0 += CH) {
+        const uint32_t nq = min(CH, n - q0);
+        __syncthreads();
+        for (uint32_t ql = warp; ql < nq; ql += kBlock / 32) {            // one warp per spike row
+            const uint32_t s = region[q0 + ql];
+            const uint32_t *row = a.bnd + (uint64_t)s * rowlen;
+            for (uint32_t bb = lane; bb < rowlen; bb += 32)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(stage + ql * rowlen + bb)), "l"(row + bb) : "memory");
+            if (lane == 0) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(srow + ql)), "l"(a.row_ptr + s) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(sdeg + ql)), "l"(a.deg + s) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (marks) phase_mark(a, 10);
+        if (warp == 0)
+            for (uint32_t ql = lane; ql < nq; ql += 32) { region_rows[q0 + ql] = srow[ql]; dsum += sdeg[ql]; }
+        for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {           // windows per tile
+            uint32_t w = 0;
+            for (uint32_t ql = lane; ql < nq; ql += 32) w += (stage[ql * rowlen + bb + 1] - stage[ql * rowlen + bb]) >> 3;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
+            if (lane == 0) stot[bb] = w;
+        }
+        __syncthreads();
+        for (uint32_t bb = threadIdx.x; bb < a.NT; bb += kBlock)            // reserve (one round trip)
+            stot[bb] = stot[bb] ? atomicAdd(wc + bb, stot[bb]) : 0u;
+        __syncthreads();
+        if (marks) phase_mark(a, 11);
+        for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
+            uint32_t *dst = a.wl + ((uint64_t)par * a.NT + bb) * a.wstride + stot[bb];
+            uint32_t carry = 0;
+            for (uint32_t j0 = 0; j0 < nq; j0 += 32) {
+                const uint32_t ql = j0 + lane;
+                uint32_t nw = 0, w0 = 0, inh = 0;
+                if (ql < nq) {                           // padded: rs, lo, hi are multiples of 8
+                    const uint32_t lo = stage[ql * rowlen + bb], hi = stage[ql * rowlen + bb + 1];
+                    nw = (hi - lo) >> 3;
+                    w0 = (uint32_t)((srow[ql] + lo) >> 3);
+                    inh = region[q0 + ql] >= a.n_exc ? 0x80000000u : 0u;
+                }
+                const uint32_t incl = warp_incl_scan(nw);
+                const uint32_t pos = carry + incl - nw;
+                for (uint32_t k = 0; k < nw; ++k) dst[pos + k] = (w0 + k) | inh;
+                carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xFFFFFFFFu, dsum, o);
+    __syncthreads();
+    return dsum;                                       // valid in warp 0
+}
+
 template <int MODEL>
 __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, const uint32_t *cnt,
                             bool write_list, uint32_t *s_count, uint32_t *stage, uint32_t *xsm = nullptr,
@@ -597,7 +671,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
         if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
         a.fired_cta[b] += n_tile;
     }
-    if (write_list && !a.desc) {                          // row starts of the spikes, all at once
+    if (write_list && !a.desc && !a.wl) {                 // row starts of the spikes, all at once
         uint32_t dsum = 0;                                // (the descriptor pass loads them itself)
         for (uint32_t q = tid; q < n_tile; q += kBlock) {
             const uint32_t s = region[q];
@@ -625,9 +699,10 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a.ent + lo), "r"((uint32_t)(hi - lo) * 2u) : "memory");
         }
     }
-    if (write_list && a.desc && !(a.dbg & 4u)) {          // padded layout: delivered events are
-        const uint64_t dsum = write_descriptors(a, t, b, n_tile, region, region_rows, stage);
-        if (tid == 0 && dsum) a.delivered_cta[b] += dsum;   // counted here from the out-degrees
+    if (write_list && (a.desc || a.wl) && !(a.dbg & 4u)) {   // padded layout: delivered events
+        const uint64_t dsum = a.wl ? write_windows(a, t, b, n_tile, region, region_rows, stage, marks)
+                                   : write_descriptors(a, t, b, n_tile, region, region_rows, stage);
+        if (tid == 0 && dsum) a.delivered_cta[b] += dsum;   // are counted here (out-degrees)
     }
     if (marks) phase_mark(a, 9);
     if constexpr (MODEL != 3) {
@@ -759,6 +834,7 @@ __device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t 
     const uint64_t *dlist = a.desc + ((uint64_t)par * a.NT + b) * a.dstride + c;   // visit v -> dlist[v * C]
     const uint4 *ent4 = reinterpret_cast<const uint4 *>(a.ent);
     uint4 *buf = wbuf + warp * (S * 32);
+    (void)ent4; (void)buf;
     // The warp's descriptors [v0, v1) are copied into shared memory first (8-byte
     // cp.async, one memory latency for the whole walk) when the CTA's visits fit.
     const bool dsmem = my <= a.dcap;
@@ -809,6 +885,9 @@ __device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t 
         done = true;
     };
     uint32_t qs[S];                                    // per stage: q of this lane's window (0: none)
+#if SPICE_DIRECT
+    uint4 vw[S];                                       // per stage: the window itself (registers)
+#endif
     uint32_t live = 0;                                 // warp-uniform: stages holding a round
     auto issue = [&](int s) {
         if (!done && r0 >= T) next_group();
@@ -824,18 +903,29 @@ __device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t 
             if (w < T) {
                 q = (inhm >> lo) & 1u ? 65536u : 1u;
                 if (!(a.dbg & 2u)) {
+#if SPICE_DIRECT
+                    const uint32_t wx = (a.dbg & 16u) ? ((wi + (w - plo)) & 0x3FFFFu) : (wi + (w - plo));   // dbg 16: L2-resident
+                    vw[s] = ld_stream_v4(a.ent + 8ull * wx);
+#else
                     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf + s * 32 + lane);
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(ent4 + (wi + (w - plo))) : "memory");
+#endif
                 }
             }
             r0 += 32;
             live |= 1u << s;
         }
         qs[s] = q;
+#if !SPICE_DIRECT
         asm volatile("cp.async.commit_group;" ::: "memory");
+#endif
     };
     auto process = [&](int s) {
+#if SPICE_DIRECT
+        if (qs[s] && !(a.dbg & 3u)) accumulate_window(cnt_s, vw[s], qs[s]);
+#else
         if (qs[s] && !(a.dbg & 3u)) accumulate_window(cnt_s, buf[s * 32 + lane], qs[s]);
+#endif
         live &= ~(1u << s);
     };
 #pragma unroll
@@ -845,7 +935,9 @@ __device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t 
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             issue((s + S - 1) % S);
+#if !SPICE_DIRECT
             asm volatile("cp.async.wait_group %0;" :: "n"(S - 1) : "memory");
+#endif
             process(s);
             if (done && live == 0) { fin = true; break; }
         }
@@ -855,6 +947,158 @@ __device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t 
     __syncthreads();
     if (marks) phase_mark(a, 5);
     return 0u;                                         // delivered events: counted at the source
+}
+
+// Ring delivery (G = 1, padded layout; default).  Consumes the segment-descriptor lists of
+// write_descriptors (one 8-byte descriptor per spike x tile, cheap to produce) but streams
+// windows like a window list: each warp expands its segment descriptors, 32 at a time,
+// into a per-warp shared-memory ring of window entries (window index | inh << 31; each
+// lane stores its own segment's windows at its exclusive-prefix position), then consumes
+// the ring 64 entries per iteration with lane L taking entries L and L + 32 (consecutive
+// windows of a segment sit in one load instruction and coalesce into one L1 line lookup),
+// the next iteration's two window loads in flight while the current windows are reduced.
+constexpr uint32_t kRing = 512;                        // ring entries per warp (power of 2)
+__device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+                                                  uint32_t *cnt, uint32_t *ring_base, bool marks = false) {
+    constexpr uint32_t NW = kBlock / 32;
+    constexpr uint32_t NONE = 0xFFFFFFFFu;
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
+    __shared__ uint32_t s_total;
+    if (tid == 0) {
+        s_total = a.dcount[t % 3];
+        if (b == 0 && c == 0) a.dcount[(t + 2) % 3] = 0u;     // next user: step t + 2's producers
+    }
+    __syncthreads();
+    if (marks) phase_mark(a, 2);
+    const uint32_t n_sp = s_total;
+    const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
+    const uint32_t v0 = (uint32_t)((uint64_t)my * warp / NW), v1 = (uint32_t)((uint64_t)my * (warp + 1) / NW);
+    const uint64_t *dlist = a.desc + ((uint64_t)par * a.NT + b) * a.dstride + c;   // visit v -> dlist[v * C]
+    uint32_t *ring = ring_base + warp * kRing;
+    auto dload = [&](uint32_t vb) -> uint64_t {
+        const uint32_t v = vb + lane;
+        return v < v1 ? dlist[(uint64_t)v * a.C] : 0ull;
+    };
+    if (marks) phase_mark(a, 3);
+    uint32_t gnext = v0;
+    uint64_t dn = dload(v0);
+    uint32_t w0 = 0, nw = 0, inh = 0, pre = 0, T = 0, c0 = 0;   // current group, c0 = expanded
+    uint32_t head = 0, tail = 0;                                // ring cursors (warp-uniform)
+    auto fill = [&](uint32_t want) {                            // expand until >= want queued
+        while (tail - head < want) {
+            if (c0 >= T) {
+                if (gnext >= v1) break;
+                const uint64_t d = dn;
+                gnext += 32;
+                dn = dload(gnext);
+                nw = (uint32_t)(d >> 32) & 0x7FFFFFFFu;
+                w0 = (uint32_t)d;
+                inh = (uint32_t)(d >> 63) << 31;
+                const uint32_t incl = warp_incl_scan(nw);
+                pre = incl - nw;
+                T = __shfl_sync(FULL, incl, 31);
+                c0 = 0;
+                continue;
+            }
+            const uint32_t take = min(T - c0, kRing - (tail - head));
+            const uint32_t klo = c0 > pre ? c0 - pre : 0u;
+            const uint32_t khi = min(pre + nw, c0 + take);
+            for (uint32_t k = klo; pre + k < khi; ++k)
+                ring[(tail + pre + k - c0) & (kRing - 1)] = (w0 + k) | inh;
+            tail += take;
+            c0 += take;
+        }
+        __syncwarp();
+    };
+    auto entry = [&](uint32_t x) -> uint32_t { return x < tail ? ring[x & (kRing - 1)] : NONE; };
+    auto load_win = [&](uint32_t e) -> uint4 {
+        if (e == NONE || (a.dbg & 2u)) return make_uint4(0, 0, 0, 0);
+        uint32_t wx = e & 0x7FFFFFFFu;
+        if (a.dbg & 16u) wx &= 0x3FFFFu;                       // diagnostics: L2-resident
+        return ld_stream_v4(a.ent + 8ull * wx);
+    };
+    fill(64);
+    uint32_t ea = entry(head + lane), eb = entry(head + 32 + lane);
+    uint4 va = load_win(ea), vb = load_win(eb);
+    head = min(head + 64, tail);
+    while (__any_sync(FULL, ea != NONE)) {
+        __syncwarp();
+        fill(64);
+        const uint32_t xa = entry(head + lane), xb = entry(head + 32 + lane);
+        const uint4 na = load_win(xa), nb = load_win(xb);
+        head = min(head + 64, tail);
+        if (!(a.dbg & 3u)) {
+            if (ea != NONE) accumulate_window(cnt_s, va, (ea >> 31) ? 65536u : 1u);
+            if (eb != NONE) accumulate_window(cnt_s, vb, (eb >> 31) ? 65536u : 1u);
+        }
+        ea = xa; eb = xb; va = na; vb = nb;
+    }
+    if (marks) phase_mark(a, 4);
+    __syncthreads();
+    if (marks) phase_mark(a, 5);
+}
+
+// Window-list delivery (G = 1, padded layout; default).  The tile's list of step t holds
+// wcount[t % 3][b] windows; the CTA's share is cut into super-rounds of 64 windows, split
+// evenly over its warps.  Per super-round a lane takes windows x = lane and x = 32 + lane:
+// two coalesced list-entry loads, two 16-byte window loads, sixteen red.shared.add.
+// Software pipeline: list entries two super-rounds ahead, windows one ahead (registers).
+__device__ __forceinline__ void deliver_tile_wl(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+                                                uint32_t *cnt, bool marks = false) {
+    constexpr uint32_t NW = kBlock / 32;
+    constexpr uint32_t NONE = 0xFFFFFFFFu;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
+    __shared__ uint32_t s_total;
+    if (tid == 0) {
+        s_total = a.wcount[(t % 3) * a.NT + b];
+        if (c == 0) a.wcount[((t + 2) % 3) * a.NT + b] = 0u;   // next user: step t + 2's producers
+    }
+    __syncthreads();
+    if (marks) phase_mark(a, 2);
+    const uint32_t total = s_total;
+    const uint32_t nsr = (total + 63u) / 64u;                  // super-rounds of the tile
+    const uint32_t c0 = (uint32_t)((uint64_t)nsr * c / a.C), c1 = (uint32_t)((uint64_t)nsr * (c + 1) / a.C);
+    const uint32_t s0 = c0 + (uint32_t)((uint64_t)(c1 - c0) * warp / NW);
+    const uint32_t s1 = c0 + (uint32_t)((uint64_t)(c1 - c0) * (warp + 1) / NW);
+    const uint32_t *list = a.wl + ((uint64_t)par * a.NT + b) * a.wstride;
+    auto load_wd = [&](uint32_t sr) -> uint2 {        // lane: windows 64 sr + lane, + 32 + lane
+        uint2 d = make_uint2(NONE, NONE);              // (consecutive windows in one instruction
+        if (sr < s1) {                                 //  coalesce within a segment's lines)
+            const uint32_t x = sr * 64u + lane;
+            if (x < total) d.x = list[x];
+            if (x + 32u < total) d.y = list[x + 32u];
+        }
+        return d;
+    };
+    auto load_win = [&](uint32_t d) -> uint4 {
+        if (d == NONE || (a.dbg & 2u)) return make_uint4(0, 0, 0, 0);
+        uint32_t wx = d & 0x7FFFFFFFu;
+        if (a.dbg & 16u) wx &= 0x3FFFFu;                       // diagnostics: L2-resident
+        return ld_stream_v4(a.ent + 8ull * wx);
+    };
+    if (marks) phase_mark(a, 3);
+    uint2 d1 = load_wd(s0), d2 = load_wd(s0 + 1);
+    uint4 va = load_win(d1.x), vb = load_win(d1.y);
+    for (uint32_t sr = s0; sr < s1; ++sr) {
+        const uint2 d0 = d1;
+        const uint4 wa = va, wb = vb;
+        d1 = d2;
+        d2 = load_wd(sr + 2);
+        va = load_win(d1.x);
+        vb = load_win(d1.y);
+        if (!(a.dbg & 3u)) {
+            if (d0.x != NONE) accumulate_window(cnt_s, wa, (d0.x >> 31) ? 65536u : 1u);
+            if (d0.y != NONE) accumulate_window(cnt_s, wb, (d0.y >> 31) ? 65536u : 1u);
+        }
+    }
+    if (marks) phase_mark(a, 4);
+    __syncthreads();
+    if (marks) phase_mark(a, 5);
 }
 
 // ------------------------------------------------------------- Brunel+ STDP
@@ -986,7 +1230,9 @@ __device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot,
 
 // Delivery shared memory: wbuf | cnt [TW + kDummy] | big [max(kStageWords, 2 dcap)] | pref | tmp
 __host__ __device__ inline uint32_t big_words(uint32_t dcap) {
-    return (uint32_t)kStageWords > 2u * dcap ? (uint32_t)kStageWords : 2u * dcap;
+    uint32_t w = (uint32_t)kStageWords > 2u * dcap ? (uint32_t)kStageWords : 2u * dcap;
+    const uint32_t ring = (kBlock / 32) * kRing;               // deliver_tile_ring's rings
+    return w > ring ? w : ring;
 }
 __device__ __forceinline__ DeliverSmem carve(const SimArgs &a, uint32_t *smem) {
     DeliverSmem sm;
@@ -1064,7 +1310,8 @@ __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
     const uint32_t b = blockIdx.x / a.C, c = blockIdx.x % a.C;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
     uint32_t d;
-    if (a.desc) { __syncthreads(); d = deliver_tile_win(a, t, b, c, sm.cnt, sm.pref, sm.tmp, sm.wbuf, sm.dsm); }
+    if (a.wl) { __syncthreads(); deliver_tile_wl(a, t, b, c, sm.cnt); d = 0; }
+    else if (a.desc) { __syncthreads(); deliver_tile_ring(a, t, b, c, sm.cnt, sm.stage); d = 0; }
     else d = deliver_tile<GS>(a, t, b, c, sm);
     uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
     if (a.C == 1u) {
@@ -1155,7 +1402,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
     __syncthreads();
     phase_mark(a, 1);
-    deliver_tile_win(a, t, b, 0, sm.cnt, sm.pref, sm.tmp, sm.wbuf, sm.dsm, true);
+    if (a.wl) deliver_tile_wl(a, t, b, 0, sm.cnt, true);
+    else deliver_tile_ring(a, t, b, 0, sm.cnt, sm.stage, true);
     phase_mark(a, 6);
     if (a.delay == 1) {
         update_tile<MODEL>(a, t + 1, b, sm.cnt, true, &s_count, sm.stage, nullptr, nullptr, true);

@@ -17,6 +17,9 @@ enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFi
 #ifndef SPICE_STAGES
 #define SPICE_STAGES 2
 #endif
+#ifndef SPICE_DIRECT
+#define SPICE_DIRECT 1          // delivery windows straight into registers (0: cp.async via smem)
+#endif
 constexpr int kBlock = SPICE_KBLOCK;  // threads per tile CTA (update / deliver / fused)
 constexpr int kStages = SPICE_STAGES; // cp.async window stages per warp in delivery
 constexpr uint32_t kDescSmem = 8192;  // default descriptor staging capacity per CTA (64 KiB)
@@ -91,7 +94,8 @@ struct SimArgs {
     uint32_t dcap;           // descriptors a delivering CTA stages in shared memory
     unsigned long long *ptimes;   // diagnostics (SPICE_PHASES=1): per CTA [16] phase clocks
     uint32_t dbg;            // diagnostics only (SPICE_DEBUG_MODE): bit0 no smem reductions,
-                             // bit1 no synapse loads, bit2 no descriptor writes
+                             // bit1 no synapse loads, bit2 no descriptor writes, bit4 window
+                             // addresses folded into 4 MB (L2-resident; wrong results)
     ModelConst mc;
     // connectivity
     const uint64_t *row_ptr; // [N+1]
@@ -114,6 +118,9 @@ struct SimArgs {
     // spike of the step restricted to tile b (list order = producer arrival order)
     uint64_t *desc;
     uint64_t dstride;        // descriptor slots per (parity, tile) list (>= owned neurons)
+    uint32_t *wl;            // window lists (default G = 1 path, see write_windows)
+    uint64_t wstride;        // entries per (parity, tile) window list (>= the tile's windows)
+    uint32_t *wcount;        // [3][NT] windows per list of step t at wcount[t % 3]
     uint32_t *dcount;        // [3] descriptors per list of step t at dcount[t % 3]
     // G = 1 tile-pair exchange (SimArgs::xbuf != nullptr): chunk (bt, g, r) of parity p holds
     // the concatenated segments, for target tile bt, of the step's spikes of source tile g

@@ -12,7 +12,7 @@ from paper_2102_04681_b200 import spice as S  # noqa: E402
 
 NAMES = {1: "counters zeroed", 2: "region prefix", 3: "descriptors staged", 4: "warp0 delivered",
          5: "delivery barrier", 6: "delivered stat", 7: "update loop", 8: "spike rows",
-         9: "descriptors written", 12: "end"}
+         10: "(prod) rows loaded", 11: "(prod) reserved", 9: "descriptors written", 12: "end"}
 which = sys.argv[1] if len(sys.argv) > 1 else "synth"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
 cfg, _ = bench.workload(which, 1)
