@@ -693,7 +693,8 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         if ((st = dalloc_t(n, &n->wcount, 3ull * n->NT, "window counters"))) return bail(st);
         CU(n, cudaMemset(n->wcount, 0, 3ull * n->NT * 4));
     }
-    if (n->G == 1 && !n->desc && !n->wl && !n->xbuf) n->fused = false;   // unpadded G = 1 (SPICE_NOPAD)
+    if (n->G == 1 && n->model != SPICE_BRUNEL_PLUS && !n->desc && !n->wl && !n->xbuf)
+        n->fused = false;                                  // unpadded G = 1 (SPICE_NOPAD)
     // ---- kernel arguments ----
     SimArgs &a = n->args;
     a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D;

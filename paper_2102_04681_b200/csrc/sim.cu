@@ -1123,11 +1123,68 @@ __device__ __forceinline__ bool plastic_edge(const SimArgs &a, uint32_t s, uint3
     return false;
 }
 
-__device__ __forceinline__ void potentiate_tile(const SimArgs &a, uint64_t t, uint32_t b) {
+// (i) potentiation.  The tile's post spikes of step t are gathered into a shared list
+// with the start of their in-synapse index ranges and an exclusive prefix of their
+// in-degrees; the flat (spike, in-synapse) index space is then spread over all threads,
+// U independent synapses per thread with every load issued before the stores (a synapse
+// is touched at most once per step, so the read-modify-writes never conflict).  Falls
+// back to one warp per bitmap word when the list does not fit the staging area.
+__device__ __forceinline__ void potentiate_tile(const SimArgs &a, uint64_t t, uint32_t b,
+                                                uint32_t *stage, uint32_t *tmp) {
+    constexpr int U = 4;
     const uint32_t *bm = step_bitmap(a, t);
     const float *x = a.xtr + (t & 1) * (uint64_t)a.N;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lo = b * a.TW, hi = min(lo + a.TW, a.n_own);
+    const uint32_t cap = ((uint32_t)kStageWords - 2u) / 4u;
+    uint64_t *base = reinterpret_cast<uint64_t *>(stage);      // [cap] in-synapse range starts
+    uint32_t *pre = stage + 2 * cap;                            // [cap + 1] in-degree prefix
+    __shared__ uint32_t s_np;
+    if (tid == 0) s_np = 0;
+    __syncthreads();
+    for (uint32_t wi = lo / 32 + tid; wi < (hi + 31) / 32; wi += kBlock) {
+        uint32_t word = bm[wi];
+        while (word) {
+            const uint32_t i = wi * 32 + __ffs(word) - 1;
+            word &= word - 1;
+            const uint32_t k = atomicAdd(&s_np, 1u);
+            if (k < cap) { base[k] = a.in_ptr[i]; pre[k] = (uint32_t)(a.in_ptr[i + 1] - a.in_ptr[i]); }
+        }
+    }
+    __syncthreads();
+    const uint32_t np = s_np;
+    if (np == 0) return;
+    if (np <= cap) {
+        block_exclusive_scan(pre, np, tmp);
+        const uint32_t total = pre[np];
+        for (uint32_t f0 = tid; f0 < total; f0 += kBlock * U) {
+            uint64_t pos[U];
+            uint32_t src[U];
+            bool ok[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t f = f0 + u * kBlock;
+                ok[u] = f < total;
+                if (ok[u]) {
+                    uint32_t l = 0, h = np;                     // largest k with pre[k] <= f
+                    while (h - l > 1) { const uint32_t m = (l + h) >> 1; if (pre[m] <= f) l = m; else h = m; }
+                    const uint64_t e = base[l] + (f - pre[l]);
+                    pos[u] = a.in_pos[e];
+                    src[u] = a.in_src[e];
+                }
+            }
+            float wv[U], xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) if (ok[u]) { wv[u] = a.w[pos[u]]; xv[u] = x[src[u]]; }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (ok[u]) {
+                    const float nw = __fadd_rn(wv[u], __fmul_rn(a.mc.Ap, xv[u]));
+                    a.w[pos[u]] = nw < a.mc.wmax ? nw : a.mc.wmax;
+                }
+        }
+        return;                                              // (the caller's barrier orders (i) before (ii))
+    }
     for (uint32_t wi = lo / 32 + warp; wi < (hi + 31) / 32; wi += kBlock / 32) {
         uint32_t word = bm[wi];
         while (word) {
@@ -1188,13 +1245,17 @@ __device__ __forceinline__ void walk_plastic(const SimArgs &a, uint32_t b, uint3
 
 template <int GS>
 __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b, uint32_t *cnt,
-                                         long long *pin, uint32_t *pref, uint32_t *tmp) {
+                                         long long *pin, uint32_t *pref, uint32_t *tmp, uint32_t *stage,
+                                         bool marks = false) {
     const uint32_t tid = threadIdx.x;
     const uint32_t par = (uint32_t)(t & 1);
-    potentiate_tile(a, t, b);
+    potentiate_tile(a, t, b, stage, tmp);
+    __syncthreads();
+    if (marks) phase_mark(a, 2);
     for (uint32_t r = tid; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
     __syncthreads();
     block_exclusive_scan(pref, a.NR, tmp);       // also orders (i) before (ii)
+    if (marks) phase_mark(a, 3);
     const uint32_t n_sp = pref[a.NR];
     const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
     uint32_t delivered = 0;
@@ -1211,7 +1272,9 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
         for (uint64_t w = (st & ~7ull) + 8u * lig; w < en; w += 8u * GS) walk_plastic(a, b, cnt, pin, w, st, en, q, s, pls);
     }
     __syncthreads();
+    if (marks) phase_mark(a, 4);
     stdp_traces(a, t, b);
+    if (marks) phase_mark(a, 5);
     return delivered;
 }
 
@@ -1345,7 +1408,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver_plastic(SimArgs a, uint32_t 
     const uint64_t t = *a.t0 + k;
     const uint32_t b = blockIdx.x;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.pin[x] = 0; }
-    const uint32_t d = deliver_tile_plastic<GS>(a, t, b, sm.cnt, sm.pin, sm.pref, sm.tmp);
+    const uint32_t d = deliver_tile_plastic<GS>(a, t, b, sm.cnt, sm.pin, sm.pref, sm.tmp, sm.stage);
     const uint64_t base = ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
         a.ring[base + x] += sm.cnt[x];
@@ -1362,9 +1425,10 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         __shared__ uint32_t s_count3;
         const uint64_t t = *a.t0 + k;
         const uint32_t b = blockIdx.x;
+        phase_mark(a, 0);
         if (threadIdx.x == 0) s_count3 = 0;
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.pin[x] = 0; }
-        const uint32_t d = deliver_tile_plastic<GS>(a, t, b, sm.cnt, sm.pin, sm.pref, sm.tmp);
+        const uint32_t d = deliver_tile_plastic<GS>(a, t, b, sm.cnt, sm.pin, sm.pref, sm.tmp, sm.stage, true);
         const uint64_t base = ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
             a.ring[base + x] += sm.cnt[x];
@@ -1372,7 +1436,9 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         }
         store_delivered(a, b, d, sm.tmp);
         __syncthreads();
-        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count3, sm.stage);
+        phase_mark(a, 6);
+        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count3, sm.stage, nullptr, nullptr, true);
+        phase_mark(a, 12);
     } else {
     extern __shared__ __align__(16) uint32_t smem[];
     DeliverSmem sm = carve(a, smem);
