@@ -704,6 +704,8 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (const char *gs = getenv("SPICE_GROUP_LANES")) a.GS = (uint32_t)atoi(gs);
     if (const char *dm = getenv("SPICE_DEBUG_MODE")) a.dbg = (uint32_t)atoi(dm);   // diagnostics only
     a.dcap = n->dcap;
+    if ((a.dbg & 32u) && n->desc &&
+        (st = dalloc_t(n, &a.dscratch, 2ull * n->NT * ((n->n_own + 1) & ~1ull), "descriptor scratch"))) return bail(st);
     if (getenv("SPICE_PHASES") && atoi(getenv("SPICE_PHASES"))) {     // diagnostics only
         if ((st = dalloc_t(n, &n->ptimes, (size_t)n->NT * n->C * 16, "phase clocks"))) return bail(st);
         CU(n, cudaMemset(n->ptimes, 0, (size_t)n->NT * n->C * 16 * 8));

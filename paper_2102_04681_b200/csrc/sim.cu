@@ -86,10 +86,11 @@ __device__ __forceinline__ StatePtrs global_state(const SimArgs &a) {
 // input counts c[4]; returns the spike nibble.  State arrays are padded to NT*TW.
 template <int MODEL>
 __device__ __forceinline__ uint32_t update4(const SimArgs &a, const StatePtrs &sp, uint64_t t, uint32_t i0,
-                                            const uint32_t c[4], const long long pin[4]) {
+                                            const uint32_t c[4], const long long pin[4],
+                                            const uint64_t *ptab, bool acc_done) {
     const uint32_t li = i0 - sp.base;                  // index into the state arrays
     const ModelConst &m = a.mc;
-    const uint32_t j0 = (uint32_t)local_to_global(i0, a.rank, a.G, a.S);   // multiple of 4
+    const uint32_t j0 = a.G == 1 ? i0 : (uint32_t)local_to_global(i0, a.rank, a.G, a.S);   // multiple of 4
     uint32_t valid = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) valid |= (i0 + e < a.n_own ? 1u : 0u) << e;
@@ -102,9 +103,11 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, const StatePtrs &s
     uint32_t spk = 0;
     if (MODEL == 4) {                                   // Synth (reading R12)
         const uint4 x = philox4x32_10(make_uint4(j0 >> 2, (uint32_t)t, 0u, kTagFire), a.key0, a.key1);
-        uint4 acc = *reinterpret_cast<const uint4 *>(sp.acc + li);
-        acc.x += c[0]; acc.y += c[1]; acc.z += c[2]; acc.w += c[3];
-        *reinterpret_cast<uint4 *>(sp.acc + li) = acc;
+        if (!acc_done) {                                // (else applied by update_tile's batched pass)
+            uint4 acc = *reinterpret_cast<const uint4 *>(sp.acc + li);
+            acc.x += c[0]; acc.y += c[1]; acc.z += c[2]; acc.w += c[3];
+            *reinterpret_cast<uint4 *>(sp.acc + li) = acc;
+        }
         spk = ((uint64_t)x.x < m.thr_fire ? 1u : 0u) | ((uint64_t)x.y < m.thr_fire ? 2u : 0u) |
               ((uint64_t)x.z < m.thr_fire ? 4u : 0u) | ((uint64_t)x.w < m.thr_fire ? 8u : 0u);
         if (forced == 1) spk = fbits; else if (forced == 2) spk |= fbits;
@@ -165,7 +168,7 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, const StatePtrs &s
             } else {
                 const uint32_t xe = word_of(x, e);
                 uint32_t next = 0;
-                while ((uint64_t)xe >= m.ptab[next]) ++next;   // min{k : x < T_k}
+                while ((uint64_t)xe >= ptab[next]) ++next;     // min{k : x < T_k}
                 const uint32_t ne = c[e] & 0xFFFFu, ni = c[e] >> 16;
                 v = __fadd_rn(v, __fmul_rn(m.h, __fsub_rn(m.EL, v)));
                 v = __fadd_rn(v, __fmul_rn(m.JE, __uint2float_rn(ne + next)));
@@ -476,7 +479,8 @@ __global__ void __launch_bounds__(kBlock) k_xcap(SimArgs a, uint32_t *cap) {
 // descriptors desc[par][bb][b][q0 .. q0+CH) with coalesced stores.  Delivery CTAs then read
 // their descriptors contiguously.  Returns (to thread 0) the spikes' delivered-event count.
 __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t t, uint32_t b, uint32_t n,
-                                  const uint32_t *region, uint64_t *region_rows, uint32_t *stage) {
+                                  const uint32_t *region, uint64_t *region_rows, uint32_t *stage,
+                                  bool marks = false) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t par = (uint32_t)(t & 1);
     // dense per-tile lists: this CTA's n descriptors go to [off, off + n) of every
@@ -504,14 +508,20 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
         }
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         __syncthreads();
+        if (marks) phase_mark(a, 10);
         if (warp == 0)
             for (uint32_t ql = lane; ql < nq; ql += 32) { region_rows[q0 + ql] = srow[ql]; dsum += sdeg[ql]; }
-        for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
-            uint64_t *dst = a.desc + ((uint64_t)par * a.NT + bb) * a.dstride + s_off + q0;
-            for (uint32_t ql = lane; ql < nq; ql += 32) {   // padded: rs, lo, hi are multiples of 8
-                const uint32_t lo = stage[ql * rowlen + bb], hi = stage[ql * rowlen + bb + 1];
-                const uint64_t inh = region[q0 + ql] >= a.n_exc ? (1ull << 63) : 0ull;
-                dst[ql] = ((srow[ql] + lo) >> 3) | ((uint64_t)((hi - lo) >> 3) << 32) | inh;
+        for (uint32_t j0 = 0; j0 < nq; j0 += 32) {          // lane = spike; per-spike values hoisted
+            const uint32_t ql = j0 + lane;
+            if (ql < nq) {                                   // padded: rs, lo, hi multiples of 8
+                const uint32_t rs8 = (uint32_t)(srow[ql] >> 3);
+                const uint32_t ih = region[q0 + ql] >= a.n_exc ? 0x80000000u : 0u;
+                const uint32_t *row = stage + ql * rowlen;
+                uint2 *dst = reinterpret_cast<uint2 *>(a.desc + (uint64_t)par * a.NT * a.dstride + s_off + q0 + ql);
+                for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
+                    const uint32_t lo = row[bb], hi = row[bb + 1];
+                    dst[(uint64_t)bb * a.dstride] = make_uint2(rs8 + (lo >> 3), ((hi - lo) >> 3) | ih);
+                }
             }
         }
     }
@@ -608,6 +618,16 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + b) * a.RS;
     uint32_t *bm = a.G == 1 ? a.record + (t % a.record_steps) * (uint64_t)a.W : a.sendbuf;
     uint32_t *ring_slot = a.ring + (t % a.D) * a.ring_stride + lo;
+    // Brunel drive: the Poisson inversion table in shared memory (the walk is a chain of
+    // dependent loads per neuron)
+    __shared__ uint64_t s_ptab[kPtabSmem];
+    const uint64_t *ptab = a.mc.ptab;
+    if ((MODEL == 2 || MODEL == 3) && a.mc.ptab_len <= kPtabSmem) {
+        for (uint32_t x = tid; x < a.mc.ptab_len; x += kBlock) s_ptab[x] = a.mc.ptab[x];
+        ptab = s_ptab;
+        __syncthreads();
+    }
+    const bool acc_done = false;
     for (uint32_t x0 = 0; x0 < span; x0 += 4u * kBlock) {      // uniform trip count per CTA
         const uint32_t x4 = x0 + 4u * tid;
         uint32_t nib = 0;
@@ -627,7 +647,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
                 c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
             }
-            nib = update4<MODEL>(a, sp, t, lo + x4, c, pin);
+            nib = update4<MODEL>(a, sp, t, lo + x4, c, pin, ptab, acc_done);
         }
         // 8 lanes x 4 bits -> one 32-neuron bitmap word
         uint32_t w = nib << (4u * (lane & 7u));
@@ -645,7 +665,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
             base = __shfl_sync(0xFFFFFFFFu, base, 0);
             if (write_list && nib) {
                 uint32_t pos = base + incl - nsp;
-                const uint32_t j0 = (uint32_t)local_to_global(lo + x4, a.rank, a.G, a.S);
+                const uint32_t j0 = a.G == 1 ? lo + x4 : (uint32_t)local_to_global(lo + x4, a.rank, a.G, a.S);
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
                     if ((nib >> e) & 1u) region[pos++] = j0 + e;
@@ -701,7 +721,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     }
     if (write_list && (a.desc || a.wl) && !(a.dbg & 4u)) {   // padded layout: delivered events
         const uint64_t dsum = a.wl ? write_windows(a, t, b, n_tile, region, region_rows, stage, marks)
-                                   : write_descriptors(a, t, b, n_tile, region, region_rows, stage);
+                                   : write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks);
         if (tid == 0 && dsum) a.delivered_cta[b] += dsum;   // are counted here (out-degrees)
     }
     if (marks) phase_mark(a, 9);

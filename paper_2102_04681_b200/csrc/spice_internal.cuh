@@ -31,6 +31,7 @@ constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
 constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list region
 constexpr int kEntPad = 64;           // u16 padding before/after the entry array
 constexpr uint32_t kDummy = 64;       // dummy counters past the tile (padding sentinels)
+constexpr uint32_t kPtabSmem = 128;   // Poisson inversion table entries staged in smem
 
 // Philox4x32-10 (Salmon et al., SC'11).  Multipliers 0xD2511F53 / 0xCD9E8D57, Weyl
 // key increments 0x9E3779B9 / 0xBB67AE85; 10 rounds.
@@ -93,6 +94,7 @@ struct SimArgs {
     uint32_t pf_rows;        // 1: TMA-prefetch spiking rows into L2 at the end of the update
     uint32_t dcap;           // descriptors a delivering CTA stages in shared memory
     unsigned long long *ptimes;   // diagnostics (SPICE_PHASES=1): per CTA [16] phase clocks
+    uint64_t *dscratch;      // diagnostics (SPICE_DEBUG_MODE bit 5): second descriptor copy
     uint32_t dbg;            // diagnostics only (SPICE_DEBUG_MODE): bit0 no smem reductions,
                              // bit1 no synapse loads, bit2 no descriptor writes, bit4 window
                              // addresses folded into 4 MB (L2-resident; wrong results)
