@@ -182,8 +182,10 @@ SPICE_API spice_status spice_info(spice_net *net, uint64_t *n_owned, uint64_t *n
 /* Run n_steps steps with each kernel launched individually and bracketed by CUDA events
  * on the library stream; writes the average device time per launch in ms:
  * [0] neuron update kernel, [1] delivery kernel, [2] fused deliver(t)+update(t+1) kernel
- * (G = 1; 0 otherwise), [3] exchange (NCCL all-gather + bitmap->list; G > 1).
- * *n_kernels = entries written (cap >= 4).  Synchronises. */
+ * (G = 1; 0 otherwise), [3] exchange (NCCL all-gather + bitmap->list; G > 1), and, when
+ * cap >= 5, [4] the fused kernel inside a captured graph of 32 back-to-back launches (the
+ * configuration spice_step runs; G = 1, 0 otherwise), timed over n_steps / 32 replays.
+ * *n_kernels = entries written (cap >= 4).  Advances the network.  Synchronises. */
 SPICE_API spice_status spice_profile(spice_net *net, uint64_t n_steps, double *ms_per_kernel,
                                      uint32_t cap, uint32_t *n_kernels);
 

@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) fill_prob_kernel(GenGeom g, GenRule r, co
             const uint32_t incl = warp_incl_scan_g(c, lane);
             uint64_t p = pos + incl - c;
             for (uint32_t e = 0; e < 4; ++e)
-                if (m >> e & 1u) ent[p++] = (uint16_t)(4u * q + e);
+                if (m >> e & 1u) ent[p++] = (uint16_t)((4u * q + e) << g.eshift);
             const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
             pos += tot;
             written += tot;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) indeg_kernel(GenGeom g, GenRule r, const 
             const uint32_t s = r.src_begin + (uint32_t)__umul64hi(r64, nsrc);
             const uint64_t seg = (uint64_t)s * (g.NT + 1) + b;
             const uint32_t slot = atomicAdd(&cnt_or_cursor[seg], 1u);
-            if (FILL) ent[row_ptr[s] + bnd[seg] + slot] = (uint16_t)(i - b * g.TW);
+            if (FILL) ent[row_ptr[s] + bnd[seg] + slot] = (uint16_t)((i - b * g.TW) << g.eshift);
         }
     }
 }
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256) pad_segments_kernel(GenGeom g, const uint
         const uint64_t base = row_ptr[s] + bnd[seg];
         const uint32_t padded = bnd[seg + 1] - bnd[seg];
         for (uint32_t e = cursor[seg]; e < padded; ++e)
-            ent[base + e] = (uint16_t)(g.TW + (((base + e) >> 3) & 63u));
+            ent[base + e] = (uint16_t)((g.TW + (((base + e) >> 3) & 63u)) << g.eshift);
     }
 }
 
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(256) plastic_kernel(GenGeom g, PlasticBoxes pb
         const uint64_t st = row_ptr[s] + bp[0];
         const uint32_t len = bp[1] - bp[0];
         for (uint32_t e = lane; e < len; e += 32) {
-            const uint32_t il = b * g.TW + ent[st + e];
+            const uint32_t il = b * g.TW + (ent[st + e] >> g.eshift);
             const bool pl = is_plastic(pb, s, (uint32_t)local_to_global(il, g.rank, g.G, g.S));
             if (MODE == 0) {
                 w[st + e] = pl ? w0 : 0.0f;

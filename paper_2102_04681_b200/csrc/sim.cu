@@ -796,12 +796,12 @@ __device__ __forceinline__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, u
 }
 
 // Eight unconditional shared-memory reductions of one padded 16-byte window (sentinel
-// entries land in the dummy counters past the tile).
+// entries land in the dummy counters past the tile).  Padded entries are byte offsets.
 __device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v, uint32_t q) {
-    const uint32_t a0 = cnt_s + ((v.x & 0xFFFFu) << 2), a1 = cnt_s + ((v.x >> 14) & ~3u);
-    const uint32_t a2 = cnt_s + ((v.y & 0xFFFFu) << 2), a3 = cnt_s + ((v.y >> 14) & ~3u);
-    const uint32_t a4 = cnt_s + ((v.z & 0xFFFFu) << 2), a5 = cnt_s + ((v.z >> 14) & ~3u);
-    const uint32_t a6 = cnt_s + ((v.w & 0xFFFFu) << 2), a7 = cnt_s + ((v.w >> 14) & ~3u);
+    const uint32_t a0 = cnt_s + (v.x & 0xFFFFu), a1 = cnt_s + (v.x >> 16);
+    const uint32_t a2 = cnt_s + (v.y & 0xFFFFu), a3 = cnt_s + (v.y >> 16);
+    const uint32_t a4 = cnt_s + (v.z & 0xFFFFu), a5 = cnt_s + (v.z >> 16);
+    const uint32_t a6 = cnt_s + (v.w & 0xFFFFu), a7 = cnt_s + (v.w >> 16);
     asm volatile(
         "red.shared.add.u32 [%0], %8;\n\t"
         "red.shared.add.u32 [%1], %8;\n\t"
@@ -1530,7 +1530,7 @@ __global__ void __launch_bounds__(kBlock) k_global_atomics(SimArgs a, uint32_t k
         const uint32_t qv = s >= a.n_exc ? 65536u : 1u;
         uint32_t *tile = slot + (uint64_t)b * a.TW;
         for (uint32_t e = lane; e < len; e += 32) {
-            const uint32_t x = a.ent[st + e];
+            const uint32_t x = (uint32_t)a.ent[st + e] >> a.eshift;
             if (x < a.TW) atomicAdd(tile + x, qv);       // skip padding sentinels
         }
         if (lane == 0 && !a.deg) delivered += len;

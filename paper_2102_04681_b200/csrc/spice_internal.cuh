@@ -32,6 +32,7 @@ constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list reg
 constexpr int kEntPad = 64;           // u16 padding before/after the entry array
 constexpr uint32_t kDummy = 64;       // dummy counters past the tile (padding sentinels)
 constexpr uint32_t kPtabSmem = 128;   // Poisson inversion table entries staged in smem
+constexpr uint32_t kMaxPadTile = 16320;   // padded layout: (TW + kDummy) * 4 must fit a u16
 
 // Philox4x32-10 (Salmon et al., SC'11).  Multipliers 0xD2511F53 / 0xCD9E8D57, Weyl
 // key increments 0x9E3779B9 / 0xBB67AE85; 10 rounds.
@@ -106,6 +107,7 @@ struct SimArgs {
     const uint32_t *deg;     // padded layout (G = 1, not Brunel+): every segment is padded to
                              // a multiple of 8 entries with sentinels >= TW (dummy counters
                              // TW .. TW+63); deg[s] = true out-degree (delivered-event count)
+    uint32_t eshift;         // entries hold (tile offset << eshift); 2 (byte offsets) when padded
     // state
     float *v, *ge, *gi;
     uint32_t *ref, *acc;

@@ -29,6 +29,7 @@ struct GenGeom {
     uint32_t N, n_own, rank, G, S, TW, NT;
     uint32_t key0, key1;
     uint32_t pad8;       // pad every (row, tile) segment to a multiple of 8 entries
+    uint32_t eshift;     // entries store (tile offset << eshift): 2 = byte offsets (padded layout)
 };
 // Count segment lengths cnt[s*(NT+1)+b] (+=) for one rule.
 cudaError_t gen_count(const GenGeom &g, const GenRule &r, uint32_t *cnt, cudaStream_t s);

@@ -272,10 +272,11 @@ class Network:
         library stream: update, deliver (unfused kernels), fused deliver(t)+update(t+1)
         (G = 1), exchange (all-gather + bitmap->list, G > 1).  Advances the network by
         2 * n_steps + 1 steps (G = 1) or n_steps steps."""
-        out = np.zeros(4, dtype=np.float64)
+        out = np.zeros(5, dtype=np.float64)
         nk = C.c_uint32()
-        _check(lib().spice_profile(self.h, n_steps, out.ctypes.data, 4, C.byref(nk)))
-        return {"update": out[0], "deliver": out[1], "fused": out[2], "exchange": out[3]}
+        _check(lib().spice_profile(self.h, n_steps, out.ctypes.data, 5, C.byref(nk)))
+        return {"update": out[0], "deliver": out[1], "fused": out[2], "exchange": out[3],
+                "fused_in_graph": out[4]}
 
     def debug_phases(self) -> np.ndarray:
         """SPICE_PHASES=1 diagnostics: (CTAs, 16) accumulated phase clocks (see spice.h)."""

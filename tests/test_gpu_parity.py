@@ -29,6 +29,8 @@ CASES = {
     "brunel1001_ragged": (W.brunel(1001, 0.2, seed=2, delay=3), dict(tile_width=64), 300),
     "synth20000": (W.synth(20000, 31, 0.005, seed=3), {}, 200),
     "synth5003_ragged_c2": (W.synth(5003, 100, 0.02, seed=4), dict(tile_width=96, ctas_per_tile=2), 150),
+    # tile wider than the padded layout allows (byte offsets in u16): unpadded generic path
+    "synth40000_wide_tile": (W.synth(40000, 31, 0.005, seed=11), dict(tile_width=16384), 60),
     "vogels_global_atomics": (W.vogels(4000, seed=9), dict(global_atomics=True), 300),
     "synth_global_atomics": (W.synth(20000, 31, 0.005, seed=8), dict(global_atomics=True), 100),
 }
@@ -197,3 +199,23 @@ def test_graph_chunks_equal_single_steps(S):
         for n in (1, 31, 33, 2, 32, 1):
             b.step(n)
         assert all(np.array_equal(x, y) for x, y in zip(a.read_spikes(0, 100), b.read_spikes(0, 100)))
+
+
+@pytest.mark.parametrize("name", ["vogels4000", "brunel3000_d15", "synth20000"])
+def test_profile_modes_keep_the_simulation_exact(S, name):
+    """spice_profile advances the network through unfused, individually launched fused and
+    graph-captured fused launches; every step must still equal the oracle's."""
+    cfg, kw, T = CASES[name]
+    o, _ = oracle_run(name)
+    want = o.spikes()
+    with S.Network(cfg, record_steps=T, **kw) as net:
+        net.step(5)
+        prof = net.profile(8)            # 8 unfused, 9 fused, 65 graph-fused steps
+        assert prof["update"] > 0 and prof["deliver"] > 0
+        assert prof["fused"] > 0 and prof["fused_in_graph"] > 0
+        done = net.stats()["steps"]
+        assert done < T
+        net.step(T - done)
+        got = net.read_spikes(0, T)
+    bad = [t for t in range(T) if not np.array_equal(got[t], want[t])]
+    assert not bad, f"first mismatching steps {bad[:5]}"
