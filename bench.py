@@ -76,6 +76,19 @@ def cpu_sample(name: str, cfg):
     return cfg, "vogels4000 (full workload)"
 
 
+def ncu_traffic(workload_name: str, delivery: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/ncu_traffic.json), when it was taken on this workload and tile geometry."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            e = json.load(f)[workload_name]
+        if e["delivery"] != delivery:
+            return None, None
+        return float(e["dram_bytes_read"] + e["dram_bytes_write"]), e["capture"]
+    except Exception:
+        return None, None
+
+
 def hbm_peak():
     try:
         with open(PEAKS_FILE) as f:
@@ -275,6 +288,9 @@ def main_spice(args):
         cpu = {"value": eps, "unit": "events/s", "cores": 1, "kind": "oracle",
                "sample": f"{desc}; {done} steps in {el:.1f} s, single thread"}
 
+    delivery = ("global-atomics (paper-style A/B)" if args.global_atomics else
+                f"tiled smem, {info['n_tiles']} tiles x {info['tile_width']} targets, {info['ctas_per_tile']} CTA/tile")
+    traffic, traffic_src = ncu_traffic(wl, delivery) if fused else (None, None)
     line = {
         "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -289,12 +305,12 @@ def main_spice(args):
                    "synapses_rank0": info["n_synapses"], "spikes_per_step": fired / args.steps,
                    "events_per_step": events / args.steps,
                    "parallelism": f"model-parallel strided neuron slices x{world}",
-                   "delivery": "global-atomics (paper-style A/B)" if args.global_atomics else
-                               f"tiled smem, {info['n_tiles']} tiles x {info['tile_width']} targets, {info['ctas_per_tile']} CTA/tile",
+                   "delivery": delivery,
                    "l2": "no flush: synapse stream per step >> 126 MB L2 is read from 12 GB/GPU",
                    "setup_s": setup_s},
         "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "bytes_per_launch": bytes_launch, "launch_ms": launch_ms,
                      "bytes_model": "SURVEY §8(d): 4 B/event + 12 B/spike (delivery bytes only)",
                      "peak_source": peak_src,

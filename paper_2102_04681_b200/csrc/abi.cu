@@ -114,7 +114,7 @@ struct spice_net {
     bool external = false;
     // geometry
     uint64_t n_own = 0, n_own_max = 0;
-    uint32_t W = 0, TW = 32, NT = 1, C = 1;
+    uint32_t W = 0, TW = 32, NT = 1, C = 1, TWs = 32;
     uint64_t ring_stride = 0;
     uint64_t nnz = 0;        // stored entries (incl. padding sentinels)
     uint64_t n_syn = 0;      // synapses (owned targets)
@@ -517,27 +517,35 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // ---- delivery tiles ----
     // padded segments + window-stream delivery: single rank, descriptor path (not Brunel+,
     // not the tile-pair exchange experiment); SPICE_NOPAD=1 keeps the unpadded layout.
-    // Padded entries are byte offsets, which caps the tile width at kMaxPadTile.
+    // Padded entries are byte offsets up to kMaxPadTile targets per tile, counter indices
+    // (one more shift per entry) up to kMaxPadTileWord.
+    // C CTAs per tile (ctas_per_tile): the tile is cut into C slices of TWs = TW / C targets
+    // (multiples of 32); CTA x updates slice x.  On the fused G = 1 path the C CTAs form a
+    // thread-block cluster that reduces the tile's counters through distributed shared memory.
+    n->C = c->ctas_per_tile ? c->ctas_per_tile : 1;
+    if (n->C > kMaxCluster) return bail(fail(n, SPICE_EINVAL, "ctas_per_tile %u > %u", n->C, kMaxCluster));
     n->pad8 = n->G == 1 && n->model != SPICE_BRUNEL_PLUS && !getenv("SPICE_XCHG") && !getenv("SPICE_NOPAD");
     if (c->tile_width) {
-        n->TW = c->tile_width;
-        if (n->TW > kMaxPadTile) n->pad8 = false;
+        const uint32_t q = 32u * n->C;
+        n->TW = (c->tile_width + q - 1) / q * q;
+        if (n->TW > kMaxPadTileWord) n->pad8 = false;
     } else {
-        const uint64_t want_tiles = (uint64_t)n->n_sm;     // one tile CTA per SM
-        uint64_t tw = (n->n_own + want_tiles - 1) / want_tiles;
-        tw = (tw + 31) / 32 * 32;
-        n->TW = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(tw, 32), n->pad8 ? kMaxPadTile : kMaxTileWidth);
+        const uint64_t want = (uint64_t)std::max(1, n->n_sm / (int)n->C) * n->C;   // one CTA per SM
+        uint64_t tws = (n->n_own + want - 1) / want;
+        tws = (tws + 31) / 32 * 32;
+        const uint64_t cap = (n->pad8 ? (n->C > 1 ? kMaxPadTileWord : kMaxPadTile) : kMaxTileWidth) / (32u * n->C) * 32u;
+        n->TW = (uint32_t)(std::min<uint64_t>(std::max<uint64_t>(tws, 32), cap) * n->C);
     }
-    n->eshift = n->pad8 ? 2u : 0u;
+    n->TWs = n->TW / n->C;
+    n->eshift = n->pad8 && n->TW <= kMaxPadTile ? 2u : 0u;
     n->NT = (uint32_t)std::max<uint64_t>(1, (n->n_own + n->TW - 1) / n->TW);
-    n->C = c->ctas_per_tile ? c->ctas_per_tile : 1;
 
     n->ring_stride = (uint64_t)n->NT * n->TW;
     n->global_atomics = (n->flags & SPICE_FLAG_GLOBAL_ATOMICS) != 0;
-    n->fused = !(n->flags & SPICE_FLAG_UNFUSED) && n->C == 1;
-    // spike-list regions: one per tile (G = 1, written by the tile's update) or one per
+    n->fused = !(n->flags & SPICE_FLAG_UNFUSED) && (n->C == 1 || n->pad8);
+    // spike-list regions: one per CTA slice (G = 1, written by the slice's update) or one per
     // kB2LWords gathered bitmap words (G > 1, written by bitmap->list)
-    if (n->G == 1) { n->NR = n->NT; n->RS = n->TW; }
+    if (n->G == 1) { n->NR = n->NT * n->C; n->RS = n->TWs; }
     else { n->NR = (uint32_t)(((uint64_t)n->G * n->W + kB2LWords - 1) / kB2LWords); n->RS = kB2LWords * 32; }
     if (n->NR > kMaxRegions) return bail(fail(n, SPICE_EINVAL, "%u spike-list regions > %u: use a wider tile_width", n->NR, kMaxRegions));
     // descriptor staging capacity: kDescSmem, shrunk (not below the update's staging area)
@@ -566,7 +574,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if ((st = dalloc_t(n, &n->record, (size_t)n->R * n->G * n->W, "spike record"))) return bail(st);
     if ((st = dalloc_t(n, &n->sendbuf, std::max<uint32_t>(n->W, 1), "send bitmap"))) return bail(st);
     if ((st = dalloc_t(n, &n->gather, (size_t)n->G * std::max<uint32_t>(n->W, 1), "gathered bitmaps"))) return bail(st);
-    if ((st = dalloc_t(n, &n->fired_cta, n->NT, "fired counters"))) return bail(st);
+    if ((st = dalloc_t(n, &n->fired_cta, nctas, "fired counters"))) return bail(st);
     if ((st = dalloc_t(n, &n->delivered_cta, nctas, "delivered counters"))) return bail(st);
     if ((st = dalloc_t(n, &n->t0, 1, "step counter"))) return bail(st);
     if ((st = dalloc_t(n, &n->force_bits, std::max<uint32_t>(n->W, 1), "force bits"))) return bail(st);
@@ -584,7 +592,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     CU(n, cudaMemsetAsync(n->sendbuf, 0, std::max<uint32_t>(n->W, 1) * 4, s));   // words past the last tile stay 0
     CU(n, cudaMemsetAsync(n->gather, 0, (size_t)n->G * std::max<uint32_t>(n->W, 1) * 4, s));
     CU(n, cudaMemsetAsync(n->record, 0, (size_t)n->R * n->G * n->W * 4, s));
-    CU(n, cudaMemsetAsync(n->fired_cta, 0, n->NT * 8ull, s));
+    CU(n, cudaMemsetAsync(n->fired_cta, 0, nctas * 8, s));
     CU(n, cudaMemsetAsync(n->delivered_cta, 0, nctas * 8, s));
     CU(n, cudaMemsetAsync(n->t0, 0, 8, s));
     CU(n, cudaMemsetAsync(n->force_bits, 0, std::max<uint32_t>(n->W, 1) * 4, s));
@@ -676,7 +684,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // through per-warp window rings (default), or per-tile window lists written by the
     // producers (SPICE_WLIST=1; measured slower: the window writes cost the producer more
     // than the consumer saves, DESIGN.md delivery log)
-    const bool segdesc = !(getenv("SPICE_WLIST") && atoi(getenv("SPICE_WLIST")));
+    const bool segdesc = !(getenv("SPICE_WLIST") && atoi(getenv("SPICE_WLIST"))) || n->eshift == 0 || n->C > 1;
     if (n->pad8 && !n->xbuf && segdesc) {
         if ((st = dalloc_t(n, &n->desc, 2ull * n->NT * ((n->n_own + 1) & ~1ull), "segment descriptors"))) return bail(st);
         if ((st = dalloc_t(n, &n->dcount, 4, "descriptor counters"))) return bail(st);
@@ -701,11 +709,12 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     }
     if (n->G == 1 && n->model != SPICE_BRUNEL_PLUS && !n->desc && !n->wl && !n->xbuf)
         n->fused = false;                                  // unpadded G = 1 (SPICE_NOPAD)
+    if (n->C > 1 && !n->desc) n->fused = false;           // cluster tiles: descriptor path only
     // ---- kernel arguments ----
     SimArgs &a = n->args;
     a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D;
     a.rank = n->rank; a.G = n->G; a.S = n->S; a.n_own = (uint32_t)n->n_own; a.W = n->W;
-    a.TW = n->TW; a.NT = n->NT; a.C = n->C; a.ring_stride = n->ring_stride; a.record_steps = n->R;
+    a.TW = n->TW; a.NT = n->NT; a.C = n->C; a.TWs = n->TWs; a.ring_stride = n->ring_stride; a.record_steps = n->R;
     a.GS = pick_group_lanes(n->mean_seg);
     if (const char *gs = getenv("SPICE_GROUP_LANES")) a.GS = (uint32_t)atoi(gs);
     if (const char *dm = getenv("SPICE_DEBUG_MODE")) a.dbg = (uint32_t)atoi(dm);   // diagnostics only
@@ -954,7 +963,7 @@ spice_status spice_force_spikes(spice_net *n, const uint32_t *ids, uint64_t coun
 spice_status spice_stats(spice_net *n, uint64_t *steps, uint64_t *fired, uint64_t *delivered) {
     CHECK_NET(n);
     CU(n, cudaStreamSynchronize(n->stream));
-    std::vector<unsigned long long> f(n->NT), d((size_t)n->NT * n->C);
+    std::vector<unsigned long long> f((size_t)n->NT * n->C), d((size_t)n->NT * n->C);
     CU(n, cudaMemcpy(f.data(), n->fired_cta, f.size() * 8, cudaMemcpyDeviceToHost));
     CU(n, cudaMemcpy(d.data(), n->delivered_cta, d.size() * 8, cudaMemcpyDeviceToHost));
     unsigned long long sf = 0, sd = 0;

@@ -605,14 +605,15 @@ __device__ __forceinline__ uint64_t write_windows(const SimArgs &a, uint64_t t, 
     return dsum;                                       // valid in warp 0
 }
 
+// Update the owned neurons [lo, lo + width) for step t (a tile, or one CTA's slice of a
+// cluster tile); b is the CTA's spike-list region / counter slot.
 template <int MODEL>
-__device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, const uint32_t *cnt,
-                            bool write_list, uint32_t *s_count, uint32_t *stage, uint32_t *xsm = nullptr,
-                            const StatePtrs *staged = nullptr, bool marks = false) {
+__device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
+                            const uint32_t *cnt, bool write_list, uint32_t *s_count, uint32_t *stage,
+                            uint32_t *xsm = nullptr, const StatePtrs *staged = nullptr, bool marks = false) {
     const StatePtrs sp = staged ? *staged : global_state(a);
     const uint32_t tid = threadIdx.x, lane = tid & 31;
-    const uint32_t lo = b * a.TW;
-    const uint32_t span = lo < a.W * 32u ? min(a.TW, a.W * 32u - lo) : 0u;   // bitmap coverage
+    const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;   // bitmap coverage
     const uint32_t par = (uint32_t)(t & 1);
     uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
     uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + b) * a.RS;
@@ -675,7 +676,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     __syncthreads();
     if (marks) phase_mark(a, 7);
     if (staged) {                                          // staged state -> global (coalesced)
-        const uint32_t nw = a.TW / 4;
+        const uint32_t nw = width / 4;
         for (uint32_t x = tid; x < nw; x += kBlock) {
             const uint32_t g = lo + 4 * x;
             if (MODEL == 4) reinterpret_cast<uint4 *>(a.acc + g)[0] = reinterpret_cast<const uint4 *>(sp.acc)[x];
@@ -796,12 +797,23 @@ __device__ __forceinline__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, u
 }
 
 // Eight unconditional shared-memory reductions of one padded 16-byte window (sentinel
-// entries land in the dummy counters past the tile).  Padded entries are byte offsets.
+// entries land in the dummy counters past the tile).  Padded entries are byte offsets
+// (tiles up to kMaxPadTile) or, WORD = true, counter indices (cluster tiles up to
+// kMaxPadTileWord).
+template <bool WORD = false>
 __device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v, uint32_t q) {
-    const uint32_t a0 = cnt_s + (v.x & 0xFFFFu), a1 = cnt_s + (v.x >> 16);
-    const uint32_t a2 = cnt_s + (v.y & 0xFFFFu), a3 = cnt_s + (v.y >> 16);
-    const uint32_t a4 = cnt_s + (v.z & 0xFFFFu), a5 = cnt_s + (v.z >> 16);
-    const uint32_t a6 = cnt_s + (v.w & 0xFFFFu), a7 = cnt_s + (v.w >> 16);
+    uint32_t a0, a1, a2, a3, a4, a5, a6, a7;
+    if (WORD) {
+        a0 = cnt_s + ((v.x & 0xFFFFu) << 2); a1 = cnt_s + ((v.x >> 14) & ~3u);
+        a2 = cnt_s + ((v.y & 0xFFFFu) << 2); a3 = cnt_s + ((v.y >> 14) & ~3u);
+        a4 = cnt_s + ((v.z & 0xFFFFu) << 2); a5 = cnt_s + ((v.z >> 14) & ~3u);
+        a6 = cnt_s + ((v.w & 0xFFFFu) << 2); a7 = cnt_s + ((v.w >> 14) & ~3u);
+    } else {
+        a0 = cnt_s + (v.x & 0xFFFFu); a1 = cnt_s + (v.x >> 16);
+        a2 = cnt_s + (v.y & 0xFFFFu); a3 = cnt_s + (v.y >> 16);
+        a4 = cnt_s + (v.z & 0xFFFFu); a5 = cnt_s + (v.z >> 16);
+        a6 = cnt_s + (v.w & 0xFFFFu); a7 = cnt_s + (v.w >> 16);
+    }
     asm volatile(
         "red.shared.add.u32 [%0], %8;\n\t"
         "red.shared.add.u32 [%1], %8;\n\t"
@@ -978,6 +990,7 @@ __device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t 
 // windows of a segment sit in one load instruction and coalesce into one L1 line lookup),
 // the next iteration's two window loads in flight while the current windows are reduced.
 constexpr uint32_t kRing = 512;                        // ring entries per warp (power of 2)
+template <bool WORD>
 __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
                                                   uint32_t *cnt, uint32_t *ring_base, bool marks = false) {
     constexpr uint32_t NW = kBlock / 32;
@@ -1051,8 +1064,8 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
         const uint4 na = load_win(xa), nb = load_win(xb);
         head = min(head + 64, tail);
         if (!(a.dbg & 3u)) {
-            if (ea != NONE) accumulate_window(cnt_s, va, (ea >> 31) ? 65536u : 1u);
-            if (eb != NONE) accumulate_window(cnt_s, vb, (eb >> 31) ? 65536u : 1u);
+            if (ea != NONE) accumulate_window<WORD>(cnt_s, va, (ea >> 31) ? 65536u : 1u);
+            if (eb != NONE) accumulate_window<WORD>(cnt_s, vb, (eb >> 31) ? 65536u : 1u);
         }
         ea = xa; eb = xb; va = na; vb = nb;
     }
@@ -1366,7 +1379,7 @@ __global__ void __launch_bounds__(kBlock) k_update(SimArgs a, uint32_t k) {
     __shared__ uint32_t s_count;
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
-    update_tile<MODEL>(a, *a.t0 + k, blockIdx.x, nullptr, a.G == 1, &s_count, stage, stage);
+    update_tile<MODEL>(a, *a.t0 + k, blockIdx.x, blockIdx.x * a.TWs, a.TWs, nullptr, a.G == 1, &s_count, stage, stage);
 }
 
 template <int GS>
@@ -1394,7 +1407,12 @@ __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
     uint32_t d;
     if (a.wl) { __syncthreads(); deliver_tile_wl(a, t, b, c, sm.cnt); d = 0; }
-    else if (a.desc) { __syncthreads(); deliver_tile_ring(a, t, b, c, sm.cnt, sm.stage); d = 0; }
+    else if (a.desc) {
+        __syncthreads();
+        if (a.eshift) deliver_tile_ring<false>(a, t, b, c, sm.cnt, sm.stage);
+        else deliver_tile_ring<true>(a, t, b, c, sm.cnt, sm.stage);
+        d = 0;
+    }
     else d = deliver_tile<GS>(a, t, b, c, sm);
     uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
     if (a.C == 1u) {
@@ -1437,6 +1455,39 @@ __global__ void __launch_bounds__(kBlock) k_deliver_plastic(SimArgs a, uint32_t 
     store_delivered(a, b, d, sm.tmp);
 }
 
+// Cluster tiles (C > 1): after every CTA of the cluster has accumulated its share of the
+// tile's visits into its own full-tile counters, CTA c sums slice c of all C counter arrays
+// (16-byte distributed-shared-memory loads, peers staggered) into its own slice.  The
+// closing arrive is matched by cluster_wait() before exit: no CTA leaves (releasing its
+// shared memory) while a peer may still read it.
+__device__ __forceinline__ void cluster_reduce_slice(const SimArgs &a, uint32_t *cnt, uint32_t c) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    uint32_t *mine = cnt + c * a.TWs;
+    const uint32_t base = smem_u32(mine);
+    for (uint32_t i = threadIdx.x * 4u; i < a.TWs; i += kBlock * 4u) {
+        uint4 acc = *reinterpret_cast<const uint4 *>(mine + i);
+#pragma unroll
+        for (uint32_t k = 1; k < kMaxCluster; ++k) {
+            if (k < a.C) {
+                uint32_t peer = c + k;
+                if (peer >= a.C) peer -= a.C;
+                uint32_t ra;
+                uint4 v;
+                asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base + 4u * i), "r"(peer));
+                asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ra));
+                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
+        }
+        *reinterpret_cast<uint4 *>(mine + i) = acc;
+    }
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 template <int MODEL, int GS>
 __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
     if constexpr (MODEL == 3) {                             // Brunel+ (delay >= 1 via the rings)
@@ -1457,7 +1508,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         store_delivered(a, b, d, sm.tmp);
         __syncthreads();
         phase_mark(a, 6);
-        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count3, sm.stage, nullptr, nullptr, true);
+        update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count3, sm.stage, nullptr, nullptr, true);
         phase_mark(a, 12);
     } else {
     extern __shared__ __align__(16) uint32_t smem[];
@@ -1474,31 +1525,38 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         const uint32_t d = exchange_consume(a, (uint32_t)(t & 1), b, cnt);
         store_delivered(a, b, d, s_tmp);
         if (a.delay == 1) {
-            update_tile<MODEL>(a, t + 1, b, cnt, true, &s_count, nullptr, smem);
+            update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, cnt, true, &s_count, nullptr, smem);
         } else {
             uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
             for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)
                 *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
             __syncthreads();
-            update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count, nullptr, smem);
+            update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count, nullptr, smem);
         }
         return;
     }
+    // tile bt = blockIdx.x / C; with C > 1 this CTA is rank c of the tile's cluster
+    const uint32_t bt = b / a.C, c = b % a.C;
     phase_mark(a, 0);
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
     __syncthreads();
     phase_mark(a, 1);
-    if (a.wl) deliver_tile_wl(a, t, b, 0, sm.cnt, true);
-    else deliver_tile_ring(a, t, b, 0, sm.cnt, sm.stage, true);
+    if (a.wl) deliver_tile_wl(a, t, bt, 0, sm.cnt, true);
+    else if (a.eshift) deliver_tile_ring<false>(a, t, bt, c, sm.cnt, sm.stage, true);
+    else deliver_tile_ring<true>(a, t, bt, c, sm.cnt, sm.stage, true);
+    if (a.C > 1) cluster_reduce_slice(a, sm.cnt, c);
+    uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice, summed
+    const uint32_t lo = b * a.TWs;
     phase_mark(a, 6);
     if (a.delay == 1) {
-        update_tile<MODEL>(a, t + 1, b, sm.cnt, true, &s_count, sm.stage, nullptr, nullptr, true);
+        update_tile<MODEL>(a, t + 1, b, lo, a.TWs, cnt, true, &s_count, sm.stage, nullptr, nullptr, true);
     } else {
-        uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
-        for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)
-            *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(sm.cnt + x);
-        update_tile<MODEL>(a, t + 1, b, nullptr, true, &s_count, sm.stage, nullptr, nullptr, true);
+        uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + lo;
+        for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u)
+            *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
+        update_tile<MODEL>(a, t + 1, b, lo, a.TWs, nullptr, true, &s_count, sm.stage, nullptr, nullptr, true);
     }
+    if (a.C > 1) cluster_wait();                         // partners done reading this CTA's counters
     phase_mark(a, 12);
     }
 }
@@ -1638,10 +1696,10 @@ cudaError_t prepare_kernels(const SimArgs &a) {
 cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s) {
     const size_t ub = a.xbuf ? xchg_kernel_smem_bytes(a.TW, a.NT) : (size_t)kStageWords * 4;
     switch (a.model) {
-    case 1: k_update<1><<<a.NT, kBlock, ub, s>>>(a, k); break;
-    case 2: k_update<2><<<a.NT, kBlock, ub, s>>>(a, k); break;
-    case 3: k_update<3><<<a.NT, kBlock, kStageWords * 4, s>>>(a, k); break;
-    case 4: k_update<4><<<a.NT, kBlock, ub, s>>>(a, k); break;
+    case 1: k_update<1><<<a.NT * a.C, kBlock, ub, s>>>(a, k); break;
+    case 2: k_update<2><<<a.NT * a.C, kBlock, ub, s>>>(a, k); break;
+    case 3: k_update<3><<<a.NT * a.C, kBlock, kStageWords * 4, s>>>(a, k); break;
+    case 4: k_update<4><<<a.NT * a.C, kBlock, ub, s>>>(a, k); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -1679,8 +1737,37 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
     return cudaGetLastError();
 }
 
+// C > 1: the C CTAs of a tile are launched as one thread-block cluster.
+template <typename K>
+static void launch_cluster(K kern, const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.NT * a.C);
+    cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = a.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a, k);
+}
+
 template <int M>
 static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
+    if (a.C > 1) {
+        switch (a.GS) {
+        case 1: launch_cluster(k_fused<M, 1>, a, k, bytes, s); break;
+        case 2: launch_cluster(k_fused<M, 2>, a, k, bytes, s); break;
+        case 4: launch_cluster(k_fused<M, 4>, a, k, bytes, s); break;
+        case 8: launch_cluster(k_fused<M, 8>, a, k, bytes, s); break;
+        case 16: launch_cluster(k_fused<M, 16>, a, k, bytes, s); break;
+        default: launch_cluster(k_fused<M, 32>, a, k, bytes, s); break;
+        }
+        return;
+    }
     switch (a.GS) {
     case 1: k_fused<M, 1><<<a.NT, kBlock, bytes, s>>>(a, k); break;
     case 2: k_fused<M, 2><<<a.NT, kBlock, bytes, s>>>(a, k); break;

@@ -25,14 +25,18 @@ constexpr int kStages = SPICE_STAGES; // cp.async window stages per warp in deli
 constexpr uint32_t kDescSmem = 8192;  // default descriptor staging capacity per CTA (64 KiB)
 constexpr int kStageWords = 12288;     // bnd rows staged per descriptor-transposition pass
 constexpr uint32_t kXRowsBytes = 128 * 1024;   // exchange producer: staged rows per batch
-constexpr uint32_t kWbufWords = (kBlock / 32) * kStages * 32 * 4;   // cp.async window stages: warps x 4 stages x 32 lanes x 16 B
+// cp.async window stages (warps x stages x 32 lanes x 16 B) of the staged window path;
+// the default (SPICE_DIRECT) keeps windows in registers and needs none
+constexpr uint32_t kWbufWords = SPICE_DIRECT ? 0u : (kBlock / 32) * kStages * 32 * 4;
 constexpr uint32_t kMaxTileWidth = 49152;   // u32 counters per tile <= 192 KiB smem
 constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
 constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list region
 constexpr int kEntPad = 64;           // u16 padding before/after the entry array
 constexpr uint32_t kDummy = 64;       // dummy counters past the tile (padding sentinels)
 constexpr uint32_t kPtabSmem = 128;   // Poisson inversion table entries staged in smem
-constexpr uint32_t kMaxPadTile = 16320;   // padded layout: (TW + kDummy) * 4 must fit a u16
+constexpr uint32_t kMaxPadTile = 16320;   // padded layout, byte-offset entries: (TW + kDummy) * 4 fits a u16
+constexpr uint32_t kMaxPadTileWord = 65472;   // padded layout, word-offset entries: TW + kDummy fits a u16
+constexpr uint32_t kMaxCluster = 8;       // CTAs per tile cluster (portable cluster size)
 
 // Philox4x32-10 (Salmon et al., SC'11).  Multipliers 0xD2511F53 / 0xCD9E8D57, Weyl
 // key increments 0x9E3779B9 / 0xBB67AE85; 10 rounds.
@@ -87,6 +91,12 @@ struct SimArgs {
     uint32_t n_own;          // owned neurons of this rank
     uint32_t W;              // bitmap words per rank
     uint32_t TW, NT, C;      // tile width, tile count, CTAs per tile
+    uint32_t TWs;            // targets per CTA slice = TW / C: CTA x updates the owned
+                             // neurons [x TWs, (x+1) TWs) and owns spike-list region x.
+                             // With C > 1 (G = 1) the C CTAs of a tile form a thread-block
+                             // cluster: each accumulates its share of the tile's visits into
+                             // a full-tile shared counter array, then reduces its slice
+                             // across the cluster through distributed shared memory
     uint32_t GS;             // lanes per segment group in delivery
     uint64_t ring_stride;    // NT * TW
     uint32_t record_steps;

@@ -29,8 +29,13 @@ CASES = {
     "brunel1001_ragged": (W.brunel(1001, 0.2, seed=2, delay=3), dict(tile_width=64), 300),
     "synth20000": (W.synth(20000, 31, 0.005, seed=3), {}, 200),
     "synth5003_ragged_c2": (W.synth(5003, 100, 0.02, seed=4), dict(tile_width=96, ctas_per_tile=2), 150),
-    # tile wider than the padded layout allows (byte offsets in u16): unpadded generic path
+    # tile wider than byte-offset entries allow: padded layout with counter-index entries
     "synth40000_wide_tile": (W.synth(40000, 31, 0.005, seed=11), dict(tile_width=16384), 60),
+    # thread-block-cluster tiles (C CTAs per tile, DSMEM reduction of the tile counters)
+    "synth40000_cluster2_word": (W.synth(40000, 31, 0.005, seed=12), dict(tile_width=20480, ctas_per_tile=2), 60),
+    "synth20000_cluster4": (W.synth(20000, 31, 0.005, seed=13), dict(ctas_per_tile=4), 100),
+    "brunel3000_d15_cluster4": (W.brunel(3000, 0.1, seed=14, delay=15), dict(tile_width=256, ctas_per_tile=4), 300),
+    "vogels4000_cluster8": (W.vogels(4000, seed=15), dict(tile_width=512, ctas_per_tile=8), 300),
     "vogels_global_atomics": (W.vogels(4000, seed=9), dict(global_atomics=True), 300),
     "synth_global_atomics": (W.synth(20000, 31, 0.005, seed=8), dict(global_atomics=True), 100),
 }

@@ -1,5 +1,5 @@
 """In-kernel phase timeline of the fused kernel (diagnostics; SPICE_PHASES=1).
-Usage: python tools/phases.py [synth|brunel100k|vogels4000] [steps]"""
+Usage: python tools/phases.py [synth|brunel100k|vogels4000] [steps] [ctas_per_tile]"""
 import os
 import sys
 
@@ -11,13 +11,14 @@ import bench  # noqa: E402
 from paper_2102_04681_b200 import spice as S  # noqa: E402
 
 NAMES = {1: "counters zeroed", 2: "region prefix", 3: "descriptors staged", 4: "warp0 delivered",
-         5: "delivery barrier", 6: "delivered stat", 7: "update loop", 8: "spike rows",
+         5: "delivery barrier", 6: "cluster reduce", 7: "update loop", 8: "spike rows",
          10: "(prod) rows loaded", 11: "(prod) reserved", 9: "descriptors written", 12: "end"}
 which = sys.argv[1] if len(sys.argv) > 1 else "synth"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
+ctas = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 cfg, _ = bench.workload(which, 1)
 mhz = float(os.environ.get("SM_MHZ", "1965"))
-with S.Network(cfg, record_steps=64) as net:
+with S.Network(cfg, record_steps=64, ctas_per_tile=ctas) as net:
     net.step(256)
     net.sync()
     p0 = net.debug_phases().astype(np.float64)
