@@ -114,7 +114,7 @@ struct spice_net {
     bool external = false;
     // geometry
     uint64_t n_own = 0, n_own_max = 0;
-    uint32_t W = 0, TW = 32, NT = 1, C = 1, TWs = 32;
+    uint32_t W = 0, TW = 32, NT = 1, C = 1, TWs = 32, rstages = 0;
     uint64_t ring_stride = 0;
     uint64_t nnz = 0;        // stored entries (incl. padding sentinels)
     uint64_t n_syn = 0;      // synapses (owned targets)
@@ -382,8 +382,8 @@ spice_status generate(spice_net *n) {
     uint32_t *cursor = nullptr;
     spice_status st;
     if ((st = dalloc_t(n, &n->row_ptr, (size_t)n->N + 1, "row_ptr"))) return st;
-    if ((st = dalloc_t(n, &n->bnd, nb, "segment bounds"))) return st;
-    CU(n, cudaMemsetAsync(n->bnd, 0, nb * 4, n->stream));
+    if ((st = dalloc_t(n, &n->bnd, nb + 4, "segment bounds"))) return st;   // + 16-byte tail pad
+    CU(n, cudaMemsetAsync(n->bnd, 0, (nb + 4) * 4, n->stream));
     // rules in ascending destination order so that per-segment appends stay sorted
     std::vector<uint32_t> order(n->rules.size());
     for (uint32_t r = 0; r < order.size(); ++r) order[r] = r;
@@ -522,9 +522,12 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // C CTAs per tile (ctas_per_tile): the tile is cut into C slices of TWs = TW / C targets
     // (multiples of 32); CTA x updates slice x.  On the fused G = 1 path the C CTAs form a
     // thread-block cluster that reduces the tile's counters through distributed shared memory.
-    n->C = c->ctas_per_tile ? c->ctas_per_tile : 1;
-    if (n->C > kMaxCluster) return bail(fail(n, SPICE_EINVAL, "ctas_per_tile %u > %u", n->C, kMaxCluster));
     n->pad8 = n->G == 1 && n->model != SPICE_BRUNEL_PLUS && !getenv("SPICE_XCHG") && !getenv("SPICE_NOPAD");
+    // auto: 2-CTA cluster tiles for large padded networks (half the spike x tile visits per
+    // CTA; measured -4 % step time on synth 3e9, DESIGN.md delivery log), else one CTA per tile
+    n->C = c->ctas_per_tile ? c->ctas_per_tile
+         : (n->pad8 && !c->tile_width && n->n_own >= (uint64_t)n->n_sm * 4096u ? 2u : 1u);
+    if (n->C > kMaxCluster) return bail(fail(n, SPICE_EINVAL, "ctas_per_tile %u > %u", n->C, kMaxCluster));
     if (c->tile_width) {
         const uint32_t q = 32u * n->C;
         n->TW = (c->tile_width + q - 1) / q * q;
@@ -551,8 +554,19 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // descriptor staging capacity: kDescSmem, shrunk (not below the update's staging area)
     // when wide tiles need the shared memory
     n->dcap = kDescSmem;
-    while (n->dcap > (uint32_t)kStageWords / 2 && tile_smem_bytes(n->TW, n->NR, n->dcap) > 227 * 1024) n->dcap -= 512;
-    if (tile_smem_bytes(n->TW, n->NR, n->dcap) > 227 * 1024) return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for shared memory", n->TW));
+    const size_t smem_max = 227 * 1024 - 2048;             // dynamic; static shared variables need the rest
+    while (n->dcap > (uint32_t)kStageWords / 2 && tile_smem_bytes(n->TW, n->NR, n->dcap, 0) > smem_max) n->dcap -= 512;
+    if (tile_smem_bytes(n->TW, n->NR, n->dcap, 0) > smem_max) return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for shared memory", n->TW));
+    // staged-ring delivery (padded layout, opt-in A/B: SPICE_RSTAGES=4|8).  Measured slower
+    // than the register ring on synth 3e9 (DESIGN.md delivery log): more windows in flight
+    // per warp do not help once the SM's outstanding-request capacity is in use.
+    n->rstages = 0;
+    if (n->pad8) {
+        if (const char *e = getenv("SPICE_RSTAGES")) {
+            const uint32_t v = (uint32_t)atoi(e);
+            if (v == 0 || ((v == 4 || v == 8) && tile_smem_bytes(n->TW, n->NR, n->dcap, v) <= smem_max)) n->rstages = v;
+        }
+    }
     // ---- NCCL communicator ----
     if (n->G > 1 && !n->external) {
         if (!nccl().ok) return bail(fail(n, SPICE_ENCCL, "libnccl.so.2 not found (set SPICE_NCCL_LIB)"));
@@ -719,6 +733,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (const char *gs = getenv("SPICE_GROUP_LANES")) a.GS = (uint32_t)atoi(gs);
     if (const char *dm = getenv("SPICE_DEBUG_MODE")) a.dbg = (uint32_t)atoi(dm);   // diagnostics only
     a.dcap = n->dcap;
+    a.rstages = n->rstages;
     if ((a.dbg & 32u) && n->desc &&
         (st = dalloc_t(n, &a.dscratch, 2ull * n->NT * ((n->n_own + 1) & ~1ull), "descriptor scratch"))) return bail(st);
     if (getenv("SPICE_PHASES") && atoi(getenv("SPICE_PHASES"))) {     // diagnostics only

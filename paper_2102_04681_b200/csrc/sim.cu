@@ -488,9 +488,13 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
     __shared__ uint32_t s_off;
     if (threadIdx.x == 0 && n) s_off = atomicAdd(&a.dcount[t % 3], n);
     const uint32_t rowlen = a.NT + 1u;
-    const uint32_t CH = max(1u, (uint32_t)kStageWords / (rowlen + 3u));
-    uint64_t *srow = reinterpret_cast<uint64_t *>(stage + CH * rowlen + (CH * rowlen & 1u));
+    // staged rows keep their global 16-byte phase h = (s rowlen) mod 4 so that they are
+    // copied in 16-byte chunks (the bnd array carries 4 words of tail padding)
+    const uint32_t rs4 = (rowlen + 6u) & ~3u;
+    const uint32_t CH = max(1u, (uint32_t)kStageWords / (rs4 + 3u));
+    uint64_t *srow = reinterpret_cast<uint64_t *>(stage + CH * rs4);
     uint32_t *sdeg = reinterpret_cast<uint32_t *>(srow + CH);
+    const uint4 *bnd4 = reinterpret_cast<const uint4 *>(a.bnd);
     uint64_t dsum = 0;
     for (uint32_t q0 = 0; q0 < n; q0 += CH) {
         const uint32_t nq = min(CH, n - q0);
@@ -498,9 +502,10 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
         // every load of the pass in flight at once (cp.async, no register round trips)
         for (uint32_t ql = warp; ql < nq; ql += kBlock / 32) {            // one warp per spike row
             const uint32_t s = region[q0 + ql];
-            const uint32_t *row = a.bnd + (uint64_t)s * rowlen;
-            for (uint32_t bb = lane; bb < rowlen; bb += 32)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(stage + ql * rowlen + bb)), "l"(row + bb) : "memory");
+            const uint64_t g0 = (uint64_t)s * rowlen;
+            const uint64_t k0 = g0 >> 2, nk = ((g0 + rowlen - 1) >> 2) - k0 + 1;
+            for (uint32_t k = lane; k < nk; k += 32)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" :: "r"(smem_u32(stage + ql * rs4 + 4u * k)), "l"(bnd4 + k0 + k) : "memory");
             if (lane == 0) {
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(srow + ql)), "l"(a.row_ptr + s) : "memory");
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(sdeg + ql)), "l"(a.deg + s) : "memory");
@@ -516,7 +521,7 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
             if (ql < nq) {                                   // padded: rs, lo, hi multiples of 8
                 const uint32_t rs8 = (uint32_t)(srow[ql] >> 3);
                 const uint32_t ih = region[q0 + ql] >= a.n_exc ? 0x80000000u : 0u;
-                const uint32_t *row = stage + ql * rowlen;
+                const uint32_t *row = stage + ql * rs4 + (uint32_t)(((uint64_t)region[q0 + ql] * rowlen) & 3u);
                 uint2 *dst = reinterpret_cast<uint2 *>(a.desc + (uint64_t)par * a.NT * a.dstride + s_off + q0 + ql);
                 for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
                     const uint32_t lo = row[bb], hi = row[bb + 1];
@@ -607,10 +612,13 @@ __device__ __forceinline__ uint64_t write_windows(const SimArgs &a, uint64_t t, 
 
 // Update the owned neurons [lo, lo + width) for step t (a tile, or one CTA's slice of a
 // cluster tile); b is the CTA's spike-list region / counter slot.
+// cl_c < kMaxCluster: cnt is this CTA's slice of a cluster tile whose C = a.C CTAs each hold
+// partial counts for it; the update adds the peers' partials (distributed shared memory).
 template <int MODEL>
 __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                             const uint32_t *cnt, bool write_list, uint32_t *s_count, uint32_t *stage,
-                            uint32_t *xsm = nullptr, const StatePtrs *staged = nullptr, bool marks = false) {
+                            uint32_t *xsm = nullptr, const StatePtrs *staged = nullptr, bool marks = false,
+                            uint32_t cl_c = kMaxCluster) {
     const StatePtrs sp = staged ? *staged : global_state(a);
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;   // bitmap coverage
@@ -642,7 +650,24 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 for (int e = 0; e < 4; ++e) { pin[e] = ps[e]; ps[e] = 0; }
             }
             if (cnt) {
-                c[0] = cnt[x4]; c[1] = cnt[x4 + 1]; c[2] = cnt[x4 + 2]; c[3] = cnt[x4 + 3];
+                uint4 cv = *reinterpret_cast<const uint4 *>(cnt + x4);
+                if (cl_c < kMaxCluster) {
+                    const uint32_t la = (uint32_t)__cvta_generic_to_shared(cnt + x4);
+#pragma unroll
+                    for (uint32_t k = 1; k < kMaxCluster; ++k) {
+                        if (k < a.C) {
+                            uint32_t peer = cl_c + k;
+                            if (peer >= a.C) peer -= a.C;
+                            uint32_t ra;
+                            uint4 v;
+                            asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(peer));
+                            asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ra));
+                            cv.x += v.x; cv.y += v.y; cv.z += v.z; cv.w += v.w;
+                        }
+                    }
+                }
+                c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
             } else {
                 const uint4 cv = *reinterpret_cast<const uint4 *>(ring_slot + x4);
                 *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
@@ -990,6 +1015,7 @@ __device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t 
 // windows of a segment sit in one load instruction and coalesce into one L1 line lookup),
 // the next iteration's two window loads in flight while the current windows are reduced.
 constexpr uint32_t kRing = 512;                        // ring entries per warp (power of 2)
+constexpr uint32_t kRingS = 256;                       // deliver_tile_rs: ring entries per warp
 template <bool WORD>
 __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
                                                   uint32_t *cnt, uint32_t *ring_base, bool marks = false) {
@@ -1069,6 +1095,117 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
         }
         ea = xa; eb = xb; va = na; vb = nb;
     }
+    if (marks) phase_mark(a, 4);
+    __syncthreads();
+    if (marks) phase_mark(a, 5);
+}
+
+// Staged ring delivery (G = 1, padded layout; default).  The descriptor expansion of
+// deliver_tile_ring (per-warp ring of window entries), but the windows are copied with
+// 16-byte cp.async into S per-warp shared-memory stages of 32 windows (one per lane) and
+// reduced S - 1 stages later: S x 32 windows per warp in flight instead of 64, so a warp's
+// share of the step (~500 windows at synth 3e9) takes ~2 memory round trips, not ~8.
+// Each lane reads back only the slot its own cp.async wrote (wait_group suffices).
+template <bool WORD, int S>
+__device__ __forceinline__ void deliver_tile_rs(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+                                                uint32_t *cnt, uint32_t *big, bool marks = false) {
+    constexpr uint32_t NW = kBlock / 32;
+    constexpr uint32_t NONE = 0xFFFFFFFFu;
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    static_assert(S >= 2 && S <= 16, "stage count");
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
+    __shared__ uint32_t s_total;
+    if (tid == 0) {
+        s_total = a.dcount[t % 3];
+        if (b == 0 && c == 0) a.dcount[(t + 2) % 3] = 0u;     // next user: step t + 2's producers
+    }
+    __syncthreads();
+    if (marks) phase_mark(a, 2);
+    const uint32_t n_sp = s_total;
+    const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
+    const uint32_t v0 = (uint32_t)((uint64_t)my * warp / NW), v1 = (uint32_t)((uint64_t)my * (warp + 1) / NW);
+    const uint64_t *dlist = a.desc + ((uint64_t)par * a.NT + b) * a.dstride + c;   // visit v -> dlist[v * C]
+    const uint4 *ent4 = reinterpret_cast<const uint4 *>(a.ent);
+    uint32_t *ring = big + warp * kRingS;
+    const uint32_t stg_s = (uint32_t)__cvta_generic_to_shared(big + NW * kRingS) + warp * (S * 32u * 16u) + lane * 16u;
+    auto dload = [&](uint32_t vb) -> uint64_t {
+        const uint32_t v = vb + lane;
+        return v < v1 ? dlist[(uint64_t)v * a.C] : 0ull;
+    };
+    if (marks) phase_mark(a, 3);
+    uint32_t gnext = v0;
+    uint64_t dn = dload(v0);
+    uint32_t w0 = 0, nw = 0, inh = 0, pre = 0, T = 0, c0 = 0;   // current group, c0 = expanded
+    uint32_t head = 0, tail = 0;                                // ring cursors (warp-uniform)
+    auto fill = [&](uint32_t want) {                            // expand until >= want queued
+        while (tail - head < want) {
+            if (c0 >= T) {
+                if (gnext >= v1) break;
+                const uint64_t d = dn;
+                gnext += 32;
+                dn = dload(gnext);
+                nw = (uint32_t)(d >> 32) & 0x7FFFFFFFu;
+                w0 = (uint32_t)d;
+                inh = (uint32_t)(d >> 63) << 31;
+                const uint32_t incl = warp_incl_scan(nw);
+                pre = incl - nw;
+                T = __shfl_sync(FULL, incl, 31);
+                c0 = 0;
+                continue;
+            }
+            const uint32_t take = min(T - c0, kRingS - (tail - head));
+            const uint32_t klo = c0 > pre ? c0 - pre : 0u;
+            const uint32_t khi = min(pre + nw, c0 + take);
+            for (uint32_t k = klo; pre + k < khi; ++k)
+                ring[(tail + pre + k - c0) & (kRingS - 1)] = (w0 + k) | inh;
+            tail += take;
+            c0 += take;
+        }
+        __syncwarp();
+    };
+    uint32_t qbits = 0;            // bit s: stage s holds a window of this lane; bit 16 + s: inh
+    uint32_t live = 0;             // warp-uniform: stages holding a round
+    bool exhausted = false;        // warp-uniform: nothing left to issue
+    auto issue = [&](int s) {
+        fill(32);
+        exhausted = head == tail;
+        const uint32_t x = head + lane;
+        const uint32_t e = x < tail ? ring[x & (kRingS - 1)] : NONE;
+        head = min(head + 32, tail);
+        qbits &= ~((1u << s) | (1u << (16 + s)));
+        if (e != NONE) {
+            if (!(a.dbg & 2u))
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                             :: "r"(stg_s + (uint32_t)s * 512u), "l"(ent4 + (e & 0x7FFFFFFFu)) : "memory");
+            qbits |= (1u << s) | ((e >> 31) << (16 + s));
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (!exhausted) live |= 1u << s;
+    };
+    auto process = [&](int s) {
+        asm volatile("cp.async.wait_group %0;" :: "n"(S - 1) : "memory");
+        if (((qbits >> s) & 1u) && !(a.dbg & 3u)) {
+            uint4 v;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(stg_s + (uint32_t)s * 512u));
+            accumulate_window<WORD>(cnt_s, v, ((qbits >> (16 + s)) & 1u) ? 65536u : 1u);
+        }
+        live &= ~(1u << s);
+    };
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) issue(s);
+    bool fin = false;
+    while (!fin) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            issue((s + S - 1) % S);
+            process(s);
+            if (exhausted && live == 0) { fin = true; break; }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (marks) phase_mark(a, 4);
     __syncthreads();
     if (marks) phase_mark(a, 5);
@@ -1311,6 +1448,22 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
     return delivered;
 }
 
+// Padded-layout delivery of tile b (CTA c of C): staged ring (a.rstages stages) or the
+// register ring; byte-offset or counter-index entries.
+__device__ __forceinline__ void deliver_padded(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+                                               uint32_t *cnt, uint32_t *big, bool marks = false) {
+    if (a.rstages == 8) {
+        if (a.eshift) deliver_tile_rs<false, 8>(a, t, b, c, cnt, big, marks);
+        else deliver_tile_rs<true, 8>(a, t, b, c, cnt, big, marks);
+    } else if (a.rstages == 4) {
+        if (a.eshift) deliver_tile_rs<false, 4>(a, t, b, c, cnt, big, marks);
+        else deliver_tile_rs<true, 4>(a, t, b, c, cnt, big, marks);
+    } else {
+        if (a.eshift) deliver_tile_ring<false>(a, t, b, c, cnt, big, marks);
+        else deliver_tile_ring<true>(a, t, b, c, cnt, big, marks);
+    }
+}
+
 __device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot, uint32_t d, uint32_t *s_tmp) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xFFFFFFFFu, d, o);
@@ -1325,10 +1478,12 @@ __device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot,
 }
 
 // Delivery shared memory: wbuf | cnt [TW + kDummy] | big [max(kStageWords, 2 dcap)] | pref | tmp
-__host__ __device__ inline uint32_t big_words(uint32_t dcap) {
+__host__ __device__ inline uint32_t big_words(uint32_t dcap, uint32_t rstages) {
     uint32_t w = (uint32_t)kStageWords > 2u * dcap ? (uint32_t)kStageWords : 2u * dcap;
     const uint32_t ring = (kBlock / 32) * kRing;               // deliver_tile_ring's rings
-    return w > ring ? w : ring;
+    w = w > ring ? w : ring;
+    const uint32_t rs = rstages ? (kBlock / 32) * (kRingS + rstages * 32u * 4u) : 0u;   // deliver_tile_rs
+    return w > rs ? w : rs;
 }
 __device__ __forceinline__ DeliverSmem carve(const SimArgs &a, uint32_t *smem) {
     DeliverSmem sm;
@@ -1339,15 +1494,15 @@ __device__ __forceinline__ DeliverSmem carve(const SimArgs &a, uint32_t *smem) {
     smem += tw4 + kDummy;
     sm.dsm = reinterpret_cast<uint64_t *>(smem);
     sm.stage = smem;
-    smem += big_words(a.dcap);
+    smem += big_words(a.dcap, a.rstages);
     sm.pref = smem;
     sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
     return sm;
 }
 
-size_t tile_smem_bytes(uint32_t TW, uint32_t NR, uint32_t dcap) {
+size_t tile_smem_bytes(uint32_t TW, uint32_t NR, uint32_t dcap, uint32_t rstages) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
-    return ((size_t)kWbufWords + tw4 + kDummy + big_words(dcap) + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
+    return ((size_t)kWbufWords + tw4 + kDummy + big_words(dcap, rstages) + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
 }
 size_t xchg_kernel_smem_bytes(uint32_t TW, uint32_t NT) {
     const size_t c = ((size_t)((TW + 3u) & ~3u)) * 4;
@@ -1409,8 +1564,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
     if (a.wl) { __syncthreads(); deliver_tile_wl(a, t, b, c, sm.cnt); d = 0; }
     else if (a.desc) {
         __syncthreads();
-        if (a.eshift) deliver_tile_ring<false>(a, t, b, c, sm.cnt, sm.stage);
-        else deliver_tile_ring<true>(a, t, b, c, sm.cnt, sm.stage);
+        deliver_padded(a, t, b, c, sm.cnt, sm.stage);
         d = 0;
     }
     else d = deliver_tile<GS>(a, t, b, c, sm);
@@ -1538,25 +1692,40 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
     // tile bt = blockIdx.x / C; with C > 1 this CTA is rank c of the tile's cluster
     const uint32_t bt = b / a.C, c = b % a.C;
     phase_mark(a, 0);
+    if (threadIdx.x == 0 && a.delay == 1) {   // this slice's neuron state -> L2 while delivering
+        const uint32_t lo0 = b * a.TWs, nb = a.TWs * 4u;
+        const void *arr[4] = {MODEL == 4 ? (const void *)(a.acc + lo0) : (const void *)(a.v + lo0),
+                              MODEL == 4 ? nullptr : (const void *)(a.ref + lo0),
+                              MODEL == 1 ? (const void *)(a.ge + lo0) : nullptr,
+                              MODEL == 1 ? (const void *)(a.gi + lo0) : nullptr};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (arr[q]) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(arr[q]), "r"(nb) : "memory");
+    }
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
     __syncthreads();
     phase_mark(a, 1);
     if (a.wl) deliver_tile_wl(a, t, bt, 0, sm.cnt, true);
-    else if (a.eshift) deliver_tile_ring<false>(a, t, bt, c, sm.cnt, sm.stage, true);
-    else deliver_tile_ring<true>(a, t, bt, c, sm.cnt, sm.stage, true);
-    if (a.C > 1) cluster_reduce_slice(a, sm.cnt, c);
-    uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice, summed
+    else deliver_padded(a, t, bt, c, sm.cnt, sm.stage, true);
+    uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice
     const uint32_t lo = b * a.TWs;
-    phase_mark(a, 6);
     if (a.delay == 1) {
-        update_tile<MODEL>(a, t + 1, b, lo, a.TWs, cnt, true, &s_count, sm.stage, nullptr, nullptr, true);
+        // C > 1: the update sums the C partial slices itself (peers read after one cluster
+        // barrier; a second one at exit keeps every CTA's counters alive until then)
+        if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        phase_mark(a, 6);
+        update_tile<MODEL>(a, t + 1, b, lo, a.TWs, cnt, true, &s_count, sm.stage, nullptr, nullptr, true,
+                           a.C > 1 ? c : kMaxCluster);
+        if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     } else {
+        if (a.C > 1) cluster_reduce_slice(a, sm.cnt, c);   // slice summed in place
+        phase_mark(a, 6);
         uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + lo;
         for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u)
             *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
         update_tile<MODEL>(a, t + 1, b, lo, a.TWs, nullptr, true, &s_count, sm.stage, nullptr, nullptr, true);
+        if (a.C > 1) cluster_wait();                     // partners done reading this CTA's counters
     }
-    if (a.C > 1) cluster_wait();                         // partners done reading this CTA's counters
     phase_mark(a, 12);
     }
 }
@@ -1654,7 +1823,7 @@ static cudaError_t allow_smem(K kern, size_t bytes) {
 }
 
 cudaError_t prepare_kernels(const SimArgs &a) {
-    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap);
+    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap, a.rstages);
     {
         const size_t ub = (size_t)kStageWords * 4;
         cudaError_t e1 = allow_smem(k_update<1>, ub);
@@ -1707,7 +1876,7 @@ cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s) {
 
 cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, int n_sm, cudaStream_t s) {
     if (global_atomics) {
-        const size_t bytes = tile_smem_bytes(0, a.NR, a.dcap);
+        const size_t bytes = tile_smem_bytes(0, a.NR, a.dcap, 0);
         k_global_atomics<<<min((uint32_t)(n_sm * 4), a.NT * a.C), kBlock, bytes, s>>>(a, k);
         return cudaGetLastError();
     }
@@ -1723,7 +1892,7 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
         }
         return cudaGetLastError();
     }
-    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap);
+    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap, a.rstages);
     if (a.xbuf) { const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT); if (xb > bytes) bytes = xb; }
     const uint32_t grid = a.NT * a.C;
     switch (a.GS) {
@@ -1779,7 +1948,7 @@ static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) 
 }
 
 cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
-    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap);
+    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap, a.rstages);
     if (a.xbuf) { const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT); if (xb > bytes) bytes = xb; }
     switch (a.model) {
     case 1: fused_m<1>(a, k, bytes, s); break;

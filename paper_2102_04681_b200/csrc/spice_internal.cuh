@@ -104,6 +104,7 @@ struct SimArgs {
     uint32_t NR, RS;         // spike-list regions
     uint32_t pf_rows;        // 1: TMA-prefetch spiking rows into L2 at the end of the update
     uint32_t dcap;           // descriptors a delivering CTA stages in shared memory
+    uint32_t rstages;        // staged-ring delivery: cp.async window stages per warp (8, 4; 0 = register ring)
     unsigned long long *ptimes;   // diagnostics (SPICE_PHASES=1): per CTA [16] phase clocks
     uint64_t *dscratch;      // diagnostics (SPICE_DEBUG_MODE bit 5): second descriptor copy
     uint32_t dbg;            // diagnostics only (SPICE_DEBUG_MODE): bit0 no smem reductions,

@@ -8,7 +8,7 @@
 namespace spice {
 
 // ---- step kernels (sim.cu) ----
-size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions, uint32_t desc_cap);
+size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions, uint32_t desc_cap, uint32_t rstages);
 size_t plastic_smem_bytes(uint32_t tile_width, uint32_t n_regions);
 size_t xchg_kernel_smem_bytes(uint32_t tile_width, uint32_t n_tiles);
 cudaError_t launch_xcap(const SimArgs &a, uint32_t *cap, cudaStream_t s);
