@@ -472,6 +472,11 @@ __global__ void __launch_bounds__(kBlock) k_xcap(SimArgs a, uint32_t *cap) {
     for (uint32_t i = threadIdx.x; i < 2 * NT; i += kBlock) cap[((uint64_t)(i >> 1) * NT + g) * 2 + (i & 1)] = e[i];
 }
 
+constexpr uint32_t kRing = 512;                        // ring entries per warp (power of 2)
+// spike IDs of the update kept in shared memory for the descriptor pass: the words of the
+// delivery area past the descriptor staging (kStageWords) and before the end of the rings
+constexpr uint32_t kSidCap = (kBlock / 32) * kRing - kStageWords;
+
 // Descriptor transposition (G = 1, padded layout): for the n spikes of region b (this
 // tile's spikes), one pass loads every spike's bnd row (a warp per spike, coalesced),
 // row start and out-degree, staged in smem (CH spikes at a time; CH covers a whole step's
@@ -480,7 +485,8 @@ __global__ void __launch_bounds__(kBlock) k_xcap(SimArgs a, uint32_t *cap) {
 // their descriptors contiguously.  Returns (to thread 0) the spikes' delivered-event count.
 __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t t, uint32_t b, uint32_t n,
                                   const uint32_t *region, uint64_t *region_rows, uint32_t *stage,
-                                  bool marks = false) {
+                                  bool marks = false, const uint32_t *sid_s = nullptr) {
+    if (sid_s && n <= kSidCap) region = sid_s;          // the spike IDs' shared-memory copy
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t par = (uint32_t)(t & 1);
     // dense per-tile lists: this CTA's n descriptors go to [off, off + n) of every
@@ -618,7 +624,7 @@ template <int MODEL>
 __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                             const uint32_t *cnt, bool write_list, uint32_t *s_count, uint32_t *stage,
                             uint32_t *xsm = nullptr, const StatePtrs *staged = nullptr, bool marks = false,
-                            uint32_t cl_c = kMaxCluster) {
+                            uint32_t cl_c = kMaxCluster, uint32_t *sid_s = nullptr) {
     const StatePtrs sp = staged ? *staged : global_state(a);
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;   // bitmap coverage
@@ -694,7 +700,11 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 const uint32_t j0 = a.G == 1 ? lo + x4 : (uint32_t)local_to_global(lo + x4, a.rank, a.G, a.S);
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    if ((nib >> e) & 1u) region[pos++] = j0 + e;
+                    if ((nib >> e) & 1u) {
+                        region[pos] = j0 + e;
+                        if (sid_s && pos < kSidCap) sid_s[pos] = j0 + e;
+                        ++pos;
+                    }
             }
         }
     }
@@ -747,7 +757,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     }
     if (write_list && (a.desc || a.wl) && !(a.dbg & 4u)) {   // padded layout: delivered events
         const uint64_t dsum = a.wl ? write_windows(a, t, b, n_tile, region, region_rows, stage, marks)
-                                   : write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks);
+                                   : write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
         if (tid == 0 && dsum) a.delivered_cta[b] += dsum;   // are counted here (out-degrees)
     }
     if (marks) phase_mark(a, 9);
@@ -1014,7 +1024,6 @@ __device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t 
 // the ring 64 entries per iteration with lane L taking entries L and L + 32 (consecutive
 // windows of a segment sit in one load instruction and coalesce into one L1 line lookup),
 // the next iteration's two window loads in flight while the current windows are reduced.
-constexpr uint32_t kRing = 512;                        // ring entries per warp (power of 2)
 constexpr uint32_t kRingS = 256;                       // deliver_tile_rs: ring entries per warp
 template <bool WORD>
 __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
@@ -1715,7 +1724,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         phase_mark(a, 6);
         update_tile<MODEL>(a, t + 1, b, lo, a.TWs, cnt, true, &s_count, sm.stage, nullptr, nullptr, true,
-                           a.C > 1 ? c : kMaxCluster);
+                           a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
         if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     } else {
         if (a.C > 1) cluster_reduce_slice(a, sm.cnt, c);   // slice summed in place
@@ -1723,7 +1732,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + lo;
         for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u)
             *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
-        update_tile<MODEL>(a, t + 1, b, lo, a.TWs, nullptr, true, &s_count, sm.stage, nullptr, nullptr, true);
+        update_tile<MODEL>(a, t + 1, b, lo, a.TWs, nullptr, true, &s_count, sm.stage, nullptr, nullptr, true,
+                           kMaxCluster, sm.stage + kStageWords);
         if (a.C > 1) cluster_wait();                     // partners done reading this CTA's counters
     }
     phase_mark(a, 12);
