@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=1000)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--setup", action="store_true",
+                    help="setup-time experiment (PAPER.md Fig. 9): generator throughput vs size, synth density 5%%")
     return ap.parse_args()
 
 
@@ -332,8 +334,59 @@ def main_spice(args):
     return 0
 
 
+SETUP_SIZES = (4_000, 16_000, 64_000, 128_000, 245_000)   # 0.8M .. 3.0e9 synapses at density 5 %
+
+
+def main_setup(args):
+    """Setup time vs network size (Fig. 9: Synth, density 5 %; P:443:
+    "our actual setup kernel generates networks at ~200M synapses/ms").  Two rules at each
+    size: the synth fixed in-degree rule K = 0.05 N (reading R9) and the paper's Bernoulli
+    descriptor {range, range, p = 0.05}.  gen_ms = device time of the generator
+    kernels; create_ms = host wall time of spice_create_network (allocation, generation,
+    state init, graph capture), each the median of `reps` creations after one warm-up."""
+    import torch
+    torch.cuda.set_device(0)
+    from paper_2102_04681_b200 import build as B
+    B.build()
+    from paper_2102_04681_b200 import spice as S
+    points = []
+    reps = 3
+    for n in SETUP_SIZES:
+        k = round(0.05 * n)
+        for kind, cfg in (("fixed_indegree", W.NetConfig(f"setup_indeg{n}", W.SYNTH, n, n,
+                                                          (W.Rule((0, n), (0, n), W.FIXED_INDEGREE, k=k),),
+                                                          0.1, 1, 1, 0.005, ())),
+                          ("fixed_prob", W.NetConfig(f"setup_prob{n}", W.SYNTH, n, n,
+                                                      (W.Rule((0, n), (0, n), W.FIXED_PROB, p=0.05),),
+                                                      0.1, 1, 1, 0.005, ()))):
+            gens, walls, syn = [], [], 0
+            for r in range(reps + 1):
+                with S.Network(cfg, record_steps=8) as net:
+                    t = net.setup_times()
+                    syn = net.info()["n_synapses"]
+                if r:
+                    gens.append(t["gen_ms"])
+                    walls.append(t["create_ms"])
+            g, w = statistics.median(gens), statistics.median(walls)
+            points.append({"n_neurons": n, "rule": kind, "synapses": syn, "gen_ms": g, "create_ms": w,
+                           "gen_synapses_per_ms": syn / g if g else None,
+                           "create_synapses_per_ms": syn / w if w else None})
+            print(f"setup n={n} {kind}: {syn:.3e} synapses, generator {g:.2f} ms ({syn / g / 1e6:.1f}M syn/ms), "
+                  f"create {w:.1f} ms", file=sys.stderr, flush=True)
+    best = max(p["gen_synapses_per_ms"] for p in points if p["gen_synapses_per_ms"])
+    line = {"metric": "setup: synapses generated per ms (generator kernels), synth density 5 %",
+            "value": best, "unit": "synapses/ms", "higher_is_better": True, "n_gpus": 1,
+            "data": "synthetic", "paper_context": "~200M synapses/ms on V100 (PAPER.md:443)",
+            "config": {"workload": "setup_synth_density5pct", "sizes": list(SETUP_SIZES), "reps": reps},
+            "points": points}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse_args()
+    if args.setup:
+        return main_setup(args)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -179,6 +179,13 @@ SPICE_API spice_status spice_info(spice_net *net, uint64_t *n_owned, uint64_t *n
                         uint32_t *n_tiles, uint32_t *tile_width, uint32_t *ctas_per_tile,
                         uint64_t *device_bytes);
 
+/* Setup cost (§IV "Setup Time": "our actual setup kernel generates
+ * networks at ~200M synapses/ms").  gen_ms: device time of the generator kernels of
+ * this slice (count, scan, fill, pad, sort; CUDA events on the library stream, without
+ * allocations or host round trips).  create_ms: host wall time of spice_create_network
+ * (allocation, generation, state init, graph capture).  Either pointer may be NULL. */
+SPICE_API spice_status spice_setup_times(spice_net *net, double *gen_ms, double *create_ms);
+
 /* Run n_steps steps with each kernel launched individually and bracketed by CUDA events
  * on the library stream; writes the average device time per launch in ms:
  * [0] neuron update kernel, [1] delivery kernel, [2] fused deliver(t)+update(t+1) kernel

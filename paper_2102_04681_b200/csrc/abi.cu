@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <chrono>
 #include <vector>
 
 #include "spice.h"
@@ -122,6 +123,7 @@ struct spice_net {
     uint32_t eshift = 0;     // entries hold (tile offset << eshift); 2 when padded
     uint32_t *deg = nullptr; // pad8: true out-degree of every source on this rank
     double mean_seg = 0;
+    double gen_ms = 0, create_ms = 0;   // setup: generator kernels (device), create (host wall)
     uint32_t NR = 1, RS = 32;    // spike-list regions
     uint32_t dcap = 0;           // descriptors staged in shared memory per delivering CTA
     unsigned long long *ptimes = nullptr;   // SPICE_PHASES diagnostics
@@ -382,6 +384,11 @@ spice_status generate(spice_net *n) {
     uint32_t *cursor = nullptr;
     spice_status st;
     if ((st = dalloc_t(n, &n->row_ptr, (size_t)n->N + 1, "row_ptr"))) return st;
+    // generator device time (P:443 quotes the setup kernel's synapses per ms): count,
+    // scan, fill, pad and sort kernels, excluding allocations and host round trips
+    cudaEvent_t eg[4] = {};
+    for (cudaEvent_t &e : eg) cudaEventCreate(&e);
+    struct EvFree { cudaEvent_t *e; ~EvFree() { for (int q = 0; q < 4; ++q) if (e[q]) cudaEventDestroy(e[q]); } } evf{eg};
     if ((st = dalloc_t(n, &n->bnd, nb + 4, "segment bounds"))) return st;   // + 16-byte tail pad
     CU(n, cudaMemsetAsync(n->bnd, 0, (nb + 4) * 4, n->stream));
     // rules in ascending destination order so that per-segment appends stay sorted
@@ -398,7 +405,9 @@ spice_status generate(spice_net *n) {
         gr.push_back(x);
         any_indeg |= R.kind == SPICE_FIXED_INDEGREE && R.k > 0;
     }
+    CU(n, cudaEventRecord(eg[0], n->stream));
     for (const GenRule &x : gr) CU(n, gen_count(g, x, n->bnd, n->stream));
+    CU(n, cudaEventRecord(eg[1], n->stream));
     uint64_t nnz = 0;
     if (n->pad8 && (st = dalloc_t(n, &n->deg, n->N, "out-degrees"))) return st;
     CU(n, gen_scan(g, n->bnd, n->row_ptr, &nnz, n->deg, n->stream));
@@ -410,10 +419,18 @@ spice_status generate(spice_net *n) {
     CU(n, cudaMemsetAsync(n->ent_alloc, 0, ((size_t)nnz + 2 * kEntPad) * 2, n->stream));
     if ((st = dalloc_t(n, &cursor, nb, "fill cursors"))) return st;
     CU(n, cudaMemsetAsync(cursor, 0, nb * 4, n->stream));
+    CU(n, cudaEventRecord(eg[2], n->stream));
     for (const GenRule &x : gr) CU(n, gen_fill(g, x, n->row_ptr, n->bnd, cursor, n->ent, n->stream));
     if (n->pad8) CU(n, gen_pad_segments(g, n->row_ptr, n->bnd, cursor, n->ent, n->stream));
     if (any_indeg) CU(n, gen_sort_segments(g, n->row_ptr, n->bnd, n->ent, n->stream));   // sentinels (>= TW) sort last
+    CU(n, cudaEventRecord(eg[3], n->stream));
     CU(n, cudaStreamSynchronize(n->stream));
+    {
+        float m01 = 0, m23 = 0;
+        cudaEventElapsedTime(&m01, eg[0], eg[1]);
+        cudaEventElapsedTime(&m23, eg[2], eg[3]);
+        n->gen_ms = (double)m01 + (double)m23;
+    }
     if (n->pad8) CU(n, gen_sum_u32(n->deg, n->N, &n->n_syn, n->stream));
     else n->n_syn = nnz;
     dfree(n, cursor);
@@ -490,6 +507,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     *out = nullptr;
     spice_status st = validate(c);
     if (st) return st;
+    const auto t_create = std::chrono::steady_clock::now();
     spice_net *n = new spice_net();
     n->model = c->model; n->N = c->n_neurons; n->n_exc = c->n_exc; n->delay = c->delay_steps;
     n->D = c->delay_steps + 1; n->rank = c->rank; n->G = c->world_size;
@@ -762,7 +780,15 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         if ((st = capture_graph(n, spice_net::kGraphSteps, &n->g_big))) return bail(st);
         if ((st = capture_graph(n, 1, &n->g_one))) return bail(st);
     }
+    n->create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_create).count();
     *out = n;
+    return SPICE_OK;
+}
+
+spice_status spice_setup_times(spice_net *n, double *gen_ms, double *create_ms) {
+    CHECK_NET(n);
+    if (gen_ms) *gen_ms = n->gen_ms;
+    if (create_ms) *create_ms = n->create_ms;
     return SPICE_OK;
 }
 

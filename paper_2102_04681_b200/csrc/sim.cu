@@ -189,11 +189,15 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, const StatePtrs &s
     return spk & valid;
 }
 
-// Diagnostics (SPICE_PHASES=1): thread 0 of every fused-kernel CTA accumulates the SM
+// Diagnostics (SPICE_PHASES=1 with a library built with -DSPICE_PHASES_BUILD=1, see
+// tools/phases.py): thread 0 of every fused-kernel CTA accumulates the SM
 // clock offset of phase boundary `slot` from the kernel start into ptimes[cta*16 + slot];
 // slot 13 counts launches, 14/15 hold %globaltimer at start/end of the last launch.
 __device__ __forceinline__ long long &phase_c0() { __shared__ long long c0; return c0; }
 __device__ __forceinline__ void phase_mark(const SimArgs &a, int slot) {
+#if !SPICE_PHASES_BUILD
+    (void)a; (void)slot;   // compiled out: even predicated-off marks cost issue slots (ncu r01u)
+#else
     if (a.ptimes && threadIdx.x == 0) {
         unsigned long long *p = a.ptimes + blockIdx.x * 16u;
         if (slot == 0) {
@@ -205,6 +209,7 @@ __device__ __forceinline__ void phase_mark(const SimArgs &a, int slot) {
             if (slot == 12) { unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p[15] = g; }
         }
     }
+#endif
 }
 
 // Update every neuron of tile b for step t.  Inputs come from `cnt` (shared memory, the

@@ -76,6 +76,7 @@ def lib():
         "spice_info": (st, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32), C.POINTER(u32),
                             C.POINTER(u32), C.POINTER(u64)]),
         "spice_kernels_per_step": (u32, [vp]),
+        "spice_setup_times": (st, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "spice_debug_phases": (st, [vp, vp, u64, C.POINTER(u64)]),
         "spice_profile": (st, [vp, u64, vp, u32, C.POINTER(u32)]),
         "spice_last_error": (C.c_char_p, []),
@@ -266,6 +267,12 @@ class Network:
         _check(lib().spice_info(self.h, C.byref(o), C.byref(s), C.byref(nt), C.byref(tw), C.byref(c), C.byref(b)))
         return {"n_owned": o.value, "n_synapses": s.value, "n_tiles": nt.value, "tile_width": tw.value,
                 "ctas_per_tile": c.value, "device_bytes": b.value}
+
+    def setup_times(self):
+        """Generator device ms and spice_create_network host wall ms of this slice."""
+        g, w = C.c_double(), C.c_double()
+        _check(lib().spice_setup_times(self.h, C.byref(g), C.byref(w)))
+        return {"gen_ms": g.value, "create_ms": w.value}
 
     def profile(self, n_steps: int):
         """Average device ms per launch, each kernel bracketed by CUDA events on the

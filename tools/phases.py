@@ -5,6 +5,17 @@ import sys
 
 os.environ["SPICE_PHASES"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# the phase clocks are compiled out of the product library: build a variant with them
+_VARIANT = "/tmp/libspice_phases.so"
+if "SPICE_LIB" not in os.environ:
+    import importlib.util  # noqa: E402
+    _spec = importlib.util.spec_from_file_location(
+        "_spice_build", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                     "paper_2102_04681_b200", "build.py"))
+    _B = importlib.util.module_from_spec(_spec)
+    _spec.loader.exec_module(_B)                   # (not via the package: it loads the library)
+    _B.build(out=_VARIANT, defines=["SPICE_PHASES_BUILD=1"])
+    os.environ["SPICE_LIB"] = _VARIANT
 import numpy as np  # noqa: E402
 
 import bench  # noqa: E402
