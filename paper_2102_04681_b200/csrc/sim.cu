@@ -87,19 +87,15 @@ __device__ __forceinline__ StatePtrs global_state(const SimArgs &a) {
 template <int MODEL>
 __device__ __forceinline__ uint32_t update4(const SimArgs &a, const StatePtrs &sp, uint64_t t, uint32_t i0,
                                             const uint32_t c[4], const long long pin[4],
-                                            const uint64_t *ptab, bool acc_done) {
+                                            const uint64_t *ptab, bool acc_done, int forced) {
     const uint32_t li = i0 - sp.base;                  // index into the state arrays
     const ModelConst &m = a.mc;
     const uint32_t j0 = a.G == 1 ? i0 : (uint32_t)local_to_global(i0, a.rank, a.G, a.S);   // multiple of 4
     uint32_t valid = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) valid |= (i0 + e < a.n_own ? 1u : 0u) << e;
-    int forced = 0;
-    uint32_t fbits = 0;
-    if (a.force_ctl[0] == t) {
-        forced = (int)a.force_ctl[1];
-        fbits = (a.force_bits[i0 >> 5] >> (i0 & 31)) & 0xFu;
-    }
+    uint32_t fbits = 0;                                // forced: teacher-forcing mode of step t
+    if (forced) fbits = (a.force_bits[i0 >> 5] >> (i0 & 31)) & 0xFu;
     uint32_t spk = 0;
     if (MODEL == 4) {                                   // Synth (reading R12)
         const uint4 x = philox4x32_10(make_uint4(j0 >> 2, (uint32_t)t, 0u, kTagFire), a.key0, a.key1);
@@ -625,7 +621,10 @@ __device__ __forceinline__ uint64_t write_windows(const SimArgs &a, uint64_t t, 
 // cluster tile); b is the CTA's spike-list region / counter slot.
 // cl_c < kMaxCluster: cnt is this CTA's slice of a cluster tile whose C = a.C CTAs each hold
 // partial counts for it; the update adds the peers' partials (distributed shared memory).
-template <int MODEL>
+// DESC = true: compile only the padded-layout descriptor path (the fused G = 1 kernel's
+// variants), keeping the inlined code on the hot path small (instruction-fetch stalls were
+// the largest stall class of the fused kernel, ncu r01u).
+template <int MODEL, bool DESC = false>
 __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                             const uint32_t *cnt, bool write_list, uint32_t *s_count, uint32_t *stage,
                             uint32_t *xsm = nullptr, const StatePtrs *staged = nullptr, bool marks = false,
@@ -648,6 +647,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
         __syncthreads();
     }
     const bool acc_done = false;
+    const int forced = a.force_ctl[0] == t ? (int)a.force_ctl[1] : 0;   // once per CTA, not per neuron
     for (uint32_t x0 = 0; x0 < span; x0 += 4u * kBlock) {      // uniform trip count per CTA
         const uint32_t x4 = x0 + 4u * tid;
         uint32_t nib = 0;
@@ -684,7 +684,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
                 c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
             }
-            nib = update4<MODEL>(a, sp, t, lo + x4, c, pin, ptab, acc_done);
+            nib = update4<MODEL>(a, sp, t, lo + x4, c, pin, ptab, acc_done, forced);
         }
         // 8 lanes x 4 bits -> one 32-neuron bitmap word
         uint32_t w = nib << (4u * (lane & 7u));
@@ -732,7 +732,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
         if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
         a.fired_cta[b] += n_tile;
     }
-    if (write_list && !a.desc && !a.wl) {                 // row starts of the spikes, all at once
+    if (!DESC && write_list && !a.desc && !a.wl) {        // row starts of the spikes, all at once
         uint32_t dsum = 0;                                // (the descriptor pass loads them itself)
         for (uint32_t q = tid; q < n_tile; q += kBlock) {
             const uint32_t s = region[q];
@@ -747,7 +747,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
         __syncthreads();
     }
     if (marks) phase_mark(a, 8);
-    if (write_list && (a.dbg & 8u) == 0 && a.pf_rows) {
+    if (!DESC && write_list && (a.dbg & 8u) == 0 && a.pf_rows) {
         // TMA L2 prefetch of every spiking row (contiguous, ~rowlen * 2 bytes): the next
         // launch's delivery reads these rows as scattered 16-byte windows from ~all CTAs;
         // pulling each row into L2 with one bulk request turns those into L2 hits.
@@ -760,13 +760,18 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a.ent + lo), "r"((uint32_t)(hi - lo) * 2u) : "memory");
         }
     }
-    if (write_list && (a.desc || a.wl) && !(a.dbg & 4u)) {   // padded layout: delivered events
+    if (DESC) {
+        if (write_list && !(a.dbg & 4u)) {
+            const uint64_t dsum = write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
+            if (tid == 0 && dsum) a.delivered_cta[b] += dsum;
+        }
+    } else if (write_list && (a.desc || a.wl) && !(a.dbg & 4u)) {   // padded layout: delivered events
         const uint64_t dsum = a.wl ? write_windows(a, t, b, n_tile, region, region_rows, stage, marks)
                                    : write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
         if (tid == 0 && dsum) a.delivered_cta[b] += dsum;   // are counted here (out-degrees)
     }
     if (marks) phase_mark(a, 9);
-    if constexpr (MODEL != 3) {
+    if constexpr (MODEL != 3 && !DESC) {
         if (write_list && a.xbuf) {
             uint32_t phase = 0;
             exchange_produce(a, par, b, region, region_rows, n_tile, carve_x(a, xsm), phase);
@@ -1032,7 +1037,8 @@ __device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t 
 constexpr uint32_t kRingS = 256;                       // deliver_tile_rs: ring entries per warp
 template <bool WORD>
 __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
-                                                  uint32_t *cnt, uint32_t *ring_base, bool marks = false) {
+                                                  uint32_t *cnt, uint32_t *ring_base, bool marks = false,
+                                                  uint32_t pre_total = 0xFFFFFFFFu) {
     constexpr uint32_t NW = kBlock / 32;
     constexpr uint32_t NONE = 0xFFFFFFFFu;
     constexpr uint32_t FULL = 0xFFFFFFFFu;
@@ -1041,7 +1047,7 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
     const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
     __shared__ uint32_t s_total;
     if (tid == 0) {
-        s_total = a.dcount[t % 3];
+        s_total = pre_total != 0xFFFFFFFFu ? pre_total : a.dcount[t % 3];   // (preloaded by thread 0)
         if (b == 0 && c == 0) a.dcount[(t + 2) % 3] = 0u;     // next user: step t + 2's producers
     }
     __syncthreads();
@@ -1465,7 +1471,8 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
 // Padded-layout delivery of tile b (CTA c of C): staged ring (a.rstages stages) or the
 // register ring; byte-offset or counter-index entries.
 __device__ __forceinline__ void deliver_padded(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
-                                               uint32_t *cnt, uint32_t *big, bool marks = false) {
+                                               uint32_t *cnt, uint32_t *big, bool marks = false,
+                                               uint32_t pre_total = 0xFFFFFFFFu) {
     if (a.rstages == 8) {
         if (a.eshift) deliver_tile_rs<false, 8>(a, t, b, c, cnt, big, marks);
         else deliver_tile_rs<true, 8>(a, t, b, c, cnt, big, marks);
@@ -1473,8 +1480,8 @@ __device__ __forceinline__ void deliver_padded(const SimArgs &a, uint64_t t, uin
         if (a.eshift) deliver_tile_rs<false, 4>(a, t, b, c, cnt, big, marks);
         else deliver_tile_rs<true, 4>(a, t, b, c, cnt, big, marks);
     } else {
-        if (a.eshift) deliver_tile_ring<false>(a, t, b, c, cnt, big, marks);
-        else deliver_tile_ring<true>(a, t, b, c, cnt, big, marks);
+        if (a.eshift) deliver_tile_ring<false>(a, t, b, c, cnt, big, marks, pre_total);
+        else deliver_tile_ring<true>(a, t, b, c, cnt, big, marks, pre_total);
     }
 }
 
@@ -1656,9 +1663,25 @@ __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int MODEL, int GS>
+// Fused-kernel variants (MODEL != 3; for Brunel+ the second parameter is the lane group GS).
+enum : int { kVXchg = 0, kVWlist = 1, kVRingB = 2, kVRingW = 3, kVRs8B = 4, kVRs8W = 5, kVRs4B = 6, kVRs4W = 7 };
+
+template <int V>
+__device__ __forceinline__ void deliver_variant(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+                                                uint32_t *cnt, uint32_t *big, uint32_t pre_total) {
+    if constexpr (V == kVWlist) deliver_tile_wl(a, t, b, 0, cnt, true);
+    else if constexpr (V == kVRingB) deliver_tile_ring<false>(a, t, b, c, cnt, big, true, pre_total);
+    else if constexpr (V == kVRingW) deliver_tile_ring<true>(a, t, b, c, cnt, big, true, pre_total);
+    else if constexpr (V == kVRs8B) deliver_tile_rs<false, 8>(a, t, b, c, cnt, big, true);
+    else if constexpr (V == kVRs8W) deliver_tile_rs<true, 8>(a, t, b, c, cnt, big, true);
+    else if constexpr (V == kVRs4B) deliver_tile_rs<false, 4>(a, t, b, c, cnt, big, true);
+    else deliver_tile_rs<true, 4>(a, t, b, c, cnt, big, true);
+}
+
+template <int MODEL, int V>
 __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
     if constexpr (MODEL == 3) {                             // Brunel+ (delay >= 1 via the rings)
+        constexpr int GS = V;
         extern __shared__ __align__(16) uint32_t smem[];
         PlasticSmem sm = carve_plastic(a, smem);
         __shared__ uint32_t s_count3;
@@ -1678,15 +1701,13 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         phase_mark(a, 6);
         update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count3, sm.stage, nullptr, nullptr, true);
         phase_mark(a, 12);
-    } else {
-    extern __shared__ __align__(16) uint32_t smem[];
-    DeliverSmem sm = carve(a, smem);
-    __shared__ uint32_t s_count;
-    const uint64_t t = *a.t0 + k;
-    const uint32_t b = blockIdx.x;
-    if (threadIdx.x == 0) s_count = 0;
-    if (a.xbuf) {                                        // tile-pair exchange
+    } else if constexpr (V == kVXchg) {                    // tile-pair exchange (experimental)
+        extern __shared__ __align__(16) uint32_t smem[];
+        __shared__ uint32_t s_count;
         __shared__ uint32_t s_tmp[32];
+        const uint64_t t = *a.t0 + k;
+        const uint32_t b = blockIdx.x;
+        if (threadIdx.x == 0) s_count = 0;
         uint32_t *cnt = smem;
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) cnt[x] = 0u;
         __syncthreads();
@@ -1701,47 +1722,55 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             __syncthreads();
             update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count, nullptr, smem);
         }
-        return;
-    }
-    // tile bt = blockIdx.x / C; with C > 1 this CTA is rank c of the tile's cluster
-    const uint32_t bt = b / a.C, c = b % a.C;
-    phase_mark(a, 0);
-    if (threadIdx.x == 0 && a.delay == 1) {   // this slice's neuron state -> L2 while delivering
-        const uint32_t lo0 = b * a.TWs, nb = a.TWs * 4u;
-        const void *arr[4] = {MODEL == 4 ? (const void *)(a.acc + lo0) : (const void *)(a.v + lo0),
-                              MODEL == 4 ? nullptr : (const void *)(a.ref + lo0),
-                              MODEL == 1 ? (const void *)(a.ge + lo0) : nullptr,
-                              MODEL == 1 ? (const void *)(a.gi + lo0) : nullptr};
+    } else {                                                 // padded layout (G = 1)
+        extern __shared__ __align__(16) uint32_t smem[];
+        DeliverSmem sm = carve(a, smem);
+        __shared__ uint32_t s_count;
+        const uint64_t t = *a.t0 + k;
+        const uint32_t b = blockIdx.x;
+        if (threadIdx.x == 0) s_count = 0;
+        // tile bt = blockIdx.x / C; with C > 1 this CTA is rank c of the tile's cluster
+        const uint32_t bt = b / a.C, c = b % a.C;
+        phase_mark(a, 0);
+        // thread 0: the step's descriptor count, loaded before the counters are zeroed
+        const uint32_t pre_total = (threadIdx.x == 0 && V != kVWlist) ? a.dcount[t % 3] : 0xFFFFFFFFu;
+        if (threadIdx.x == 0 && a.delay == 1) {   // this slice's neuron state -> L2 while delivering
+            const uint32_t lo0 = b * a.TWs, nb = a.TWs * 4u;
+            const void *arr[4] = {MODEL == 4 ? (const void *)(a.acc + lo0) : (const void *)(a.v + lo0),
+                                  MODEL == 4 ? nullptr : (const void *)(a.ref + lo0),
+                                  MODEL == 1 ? (const void *)(a.ge + lo0) : nullptr,
+                                  MODEL == 1 ? (const void *)(a.gi + lo0) : nullptr};
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (arr[q]) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(arr[q]), "r"(nb) : "memory");
-    }
-    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
-    __syncthreads();
-    phase_mark(a, 1);
-    if (a.wl) deliver_tile_wl(a, t, bt, 0, sm.cnt, true);
-    else deliver_padded(a, t, bt, c, sm.cnt, sm.stage, true);
-    uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice
-    const uint32_t lo = b * a.TWs;
-    if (a.delay == 1) {
-        // C > 1: the update sums the C partial slices itself (peers read after one cluster
-        // barrier; a second one at exit keeps every CTA's counters alive until then)
-        if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        phase_mark(a, 6);
-        update_tile<MODEL>(a, t + 1, b, lo, a.TWs, cnt, true, &s_count, sm.stage, nullptr, nullptr, true,
-                           a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
-        if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    } else {
-        if (a.C > 1) cluster_reduce_slice(a, sm.cnt, c);   // slice summed in place
-        phase_mark(a, 6);
-        uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + lo;
-        for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u)
-            *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
-        update_tile<MODEL>(a, t + 1, b, lo, a.TWs, nullptr, true, &s_count, sm.stage, nullptr, nullptr, true,
-                           kMaxCluster, sm.stage + kStageWords);
-        if (a.C > 1) cluster_wait();                     // partners done reading this CTA's counters
-    }
-    phase_mark(a, 12);
+            for (int q = 0; q < 4; ++q)
+                if (arr[q]) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(arr[q]), "r"(nb) : "memory");
+        }
+        for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)      // TW is a multiple of 32
+            *reinterpret_cast<uint4 *>(sm.cnt + x) = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+        phase_mark(a, 1);
+        deliver_variant<V>(a, t, bt, c, sm.cnt, sm.stage, pre_total);
+        uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice
+        const uint32_t lo = b * a.TWs;
+        constexpr bool DESC = V != kVWlist;
+        if (a.delay == 1) {
+            // C > 1: the update sums the C partial slices itself (peers read after one cluster
+            // barrier; a second one at exit keeps every CTA's counters alive until then)
+            if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+            phase_mark(a, 6);
+            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, true, &s_count, sm.stage, nullptr, nullptr, true,
+                                     a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
+            if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        } else {
+            if (a.C > 1) cluster_reduce_slice(a, sm.cnt, c);   // slice summed in place
+            phase_mark(a, 6);
+            uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + lo;
+            for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u)
+                *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
+            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, true, &s_count, sm.stage, nullptr, nullptr, true,
+                                     kMaxCluster, sm.stage + kStageWords);
+            if (a.C > 1) cluster_wait();                     // partners done reading this CTA's counters
+        }
+        phase_mark(a, 12);
     }
 }
 
@@ -1859,8 +1888,9 @@ cudaError_t prepare_kernels(const SimArgs &a) {
 #define ALLOW(kern) if (!e) e = allow_smem(kern, bytes)
     ALLOW(k_deliver<1>); ALLOW(k_deliver<2>); ALLOW(k_deliver<4>); ALLOW(k_deliver<8>);
     ALLOW(k_deliver<16>); ALLOW(k_deliver<32>);
-#define ALLOW_M(M) ALLOW((k_fused<M, 1>)); ALLOW((k_fused<M, 2>)); ALLOW((k_fused<M, 4>)); \
-    ALLOW((k_fused<M, 8>)); ALLOW((k_fused<M, 16>)); ALLOW((k_fused<M, 32>))
+#define ALLOW_M(M) ALLOW((k_fused<M, kVXchg>)); ALLOW((k_fused<M, kVWlist>)); ALLOW((k_fused<M, kVRingB>)); \
+    ALLOW((k_fused<M, kVRingW>)); ALLOW((k_fused<M, kVRs8B>)); ALLOW((k_fused<M, kVRs8W>)); \
+    ALLOW((k_fused<M, kVRs4B>)); ALLOW((k_fused<M, kVRs4W>))
     ALLOW_M(1); ALLOW_M(2); ALLOW_M(4);
     ALLOW(k_global_atomics);
     if (a.model == 3) {
@@ -1921,6 +1951,15 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
     return cudaGetLastError();
 }
 
+static int fused_variant(const SimArgs &a) {
+    if (a.xbuf) return kVXchg;
+    if (a.wl) return kVWlist;
+    const bool w = a.eshift == 0;
+    if (a.rstages == 8) return w ? kVRs8W : kVRs8B;
+    if (a.rstages == 4) return w ? kVRs4W : kVRs4B;
+    return w ? kVRingW : kVRingB;
+}
+
 // C > 1: the C CTAs of a tile are launched as one thread-block cluster.
 template <typename K>
 static void launch_cluster(K kern, const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
@@ -1939,26 +1978,35 @@ static void launch_cluster(K kern, const SimArgs &a, uint32_t k, size_t bytes, c
     cudaLaunchKernelEx(&cfg, kern, a, k);
 }
 
+template <int M, int V>
+static void fused_v(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
+    if (a.C > 1) launch_cluster(k_fused<M, V>, a, k, bytes, s);
+    else k_fused<M, V><<<a.NT, kBlock, bytes, s>>>(a, k);
+}
+
 template <int M>
 static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
-    if (a.C > 1) {
+    if constexpr (M == 3) {                               // Brunel+: lane groups (C = 1)
         switch (a.GS) {
-        case 1: launch_cluster(k_fused<M, 1>, a, k, bytes, s); break;
-        case 2: launch_cluster(k_fused<M, 2>, a, k, bytes, s); break;
-        case 4: launch_cluster(k_fused<M, 4>, a, k, bytes, s); break;
-        case 8: launch_cluster(k_fused<M, 8>, a, k, bytes, s); break;
-        case 16: launch_cluster(k_fused<M, 16>, a, k, bytes, s); break;
-        default: launch_cluster(k_fused<M, 32>, a, k, bytes, s); break;
+        case 1: k_fused<M, 1><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+        case 2: k_fused<M, 2><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+        case 4: k_fused<M, 4><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+        case 8: k_fused<M, 8><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+        case 16: k_fused<M, 16><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+        default: k_fused<M, 32><<<a.NT, kBlock, bytes, s>>>(a, k); break;
         }
         return;
-    }
-    switch (a.GS) {
-    case 1: k_fused<M, 1><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-    case 2: k_fused<M, 2><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-    case 4: k_fused<M, 4><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-    case 8: k_fused<M, 8><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-    case 16: k_fused<M, 16><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-    default: k_fused<M, 32><<<a.NT, kBlock, bytes, s>>>(a, k); break;
+    } else {
+        switch (fused_variant(a)) {
+        case kVXchg: fused_v<M, kVXchg>(a, k, bytes, s); break;
+        case kVWlist: fused_v<M, kVWlist>(a, k, bytes, s); break;
+        case kVRingB: fused_v<M, kVRingB>(a, k, bytes, s); break;
+        case kVRingW: fused_v<M, kVRingW>(a, k, bytes, s); break;
+        case kVRs8B: fused_v<M, kVRs8B>(a, k, bytes, s); break;
+        case kVRs8W: fused_v<M, kVRs8W>(a, k, bytes, s); break;
+        case kVRs4B: fused_v<M, kVRs4B>(a, k, bytes, s); break;
+        default: fused_v<M, kVRs4W>(a, k, bytes, s); break;
+        }
     }
 }
 
