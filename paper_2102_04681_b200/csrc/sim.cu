@@ -59,6 +59,12 @@ __device__ __forceinline__ void block_exclusive_scan(uint32_t *arr, uint32_t n, 
     __syncthreads();
 }
 
+// t mod m for a step counter: 32-bit remainder while t < 2^32 (the 64-bit remainder is a
+// ~100-instruction subroutine every thread would run once per launch)
+__device__ __forceinline__ uint64_t mod32(uint64_t t, uint32_t m) {
+    return (t >> 32) ? t % m : (uint64_t)((uint32_t)t % m);
+}
+
 __device__ __forceinline__ uint4 ld_stream_v4(const uint16_t *p) {
     uint4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -635,8 +641,8 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     const uint32_t par = (uint32_t)(t & 1);
     uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
     uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + b) * a.RS;
-    uint32_t *bm = a.G == 1 ? a.record + (t % a.record_steps) * (uint64_t)a.W : a.sendbuf;
-    uint32_t *ring_slot = a.ring + (t % a.D) * a.ring_stride + lo;
+    uint32_t *bm = a.G == 1 ? a.record + mod32(t, a.record_steps) * (uint64_t)a.W : a.sendbuf;
+    uint32_t *ring_slot = a.ring + mod32(t, a.D) * a.ring_stride + lo;
     // Brunel drive: the Poisson inversion table in shared memory (the walk is a chain of
     // dependent loads per neuron)
     __shared__ uint64_t s_ptab[kPtabSmem];
@@ -649,6 +655,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     const bool acc_done = false;
     const int forced = a.force_ctl[0] == t ? (int)a.force_ctl[1] : 0;   // once per CTA, not per neuron
     for (uint32_t x0 = 0; x0 < span; x0 += 4u * kBlock) {      // uniform trip count per CTA
+        if (x0 + 4u * (tid & ~31u) >= span) continue;             // whole warp past the slice
         const uint32_t x4 = x0 + 4u * tid;
         uint32_t nib = 0;
         const bool act = x4 < span && lo + x4 < a.n_own;
@@ -656,7 +663,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
             uint32_t c[4];
             long long pin[4] = {0, 0, 0, 0};
             if (MODEL == 3) {
-                long long *ps = a.pring + (t % a.D) * a.ring_stride + lo + x4;
+                long long *ps = a.pring + mod32(t, a.D) * a.ring_stride + lo + x4;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) { pin[e] = ps[e]; ps[e] = 0; }
             }
@@ -664,18 +671,16 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 uint4 cv = *reinterpret_cast<const uint4 *>(cnt + x4);
                 if (cl_c < kMaxCluster) {
                     const uint32_t la = (uint32_t)__cvta_generic_to_shared(cnt + x4);
-#pragma unroll
-                    for (uint32_t k = 1; k < kMaxCluster; ++k) {
-                        if (k < a.C) {
-                            uint32_t peer = cl_c + k;
-                            if (peer >= a.C) peer -= a.C;
-                            uint32_t ra;
-                            uint4 v;
-                            asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(peer));
-                            asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ra));
-                            cv.x += v.x; cv.y += v.y; cv.z += v.z; cv.w += v.w;
-                        }
+#pragma unroll 1
+                    for (uint32_t k = 1; k < a.C; ++k) {
+                        uint32_t peer = cl_c + k;
+                        if (peer >= a.C) peer -= a.C;
+                        uint32_t ra;
+                        uint4 v;
+                        asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(peer));
+                        asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ra));
+                        cv.x += v.x; cv.y += v.y; cv.z += v.z; cv.w += v.w;
                     }
                 }
                 c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
@@ -1299,7 +1304,7 @@ __device__ __forceinline__ void deliver_tile_wl(const SimArgs &a, uint64_t t, ui
 // (iii) traces advance x(t+1) = a+ (x(t) + s(t)), y likewise.  Every synapse touched by
 // CTA b has its target in tile b, so no two CTAs write the same weight.
 __device__ __forceinline__ const uint32_t *step_bitmap(const SimArgs &a, uint64_t t) {
-    return a.record + (t % a.record_steps) * (uint64_t)a.G * a.W + (uint64_t)a.rank * a.W;
+    return a.record + mod32(t, a.record_steps) * (uint64_t)a.G * a.W + (uint64_t)a.rank * a.W;
 }
 
 __device__ __forceinline__ bool plastic_src(const SimArgs &a, uint32_t s) {
@@ -1401,7 +1406,7 @@ __device__ __forceinline__ void stdp_traces(const SimArgs &a, uint64_t t, uint32
     float *xn = a.xtr + ((t + 1) & 1) * (uint64_t)a.N;
     const uint32_t per = (a.N + a.NT * a.C - 1) / (a.NT * a.C);
     const uint32_t j0 = blockIdx.x * per, j1 = min(a.N, j0 + per);
-    const uint32_t *gbm = a.record + (t % a.record_steps) * (uint64_t)a.G * a.W;
+    const uint32_t *gbm = a.record + mod32(t, a.record_steps) * (uint64_t)a.G * a.W;
     for (uint32_t j = j0 + threadIdx.x; j < j1; j += kBlock) {
         const uint32_t r = (j / a.S) % a.G;
         const uint32_t il = (j / a.S / a.G) * a.S + j % a.S;
@@ -1568,7 +1573,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) smem[x] = 0u;
         __syncthreads();
         const uint32_t d = exchange_consume(a, (uint32_t)(t & 1), b, smem);
-        uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
+        uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u) {
             uint4 o = *reinterpret_cast<uint4 *>(dst + x);
             o.x += smem[x]; o.y += smem[x + 1]; o.z += smem[x + 2]; o.w += smem[x + 3];
@@ -1589,7 +1594,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
         d = 0;
     }
     else d = deliver_tile<GS>(a, t, b, c, sm);
-    uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
+    uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
     if (a.C == 1u) {
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u) {
             uint4 o = *reinterpret_cast<uint4 *>(dst + x);
@@ -1622,7 +1627,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver_plastic(SimArgs a, uint32_t 
     const uint32_t b = blockIdx.x;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.pin[x] = 0; }
     const uint32_t d = deliver_tile_plastic<GS>(a, t, b, sm.cnt, sm.pin, sm.pref, sm.tmp, sm.stage);
-    const uint64_t base = ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
+    const uint64_t base = mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
         a.ring[base + x] += sm.cnt[x];
         a.pring[base + x] += sm.pin[x];
@@ -1691,7 +1696,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         if (threadIdx.x == 0) s_count3 = 0;
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.pin[x] = 0; }
         const uint32_t d = deliver_tile_plastic<GS>(a, t, b, sm.cnt, sm.pin, sm.pref, sm.tmp, sm.stage, true);
-        const uint64_t base = ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
+        const uint64_t base = mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
             a.ring[base + x] += sm.cnt[x];
             a.pring[base + x] += sm.pin[x];
@@ -1716,7 +1721,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         if (a.delay == 1) {
             update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, cnt, true, &s_count, nullptr, smem);
         } else {
-            uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + (uint64_t)b * a.TW;
+            uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
             for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)
                 *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
             __syncthreads();
@@ -1763,7 +1768,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         } else {
             if (a.C > 1) cluster_reduce_slice(a, sm.cnt, c);   // slice summed in place
             phase_mark(a, 6);
-            uint32_t *dst = a.ring + ((t + a.delay) % a.D) * a.ring_stride + lo;
+            uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + lo;
             for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u)
                 *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
             update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, true, &s_count, sm.stage, nullptr, nullptr, true,
@@ -1787,7 +1792,7 @@ __global__ void __launch_bounds__(kBlock) k_global_atomics(SimArgs a, uint32_t k
     const uint32_t n_sp = pref[a.NR];
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
-    uint32_t *slot = a.ring + ((t + a.delay) % a.D) * a.ring_stride;
+    uint32_t *slot = a.ring + mod32(t + a.delay, a.D) * a.ring_stride;
     const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
     uint32_t delivered = 0;
     for (uint64_t w = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); w < (uint64_t)a.NT * n_sp; w += nwarps) {
@@ -1823,7 +1828,7 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
         const uint32_t idx = r * kB2LWords + q0 + threadIdx.x;
         const bool in = q0 + threadIdx.x < kB2LWords && idx < nw;
         const uint32_t word = in ? a.gather[idx] : 0u;
-        if (in) a.record[(t % a.record_steps) * (uint64_t)nw + idx] = word;
+        if (in) a.record[mod32(t, a.record_steps) * (uint64_t)nw + idx] = word;
         const uint32_t cnt = __popc(word), incl = warp_incl_scan(cnt);
         const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
         uint32_t base = 0;
