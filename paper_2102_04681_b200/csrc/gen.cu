@@ -239,7 +239,59 @@ __global__ void scan_apply(const uint64_t *in, uint64_t n, const uint64_t *sums,
     if (i == n - 1) out[n] = sums[blockIdx.x] + buf[threadIdx.x];
 }
 
-// Insertion sort of each (row, tile) segment (fixed in-degree fills out of order).
+// Segment sort, one warp per (row, tile) segment of length in (lo, 32 R]: a bitonic
+// network over 32 R keys in registers (key lane + 32 r in k[r]; missing keys are 0x10000
+// and sort last).  R = 2 takes segments of 2..64 entries, R = 4 those of 65..128, and
+// sort_segments_kernel the rest (fixed in-degree fills segments out of order).
+template <int R>
+__global__ void __launch_bounds__(256) sort_segments_warp_kernel(GenGeom g, const uint64_t *row_ptr,
+                                                                 const uint32_t *bnd, uint16_t *ent,
+                                                                 uint32_t lo) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t total = (uint64_t)g.N * g.NT;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; w < total; w += nwarps) {
+        const uint32_t s = (uint32_t)(w / g.NT), b = (uint32_t)(w % g.NT);
+        const uint64_t seg = (uint64_t)s * (g.NT + 1) + b;
+        const uint32_t b0 = bnd[seg], b1 = bnd[seg + 1];
+        const uint32_t len = b1 - b0;
+        if (len <= lo || len > 32u * R) continue;            // warp-uniform
+        uint16_t *p = ent + row_ptr[s] + b0;
+        uint32_t k[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) k[r] = lane + 32u * r < len ? p[lane + 32u * r] : 0x10000u;
+#pragma unroll
+        for (uint32_t size = 2; size <= 32u * R; size <<= 1) {
+#pragma unroll
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                if (stride >= 32) {                          // partner in register r ^ (stride / 32)
+                    const uint32_t rs = stride / 32;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        if (r & rs) continue;
+                        const int r2 = r | (int)rs;
+                        const bool up = ((lane + 32u * r) & size) == 0;
+                        const uint32_t a = min(k[r], k[r2]), z = max(k[r], k[r2]);
+                        k[r] = up ? a : z;
+                        k[r2] = up ? z : a;
+                    }
+                } else {
+                    const bool lower = (lane & stride) == 0;     // this element has the lower index
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, k[r], stride);
+                        const bool up = ((lane + 32u * r) & size) == 0;
+                        k[r] = (lower == up) ? min(k[r], o) : max(k[r], o);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) if (lane + 32u * r < len) p[lane + 32u * r] = (uint16_t)k[r];
+    }
+}
+
+// Insertion sort, one thread per (row, tile) segment longer than 128 entries.
 __global__ void __launch_bounds__(256) sort_segments_kernel(GenGeom g, const uint64_t *row_ptr,
                                                             const uint32_t *bnd, uint16_t *ent) {
     const uint64_t total = (uint64_t)g.N * g.NT;
@@ -248,7 +300,7 @@ __global__ void __launch_bounds__(256) sort_segments_kernel(GenGeom g, const uin
         const uint32_t s = (uint32_t)(w / g.NT), b = (uint32_t)(w % g.NT);
         const uint64_t seg = (uint64_t)s * (g.NT + 1) + b;
         const uint32_t b0 = bnd[seg], b1 = bnd[seg + 1];
-        if (b1 - b0 < 2) continue;
+        if (b1 - b0 <= 128) continue;                        // (sorted by the warp kernels)
         uint16_t *p = ent + row_ptr[s] + b0;
         const uint32_t len = b1 - b0;
         for (uint32_t x = 1; x < len; ++x) {
@@ -357,6 +409,8 @@ cudaError_t gen_sum_u32(const uint32_t *x, uint64_t n, uint64_t *out_host, cudaS
 
 cudaError_t gen_sort_segments(const GenGeom &g, const uint64_t *row_ptr, const uint32_t *bnd,
                               uint16_t *ent, cudaStream_t s) {
+    sort_segments_warp_kernel<2><<<grid_for((uint64_t)g.N * g.NT * 32, 256), 256, 0, s>>>(g, row_ptr, bnd, ent, 1u);
+    sort_segments_warp_kernel<4><<<grid_for((uint64_t)g.N * g.NT * 32, 256), 256, 0, s>>>(g, row_ptr, bnd, ent, 64u);
     sort_segments_kernel<<<grid_for((uint64_t)g.N * g.NT, 256), 256, 0, s>>>(g, row_ptr, bnd, ent);
     return cudaGetLastError();
 }
