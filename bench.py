@@ -46,6 +46,8 @@ def parse_args():
     ap.add_argument("--tile-width", type=int, default=0)
     ap.add_argument("--ctas-per-tile", type=int, default=0)
     ap.add_argument("--global-atomics", action="store_true", help="paper-style delivery (A/B)")
+    ap.add_argument("--unfused", action="store_true",
+                    help="separate update and delivery launches per step (the G > 1 kernel sequence, A/B)")
     ap.add_argument("--profile-steps", type=int, default=200)
     ap.add_argument("--e2e-steps", type=int, default=1000)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -209,7 +211,7 @@ def main_spice(args):
     t0 = time.perf_counter()
     net = S.Network(cfg, rank=rank, world_size=world, device=local, nccl_id=nccl_id,
                     record_steps=record, global_atomics=args.global_atomics,
-                    tile_width=args.tile_width, ctas_per_tile=args.ctas_per_tile)
+                    tile_width=args.tile_width, ctas_per_tile=args.ctas_per_tile, unfused=args.unfused)
     setup_s = time.perf_counter() - t0
     info = net.info()
 

@@ -540,7 +540,8 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // C CTAs per tile (ctas_per_tile): the tile is cut into C slices of TWs = TW / C targets
     // (multiples of 32); CTA x updates slice x.  On the fused G = 1 path the C CTAs form a
     // thread-block cluster that reduces the tile's counters through distributed shared memory.
-    n->pad8 = n->G == 1 && n->model != SPICE_BRUNEL_PLUS && !getenv("SPICE_XCHG") && !getenv("SPICE_NOPAD");
+    // (G > 1: the bitmap->list kernel writes the descriptors of the gathered spikes)
+    n->pad8 = n->model != SPICE_BRUNEL_PLUS && !getenv("SPICE_XCHG") && !getenv("SPICE_NOPAD");
     // auto: 2-CTA cluster tiles for large padded networks (half the spike x tile visits per
     // CTA; measured -4 % step time on synth 3e9, DESIGN.md delivery log), else one CTA per tile
     n->C = c->ctas_per_tile ? c->ctas_per_tile
@@ -716,9 +717,11 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // through per-warp window rings (default), or per-tile window lists written by the
     // producers (SPICE_WLIST=1; measured slower: the window writes cost the producer more
     // than the consumer saves, DESIGN.md delivery log)
-    const bool segdesc = !(getenv("SPICE_WLIST") && atoi(getenv("SPICE_WLIST"))) || n->eshift == 0 || n->C > 1;
+    const bool segdesc = !(getenv("SPICE_WLIST") && atoi(getenv("SPICE_WLIST"))) || n->eshift == 0 || n->C > 1 || n->G > 1;
     if (n->pad8 && !n->xbuf && segdesc) {
-        if ((st = dalloc_t(n, &n->desc, 2ull * n->NT * ((n->n_own + 1) & ~1ull), "segment descriptors"))) return bail(st);
+        // a tile's list holds every spike of the step: the rank's own (G = 1) or all N (G > 1)
+        const uint64_t dstride = ((n->G == 1 ? n->n_own : (uint64_t)n->N) + 1) & ~1ull;
+        if ((st = dalloc_t(n, &n->desc, 2ull * n->NT * dstride, "segment descriptors"))) return bail(st);
         if ((st = dalloc_t(n, &n->dcount, 4, "descriptor counters"))) return bail(st);
         CU(n, cudaMemset(n->dcount, 0, 16));
     } else if (n->pad8 && !n->xbuf) {
@@ -766,7 +769,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.row_ptr = n->row_ptr; a.bnd = n->bnd; a.ent = n->ent; a.deg = n->deg; a.eshift = n->eshift;
     a.v = n->v; a.ge = n->ge; a.gi = n->gi; a.ref = n->ref; a.acc = n->acc; a.ring = n->ring;
     a.sl_ids = n->sl_ids; a.sl_rows = n->sl_rows; a.sl_counts = n->sl_counts; a.desc = n->desc;
-    a.dstride = (n->n_own + 1) & ~1ull; a.dcount = n->dcount;
+    a.dstride = ((n->G == 1 ? n->n_own : (uint64_t)n->N) + 1) & ~1ull; a.dcount = n->dcount;
     a.wl = n->wl; a.wstride = n->wstride; a.wcount = n->wcount;
     a.xbuf = n->xbuf; a.xoff = n->xoff; a.xcnt = n->xcnt; a.xtotal = n->xtotal; a.xrows_bytes = kXRowsBytes; a.record = n->record; a.sendbuf = n->sendbuf;
     a.gather = n->gather; a.fired_cta = n->fired_cta; a.delivered_cta = n->delivered_cta;

@@ -1849,7 +1849,16 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) a.sl_counts[par * a.NR + r] = s_count;
+    const uint32_t n = s_count;
+    if (threadIdx.x == 0) a.sl_counts[par * a.NR + r] = n;
+    if (a.desc) {
+        // padded layout (G > 1): the region's spikes -> transposed segment descriptors of
+        // every local tile, as the G = 1 update writes them for its own spikes; the
+        // delivered events on this rank (out-degrees onto local targets) are counted here
+        extern __shared__ __align__(16) uint32_t stage[];
+        const uint64_t dsum = write_descriptors(a, t, r, n, region, region_rows, stage);
+        if (threadIdx.x == 0 && dsum) atomicAdd(&a.delivered_cta[r % (a.NT * a.C)], (unsigned long long)dsum);
+    }
 }
 
 __global__ void k_advance(uint64_t *t0, uint32_t steps) { *t0 += steps; }
@@ -1898,6 +1907,7 @@ cudaError_t prepare_kernels(const SimArgs &a) {
     ALLOW((k_fused<M, kVRs4B>)); ALLOW((k_fused<M, kVRs4W>))
     ALLOW_M(1); ALLOW_M(2); ALLOW_M(4);
     ALLOW(k_global_atomics);
+    if (!e) e = allow_smem(k_b2l, (size_t)kStageWords * 4);
     if (a.model == 3) {
         const size_t pb = plastic_smem_bytes(a.TW, a.NR);
 #define ALLOWP(kern) if (!e) e = allow_smem(kern, pb)
@@ -2029,7 +2039,7 @@ cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
 }
 
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s) {
-    k_b2l<<<a.NR, kBlock, 0, s>>>(a, k);
+    k_b2l<<<a.NR, kBlock, a.desc ? (size_t)kStageWords * 4 : 0, s>>>(a, k);
     return cudaGetLastError();
 }
 

@@ -128,17 +128,18 @@ def test_teacher_forced_inputs_every_step(S, name):
 
 
 @pytest.mark.parametrize("G", [2, 3, 4])
-@pytest.mark.parametrize("name", ["vogels4000", "brunel3000_d15", "synth20000"])
+@pytest.mark.parametrize("name", ["vogels4000", "brunel3000_d15", "synth20000", "synth20000_cluster4",
+                                  "brunel3000_d15_cluster4"])
 def test_virtual_ranks_match_single_gpu(S, G, name):
     """G network slices on one GPU with the bitmap exchange done through the C ABI:
     slice connectivity = descriptor split, merged spike trains identical to
     the G=1 oracle (partition invariance), owned states identical."""
-    cfg, _, T = CASES[name]
+    cfg, kw, T = CASES[name]
     T = min(T, 200)
     o, _ = oracle_run(name)
     Sw = 32
     nets = [S.Network(cfg, rank=g, world_size=G, slice_width=Sw, external_exchange=True,
-                      record_steps=T) for g in range(G)]
+                      record_steps=T, **kw) for g in range(G)]
     try:
         for g, net in enumerate(nets):
             assert_same_csr(net, O.OracleNet(cfg, part=(g, G, Sw)))
