@@ -223,6 +223,13 @@ SPICE_API spice_status spice_nccl_unique_id(void *out128);
  * then call end, which enqueues bitmap->list conversion and delivery. */
 SPICE_API spice_status spice_exchange_begin(spice_net *net);
 SPICE_API spice_status spice_exchange_end(spice_net *net);
+/* The NCCL graph's G > 1 step sequence (padded layout): end_fused enqueues bitmap->list
+ * + descriptors of step t and the fused kernel (delivery of t, update of t + 1), leaving
+ * step t+1's bitmap in the send buffer, so the next step starts with the exchange (no
+ * begin).  Sequence: begin; (exchange, end_fused) x (T - 1); exchange, end.  The network
+ * state is consistent only after a plain end.  SPICE_ESTATE when the network has no fused
+ * G > 1 path (G = 1, unpadded layout, global atomics). */
+SPICE_API spice_status spice_exchange_end_fused(spice_net *net);
 /* Device-to-device copy of src's send buffer into dst's receive segment for src's rank
  * (both handles on the same device; ordered after src's update; returns when done). */
 SPICE_API spice_status spice_exchange_put(spice_net *dst, spice_net *src);

@@ -1737,6 +1737,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         // tile bt = blockIdx.x / C; with C > 1 this CTA is rank c of the tile's cluster
         const uint32_t bt = b / a.C, c = b % a.C;
         phase_mark(a, 0);
+        // (G > 1: the update of t+1 only writes the send bitmap; the lists and descriptors of
+        //  the gathered spikes come from bitmap->list)
         // thread 0: the step's descriptor count, loaded before the counters are zeroed
         const uint32_t pre_total = (threadIdx.x == 0 && V != kVWlist) ? a.dcount[t % 3] : 0xFFFFFFFFu;
         if (threadIdx.x == 0 && a.delay == 1) {   // this slice's neuron state -> L2 while delivering
@@ -1762,7 +1764,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             // barrier; a second one at exit keeps every CTA's counters alive until then)
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
             phase_mark(a, 6);
-            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, true, &s_count, sm.stage, nullptr, nullptr, true,
+            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, a.G == 1, &s_count, sm.stage, nullptr, nullptr, true,
                                      a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         } else {
@@ -1771,7 +1773,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + lo;
             for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u)
                 *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
-            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, true, &s_count, sm.stage, nullptr, nullptr, true,
+            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, a.G == 1, &s_count, sm.stage, nullptr, nullptr, true,
                                      kMaxCluster, sm.stage + kStageWords);
             if (a.C > 1) cluster_wait();                     // partners done reading this CTA's counters
         }

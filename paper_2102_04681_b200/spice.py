@@ -83,6 +83,7 @@ def lib():
         "spice_nccl_unique_id": (st, [vp]),
         "spice_exchange_begin": (st, [vp]),
         "spice_exchange_end": (st, [vp]),
+        "spice_exchange_end_fused": (st, [vp]),
         "spice_exchange_put": (st, [vp, vp]),
         "spice_partition_owner": (u32, [u64, u32, u32]),
         "spice_partition_local_to_global": (u64, [u64, u32, u32, u32]),
@@ -312,6 +313,10 @@ class Network:
 
     def exchange_end(self) -> None:
         _check(lib().spice_exchange_end(self.h))
+
+    def exchange_end_fused(self) -> None:
+        """G > 1 graph sequence: bitmap->list(t) + fused deliver(t)/update(t+1)."""
+        _check(lib().spice_exchange_end_fused(self.h))
 
     def exchange_put_from(self, src: "Network") -> None:
         _check(lib().spice_exchange_put(self.h, src.h))

@@ -127,10 +127,11 @@ def test_teacher_forced_inputs_every_step(S, name):
                 assert np.array_equal(net.input(rel)[0], o.input(rel)[0]), (t, rel)
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("G", [2, 3, 4])
 @pytest.mark.parametrize("name", ["vogels4000", "brunel3000_d15", "synth20000", "synth20000_cluster4",
                                   "brunel3000_d15_cluster4"])
-def test_virtual_ranks_match_single_gpu(S, G, name):
+def test_virtual_ranks_match_single_gpu(S, G, name, fused):
     """G network slices on one GPU with the bitmap exchange done through the C ABI:
     slice connectivity = descriptor split, merged spike trains identical to
     the G=1 oracle (partition invariance), owned states identical."""
@@ -143,14 +144,24 @@ def test_virtual_ranks_match_single_gpu(S, G, name):
     try:
         for g, net in enumerate(nets):
             assert_same_csr(net, O.OracleNet(cfg, part=(g, G, Sw)))
-        for _ in range(T):
+        if fused:       # the NCCL graph's sequence: begin; (exchange, end_fused) x (T-1); exchange, end
             for n in nets:
                 n.exchange_begin()
-            for d in nets:
-                for s in nets:
-                    d.exchange_put_from(s)
-            for n in nets:
-                n.exchange_end()
+            for t in range(T):
+                for d in nets:
+                    for s in nets:
+                        d.exchange_put_from(s)
+                for n in nets:
+                    n.exchange_end_fused() if t + 1 < T else n.exchange_end()
+        else:
+            for _ in range(T):
+                for n in nets:
+                    n.exchange_begin()
+                for d in nets:
+                    for s in nets:
+                        d.exchange_put_from(s)
+                for n in nets:
+                    n.exchange_end()
         want = o.spikes()[:T]
         for n in nets:
             got = n.read_spikes(0, T)
