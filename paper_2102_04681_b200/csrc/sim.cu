@@ -490,6 +490,17 @@ constexpr uint32_t kSidCap = (kBlock / 32) * kRing - kStageWords;
 // tile list in the common case), then writes, for every destination tile bb, the
 // descriptors desc[par][bb][b][q0 .. q0+CH) with coalesced stores.  Delivery CTAs then read
 // their descriptors contiguously.  Returns (to thread 0) the spikes' delivered-event count.
+// Staging geometry of write_descriptors (shared with the update's early row staging).
+struct DescStage { uint32_t rowlen, rs4, CH; };
+__device__ __forceinline__ DescStage desc_stage(const SimArgs &a) {
+    DescStage d;
+    d.rowlen = a.NT + 1u;
+    // staged rows keep their global 16-byte phase h = (s rowlen) mod 4 so that they are
+    // copied in 16-byte chunks (the bnd array carries 4 words of tail padding)
+    d.rs4 = (d.rowlen + 6u) & ~3u;
+    d.CH = max(1u, (uint32_t)kStageWords / (d.rs4 + 3u));
+    return d;
+}
 __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t t, uint32_t b, uint32_t n,
                                   const uint32_t *region, uint64_t *region_rows, uint32_t *stage,
                                   bool marks = false, const uint32_t *sid_s = nullptr) {
@@ -500,11 +511,8 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
     // destination tile's list of step t (one atomic on the step's counter)
     __shared__ uint32_t s_off;
     if (threadIdx.x == 0 && n) s_off = atomicAdd(&a.dcount[t % 3], n);
-    const uint32_t rowlen = a.NT + 1u;
-    // staged rows keep their global 16-byte phase h = (s rowlen) mod 4 so that they are
-    // copied in 16-byte chunks (the bnd array carries 4 words of tail padding)
-    const uint32_t rs4 = (rowlen + 6u) & ~3u;
-    const uint32_t CH = max(1u, (uint32_t)kStageWords / (rs4 + 3u));
+    const DescStage ds = desc_stage(a);
+    const uint32_t rowlen = ds.rowlen, rs4 = ds.rs4, CH = ds.CH;
     uint64_t *srow = reinterpret_cast<uint64_t *>(stage + CH * rs4);
     uint32_t *sdeg = reinterpret_cast<uint32_t *>(srow + CH);
     const uint4 *bnd4 = reinterpret_cast<const uint4 *>(a.bnd);
@@ -1766,6 +1774,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             phase_mark(a, 6);
             update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, a.G == 1, &s_count, sm.stage, nullptr, nullptr, true,
                                      a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
+            // (an arrive right after the update loop, waited at exit, measured 0.5 us slower)
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         } else {
             if (a.C > 1) cluster_reduce_slice(a, sm.cnt, c);   // slice summed in place
