@@ -1112,21 +1112,28 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
         if (a.dbg & 16u) wx &= 0x3FFFFu;                       // diagnostics: L2-resident
         return ld_stream_v4(a.ent + 8ull * wx);
     };
-    fill(64);
-    uint32_t ea = entry(head + lane), eb = entry(head + 32 + lane);
-    uint4 va = load_win(ea), vb = load_win(eb);
-    head = min(head + 64, tail);
-    while (__any_sync(FULL, ea != NONE)) {
+    constexpr uint32_t RW = SPICE_RW;                  // windows per lane per iteration
+    fill(32u * RW);
+    uint32_t e[RW];
+    uint4 v[RW];
+#pragma unroll
+    for (uint32_t r = 0; r < RW; ++r) { e[r] = entry(head + 32u * r + lane); v[r] = load_win(e[r]); }
+    head = min(head + 32u * RW, tail);
+    while (__any_sync(FULL, e[0] != NONE)) {
         __syncwarp();
-        fill(64);
-        const uint32_t xa = entry(head + lane), xb = entry(head + 32 + lane);
-        const uint4 na = load_win(xa), nb = load_win(xb);
-        head = min(head + 64, tail);
+        fill(32u * RW);
+        uint32_t x[RW];
+        uint4 nv[RW];
+#pragma unroll
+        for (uint32_t r = 0; r < RW; ++r) { x[r] = entry(head + 32u * r + lane); nv[r] = load_win(x[r]); }
+        head = min(head + 32u * RW, tail);
         if (!(a.dbg & 3u)) {
-            if (ea != NONE) accumulate_window<WORD>(cnt_s, va, (ea >> 31) ? 65536u : 1u);
-            if (eb != NONE) accumulate_window<WORD>(cnt_s, vb, (eb >> 31) ? 65536u : 1u);
+#pragma unroll
+            for (uint32_t r = 0; r < RW; ++r)
+                if (e[r] != NONE) accumulate_window<WORD>(cnt_s, v[r], (e[r] >> 31) ? 65536u : 1u);
         }
-        ea = xa; eb = xb; va = na; vb = nb;
+#pragma unroll
+        for (uint32_t r = 0; r < RW; ++r) { e[r] = x[r]; v[r] = nv[r]; }
     }
     if (marks) phase_mark(a, 4);
     __syncthreads();
