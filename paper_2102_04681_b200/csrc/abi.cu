@@ -688,6 +688,9 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         CU(n, cudaMemcpyAsync(n->ptab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, s));
         n->mc.ptab = n->ptab;
         n->mc.ptab_len = (uint32_t)tab.size();
+        uint32_t p2 = 1;
+        while (p2 < n->mc.ptab_len) p2 <<= 1;
+        n->mc.ptab_half = p2 >> 1;
     }
     CU(n, cudaStreamSynchronize(s));
     // ---- tile-pair exchange (G = 1): static chunk capacities from the connectivity ----

@@ -159,6 +159,17 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, const StatePtrs &s
         uint4 x = make_uint4(0, 0, 0, 0);
         if (rfv[0] == 0u || rfv[1] == 0u || rfv[2] == 0u || rfv[3] == 0u)
             x = philox4x32_10(make_uint4(j0 >> 2, (uint32_t)t, 0u, kTagExt), a.key0, a.key1);
+        // n_ext = min{k : x < T_k} = #{k : T_k <= x} (the table is non-decreasing and ends with
+        // 2^32): a branch-free binary search, the four neurons' searches interleaved (one
+        // dependent table load per halving instead of a walk of ~lambda loads per neuron)
+        uint32_t nx[4] = {0u, 0u, 0u, 0u};
+        for (uint32_t step = a.mc.ptab_half; step > 0; step >>= 1) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t q = nx[e] + step - 1u;
+                if (q < a.mc.ptab_len && ptab[q] <= (uint64_t)word_of(x, e)) nx[e] += step;
+            }
+        }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             float v = vv[e];
@@ -168,9 +179,7 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, const StatePtrs &s
                 ref -= 1u;
                 v = m.Vr;                              // input and drive discarded
             } else {
-                const uint32_t xe = word_of(x, e);
-                uint32_t next = 0;
-                while ((uint64_t)xe >= ptab[next]) ++next;     // min{k : x < T_k}
+                const uint32_t next = nx[e];
                 const uint32_t ne = c[e] & 0xFFFFu, ni = c[e] >> 16;
                 v = __fadd_rn(v, __fmul_rn(m.h, __fsub_rn(m.EL, v)));
                 v = __fadd_rn(v, __fmul_rn(m.JE, __uint2float_rn(ne + next)));
@@ -1756,14 +1765,15 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         //  the gathered spikes come from bitmap->list)
         // thread 0: the step's descriptor count, loaded before the counters are zeroed
         const uint32_t pre_total = (threadIdx.x == 0 && V != kVWlist) ? a.dcount[t % 3] : 0xFFFFFFFFu;
-        if (threadIdx.x == 0 && a.delay == 1) {   // this slice's neuron state -> L2 while delivering
+        if (threadIdx.x == 0) {   // this slice's neuron state (+ input slot t+1) -> L2 while delivering
             const uint32_t lo0 = b * a.TWs, nb = a.TWs * 4u;
-            const void *arr[4] = {MODEL == 4 ? (const void *)(a.acc + lo0) : (const void *)(a.v + lo0),
+            const void *arr[5] = {MODEL == 4 ? (const void *)(a.acc + lo0) : (const void *)(a.v + lo0),
                                   MODEL == 4 ? nullptr : (const void *)(a.ref + lo0),
                                   MODEL == 1 ? (const void *)(a.ge + lo0) : nullptr,
-                                  MODEL == 1 ? (const void *)(a.gi + lo0) : nullptr};
+                                  MODEL == 1 ? (const void *)(a.gi + lo0) : nullptr,
+                                  a.delay > 1 ? (const void *)(a.ring + mod32(t + 1, a.D) * a.ring_stride + lo0) : nullptr};
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < 5; ++q)
                 if (arr[q]) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(arr[q]), "r"(nb) : "memory");
         }
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)      // TW is a multiple of 32

@@ -75,6 +75,7 @@ struct ModelConst {
     uint64_t thr_fire;                                // synth: floor(a 2^32) (2^32 = always)
     const uint64_t *ptab;                             // Brunel: Poisson inversion table
     uint32_t ptab_len;
+    uint32_t ptab_half;                               // half the power of two >= ptab_len
     float ap, am, Ap, Am, wmax;                       // Brunel+ STDP (reading R13)
 };
 
