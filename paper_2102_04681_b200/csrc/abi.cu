@@ -124,6 +124,9 @@ struct spice_net {
     uint32_t *deg = nullptr; // pad8: true out-degree of every source on this rank
     double mean_seg = 0;
     double gen_ms = 0, create_ms = 0;   // setup: generator kernels (device), create (host wall)
+    uint32_t *hbm = nullptr;            // pinned host staging of recorded bitmaps (read_spikes)
+    uint64_t hbm_words = 0;
+    std::vector<std::vector<uint32_t>> hdec;   // decoded per-step lists (reused)
     uint32_t NR = 1, RS = 32;    // spike-list regions
     uint32_t dcap = 0;           // descriptors staged in shared memory per delivering CTA
     unsigned long long *ptimes = nullptr;   // SPICE_PHASES diagnostics
@@ -345,6 +348,7 @@ void destroy(spice_net *n) {
     for (void *p : n->allocs) cudaFree(p);
     n->allocs.clear();
     if (n->ev) cudaEventDestroy(n->ev);
+    if (n->hbm) cudaFreeHost(n->hbm);
     if (n->stream) cudaStreamDestroy(n->stream);
     delete n;
 }
@@ -875,15 +879,31 @@ spice_status spice_read_spikes(spice_net *n, uint64_t t_begin, uint64_t t_end, u
         return fail(n, SPICE_ERANGE, "steps [%llu, %llu) not in the record ring (have [%llu, %llu))",
                     (unsigned long long)t_begin, (unsigned long long)t_end,
                     (unsigned long long)(n->t_host > n->R ? n->t_host - n->R : 0), (unsigned long long)n->t_host);
-    CU(n, cudaStreamSynchronize(n->stream));
     const uint64_t words = (uint64_t)n->G * n->W;
-    std::vector<uint32_t> bm(words);
-    std::vector<std::vector<uint32_t>> per(t_end - t_begin);
+    const uint64_t nsteps = t_end - t_begin;
+    // bitmaps of the requested steps -> a pinned host buffer (one async copy per contiguous
+    // run of ring slots, one stream synchronisation), then decoded on the host
+    if (n->hbm_words < nsteps * words) {
+        if (n->hbm) cudaFreeHost(n->hbm);
+        n->hbm = nullptr;
+        n->hbm_words = 0;
+        CU(n, cudaMallocHost(reinterpret_cast<void **>(&n->hbm), std::max<uint64_t>(nsteps * words, 1) * 4));
+        n->hbm_words = nsteps * words;
+    }
+    for (uint64_t t = t_begin; t < t_end;) {
+        const uint64_t slot = t % n->R;
+        const uint64_t run = std::min<uint64_t>(t_end - t, n->R - slot);
+        CU(n, cudaMemcpyAsync(n->hbm + (t - t_begin) * words, n->record + slot * words, run * words * 4,
+                              cudaMemcpyDeviceToHost, n->stream));
+        t += run;
+    }
+    CU(n, cudaStreamSynchronize(n->stream));
+    std::vector<std::vector<uint32_t>> &per = n->hdec;
+    per.resize(nsteps);
     uint64_t tot = 0;
     for (uint64_t t = t_begin; t < t_end; ++t) {
-        CU(n, cudaMemcpy(bm.data(), n->record + (t % n->R) * words, words * 4, cudaMemcpyDeviceToHost));
         std::vector<uint32_t> &L = per[t - t_begin];
-        decode_into(bm.data(), n->G, n->W, n->S, L);
+        decode_into(n->hbm + (t - t_begin) * words, n->G, n->W, n->S, L);
         tot += L.size();
     }
     if (total) *total = tot;
