@@ -518,8 +518,11 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
     const uint32_t par = (uint32_t)(t & 1);
     // dense per-tile lists: this CTA's n descriptors go to [off, off + n) of every
     // destination tile's list of step t (one atomic on the step's counter)
+    // (the reservation's latency overlaps the row loads: thread 0 publishes it after issuing
+    //  its copies; the pass's closing barrier orders it before the descriptor writes)
     __shared__ uint32_t s_off;
-    if (threadIdx.x == 0 && n) s_off = atomicAdd(&a.dcount[t % 3], n);
+    uint32_t off_reg = 0;
+    if (threadIdx.x == 0 && n) off_reg = atomicAdd(&a.dcount[t % 3], n);
     const DescStage ds = desc_stage(a);
     const uint32_t rowlen = ds.rowlen, rs4 = ds.rs4, CH = ds.CH;
     uint64_t *srow = reinterpret_cast<uint64_t *>(stage + CH * rs4);
@@ -541,6 +544,7 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(sdeg + ql)), "l"(a.deg + s) : "memory");
             }
         }
+        if (threadIdx.x == 0 && q0 == 0) s_off = off_reg;
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         __syncthreads();
         if (marks) phase_mark(a, 10);
@@ -752,7 +756,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     const uint32_t n_tile = *s_count;
     if (tid == 0) {
         if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
-        a.fired_cta[b] += n_tile;
+        if (n_tile) atomicAdd(&a.fired_cta[b], (unsigned long long)n_tile);   // RED: no load on the path
     }
     if (!DESC && write_list && !a.desc && !a.wl) {        // row starts of the spikes, all at once
         uint32_t dsum = 0;                                // (the descriptor pass loads them itself)
@@ -785,12 +789,12 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     if (DESC) {
         if (write_list && !(a.dbg & 4u)) {
             const uint64_t dsum = write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
-            if (tid == 0 && dsum) a.delivered_cta[b] += dsum;
+            if (tid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
         }
     } else if (write_list && (a.desc || a.wl) && !(a.dbg & 4u)) {   // padded layout: delivered events
         const uint64_t dsum = a.wl ? write_windows(a, t, b, n_tile, region, region_rows, stage, marks)
                                    : write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
-        if (tid == 0 && dsum) a.delivered_cta[b] += dsum;   // are counted here (out-degrees)
+        if (tid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);   // (out-degrees)
     }
     if (marks) phase_mark(a, 9);
     if constexpr (MODEL != 3 && !DESC) {
@@ -1523,7 +1527,7 @@ __device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot,
     if (threadIdx.x == 0) {
         unsigned long long tot = 0;
         for (int w = 0; w < kBlock / 32; ++w) tot += s_tmp[w];
-        a.delivered_cta[slot] += tot;
+        if (tot) atomicAdd(&a.delivered_cta[slot], tot);
     }
 }
 
