@@ -29,7 +29,8 @@ __device__ __forceinline__ uint32_t warp_incl_scan_g(uint32_t x, uint32_t lane) 
 __device__ __forceinline__ uint32_t prob_bits4(const GenGeom &g, const GenRule &r, uint32_t s,
                                                uint32_t i0) {
     if (i0 >= g.n_own) return 0u;
-    const uint32_t j0 = (uint32_t)local_to_global(i0, g.rank, g.G, g.S);   // multiple of 4
+    // (32-bit index math: a 64-bit division per Philox call cost more than the Philox call)
+    const uint32_t j0 = g.G == 1 ? i0 : (i0 / g.S * g.G + g.rank) * g.S + i0 % g.S;   // multiple of 4
     const uint4 x = philox4x32_10(make_uint4(s, j0 >> 2, r.index, kTagConn), g.key0, g.key1);
     uint32_t m = 0;
 #pragma unroll
@@ -108,10 +109,12 @@ __global__ void __launch_bounds__(256) indeg_kernel(GenGeom g, GenRule r, const 
     const uint32_t kp = (r.k + 1u) / 2u;
     const uint64_t total = (uint64_t)g.n_own * kp;
     const uint64_t nsrc = (uint64_t)r.src_end - r.src_begin;
+    const bool narrow = total < (1ull << 32);            // 32-bit index math when it fits
     for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total;
          w += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t i = (uint32_t)(w / kp), pr = (uint32_t)(w % kp);
-        const uint32_t j = (uint32_t)local_to_global(i, g.rank, g.G, g.S);
+        const uint32_t i = narrow ? (uint32_t)w / kp : (uint32_t)(w / kp);
+        const uint32_t pr = narrow ? (uint32_t)w - i * kp : (uint32_t)(w % kp);
+        const uint32_t j = g.G == 1 ? i : (i / g.S * g.G + g.rank) * g.S + i % g.S;
         if (j < r.dst_begin || j >= r.dst_end) continue;
         const uint4 x = philox4x32_10(make_uint4(j, pr, r.index, kTagIndeg), g.key0, g.key1);
         const uint32_t b = i / g.TW;
