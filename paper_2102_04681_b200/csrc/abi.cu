@@ -736,13 +736,15 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // producers (SPICE_WLIST=1; measured slower: the window writes cost the producer more
     // than the consumer saves, DESIGN.md delivery log)
     const bool segdesc = !(getenv("SPICE_WLIST") && atoi(getenv("SPICE_WLIST"))) || n->eshift == 0 || n->C > 1 || n->G > 1;
-    if (n->pad8 && !n->xbuf && segdesc) {
+    // (not with the paper-style global-atomics delivery: it walks the spike lists itself, and
+    //  nothing would recycle the descriptor-list counters)
+    if (n->pad8 && !n->xbuf && segdesc && !n->global_atomics) {
         // a tile's list holds every spike of the step: the rank's own (G = 1) or all N (G > 1)
         const uint64_t dstride = ((n->G == 1 ? n->n_own : (uint64_t)n->N) + 1) & ~1ull;
         if ((st = dalloc_t(n, &n->desc, 2ull * n->NT * dstride, "segment descriptors"))) return bail(st);
         if ((st = dalloc_t(n, &n->dcount, 4, "descriptor counters"))) return bail(st);
         CU(n, cudaMemset(n->dcount, 0, 16));
-    } else if (n->pad8 && !n->xbuf) {
+    } else if (n->pad8 && !n->xbuf && !n->global_atomics) {
         unsigned long long *tw = nullptr;
         if ((st = dalloc_t(n, &tw, n->NT, "tile windows"))) return bail(st);
         CU(n, cudaMemsetAsync(tw, 0, n->NT * 8ull, s));

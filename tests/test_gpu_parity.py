@@ -38,6 +38,9 @@ CASES = {
     "vogels4000_cluster8": (W.vogels(4000, seed=15), dict(tile_width=512, ctas_per_tile=8), 300),
     "vogels_global_atomics": (W.vogels(4000, seed=9), dict(global_atomics=True), 300),
     "synth_global_atomics": (W.synth(20000, 31, 0.005, seed=8), dict(global_atomics=True), 100),
+    # long enough that per-step list counters must be recycled (regression: they were not)
+    "synth_global_atomics_long": (W.synth(5003, 31, 0.05, seed=16), dict(global_atomics=True), 800),
+    "synth_long_unfused_c2": (W.synth(5003, 31, 0.05, seed=17), dict(unfused=True, ctas_per_tile=2), 800),
 }
 
 _oracle_cache = {}
