@@ -260,7 +260,9 @@ def main_spice(args):
     bytes_launch = 4.0 * ev_step + 12.0 * sp_step
     peak, peak_src = hbm_peak()
     fused = prof["fused"] > 0
-    kern = "k_fused (deliver t + update t+1)" if fused else ("k_global_atomics" if args.global_atomics else "k_deliver")
+    small = net.launches(32) == 2                  # one-CTA persistent kernel (small networks)
+    kern = ("k_small (whole steps, one CTA, 32 per launch)" if small else
+            "k_fused (deliver t + update t+1)") if fused else ("k_global_atomics" if args.global_atomics else "k_deliver")
     # the fused kernel as spice_step runs it (graph of back-to-back launches); the
     # individually launched timings above carry per-launch overhead the graph does not
     launch_ms = (prof["fused_in_graph"] or prof["fused"]) if fused else prof["deliver"]
@@ -293,6 +295,7 @@ def main_spice(args):
                "sample": f"{desc}; {done} steps in {el:.1f} s, single thread"}
 
     delivery = ("global-atomics (paper-style A/B)" if args.global_atomics else
+                f"one CTA, {info['tile_width']} targets in smem, 32 steps per launch" if small else
                 f"tiled smem, {info['n_tiles']} tiles x {info['tile_width']} targets, {info['ctas_per_tile']} CTA/tile")
     traffic, traffic_src = ncu_traffic(wl, delivery) if fused else (None, None)
     line = {
@@ -324,7 +327,7 @@ def main_spice(args):
         "e2e": {"value": e2e_value, "unit": "events/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                 "note": "spice_step(1) + spice_read_spikes of that step to host, every step"},
-        "gpu_launches": net.kernels_per_step() * args.steps + (args.steps + 31) // 32,
+        "gpu_launches": net.launches(args.steps),
         "clocks": ck,
         "cpu_baseline": cpu,
     }

@@ -207,6 +207,9 @@ SPICE_API spice_status spice_debug_phases(spice_net *net, uint64_t *out, uint64_
 
 /* Number of kernels the library launches per simulated step (evidence for benches). */
 SPICE_API uint32_t spice_kernels_per_step(spice_net *net);
+/* Exact number of this library's kernel launches enqueued by spice_step(net, n_steps)
+ * (NCCL's own kernels excluded); small networks run a whole graph chunk in one launch. */
+SPICE_API uint64_t spice_launches(spice_net *net, uint64_t n_steps);
 
 /* Thread-local message of the last failing call ("" if none). */
 SPICE_API const char *spice_last_error(void);

@@ -124,6 +124,7 @@ struct spice_net {
     uint32_t *deg = nullptr; // pad8: true out-degree of every source on this rank
     double mean_seg = 0;
     double gen_ms = 0, create_ms = 0;   // setup: generator kernels (device), create (host wall)
+    bool small = false;                 // one-CTA persistent step kernel (k_small)
     uint32_t *hbm = nullptr;            // pinned host staging of recorded bitmaps (read_spikes)
     uint64_t hbm_words = 0;
     std::vector<std::vector<uint32_t>> hdec;   // decoded per-step lists (reused)
@@ -296,7 +297,9 @@ void build_model_const(spice_net *n) {
 spice_status enqueue_steps(spice_net *n, uint32_t steps) {
     cudaStream_t s = n->stream;
     const SimArgs &a = n->args;
-    if (n->G == 1 && n->fused && !n->global_atomics) {
+    if (n->small) {                                        // one launch for the whole chunk
+        CU(n, launch_small(a, 0, steps, s));
+    } else if (n->G == 1 && n->fused && !n->global_atomics) {
         CU(n, launch_update(a, 0, s));
         for (uint32_t k = 0; k + 1 < steps; ++k) CU(n, launch_fused(a, k, s));   // deliver(k)+update(k+1)
         CU(n, launch_deliver(a, steps - 1, false, n->n_sm, s));
@@ -562,7 +565,19 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     n->C = c->ctas_per_tile ? c->ctas_per_tile
          : (n->pad8 && !c->tile_width && n->n_own >= (uint64_t)n->n_sm * 4096u ? 2u : 1u);
     if (n->C > kMaxCluster) return bail(fail(n, SPICE_EINVAL, "ctas_per_tile %u > %u", n->C, kMaxCluster));
-    if (c->tile_width) {
+    // small networks: one tile of all owned neurons, one CTA runs whole graph chunks
+    // (k_small); auto only, SPICE_NOSMALL=1 disables (A/B)
+    {
+        const uint64_t tw = (n->n_own + 31) / 32 * 32;
+        n->small = n->G == 1 && n->pad8 && !c->tile_width && !c->ctas_per_tile && n->C == 1 &&
+                   c->delay_steps == 1 && (n->model == SPICE_VOGELS || n->model == SPICE_BRUNEL || n->model == SPICE_SYNTH) &&
+                   !(n->flags & (SPICE_FLAG_GLOBAL_ATOMICS | SPICE_FLAG_EXTERNAL_EXCHANGE | SPICE_FLAG_UNFUSED)) &&
+                   tw >= 32 && tw <= kMaxPadTileWord && small_smem_bytes((uint32_t)tw, n->model) <= 227 * 1024 - 2048 &&
+                   !getenv("SPICE_NOSMALL");
+    }
+    if (n->small) {
+        n->TW = (uint32_t)((n->n_own + 31) / 32 * 32);
+    } else if (c->tile_width) {
         const uint32_t q = 32u * n->C;
         n->TW = (c->tile_width + q - 1) / q * q;
         if (n->TW > kMaxPadTileWord) n->pad8 = false;
@@ -1129,8 +1144,17 @@ spice_status spice_profile(spice_net *n, uint64_t steps, double *ms, uint32_t ca
         CU(n, launch_advance(n->t0, 1, s));
         n->t_host += 1;
     }
+    // (2s) small networks: the one-CTA step kernel, one step per launch ("fused" slot)
+    if (n->small && steps > 0) {
+        for (uint64_t q = 0; q < steps; ++q) {
+            spice_status st = timed(2, [&]() -> spice_status { CU(n, launch_small(a, 0, 1, s)); return SPICE_OK; });
+            if (st) return st;
+            CU(n, launch_advance(n->t0, 1, s));
+            n->t_host += 1;
+        }
+    }
     // (2) the fused kernel (G = 1): update(t), then fused launches deliver(t)+update(t+1)
-    if (n->G == 1 && n->fused && !n->global_atomics && steps > 0) {
+    if (!n->small && n->G == 1 && n->fused && !n->global_atomics && steps > 0) {
         CU(n, launch_update(a, 0, s));
         for (uint64_t q = 0; q < steps; ++q) {
             spice_status st = timed(2, [&]() -> spice_status { CU(n, launch_fused(a, 0, s)); return SPICE_OK; });
@@ -1170,11 +1194,12 @@ spice_status spice_profile(spice_net *n, uint64_t steps, double *ms, uint32_t ca
     double in_graph = 0.0;
     if (cap >= 5 && n->G == 1 && n->fused && !n->global_atomics && steps > 0) {
         constexpr uint32_t kProf = 32;
-        CU(n, launch_update(a, 0, s));
+        if (!n->small) CU(n, launch_update(a, 0, s));
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;
         CU(n, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        for (uint32_t k = 0; k < kProf; ++k) launch_fused(a, k, s);
+        if (n->small) launch_small(a, 0, kProf, s);       // (per step: the chunk's time / kProf)
+        else for (uint32_t k = 0; k < kProf; ++k) launch_fused(a, k, s);
         launch_advance(n->t0, kProf, s);
         CU(n, cudaStreamEndCapture(s, &g));
         cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
@@ -1191,9 +1216,11 @@ spice_status spice_profile(spice_net *n, uint64_t steps, double *ms, uint32_t ca
         in_graph = x / (double)(reps * kProf);
         cudaGraphExecDestroy(ge);
         n->t_host += (reps + 1) * kProf;
-        CU(n, launch_deliver(a, 0, false, n->n_sm, s));
-        CU(n, launch_advance(n->t0, 1, s));
-        n->t_host += 1;
+        if (!n->small) {                                   // close the fused sequence
+            CU(n, launch_deliver(a, 0, false, n->n_sm, s));
+            CU(n, launch_advance(n->t0, 1, s));
+            n->t_host += 1;
+        }
     }
     CU(n, cudaStreamSynchronize(s));
     cudaEventDestroy(e0);
@@ -1213,6 +1240,15 @@ spice_status spice_debug_phases(spice_net *n, uint64_t *out, uint64_t cap, uint6
     CU(n, cudaStreamSynchronize(n->stream));
     CU(n, cudaMemcpy(out, n->ptimes, m * 8, cudaMemcpyDeviceToHost));
     return SPICE_OK;
+}
+
+uint64_t spice_launches(spice_net *n, uint64_t steps) {
+    if (!n) return 0;
+    const uint64_t chunks = steps / spice_net::kGraphSteps, rest = steps % spice_net::kGraphSteps;
+    if (n->small) return 2 * chunks + 2 * rest;            // k_small + k_advance per graph replay
+    const uint64_t per = spice_kernels_per_step(n);
+    // + one k_advance per replay; the fused sequences open with an update (G = 1 and G > 1)
+    return per * steps + chunks + rest + (n->fused && !n->global_atomics ? chunks + rest : 0);
 }
 
 uint32_t spice_kernels_per_step(spice_net *n) {

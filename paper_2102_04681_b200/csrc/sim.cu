@@ -1811,6 +1811,98 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
     }
 }
 
+// Small networks (G = 1, delay 1, one tile of all owned neurons, fits shared memory): one
+// CTA runs nsteps whole steps per launch.  Neuron state and the input counters live in
+// shared memory for the launch; a step is update(t) (the shared update code: bitmap into
+// the record ring, states written through to global) -> delivery of the step's spikes,
+// found in the bitmap, warp per spike, lanes over the row's 16-byte windows, into the
+// zeroed counters.  At the launch boundaries the inputs move through ring slots t0 % D /
+// (t0 + nsteps) % D, so every other kernel sequence (unfused, profile, external) stays
+// interchangeable.  Replaces 32 grid-wide kernel boundaries per graph by one.
+__host__ __device__ inline size_t small_smem_words(uint32_t TW, uint32_t model) {
+    const uint32_t sw = model == 4 ? 1u : (model == 1 ? 4u : 2u);    // state words per neuron
+    return (size_t)TW + kDummy + (size_t)sw * TW;
+}
+size_t small_smem_bytes(uint32_t TW, uint32_t model) { return small_smem_words(TW, model) * 4 + 16; }
+
+template <int MODEL>
+__global__ void __launch_bounds__(kBlock) k_small(SimArgs a, uint32_t k0, uint32_t nsteps) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ uint32_t s_count;
+    __shared__ unsigned long long s_deliv;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t TW = a.TW;                               // multiple of 32, covers n_own
+    uint32_t *cnt = smem;
+    uint32_t *st = smem + TW + kDummy;                      // 16-byte aligned (TW, kDummy % 4 == 0)
+    StatePtrs sp{nullptr, nullptr, nullptr, nullptr, nullptr, 0u};
+    if (MODEL == 4) { sp.acc = st; }
+    else if (MODEL == 1) { sp.v = reinterpret_cast<float *>(st); sp.ge = reinterpret_cast<float *>(st + TW);
+                           sp.gi = reinterpret_cast<float *>(st + 2 * TW); sp.ref = st + 3 * TW; }
+    else { sp.v = reinterpret_cast<float *>(st); sp.ref = st + TW; }
+    const uint64_t t0 = *a.t0 + k0;
+    uint32_t *slot0 = a.ring + mod32(t0, a.D) * a.ring_stride;
+    for (uint32_t x = tid * 4u; x < TW; x += kBlock * 4u) {    // stage state + step t0's inputs
+        if (MODEL == 4) *reinterpret_cast<uint4 *>(sp.acc + x) = *reinterpret_cast<const uint4 *>(a.acc + x);
+        if (MODEL != 4) *reinterpret_cast<float4 *>(sp.v + x) = *reinterpret_cast<const float4 *>(a.v + x);
+        if (MODEL != 4) *reinterpret_cast<uint4 *>(sp.ref + x) = *reinterpret_cast<const uint4 *>(a.ref + x);
+        if (MODEL == 1) *reinterpret_cast<float4 *>(sp.ge + x) = *reinterpret_cast<const float4 *>(a.ge + x);
+        if (MODEL == 1) *reinterpret_cast<float4 *>(sp.gi + x) = *reinterpret_cast<const float4 *>(a.gi + x);
+        *reinterpret_cast<uint4 *>(cnt + x) = *reinterpret_cast<const uint4 *>(slot0 + x);
+        *reinterpret_cast<uint4 *>(slot0 + x) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (tid == 0) { s_count = 0; s_deliv = 0; }
+    __syncthreads();
+    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
+    const uint4 *ent4 = reinterpret_cast<const uint4 *>(a.ent);
+    uint64_t deliv = 0;
+    for (uint32_t q = 0; q < nsteps; ++q) {
+        const uint64_t t = t0 + q;
+        update_tile<MODEL>(a, t, 0, 0, TW, cnt, false, &s_count, nullptr, nullptr, &sp);   // ends with a barrier
+        for (uint32_t x = tid * 4u; x < TW; x += kBlock * 4u)
+            *reinterpret_cast<uint4 *>(cnt + x) = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+        const uint32_t *bm = a.record + mod32(t, a.record_steps) * (uint64_t)a.W;
+        for (uint32_t wi = warp; wi < a.W; wi += kBlock / 32) {
+            uint32_t word = bm[wi];
+            while (word) {                                   // warp-uniform
+                const uint32_t sidx = wi * 32u + (uint32_t)__ffs(word) - 1u;
+                word &= word - 1u;
+                const uint64_t rs = a.row_ptr[sidx];
+                const uint32_t w0 = (uint32_t)((rs + a.bnd[2u * sidx]) >> 3), w1 = (uint32_t)((rs + a.bnd[2u * sidx + 1u]) >> 3);
+                const uint32_t qv = sidx >= a.n_exc ? 65536u : 1u;
+                for (uint32_t w = w0 + lane; w < w1; w += 32) {
+                    const uint4 v = ent4[w];
+                    if (a.eshift) accumulate_window<false>(cnt_s, v, qv);
+                    else accumulate_window<true>(cnt_s, v, qv);
+                }
+                if (lane == 0) deliv += a.deg[sidx];
+            }
+        }
+        __syncthreads();
+    }
+    // step t0 + nsteps's inputs -> its ring slot (added: the slot is otherwise empty)
+    uint32_t *slot1 = a.ring + mod32(t0 + nsteps, a.D) * a.ring_stride;
+    for (uint32_t x = tid * 4u; x < TW; x += kBlock * 4u) {
+        uint4 o = *reinterpret_cast<uint4 *>(slot1 + x);
+        o.x += cnt[x]; o.y += cnt[x + 1]; o.z += cnt[x + 2]; o.w += cnt[x + 3];
+        *reinterpret_cast<uint4 *>(slot1 + x) = o;
+    }
+    if (lane == 0 && deliv) atomicAdd(&s_deliv, (unsigned long long)deliv);
+    __syncthreads();
+    if (tid == 0 && s_deliv) atomicAdd(&a.delivered_cta[0], s_deliv);
+}
+
+cudaError_t launch_small(const SimArgs &a, uint32_t k0, uint32_t nsteps, cudaStream_t s) {
+    const size_t bytes = small_smem_bytes(a.TW, a.model);
+    switch (a.model) {
+    case 1: k_small<1><<<1, kBlock, bytes, s>>>(a, k0, nsteps); break;
+    case 2: k_small<2><<<1, kBlock, bytes, s>>>(a, k0, nsteps); break;
+    case 4: k_small<4><<<1, kBlock, bytes, s>>>(a, k0, nsteps); break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 // Paper-style baseline: warp w delivers spike (w mod |S|) to tile (w / |S|), column-wise
 // (P:200), with one global atomic per event.
 __global__ void __launch_bounds__(kBlock) k_global_atomics(SimArgs a, uint32_t k) {
@@ -1939,6 +2031,14 @@ cudaError_t prepare_kernels(const SimArgs &a) {
     ALLOW((k_fused<M, kVRs4B>)); ALLOW((k_fused<M, kVRs4W>))
     ALLOW_M(1); ALLOW_M(2); ALLOW_M(4);
     ALLOW(k_global_atomics);
+    {
+        const size_t sb = small_smem_bytes(a.TW, a.model);
+        if (!e && sb <= 227 * 1024 - 2048) {
+            e = allow_smem(k_small<1>, sb);
+            if (!e) e = allow_smem(k_small<2>, sb);
+            if (!e) e = allow_smem(k_small<4>, sb);
+        }
+    }
     if (!e) e = allow_smem(k_b2l, (size_t)kStageWords * 4);
     if (a.model == 3) {
         const size_t pb = plastic_smem_bytes(a.TW, a.NR);

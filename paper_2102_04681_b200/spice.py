@@ -76,6 +76,7 @@ def lib():
         "spice_info": (st, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32), C.POINTER(u32),
                             C.POINTER(u32), C.POINTER(u64)]),
         "spice_kernels_per_step": (u32, [vp]),
+        "spice_launches": (u64, [vp, u64]),
         "spice_setup_times": (st, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "spice_debug_phases": (st, [vp, vp, u64, C.POINTER(u64)]),
         "spice_profile": (st, [vp, u64, vp, u32, C.POINTER(u32)]),
@@ -299,6 +300,10 @@ class Network:
 
     def kernels_per_step(self) -> int:
         return lib().spice_kernels_per_step(self.h)
+
+    def launches(self, n_steps: int) -> int:
+        """Kernel launches spice_step(n_steps) enqueues (NCCL's own excluded)."""
+        return lib().spice_launches(self.h, n_steps)
 
     @property
     def stream(self) -> int:
