@@ -898,160 +898,6 @@ __device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v,
         : "memory");
 }
 
-// Window-stream delivery (G = 1, padded layout), software-pipelined through shared memory.
-//  * The CTA's visits (spike x this tile, for spikes p with p % C == c) are split evenly
-//    across its warps (flat prefix over the spike-list regions).
-//  * A warp takes its visits 32 at a time (a "group"): lane L loads the descriptor of visit
-//    L (coalesced, prefetched one group ahead); a warp scan of the segments' window counts
-//    concatenates their windows into one stream of T windows.
-//  * The stream is consumed 32 windows per round, one window per lane.  The owner of
-//    every (non-empty, compacted) segment starting inside the round sets bit (start - r0);
-//    one redux.sync.or gives the round's start mask, so lane L's segment is
-//    sprev + popc(mask & lanes <= L) (sprev: segment of window r0 - 1).  Lane L then
-//    copies its window into its slot of a per-warp shared-memory stage with cp.async
-//    (LDGSTS, L2 only).  S stages are in flight; processing a stage is one 16-byte shared
-//    load and eight unconditional red.shared.add (no masks: padding maps to dummies).
-// Segment length no longer sets the lane mapping: short and long segments fill the same
-// rounds, and the per-visit bookkeeping is one descriptor load and one scan step.
-__device__ __forceinline__ uint32_t deliver_tile_win(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
-                                     uint32_t *cnt, uint32_t *pref, uint32_t *tmp, uint4 *wbuf, uint64_t *dsm,
-                                     bool marks = false) {
-    constexpr int S = kStages;
-    constexpr uint32_t NW = kBlock / 32;
-    constexpr uint32_t FULL = 0xFFFFFFFFu;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t par = (uint32_t)(t & 1);
-    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
-    // the step's dense descriptor list of this tile: total from the step counter (CTA 0
-    // also clears the counter step t + 2 will use; nobody touches it in this launch)
-    __shared__ uint32_t s_total;
-    if (tid == 0) {
-        s_total = a.dcount[t % 3];
-        if (b == 0 && c == 0) a.dcount[(t + 2) % 3] = 0u;
-    }
-    __syncthreads();
-    if (marks) phase_mark(a, 2);
-    const uint32_t n_sp = s_total;
-    const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
-    const uint32_t v0 = (uint32_t)((uint64_t)my * warp / NW), v1 = (uint32_t)((uint64_t)my * (warp + 1) / NW);
-    const uint64_t *dlist = a.desc + ((uint64_t)par * a.NT + b) * a.dstride + c;   // visit v -> dlist[v * C]
-    const uint4 *ent4 = reinterpret_cast<const uint4 *>(a.ent);
-    uint4 *buf = wbuf + warp * (S * 32);
-    (void)ent4; (void)buf;
-    // The warp's descriptors [v0, v1) are copied into shared memory first (8-byte
-    // cp.async, one memory latency for the whole walk) when the CTA's visits fit.
-    const bool dsmem = my <= a.dcap;
-    if (dsmem) {
-        for (uint32_t v = v0 + lane; v < v1; v += 32) {
-            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dsm + v);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa), "l"(dlist + (uint64_t)v * a.C) : "memory");
-        }
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
-    }
-    if (marks) phase_mark(a, 3);
-    auto dload32 = [&](uint32_t vbase) -> uint64_t {   // descriptor of visit vbase + lane (0: none)
-        const uint32_t v = vbase + lane;
-        if (v >= v1) return 0ull;
-        return dsmem ? dsm[v] : dlist[(uint64_t)v * a.C];
-    };
-    uint32_t gnext = v0;                               // first visit of the next group
-    uint64_t dn = dload32(v0);                         // its descriptors (prefetched)
-    uint32_t cw = 0, pw = 0, nwl = 0, T = 0, inhm = 0, r0 = 0, sprev = 0;   // current group
-    bool done = false;
-    const uint32_t lmask_le = 0xFFFFFFFFu >> (31u - lane);
-    auto next_group = [&]() {
-        while (gnext < v1) {
-            uint64_t d = dn;
-            gnext += 32;
-            dn = dload32(gnext);
-            uint32_t nw = (uint32_t)(d >> 32) & 0x7FFFFFFFu;
-            const uint32_t nzm = __ballot_sync(FULL, nw != 0u);
-            if (nzm & (nzm + 1u)) {                    // empty segments before non-empty ones:
-                const uint32_t k = __popc(nzm);        // compact (lane j <- j-th non-empty)
-                const uint32_t src = lane < k ? __fns(nzm, 0u, (int)lane + 1) : lane;
-                const uint32_t lo32 = __shfl_sync(FULL, (uint32_t)d, src);
-                const uint32_t hi32 = __shfl_sync(FULL, (uint32_t)(d >> 32), src);
-                d = lane < k ? (((uint64_t)hi32 << 32) | lo32) : 0ull;
-                nw = (uint32_t)(d >> 32) & 0x7FFFFFFFu;
-            }
-            cw = (uint32_t)d;
-            nwl = nw;
-            const uint32_t incl = warp_incl_scan(nw);
-            pw = incl - nw;
-            T = __shfl_sync(FULL, incl, 31);
-            inhm = __ballot_sync(FULL, (uint32_t)(d >> 63));
-            r0 = 0;
-            sprev = 0xFFFFFFFFu;                       // segment 0 starts at window 0
-            if (T) return;
-        }
-        done = true;
-    };
-    uint32_t qs[S];                                    // per stage: q of this lane's window (0: none)
-#if SPICE_DIRECT
-    uint4 vw[S];                                       // per stage: the window itself (registers)
-#endif
-    uint32_t live = 0;                                 // warp-uniform: stages holding a round
-    auto issue = [&](int s) {
-        if (!done && r0 >= T) next_group();
-        uint32_t q = 0;
-        if (!done) {
-            const uint32_t w = r0 + lane;
-            const uint32_t dd = pw - r0;               // my segment's start, relative to the round
-            const uint32_t smask = __reduce_or_sync(FULL, (nwl != 0u && dd < 32u) ? 1u << dd : 0u);
-            const uint32_t lo = (sprev + __popc(smask & lmask_le)) & 31u;
-            sprev += __popc(smask);
-            const uint32_t wi = __shfl_sync(FULL, cw, lo);
-            const uint32_t plo = __shfl_sync(FULL, pw, lo);
-            if (w < T) {
-                q = (inhm >> lo) & 1u ? 65536u : 1u;
-                if (!(a.dbg & 2u)) {
-#if SPICE_DIRECT
-                    const uint32_t wx = (a.dbg & 16u) ? ((wi + (w - plo)) & 0x3FFFFu) : (wi + (w - plo));   // dbg 16: L2-resident
-                    vw[s] = ld_stream_v4(a.ent + 8ull * wx);
-#else
-                    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf + s * 32 + lane);
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(ent4 + (wi + (w - plo))) : "memory");
-#endif
-                }
-            }
-            r0 += 32;
-            live |= 1u << s;
-        }
-        qs[s] = q;
-#if !SPICE_DIRECT
-        asm volatile("cp.async.commit_group;" ::: "memory");
-#endif
-    };
-    auto process = [&](int s) {
-#if SPICE_DIRECT
-        if (qs[s] && !(a.dbg & 3u)) accumulate_window(cnt_s, vw[s], qs[s]);
-#else
-        if (qs[s] && !(a.dbg & 3u)) accumulate_window(cnt_s, buf[s * 32 + lane], qs[s]);
-#endif
-        live &= ~(1u << s);
-    };
-#pragma unroll
-    for (int s = 0; s < S - 1; ++s) issue(s);
-    bool fin = false;
-    while (!fin) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            issue((s + S - 1) % S);
-#if !SPICE_DIRECT
-            asm volatile("cp.async.wait_group %0;" :: "n"(S - 1) : "memory");
-#endif
-            process(s);
-            if (done && live == 0) { fin = true; break; }
-        }
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if (marks) phase_mark(a, 4);
-    __syncthreads();
-    if (marks) phase_mark(a, 5);
-    return 0u;                                         // delivered events: counted at the source
-}
-
 // Ring delivery (G = 1, padded layout; default).  Consumes the segment-descriptor lists of
 // write_descriptors (one 8-byte descriptor per spike x tile, cheap to produce) but streams
 // windows like a window list: each warp expands its segment descriptors, 32 at a time,
