@@ -655,7 +655,7 @@ template <int MODEL, bool DESC = false>
 __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                             const uint32_t *cnt, bool write_list, uint32_t *s_count, uint32_t *stage,
                             uint32_t *xsm = nullptr, const StatePtrs *staged = nullptr, bool marks = false,
-                            uint32_t cl_c = kMaxCluster, uint32_t *sid_s = nullptr) {
+                            uint32_t cl_c = kMaxCluster, uint32_t *sid_s = nullptr, uint32_t *bm_s = nullptr) {
     const StatePtrs sp = staged ? *staged : global_state(a);
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;   // bitmap coverage
@@ -717,7 +717,10 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
         w |= __shfl_xor_sync(0xFFFFFFFFu, w, 1);
         w |= __shfl_xor_sync(0xFFFFFFFFu, w, 2);
         w |= __shfl_xor_sync(0xFFFFFFFFu, w, 4);
-        if ((lane & 7u) == 0 && x4 < span) bm[(lo + x4) >> 5] = w;
+        if ((lane & 7u) == 0 && x4 < span) {
+            bm[(lo + x4) >> 5] = w;
+            if (bm_s) bm_s[x4 >> 5] = w;                  // (k_small: the step's bitmap in smem)
+        }
         // append spikes to this tile's list region (warp-aggregated smem counter)
         const uint32_t nsp = __popc(nib);
         const uint32_t incl = warp_incl_scan(nsp);
@@ -1665,11 +1668,18 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
 // zeroed counters.  At the launch boundaries the inputs move through ring slots t0 % D /
 // (t0 + nsteps) % D, so every other kernel sequence (unfused, profile, external) stays
 // interchangeable.  Replaces 32 grid-wide kernel boundaries per graph by one.
-__host__ __device__ inline size_t small_smem_words(uint32_t TW, uint32_t model) {
+__host__ __device__ inline size_t small_smem_words(uint32_t TW, uint32_t model, bool rows) {
     const uint32_t sw = model == 4 ? 1u : (model == 1 ? 4u : 2u);    // state words per neuron
-    return (size_t)TW + kDummy + (size_t)sw * TW;
+    // counters, state, the step's bitmap, [per-source first window, end window, out-degree]
+    return (size_t)TW + kDummy + (size_t)sw * TW + TW / 32 + (rows ? 3ull * TW : 0ull);
 }
-size_t small_smem_bytes(uint32_t TW, uint32_t model) { return small_smem_words(TW, model) * 4 + 16; }
+constexpr size_t kSmallSmemMax = 227 * 1024 - 2048;
+__host__ __device__ inline bool small_rows(uint32_t TW, uint32_t model) {
+    return small_smem_words(TW, model, true) * 4 + 16 <= kSmallSmemMax;
+}
+size_t small_smem_bytes(uint32_t TW, uint32_t model) {
+    return small_smem_words(TW, model, small_rows(TW, model)) * 4 + 16;
+}
 
 template <int MODEL>
 __global__ void __launch_bounds__(kBlock) k_small(SimArgs a, uint32_t k0, uint32_t nsteps) {
@@ -1685,6 +1695,16 @@ __global__ void __launch_bounds__(kBlock) k_small(SimArgs a, uint32_t k0, uint32
     else if (MODEL == 1) { sp.v = reinterpret_cast<float *>(st); sp.ge = reinterpret_cast<float *>(st + TW);
                            sp.gi = reinterpret_cast<float *>(st + 2 * TW); sp.ref = st + 3 * TW; }
     else { sp.v = reinterpret_cast<float *>(st); sp.ref = st + TW; }
+    uint32_t *bm_s = st + (MODEL == 4 ? 1u : (MODEL == 1 ? 4u : 2u)) * TW;
+    const bool rows = small_rows(TW, MODEL);               // (uniform)
+    uint32_t *rw0 = bm_s + TW / 32, *rw1 = rw0 + TW, *rdg = rw1 + TW;
+    if (rows)                                               // sources' windows, staged once
+        for (uint32_t x = tid; x < a.n_own; x += kBlock) {
+            const uint64_t rs = a.row_ptr[x];
+            rw0[x] = (uint32_t)((rs + a.bnd[2u * x]) >> 3);
+            rw1[x] = (uint32_t)((rs + a.bnd[2u * x + 1u]) >> 3);
+            rdg[x] = a.deg[x];
+        }
     const uint64_t t0 = *a.t0 + k0;
     uint32_t *slot0 = a.ring + mod32(t0, a.D) * a.ring_stride;
     for (uint32_t x = tid * 4u; x < TW; x += kBlock * 4u) {    // stage state + step t0's inputs
@@ -1703,25 +1723,29 @@ __global__ void __launch_bounds__(kBlock) k_small(SimArgs a, uint32_t k0, uint32
     uint64_t deliv = 0;
     for (uint32_t q = 0; q < nsteps; ++q) {
         const uint64_t t = t0 + q;
-        update_tile<MODEL>(a, t, 0, 0, TW, cnt, false, &s_count, nullptr, nullptr, &sp);   // ends with a barrier
+        update_tile<MODEL>(a, t, 0, 0, TW, cnt, false, &s_count, nullptr, nullptr, &sp, false, kMaxCluster,
+                           nullptr, bm_s);                   // ends with a barrier
         for (uint32_t x = tid * 4u; x < TW; x += kBlock * 4u)
             *reinterpret_cast<uint4 *>(cnt + x) = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
-        const uint32_t *bm = a.record + mod32(t, a.record_steps) * (uint64_t)a.W;
         for (uint32_t wi = warp; wi < a.W; wi += kBlock / 32) {
-            uint32_t word = bm[wi];
+            uint32_t word = bm_s[wi];
             while (word) {                                   // warp-uniform
                 const uint32_t sidx = wi * 32u + (uint32_t)__ffs(word) - 1u;
                 word &= word - 1u;
-                const uint64_t rs = a.row_ptr[sidx];
-                const uint32_t w0 = (uint32_t)((rs + a.bnd[2u * sidx]) >> 3), w1 = (uint32_t)((rs + a.bnd[2u * sidx + 1u]) >> 3);
+                uint32_t w0, w1;
+                if (rows) { w0 = rw0[sidx]; w1 = rw1[sidx]; }
+                else {
+                    const uint64_t rs = a.row_ptr[sidx];
+                    w0 = (uint32_t)((rs + a.bnd[2u * sidx]) >> 3); w1 = (uint32_t)((rs + a.bnd[2u * sidx + 1u]) >> 3);
+                }
                 const uint32_t qv = sidx >= a.n_exc ? 65536u : 1u;
                 for (uint32_t w = w0 + lane; w < w1; w += 32) {
                     const uint4 v = ent4[w];
                     if (a.eshift) accumulate_window<false>(cnt_s, v, qv);
                     else accumulate_window<true>(cnt_s, v, qv);
                 }
-                if (lane == 0) deliv += a.deg[sidx];
+                if (lane == 0) deliv += rows ? rdg[sidx] : a.deg[sidx];
             }
         }
         __syncthreads();
