@@ -27,6 +27,8 @@ CASES = {
     "vogels4000_t32_c3": (W.vogels(4000), dict(tile_width=32, ctas_per_tile=3), 400),
     "brunel3000_d15": (W.brunel(3000, 0.1, seed=5, delay=15), {}, 400),
     "brunel1001_ragged": (W.brunel(1001, 0.2, seed=2, delay=3), dict(tile_width=64), 300),
+    # delay 1 Brunel: the small-network one-CTA kernel with the Poisson drive
+    "brunel2000_d1_small": (W.brunel(2000, 0.1, seed=18, delay=1), {}, 300),
     "synth20000": (W.synth(20000, 31, 0.005, seed=3), {}, 200),
     "synth5003_ragged_c2": (W.synth(5003, 100, 0.02, seed=4), dict(tile_width=96, ctas_per_tile=2), 150),
     # tile wider than byte-offset entries allow: padded layout with counter-index entries
