@@ -1294,19 +1294,26 @@ __device__ __forceinline__ void stdp_traces(const SimArgs &a, uint64_t t, uint32
 
 __device__ __forceinline__ void walk_plastic(const SimArgs &a, uint32_t b, uint32_t *cnt, long long *pin,
                                              uint64_t w, uint64_t st, uint64_t en, uint32_t q,
-                                             uint32_t s, bool pls) {
+                                             uint32_t s, bool pls, const float *ys) {
     const uint4 v = ld_stream_v4(a.ent + w);
     const uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
                            v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
+    float wv8[8];
+    if (pls) {                           // the window's 8 weights in two 16-byte loads (w % 8 == 0)
+        const float4 w0 = reinterpret_cast<const float4 *>(a.w + w)[0];
+        const float4 w1 = reinterpret_cast<const float4 *>(a.w + w)[1];
+        wv8[0] = w0.x; wv8[1] = w0.y; wv8[2] = w0.z; wv8[3] = w0.w;
+        wv8[4] = w1.x; wv8[5] = w1.y; wv8[6] = w1.z; wv8[7] = w1.w;
+    }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
         if (w + u < st || w + u >= en) continue;
         const uint32_t off = e[u];
         const uint32_t il = b * a.TW + off;
         if (pls && plastic_edge(a, s, (uint32_t)local_to_global(il, a.rank, a.G, a.S))) {
-            float wv = __fsub_rn(a.w[w + u], __fmul_rn(a.mc.Am, a.ytr[il]));
+            float wv = __fsub_rn(wv8[u], __fmul_rn(a.mc.Am, ys ? ys[off] : a.ytr[il]));
             wv = wv > 0.0f ? wv : 0.0f;
-            a.w[w + u] = wv;
+            a.w[w + u] = wv;             // (only this segment's entries: a window may span two tiles)
             atomicAdd(reinterpret_cast<unsigned long long *>(&pin[off]),
                       (unsigned long long)__double2ll_rn((double)wv * 4294967296.0));
         } else {
@@ -1326,6 +1333,11 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
     if (marks) phase_mark(a, 2);
     for (uint32_t r = tid; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
     __syncthreads();
+    // the tile's post traces y in shared memory for the depression (the potentiation pass
+    // that used `stage` is complete: block_exclusive_scan's barriers order it)
+    float *ys = a.TW <= (uint32_t)kStageWords ? reinterpret_cast<float *>(stage) : nullptr;
+    if (ys)
+        for (uint32_t x = tid; x < a.TW; x += kBlock) ys[x] = b * a.TW + x < a.n_own ? a.ytr[b * a.TW + x] : 0.0f;
     block_exclusive_scan(pref, a.NR, tmp);       // also orders (i) before (ii)
     if (marks) phase_mark(a, 3);
     const uint32_t n_sp = pref[a.NR];
@@ -1341,7 +1353,7 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
         const uint32_t q = s >= a.n_exc ? 65536u : 1u;
         const bool pls = plastic_src(a, s);
         if (lig == 0) delivered += (uint32_t)(en - st);
-        for (uint64_t w = (st & ~7ull) + 8u * lig; w < en; w += 8u * GS) walk_plastic(a, b, cnt, pin, w, st, en, q, s, pls);
+        for (uint64_t w = (st & ~7ull) + 8u * lig; w < en; w += 8u * GS) walk_plastic(a, b, cnt, pin, w, st, en, q, s, pls, ys);
     }
     __syncthreads();
     if (marks) phase_mark(a, 4);
