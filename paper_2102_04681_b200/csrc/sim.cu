@@ -682,11 +682,23 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     }
     const bool acc_done = false;
     const int forced = a.force_ctl[0] == t ? (int)a.force_ctl[1] : 0;   // once per CTA, not per neuron
+    // synth accumulators (global, one RMW per neuron): the next iteration's values are loaded
+    // one iteration ahead, so the loop pays the load latency once rather than per iteration
+    constexpr bool ACC_PF = MODEL == 4 && SPICE_ACC_PREFETCH;
+    const bool acc_pf = ACC_PF && staged == nullptr;
+    uint4 acc_next = make_uint4(0u, 0u, 0u, 0u);
+    if (acc_pf && 4u * tid < span && lo + 4u * tid < a.n_own)
+        acc_next = *reinterpret_cast<const uint4 *>(a.acc + lo + 4u * tid);
     for (uint32_t x0 = 0; x0 < span; x0 += 4u * kBlock) {      // uniform trip count per CTA
         if (x0 + 4u * (tid & ~31u) >= span) continue;             // whole warp past the slice
         const uint32_t x4 = x0 + 4u * tid;
         uint32_t nib = 0;
         const bool act = x4 < span && lo + x4 < a.n_own;
+        uint4 acc_cur = acc_next;
+        if (acc_pf) {
+            const uint32_t xn = x4 + 4u * kBlock;
+            if (xn < span && lo + xn < a.n_own) acc_next = *reinterpret_cast<const uint4 *>(a.acc + lo + xn);
+        }
         if (act) {
             uint32_t c[4];
             long long pin[4] = {0, 0, 0, 0};
@@ -717,7 +729,11 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                 *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
                 c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
             }
-            nib = update4<MODEL>(a, sp, t, lo + x4, c, pin, ptab, acc_done, forced);
+            if (acc_pf) {                                  // (update4 then skips its own RMW)
+                acc_cur.x += c[0]; acc_cur.y += c[1]; acc_cur.z += c[2]; acc_cur.w += c[3];
+                *reinterpret_cast<uint4 *>(a.acc + lo + x4) = acc_cur;
+            }
+            nib = update4<MODEL>(a, sp, t, lo + x4, c, pin, ptab, acc_done || acc_pf, forced);
         }
         // 8 lanes x 4 bits -> one 32-neuron bitmap word
         uint32_t w = nib << (4u * (lane & 7u));

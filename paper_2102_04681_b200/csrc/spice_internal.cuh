@@ -20,6 +20,9 @@ enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFi
 #ifndef SPICE_PHASES_BUILD
 #define SPICE_PHASES_BUILD 0    // in-kernel phase clocks (tools/phases.py builds a variant)
 #endif
+#ifndef SPICE_ACC_PREFETCH
+#define SPICE_ACC_PREFETCH 1    // synth update: accumulators loaded one loop iteration ahead
+#endif
 #ifndef SPICE_RW
 #define SPICE_RW 2              // ring delivery: 16-byte windows per lane per iteration
 #endif
