@@ -442,3 +442,125 @@ def test_stdp_disabled_equals_brunel_and_weights_clamped():
     wmax = W.brunel_plus(n).params[14]
     assert w.min() >= 0 and w.max() <= np.float32(wmax)
     assert np.any(w != np.float32(W.brunel_plus(n).params[15]))
+
+
+# ------------------------------------------------ update-rule pins (round 2)
+def _vogels_params_frozen_v(**kw):
+    prm = list(W.vogels_params())
+    prm[2] = 1e9                               # V_t: the target never fires
+    for i, v in kw.items():
+        prm[i] = v
+    return prm
+
+
+@pytest.mark.parametrize("precision,tol", [("ref64", 1e-14), ("mirror32", 2e-6)])
+def test_vogels_conductance_jump(precision, tol):
+    """Vogels COBA input (readings R3/R10; P:395 defers the model to [vogels2005]): n_e
+    excitatory and n_i inhibitory spikes arriving at step t raise the conductances by
+    dg_e n_e and dg_i n_i before the Euler step, which then uses the raised values, and
+    the conductances decay afterwards:
+        ge' = ge0 + dg_e n_e,  gi' = gi0 + dg_i n_i,
+        v   = v0 + h((E_L - v0) + ge'(E_e - v0) + gi'(E_i - v0)),
+        ge  = ge'(1 - dt/tau_e),  gi = gi'(1 - dt/tau_i).
+    n_e = 2 != n_i = 3, dg_e != dg_i and tau_e != tau_i, so swapping the two receptors
+    anywhere (unpacking, weights or decay) changes the result."""
+    prm = _vogels_params_frozen_v()
+    # sources 0,1 excitatory; 2,3,4 inhibitory; target 5 (n_exc = 2)
+    rules = [W.Rule((0, 2), (5, 6), W.FIXED_PROB, 1.0), W.Rule((2, 5), (5, 6), W.FIXED_PROB, 1.0)]
+    cfg = _cfg(W.VOGELS, 6, 2, rules, prm)
+    net = O.OracleNet(cfg, precision)
+    net.force_next([0, 1, 2, 3, 4], "replace")
+    net.step(1)                                 # step 0: the five sources fire, delivered for step 1
+    ge0, gi0, v0 = 0.75, 1.5, -55.0
+    for f, x in ((O.F_GE, ge0), (O.F_GI, gi0), (O.F_V, v0)):
+        s = net.state(f).copy(); s[5] = x; net.set_state(f, s)
+    net.step(1)
+    dge, dgi, EL, Ee, Ei = prm[9], prm[10], prm[1], prm[5], prm[6]
+    h, ke, ki = 0.1 / prm[0], 0.1 / prm[7], 0.1 / prm[8]
+    ge1, gi1 = ge0 + dge * 2, gi0 + dgi * 3
+    v = v0 + h * ((EL - v0) + ge1 * (Ee - v0) + gi1 * (Ei - v0))
+    got = {f: float(net.state(f)[5]) for f in (O.F_GE, O.F_GI, O.F_V)}
+    assert abs(got[O.F_GE] - ge1 * (1 - ke)) <= tol * ge1
+    assert abs(got[O.F_GI] - gi1 * (1 - ki)) <= tol * gi1
+    assert abs(got[O.F_V] - v) <= tol * abs(v)
+
+
+def test_brunel_drive_is_poisson():
+    """Brunel external drive (reading R12): per neuron and step n_ext ~ Poisson(lambda)
+    by inversion of Philox words against the CDF table.  With no leak (tau = 1e300:
+    h rounds to 0 in fp32), J_E = 1 (dyadic), no refractoriness and an unreachable
+    threshold, each step raises V by exactly n_ext, so the V increments of 1000
+    unconnected neurons over 100 steps are 1e5 Poisson draws: chi-square against the
+    Poisson pmf (pooled bins with >= 5 expected) p > 1e-4, mean within 5 sigma."""
+    n, T = 1000, 100
+    for lam in (2.0, 16.0):
+        prm = _brunel_params(tau=1e300, JE=1.0, theta=1e30, tref=0.0, lam=lam, vlo=0.0, vhi=0.0)
+        net = O.OracleNet(_cfg(W.BRUNEL, n, n, [], prm, seed=17))
+        prev = net.state(O.F_V).astype(np.float64)
+        draws = []
+        for _ in range(T):
+            net.step(1)
+            cur = net.state(O.F_V).astype(np.float64)
+            draws.append(cur - prev)
+            prev = cur
+        x = np.concatenate(draws)
+        assert np.all(x == np.round(x)) and x.min() >= 0
+        x = x.astype(np.int64)
+        m = x.size
+        assert abs(x.mean() - lam) < 5 * np.sqrt(lam / m)
+        kmax = int(x.max()) + 1
+        obs = np.bincount(x, minlength=kmax + 1).astype(np.float64)
+        pmf = st.poisson.pmf(np.arange(kmax + 1), lam)
+        pmf[-1] += st.poisson.sf(kmax, lam)
+        exp = pmf * m
+        # pool the tails until every bin expects >= 5
+        lo = 0
+        while exp[:lo + 1].sum() < 5:
+            lo += 1
+        hi = kmax
+        while exp[hi:].sum() < 5:
+            hi -= 1
+        o = np.concatenate(([obs[:lo + 1].sum()], obs[lo + 1:hi], [obs[hi:].sum()]))
+        e = np.concatenate(([exp[:lo + 1].sum()], exp[lo + 1:hi], [exp[hi:].sum()]))
+        chi2 = ((o - e) ** 2 / e).sum()
+        assert st.chi2.sf(chi2, len(o) - 1) > 1e-4, (lam, chi2, len(o))
+
+
+@pytest.mark.parametrize("precision", ["ref64", "mirror32"])
+def test_brunel_inhibitory_weight(precision):
+    """Brunel inhibitory coupling (reading R7, Brunel 2000 model A: J_I = -g J_E): with
+    no leak and no drive, one excitatory and two inhibitory spikes arriving together
+    change V by J_E - 2 g J_E exactly (J_E = 0.5, g = 5: 10 -> 5.5; dyadic values)."""
+    prm = _brunel_params(tau=1e300, JE=0.5, g=5.0, lam=0.0, vlo=10.0, vhi=10.0, theta=1e9)
+    rules = [W.Rule((0, 3), (3, 4), W.FIXED_PROB, 1.0)]
+    cfg = _cfg(W.BRUNEL, 4, 1, rules, prm)      # 0 excitatory, 1 and 2 inhibitory
+    net = O.OracleNet(cfg, precision)
+    net.force_next([0, 1, 2], "replace")
+    net.step(1)
+    assert net.state(O.F_V)[3] == 10.0
+    net.step(1)
+    assert net.state(O.F_V)[3] == 10.0 + 0.5 - 2 * 5.0 * 0.5
+    # inhibitory only: two spikes of J_I = -2.5
+    net.force_next([1, 2], "replace")
+    net.step(2)
+    assert net.state(O.F_V)[3] == 5.5 - 5.0
+
+
+@pytest.mark.parametrize("G,S", [(1, 1), (3, 32)])
+def test_sampled_rows_and_columns_match_csr(G, S):
+    """The full-size checkers orc_row / orc_col (reading R17) regenerate exactly the rows
+    and columns of the built CSR, for fixed-probability and fixed-in-degree rules, with
+    and without the ownership filter."""
+    for cfg in (W.brunel(700, 0.1, seed=21), W.synth(900, 17, seed=22)):
+        full_rp, full_tg = O.OracleNet(cfg).csr()
+        for g in range(G):
+            part = (g, G, S) if G > 1 else None
+            rp, tg = O.OracleNet(cfg, part=part).csr()
+            for s in range(0, cfg.n, 7):
+                assert np.array_equal(O.row(cfg, s, part), tg[rp[s]:rp[s + 1]])
+        src = np.repeat(np.arange(cfg.n), np.diff(full_rp.astype(np.int64)))
+        order = np.lexsort((src, full_tg))
+        tg_sorted, src_sorted = full_tg[order], src[order]
+        starts = np.searchsorted(tg_sorted, np.arange(cfg.n + 1))
+        for j in range(0, cfg.n, 11):
+            assert np.array_equal(O.col(cfg, j), src_sorted[starts[j]:starts[j + 1]])
