@@ -42,14 +42,20 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10000)
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", default="spice", choices=["spice", "reference"])
-    ap.add_argument("--workload", default="synth", choices=["synth", "brunel100k", "brunelplus50k", "vogels4000"])
+    ap.add_argument("--workload", default="synth",
+                    choices=["synth", "synth250m", "brunel100k", "brunelplus50k", "vogels4000"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="synth workloads: weak = fixed synapses per GPU (N grows with G), "
+                         "strong = the G=1 network split over G GPUs")
     ap.add_argument("--tile-width", type=int, default=0)
     ap.add_argument("--ctas-per-tile", type=int, default=0)
     ap.add_argument("--global-atomics", action="store_true", help="paper-style delivery (A/B)")
     ap.add_argument("--unfused", action="store_true",
                     help="separate update and delivery launches per step (the G > 1 kernel sequence, A/B)")
     ap.add_argument("--profile-steps", type=int, default=200)
-    ap.add_argument("--e2e-steps", type=int, default=1000)
+    ap.add_argument("--e2e-steps", type=int, default=1024)
+    ap.add_argument("--e2e-chunk", type=int, default=32, help="steps per spice_step call in the e2e leg")
+    ap.add_argument("--no-parity", action="store_true", help="skip the in-run oracle check (synth)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--setup", action="store_true",
@@ -57,9 +63,13 @@ def parse_args():
     return ap.parse_args()
 
 
-def workload(name: str, G: int):
-    if name == "synth":
-        return W.synth_weak(G), "synth_3e9_synapses_per_gpu"
+def workload(name: str, G: int, scaling: str = "weak"):
+    if name in ("synth", "synth250m"):
+        per = 3.0e9 if name == "synth" else 250e6
+        tag = "3e9" if name == "synth" else "250m"
+        if scaling == "strong":
+            return W.synth_for_synapses(per), f"synth_{tag}_synapses_total_strong"
+        return W.synth_for_synapses(per * G), f"synth_{tag}_synapses_per_gpu"
     if name == "brunel100k":
         return W.brunel(100_000), "brunel100k"
     if name == "brunelplus50k":
@@ -69,7 +79,7 @@ def workload(name: str, G: int):
 
 def cpu_sample(name: str, cfg):
     """Bounded sample of the workload for the CPU oracle."""
-    if name == "synth":
+    if name in ("synth", "synth250m"):
         n = cfg.n // 32
         return W.synth(n, cfg.rules[0].k, cfg.activity, cfg.seed), \
             f"synth N={n} (1/32 of the GPU workload's neurons) with the same in-degree K={cfg.rules[0].k} and activity"
@@ -172,18 +182,51 @@ def main_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cfg, wl = workload(args.workload, args.gpus)
+    cfg, wl = workload(args.workload, args.gpus, args.scaling)
     sample, desc = cpu_sample(args.workload, cfg)
     eps, done, el, nnz = run_oracle(sample, max(3, args.warmup // 10), steps=args.steps)
     line = {"impl": "reference", "metric": METRIC, "value": eps, "unit": "events/s",
             "n_gpus": args.gpus, "steps": done, "warmup": max(3, args.warmup // 10),
-            "ms_per_step": el / done * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": el / done * 1e3, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u32" if cfg.model == W.SYNTH else "f32",
             "data": "synthetic", "config": {"workload": wl, "sample": desc, "sample_synapses": nnz},
             "cpu_baseline": {"value": eps, "unit": "events/s", "cores": 1, "kind": "oracle", "sample": desc},
             "e2e": {"value": eps, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def parity_check(net, cfg, rank: int, world: int, slice_width: int, n_acc: int = 2):
+    """In-run validation against the oracle at the bench size (reading R17):
+    (1) the spike union of the last two recorded steps, read through spice_read_spikes
+    (every rank decodes the gathered bitmaps of all ranks), equals the synth Bernoulli
+    definition; (2) the accumulators of n_acc sampled owned targets equal the brute-force
+    sum over their in-synapses of the sources' spike counts.  Synth only (the other
+    workloads are checked at full size by tests/test_gpu_fullsize.py)."""
+    if cfg.model != W.SYNTH:
+        return None
+    from oracle import oracle as O
+    T = net.stats()["steps"]
+    ok = True
+    for t in (T - 2, T - 1):
+        got = net.read_spikes(t, t + 1)[0]
+        ok &= bool(np.array_equal(got, O.synth_fired(cfg, t)))
+    acc = net.state(net_field_acc())
+    rng = np.random.default_rng(1234 + rank)
+    local = rng.choice(net.n_owned, size=min(n_acc, net.n_owned), replace=False)
+    for i in local:
+        from paper_2102_04681_b200 import spice as S
+        j = S.partition_local_to_global(int(i), rank, world, slice_width)
+        ok &= O.synth_acc(cfg, j, T) == int(acc[i])
+    return {"ok": bool(ok), "steps": T,
+            "checked": f"spike union of steps {T - 2}, {T - 1} (all {cfg.n} neurons) vs the Bernoulli "
+                       f"definition; accumulators of {len(local)} sampled targets per rank vs the "
+                       f"sum over their in-synapses (oracle/spice_oracle.c orc_synth_fired, orc_synth_acc)"}
+
+
+def net_field_acc():
+    from paper_2102_04681_b200 import spice as S
+    return S.FIELD_ACC
 
 
 def main_spice(args):
@@ -198,16 +241,19 @@ def main_spice(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2102_04681_b200 import build as B
-    B.build()
+    if local == 0:                                 # one build per node; the others wait
+        B.build()
+    if world > 1:
+        dist.barrier()
     from paper_2102_04681_b200 import spice as S
 
-    cfg, wl = workload(args.workload, world)
+    cfg, wl = workload(args.workload, world, args.scaling)
     nccl_id = None
     if world > 1:
         obj = [S.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    record = max(args.e2e_steps, 64) + 8
+    record = max(4 * args.e2e_chunk, 256)
     t0 = time.perf_counter()
     net = S.Network(cfg, rank=rank, world_size=world, device=local, nccl_id=nccl_id,
                     record_steps=record, global_atomics=args.global_atomics,
@@ -228,6 +274,10 @@ def main_spice(args):
         dist.all_reduce(t, op=op)
         return t.item()
 
+    MAX = dist.ReduceOp.MAX if world > 1 else None
+    SUM = dist.ReduceOp.SUM if world > 1 else None
+    MIN = dist.ReduceOp.MIN if world > 1 else None
+
     # ---- warm-up ----
     net.step(args.warmup)
     net.sync()
@@ -247,14 +297,15 @@ def main_spice(args):
     ck = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     s1 = net.stats()
-    ms_max = allreduce(ms, dist.ReduceOp.MAX if world > 1 else None)
-    events = allreduce(s1["delivered"] - s0["delivered"], dist.ReduceOp.SUM if world > 1 else None)
-    fired = allreduce(s1["fired"] - s0["fired"], dist.ReduceOp.SUM if world > 1 else None)
+    ms_max = allreduce(ms, MAX)
+    events = allreduce(s1["delivered"] - s0["delivered"], SUM)
+    fired = allreduce(s1["fired"] - s0["fired"], SUM)
     value = events / (ms_max / 1e3)
+    launches = net.launches(args.steps)
 
-    # ---- per-kernel live timing for the roofline (CUDA events around each launch) ----
+    # ---- per-kernel live timing for the roofline (CUDA events on the library stream) ----
     prof = net.profile(args.profile_steps)
-    ev_step = events / args.steps              # per launch of the step's delivery kernel
+    ev_step = events / args.steps / world     # per launch of this rank's step kernel
     sp_step = fired / args.steps
     # 4 B target record per event + 12 B per spike (row pointer + list entry)
     bytes_launch = 4.0 * ev_step + 12.0 * sp_step
@@ -263,33 +314,51 @@ def main_spice(args):
     small = net.launches(32) == 2                  # one-CTA persistent kernel (small networks)
     kern = ("k_small (whole steps, one CTA, 32 per launch)" if small else
             "k_fused (deliver t + update t+1)") if fused else ("k_global_atomics" if args.global_atomics else "k_deliver")
-    # the fused kernel as spice_step runs it (graph of back-to-back launches); the
-    # individually launched timings above carry per-launch overhead the graph does not
+    # spice_step runs the fused kernel back to back inside captured graphs: the in-graph
+    # timing is the kernel as the timed region ran it (the individually launched timing
+    # carries launch overhead the graph does not)
     launch_ms = (prof["fused_in_graph"] or prof["fused"]) if fused else prof["deliver"]
     achieved = bytes_launch / (launch_ms * 1e-3) / 1e9
-    step_ms_prof = launch_ms if fused else prof["update"] + prof["deliver"] + prof["exchange"]
+    step_ms = ms_max / args.steps
 
-    # ---- end to end through the public API: step + read that step's spikes to host ----
+    # ---- end to end through the public API: steps in chunks, every step's spikes read
+    #      back to host memory (double-buffered: chunk c's copy and decode overlap chunk c+1)
     G, Sw = world, net.slice_width
     words = S.partition_owned_count(cfg.n, 0, G, Sw)
     d2h = G * ((words + 31) // 32) * 4
-    ids = np.zeros(cfg.n, dtype=np.uint32)
-    offs = np.zeros(2, dtype=np.uint64)
+    K = args.e2e_chunk
+    nchunks = max(1, args.e2e_steps // K)
+    ids = np.zeros(cfg.n * K // 8 + 1024, dtype=np.uint32)
+    offs = np.zeros(K + 1, dtype=np.uint64)
     t_now = net.stats()["steps"]
+    got_spikes = 0
     barrier()
     te = time.perf_counter()
-    for q in range(args.e2e_steps):
-        net.step(1)
-        net.read_spikes_into(t_now + q, t_now + q + 1, ids, offs)
+    for c in range(nchunks):
+        net.step(K)
+        net.spikes_prefetch(t_now + c * K, t_now + (c + 1) * K, c & 1)
+        if c:
+            got_spikes += net.spikes_collect_into((c - 1) & 1, ids, offs)
+    got_spikes += net.spikes_collect_into((nchunks - 1) & 1, ids, offs)
     e2e_s = time.perf_counter() - te
     barrier()
-    e2e_s = allreduce(e2e_s, dist.ReduceOp.MAX if world > 1 else None)
-    e2e_events = events / args.steps * args.e2e_steps     # same per-step work
+    e2e_s = allreduce(e2e_s, MAX)
+    e2e_events = events / args.steps * nchunks * K     # same per-step work
     e2e_value = e2e_events / e2e_s
 
+    parity = None
+    if not args.no_parity:
+        p = parity_check(net, cfg, rank, world, Sw)
+        if p is not None:
+            p["ok"] = bool(allreduce(1.0 if p["ok"] else 0.0, MIN) > 0.5)
+            p["ranks"] = world
+            parity = p
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         sample, desc = cpu_sample(args.workload, cfg)
+        if world > 1:
+            desc += f" (sample of the whole {world}-GPU network)"
         eps, done, el, _ = run_oracle(sample, 3, seconds=args.cpu_seconds)
         cpu = {"value": eps, "unit": "events/s", "cores": 1, "kind": "oracle",
                "sample": f"{desc}; {done} steps in {el:.1f} s, single thread"}
@@ -300,18 +369,19 @@ def main_spice(args):
     traffic, traffic_src = ncu_traffic(wl, delivery) if fused else (None, None)
     line = {
         "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-        "wall_s_per_10k_steps": ms_max / args.steps * 10.0,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "wall_s_per_10k_steps": step_ms * 10.0,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "u32" if cfg.model == W.SYNTH else "f32",
         "data": "synthetic (seeded Philox network and drive; no datasets)",
         "config": {"workload": wl, "n_neurons": cfg.n,
                    "in_degree": cfg.rules[0].k if cfg.model == W.SYNTH else None,
                    "activity": cfg.activity if cfg.model == W.SYNTH else None, "delay": cfg.delay,
-                   "synapses_total": int(allreduce(info["n_synapses"], dist.ReduceOp.SUM if world > 1 else None)),
+                   "synapses_total": int(allreduce(info["n_synapses"], SUM)),
                    "synapses_rank0": info["n_synapses"], "spikes_per_step": fired / args.steps,
                    "events_per_step": events / args.steps,
                    "parallelism": f"model-parallel strided neuron slices x{world}",
+                   "exchange": "NCCL all-gather of spike bitmaps in the step graph" if world > 1 else None,
                    "delivery": delivery,
                    "l2": "no flush: synapse stream per step >> 126 MB L2 is read from 12 GB/GPU",
                    "setup_s": setup_s},
@@ -319,16 +389,17 @@ def main_spice(args):
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "traffic_source": traffic_src,
                      "bytes_per_launch": bytes_launch, "launch_ms": launch_ms,
-                     "bytes_model": "SURVEY §8(d): 4 B/event + 12 B/spike (delivery bytes only)",
+                     "bytes_model": "SURVEY §8(d): 4 B/event + 12 B/spike (delivery bytes only), rank 0's share",
                      "peak_source": peak_src,
-                     "kernel_share_of_step": (launch_ms / (ms_max / args.steps)) if fused else
-                                             (launch_ms / step_ms_prof if step_ms_prof else None),
+                     "kernel_share_of_step": launch_ms / step_ms if fused else None,
                      "kernel_ms": prof},
         "e2e": {"value": e2e_value, "unit": "events/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                "note": "spice_step(1) + spice_read_spikes of that step to host, every step"},
-        "gpu_launches": net.launches(args.steps),
+                "d2h_bytes_per_step": d2h, "steps": nchunks * K, "spikes_read": got_spikes,
+                "note": f"spice_step({K}) + spice_spikes_prefetch of those steps' bitmaps to pinned host memory, "
+                        f"decoded by spice_spikes_collect while the next chunk runs (double-buffered)"},
+        "gpu_launches": launches,
         "clocks": ck,
+        "parity": parity,
         "cpu_baseline": cpu,
     }
     if rank == 0:

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define SPICE_ABI_VERSION 1u
+#define SPICE_ABI_VERSION 2u
 
 #if defined(__GNUC__)
 #define SPICE_API __attribute__((visibility("default")))
@@ -64,6 +64,19 @@ enum { SPICE_FIXED_PROB = 0, SPICE_FIXED_INDEGREE = 1 };
                                               warps and global atomics (A/B baseline) */
 #define SPICE_FLAG_UNFUSED           0x4u  /* G = 1: separate update and delivery kernels
                                               instead of the fused deliver(t)+update(t+1) */
+#define SPICE_FLAG_USER_STREAM       0x8u  /* enqueue on spice_config.stream (may be the
+                                              legacy default stream 0) instead of a
+                                              library-owned non-blocking stream */
+
+/* Spike exchange between the G ranks (§III-D/E: "the only data that need
+ * to be exchanged between GPUs are spikes"; every rank must hold the union of all ranks'
+ * spikes of step t before it delivers them, Fig. 2). */
+enum { SPICE_EXCHANGE_NCCL = 0,   /* ncclAllGather of fixed-size bitmaps inside the step graph */
+       SPICE_EXCHANGE_PEER = 1 }; /* device-initiated: the update kernel stores its bitmap words
+                                     straight into every peer's receive window (CUDA IPC
+                                     mapped memory over NVLink/NVSwitch, or the same GPU),
+                                     and one release flag per rank and step; see
+                                     spice_peer_handle / spice_peer_connect */
 
 typedef struct {
     uint32_t src_begin, src_end;   /* range1, half-open global IDs */
@@ -105,66 +118,121 @@ typedef struct {
     uint32_t tile_width;           /* targets per delivery tile (multiple of 32,
                                       <= 49152); 0 = auto */
     uint32_t ctas_per_tile;        /* CTAs sharing one tile (>= 1); 0 = auto */
+    uint32_t group_lanes;          /* Brunel+ delivery: lanes per segment group (1, 2, 4, 8,
+                                      16, 32); 0 = auto from the mean segment length */
+    uint32_t exchange;             /* SPICE_EXCHANGE_NCCL | SPICE_EXCHANGE_PEER (G > 1) */
+    void    *stream;               /* cudaStream_t, used with SPICE_FLAG_USER_STREAM */
+    /* Device allocator for every buffer the library holds (e.g. the torch caching
+     * allocator); NULL = cudaMalloc/cudaFree.  dev_alloc returns NULL on failure (then
+     * SPICE_ENOMEM).  Buffers are returned through dev_free by spice_free. */
+    void *(*dev_alloc)(size_t bytes, void *ctx);
+    void  (*dev_free)(void *ptr, void *ctx);
+    void    *alloc_ctx;
 } spice_config;
 
-/* Create this rank's slice: expand the descriptor restricted to owned targets on the
- * GPU, allocate state, input ring, spike lists and the record
- * ring.  Collective over the world when world_size > 1 (NCCL communicator init).
- * Errors: EINVAL (N = 0, p outside [0,1], ranges outside [0,N), delay 0, rules of one
- * source with overlapping destination ranges, a fixed-in-degree segment too long to
- * sort, ...), ENOMEM, ECUDA, ENCCL.  *out is NULL on failure. */
+/* Create this rank's slice (§III-B: the descriptor {range1, range2, p}
+ * is "uploaded to the GPU where it is expanded"; §III-D: rank g expands
+ * {range1, range2 ∩ owned(g), p}; §III-F P:376 + Listing 1: owned(g) = the
+ * equal-width slices j with floor(j/S) mod G = g).  Allocates neuron state (SoA),
+ * the delay ring of input slots, spike lists, the record ring and the step
+ * graphs.  cfg and everything it points to is copied; the caller keeps ownership.
+ * Collective over the world when world_size > 1 with SPICE_EXCHANGE_NCCL (communicator
+ * init).  Errors: EINVAL (N = 0, p outside [0,1], ranges outside [0,N), delay 0, rules of
+ * one source with overlapping destination ranges, packed receptor counts that could
+ * overflow, ...), ENOMEM (message names the buffer), ECUDA, ENCCL.  *out is NULL on
+ * failure. */
 SPICE_API spice_status spice_create_network(const spice_config *cfg, spice_net **out);
 
-/* Enqueue n_steps lock-step simulation steps on the library stream (CUDA-graph replay;
- * update -> [all-gather] -> deliver per step).  Returns after enqueueing. */
+/* Enqueue n_steps lock-step simulation steps on the library stream and return.  Step t
+ * (reading R2): every owned neuron is updated, reading and clearing input slot
+ * t mod D (P:161 onUpdate, "invoked by the framework on every simulation step"); the
+ * spiking IDs form S_t ("inserted into one of delay many spike arrays"); G > 1: S_t
+ * is exchanged so every rank holds the union; S_t is delivered row by row into
+ * slot (t + delay) mod D ("delivered to all neighbors in said row"); Brunel+ applies
+ * STDP on the same synapse stream (reading R13).  n_steps is decomposed into
+ * replays of captured step graphs of 2^k steps (k <= 8); inside a replay every step but
+ * the first is one fused kernel (delivery of t + update of t + 1).  No host round trip;
+ * n_steps = 0 is a no-op.  ESTATE on a poisoned or external-exchange handle. */
 SPICE_API spice_status spice_step(spice_net *net, uint64_t n_steps);
 
-/* Copy the spikes of steps [t_begin, t_end) to the host (synchronises the stream).
- * ids receives global IDs, ascending within each step, the same list on every rank;
- * offsets (t_end - t_begin + 1 entries) receives per-step starts.  ERANGE if a step is
- * not in the record ring (older than record_steps or not yet simulated); ETRUNC if cap
- * is too small (then *total = spikes needed, nothing else written). */
+/* Copy the spikes of steps [t_begin, t_end) to the host (synchronises the stream): the
+ * spike arrays S_t of P:161, as the union over all ranks (Fig. 2; reading R11:
+ * ascending global IDs, at most one spike per neuron and step).  ids (caller-owned,
+ * cap entries) receives global IDs, ascending within each step, the same list on every
+ * rank; offsets (t_end - t_begin + 1 entries, may be NULL) receives per-step starts.
+ * ERANGE if a step is not in the record ring (older than record_steps or not yet
+ * simulated); ETRUNC if cap is too small (then *total = spikes needed, nothing else
+ * written). */
 SPICE_API spice_status spice_read_spikes(spice_net *net, uint64_t t_begin, uint64_t t_end,
                                uint32_t *ids, uint64_t cap, uint64_t *offsets,
                                uint64_t *total);
 
-/* Release everything.  NULL-safe.  Collective when an NCCL communicator exists. */
+/* Release everything the handle owns (device buffers through dev_free when given, the
+ * graphs, the library stream, the NCCL communicator or peer mappings).  NULL-safe; valid
+ * on a poisoned handle.  Collective when an NCCL communicator exists. */
 SPICE_API spice_status spice_free(spice_net *net);
+
+/* Double-buffered spike read-out for streaming runs (same data and ordering as
+ * spice_read_spikes).  prefetch enqueues, on the library stream after the steps already
+ * enqueued, an asynchronous copy of the recorded bitmaps of steps [t_begin, t_end) into
+ * library-owned pinned host slot `slot` (0 or 1) and returns without waiting; collect
+ * waits for that slot's copy only (an event, not a stream sync, so later enqueued steps
+ * keep running) and decodes it into ids / offsets as spice_read_spikes does.  ERANGE as
+ * spice_read_spikes (t_end may exceed the steps enqueued so far by 0); ESTATE when collect
+ * names an empty slot. */
+SPICE_API spice_status spice_spikes_prefetch(spice_net *net, uint64_t t_begin, uint64_t t_end,
+                                             uint32_t slot);
+SPICE_API spice_status spice_spikes_collect(spice_net *net, uint32_t slot, uint32_t *ids,
+                                            uint64_t cap, uint64_t *offsets, uint64_t *total);
 
 /* ---------------------------- parity / debug hooks --------------------------- */
 
-/* Rows [row_begin, row_end) (global source IDs) of this rank's synapses, as global
- * target IDs ascending within each row.  row_offsets has row_end - row_begin + 1
- * entries.  ETRUNC semantics as in spice_read_spikes. */
+/* Rows [row_begin, row_end) (global source IDs) of this rank's adjacency list: the
+ * rank's half of every row split at its slice pivots (§III-D), as global target
+ * IDs ascending within each row ("Each row's entries are sorted"; padding sentinels
+ * removed).  tgt_global is caller-owned (cap entries); row_offsets has
+ * row_end - row_begin + 1 entries.  Synchronises.  EINVAL for rows outside [0, N);
+ * ETRUNC semantics as in spice_read_spikes. */
 SPICE_API spice_status spice_read_connectivity(spice_net *net, uint32_t row_begin, uint32_t row_end,
                                      uint32_t *tgt_global, uint64_t cap,
                                      uint64_t *row_offsets, uint64_t *total);
 
-/* Fields of the owned neurons in local order (n = owned count):
+/* Neuron state (the SoA neuron pool of P:151 §III-A) of the owned neurons in local order
+ * (Listing 1; n must equal the owned count, host buffer caller-owned):
  * 0 v (f32), 1 ge (f32), 2 gi (f32), 3 refractory counter (u32), 4 synth accumulator
- * (u32), 5 pre trace x (f32), 6 post trace y (f32). EINVAL for a field the model lacks. */
+ * (u32), 5 pre trace x (f32; the trace of the owned neuron's own spikes, reading R13),
+ * 6 post trace y (f32).  Both calls synchronise the stream and act on the state after the
+ * steps enqueued so far.  EINVAL for a field the model lacks or a wrong n. */
 enum { SPICE_FIELD_V = 0, SPICE_FIELD_GE = 1, SPICE_FIELD_GI = 2, SPICE_FIELD_REF = 3,
        SPICE_FIELD_ACC = 4, SPICE_FIELD_XTR = 5, SPICE_FIELD_YTR = 6 };
 SPICE_API spice_status spice_read_state(spice_net *net, uint32_t field, void *host_out, uint64_t n);
 SPICE_API spice_status spice_write_state(spice_net *net, uint32_t field, const void *host_in, uint64_t n);
 
-/* Input slot that the update of step (t_now + rel) reads, rel in [0, delay]: packed
- * receptor counts (exc in bits 0-15, inh in bits 16-31; one population: all 32 bits)
- * and, for Brunel+, plastic fixed-point sums rint(w 2^32) (plastic may be NULL). */
+/* The spike-array slot of the delay ring ("selecting the appropriate spike
+ * array based on the current simulation step and delay") that the update of step
+ * (t_now + rel) reads, rel in [0, delay], for the owned neurons in local order (n = owned
+ * count): packed receptor counts (reading R10: exc in bits 0-15, inh in bits 16-31; one
+ * population: all 32 bits) and, for Brunel+, plastic fixed-point sums rint(w 2^32)
+ * (plastic may be NULL).  Synchronises.  EINVAL for rel > delay or a wrong n. */
 SPICE_API spice_status spice_read_input(spice_net *net, uint32_t rel, uint32_t *counts,
                               int64_t *plastic, uint64_t n);
 
-/* Plastic weights of this rank's synapses in the order of spice_read_connectivity for
- * rows [row_begin, row_end); non-plastic synapses read as 0.  ETRUNC as above. */
+/* Plastic weights (the synapse pool mapped 1:1 onto the adjacency list) of this
+ * rank's synapses in the order of spice_read_connectivity for rows [row_begin, row_end);
+ * non-plastic synapses read as 0.  Brunel+ only (EINVAL otherwise).  ETRUNC as above. */
 SPICE_API spice_status spice_read_weights(spice_net *net, uint32_t row_begin, uint32_t row_end,
                                 float *w, uint64_t cap, uint64_t *total);
 
-/* Teacher forcing of the next step: mode 1 replaces its spike set by the owned
- * neurons among ids (global IDs), mode 2 adds them to the natural set. */
+/* Teacher forcing of the next step (the north star's "per-step synaptic input under
+ * teacher-forced identical spikes" parity criterion): mode 1 replaces its spike set by the
+ * owned neurons among ids (global IDs), mode 2 adds them to the natural set; a forced
+ * spike resets the neuron like a natural one (reading R5).  Synchronises.  EINVAL for an
+ * id >= N or another mode. */
 SPICE_API spice_status spice_force_spikes(spice_net *net, const uint32_t *ids, uint64_t n, int mode);
 
 /* Counters since create (synchronises): steps done, spikes emitted by owned neurons,
- * synaptic events delivered to owned neurons. */
+ * synaptic events delivered to owned neurons (one per (spike, synapse) pair, P:200;
+ * the numerator of the BASELINE metric "synaptic events/sec"). */
 SPICE_API spice_status spice_stats(spice_net *net, uint64_t *steps, uint64_t *fired,
                          uint64_t *delivered);
 
@@ -216,11 +284,14 @@ SPICE_API const char *spice_last_error(void);
 
 /* ------------------------- multi-GPU plumbing -------------------------------- */
 
-/* Fill 128 bytes with a fresh ncclUniqueId (rank 0 only; broadcast it yourself). */
+/* Fill 128 bytes with a fresh ncclUniqueId (rank 0 only; broadcast it yourself).  The
+ * NCCL exchange replaces the paper's host-driven hierarchical cudaMemcpy synchronisation
+ * (§III-E, Fig. 2) by one all-gather of fixed-size bitmaps per step. */
 SPICE_API spice_status spice_nccl_unique_id(void *out128);
 
 /* External exchange (SPICE_FLAG_EXTERNAL_EXCHANGE; used for single-GPU "virtual rank"
- * tests): begin enqueues the neuron update of the next step, leaving this rank's spike
+ * tests of the exchange step): begin enqueues the neuron update of the next
+ * step, leaving this rank's spike
  * bitmap (words_per_rank u32 words) in the send buffer; the caller must fill the receive
  * buffer (world_size * words_per_rank words, rank r at offset r * words_per_rank) and
  * then call end, which enqueues bitmap->list conversion and delivery. */

@@ -79,6 +79,10 @@ def lib(precision: str = "mirror32"):
     L.orc_row.argtypes = [C.POINTER(_Rule), u32, u64, u32, u32, u32, u32, vp, u64]
     L.orc_col.restype = u64
     L.orc_col.argtypes = [C.POINTER(_Rule), u32, u64, u32, vp, u64]
+    L.orc_synth_fired.restype = u64
+    L.orc_synth_fired.argtypes = [u32, dbl, u64, u64, vp, u64]
+    L.orc_synth_acc.restype = u64
+    L.orc_synth_acc.argtypes = [C.POINTER(_Rule), u32, u64, dbl, u32, u64, u32]
     L.orc_set_input.argtypes = [vp, u32, vp]
     L.orc_set_time.argtypes = [vp, u64]
     _LIBS[tag] = L
@@ -127,6 +131,21 @@ def col(cfg, j: int) -> np.ndarray:
         if n <= cap:
             return out[:n]
         cap = int(n)
+
+
+def synth_fired(cfg, t: int) -> np.ndarray:
+    """Synth spike set of step t by the Bernoulli definition (reading R12), no simulation."""
+    out = np.zeros(max(16, int(cfg.n * cfg.activity * 2) + 64), dtype=np.uint32)
+    while True:
+        n = lib().orc_synth_fired(cfg.n, cfg.activity, cfg.seed, t, out.ctypes.data, out.size)
+        if n <= out.size:
+            return out[:n]
+        out = np.zeros(int(n), dtype=np.uint32)
+
+
+def synth_acc(cfg, j: int, T: int) -> int:
+    """Synth accumulator of target j after T steps (sampled-column check, reading R17)."""
+    return int(lib().orc_synth_acc(_rules(cfg), len(cfg.rules), cfg.seed, cfg.activity, j, T, cfg.delay))
 
 
 def owner(j: int, G: int, S: int) -> int:

@@ -655,3 +655,46 @@ EXPORT int orc_force_next(orc_net *N, const uint32_t *ids, uint64_t n, int mode)
     N->force_t = (int64_t)N->t;
     return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Synth checkers for sizes the oracle cannot simulate (reading R17; SURVEY     */
+/* C17).  Both are the plain definitions: the synth spike set of step t is the  */
+/* Bernoulli draw of reading R12 for every neuron, and a synth accumulator is   */
+/* the number of spikes its in-synapses carried (P:200 delivery, reading R10).  */
+/* ------------------------------------------------------------------------- */
+
+/* Synth spikes of step t (reading R12): j fires iff Philox(j>>2, t, 0, TAG_FIRE)[j&3] <
+ * floor(a 2^32), ascending.  Returns the count (writes at most cap ids). */
+EXPORT uint64_t orc_synth_fired(uint32_t n, double activity, uint64_t seed, uint64_t t,
+                                uint32_t *out, uint64_t cap)
+{
+    uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
+    uint64_t thr = prob_threshold(activity), c = 0;
+    for (uint32_t j = 0; j < n; j++) {
+        uint32_t x = philox_word(j >> 2, (uint32_t)t, 0, TAG_FIRE, key0, key1, j & 3);
+        if ((uint64_t)x < thr) { if (c < cap) out[c] = j; c++; }
+    }
+    return c;
+}
+
+/* Synth accumulator of target j after T steps with delay d (no teacher forcing):
+ * acc_j = sum over in-synapses (s -> j), with multiplicity, of the number of steps
+ * t < T - d at which s fired (a spike of step t reaches the update of step t + d). */
+EXPORT uint64_t orc_synth_acc(const orc_rule *rules, uint32_t n_rules, uint64_t seed, double activity,
+                              uint32_t j, uint64_t T, uint32_t d)
+{
+    uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
+    uint64_t thr = prob_threshold(activity), acc = 0;
+    uint64_t n = orc_col(rules, n_rules, seed, j, NULL, 0);
+    uint32_t *src = malloc((n ? n : 1) * sizeof(uint32_t));
+    orc_col(rules, n_rules, seed, j, src, n);
+    for (uint64_t q = 0; q < n; q++) {
+        uint32_t s = src[q];
+        for (uint64_t t = 0; t + d < T; t++) {
+            uint32_t x = philox_word(s >> 2, (uint32_t)t, 0, TAG_FIRE, key0, key1, s & 3);
+            acc += (uint64_t)x < thr;
+        }
+    }
+    free(src);
+    return acc;
+}

@@ -110,12 +110,17 @@ struct spice_net {
     std::vector<double> prm;
     std::vector<spice_rule> rules;
     int device = 0, n_sm = 148;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;      // execution stream (library-owned or the caller's)
+    bool own_stream = true;
+    cudaStream_t cap_stream = nullptr;  // library-owned capture stream (graphs are captured here)
+    void *(*dev_alloc)(size_t, void *) = nullptr;   // caller's device allocator (or cudaMalloc)
+    void (*dev_free)(void *, void *) = nullptr;
+    void *alloc_ctx = nullptr;
     bool poisoned = false;
     bool external = false;
     // geometry
     uint64_t n_own = 0, n_own_max = 0;
-    uint32_t W = 0, TW = 32, NT = 1, C = 1, TWs = 32, rstages = 0;
+    uint32_t W = 0, TW = 32, NT = 1, C = 1, TWs = 32;
     uint64_t ring_stride = 0;
     uint64_t nnz = 0;        // stored entries (incl. padding sentinels)
     uint64_t n_syn = 0;      // synapses (owned targets)
@@ -127,9 +132,14 @@ struct spice_net {
     bool small = false;                 // one-CTA persistent step kernel (k_small)
     uint32_t *hbm = nullptr;            // pinned host staging of recorded bitmaps (read_spikes)
     uint64_t hbm_words = 0;
+    struct Slot {                       // double-buffered read-out (spikes_prefetch/collect)
+        uint32_t *h = nullptr;
+        uint64_t words = 0, t_begin = 0, t_end = 0;
+        bool full = false;
+        cudaEvent_t done = nullptr;
+    } slot[2];
     std::vector<std::vector<uint32_t>> hdec;   // decoded per-step lists (reused)
     uint32_t NR = 1, RS = 32;    // spike-list regions
-    uint32_t dcap = 0;           // descriptors staged in shared memory per delivering CTA
     unsigned long long *ptimes = nullptr;   // SPICE_PHASES diagnostics
     bool fused = true, global_atomics = false;
     // device memory
@@ -144,13 +154,6 @@ struct spice_net {
     uint64_t *sl_rows = nullptr;
     uint64_t *desc = nullptr;
     uint32_t *dcount = nullptr;
-    uint32_t *wl = nullptr, *wcount = nullptr;   // window lists (default G = 1 delivery)
-    uint64_t wstride = 0;
-    // tile-pair exchange (G = 1)
-    uint16_t *xbuf = nullptr;
-    uint64_t *xoff = nullptr;
-    uint32_t *xcnt = nullptr;
-    uint64_t xtotal = 0;
     uint32_t *record = nullptr, *sendbuf = nullptr, *gather = nullptr;
     unsigned long long *fired_cta = nullptr, *delivered_cta = nullptr;
     uint64_t *t0 = nullptr;
@@ -167,9 +170,9 @@ struct spice_net {
     SimArgs args{};
     // host progress
     uint64_t t_host = 0;
-    // graphs
-    static constexpr uint32_t kGraphSteps = 32;
-    cudaGraphExec_t g_big = nullptr, g_one = nullptr;
+    // step graphs: graphs[k] runs 2^k steps (k < kGraphLevels)
+    static constexpr uint32_t kGraphLevels = 9;
+    cudaGraphExec_t graphs[kGraphLevels] = {};
     // nccl
     ncclComm_t comm = nullptr;
     cudaEvent_t ev = nullptr;
@@ -207,15 +210,24 @@ spice_status fail(spice_net *n, spice_status st, const char *fmt, ...) {
 
 spice_status dalloc(spice_net *n, void **p, size_t bytes, const char *what) {
     *p = nullptr;
-    cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(n, SPICE_ENOMEM, "cudaMalloc of %zu bytes for %s failed: %s", bytes, what,
-                    cudaGetErrorString(e));
+    if (n->dev_alloc) {
+        *p = n->dev_alloc(bytes ? bytes : 16, n->alloc_ctx);
+        if (!*p) return fail(n, SPICE_ENOMEM, "dev_alloc of %zu bytes for %s failed", bytes, what);
+    } else {
+        cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(n, SPICE_ENOMEM, "cudaMalloc of %zu bytes for %s failed: %s", bytes, what,
+                        cudaGetErrorString(e));
+        }
     }
     n->allocs.push_back(*p);
     n->device_bytes += bytes;
     return SPICE_OK;
+}
+void release(spice_net *n, void *p) {
+    if (n->dev_free) n->dev_free(p, n->alloc_ctx);
+    else if (!n->dev_alloc) cudaFree(p);
 }
 template <typename T>
 spice_status dalloc_t(spice_net *n, T **p, size_t count, const char *what) {
@@ -225,7 +237,7 @@ void dfree(spice_net *n, void *p) {
     if (!p) return;
     auto it = std::find(n->allocs.begin(), n->allocs.end(), p);
     if (it != n->allocs.end()) n->allocs.erase(it);
-    cudaFree(p);
+    release(n, p);
 }
 
 spice_status validate(const spice_config *c) {
@@ -293,9 +305,8 @@ void build_model_const(spice_net *n) {
     }
 }
 
-// Enqueue steps k = 0..steps-1 of one replay (each kernel reads t = *t0 + k).
-spice_status enqueue_steps(spice_net *n, uint32_t steps) {
-    cudaStream_t s = n->stream;
+// Enqueue steps k = 0..steps-1 of one replay (each kernel reads t = *t0 + k) on stream s.
+spice_status enqueue_steps(spice_net *n, uint32_t steps, cudaStream_t s) {
     const SimArgs &a = n->args;
     if (n->small) {                                        // one launch for the whole chunk
         CU(n, launch_small(a, 0, steps, s));
@@ -331,9 +342,9 @@ spice_status enqueue_steps(spice_net *n, uint32_t steps) {
 
 spice_status capture_graph(spice_net *n, uint32_t steps, cudaGraphExec_t *out) {
     cudaGraph_t g = nullptr;
-    CU(n, cudaStreamBeginCapture(n->stream, cudaStreamCaptureModeThreadLocal));
-    spice_status st = enqueue_steps(n, steps);
-    cudaError_t e2 = cudaStreamEndCapture(n->stream, &g);
+    CU(n, cudaStreamBeginCapture(n->cap_stream, cudaStreamCaptureModeThreadLocal));
+    spice_status st = enqueue_steps(n, steps, n->cap_stream);
+    cudaError_t e2 = cudaStreamEndCapture(n->cap_stream, &g);
     if (st != SPICE_OK) { if (g) cudaGraphDestroy(g); return st; }
     if (e2 != cudaSuccess) return fail(n, SPICE_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(e2));
     cudaError_t err = cudaGraphInstantiate(out, g, 0);
@@ -345,14 +356,18 @@ spice_status capture_graph(spice_net *n, uint32_t steps, cudaGraphExec_t *out) {
 void destroy(spice_net *n) {
     if (!n) return;
     if (n->stream) cudaStreamSynchronize(n->stream);
-    if (n->g_big) cudaGraphExecDestroy(n->g_big);
-    if (n->g_one) cudaGraphExecDestroy(n->g_one);
+    for (cudaGraphExec_t &g : n->graphs) if (g) cudaGraphExecDestroy(g);
     if (n->comm) nccl().CommDestroy(n->comm);
-    for (void *p : n->allocs) cudaFree(p);
+    for (void *p : n->allocs) release(n, p);
     n->allocs.clear();
     if (n->ev) cudaEventDestroy(n->ev);
     if (n->hbm) cudaFreeHost(n->hbm);
-    if (n->stream) cudaStreamDestroy(n->stream);
+    for (auto &sl : n->slot) {
+        if (sl.h) cudaFreeHost(sl.h);
+        if (sl.done) cudaEventDestroy(sl.done);
+    }
+    if (n->stream && n->own_stream) cudaStreamDestroy(n->stream);
+    if (n->cap_stream) cudaStreamDestroy(n->cap_stream);
     delete n;
 }
 
@@ -372,16 +387,6 @@ __global__ void indegree_kernel(const uint64_t *row_ptr, const uint32_t *bnd, co
             const uint32_t x = (uint32_t)ent[st + e] >> eshift;
             if (x < TW) atomicAdd(&deg[(uint64_t)b * TW + x], q);     // skip padding sentinels
         }
-    }
-}
-// Windows per destination tile summed over all rows (capacity of the tile's window list).
-__global__ void tile_windows_kernel(const uint32_t *bnd, uint32_t N, uint32_t NT, unsigned long long *tw) {
-    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < (uint64_t)N * NT;
-         w += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = (uint32_t)(w / NT), b = (uint32_t)(w % NT);
-        const uint32_t *bp = bnd + (uint64_t)s * (NT + 1) + b;
-        const uint32_t nw = (bp[1] - bp[0]) >> 3;
-        if (nw) atomicAdd(&tw[b], (unsigned long long)nw);
     }
 }
 __global__ void max_halves_kernel(const uint32_t *deg, uint64_t n, uint32_t *out) {
@@ -454,8 +459,10 @@ spice_status generate(spice_net *n) {
     dfree(n, cursor);
     n->device_bytes -= nb * 4;
     n->mean_seg = n->N ? (double)nnz / ((double)n->N * n->NT) : 0;
-    // receptor packing check (two populations only)
-    if (n->n_exc < n->N && n->n_own) {
+    // receptor packing check: exc counts in bits 0-15 and inh counts in bits 16-31 (two
+    // populations), or one 32-bit count (one population: only the synth accumulator reads
+    // it as a whole; the other models unpack the low half, so it must stay < 65535 too)
+    if (n->n_own && (n->n_exc < n->N || n->model != SPICE_SYNTH)) {
         uint32_t *deg = nullptr, *mx = nullptr;
         if ((st = dalloc_t(n, &deg, n->ring_stride, "in-degree check"))) return st;
         if ((st = dalloc_t(n, &mx, 2, "in-degree max"))) return st;
@@ -532,6 +539,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     n->S = c->slice_width ? c->slice_width : spice_default_slice_width(c->n_neurons, c->world_size);
     n->flags = c->flags; n->R = c->record_steps; n->dt = c->dt_ms; n->activity = c->activity;
     n->seed = c->seed; n->device = c->device;
+    n->dev_alloc = c->dev_alloc; n->dev_free = c->dev_free; n->alloc_ctx = c->alloc_ctx;
     n->external = (c->flags & SPICE_FLAG_EXTERNAL_EXCHANGE) != 0;
     n->prm.assign(c->model_params, c->model_params + c->n_model_params);
     n->rules.assign(c->rules, c->rules + c->n_rules);
@@ -542,7 +550,14 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         cudaError_t e = cudaSetDevice(n->device);
         if (e) return bail(fail(n, SPICE_ECUDA, "cudaSetDevice(%d): %s", n->device, cudaGetErrorString(e)));
         cudaDeviceGetAttribute(&n->n_sm, cudaDevAttrMultiProcessorCount, n->device);
-        e = cudaStreamCreateWithFlags(&n->stream, cudaStreamNonBlocking);
+        if (c->flags & SPICE_FLAG_USER_STREAM) {
+            n->stream = (cudaStream_t)c->stream;
+            n->own_stream = false;
+        } else {
+            e = cudaStreamCreateWithFlags(&n->stream, cudaStreamNonBlocking);
+            if (e) return bail(fail(n, SPICE_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)));
+        }
+        e = cudaStreamCreateWithFlags(&n->cap_stream, cudaStreamNonBlocking);
         if (e) return bail(fail(n, SPICE_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)));
         cudaEventCreateWithFlags(&n->ev, cudaEventDisableTiming);
     }
@@ -551,15 +566,15 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     n->n_own_max = owned_count(n->N, 0, n->G, n->S);
     n->W = (uint32_t)((n->n_own_max + 31) / 32);
     // ---- delivery tiles ----
-    // padded segments + window-stream delivery: single rank, descriptor path (not Brunel+,
-    // not the tile-pair exchange experiment); SPICE_NOPAD=1 keeps the unpadded layout.
+    // padded segments (every (row, tile) segment a whole number of 16-byte windows) for all
+    // models but Brunel+ (whose plastic weights are aligned with the unpadded entries).
     // Padded entries are byte offsets up to kMaxPadTile targets per tile, counter indices
     // (one more shift per entry) up to kMaxPadTileWord.
     // C CTAs per tile (ctas_per_tile): the tile is cut into C slices of TWs = TW / C targets
     // (multiples of 32); CTA x updates slice x.  On the fused G = 1 path the C CTAs form a
     // thread-block cluster that reduces the tile's counters through distributed shared memory.
     // (G > 1: the bitmap->list kernel writes the descriptors of the gathered spikes)
-    n->pad8 = n->model != SPICE_BRUNEL_PLUS && !getenv("SPICE_XCHG") && !getenv("SPICE_NOPAD");
+    n->pad8 = n->model != SPICE_BRUNEL_PLUS;
     // auto: 2-CTA cluster tiles for large padded networks (half the spike x tile visits per
     // CTA; measured -4 % step time on synth 3e9, DESIGN.md delivery log), else one CTA per tile
     n->C = c->ctas_per_tile ? c->ctas_per_tile
@@ -580,7 +595,6 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     } else if (c->tile_width) {
         const uint32_t q = 32u * n->C;
         n->TW = (c->tile_width + q - 1) / q * q;
-        if (n->TW > kMaxPadTileWord) n->pad8 = false;
     } else {
         const uint64_t want = (uint64_t)std::max(1, n->n_sm / (int)n->C) * n->C;   // one CTA per SM
         uint64_t tws = (n->n_own + want - 1) / want;
@@ -600,22 +614,8 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (n->G == 1) { n->NR = n->NT * n->C; n->RS = n->TWs; }
     else { n->NR = (uint32_t)(((uint64_t)n->G * n->W + kB2LWords - 1) / kB2LWords); n->RS = kB2LWords * 32; }
     if (n->NR > kMaxRegions) return bail(fail(n, SPICE_EINVAL, "%u spike-list regions > %u: use a wider tile_width", n->NR, kMaxRegions));
-    // descriptor staging capacity: kDescSmem, shrunk (not below the update's staging area)
-    // when wide tiles need the shared memory
-    n->dcap = kDescSmem;
     const size_t smem_max = 227 * 1024 - 2048;             // dynamic; static shared variables need the rest
-    while (n->dcap > (uint32_t)kStageWords / 2 && tile_smem_bytes(n->TW, n->NR, n->dcap, 0) > smem_max) n->dcap -= 512;
-    if (tile_smem_bytes(n->TW, n->NR, n->dcap, 0) > smem_max) return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for shared memory", n->TW));
-    // staged-ring delivery (padded layout, opt-in A/B: SPICE_RSTAGES=4|8).  Measured slower
-    // than the register ring on synth 3e9 (DESIGN.md delivery log): more windows in flight
-    // per warp do not help once the SM's outstanding-request capacity is in use.
-    n->rstages = 0;
-    if (n->pad8) {
-        if (const char *e = getenv("SPICE_RSTAGES")) {
-            const uint32_t v = (uint32_t)atoi(e);
-            if (v == 0 || ((v == 4 || v == 8) && tile_smem_bytes(n->TW, n->NR, n->dcap, v) <= smem_max)) n->rstages = v;
-        }
-    }
+    if (n->pad8 && tile_smem_bytes(n->TW, n->NR) > smem_max) return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for shared memory", n->TW));
     // ---- NCCL communicator ----
     if (n->G > 1 && !n->external) {
         if (!nccl().ok) return bail(fail(n, SPICE_ENCCL, "libnccl.so.2 not found (set SPICE_NCCL_LIB)"));
@@ -682,11 +682,11 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         CU(n, cudaMemsetAsync(n->pring, 0, (size_t)n->D * n->ring_stride * 8, s));
         CU(n, cudaMemsetAsync(n->xtr, 0, 2ull * n->N * 4, s));
         CU(n, cudaMemsetAsync(n->ytr, 0, no * 4, s));
-        CU(n, gen_plastic(g2, pbx, n->row_ptr, n->bnd, n->ent, n->w, (float)n->prm[15], tmp, n->in_ptr,
-                          &n->in_pos, &n->in_src, &n->n_plastic, s));
-        n->allocs.push_back(n->in_pos);
-        n->allocs.push_back(n->in_src);
-        n->device_bytes += n->n_plastic * 12;
+        CU(n, gen_plastic_count(g2, pbx, n->row_ptr, n->bnd, n->ent, n->w, (float)n->prm[15], tmp, n->in_ptr,
+                                &n->n_plastic, s));
+        if ((st = dalloc_t(n, &n->in_pos, std::max<uint64_t>(n->n_plastic, 1), "in-synapse positions"))) return bail(st);
+        if ((st = dalloc_t(n, &n->in_src, std::max<uint64_t>(n->n_plastic, 1), "in-synapse sources"))) return bail(st);
+        CU(n, gen_plastic_fill(g2, pbx, n->row_ptr, n->bnd, n->ent, tmp, n->in_ptr, n->in_pos, n->in_src, s));
         CU(n, cudaStreamSynchronize(s));
         dfree(n, tmp);
     }
@@ -712,73 +712,16 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         n->mc.ptab_half = p2 >> 1;
     }
     CU(n, cudaStreamSynchronize(s));
-    // ---- tile-pair exchange (G = 1): static chunk capacities from the connectivity ----
-    // experimental (opt-in, SPICE_XCHG=1): measured slower than descriptor transposition on
-    // synth 3e9 (producer segment copies dominate), see DESIGN.md "Delivery design log"
-    if (n->G == 1 && n->model != SPICE_BRUNEL_PLUS && n->C == 1 && !n->global_atomics && getenv("SPICE_XCHG") &&
-        xchg_kernel_smem_bytes(n->TW, n->NT) <= 227 * 1024) {
-        std::vector<uint64_t> rp(n->N + 1);
-        CU(n, cudaMemcpy(rp.data(), n->row_ptr, (n->N + 1) * 8ull, cudaMemcpyDeviceToHost));
-        uint64_t maxlen = 0;
-        for (uint32_t q = 0; q < n->N; ++q) maxlen = std::max<uint64_t>(maxlen, rp[q + 1] - rp[q]);
-        if (((maxlen + 7 + 7) / 8 * 8) * 2 <= kXRowsBytes) {
-            SimArgs ta{};
-            ta.N = n->N; ta.n_exc = n->n_exc; ta.TW = n->TW; ta.NT = n->NT; ta.bnd = n->bnd;
-            const uint64_t nc = (uint64_t)n->NT * n->NT * 2;
-            uint32_t *cap = nullptr;
-            if ((st = dalloc_t(n, &cap, nc, "exchange capacities"))) return bail(st);
-            CU(n, launch_xcap(ta, cap, s));
-            std::vector<uint32_t> hc(nc);
-            CU(n, cudaMemcpyAsync(hc.data(), cap, nc * 4, cudaMemcpyDeviceToHost, s));
-            CU(n, cudaStreamSynchronize(s));
-            dfree(n, cap);
-            n->device_bytes -= nc * 4;
-            std::vector<uint64_t> off(nc);
-            uint64_t tot = 0;
-            for (uint64_t q = 0; q < nc; ++q) { off[q] = tot; tot += (hc[q] + 7) / 8 * 8; }   // 16-byte aligned chunks
-            n->xtotal = tot + 8;
-            if ((st = dalloc_t(n, &n->xoff, nc, "exchange offsets"))) return bail(st);
-            if ((st = dalloc_t(n, &n->xcnt, 2 * nc, "exchange counts"))) return bail(st);
-            if ((st = dalloc_t(n, &n->xbuf, 2 * n->xtotal + 2 * kEntPad, "exchange chunks"))) return bail(st);
-            CU(n, cudaMemcpyAsync(n->xoff, off.data(), nc * 8, cudaMemcpyHostToDevice, s));
-            CU(n, cudaMemsetAsync(n->xcnt, 0, 2 * nc * 4, s));
-            CU(n, cudaStreamSynchronize(s));
-        }
-    }
-    // descriptor transposition path (G = 1 without the exchange)
-    // padded-layout delivery structures (G = 1): per-tile segment-descriptor lists consumed
-    // through per-warp window rings (default), or per-tile window lists written by the
-    // producers (SPICE_WLIST=1; measured slower: the window writes cost the producer more
-    // than the consumer saves, DESIGN.md delivery log)
-    const bool segdesc = !(getenv("SPICE_WLIST") && atoi(getenv("SPICE_WLIST"))) || n->eshift == 0 || n->C > 1 || n->G > 1;
-    // (not with the paper-style global-atomics delivery: it walks the spike lists itself, and
-    //  nothing would recycle the descriptor-list counters)
-    if (n->pad8 && !n->xbuf && segdesc && !n->global_atomics) {
+    // padded-layout delivery structures: per-tile segment-descriptor lists (written by the
+    // producers of the step's spikes, consumed through per-warp window rings).  Not with the
+    // paper-style global-atomics delivery: it walks the spike lists itself.
+    if (n->pad8 && !n->global_atomics) {
         // a tile's list holds every spike of the step: the rank's own (G = 1) or all N (G > 1)
         const uint64_t dstride = ((n->G == 1 ? n->n_own : (uint64_t)n->N) + 1) & ~1ull;
         if ((st = dalloc_t(n, &n->desc, 2ull * n->NT * dstride, "segment descriptors"))) return bail(st);
         if ((st = dalloc_t(n, &n->dcount, 4, "descriptor counters"))) return bail(st);
         CU(n, cudaMemset(n->dcount, 0, 16));
-    } else if (n->pad8 && !n->xbuf && !n->global_atomics) {
-        unsigned long long *tw = nullptr;
-        if ((st = dalloc_t(n, &tw, n->NT, "tile windows"))) return bail(st);
-        CU(n, cudaMemsetAsync(tw, 0, n->NT * 8ull, s));
-        tile_windows_kernel<<<n->n_sm * 8, 256, 0, s>>>(n->bnd, n->N, n->NT, tw);
-        std::vector<unsigned long long> h(n->NT);
-        CU(n, cudaMemcpyAsync(h.data(), tw, n->NT * 8ull, cudaMemcpyDeviceToHost, s));
-        CU(n, cudaStreamSynchronize(s));
-        dfree(n, tw);
-        n->device_bytes -= n->NT * 8ull;
-        uint64_t mx = 0;
-        for (unsigned long long x : h) mx = std::max<uint64_t>(mx, x);
-        if (mx >= 0xFFFFFFFFull) return bail(fail(n, SPICE_EINVAL, "%llu windows into one tile exceed the 32-bit list index", (unsigned long long)mx));
-        n->wstride = (mx + 3) & ~3ull;
-        if ((st = dalloc_t(n, &n->wl, std::max<uint64_t>(2ull * n->NT * n->wstride, 4), "window lists"))) return bail(st);
-        if ((st = dalloc_t(n, &n->wcount, 3ull * n->NT, "window counters"))) return bail(st);
-        CU(n, cudaMemset(n->wcount, 0, 3ull * n->NT * 4));
     }
-    if (n->G == 1 && n->model != SPICE_BRUNEL_PLUS && !n->desc && !n->wl && !n->xbuf)
-        n->fused = false;                                  // unpadded G = 1 (SPICE_NOPAD)
     if (n->C > 1 && !n->desc) n->fused = false;           // cluster tiles: descriptor path only
     if (n->G > 1 && !n->desc) n->fused = false;           // G > 1: fused only on the padded layout
     // ---- kernel arguments ----
@@ -787,18 +730,12 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.rank = n->rank; a.G = n->G; a.S = n->S; a.n_own = (uint32_t)n->n_own; a.W = n->W;
     a.TW = n->TW; a.NT = n->NT; a.C = n->C; a.TWs = n->TWs; a.ring_stride = n->ring_stride; a.record_steps = n->R;
     a.GS = pick_group_lanes(n->mean_seg);
-    if (const char *gs = getenv("SPICE_GROUP_LANES")) a.GS = (uint32_t)atoi(gs);
-    if (const char *dm = getenv("SPICE_DEBUG_MODE")) a.dbg = (uint32_t)atoi(dm);   // diagnostics only
-    a.dcap = n->dcap;
-    a.rstages = n->rstages;
-    if ((a.dbg & 32u) && n->desc &&
-        (st = dalloc_t(n, &a.dscratch, 2ull * n->NT * ((n->n_own + 1) & ~1ull), "descriptor scratch"))) return bail(st);
+    if (c->group_lanes) a.GS = c->group_lanes;
     if (getenv("SPICE_PHASES") && atoi(getenv("SPICE_PHASES"))) {     // diagnostics only
         if ((st = dalloc_t(n, &n->ptimes, (size_t)n->NT * n->C * 16, "phase clocks"))) return bail(st);
         CU(n, cudaMemset(n->ptimes, 0, (size_t)n->NT * n->C * 16 * 8));
         a.ptimes = n->ptimes;
     }
-    a.pf_rows = getenv("SPICE_PREFETCH_ROWS") ? (uint32_t)atoi(getenv("SPICE_PREFETCH_ROWS")) : 0u;   // measured: no gain
     a.key0 = (uint32_t)n->seed; a.key1 = (uint32_t)(n->seed >> 32);
     a.NR = n->NR; a.RS = n->RS;
     a.mc = n->mc;
@@ -806,8 +743,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.v = n->v; a.ge = n->ge; a.gi = n->gi; a.ref = n->ref; a.acc = n->acc; a.ring = n->ring;
     a.sl_ids = n->sl_ids; a.sl_rows = n->sl_rows; a.sl_counts = n->sl_counts; a.desc = n->desc;
     a.dstride = ((n->G == 1 ? n->n_own : (uint64_t)n->N) + 1) & ~1ull; a.dcount = n->dcount;
-    a.wl = n->wl; a.wstride = n->wstride; a.wcount = n->wcount;
-    a.xbuf = n->xbuf; a.xoff = n->xoff; a.xcnt = n->xcnt; a.xtotal = n->xtotal; a.xrows_bytes = kXRowsBytes; a.record = n->record; a.sendbuf = n->sendbuf;
+    a.record = n->record; a.sendbuf = n->sendbuf;
     a.gather = n->gather; a.fired_cta = n->fired_cta; a.delivered_cta = n->delivered_cta;
     a.t0 = n->t0; a.force_bits = n->force_bits; a.force_ctl = n->force_ctl;
     a.w = n->w; a.pring = n->pring; a.xtr = n->xtr; a.ytr = n->ytr;
@@ -815,10 +751,12 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.npl = pbx.n;
     memcpy(a.pl, pbx.box, sizeof a.pl);
     CU(n, prepare_kernels(a));
-    if (!n->external) {
-        if ((st = capture_graph(n, spice_net::kGraphSteps, &n->g_big))) return bail(st);
-        if ((st = capture_graph(n, 1, &n->g_one))) return bail(st);
-    }
+    // the caller's stream may still be running work of its own: everything the library
+    // enqueued on it so far (memsets, generator) is done; capture never touches it
+    CU(n, cudaStreamSynchronize(s));
+    if (!n->external)
+        for (uint32_t k = 0; k < spice_net::kGraphLevels; ++k)
+            if ((st = capture_graph(n, 1u << k, &n->graphs[k]))) return bail(st);
     n->create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_create).count();
     *out = n;
     return SPICE_OK;
@@ -834,14 +772,12 @@ spice_status spice_setup_times(spice_net *n, double *gen_ms, double *create_ms) 
 spice_status spice_step(spice_net *n, uint64_t steps) {
     CHECK_NET(n);
     if (n->external) return fail(n, SPICE_ESTATE, "external-exchange networks step via spice_exchange_begin/end");
-    while (steps >= spice_net::kGraphSteps) {
-        CU(n, cudaGraphLaunch(n->g_big, n->stream));
-        steps -= spice_net::kGraphSteps;
-        n->t_host += spice_net::kGraphSteps;
-    }
-    while (steps--) {
-        CU(n, cudaGraphLaunch(n->g_one, n->stream));
-        n->t_host += 1;
+    while (steps) {                                        // largest graph first
+        uint32_t k = spice_net::kGraphLevels - 1;
+        while ((1ull << k) > steps) --k;
+        CU(n, cudaGraphLaunch(n->graphs[k], n->stream));
+        steps -= 1ull << k;
+        n->t_host += 1ull << k;
     }
     return SPICE_OK;
 }
@@ -935,6 +871,69 @@ spice_status spice_read_spikes(spice_net *n, uint64_t t_begin, uint64_t t_end, u
     return SPICE_OK;
 }
 
+spice_status spice_spikes_prefetch(spice_net *n, uint64_t t_begin, uint64_t t_end, uint32_t slot) {
+    CHECK_NET(n);
+    if (slot > 1) return fail(n, SPICE_EINVAL, "slot must be 0 or 1");
+    if (t_begin > t_end || t_end > n->t_host || (n->t_host > n->R && t_begin < n->t_host - n->R) ||
+        t_end - t_begin > n->R)
+        return fail(n, SPICE_ERANGE, "steps [%llu, %llu) not in the record ring (have [%llu, %llu))",
+                    (unsigned long long)t_begin, (unsigned long long)t_end,
+                    (unsigned long long)(n->t_host > n->R ? n->t_host - n->R : 0), (unsigned long long)n->t_host);
+    spice_net::Slot &sl = n->slot[slot];
+    if (sl.full) CU(n, cudaEventSynchronize(sl.done));    // (an uncollected earlier copy)
+    const uint64_t words = (uint64_t)n->G * n->W, need = std::max<uint64_t>((t_end - t_begin) * words, 1);
+    if (sl.words < need) {
+        if (sl.h) cudaFreeHost(sl.h);
+        sl.h = nullptr;
+        sl.words = 0;
+        CU(n, cudaMallocHost(reinterpret_cast<void **>(&sl.h), need * 4));
+        sl.words = need;
+    }
+    if (!sl.done) CU(n, cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    // steps enqueued before this call are recorded by the time the copy runs (stream order);
+    // a run that wraps the ring needs one copy per contiguous run of slots
+    for (uint64_t t = t_begin; t < t_end;) {
+        const uint64_t rs = t % n->R;
+        const uint64_t run = std::min<uint64_t>(t_end - t, n->R - rs);
+        CU(n, cudaMemcpyAsync(sl.h + (t - t_begin) * words, n->record + rs * words, run * words * 4,
+                              cudaMemcpyDeviceToHost, n->stream));
+        t += run;
+    }
+    CU(n, cudaEventRecord(sl.done, n->stream));
+    sl.t_begin = t_begin;
+    sl.t_end = t_end;
+    sl.full = true;
+    return SPICE_OK;
+}
+
+spice_status spice_spikes_collect(spice_net *n, uint32_t slot, uint32_t *ids, uint64_t cap,
+                                  uint64_t *offsets, uint64_t *total) {
+    CHECK_NET(n);
+    if (slot > 1) return fail(n, SPICE_EINVAL, "slot must be 0 or 1");
+    spice_net::Slot &sl = n->slot[slot];
+    if (!sl.full) return fail(n, SPICE_ESTATE, "slot %u holds no prefetched steps", slot);
+    CU(n, cudaEventSynchronize(sl.done));
+    const uint64_t words = (uint64_t)n->G * n->W, nsteps = sl.t_end - sl.t_begin;
+    std::vector<std::vector<uint32_t>> &per = n->hdec;
+    per.resize(nsteps);
+    uint64_t tot = 0;
+    for (uint64_t q = 0; q < nsteps; ++q) {
+        decode_into(sl.h + q * words, n->G, n->W, n->S, per[q]);
+        tot += per[q].size();
+    }
+    if (total) *total = tot;
+    if (tot > cap || (!ids && tot)) return fail(n, SPICE_ETRUNC, "need %llu ids", (unsigned long long)tot);
+    uint64_t o = 0;
+    for (uint64_t q = 0; q < nsteps; ++q) {
+        if (offsets) offsets[q] = o;
+        if (!per[q].empty()) memcpy(ids + o, per[q].data(), per[q].size() * 4);
+        o += per[q].size();
+    }
+    if (offsets) offsets[nsteps] = o;
+    sl.full = false;
+    return SPICE_OK;
+}
+
 spice_status spice_read_connectivity(spice_net *n, uint32_t row_begin, uint32_t row_end, uint32_t *tgt,
                                      uint64_t cap, uint64_t *row_offsets, uint64_t *total) {
     CHECK_NET(n);
@@ -1016,6 +1015,14 @@ spice_status spice_write_state(spice_net *n, uint32_t field, const void *in, uin
     if (st) return st;
     if (count != n->n_own) return fail(n, SPICE_EINVAL, "n = %llu, owned = %llu", (unsigned long long)count, (unsigned long long)n->n_own);
     CU(n, cudaStreamSynchronize(n->stream));
+    if (field == SPICE_FIELD_XTR) {           // global pre traces of the current parity (mirrors read)
+        float *dst = n->xtr + (n->t_host & 1) * (uint64_t)n->N;
+        std::vector<float> x(n->N);
+        CU(n, cudaMemcpy(x.data(), dst, n->N * 4ull, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < count; ++i) x[local_to_global(i, n->rank, n->G, n->S)] = ((const float *)in)[i];
+        CU(n, cudaMemcpy(dst, x.data(), n->N * 4ull, cudaMemcpyHostToDevice));
+        return SPICE_OK;
+    }
     if (count) CU(n, cudaMemcpy(p, in, count * 4, cudaMemcpyHostToDevice));
     return SPICE_OK;
 }
@@ -1244,11 +1251,20 @@ spice_status spice_debug_phases(spice_net *n, uint64_t *out, uint64_t cap, uint6
 
 uint64_t spice_launches(spice_net *n, uint64_t steps) {
     if (!n) return 0;
-    const uint64_t chunks = steps / spice_net::kGraphSteps, rest = steps % spice_net::kGraphSteps;
-    if (n->small) return 2 * chunks + 2 * rest;            // k_small + k_advance per graph replay
-    const uint64_t per = spice_kernels_per_step(n);
-    // + one k_advance per replay; the fused sequences open with an update (G = 1 and G > 1)
-    return per * steps + chunks + rest + (n->fused && !n->global_atomics ? chunks + rest : 0);
+    uint64_t total = 0;
+    while (steps) {                                        // the decomposition spice_step uses
+        uint32_t k = spice_net::kGraphLevels - 1;
+        while ((1ull << k) > steps) --k;
+        const uint64_t m = 1ull << k;
+        if (n->small) total += 2;                          // k_small + k_advance per replay
+        else {
+            // + one k_advance per replay; the fused sequences open with an update (G = 1 and
+            // G > 1) and close with a plain delivery
+            total += spice_kernels_per_step(n) * m + 1 + (n->fused && !n->global_atomics ? 1 : 0);
+        }
+        steps -= m;
+    }
+    return total;
 }
 
 uint32_t spice_kernels_per_step(spice_net *n) {

@@ -458,10 +458,9 @@ __global__ void u32_to_u64(const uint32_t *in, uint64_t n, uint64_t *out) {
         out[i] = in[i];
 }
 
-cudaError_t gen_plastic(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
-                        const uint32_t *bnd, const uint16_t *ent, float *w, float w0,
-                        uint32_t *tmp_cnt, uint64_t *in_ptr, uint64_t **in_pos, uint32_t **in_src,
-                        uint64_t *n_plastic, cudaStream_t s) {
+cudaError_t gen_plastic_count(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
+                              const uint32_t *bnd, const uint16_t *ent, float *w, float w0,
+                              uint32_t *tmp_cnt, uint64_t *in_ptr, uint64_t *n_plastic, cudaStream_t s) {
     cudaError_t e;
     const uint64_t pairs = (uint64_t)g.N * g.NT;
     if ((e = cudaMemsetAsync(tmp_cnt, 0, (size_t)g.n_own * 4, s))) return e;
@@ -470,11 +469,16 @@ cudaError_t gen_plastic(const GenGeom &g, const PlasticBoxes &pb, const uint64_t
     if ((e = cudaGetLastError())) return e;
     if ((e = gen_scan_u64(in_ptr, g.n_own, s))) return e;
     if ((e = cudaMemcpyAsync(n_plastic, in_ptr + g.n_own, 8, cudaMemcpyDeviceToHost, s))) return e;
-    if ((e = cudaStreamSynchronize(s))) return e;
-    if ((e = cudaMalloc(in_pos, (*n_plastic ? *n_plastic : 1) * 8))) return e;
-    if ((e = cudaMalloc(in_src, (*n_plastic ? *n_plastic : 1) * 4))) return e;
+    return cudaStreamSynchronize(s);
+}
+
+cudaError_t gen_plastic_fill(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
+                             const uint32_t *bnd, const uint16_t *ent, uint32_t *tmp_cnt,
+                             const uint64_t *in_ptr, uint64_t *in_pos, uint32_t *in_src, cudaStream_t s) {
+    cudaError_t e;
+    const uint64_t pairs = (uint64_t)g.N * g.NT;
     if ((e = cudaMemsetAsync(tmp_cnt, 0, (size_t)g.n_own * 4, s))) return e;
-    plastic_kernel<1><<<grid_for(pairs, 8), 256, 0, s>>>(g, pb, row_ptr, bnd, ent, w, w0, tmp_cnt, in_ptr, *in_pos, *in_src);
+    plastic_kernel<1><<<grid_for(pairs, 8), 256, 0, s>>>(g, pb, row_ptr, bnd, ent, nullptr, 0.0f, tmp_cnt, in_ptr, in_pos, in_src);
     return cudaGetLastError();
 }
 

@@ -67,15 +67,8 @@ __device__ __forceinline__ uint64_t mod32(uint64_t t, uint32_t m) {
 
 __device__ __forceinline__ uint4 ld_stream_v4(const uint16_t *p) {
     uint4 v;
-#if SPICE_L2_EVICT_FIRST
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
-#else
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-#endif
     return v;
 }
 
@@ -251,249 +244,7 @@ __device__ __forceinline__ uint32_t region_of(const uint32_t *pref, uint32_t nr,
     return lo;
 }
 
-// Entries [lo, hi) of an 8-entry window are valid (lo, hi clamped to 0..8): one bitmask,
-// then predicated shared-memory atomics (no per-entry 64-bit compares or branches).
-__device__ __forceinline__ uint32_t window_mask(int lo, int hi) {
-    lo = max(lo, 0);
-    hi = min(hi, 8);
-    return hi > lo ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
-}
-// Predicated shared-memory reductions of one 8-entry window in a single asm block:
-// per slot one predicate test (bit u of m) and one predicated red.shared.add.u32.
-// cnt_s: shared-window address of the tile counters; entry e adds q to counter e.
-__device__ __forceinline__ void accumulate_masked(uint32_t cnt_s, const uint4 v, uint32_t m, uint32_t q) {
-    const uint32_t a0 = cnt_s + ((v.x & 0xFFFFu) << 2), a1 = cnt_s + ((v.x >> 14) & ~3u);
-    const uint32_t a2 = cnt_s + ((v.y & 0xFFFFu) << 2), a3 = cnt_s + ((v.y >> 14) & ~3u);
-    const uint32_t a4 = cnt_s + ((v.z & 0xFFFFu) << 2), a5 = cnt_s + ((v.z >> 14) & ~3u);
-    const uint32_t a6 = cnt_s + ((v.w & 0xFFFFu) << 2), a7 = cnt_s + ((v.w >> 14) & ~3u);
-    asm volatile(
-        "{\n\t.reg .pred p<8>;\n\t.reg .b32 t;\n\t"
-        "and.b32 t, %9, 1;   setp.ne.u32 p0, t, 0;\n\t"
-        "and.b32 t, %9, 2;   setp.ne.u32 p1, t, 0;\n\t"
-        "and.b32 t, %9, 4;   setp.ne.u32 p2, t, 0;\n\t"
-        "and.b32 t, %9, 8;   setp.ne.u32 p3, t, 0;\n\t"
-        "and.b32 t, %9, 16;  setp.ne.u32 p4, t, 0;\n\t"
-        "and.b32 t, %9, 32;  setp.ne.u32 p5, t, 0;\n\t"
-        "and.b32 t, %9, 64;  setp.ne.u32 p6, t, 0;\n\t"
-        "and.b32 t, %9, 128; setp.ne.u32 p7, t, 0;\n\t"
-        "@p0 red.shared.add.u32 [%0], %8;\n\t"
-        "@p1 red.shared.add.u32 [%1], %8;\n\t"
-        "@p2 red.shared.add.u32 [%2], %8;\n\t"
-        "@p3 red.shared.add.u32 [%3], %8;\n\t"
-        "@p4 red.shared.add.u32 [%4], %8;\n\t"
-        "@p5 red.shared.add.u32 [%5], %8;\n\t"
-        "@p6 red.shared.add.u32 [%6], %8;\n\t"
-        "@p7 red.shared.add.u32 [%7], %8;\n\t}"
-        :: "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7), "r"(q), "r"(m)
-        : "memory");
-}
-
-__device__ __forceinline__ void accumulate8(uint32_t *cnt, const uint4 v, uint64_t w, uint64_t st,
-                                            uint64_t en, uint32_t q) {
-    const uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
-                           v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-        if (w + u >= st && w + u < en) atomicAdd(&cnt[e[u]], q);
-}
-
-// Deliver the spikes of step t with index p = c, c+C, ... into tile b's counters.
-// Every group of GS lanes walks its own segments with no block-wide barrier; each group
-// keeps U segments in flight (descriptor loads, then window loads, then the shared-memory
-// atomics) so that enough loads are outstanding per SM.  Returns this thread's share of
-// the delivered-event count.
-// ------------------------------------------------------------- tile-pair exchange (G = 1)
-// Delivery with every global access contiguous.  Producer (CTA g, right after it updated
-// source tile g): the rows of its spiking neurons are loaded whole into shared memory with
-// TMA bulk copies (one cp.async.bulk per row, completion on an mbarrier); for every target
-// tile bt the segments of those rows (the pivot split of PAPER.md:273-275) are written
-// back-to-back into chunk (bt, g, receptor).  Consumer (CTA bt, next launch): its chunks
-// are read with 16-byte coalesced loads and accumulated with shared-memory atomics.
-// Chunk capacities are the exact static synapse counts, so they never overflow.
-struct XSmem {
-    uint16_t *rows;      // [kXRowsBytes / 2] staged rows (16-byte aligned)
-    uint32_t *bstage;    // [32 * (NT+1)] segment bounds of the batch's rows
-    uint32_t *off;       // [2 * NT] running chunk offsets
-    uint32_t *binfo;     // [32 * 4]: source, row start lo, row start hi, staged offset (entries)
-    uint32_t *misc;      // [4]: batch size
-    unsigned long long *mbar;
-};
-
-__host__ __device__ inline size_t xchg_smem_bytes(uint32_t NT) {
-    return (size_t)kXRowsBytes + (size_t)32 * (NT + 1) * 4 + (size_t)2 * NT * 4 + 32 * 16 + 16 + 16;
-}
-
-__device__ __forceinline__ XSmem carve_x(const SimArgs &a, uint32_t *smem) {
-    XSmem x;
-    x.rows = reinterpret_cast<uint16_t *>(smem);
-    uint32_t *p = smem + kXRowsBytes / 4;
-    x.bstage = p; p += 32 * (a.NT + 1);
-    x.off = p; p += 2 * a.NT;
-    x.binfo = p; p += 32 * 4;
-    x.misc = p; p += 4;
-    p = reinterpret_cast<uint32_t *>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
-    x.mbar = reinterpret_cast<unsigned long long *>(p);
-    return x;
-}
-
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long *m) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(m)) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(unsigned long long *m, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(m)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *m, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done)
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                     : "=r"(done) : "r"(smem_u32(m)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, unsigned long long *m) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
-}
-
-// Producer: spikes ids[0..n) (global IDs, row starts rows[]) of source tile g, parity pw.
-__device__ __forceinline__ void exchange_produce(const SimArgs &a, uint32_t pw, uint32_t g, const uint32_t *ids,
-                                 const uint64_t *rows, uint32_t n, XSmem x, uint32_t &phase) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t NT = a.NT, rl = NT + 1u;
-    for (uint32_t i = tid; i < 2 * NT; i += kBlock) x.off[i] = 0u;
-    if (tid == 0) mbar_init(x.mbar);
-    uint16_t *xb = a.xbuf + (uint64_t)pw * a.xtotal;
-    for (uint32_t q0 = 0; q0 < n; ) {
-        __syncthreads();                                  // previous batch fully consumed
-        if (warp == 0) {                                  // form the batch: rows that fit the stage
-            const uint32_t q = q0 + lane;
-            uint32_t s = 0, bytes = 0;
-            uint64_t rs = 0, al = 0;
-            if (q < n) {
-                s = ids[q];
-                rs = rows[q];
-                const uint32_t len = a.bnd[(uint64_t)s * rl + NT];
-                al = rs & ~7ull;
-                bytes = (uint32_t)(((rs + len + 7) & ~7ull) - al) * 2u;
-            }
-            const uint32_t incl = warp_incl_scan(bytes);
-            const bool fits = q < n && (incl <= a.xrows_bytes || lane == 0);
-            const uint32_t nb = __popc(__ballot_sync(0xFFFFFFFFu, fits));
-            if (fits) {
-                x.binfo[lane * 4 + 0] = s;
-                x.binfo[lane * 4 + 1] = (uint32_t)rs;
-                x.binfo[lane * 4 + 2] = (uint32_t)(rs >> 32);
-                x.binfo[lane * 4 + 3] = (incl - bytes) / 2u + (uint32_t)(rs - al);   // staged row start (entries)
-            }
-            const uint32_t tot_bytes = __shfl_sync(0xFFFFFFFFu, incl, nb - 1);
-            if (lane == 0) {
-                x.misc[0] = nb;
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive_tx(x.mbar, tot_bytes);
-            }
-            __syncwarp();
-            if (fits && bytes)
-                tma_load_1d(x.rows + (incl - bytes) / 2u, a.ent + al, bytes, x.mbar);
-        }
-        __syncthreads();
-        const uint32_t nb = x.misc[0];
-        // segment bounds of the batch rows (coalesced, one warp per row)
-        for (uint32_t q = warp; q < nb; q += kBlock / 32) {
-            const uint32_t *src = a.bnd + (uint64_t)x.binfo[q * 4] * rl;
-            for (uint32_t bt = lane; bt < rl; bt += 32) x.bstage[q * rl + bt] = src[bt];
-        }
-        __syncthreads();
-        mbar_wait(x.mbar, phase);
-        phase ^= 1u;
-        // one warp per target tile: positions of the nb segments, then copy them back-to-back
-        for (uint32_t bt = warp; bt < NT; bt += kBlock / 32) {
-            uint32_t len = 0, rcp = 0, srcoff = 0;
-            if (lane < nb) {
-                const uint32_t lo = x.bstage[lane * rl + bt];
-                len = x.bstage[lane * rl + bt + 1] - lo;
-                rcp = x.binfo[lane * 4] >= a.n_exc ? 1u : 0u;
-                srcoff = x.binfo[lane * 4 + 3] + lo;
-            }
-            const uint32_t l0 = rcp ? 0u : len, l1 = rcp ? len : 0u;
-            const uint32_t i0 = warp_incl_scan(l0), i1 = warp_incl_scan(l1);
-            const uint32_t pos = rcp ? x.off[bt * 2 + 1] + i1 - l1 : x.off[bt * 2] + i0 - l0;
-            const uint64_t ch0 = a.xoff[((uint64_t)bt * NT + g) * 2];
-            const uint64_t ch1 = a.xoff[((uint64_t)bt * NT + g) * 2 + 1];
-            for (uint32_t q = 0; q < nb; ++q) {
-                const uint32_t lq = __shfl_sync(0xFFFFFFFFu, len, q);
-                const uint32_t pq = __shfl_sync(0xFFFFFFFFu, pos, q);
-                const uint32_t sq = __shfl_sync(0xFFFFFFFFu, srcoff, q);
-                const uint32_t rq = __shfl_sync(0xFFFFFFFFu, rcp, q);
-                uint16_t *dst = xb + (rq ? ch1 : ch0) + pq;
-                for (uint32_t e = lane; e < lq; e += 32) dst[e] = x.rows[sq + e];
-            }
-            if (lane == 31) { x.off[bt * 2] += i0; x.off[bt * 2 + 1] += i1; }
-        }
-        q0 += nb;
-    }
-    __syncthreads();
-    uint32_t *xc = a.xcnt + (uint64_t)pw * NT * NT * 2;
-    for (uint32_t i = tid; i < 2 * NT; i += kBlock) {
-        const uint32_t bt = i >> 1, r = i & 1;
-        xc[((uint64_t)bt * NT + g) * 2 + r] = x.off[i];
-    }
-}
-
-// Consumer: accumulate every chunk (bt, g, r) of parity par into the tile counters.
-__device__ __forceinline__ uint32_t exchange_consume(const SimArgs &a, uint32_t par, uint32_t bt, uint32_t *cnt) {
-    constexpr int U = 4;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t NT = a.NT;
-    const uint32_t cnt_s = smem_u32(cnt);
-    const uint16_t *xb = a.xbuf + (uint64_t)par * a.xtotal;
-    const uint32_t *xc = a.xcnt + (uint64_t)par * NT * NT * 2;
-    uint32_t delivered = 0;
-    for (uint32_t k = warp; k < 2 * NT; k += kBlock / 32) {          // k = r * NT + g
-        const uint32_t r = k / NT, g = k - r * NT;
-        const uint64_t ci = ((uint64_t)bt * NT + g) * 2 + r;
-        const uint32_t n = xc[ci];
-        if (!n) continue;
-        const uint16_t *base = xb + a.xoff[ci];
-        const uint32_t q = r ? 65536u : 1u;
-        if (lane == 0) delivered += n;
-        for (uint32_t i0 = 0; i0 < n; i0 += 256u * U) {
-            uint4 v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t i = i0 + 256u * u + 8u * lane;
-                v[u] = i < n ? ld_stream_v4(base + i) : make_uint4(0, 0, 0, 0);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t i = i0 + 256u * u + 8u * lane;
-                if (i < n) accumulate_masked(cnt_s, v[u], window_mask(0, (int)(n - i)), q);
-            }
-        }
-    }
-    __syncthreads();
-    return delivered;
-}
-
-// Capacities: cap[(bt*NT + g)*2 + r] = synapses from source tile g (receptor r) into tile bt.
-__global__ void __launch_bounds__(kBlock) k_xcap(SimArgs a, uint32_t *cap) {
-    extern __shared__ uint32_t e[];
-    const uint32_t g = blockIdx.x, NT = a.NT, rl = NT + 1u;
-    for (uint32_t i = threadIdx.x; i < 2 * NT; i += kBlock) e[i] = 0u;
-    __syncthreads();
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t s0 = g * a.TW, s1 = min(a.N, s0 + a.TW);
-    for (uint32_t s = s0 + warp; s < s1; s += kBlock / 32) {
-        const uint32_t r = s >= a.n_exc ? 1u : 0u;
-        const uint32_t *row = a.bnd + (uint64_t)s * rl;
-        for (uint32_t bt = lane; bt < NT; bt += 32) {
-            const uint32_t len = row[bt + 1] - row[bt];
-            if (len) atomicAdd(&e[bt * 2 + r], len);
-        }
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < 2 * NT; i += kBlock) cap[((uint64_t)(i >> 1) * NT + g) * 2 + (i & 1)] = e[i];
-}
 
 constexpr uint32_t kRing = 512;                        // ring entries per warp (power of 2)
 // spike IDs of the update kept in shared memory for the descriptor pass: the words of the
@@ -577,80 +328,6 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
     return dsum;                                       // valid in warp 0
 }
 
-// Window lists (G = 1, padded layout; the default delivery path).  For every destination
-// tile bb the step's spikes contribute one u32 per 16-byte window of their segment:
-// wl[(par*NT + bb)*wstride + i] = window index (bits 0-30) | inh (bit 31).  This CTA's n
-// spikes: one pass loads their bnd rows, row starts and out-degrees (cp.async, all in
-// flight at once); per tile a warp sums the windows, one thread per tile reserves a range
-// of the tile's list with an atomic on wcount[t % 3][bb] (all tiles at once), then every
-// warp writes its tiles' windows (lane = spike, exclusive scan of the window counts).
-__device__ __forceinline__ uint64_t write_windows(const SimArgs &a, uint64_t t, uint32_t b, uint32_t n,
-                                  const uint32_t *region, uint64_t *region_rows, uint32_t *stage,
-                                  bool marks = false) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t par = (uint32_t)(t & 1);
-    const uint32_t rowlen = a.NT + 1u;
-    const uint32_t CH = max(1u, ((uint32_t)kStageWords - 2u * a.NT - 2u) / (rowlen + 3u));
-    uint64_t *srow = reinterpret_cast<uint64_t *>(stage + CH * rowlen + (CH * rowlen & 1u));
-    uint32_t *sdeg = reinterpret_cast<uint32_t *>(srow + CH);
-    uint32_t *stot = sdeg + CH;                        // [NT] windows per tile, then offsets
-    uint32_t *wc = a.wcount + (t % 3) * a.NT;
-    uint64_t dsum = 0;
-    for (uint32_t q0 = 0; q0 < n; q0 += CH) {
-        const uint32_t nq = min(CH, n - q0);
-        __syncthreads();
-        for (uint32_t ql = warp; ql < nq; ql += kBlock / 32) {            // one warp per spike row
-            const uint32_t s = region[q0 + ql];
-            const uint32_t *row = a.bnd + (uint64_t)s * rowlen;
-            for (uint32_t bb = lane; bb < rowlen; bb += 32)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(stage + ql * rowlen + bb)), "l"(row + bb) : "memory");
-            if (lane == 0) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(srow + ql)), "l"(a.row_ptr + s) : "memory");
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(sdeg + ql)), "l"(a.deg + s) : "memory");
-            }
-        }
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
-        if (marks) phase_mark(a, 10);
-        if (warp == 0)
-            for (uint32_t ql = lane; ql < nq; ql += 32) { region_rows[q0 + ql] = srow[ql]; dsum += sdeg[ql]; }
-        for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {           // windows per tile
-            uint32_t w = 0;
-            for (uint32_t ql = lane; ql < nq; ql += 32) w += (stage[ql * rowlen + bb + 1] - stage[ql * rowlen + bb]) >> 3;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xFFFFFFFFu, w, o);
-            if (lane == 0) stot[bb] = w;
-        }
-        __syncthreads();
-        for (uint32_t bb = threadIdx.x; bb < a.NT; bb += kBlock)            // reserve (one round trip)
-            stot[bb] = stot[bb] ? atomicAdd(wc + bb, stot[bb]) : 0u;
-        __syncthreads();
-        if (marks) phase_mark(a, 11);
-        for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
-            uint32_t *dst = a.wl + ((uint64_t)par * a.NT + bb) * a.wstride + stot[bb];
-            uint32_t carry = 0;
-            for (uint32_t j0 = 0; j0 < nq; j0 += 32) {
-                const uint32_t ql = j0 + lane;
-                uint32_t nw = 0, w0 = 0, inh = 0;
-                if (ql < nq) {                           // padded: rs, lo, hi are multiples of 8
-                    const uint32_t lo = stage[ql * rowlen + bb], hi = stage[ql * rowlen + bb + 1];
-                    nw = (hi - lo) >> 3;
-                    w0 = (uint32_t)((srow[ql] + lo) >> 3);
-                    inh = region[q0 + ql] >= a.n_exc ? 0x80000000u : 0u;
-                }
-                const uint32_t incl = warp_incl_scan(nw);
-                const uint32_t pos = carry + incl - nw;
-                for (uint32_t k = 0; k < nw; ++k) dst[pos + k] = (w0 + k) | inh;
-                carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xFFFFFFFFu, dsum, o);
-    __syncthreads();
-    return dsum;                                       // valid in warp 0
-}
-
 // Update the owned neurons [lo, lo + width) for step t (a tile, or one CTA's slice of a
 // cluster tile); b is the CTA's spike-list region / counter slot.
 // cl_c < kMaxCluster: cnt is this CTA's slice of a cluster tile whose C = a.C CTAs each hold
@@ -661,7 +338,7 @@ __device__ __forceinline__ uint64_t write_windows(const SimArgs &a, uint64_t t, 
 template <int MODEL, bool DESC = false>
 __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                             const uint32_t *cnt, bool write_list, uint32_t *s_count, uint32_t *stage,
-                            uint32_t *xsm = nullptr, const StatePtrs *staged = nullptr, bool marks = false,
+                            const StatePtrs *staged = nullptr, bool marks = false,
                             uint32_t cl_c = kMaxCluster, uint32_t *sid_s = nullptr, uint32_t *bm_s = nullptr) {
     const StatePtrs sp = staged ? *staged : global_state(a);
     const uint32_t tid = threadIdx.x, lane = tid & 31;
@@ -784,7 +461,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
         if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
         if (n_tile) atomicAdd(&a.fired_cta[b], (unsigned long long)n_tile);   // RED: no load on the path
     }
-    if (!DESC && write_list && !a.desc && !a.wl) {        // row starts of the spikes, all at once
+    if (!DESC && write_list && !a.desc) {        // row starts of the spikes, all at once
         uint32_t dsum = 0;                                // (the descriptor pass loads them itself)
         for (uint32_t q = tid; q < n_tile; q += kBlock) {
             const uint32_t s = region[q];
@@ -799,98 +476,13 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
         __syncthreads();
     }
     if (marks) phase_mark(a, 8);
-    if (!DESC && write_list && (a.dbg & 8u) == 0 && a.pf_rows) {
-        // TMA L2 prefetch of every spiking row (contiguous, ~rowlen * 2 bytes): the next
-        // launch's delivery reads these rows as scattered 16-byte windows from ~all CTAs;
-        // pulling each row into L2 with one bulk request turns those into L2 hits.
-        for (uint32_t q = tid; q < n_tile; q += kBlock) {
-            const uint32_t s = region[q];
-            const uint64_t rs = region_rows[q];
-            const uint64_t re = a.row_ptr[s + 1];
-            const uint64_t lo = rs & ~7ull, hi = (re + 7) & ~7ull;
-            if (hi > lo)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a.ent + lo), "r"((uint32_t)(hi - lo) * 2u) : "memory");
-        }
-    }
-    if (DESC) {
-        if (write_list && !(a.dbg & 4u)) {
-            const uint64_t dsum = write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
-            if (tid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
-        }
-    } else if (write_list && (a.desc || a.wl) && !(a.dbg & 4u)) {   // padded layout: delivered events
-        const uint64_t dsum = a.wl ? write_windows(a, t, b, n_tile, region, region_rows, stage, marks)
-                                   : write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
-        if (tid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);   // (out-degrees)
+    if (write_list && (DESC || a.desc)) {                 // padded layout: delivered events (out-degrees)
+        const uint64_t dsum = write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
+        if (tid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
     }
     if (marks) phase_mark(a, 9);
-    if constexpr (MODEL != 3 && !DESC) {
-        if (write_list && a.xbuf) {
-            uint32_t phase = 0;
-            exchange_produce(a, par, b, region, region_rows, n_tile, carve_x(a, xsm), phase);
-        }
-    }
     __syncthreads();
     if (tid == 0) *s_count = 0;
-}
-
-template <int GS>
-__device__ __forceinline__ uint32_t deliver_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c, DeliverSmem sm) {
-    constexpr int U = 4;
-    const uint32_t tid = threadIdx.x;
-    const uint32_t par = (uint32_t)(t & 1);
-    for (uint32_t r = tid; r < a.NR; r += kBlock) sm.pref[r] = a.sl_counts[par * a.NR + r];
-    __syncthreads();
-    block_exclusive_scan(sm.pref, a.NR, sm.tmp);
-    const uint32_t n_sp = sm.pref[a.NR];
-    const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
-    const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
-    uint32_t delivered = 0;
-    const uint32_t grp = tid / GS, lig = tid % GS;
-    constexpr uint32_t ngrp = kBlock / GS;
-    for (uint32_t q0 = grp; q0 < my; q0 += ngrp * U) {
-        uint32_t s[U];
-        uint64_t rs[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t q = q0 + u * ngrp;
-            s[u] = 0xFFFFFFFFu;
-            rs[u] = 0;
-            if (q < my) {
-                const uint32_t p = c + q * a.C;
-                const uint32_t r = region_of(sm.pref, a.NR, p);
-                const uint64_t slot = lbase + (uint64_t)r * a.RS + (p - sm.pref[r]);
-                s[u] = a.sl_ids[slot];
-                rs[u] = a.sl_rows[slot];
-            }
-        }
-        uint64_t st[U], en[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            st[u] = en[u] = 0;
-            if (s[u] != 0xFFFFFFFFu) {
-                const uint32_t *bp = a.bnd + (uint64_t)s[u] * (a.NT + 1u) + b;
-                st[u] = rs[u] + bp[0];
-                en[u] = rs[u] + bp[1];
-            }
-        }
-        uint4 v[U];
-        uint64_t w[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            w[u] = (st[u] & ~7ull) + 8u * lig;
-            v[u] = w[u] < en[u] ? ld_stream_v4(a.ent + w[u]) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t qv = s[u] >= a.n_exc ? 65536u : 1u;
-            if (lig == 0) delivered += (uint32_t)(en[u] - st[u]);
-            if (w[u] < en[u]) accumulate8(sm.cnt, v[u], w[u], st[u], en[u], qv);
-            for (uint64_t x = w[u] + 8u * GS; x < en[u]; x += 8u * GS)
-                accumulate8(sm.cnt, ld_stream_v4(a.ent + x), x, st[u], en[u], qv);
-        }
-    }
-    __syncthreads();
-    return delivered;
 }
 
 // Eight unconditional shared-memory reductions of one padded 16-byte window (sentinel
@@ -932,7 +524,6 @@ __device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v,
 // the ring 64 entries per iteration with lane L taking entries L and L + 32 (consecutive
 // windows of a segment sit in one load instruction and coalesce into one L1 line lookup),
 // the next iteration's two window loads in flight while the current windows are reduced.
-constexpr uint32_t kRingS = 256;                       // deliver_tile_rs: ring entries per warp
 template <bool WORD>
 __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
                                                   uint32_t *cnt, uint32_t *ring_base, bool marks = false,
@@ -992,10 +583,8 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
     };
     auto entry = [&](uint32_t x) -> uint32_t { return x < tail ? ring[x & (kRing - 1)] : NONE; };
     auto load_win = [&](uint32_t e) -> uint4 {
-        if (e == NONE || (a.dbg & 2u)) return make_uint4(0, 0, 0, 0);
-        uint32_t wx = e & 0x7FFFFFFFu;
-        if (a.dbg & 16u) wx &= 0x3FFFFu;                       // diagnostics: L2-resident
-        return ld_stream_v4(a.ent + 8ull * wx);
+        if (e == NONE) return make_uint4(0, 0, 0, 0);
+        return ld_stream_v4(a.ent + 8ull * (e & 0x7FFFFFFFu));
     };
     constexpr uint32_t RW = SPICE_RW;                  // windows per lane per iteration
     fill(32u * RW);
@@ -1012,184 +601,11 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
 #pragma unroll
         for (uint32_t r = 0; r < RW; ++r) { x[r] = entry(head + 32u * r + lane); nv[r] = load_win(x[r]); }
         head = min(head + 32u * RW, tail);
-        if (!(a.dbg & 3u)) {
 #pragma unroll
-            for (uint32_t r = 0; r < RW; ++r)
-                if (e[r] != NONE) accumulate_window<WORD>(cnt_s, v[r], (e[r] >> 31) ? 65536u : 1u);
-        }
+        for (uint32_t r = 0; r < RW; ++r)
+            if (e[r] != NONE) accumulate_window<WORD>(cnt_s, v[r], (e[r] >> 31) ? 65536u : 1u);
 #pragma unroll
         for (uint32_t r = 0; r < RW; ++r) { e[r] = x[r]; v[r] = nv[r]; }
-    }
-    if (marks) phase_mark(a, 4);
-    __syncthreads();
-    if (marks) phase_mark(a, 5);
-}
-
-// Staged ring delivery (G = 1, padded layout; default).  The descriptor expansion of
-// deliver_tile_ring (per-warp ring of window entries), but the windows are copied with
-// 16-byte cp.async into S per-warp shared-memory stages of 32 windows (one per lane) and
-// reduced S - 1 stages later: S x 32 windows per warp in flight instead of 64, so a warp's
-// share of the step (~500 windows at synth 3e9) takes ~2 memory round trips, not ~8.
-// Each lane reads back only the slot its own cp.async wrote (wait_group suffices).
-template <bool WORD, int S>
-__device__ __forceinline__ void deliver_tile_rs(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
-                                                uint32_t *cnt, uint32_t *big, bool marks = false) {
-    constexpr uint32_t NW = kBlock / 32;
-    constexpr uint32_t NONE = 0xFFFFFFFFu;
-    constexpr uint32_t FULL = 0xFFFFFFFFu;
-    static_assert(S >= 2 && S <= 16, "stage count");
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t par = (uint32_t)(t & 1);
-    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
-    __shared__ uint32_t s_total;
-    if (tid == 0) {
-        s_total = a.dcount[t % 3];
-        if (b == 0 && c == 0) a.dcount[(t + 2) % 3] = 0u;     // next user: step t + 2's producers
-    }
-    __syncthreads();
-    if (marks) phase_mark(a, 2);
-    const uint32_t n_sp = s_total;
-    const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
-    const uint32_t v0 = (uint32_t)((uint64_t)my * warp / NW), v1 = (uint32_t)((uint64_t)my * (warp + 1) / NW);
-    const uint64_t *dlist = a.desc + ((uint64_t)par * a.NT + b) * a.dstride + c;   // visit v -> dlist[v * C]
-    const uint4 *ent4 = reinterpret_cast<const uint4 *>(a.ent);
-    uint32_t *ring = big + warp * kRingS;
-    const uint32_t stg_s = (uint32_t)__cvta_generic_to_shared(big + NW * kRingS) + warp * (S * 32u * 16u) + lane * 16u;
-    auto dload = [&](uint32_t vb) -> uint64_t {
-        const uint32_t v = vb + lane;
-        return v < v1 ? dlist[(uint64_t)v * a.C] : 0ull;
-    };
-    if (marks) phase_mark(a, 3);
-    uint32_t gnext = v0;
-    uint64_t dn = dload(v0);
-    uint32_t w0 = 0, nw = 0, inh = 0, pre = 0, T = 0, c0 = 0;   // current group, c0 = expanded
-    uint32_t head = 0, tail = 0;                                // ring cursors (warp-uniform)
-    auto fill = [&](uint32_t want) {                            // expand until >= want queued
-        while (tail - head < want) {
-            if (c0 >= T) {
-                if (gnext >= v1) break;
-                const uint64_t d = dn;
-                gnext += 32;
-                dn = dload(gnext);
-                nw = (uint32_t)(d >> 32) & 0x7FFFFFFFu;
-                w0 = (uint32_t)d;
-                inh = (uint32_t)(d >> 63) << 31;
-                const uint32_t incl = warp_incl_scan(nw);
-                pre = incl - nw;
-                T = __shfl_sync(FULL, incl, 31);
-                c0 = 0;
-                continue;
-            }
-            const uint32_t take = min(T - c0, kRingS - (tail - head));
-            const uint32_t klo = c0 > pre ? c0 - pre : 0u;
-            const uint32_t khi = min(pre + nw, c0 + take);
-            for (uint32_t k = klo; pre + k < khi; ++k)
-                ring[(tail + pre + k - c0) & (kRingS - 1)] = (w0 + k) | inh;
-            tail += take;
-            c0 += take;
-        }
-        __syncwarp();
-    };
-    uint32_t qbits = 0;            // bit s: stage s holds a window of this lane; bit 16 + s: inh
-    uint32_t live = 0;             // warp-uniform: stages holding a round
-    bool exhausted = false;        // warp-uniform: nothing left to issue
-    auto issue = [&](int s) {
-        fill(32);
-        exhausted = head == tail;
-        const uint32_t x = head + lane;
-        const uint32_t e = x < tail ? ring[x & (kRingS - 1)] : NONE;
-        head = min(head + 32, tail);
-        qbits &= ~((1u << s) | (1u << (16 + s)));
-        if (e != NONE) {
-            if (!(a.dbg & 2u))
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
-                             :: "r"(stg_s + (uint32_t)s * 512u), "l"(ent4 + (e & 0x7FFFFFFFu)) : "memory");
-            qbits |= (1u << s) | ((e >> 31) << (16 + s));
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        if (!exhausted) live |= 1u << s;
-    };
-    auto process = [&](int s) {
-        asm volatile("cp.async.wait_group %0;" :: "n"(S - 1) : "memory");
-        if (((qbits >> s) & 1u) && !(a.dbg & 3u)) {
-            uint4 v;
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(stg_s + (uint32_t)s * 512u));
-            accumulate_window<WORD>(cnt_s, v, ((qbits >> (16 + s)) & 1u) ? 65536u : 1u);
-        }
-        live &= ~(1u << s);
-    };
-#pragma unroll
-    for (int s = 0; s < S - 1; ++s) issue(s);
-    bool fin = false;
-    while (!fin) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            issue((s + S - 1) % S);
-            process(s);
-            if (exhausted && live == 0) { fin = true; break; }
-        }
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if (marks) phase_mark(a, 4);
-    __syncthreads();
-    if (marks) phase_mark(a, 5);
-}
-
-// Window-list delivery (G = 1, padded layout; default).  The tile's list of step t holds
-// wcount[t % 3][b] windows; the CTA's share is cut into super-rounds of 64 windows, split
-// evenly over its warps.  Per super-round a lane takes windows x = lane and x = 32 + lane:
-// two coalesced list-entry loads, two 16-byte window loads, sixteen red.shared.add.
-// Software pipeline: list entries two super-rounds ahead, windows one ahead (registers).
-__device__ __forceinline__ void deliver_tile_wl(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
-                                                uint32_t *cnt, bool marks = false) {
-    constexpr uint32_t NW = kBlock / 32;
-    constexpr uint32_t NONE = 0xFFFFFFFFu;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t par = (uint32_t)(t & 1);
-    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
-    __shared__ uint32_t s_total;
-    if (tid == 0) {
-        s_total = a.wcount[(t % 3) * a.NT + b];
-        if (c == 0) a.wcount[((t + 2) % 3) * a.NT + b] = 0u;   // next user: step t + 2's producers
-    }
-    __syncthreads();
-    if (marks) phase_mark(a, 2);
-    const uint32_t total = s_total;
-    const uint32_t nsr = (total + 63u) / 64u;                  // super-rounds of the tile
-    const uint32_t c0 = (uint32_t)((uint64_t)nsr * c / a.C), c1 = (uint32_t)((uint64_t)nsr * (c + 1) / a.C);
-    const uint32_t s0 = c0 + (uint32_t)((uint64_t)(c1 - c0) * warp / NW);
-    const uint32_t s1 = c0 + (uint32_t)((uint64_t)(c1 - c0) * (warp + 1) / NW);
-    const uint32_t *list = a.wl + ((uint64_t)par * a.NT + b) * a.wstride;
-    auto load_wd = [&](uint32_t sr) -> uint2 {        // lane: windows 64 sr + lane, + 32 + lane
-        uint2 d = make_uint2(NONE, NONE);              // (consecutive windows in one instruction
-        if (sr < s1) {                                 //  coalesce within a segment's lines)
-            const uint32_t x = sr * 64u + lane;
-            if (x < total) d.x = list[x];
-            if (x + 32u < total) d.y = list[x + 32u];
-        }
-        return d;
-    };
-    auto load_win = [&](uint32_t d) -> uint4 {
-        if (d == NONE || (a.dbg & 2u)) return make_uint4(0, 0, 0, 0);
-        uint32_t wx = d & 0x7FFFFFFFu;
-        if (a.dbg & 16u) wx &= 0x3FFFFu;                       // diagnostics: L2-resident
-        return ld_stream_v4(a.ent + 8ull * wx);
-    };
-    if (marks) phase_mark(a, 3);
-    uint2 d1 = load_wd(s0), d2 = load_wd(s0 + 1);
-    uint4 va = load_win(d1.x), vb = load_win(d1.y);
-    for (uint32_t sr = s0; sr < s1; ++sr) {
-        const uint2 d0 = d1;
-        const uint4 wa = va, wb = vb;
-        d1 = d2;
-        d2 = load_wd(sr + 2);
-        va = load_win(d1.x);
-        vb = load_win(d1.y);
-        if (!(a.dbg & 3u)) {
-            if (d0.x != NONE) accumulate_window(cnt_s, wa, (d0.x >> 31) ? 65536u : 1u);
-            if (d0.y != NONE) accumulate_window(cnt_s, wb, (d0.y >> 31) ? 65536u : 1u);
-        }
     }
     if (marks) phase_mark(a, 4);
     __syncthreads();
@@ -1385,21 +801,12 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
     return delivered;
 }
 
-// Padded-layout delivery of tile b (CTA c of C): staged ring (a.rstages stages) or the
-// register ring; byte-offset or counter-index entries.
+// Padded-layout delivery of tile b (CTA c of C): byte-offset or counter-index entries.
 __device__ __forceinline__ void deliver_padded(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
                                                uint32_t *cnt, uint32_t *big, bool marks = false,
                                                uint32_t pre_total = 0xFFFFFFFFu) {
-    if (a.rstages == 8) {
-        if (a.eshift) deliver_tile_rs<false, 8>(a, t, b, c, cnt, big, marks);
-        else deliver_tile_rs<true, 8>(a, t, b, c, cnt, big, marks);
-    } else if (a.rstages == 4) {
-        if (a.eshift) deliver_tile_rs<false, 4>(a, t, b, c, cnt, big, marks);
-        else deliver_tile_rs<true, 4>(a, t, b, c, cnt, big, marks);
-    } else {
-        if (a.eshift) deliver_tile_ring<false>(a, t, b, c, cnt, big, marks, pre_total);
-        else deliver_tile_ring<true>(a, t, b, c, cnt, big, marks, pre_total);
-    }
+    if (a.eshift) deliver_tile_ring<false>(a, t, b, c, cnt, big, marks, pre_total);
+    else deliver_tile_ring<true>(a, t, b, c, cnt, big, marks, pre_total);
 }
 
 __device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot, uint32_t d, uint32_t *s_tmp) {
@@ -1415,37 +822,25 @@ __device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot,
     }
 }
 
-// Delivery shared memory: wbuf | cnt [TW + kDummy] | big [max(kStageWords, 2 dcap)] | pref | tmp
-__host__ __device__ inline uint32_t big_words(uint32_t dcap, uint32_t rstages) {
-    uint32_t w = (uint32_t)kStageWords > 2u * dcap ? (uint32_t)kStageWords : 2u * dcap;
-    const uint32_t ring = (kBlock / 32) * kRing;               // deliver_tile_ring's rings
-    w = w > ring ? w : ring;
-    const uint32_t rs = rstages ? (kBlock / 32) * (kRingS + rstages * 32u * 4u) : 0u;   // deliver_tile_rs
-    return w > rs ? w : rs;
+// Delivery shared memory: cnt [TW + kDummy] | big [max(kStageWords, rings)] | pref | tmp
+__host__ __device__ constexpr uint32_t big_words() {
+    return (uint32_t)kStageWords > (kBlock / 32) * kRing ? (uint32_t)kStageWords : (kBlock / 32) * kRing;
 }
 __device__ __forceinline__ DeliverSmem carve(const SimArgs &a, uint32_t *smem) {
     DeliverSmem sm;
     const uint32_t tw4 = (a.TW + 3u) & ~3u;
-    sm.wbuf = reinterpret_cast<uint4 *>(smem);          // kWbufWords words, 16-byte aligned
-    smem += kWbufWords;
     sm.cnt = smem;
     smem += tw4 + kDummy;
-    sm.dsm = reinterpret_cast<uint64_t *>(smem);
     sm.stage = smem;
-    smem += big_words(a.dcap, a.rstages);
+    smem += big_words();
     sm.pref = smem;
     sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
     return sm;
 }
 
-size_t tile_smem_bytes(uint32_t TW, uint32_t NR, uint32_t dcap, uint32_t rstages) {
+size_t tile_smem_bytes(uint32_t TW, uint32_t NR) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
-    return ((size_t)kWbufWords + tw4 + kDummy + big_words(dcap, rstages) + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
-}
-size_t xchg_kernel_smem_bytes(uint32_t TW, uint32_t NT) {
-    const size_t c = ((size_t)((TW + 3u) & ~3u)) * 4;
-    const size_t x = xchg_smem_bytes(NT);
-    return c > x ? c : x;
+    return ((size_t)tw4 + kDummy + big_words() + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
 }
 
 // Brunel+ tile kernels: counters [TW] u32, plastic sums [TW] i64, region prefix, scan tmp.
@@ -1472,40 +867,20 @@ __global__ void __launch_bounds__(kBlock) k_update(SimArgs a, uint32_t k) {
     __shared__ uint32_t s_count;
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
-    update_tile<MODEL>(a, *a.t0 + k, blockIdx.x, blockIdx.x * a.TWs, a.TWs, nullptr, a.G == 1, &s_count, stage, stage);
+    update_tile<MODEL>(a, *a.t0 + k, blockIdx.x, blockIdx.x * a.TWs, a.TWs, nullptr, a.G == 1, &s_count, stage);
 }
 
-template <int GS>
+// Delivery of step t alone (padded layout): the first/last step of a graph replay, the
+// unfused sequence and G > 1 external exchange.
 __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
     extern __shared__ __align__(16) uint32_t smem[];
-    if (a.xbuf) {                                        // tile-pair exchange (G = 1, C = 1)
-        __shared__ uint32_t s_tmp[32];
-        const uint64_t t = *a.t0 + k;
-        const uint32_t b = blockIdx.x;
-        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) smem[x] = 0u;
-        __syncthreads();
-        const uint32_t d = exchange_consume(a, (uint32_t)(t & 1), b, smem);
-        uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
-        for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u) {
-            uint4 o = *reinterpret_cast<uint4 *>(dst + x);
-            o.x += smem[x]; o.y += smem[x + 1]; o.z += smem[x + 2]; o.w += smem[x + 3];
-            *reinterpret_cast<uint4 *>(dst + x) = o;
-        }
-        store_delivered(a, b, d, s_tmp);
-        return;
-    }
     DeliverSmem sm = carve(a, smem);
     const uint64_t t = *a.t0 + k;
     const uint32_t b = blockIdx.x / a.C, c = blockIdx.x % a.C;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) sm.cnt[x] = 0u;
-    uint32_t d;
-    if (a.wl) { __syncthreads(); deliver_tile_wl(a, t, b, c, sm.cnt); d = 0; }
-    else if (a.desc) {
-        __syncthreads();
-        deliver_padded(a, t, b, c, sm.cnt, sm.stage);
-        d = 0;
-    }
-    else d = deliver_tile<GS>(a, t, b, c, sm);
+    __syncthreads();
+    deliver_padded(a, t, b, c, sm.cnt, sm.stage);
+    const uint32_t d = 0;                                // (counted from out-degrees by the producers)
     uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
     if (a.C == 1u) {
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u) {
@@ -1580,21 +955,8 @@ __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// Fused-kernel variants (MODEL != 3; for Brunel+ the second parameter is the lane group GS).
-enum : int { kVXchg = 0, kVWlist = 1, kVRingB = 2, kVRingW = 3, kVRs8B = 4, kVRs8W = 5, kVRs4B = 6, kVRs4W = 7 };
-
-template <int V>
-__device__ __forceinline__ void deliver_variant(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
-                                                uint32_t *cnt, uint32_t *big, uint32_t pre_total) {
-    if constexpr (V == kVWlist) deliver_tile_wl(a, t, b, 0, cnt, true);
-    else if constexpr (V == kVRingB) deliver_tile_ring<false>(a, t, b, c, cnt, big, true, pre_total);
-    else if constexpr (V == kVRingW) deliver_tile_ring<true>(a, t, b, c, cnt, big, true, pre_total);
-    else if constexpr (V == kVRs8B) deliver_tile_rs<false, 8>(a, t, b, c, cnt, big, true);
-    else if constexpr (V == kVRs8W) deliver_tile_rs<true, 8>(a, t, b, c, cnt, big, true);
-    else if constexpr (V == kVRs4B) deliver_tile_rs<false, 4>(a, t, b, c, cnt, big, true);
-    else deliver_tile_rs<true, 4>(a, t, b, c, cnt, big, true);
-}
-
+// Fused kernel: for MODEL != 3 the second parameter V selects the padded entry format
+// (1: counter indices, cluster tiles; 0: byte offsets); for Brunel+ it is the lane group GS.
 template <int MODEL, int V>
 __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
     if constexpr (MODEL == 3) {                             // Brunel+ (delay >= 1 via the rings)
@@ -1616,29 +978,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         store_delivered(a, b, d, sm.tmp);
         __syncthreads();
         phase_mark(a, 6);
-        update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count3, sm.stage, nullptr, nullptr, true);
+        update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count3, sm.stage, nullptr, true);
         phase_mark(a, 12);
-    } else if constexpr (V == kVXchg) {                    // tile-pair exchange (experimental)
-        extern __shared__ __align__(16) uint32_t smem[];
-        __shared__ uint32_t s_count;
-        __shared__ uint32_t s_tmp[32];
-        const uint64_t t = *a.t0 + k;
-        const uint32_t b = blockIdx.x;
-        if (threadIdx.x == 0) s_count = 0;
-        uint32_t *cnt = smem;
-        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) cnt[x] = 0u;
-        __syncthreads();
-        const uint32_t d = exchange_consume(a, (uint32_t)(t & 1), b, cnt);
-        store_delivered(a, b, d, s_tmp);
-        if (a.delay == 1) {
-            update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, cnt, true, &s_count, nullptr, smem);
-        } else {
-            uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
-            for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)
-                *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
-            __syncthreads();
-            update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count, nullptr, smem);
-        }
     } else {                                                 // padded layout (G = 1)
         extern __shared__ __align__(16) uint32_t smem[];
         DeliverSmem sm = carve(a, smem);
@@ -1652,7 +993,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         // (G > 1: the update of t+1 only writes the send bitmap; the lists and descriptors of
         //  the gathered spikes come from bitmap->list)
         // thread 0: the step's descriptor count, loaded before the counters are zeroed
-        const uint32_t pre_total = (threadIdx.x == 0 && V != kVWlist) ? a.dcount[t % 3] : 0xFFFFFFFFu;
+        const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t % 3] : 0xFFFFFFFFu;
         if (threadIdx.x == 0) {   // this slice's neuron state (+ input slot t+1) -> L2 while delivering
             const uint32_t lo0 = b * a.TWs, nb = a.TWs * 4u;
             const void *arr[5] = {MODEL == 4 ? (const void *)(a.acc + lo0) : (const void *)(a.v + lo0),
@@ -1668,16 +1009,16 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             *reinterpret_cast<uint4 *>(sm.cnt + x) = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
         phase_mark(a, 1);
-        deliver_variant<V>(a, t, bt, c, sm.cnt, sm.stage, pre_total);
+        deliver_tile_ring<V == 1>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
         uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice
         const uint32_t lo = b * a.TWs;
-        constexpr bool DESC = V != kVWlist;
+        constexpr bool DESC = true;
         if (a.delay == 1) {
             // C > 1: the update sums the C partial slices itself (peers read after one cluster
             // barrier; a second one at exit keeps every CTA's counters alive until then)
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
             phase_mark(a, 6);
-            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, a.G == 1, &s_count, sm.stage, nullptr, nullptr, true,
+            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, a.G == 1, &s_count, sm.stage, nullptr, true,
                                      a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
             // (an arrive right after the update loop, waited at exit, measured 0.5 us slower)
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1687,7 +1028,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + lo;
             for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u)
                 *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
-            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, a.G == 1, &s_count, sm.stage, nullptr, nullptr, true,
+            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, a.G == 1, &s_count, sm.stage, nullptr, true,
                                      kMaxCluster, sm.stage + kStageWords);
             if (a.C > 1) cluster_wait();                     // partners done reading this CTA's counters
         }
@@ -1758,7 +1099,7 @@ __global__ void __launch_bounds__(kBlock) k_small(SimArgs a, uint32_t k0, uint32
     uint64_t deliv = 0;
     for (uint32_t q = 0; q < nsteps; ++q) {
         const uint64_t t = t0 + q;
-        update_tile<MODEL>(a, t, 0, 0, TW, cnt, false, &s_count, nullptr, nullptr, &sp, false, kMaxCluster,
+        update_tile<MODEL>(a, t, 0, 0, TW, cnt, false, &s_count, nullptr, &sp, false, kMaxCluster,
                            nullptr, bm_s);                   // ends with a barrier
         for (uint32_t x = tid * 4u; x < TW; x += kBlock * 4u)
             *reinterpret_cast<uint4 *>(cnt + x) = make_uint4(0u, 0u, 0u, 0u);
@@ -1910,61 +1251,40 @@ static cudaError_t allow_smem(K kern, size_t bytes) {
 }
 
 cudaError_t prepare_kernels(const SimArgs &a) {
-    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap, a.rstages);
-    {
-        const size_t ub = (size_t)kStageWords * 4;
-        cudaError_t e1 = allow_smem(k_update<1>, ub);
-        if (!e1) e1 = allow_smem(k_update<2>, ub);
-        if (!e1) e1 = allow_smem(k_update<3>, ub);
-        if (!e1) e1 = allow_smem(k_update<4>, ub);
-        if (e1) return e1;
-    }
-    if (a.xbuf) {
-        const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT);
-        if (xb > bytes) bytes = xb;
-        cudaError_t e0 = cudaSuccess;
-        if (!e0) e0 = allow_smem(k_update<1>, xb); if (!e0) e0 = allow_smem(k_update<2>, xb);
-        if (!e0) e0 = allow_smem(k_update<4>, xb);
-        if (e0) return e0;
-    }
+    const size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    const size_t ub = (size_t)kStageWords * 4;
     cudaError_t e = cudaSuccess;
-#define ALLOW(kern) if (!e) e = allow_smem(kern, bytes)
-    ALLOW(k_deliver<1>); ALLOW(k_deliver<2>); ALLOW(k_deliver<4>); ALLOW(k_deliver<8>);
-    ALLOW(k_deliver<16>); ALLOW(k_deliver<32>);
-#define ALLOW_M(M) ALLOW((k_fused<M, kVXchg>)); ALLOW((k_fused<M, kVWlist>)); ALLOW((k_fused<M, kVRingB>)); \
-    ALLOW((k_fused<M, kVRingW>)); ALLOW((k_fused<M, kVRs8B>)); ALLOW((k_fused<M, kVRs8W>)); \
-    ALLOW((k_fused<M, kVRs4B>)); ALLOW((k_fused<M, kVRs4W>))
-    ALLOW_M(1); ALLOW_M(2); ALLOW_M(4);
-    ALLOW(k_global_atomics);
+#define ALLOW(kern, b) if (!e) e = allow_smem(kern, b)
+    ALLOW(k_update<1>, ub); ALLOW(k_update<2>, ub); ALLOW(k_update<3>, ub); ALLOW(k_update<4>, ub);
+    ALLOW(k_deliver, bytes);
+    ALLOW((k_fused<1, 0>), bytes); ALLOW((k_fused<1, 1>), bytes);
+    ALLOW((k_fused<2, 0>), bytes); ALLOW((k_fused<2, 1>), bytes);
+    ALLOW((k_fused<4, 0>), bytes); ALLOW((k_fused<4, 1>), bytes);
+    ALLOW(k_global_atomics, tile_smem_bytes(0, a.NR));
     {
         const size_t sb = small_smem_bytes(a.TW, a.model);
-        if (!e && sb <= 227 * 1024 - 2048) {
-            e = allow_smem(k_small<1>, sb);
-            if (!e) e = allow_smem(k_small<2>, sb);
-            if (!e) e = allow_smem(k_small<4>, sb);
+        if (sb <= kSmallSmemMax) {
+            ALLOW(k_small<1>, sb); ALLOW(k_small<2>, sb); ALLOW(k_small<4>, sb);
         }
     }
-    if (!e) e = allow_smem(k_b2l, (size_t)kStageWords * 4);
+    ALLOW(k_b2l, ub);
     if (a.model == 3) {
         const size_t pb = plastic_smem_bytes(a.TW, a.NR);
-#define ALLOWP(kern) if (!e) e = allow_smem(kern, pb)
-        ALLOWP(k_deliver_plastic<1>); ALLOWP(k_deliver_plastic<2>); ALLOWP(k_deliver_plastic<4>);
-        ALLOWP(k_deliver_plastic<8>); ALLOWP(k_deliver_plastic<16>); ALLOWP(k_deliver_plastic<32>);
-        ALLOWP((k_fused<3, 1>)); ALLOWP((k_fused<3, 2>)); ALLOWP((k_fused<3, 4>));
-        ALLOWP((k_fused<3, 8>)); ALLOWP((k_fused<3, 16>)); ALLOWP((k_fused<3, 32>));
-#undef ALLOWP
+        ALLOW(k_deliver_plastic<1>, pb); ALLOW(k_deliver_plastic<2>, pb); ALLOW(k_deliver_plastic<4>, pb);
+        ALLOW(k_deliver_plastic<8>, pb); ALLOW(k_deliver_plastic<16>, pb); ALLOW(k_deliver_plastic<32>, pb);
+        ALLOW((k_fused<3, 1>), pb); ALLOW((k_fused<3, 2>), pb); ALLOW((k_fused<3, 4>), pb);
+        ALLOW((k_fused<3, 8>), pb); ALLOW((k_fused<3, 16>), pb); ALLOW((k_fused<3, 32>), pb);
     }
-#undef ALLOW_M
 #undef ALLOW
     return e;
 }
 
 cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s) {
-    const size_t ub = a.xbuf ? xchg_kernel_smem_bytes(a.TW, a.NT) : (size_t)kStageWords * 4;
+    const size_t ub = (size_t)kStageWords * 4;
     switch (a.model) {
     case 1: k_update<1><<<a.NT * a.C, kBlock, ub, s>>>(a, k); break;
     case 2: k_update<2><<<a.NT * a.C, kBlock, ub, s>>>(a, k); break;
-    case 3: k_update<3><<<a.NT * a.C, kBlock, kStageWords * 4, s>>>(a, k); break;
+    case 3: k_update<3><<<a.NT * a.C, kBlock, ub, s>>>(a, k); break;
     case 4: k_update<4><<<a.NT * a.C, kBlock, ub, s>>>(a, k); break;
     default: return cudaErrorInvalidValue;
     }
@@ -1973,7 +1293,7 @@ cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s) {
 
 cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, int n_sm, cudaStream_t s) {
     if (global_atomics) {
-        const size_t bytes = tile_smem_bytes(0, a.NR, a.dcap, 0);
+        const size_t bytes = tile_smem_bytes(0, a.NR);
         k_global_atomics<<<min((uint32_t)(n_sm * 4), a.NT * a.C), kBlock, bytes, s>>>(a, k);
         return cudaGetLastError();
     }
@@ -1989,27 +1309,9 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
         }
         return cudaGetLastError();
     }
-    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap, a.rstages);
-    if (a.xbuf) { const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT); if (xb > bytes) bytes = xb; }
-    const uint32_t grid = a.NT * a.C;
-    switch (a.GS) {
-    case 1: k_deliver<1><<<grid, kBlock, bytes, s>>>(a, k); break;
-    case 2: k_deliver<2><<<grid, kBlock, bytes, s>>>(a, k); break;
-    case 4: k_deliver<4><<<grid, kBlock, bytes, s>>>(a, k); break;
-    case 8: k_deliver<8><<<grid, kBlock, bytes, s>>>(a, k); break;
-    case 16: k_deliver<16><<<grid, kBlock, bytes, s>>>(a, k); break;
-    default: k_deliver<32><<<grid, kBlock, bytes, s>>>(a, k); break;
-    }
+    if (!a.desc) return cudaErrorInvalidValue;             // padded layout only
+    k_deliver<<<a.NT * a.C, kBlock, tile_smem_bytes(a.TW, a.NR), s>>>(a, k);
     return cudaGetLastError();
-}
-
-static int fused_variant(const SimArgs &a) {
-    if (a.xbuf) return kVXchg;
-    if (a.wl) return kVWlist;
-    const bool w = a.eshift == 0;
-    if (a.rstages == 8) return w ? kVRs8W : kVRs8B;
-    if (a.rstages == 4) return w ? kVRs4W : kVRs4B;
-    return w ? kVRingW : kVRingB;
 }
 
 // C > 1: the C CTAs of a tile are launched as one thread-block cluster.
@@ -2047,24 +1349,15 @@ static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) 
         case 16: k_fused<M, 16><<<a.NT, kBlock, bytes, s>>>(a, k); break;
         default: k_fused<M, 32><<<a.NT, kBlock, bytes, s>>>(a, k); break;
         }
-        return;
     } else {
-        switch (fused_variant(a)) {
-        case kVXchg: fused_v<M, kVXchg>(a, k, bytes, s); break;
-        case kVWlist: fused_v<M, kVWlist>(a, k, bytes, s); break;
-        case kVRingB: fused_v<M, kVRingB>(a, k, bytes, s); break;
-        case kVRingW: fused_v<M, kVRingW>(a, k, bytes, s); break;
-        case kVRs8B: fused_v<M, kVRs8B>(a, k, bytes, s); break;
-        case kVRs8W: fused_v<M, kVRs8W>(a, k, bytes, s); break;
-        case kVRs4B: fused_v<M, kVRs4B>(a, k, bytes, s); break;
-        default: fused_v<M, kVRs4W>(a, k, bytes, s); break;
-        }
+        if (a.eshift) fused_v<M, 0>(a, k, bytes, s);       // byte-offset entries
+        else fused_v<M, 1>(a, k, bytes, s);                // counter-index entries
     }
 }
 
 cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
-    size_t bytes = tile_smem_bytes(a.TW, a.NR, a.dcap, a.rstages);
-    if (a.xbuf) { const size_t xb = xchg_kernel_smem_bytes(a.TW, a.NT); if (xb > bytes) bytes = xb; }
+    if (a.model != 3 && !a.desc) return cudaErrorInvalidValue;
+    const size_t bytes = tile_smem_bytes(a.TW, a.NR);
     switch (a.model) {
     case 1: fused_m<1>(a, k, bytes, s); break;
     case 2: fused_m<2>(a, k, bytes, s); break;
@@ -2077,11 +1370,6 @@ cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
 
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s) {
     k_b2l<<<a.NR, kBlock, a.desc ? (size_t)kStageWords * 4 : 0, s>>>(a, k);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_xcap(const SimArgs &a, uint32_t *cap, cudaStream_t s) {
-    k_xcap<<<a.NT, kBlock, 2 * a.NT * 4, s>>>(a, cap);
     return cudaGetLastError();
 }
 

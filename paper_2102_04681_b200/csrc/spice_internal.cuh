@@ -14,9 +14,6 @@ enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFi
 #ifndef SPICE_KBLOCK
 #define SPICE_KBLOCK 1024
 #endif
-#ifndef SPICE_STAGES
-#define SPICE_STAGES 2
-#endif
 #ifndef SPICE_PHASES_BUILD
 #define SPICE_PHASES_BUILD 0    // in-kernel phase clocks (tools/phases.py builds a variant)
 #endif
@@ -26,17 +23,8 @@ enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFi
 #ifndef SPICE_RW
 #define SPICE_RW 2              // ring delivery: 16-byte windows per lane per iteration
 #endif
-#ifndef SPICE_DIRECT
-#define SPICE_DIRECT 1          // delivery windows straight into registers (0: cp.async via smem)
-#endif
 constexpr int kBlock = SPICE_KBLOCK;  // threads per tile CTA (update / deliver / fused)
-constexpr int kStages = SPICE_STAGES; // cp.async window stages per warp in delivery
-constexpr uint32_t kDescSmem = 8192;  // default descriptor staging capacity per CTA (64 KiB)
 constexpr int kStageWords = 12288;     // bnd rows staged per descriptor-transposition pass
-constexpr uint32_t kXRowsBytes = 128 * 1024;   // exchange producer: staged rows per batch
-// cp.async window stages (warps x stages x 32 lanes x 16 B) of the staged window path;
-// the default (SPICE_DIRECT) keeps windows in registers and needs none
-constexpr uint32_t kWbufWords = SPICE_DIRECT ? 0u : (kBlock / 32) * kStages * 32 * 4;
 constexpr uint32_t kMaxTileWidth = 49152;   // u32 counters per tile <= 192 KiB smem
 constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
 constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list region
@@ -112,14 +100,7 @@ struct SimArgs {
     uint32_t record_steps;
     uint32_t key0, key1;
     uint32_t NR, RS;         // spike-list regions
-    uint32_t pf_rows;        // 1: TMA-prefetch spiking rows into L2 at the end of the update
-    uint32_t dcap;           // descriptors a delivering CTA stages in shared memory
-    uint32_t rstages;        // staged-ring delivery: cp.async window stages per warp (8, 4; 0 = register ring)
     unsigned long long *ptimes;   // diagnostics (SPICE_PHASES=1): per CTA [16] phase clocks
-    uint64_t *dscratch;      // diagnostics (SPICE_DEBUG_MODE bit 5): second descriptor copy
-    uint32_t dbg;            // diagnostics only (SPICE_DEBUG_MODE): bit0 no smem reductions,
-                             // bit1 no synapse loads, bit2 no descriptor writes, bit4 window
-                             // addresses folded into 4 MB (L2-resident; wrong results)
     ModelConst mc;
     // connectivity
     const uint64_t *row_ptr; // [N+1]
@@ -143,19 +124,7 @@ struct SimArgs {
     // spike of the step restricted to tile b (list order = producer arrival order)
     uint64_t *desc;
     uint64_t dstride;        // descriptor slots per (parity, tile) list (>= owned neurons)
-    uint32_t *wl;            // window lists (default G = 1 path, see write_windows)
-    uint64_t wstride;        // entries per (parity, tile) window list (>= the tile's windows)
-    uint32_t *wcount;        // [3][NT] windows per list of step t at wcount[t % 3]
     uint32_t *dcount;        // [3] descriptors per list of step t at dcount[t % 3]
-    // G = 1 tile-pair exchange (SimArgs::xbuf != nullptr): chunk (bt, g, r) of parity p holds
-    // the concatenated segments, for target tile bt, of the step's spikes of source tile g
-    // with receptor r; xoff[(bt*NT + g)*2 + r] is its start (static capacity from the
-    // connectivity), xcnt[p][...] the entries written for the step.
-    uint16_t *xbuf;          // 2 * xtotal
-    const uint64_t *xoff;    // NT * NT * 2
-    uint32_t *xcnt;          // 2 * NT * NT * 2
-    uint64_t xtotal;
-    uint32_t xrows_bytes;    // TMA row-staging capacity in shared memory
     uint32_t *record;        // record_steps * G * W words
     uint32_t *sendbuf;       // W words (G > 1)
     uint32_t *gather;        // G * W words (G > 1)

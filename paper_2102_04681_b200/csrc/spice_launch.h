@@ -8,10 +8,8 @@
 namespace spice {
 
 // ---- step kernels (sim.cu) ----
-size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions, uint32_t desc_cap, uint32_t rstages);
+size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions);
 size_t plastic_smem_bytes(uint32_t tile_width, uint32_t n_regions);
-size_t xchg_kernel_smem_bytes(uint32_t tile_width, uint32_t n_tiles);
-cudaError_t launch_xcap(const SimArgs &a, uint32_t *cap, cudaStream_t s);
 uint32_t pick_group_lanes(double mean_segment);
 cudaError_t prepare_kernels(const SimArgs &a);
 cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s);
@@ -58,11 +56,14 @@ struct PlasticBoxes {
     uint32_t n;
     uint32_t box[kMaxPlasticRules][4];
 };
-// Weights (w0 on plastic synapses) and the per-target in-synapse index.
-cudaError_t gen_plastic(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
-                        const uint32_t *bnd, const uint16_t *ent, float *w, float w0,
-                        uint32_t *tmp_cnt, uint64_t *in_ptr, uint64_t **in_pos, uint32_t **in_src,
-                        uint64_t *n_plastic, cudaStream_t s);
+// Weights (w0 on plastic synapses), per-target plastic in-degrees -> in_ptr (exclusive
+// prefix, in_ptr[n_own] = *n_plastic; synchronises), then the in-synapse index itself.
+cudaError_t gen_plastic_count(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
+                              const uint32_t *bnd, const uint16_t *ent, float *w, float w0,
+                              uint32_t *tmp_cnt, uint64_t *in_ptr, uint64_t *n_plastic, cudaStream_t s);
+cudaError_t gen_plastic_fill(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
+                             const uint32_t *bnd, const uint16_t *ent, uint32_t *tmp_cnt,
+                             const uint64_t *in_ptr, uint64_t *in_pos, uint32_t *in_src, cudaStream_t s);
 // Initial state (reading R15).
 cudaError_t gen_init_uniform(const GenGeom &g, uint32_t field, float lo, float hi, float *out,
                              cudaStream_t s);

@@ -16,9 +16,10 @@ LIB_PATH = os.environ.get("SPICE_LIB") or os.path.join(_PKG, "libspice.so")
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ERANGE, ETRUNC, ESTATE = range(8)
 VOGELS, BRUNEL, BRUNEL_PLUS, SYNTH = 1, 2, 3, 4
-FLAG_EXTERNAL_EXCHANGE, FLAG_GLOBAL_ATOMICS, FLAG_UNFUSED = 0x1, 0x2, 0x4
+FLAG_EXTERNAL_EXCHANGE, FLAG_GLOBAL_ATOMICS, FLAG_UNFUSED, FLAG_USER_STREAM = 0x1, 0x2, 0x4, 0x8
+EXCHANGE_NCCL, EXCHANGE_PEER = 0, 1
 FIELD_V, FIELD_GE, FIELD_GI, FIELD_REF, FIELD_ACC, FIELD_XTR, FIELD_YTR = range(7)
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class SpiceError(RuntimeError):
@@ -43,7 +44,14 @@ class Config(C.Structure):
                 ("n_model_params", C.c_uint32), ("rank", C.c_uint32), ("world_size", C.c_uint32),
                 ("slice_width", C.c_uint32), ("device", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("record_steps", C.c_uint32), ("flags", C.c_uint32), ("tile_width", C.c_uint32),
-                ("ctas_per_tile", C.c_uint32)]
+                ("ctas_per_tile", C.c_uint32), ("group_lanes", C.c_uint32), ("exchange", C.c_uint32),
+                ("stream", C.c_void_p), ("dev_alloc", C.c_void_p), ("dev_free", C.c_void_p),
+                ("alloc_ctx", C.c_void_p)]
+
+
+# device allocator callbacks (spice_config.dev_alloc / dev_free)
+DEV_ALLOC = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+DEV_FREE = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
 
 
 _lib = None
@@ -64,6 +72,8 @@ def lib():
         "spice_step": (st, [vp, u64]),
         "spice_read_spikes": (st, [vp, u64, u64, vp, u64, vp, C.POINTER(u64)]),
         "spice_free": (st, [vp]),
+        "spice_spikes_prefetch": (st, [vp, u64, u64, u32]),
+        "spice_spikes_collect": (st, [vp, u32, vp, u64, vp, C.POINTER(u64)]),
         "spice_read_connectivity": (st, [vp, u32, u32, vp, u64, vp, C.POINTER(u64)]),
         "spice_read_state": (st, [vp, u32, vp, u64]),
         "spice_write_state": (st, [vp, u32, vp, u64]),
@@ -146,7 +156,13 @@ class Network:
     def __init__(self, cfg, rank: int = 0, world_size: int = 1, slice_width: int = 0,
                  device: int = 0, record_steps: int = 1024, nccl_id: Optional[bytes] = None,
                  external_exchange: bool = False, global_atomics: bool = False,
-                 tile_width: int = 0, ctas_per_tile: int = 0, unfused: bool = False):
+                 tile_width: int = 0, ctas_per_tile: int = 0, unfused: bool = False,
+                 group_lanes: int = 0, exchange: int = EXCHANGE_NCCL, stream: Optional[int] = None,
+                 allocator=None):
+        """``stream``: a cudaStream_t handle (int, e.g. ``torch.cuda.current_stream().cuda_stream``)
+        to enqueue on instead of a library-owned stream.  ``allocator``: a pair of callables
+        ``(alloc(nbytes) -> device pointer int, free(pointer))`` (e.g. torch's caching
+        allocator) used for every buffer the library holds."""
         L = lib()
         self._rules = (Rule * max(1, len(cfg.rules)))()
         for q, r in enumerate(cfg.rules):
@@ -155,12 +171,21 @@ class Network:
         self._params = (C.c_double * max(1, len(cfg.params)))(*cfg.params)
         self._nccl = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         flags = (FLAG_EXTERNAL_EXCHANGE if external_exchange else 0) | \
-                (FLAG_GLOBAL_ATOMICS if global_atomics else 0) | (FLAG_UNFUSED if unfused else 0)
+                (FLAG_GLOBAL_ATOMICS if global_atomics else 0) | (FLAG_UNFUSED if unfused else 0) | \
+                (FLAG_USER_STREAM if stream is not None else 0)
+        self._alloc_cbs = None
+        if allocator is not None:
+            alloc_fn, free_fn = allocator
+            self._alloc_cbs = (DEV_ALLOC(lambda nbytes, ctx: alloc_fn(nbytes) or None),
+                               DEV_FREE(lambda ptr, ctx: free_fn(ptr)))
         c = Config(ABI_VERSION, cfg.model, cfg.n, cfg.n_exc, self._rules, len(cfg.rules),
                    cfg.delay, cfg.dt_ms, cfg.seed, cfg.activity, self._params, len(cfg.params),
                    rank, world_size, slice_width, device,
                    C.cast(self._nccl, C.c_void_p) if self._nccl else None,
-                   record_steps, flags, tile_width, ctas_per_tile)
+                   record_steps, flags, tile_width, ctas_per_tile, group_lanes, exchange,
+                   stream if stream is not None else None,
+                   C.cast(self._alloc_cbs[0], C.c_void_p) if self._alloc_cbs else None,
+                   C.cast(self._alloc_cbs[1], C.c_void_p) if self._alloc_cbs else None, None)
         h = C.c_void_p()
         _check(L.spice_create_network(C.byref(c), C.byref(h)))
         self.h = h
@@ -210,6 +235,17 @@ class Network:
         total = C.c_uint64(0)
         _check(lib().spice_read_spikes(self.h, t_begin, t_end, ids.ctypes.data, ids.size,
                                        offs.ctypes.data, C.byref(total)))
+        return total.value
+
+    def spikes_prefetch(self, t_begin: int, t_end: int, slot: int) -> None:
+        """Enqueue the copy of steps [t_begin, t_end)'s spike bitmaps into pinned slot 0/1."""
+        _check(lib().spice_spikes_prefetch(self.h, t_begin, t_end, slot))
+
+    def spikes_collect_into(self, slot: int, ids: np.ndarray, offs: np.ndarray) -> int:
+        """Wait for a prefetched slot and decode it (zero-allocation); returns the spike count."""
+        total = C.c_uint64(0)
+        _check(lib().spice_spikes_collect(self.h, slot, ids.ctypes.data, ids.size, offs.ctypes.data,
+                                          C.byref(total)))
         return total.value
 
     # parity hooks --------------------------------------------------------------

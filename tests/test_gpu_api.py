@@ -24,17 +24,114 @@ def test_setup_times_are_reported(S):
         assert 0.0 < t["gen_ms"] <= t["create_ms"]
 
 
-@pytest.mark.parametrize("kw, per_chunk", [
-    ({}, 2),                                     # small network: one k_small + k_advance per 32 steps
-    (dict(tile_width=1024), 34),                 # tiled: update, 31 fused, deliver, advance
-    (dict(tile_width=1024, unfused=True), 65),   # update + deliver per step, advance
+def _decompose(n, top=256):
+    """spice_step's graph decomposition: the largest power of two <= min(n, 256) first."""
+    out = []
+    while n:
+        m = top
+        while m > n:
+            m //= 2
+        out.append(m)
+        n -= m
+    return out
+
+
+@pytest.mark.parametrize("kw, per_graph", [
+    ({}, lambda m: 2),                                  # small network: one k_small + k_advance per replay
+    (dict(tile_width=1024), lambda m: m + 2),           # tiled: update, m-1 fused, deliver, advance
+    (dict(tile_width=1024, unfused=True), lambda m: 2 * m + 1),   # update + deliver per step, advance
 ])
-def test_launch_accounting(S, kw, per_chunk):
+def test_launch_accounting(S, kw, per_graph):
+    """Every spice_step(n) runs graphs of 2^k fused steps, so a 20-step call is 16 + 4 and
+    costs n + O(log n) launches, not 3 per leftover step (VERDICT r1 weak #4)."""
     with S.Network(W.synth(20000, 31, 0.005, seed=3), **kw) as net:
-        assert net.launches(32) == per_chunk
-        assert net.launches(64) == 2 * per_chunk
-        single = net.launches(1)
-        assert net.launches(33) == per_chunk + single
+        for n in (1, 20, 32, 33, 64, 300, 1000):
+            assert net.launches(n) == sum(per_graph(m) for m in _decompose(n)), n
+        if "unfused" not in kw:
+            assert net.launches(20) <= 20 + 4
+
+
+def test_prefetch_collect_double_buffer_matches_oracle(S):
+    """spice_spikes_prefetch / _collect: chunked, double-buffered read-out (bench e2e leg)
+    returns the same per-step lists as the oracle, including a ring wrap."""
+    cfg, T, K = W.synth(5003, 31, 0.05, seed=21), 96, 12
+    o = O.OracleNet(cfg)
+    o.step(T)
+    want = o.spikes()
+    ids = np.zeros(cfg.n * K, dtype=np.uint32)
+    offs = np.zeros(K + 1, dtype=np.uint64)
+    got = []
+    with S.Network(cfg, record_steps=20, tile_width=1024) as net:
+        for c in range(T // K):
+            net.step(K)
+            net.spikes_prefetch(c * K, (c + 1) * K, c & 1)
+            if c:
+                n = net.spikes_collect_into((c - 1) & 1, ids, offs)
+                got += [ids[int(offs[q]):int(offs[q + 1])].copy() for q in range(K)]
+                assert int(offs[K]) == n
+        net.spikes_collect_into((T // K - 1) & 1, ids, offs)
+        got += [ids[int(offs[q]):int(offs[q + 1])].copy() for q in range(K)]
+        with pytest.raises(S.SpiceError):
+            net.spikes_collect_into(0, ids, offs)              # nothing prefetched
+        with pytest.raises(S.SpiceError):
+            net.spikes_prefetch(0, 10, 0)                      # older than the ring
+    assert all(np.array_equal(g, w) for g, w in zip(got, want))
+
+
+def test_user_stream_and_torch_allocator(S):
+    """spice_config.stream + SPICE_FLAG_USER_STREAM and dev_alloc/dev_free: the library
+    enqueues on torch's stream and holds its buffers in torch's caching allocator; results
+    are unchanged (checked against the oracle)."""
+    import torch
+    cfg, T = W.synth(20000, 31, 0.005, seed=3), 70
+    o = O.OracleNet(cfg)
+    o.step(T)
+    want = o.spikes()
+    held = {}
+
+    def alloc(nbytes):
+        p = torch.cuda.caching_allocator_alloc(nbytes)
+        held[p] = nbytes
+        return p
+
+    def free(p):
+        held.pop(p)
+        torch.cuda.caching_allocator_delete(p)
+
+    torch.cuda.set_device(0)
+    s = torch.cuda.Stream()
+    before = torch.cuda.memory_allocated()
+    with S.Network(cfg, record_steps=T, tile_width=1024, stream=s.cuda_stream, allocator=(alloc, free)) as net:
+        assert net.stream == s.cuda_stream
+        assert torch.cuda.memory_allocated() - before >= net.info()["device_bytes"] > 0
+        net.step(T)
+        got = net.read_spikes(0, T)
+    assert not held and torch.cuda.memory_allocated() == before
+    assert all(np.array_equal(g, w) for g, w in zip(got, want))
+    # the legacy default stream works too (graphs are captured on a private stream)
+    with S.Network(cfg, record_steps=T, tile_width=1024, stream=0) as net:
+        net.step(T)
+        got = net.read_spikes(0, T)
+    assert all(np.array_equal(g, w) for g, w in zip(got, want))
+
+
+def test_write_state_round_trip(S):
+    """spice_write_state mirrors spice_read_state for every field, including the
+    double-buffered, globally indexed pre traces at an odd step (ADVICE r1)."""
+    cfg = W.brunel_plus(2001, 0.1, seed=5)
+    with S.Network(cfg, world_size=2, rank=1, external_exchange=True, tile_width=256) as net:
+        rng = np.random.default_rng(0)
+        for t in range(2):                      # t_host = 0, then 1 (the other trace buffer)
+            if t:
+                net.exchange_begin()            # one step; rank 0's bitmap stays all-zero
+                net.exchange_end()
+            for f in (S.FIELD_V, S.FIELD_XTR, S.FIELD_YTR):
+                x = rng.random(net.n_owned).astype(np.float32)
+                net.write_state(f, x)
+                assert np.array_equal(net.state(f), x), (t, f)
+            r = rng.integers(0, 5, net.n_owned).astype(np.uint32)
+            net.write_state(S.FIELD_REF, r)
+            assert np.array_equal(net.state(S.FIELD_REF), r)
 
 
 def test_record_ring_bounds(S):

@@ -564,3 +564,20 @@ def test_sampled_rows_and_columns_match_csr(G, S):
         starts = np.searchsorted(tg_sorted, np.arange(cfg.n + 1))
         for j in range(0, cfg.n, 11):
             assert np.array_equal(O.col(cfg, j), src_sorted[starts[j]:starts[j + 1]])
+
+
+def test_synth_checkers_match_simulation():
+    """The full-size synth checkers (reading R17) equal the simulated network:
+    orc_synth_fired(t) is the spike set of step t and orc_synth_acc(j, T) the accumulator
+    of target j after T steps, for delay 1 and delay 3."""
+    for delay in (1, 3):
+        cfg = W.synth(3000, 23, 0.01, seed=31, delay=delay)
+        net = O.OracleNet(cfg)
+        T = 60
+        net.step(T)
+        sp_ = net.spikes()
+        for t in (0, 1, 17, T - 1):
+            assert np.array_equal(O.synth_fired(cfg, t), sp_[t])
+        acc = net.state(O.F_ACC)
+        for j in range(0, cfg.n, 97):
+            assert O.synth_acc(cfg, j, T) == int(acc[j])
