@@ -4,10 +4,13 @@
 """
 from __future__ import annotations
 
+import fcntl
 import importlib.util
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -41,27 +44,36 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
-    """Compile the library (to `out` with extra -D `defines` for A/B variants)."""
+    """Compile the library (to `out` with extra -D `defines` for A/B variants).  Objects go
+    to a private temporary directory and the finished library is renamed into place under
+    an exclusive file lock, so concurrent builders (one per rank) cannot see each other's
+    half-written files; a builder that waited for the lock rebuilds only if still stale."""
     target = out or LIB
     if not out and not force and not _stale():
         return LIB
-    objs = []
-    flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-                    "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_include(),
-                    "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-    if verbose:
-        flags += ["-Xptxas", "-v"]
-    flags += [f"-D{d}" for d in defines]
-    for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [nvcc()] + flags + ["-c", os.path.join(CSRC, src), "-o", obj]
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
-    tmp = target + ".tmp"
-    subprocess.run([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"], check=True)
-    os.replace(tmp, target)
-    for o in objs:
-        os.remove(o)
+    with open(target + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not out and not force and not _stale():
+            return LIB
+        flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+                        "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_include(),
+                        "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+        if verbose:
+            flags += ["-Xptxas", "-v"]
+        flags += [f"-D{d}" for d in defines]
+        tmpdir = tempfile.mkdtemp(prefix="spice_build_")
+        try:
+            objs = []
+            for src in SOURCES:
+                obj = os.path.join(tmpdir, src.replace(".cu", ".o"))
+                subprocess.run([nvcc()] + flags + ["-c", os.path.join(CSRC, src), "-o", obj], check=True)
+                objs.append(obj)
+            tmp = os.path.join(tmpdir, "lib.so")
+            subprocess.run([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl", "-lpthread"], check=True)
+            shutil.move(tmp, target + f".tmp{os.getpid()}")
+            os.replace(target + f".tmp{os.getpid()}", target)
+        finally:
+            shutil.rmtree(tmpdir, ignore_errors=True)
     return target
 
 

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <string>
 #include <chrono>
+#include <thread>
 #include <vector>
 
 #include "spice.h"
@@ -67,6 +68,32 @@ void decode_into(const uint32_t *bm, uint32_t G, uint32_t W, uint32_t S, std::ve
             }
         }
     if (G > 1) std::sort(L.begin(), L.end());
+}
+
+// Decode nsteps consecutive steps of gathered bitmaps (words per step each) into per[q];
+// independent steps are decoded on up to 8 host threads (the host side of a streaming
+// read-out would otherwise be slower than the GPU steps it reads, at 1e6+ neurons).
+uint64_t decode_steps(const uint32_t *bm, uint64_t nsteps, uint64_t words, uint32_t G, uint32_t W,
+                      uint32_t S, std::vector<std::vector<uint32_t>> &per) {
+    per.resize(nsteps);
+    const uint64_t work = nsteps * words;
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = std::max(1u, std::min<unsigned>(nt ? nt : 1, 8));
+    if (work < (1u << 16) || nsteps < 2) nt = 1;
+    nt = (unsigned)std::min<uint64_t>(nt, nsteps);
+    auto body = [&](unsigned id) {
+        for (uint64_t q = id; q < nsteps; q += nt) decode_into(bm + q * words, G, W, S, per[q]);
+    };
+    if (nt == 1) body(0);
+    else {
+        std::vector<std::thread> th;
+        for (unsigned id = 1; id < nt; ++id) th.emplace_back(body, id);
+        body(0);
+        for (auto &x : th) x.join();
+    }
+    uint64_t tot = 0;
+    for (auto &L : per) tot += L.size();
+    return tot;
 }
 
 uint64_t owned_count(uint64_t n, uint32_t g, uint32_t G, uint32_t S) {
@@ -852,13 +879,7 @@ spice_status spice_read_spikes(spice_net *n, uint64_t t_begin, uint64_t t_end, u
     }
     CU(n, cudaStreamSynchronize(n->stream));
     std::vector<std::vector<uint32_t>> &per = n->hdec;
-    per.resize(nsteps);
-    uint64_t tot = 0;
-    for (uint64_t t = t_begin; t < t_end; ++t) {
-        std::vector<uint32_t> &L = per[t - t_begin];
-        decode_into(n->hbm + (t - t_begin) * words, n->G, n->W, n->S, L);
-        tot += L.size();
-    }
+    const uint64_t tot = decode_steps(n->hbm, nsteps, words, n->G, n->W, n->S, per);
     if (total) *total = tot;
     if (tot > cap || (!ids && tot)) return fail(n, SPICE_ETRUNC, "need %llu ids", (unsigned long long)tot);
     uint64_t o = 0;
@@ -915,12 +936,7 @@ spice_status spice_spikes_collect(spice_net *n, uint32_t slot, uint32_t *ids, ui
     CU(n, cudaEventSynchronize(sl.done));
     const uint64_t words = (uint64_t)n->G * n->W, nsteps = sl.t_end - sl.t_begin;
     std::vector<std::vector<uint32_t>> &per = n->hdec;
-    per.resize(nsteps);
-    uint64_t tot = 0;
-    for (uint64_t q = 0; q < nsteps; ++q) {
-        decode_into(sl.h + q * words, n->G, n->W, n->S, per[q]);
-        tot += per[q].size();
-    }
+    const uint64_t tot = decode_steps(sl.h, nsteps, words, n->G, n->W, n->S, per);
     if (total) *total = tot;
     if (tot > cap || (!ids && tot)) return fail(n, SPICE_ETRUNC, "need %llu ids", (unsigned long long)tot);
     uint64_t o = 0;

@@ -32,6 +32,13 @@ CASES = {
     "bplus3000": (W.brunel_plus(3000, 0.1, seed=5), {}, 300),
     "bplus3000_strong_t64": (_stronger_stdp(W.brunel_plus(3000, 0.1, seed=6)), dict(tile_width=64), 300),
     "bplus2001_ragged": (_stronger_stdp(W.brunel_plus(2001, 0.15, seed=7, delay=3)), dict(tile_width=96), 200),
+    # mean segment 300/8 = 37.5 entries: the automatic lane-group rule picks GS = 8, the
+    # launch variant of the Brunel+ 50K bench geometry
+    "bplus3000_t384_autogs8": (_stronger_stdp(W.brunel_plus(3000, 0.1, seed=8)), dict(tile_width=384), 250),
+    # every other lane-group width through spice_config.group_lanes
+    "bplus3000_gs16": (_stronger_stdp(W.brunel_plus(3000, 0.1, seed=9)), dict(tile_width=384, group_lanes=16), 200),
+    "bplus3000_gs32": (_stronger_stdp(W.brunel_plus(3000, 0.1, seed=10)), dict(group_lanes=32), 200),
+    "bplus2001_gs1": (_stronger_stdp(W.brunel_plus(2001, 0.15, seed=11, delay=2)), dict(tile_width=128, group_lanes=1), 200),
 }
 
 
