@@ -118,8 +118,6 @@ typedef struct {
     uint32_t tile_width;           /* targets per delivery tile (multiple of 32,
                                       <= 49152); 0 = auto */
     uint32_t ctas_per_tile;        /* CTAs sharing one tile (>= 1); 0 = auto */
-    uint32_t group_lanes;          /* Brunel+ delivery: lanes per segment group (1, 2, 4, 8,
-                                      16, 32); 0 = auto from the mean segment length */
     uint32_t exchange;             /* SPICE_EXCHANGE_NCCL | SPICE_EXCHANGE_PEER (G > 1) */
     void    *stream;               /* cudaStream_t, used with SPICE_FLAG_USER_STREAM */
     /* Device allocator for every buffer the library holds (e.g. the torch caching

@@ -190,8 +190,8 @@ struct spice_net {
     // Brunel+
     float *w = nullptr, *xtr = nullptr, *ytr = nullptr;
     long long *pring = nullptr;
-    uint64_t *in_ptr = nullptr, *in_pos = nullptr;
-    uint32_t *in_src = nullptr;
+    uint64_t *in_ptr = nullptr;
+    uint32_t *in_pos = nullptr, *in_src = nullptr;
     uint64_t n_plastic = 0;
     ModelConst mc{};
     SimArgs args{};
@@ -643,6 +643,8 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (n->NR > kMaxRegions) return bail(fail(n, SPICE_EINVAL, "%u spike-list regions > %u: use a wider tile_width", n->NR, kMaxRegions));
     const size_t smem_max = 227 * 1024 - 2048;             // dynamic; static shared variables need the rest
     if (n->pad8 && tile_smem_bytes(n->TW, n->NR) > smem_max) return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for shared memory", n->TW));
+    if (n->model == SPICE_BRUNEL_PLUS && plastic_smem_bytes(n->TW, n->NR) > smem_max)
+        return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for the Brunel+ tile kernels", n->TW));
     // ---- NCCL communicator ----
     if (n->G > 1 && !n->external) {
         if (!nccl().ok) return bail(fail(n, SPICE_ENCCL, "libnccl.so.2 not found (set SPICE_NCCL_LIB)"));
@@ -700,6 +702,9 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         g2.N = n->N; g2.n_own = (uint32_t)n->n_own; g2.rank = n->rank; g2.G = n->G; g2.S = n->S;
         g2.TW = n->TW; g2.NT = n->NT; g2.key0 = (uint32_t)n->seed; g2.key1 = (uint32_t)(n->seed >> 32);
         uint32_t *tmp = nullptr;
+        if (n->nnz >= (1ull << 32))
+            return bail(fail(n, SPICE_EINVAL, "Brunel+ slices hold < 2^32 synapses per rank (32-bit in-synapse index); got %llu",
+                             (unsigned long long)n->nnz));
         if ((st = dalloc_t(n, &n->w, n->nnz + 8, "plastic weights"))) return bail(st);
         if ((st = dalloc_t(n, &n->pring, (size_t)n->D * n->ring_stride, "plastic input ring"))) return bail(st);
         if ((st = dalloc_t(n, &n->xtr, 2ull * n->N, "pre traces"))) return bail(st);
@@ -756,8 +761,6 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D;
     a.rank = n->rank; a.G = n->G; a.S = n->S; a.n_own = (uint32_t)n->n_own; a.W = n->W;
     a.TW = n->TW; a.NT = n->NT; a.C = n->C; a.TWs = n->TWs; a.ring_stride = n->ring_stride; a.record_steps = n->R;
-    a.GS = pick_group_lanes(n->mean_seg);
-    if (c->group_lanes) a.GS = c->group_lanes;
     if (getenv("SPICE_PHASES") && atoi(getenv("SPICE_PHASES"))) {     // diagnostics only
         if ((st = dalloc_t(n, &n->ptimes, (size_t)n->NT * n->C * 16, "phase clocks"))) return bail(st);
         CU(n, cudaMemset(n->ptimes, 0, (size_t)n->NT * n->C * 16 * 8));
@@ -1070,6 +1073,7 @@ spice_status spice_read_weights(spice_net *n, uint32_t row_begin, uint32_t row_e
     if (total) *total = tot;
     if (tot > cap || (!w && tot)) return fail(n, SPICE_ETRUNC, "need %llu weights", (unsigned long long)tot);
     if (tot) CU(n, cudaMemcpy(w, n->w + rp[0], tot * 4, cudaMemcpyDeviceToHost));
+    for (uint64_t q = 0; q < tot; ++q) if (w[q] < 0.0f) w[q] = 0.0f;   // static synapses' sentinel
     return SPICE_OK;
 }
 

@@ -430,7 +430,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) plastic_kernel(GenGeom g, PlasticBoxes pb, const uint64_t *row_ptr,
                                                       const uint32_t *bnd, const uint16_t *ent, float *w,
                                                       float w0, uint32_t *cnt_or_cursor,
-                                                      const uint64_t *in_ptr, uint64_t *in_pos,
+                                                      const uint64_t *in_ptr, uint32_t *in_pos,
                                                       uint32_t *in_src) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t)gridDim.x * 8;
@@ -443,11 +443,11 @@ __global__ void __launch_bounds__(256) plastic_kernel(GenGeom g, PlasticBoxes pb
             const uint32_t il = b * g.TW + (ent[st + e] >> g.eshift);
             const bool pl = is_plastic(pb, s, (uint32_t)local_to_global(il, g.rank, g.G, g.S));
             if (MODE == 0) {
-                w[st + e] = pl ? w0 : 0.0f;
+                w[st + e] = pl ? w0 : -1.0f;         // static synapses: negative sentinel
                 if (pl) atomicAdd(&cnt_or_cursor[il], 1u);
             } else if (pl) {
                 const uint64_t k = in_ptr[il] + atomicAdd(&cnt_or_cursor[il], 1u);
-                in_pos[k] = st + e;
+                in_pos[k] = (uint32_t)(st + e);
                 in_src[k] = s;
             }
         }
@@ -474,7 +474,7 @@ cudaError_t gen_plastic_count(const GenGeom &g, const PlasticBoxes &pb, const ui
 
 cudaError_t gen_plastic_fill(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
                              const uint32_t *bnd, const uint16_t *ent, uint32_t *tmp_cnt,
-                             const uint64_t *in_ptr, uint64_t *in_pos, uint32_t *in_src, cudaStream_t s) {
+                             const uint64_t *in_ptr, uint32_t *in_pos, uint32_t *in_src, cudaStream_t s) {
     cudaError_t e;
     const uint64_t pairs = (uint64_t)g.N * g.NT;
     if ((e = cudaMemsetAsync(tmp_cnt, 0, (size_t)g.n_own * 4, s))) return e;

@@ -8,11 +8,12 @@
 //                    4 neurons per thread (one Philox call covers 4 consecutive IDs),
 //                    4-bit nibbles OR-reduced into 32-bit bitmap words, spikes appended
 //                    to the tile's own list region (no global atomics)
-//   k_deliver<GS>    destination-tiled delivery of step t (a3): segment descriptors of the
-//                    spiking rows staged in smem, GS lanes per segment load 16-byte windows
-//                    of u16 offsets, shared-memory atomicAdd of packed receptor counts,
-//                    then the tile is added to the input ring slot of step t + delay
-//   k_fused<M,GS>    deliver(t) + update(t+1) of the same tile in one CTA (G = 1): with
+//   k_deliver        destination-tiled delivery of step t (a3): per-tile lists of segment
+//                    descriptors of the spiking rows, expanded per warp into a ring of
+//                    16-byte windows of u16 offsets, shared-memory atomicAdd of packed
+//                    receptor counts, then the tile is added to the input ring slot t + delay
+//   k_deliver_plastic Brunel+ (a4): potentiation, depression and delivery of a tile
+//   k_fused<M,V>     deliver(t) + update(t+1) of the same tile in one CTA (G = 1): with
 //                    delay 1 the tile's inputs never leave shared memory; one launch per
 //                    step, the kernel boundary is the step barrier
 //   k_global_atomics paper-style column-wise warps with global atomics:
@@ -669,7 +670,7 @@ __device__ __forceinline__ void potentiate_tile(const SimArgs &a, uint64_t t, ui
         block_exclusive_scan(pre, np, tmp);
         const uint32_t total = pre[np];
         for (uint32_t f0 = tid; f0 < total; f0 += kBlock * U) {
-            uint64_t pos[U];
+            uint32_t pos[U];
             uint32_t src[U];
             bool ok[U];
 #pragma unroll
@@ -702,7 +703,7 @@ __device__ __forceinline__ void potentiate_tile(const SimArgs &a, uint64_t t, ui
             const uint32_t i = wi * 32 + __ffs(word) - 1;
             word &= word - 1;
             for (uint64_t e = a.in_ptr[i] + lane; e < a.in_ptr[i + 1]; e += 32) {
-                const uint64_t pos = a.in_pos[e];
+                const uint32_t pos = a.in_pos[e];
                 const float wv = __fadd_rn(a.w[pos], __fmul_rn(a.mc.Ap, x[a.in_src[e]]));
                 a.w[pos] = wv < a.mc.wmax ? wv : a.mc.wmax;
             }
@@ -731,68 +732,96 @@ __device__ __forceinline__ void stdp_traces(const SimArgs &a, uint64_t t, uint32
     }
 }
 
-__device__ __forceinline__ void walk_plastic(const SimArgs &a, uint32_t b, uint32_t *cnt, long long *pin,
-                                             uint64_t w, uint64_t st, uint64_t en, uint32_t q,
-                                             uint32_t s, bool pls, const float *ys) {
-    const uint4 v = ld_stream_v4(a.ent + w);
-    const uint32_t e[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
-                           v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
-    float wv8[8];
-    if (pls) {                           // the window's 8 weights in two 16-byte loads (w % 8 == 0)
-        const float4 w0 = reinterpret_cast<const float4 *>(a.w + w)[0];
-        const float4 w1 = reinterpret_cast<const float4 *>(a.w + w)[1];
-        wv8[0] = w0.x; wv8[1] = w0.y; wv8[2] = w0.z; wv8[3] = w0.w;
-        wv8[4] = w1.x; wv8[5] = w1.y; wv8[6] = w1.z; wv8[7] = w1.w;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        if (w + u < st || w + u >= en) continue;
-        const uint32_t off = e[u];
-        const uint32_t il = b * a.TW + off;
-        if (pls && plastic_edge(a, s, (uint32_t)local_to_global(il, a.rank, a.G, a.S))) {
-            float wv = __fsub_rn(wv8[u], __fmul_rn(a.mc.Am, ys ? ys[off] : a.ytr[il]));
-            wv = wv > 0.0f ? wv : 0.0f;
-            a.w[w + u] = wv;             // (only this segment's entries: a window may span two tiles)
-            atomicAdd(reinterpret_cast<unsigned long long *>(&pin[off]),
-                      (unsigned long long)__double2ll_rn((double)wv * 4294967296.0));
-        } else {
-            atomicAdd(&cnt[off], q);
-        }
+// (ii)+(iii) depression and delivery of the step's spikes into tile b, over the flattened
+// (segment, entry) event space of the tile: the segments of up to kPlSeg spikes at a time
+// are staged in shared memory (entry start, length, source flags), their lengths scanned,
+// and every thread takes events f = tid, tid + kBlock, ... (U in flight, all loads issued
+// before any update): consecutive events of a segment are consecutive threads, so the
+// entry and weight loads coalesce, and a tile's ~10^3-10^4 events per step are spread over
+// all 1024 threads instead of one lane group per segment.  Plastic synapses (weight >= 0;
+// static ones hold the sentinel -1) are depressed, stored and delivered as fixed point
+// rint(w 2^32) accumulated exactly in two u32 shared words (low word with carry detection
+// from the returned old value: native 32-bit shared atomics, no 64-bit CAS loop); static
+// synapses add their packed receptor count.
+constexpr uint32_t kPlSeg = 2048;                     // segments staged per pass
+constexpr uint32_t kPlU = 4;                          // events in flight per thread
+
+__device__ __forceinline__ void plastic_event(const SimArgs &a, uint32_t *cnt, uint32_t *plo, uint32_t *phi,
+                                              const float *ys, uint32_t e, uint32_t off, uint32_t fl, float wv) {
+    if (wv >= 0.0f) {                                // plastic: depress (reading R13 (ii)), then deliver
+        float nw = __fsub_rn(wv, __fmul_rn(a.mc.Am, ys[off]));
+        nw = nw > 0.0f ? nw : 0.0f;
+        a.w[e] = nw;
+        const uint64_t q = (uint64_t)__double2ll_rn((double)nw * 4294967296.0);
+        const uint32_t lo = (uint32_t)q, hi = (uint32_t)(q >> 32);
+        const uint32_t old = atomicAdd(&plo[off], lo);
+        const uint32_t carry = old + lo < old ? 1u : 0u;
+        if (hi + carry) atomicAdd(&phi[off], hi + carry);
+    } else {
+        atomicAdd(&cnt[off], (fl & 1u) ? 65536u : 1u);
     }
 }
 
-template <int GS>
 __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b, uint32_t *cnt,
-                                         long long *pin, uint32_t *pref, uint32_t *tmp, uint32_t *stage,
-                                         bool marks = false) {
+                                                         uint32_t *plo, uint32_t *phi, uint32_t *pref, uint32_t *tmp,
+                                                         uint32_t *stage, float *ys, bool marks = false) {
     const uint32_t tid = threadIdx.x;
     const uint32_t par = (uint32_t)(t & 1);
     potentiate_tile(a, t, b, stage, tmp);
     __syncthreads();
     if (marks) phase_mark(a, 2);
     for (uint32_t r = tid; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
+    // the tile's post traces y in shared memory for the depression
+    for (uint32_t x = tid; x < a.TW; x += kBlock) ys[x] = b * a.TW + x < a.n_own ? a.ytr[b * a.TW + x] : 0.0f;
     __syncthreads();
-    // the tile's post traces y in shared memory for the depression (the potentiation pass
-    // that used `stage` is complete: block_exclusive_scan's barriers order it)
-    float *ys = a.TW <= (uint32_t)kStageWords ? reinterpret_cast<float *>(stage) : nullptr;
-    if (ys)
-        for (uint32_t x = tid; x < a.TW; x += kBlock) ys[x] = b * a.TW + x < a.n_own ? a.ytr[b * a.TW + x] : 0.0f;
-    block_exclusive_scan(pref, a.NR, tmp);       // also orders (i) before (ii)
+    block_exclusive_scan(pref, a.NR, tmp);       // (its barriers also order (i) before (ii))
     if (marks) phase_mark(a, 3);
     const uint32_t n_sp = pref[a.NR];
     const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
+    uint32_t *sst = stage, *slen = stage + kPlSeg, *sfl = stage + 2 * kPlSeg + 1;   // (stage: 3 kPlSeg + 1 words)
     uint32_t delivered = 0;
-    const uint32_t grp = tid / GS, lig = tid % GS;
-    for (uint32_t p = grp; p < n_sp; p += kBlock / GS) {
-        const uint32_t r = region_of(pref, a.NR, p);
-        const uint64_t slot = lbase + (uint64_t)r * a.RS + (p - pref[r]);
-        const uint32_t s = a.sl_ids[slot];
-        const uint32_t *bp = a.bnd + (uint64_t)s * (a.NT + 1u) + b;
-        const uint64_t st = a.sl_rows[slot] + bp[0], en = a.sl_rows[slot] + bp[1];
-        const uint32_t q = s >= a.n_exc ? 65536u : 1u;
-        const bool pls = plastic_src(a, s);
-        if (lig == 0) delivered += (uint32_t)(en - st);
-        for (uint64_t w = (st & ~7ull) + 8u * lig; w < en; w += 8u * GS) walk_plastic(a, b, cnt, pin, w, st, en, q, s, pls, ys);
+    for (uint32_t q0 = 0; q0 < n_sp; q0 += kPlSeg) {
+        const uint32_t nq = min(kPlSeg, n_sp - q0);
+        __syncthreads();                          // previous pass done with the staging
+        for (uint32_t q = tid; q < nq; q += kBlock) {
+            const uint32_t p = q0 + q;
+            const uint32_t r = region_of(pref, a.NR, p);
+            const uint64_t slot = lbase + (uint64_t)r * a.RS + (p - pref[r]);
+            const uint32_t s = a.sl_ids[slot];
+            const uint32_t *bp = a.bnd + (uint64_t)s * (a.NT + 1u) + b;
+            const uint32_t lo = bp[0], hi = bp[1];
+            sst[q] = (uint32_t)(a.sl_rows[slot] + lo);
+            slen[q] = hi - lo;
+            sfl[q] = (s >= a.n_exc ? 1u : 0u) | (plastic_src(a, s) ? 2u : 0u);
+        }
+        __syncthreads();
+        block_exclusive_scan(slen, nq, tmp);      // slen -> event prefix, slen[nq] = events
+        const uint32_t ne = slen[nq];
+        if (tid == 0) delivered += ne;
+        for (uint32_t f0 = tid; f0 < ne; f0 += kBlock * kPlU) {
+            uint32_t e[kPlU], off[kPlU], fl[kPlU];
+            float wv[kPlU];
+#pragma unroll
+            for (uint32_t u = 0; u < kPlU; ++u) {
+                const uint32_t f = f0 + u * kBlock;
+                e[u] = 0xFFFFFFFFu;
+                if (f < ne) {
+                    uint32_t l = 0, h = nq;                  // largest q with slen[q] <= f
+                    while (h - l > 1) { const uint32_t m = (l + h) >> 1; if (slen[m] <= f) l = m; else h = m; }
+                    e[u] = sst[l] + (f - slen[l]);
+                    fl[u] = sfl[l];
+                }
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < kPlU; ++u)
+                if (e[u] != 0xFFFFFFFFu) {
+                    off[u] = a.ent[e[u]];
+                    wv[u] = (fl[u] & 2u) ? a.w[e[u]] : -1.0f;
+                }
+#pragma unroll
+            for (uint32_t u = 0; u < kPlU; ++u)
+                if (e[u] != 0xFFFFFFFFu) plastic_event(a, cnt, plo, phi, ys, e[u], off[u], fl[u], wv[u]);
+        }
     }
     __syncthreads();
     if (marks) phase_mark(a, 4);
@@ -843,21 +872,32 @@ size_t tile_smem_bytes(uint32_t TW, uint32_t NR) {
     return ((size_t)tw4 + kDummy + big_words() + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
 }
 
-// Brunel+ tile kernels: counters [TW] u32, plastic sums [TW] i64, region prefix, scan tmp.
+// Brunel+ tile kernels: counters, plastic fixed-point low / high words, post traces y
+// ([TW] each), region prefix, scan tmp, staging.
 size_t plastic_smem_bytes(uint32_t TW, uint32_t NR) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
-    return (size_t)tw4 * 4 + (size_t)tw4 * 8 + (((NR + 1 + 3) & ~3u) + 32 + kStageWords) * 4 + 16;
+    return ((size_t)4 * tw4 + ((NR + 1 + 3) & ~3u) + 32 + kStageWords) * 4 + 16;
 }
-struct PlasticSmem { uint32_t *cnt; long long *pin; uint32_t *pref; uint32_t *tmp; uint32_t *stage; };
+struct PlasticSmem { uint32_t *cnt, *plo, *phi; float *ys; uint32_t *pref, *tmp, *stage; };
 __device__ __forceinline__ PlasticSmem carve_plastic(const SimArgs &a, uint32_t *smem) {
     PlasticSmem sm;
     const uint32_t tw4 = (a.TW + 3u) & ~3u;
-    sm.pin = reinterpret_cast<long long *>(smem);          // 8-byte aligned first
-    sm.cnt = smem + 2 * tw4;
-    sm.pref = sm.cnt + tw4;
+    sm.cnt = smem;
+    sm.plo = smem + tw4;
+    sm.phi = smem + 2 * tw4;
+    sm.ys = reinterpret_cast<float *>(smem + 3 * tw4);
+    sm.pref = smem + 4 * tw4;
     sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
     sm.stage = sm.tmp + 32;
     return sm;
+}
+// the tile's delivered step: counters -> ring slot t + delay, fixed-point sums -> plastic ring
+__device__ __forceinline__ void plastic_flush(const SimArgs &a, uint64_t t, uint32_t b, const PlasticSmem &sm) {
+    const uint64_t base = mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
+    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
+        a.ring[base + x] += sm.cnt[x];
+        a.pring[base + x] += (long long)(((uint64_t)sm.phi[x] << 32) | sm.plo[x]);
+    }
 }
 
 // ------------------------------------------------------------------ kernels
@@ -906,19 +946,14 @@ __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
     if (a.C != 1u && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-template <int GS>
 __global__ void __launch_bounds__(kBlock) k_deliver_plastic(SimArgs a, uint32_t k) {
     extern __shared__ __align__(16) uint32_t smem[];
     PlasticSmem sm = carve_plastic(a, smem);
     const uint64_t t = *a.t0 + k;
     const uint32_t b = blockIdx.x;
-    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.pin[x] = 0; }
-    const uint32_t d = deliver_tile_plastic<GS>(a, t, b, sm.cnt, sm.pin, sm.pref, sm.tmp, sm.stage);
-    const uint64_t base = mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
-    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
-        a.ring[base + x] += sm.cnt[x];
-        a.pring[base + x] += sm.pin[x];
-    }
+    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.plo[x] = 0u; sm.phi[x] = 0u; }
+    const uint32_t d = deliver_tile_plastic(a, t, b, sm.cnt, sm.plo, sm.phi, sm.pref, sm.tmp, sm.stage, sm.ys);
+    plastic_flush(a, t, b, sm);
     store_delivered(a, b, d, sm.tmp);
 }
 
@@ -956,11 +991,10 @@ __device__ __forceinline__ void cluster_wait() {
 }
 
 // Fused kernel: for MODEL != 3 the second parameter V selects the padded entry format
-// (1: counter indices, cluster tiles; 0: byte offsets); for Brunel+ it is the lane group GS.
+// (1: counter indices, cluster tiles; 0: byte offsets); Brunel+ has one variant (V = 0).
 template <int MODEL, int V>
 __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
     if constexpr (MODEL == 3) {                             // Brunel+ (delay >= 1 via the rings)
-        constexpr int GS = V;
         extern __shared__ __align__(16) uint32_t smem[];
         PlasticSmem sm = carve_plastic(a, smem);
         __shared__ uint32_t s_count3;
@@ -968,13 +1002,9 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         const uint32_t b = blockIdx.x;
         phase_mark(a, 0);
         if (threadIdx.x == 0) s_count3 = 0;
-        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.pin[x] = 0; }
-        const uint32_t d = deliver_tile_plastic<GS>(a, t, b, sm.cnt, sm.pin, sm.pref, sm.tmp, sm.stage, true);
-        const uint64_t base = mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
-        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
-            a.ring[base + x] += sm.cnt[x];
-            a.pring[base + x] += sm.pin[x];
-        }
+        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.plo[x] = 0u; sm.phi[x] = 0u; }
+        const uint32_t d = deliver_tile_plastic(a, t, b, sm.cnt, sm.plo, sm.phi, sm.pref, sm.tmp, sm.stage, sm.ys, true);
+        plastic_flush(a, t, b, sm);
         store_delivered(a, b, d, sm.tmp);
         __syncthreads();
         phase_mark(a, 6);
@@ -1234,17 +1264,6 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
 __global__ void k_advance(uint64_t *t0, uint32_t steps) { *t0 += steps; }
 
 // ------------------------------------------------------------------ launchers
-static uint32_t group_lanes(double mean_seg) {   // 8 entries (16 B) per lane
-    if (mean_seg <= 6) return 1;
-    if (mean_seg <= 12) return 2;
-    if (mean_seg <= 26) return 4;
-    if (mean_seg <= 56) return 8;
-    if (mean_seg <= 120) return 16;
-    return 32;
-}
-
-uint32_t pick_group_lanes(double mean_seg) { return group_lanes(mean_seg); }
-
 template <typename K>
 static cudaError_t allow_smem(K kern, size_t bytes) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -1270,10 +1289,8 @@ cudaError_t prepare_kernels(const SimArgs &a) {
     ALLOW(k_b2l, ub);
     if (a.model == 3) {
         const size_t pb = plastic_smem_bytes(a.TW, a.NR);
-        ALLOW(k_deliver_plastic<1>, pb); ALLOW(k_deliver_plastic<2>, pb); ALLOW(k_deliver_plastic<4>, pb);
-        ALLOW(k_deliver_plastic<8>, pb); ALLOW(k_deliver_plastic<16>, pb); ALLOW(k_deliver_plastic<32>, pb);
-        ALLOW((k_fused<3, 1>), pb); ALLOW((k_fused<3, 2>), pb); ALLOW((k_fused<3, 4>), pb);
-        ALLOW((k_fused<3, 8>), pb); ALLOW((k_fused<3, 16>), pb); ALLOW((k_fused<3, 32>), pb);
+        ALLOW(k_deliver_plastic, pb);
+        ALLOW((k_fused<3, 0>), pb);
     }
 #undef ALLOW
     return e;
@@ -1299,14 +1316,7 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
     }
     if (a.model == 3) {
         const size_t pb = plastic_smem_bytes(a.TW, a.NR);
-        switch (a.GS) {
-        case 1: k_deliver_plastic<1><<<a.NT, kBlock, pb, s>>>(a, k); break;
-        case 2: k_deliver_plastic<2><<<a.NT, kBlock, pb, s>>>(a, k); break;
-        case 4: k_deliver_plastic<4><<<a.NT, kBlock, pb, s>>>(a, k); break;
-        case 8: k_deliver_plastic<8><<<a.NT, kBlock, pb, s>>>(a, k); break;
-        case 16: k_deliver_plastic<16><<<a.NT, kBlock, pb, s>>>(a, k); break;
-        default: k_deliver_plastic<32><<<a.NT, kBlock, pb, s>>>(a, k); break;
-        }
+        k_deliver_plastic<<<a.NT, kBlock, pb, s>>>(a, k);
         return cudaGetLastError();
     }
     if (!a.desc) return cudaErrorInvalidValue;             // padded layout only
@@ -1340,15 +1350,8 @@ static void fused_v(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) 
 
 template <int M>
 static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
-    if constexpr (M == 3) {                               // Brunel+: lane groups (C = 1)
-        switch (a.GS) {
-        case 1: k_fused<M, 1><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-        case 2: k_fused<M, 2><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-        case 4: k_fused<M, 4><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-        case 8: k_fused<M, 8><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-        case 16: k_fused<M, 16><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-        default: k_fused<M, 32><<<a.NT, kBlock, bytes, s>>>(a, k); break;
-        }
+    if constexpr (M == 3) {                               // Brunel+ (C = 1)
+        k_fused<M, 0><<<a.NT, kBlock, bytes, s>>>(a, k);
     } else {
         if (a.eshift) fused_v<M, 0>(a, k, bytes, s);       // byte-offset entries
         else fused_v<M, 1>(a, k, bytes, s);                // counter-index entries

@@ -95,7 +95,6 @@ struct SimArgs {
                              // cluster: each accumulates its share of the tile's visits into
                              // a full-tile shared counter array, then reduces its slice
                              // across the cluster through distributed shared memory
-    uint32_t GS;             // lanes per segment group in delivery
     uint64_t ring_stride;    // NT * TW
     uint32_t record_steps;
     uint32_t key0, key1;
@@ -138,7 +137,7 @@ struct SimArgs {
     float *xtr;              // 2 * N
     float *ytr;              // ring_stride
     const uint64_t *in_ptr;  // [n_own + 1]
-    const uint64_t *in_pos;
+    const uint32_t *in_pos;  // entry index of each plastic in-synapse (nnz < 2^32 for Brunel+)
     const uint32_t *in_src;
     uint32_t npl;                                  // plastic boxes (src x dst ranges)
     uint32_t pl[kMaxPlasticRules][4];

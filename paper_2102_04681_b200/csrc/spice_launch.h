@@ -10,7 +10,6 @@ namespace spice {
 // ---- step kernels (sim.cu) ----
 size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions);
 size_t plastic_smem_bytes(uint32_t tile_width, uint32_t n_regions);
-uint32_t pick_group_lanes(double mean_segment);
 cudaError_t prepare_kernels(const SimArgs &a);
 cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, int n_sm, cudaStream_t s);
@@ -63,7 +62,7 @@ cudaError_t gen_plastic_count(const GenGeom &g, const PlasticBoxes &pb, const ui
                               uint32_t *tmp_cnt, uint64_t *in_ptr, uint64_t *n_plastic, cudaStream_t s);
 cudaError_t gen_plastic_fill(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
                              const uint32_t *bnd, const uint16_t *ent, uint32_t *tmp_cnt,
-                             const uint64_t *in_ptr, uint64_t *in_pos, uint32_t *in_src, cudaStream_t s);
+                             const uint64_t *in_ptr, uint32_t *in_pos, uint32_t *in_src, cudaStream_t s);
 // Initial state (reading R15).
 cudaError_t gen_init_uniform(const GenGeom &g, uint32_t field, float lo, float hi, float *out,
                              cudaStream_t s);

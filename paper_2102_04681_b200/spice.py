@@ -44,7 +44,7 @@ class Config(C.Structure):
                 ("n_model_params", C.c_uint32), ("rank", C.c_uint32), ("world_size", C.c_uint32),
                 ("slice_width", C.c_uint32), ("device", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("record_steps", C.c_uint32), ("flags", C.c_uint32), ("tile_width", C.c_uint32),
-                ("ctas_per_tile", C.c_uint32), ("group_lanes", C.c_uint32), ("exchange", C.c_uint32),
+                ("ctas_per_tile", C.c_uint32), ("exchange", C.c_uint32),
                 ("stream", C.c_void_p), ("dev_alloc", C.c_void_p), ("dev_free", C.c_void_p),
                 ("alloc_ctx", C.c_void_p)]
 
@@ -157,7 +157,7 @@ class Network:
                  device: int = 0, record_steps: int = 1024, nccl_id: Optional[bytes] = None,
                  external_exchange: bool = False, global_atomics: bool = False,
                  tile_width: int = 0, ctas_per_tile: int = 0, unfused: bool = False,
-                 group_lanes: int = 0, exchange: int = EXCHANGE_NCCL, stream: Optional[int] = None,
+                 exchange: int = EXCHANGE_NCCL, stream: Optional[int] = None,
                  allocator=None):
         """``stream``: a cudaStream_t handle (int, e.g. ``torch.cuda.current_stream().cuda_stream``)
         to enqueue on instead of a library-owned stream.  ``allocator``: a pair of callables
@@ -182,7 +182,7 @@ class Network:
                    cfg.delay, cfg.dt_ms, cfg.seed, cfg.activity, self._params, len(cfg.params),
                    rank, world_size, slice_width, device,
                    C.cast(self._nccl, C.c_void_p) if self._nccl else None,
-                   record_steps, flags, tile_width, ctas_per_tile, group_lanes, exchange,
+                   record_steps, flags, tile_width, ctas_per_tile, exchange,
                    stream if stream is not None else None,
                    C.cast(self._alloc_cbs[0], C.c_void_p) if self._alloc_cbs else None,
                    C.cast(self._alloc_cbs[1], C.c_void_p) if self._alloc_cbs else None, None)

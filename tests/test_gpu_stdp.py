@@ -32,13 +32,9 @@ CASES = {
     "bplus3000": (W.brunel_plus(3000, 0.1, seed=5), {}, 300),
     "bplus3000_strong_t64": (_stronger_stdp(W.brunel_plus(3000, 0.1, seed=6)), dict(tile_width=64), 300),
     "bplus2001_ragged": (_stronger_stdp(W.brunel_plus(2001, 0.15, seed=7, delay=3)), dict(tile_width=96), 200),
-    # mean segment 300/8 = 37.5 entries: the automatic lane-group rule picks GS = 8, the
-    # launch variant of the Brunel+ 50K bench geometry
-    "bplus3000_t384_autogs8": (_stronger_stdp(W.brunel_plus(3000, 0.1, seed=8)), dict(tile_width=384), 250),
-    # every other lane-group width through spice_config.group_lanes
-    "bplus3000_gs16": (_stronger_stdp(W.brunel_plus(3000, 0.1, seed=9)), dict(tile_width=384, group_lanes=16), 200),
-    "bplus3000_gs32": (_stronger_stdp(W.brunel_plus(3000, 0.1, seed=10)), dict(group_lanes=32), 200),
-    "bplus2001_gs1": (_stronger_stdp(W.brunel_plus(2001, 0.15, seed=11, delay=2)), dict(tile_width=128, group_lanes=1), 200),
+    # the Brunel+ 50K bench geometry's segment length (~35 entries per (row, tile))
+    "bplus3000_t384": (_stronger_stdp(W.brunel_plus(3000, 0.1, seed=8)), dict(tile_width=384), 250),
+    "bplus2001_t32": (_stronger_stdp(W.brunel_plus(2001, 0.15, seed=11, delay=2)), dict(tile_width=32), 200),
 }
 
 
@@ -113,3 +109,29 @@ def test_brunel_plus_virtual_ranks(S, G):
     finally:
         for n in nets:
             n.free()
+
+
+def test_brunel_plus_teacher_forced_bursts(S):
+    """Steps with more spikes than one staging pass of the flattened delivery holds (2048
+    segments per tile per pass): forced bursts of 2500 spikes, weights, inputs and spike
+    trains still bit-exact against the oracle."""
+    cfg = _stronger_stdp(W.brunel_plus(3000, 0.1, seed=12))
+    rng = np.random.default_rng(3)
+    o = O.OracleNet(cfg)
+    with S.Network(cfg, record_steps=64, tile_width=384) as net:
+        for t in range(40):
+            if t % 7 == 3:
+                ids = np.sort(rng.choice(cfg.n, 2500, replace=False)).astype(np.uint32)
+                o.force_next(ids, "add")
+                net.force_next(ids, "add")
+            o.step(1)
+            net.step(1)
+        want = o.spikes()
+        got = net.read_spikes(0, 40)
+        assert all(np.array_equal(x, y) for x, y in zip(got, want))
+        assert max(len(x) for x in want) >= 2500
+        assert np.array_equal(net.weights(), np.maximum(o.weights(), 0))
+        for rel in range(cfg.delay + 1):
+            c1, p1 = net.input(rel)
+            c2, p2 = o.input(rel)
+            assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
