@@ -565,6 +565,8 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     n->D = c->delay_steps + 1; n->rank = c->rank; n->G = c->world_size;
     n->S = c->slice_width ? c->slice_width : spice_default_slice_width(c->n_neurons, c->world_size);
     n->flags = c->flags; n->R = c->record_steps; n->dt = c->dt_ms; n->activity = c->activity;
+    // Brunel+ reads step t's bitmap while the same launch writes step t + 1's: two slots
+    if (n->model == SPICE_BRUNEL_PLUS && n->R < 2) n->R = 2;
     n->seed = c->seed; n->device = c->device;
     n->dev_alloc = c->dev_alloc; n->dev_free = c->dev_free; n->alloc_ctx = c->alloc_ctx;
     n->external = (c->flags & SPICE_FLAG_EXTERNAL_EXCHANGE) != 0;

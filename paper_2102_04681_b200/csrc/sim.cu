@@ -732,27 +732,45 @@ __device__ __forceinline__ void stdp_traces(const SimArgs &a, uint64_t t, uint32
     }
 }
 
-// (ii)+(iii) depression and delivery of the step's spikes into tile b, over the flattened
-// (segment, entry) event space of the tile: the segments of up to kPlSeg spikes at a time
-// are staged in shared memory (entry start, length, source flags), their lengths scanned,
-// and every thread takes events f = tid, tid + kBlock, ... (U in flight, all loads issued
-// before any update): consecutive events of a segment are consecutive threads, so the
-// entry and weight loads coalesce, and a tile's ~10^3-10^4 events per step are spread over
-// all 1024 threads instead of one lane group per segment.  Plastic synapses (weight >= 0;
-// static ones hold the sentinel -1) are depressed, stored and delivered as fixed point
-// rint(w 2^32) accumulated exactly in two u32 shared words (low word with carry detection
-// from the returned old value: native 32-bit shared atomics, no 64-bit CAS loop); static
-// synapses add their packed receptor count.
-constexpr uint32_t kPlSeg = 2048;                     // segments staged per pass
+// Global spike bit of source j in the gathered bitmaps of step t (Listing 1 inverse).
+__device__ __forceinline__ bool spiked_global(const SimArgs &a, const uint32_t *gbm, uint32_t j) {
+    if (a.G == 1) return (gbm[j >> 5] >> (j & 31)) & 1u;
+    const uint32_t r = (j / a.S) % a.G, il = (j / a.S / a.G) * a.S + j % a.S;
+    return (gbm[(uint64_t)r * a.W + (il >> 5)] >> (il & 31)) & 1u;
+}
+
+// (i)-(iii) of a step for tile b as ONE flattened event space spread over all threads:
+//   delivery events: every (segment, entry) of the step's spiking rows into tile b.
+//     Consecutive events of a segment are consecutive threads (entry and weight loads
+//     coalesce).  A plastic synapse (weight >= 0; static ones hold the sentinel -1) whose
+//     post neuron also spiked at t is first potentiated (w = min(w_max, w + A+ x_pre(t))),
+//     then depressed (w = max(0, w - A- y_post(t))), stored and delivered as fixed point
+//     rint(w 2^32), summed exactly in two u32 shared words (low word with carry detection
+//     from the returned old value: native 32-bit shared atomics, no 64-bit CAS loop);
+//     static synapses add their packed receptor count.
+//   potentiation events: CTA b's equal share of the step's global (post spike, plastic
+//     in-synapse) space, so a tile with many post spikes does not stall the step.  The
+//     in-synapses whose pre neuron also spiked at t are skipped here (their delivery
+//     event potentiates them first), so the two event sets touch disjoint weights and
+//     need no ordering: every weight sees exactly the eager oracle's operations in its
+//     order (reading R13).
+// Segments are staged kPlSeg spikes per pass; a step with more spikes than one pass holds
+// falls back to tile-local potentiation (potentiate_tile) before the delivery passes.
+constexpr uint32_t kPlSeg = 1900;                     // spikes staged per pass (6 words each)
 constexpr uint32_t kPlU = 4;                          // events in flight per thread
 
-__device__ __forceinline__ void plastic_event(const SimArgs &a, uint32_t *cnt, uint32_t *plo, uint32_t *phi,
-                                              const float *ys, uint32_t e, uint32_t off, uint32_t fl, float wv) {
-    if (wv >= 0.0f) {                                // plastic: depress (reading R13 (ii)), then deliver
-        float nw = __fsub_rn(wv, __fmul_rn(a.mc.Am, ys[off]));
+__device__ __forceinline__ void plastic_deliver(const SimArgs &a, uint32_t *cnt, uint32_t *plo, uint32_t *phi,
+                                                const float *ys, const uint32_t *tb, uint32_t e, uint32_t off,
+                                                uint32_t fl, float wv, float xpre, bool pot_first) {
+    if (wv >= 0.0f) {
+        if (pot_first && ((tb[off >> 5] >> (off & 31)) & 1u)) {   // post spiked at t as well: (i) first
+            const float pw = __fadd_rn(wv, __fmul_rn(a.mc.Ap, xpre));
+            wv = pw < a.mc.wmax ? pw : a.mc.wmax;
+        }
+        float nw = __fsub_rn(wv, __fmul_rn(a.mc.Am, ys[off]));     // (ii)
         nw = nw > 0.0f ? nw : 0.0f;
         a.w[e] = nw;
-        const uint64_t q = (uint64_t)__double2ll_rn((double)nw * 4294967296.0);
+        const uint64_t q = (uint64_t)__double2ll_rn((double)nw * 4294967296.0);   // (iii)
         const uint32_t lo = (uint32_t)q, hi = (uint32_t)(q >> 32);
         const uint32_t old = atomicAdd(&plo[off], lo);
         const uint32_t carry = old + lo < old ? 1u : 0u;
@@ -762,25 +780,35 @@ __device__ __forceinline__ void plastic_event(const SimArgs &a, uint32_t *cnt, u
     }
 }
 
-__device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b, uint32_t *cnt,
-                                                         uint32_t *plo, uint32_t *phi, uint32_t *pref, uint32_t *tmp,
-                                                         uint32_t *stage, float *ys, bool marks = false) {
+struct PlasticSmem { uint32_t *cnt, *plo, *phi; float *ys; uint32_t *tb, *pref, *tmp, *stage; };
+
+__device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b,
+                                                         const PlasticSmem &sm, bool marks = false) {
     const uint32_t tid = threadIdx.x;
     const uint32_t par = (uint32_t)(t & 1);
-    potentiate_tile(a, t, b, stage, tmp);
-    __syncthreads();
-    if (marks) phase_mark(a, 2);
+    uint32_t *pref = sm.pref, *tmp = sm.tmp, *stage = sm.stage;
+    const uint32_t *bm = step_bitmap(a, t);
+    const uint32_t *gbm = a.record + mod32(t, a.record_steps) * (uint64_t)a.G * a.W;
+    const float *xo = a.xtr + (t & 1) * (uint64_t)a.N;
     for (uint32_t r = tid; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
-    // the tile's post traces y in shared memory for the depression
-    for (uint32_t x = tid; x < a.TW; x += kBlock) ys[x] = b * a.TW + x < a.n_own ? a.ytr[b * a.TW + x] : 0.0f;
+    // the tile's post traces y and post spike bits of step t
+    for (uint32_t x = tid; x < a.TW; x += kBlock) sm.ys[x] = b * a.TW + x < a.n_own ? a.ytr[b * a.TW + x] : 0.0f;
+    for (uint32_t x = tid; x < a.TW / 32; x += kBlock) sm.tb[x] = b * a.TW + 32 * x < a.n_own ? bm[b * a.TW / 32 + x] : 0u;
     __syncthreads();
-    block_exclusive_scan(pref, a.NR, tmp);       // (its barriers also order (i) before (ii))
-    if (marks) phase_mark(a, 3);
+    block_exclusive_scan(pref, a.NR, tmp);
     const uint32_t n_sp = pref[a.NR];
+    const bool merged = n_sp <= kPlSeg;
+    if (!merged) {                                    // (i) tile-local, before every delivery pass
+        potentiate_tile(a, t, b, stage, tmp);
+        __syncthreads();
+    }
+    if (marks) phase_mark(a, 2);
     const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
-    uint32_t *sst = stage, *slen = stage + kPlSeg, *sfl = stage + 2 * kPlSeg + 1;   // (stage: 3 kPlSeg + 1 words)
+    uint32_t *sst = stage, *slen = stage + kPlSeg, *sfl = stage + 2 * kPlSeg + 1;
+    float *sx = reinterpret_cast<float *>(stage + 3 * kPlSeg + 1);
+    uint32_t *spre = stage + 4 * kPlSeg + 1, *sinb = stage + 5 * kPlSeg + 2;
     uint32_t delivered = 0;
-    for (uint32_t q0 = 0; q0 < n_sp; q0 += kPlSeg) {
+    for (uint32_t q0 = 0; q0 < max(n_sp, 1u); q0 += kPlSeg) {
         const uint32_t nq = min(kPlSeg, n_sp - q0);
         __syncthreads();                          // previous pass done with the staging
         for (uint32_t q = tid; q < nq; q += kBlock) {
@@ -790,38 +818,80 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
             const uint32_t s = a.sl_ids[slot];
             const uint32_t *bp = a.bnd + (uint64_t)s * (a.NT + 1u) + b;
             const uint32_t lo = bp[0], hi = bp[1];
+            const bool pls = plastic_src(a, s);
             sst[q] = (uint32_t)(a.sl_rows[slot] + lo);
             slen[q] = hi - lo;
-            sfl[q] = (s >= a.n_exc ? 1u : 0u) | (plastic_src(a, s) ? 2u : 0u);
+            sfl[q] = (s >= a.n_exc ? 1u : 0u) | (pls ? 2u : 0u);
+            sx[q] = pls ? xo[s] : 0.0f;
+            uint32_t indeg = 0, inb = 0;
+            if (merged && (a.G == 1 || (s / a.S) % a.G == a.rank)) {     // owned post neuron
+                const uint32_t li = a.G == 1 ? s : (s / a.S / a.G) * a.S + s % a.S;
+                inb = (uint32_t)a.in_ptr[li];
+                indeg = (uint32_t)a.in_ptr[li + 1] - inb;
+            }
+            spre[q] = indeg;
+            sinb[q] = inb;
         }
         __syncthreads();
-        block_exclusive_scan(slen, nq, tmp);      // slen -> event prefix, slen[nq] = events
+        block_exclusive_scan(slen, nq, tmp);      // slen -> delivery-event prefix
+        if (merged) block_exclusive_scan(spre, nq, tmp);    // spre -> potentiation-event prefix
+        if (marks) phase_mark(a, 3);
         const uint32_t ne = slen[nq];
+        uint32_t p0 = 0, np = 0;
+        if (merged) {                             // this CTA's share of the step's potentiation
+            const uint32_t ep = spre[nq];
+            p0 = (uint32_t)((uint64_t)ep * blockIdx.x / gridDim.x);
+            np = (uint32_t)((uint64_t)ep * (blockIdx.x + 1) / gridDim.x) - p0;
+        }
         if (tid == 0) delivered += ne;
-        for (uint32_t f0 = tid; f0 < ne; f0 += kBlock * kPlU) {
-            uint32_t e[kPlU], off[kPlU], fl[kPlU];
-            float wv[kPlU];
+        const uint32_t total = ne + np;
+        for (uint32_t f0 = tid; f0 < total; f0 += kBlock * kPlU) {
+            uint32_t e[kPlU], x1[kPlU], fl[kPlU];
+            float wv[kPlU], xv[kPlU];
+            bool skip[kPlU];
 #pragma unroll
-            for (uint32_t u = 0; u < kPlU; ++u) {
+            for (uint32_t u = 0; u < kPlU; ++u) {     // indices (shared memory) + first loads
                 const uint32_t f = f0 + u * kBlock;
-                e[u] = 0xFFFFFFFFu;
+                fl[u] = 0xFFFFFFFFu;                  // none
                 if (f < ne) {
-                    uint32_t l = 0, h = nq;                  // largest q with slen[q] <= f
+                    uint32_t l = 0, h = nq;           // largest q with slen[q] <= f
                     while (h - l > 1) { const uint32_t m = (l + h) >> 1; if (slen[m] <= f) l = m; else h = m; }
                     e[u] = sst[l] + (f - slen[l]);
                     fl[u] = sfl[l];
+                    xv[u] = sx[l];
+                    x1[u] = a.ent[e[u]];
+                    wv[u] = (fl[u] & 2u) ? a.w[e[u]] : -1.0f;
+                } else if (f < total) {
+                    const uint32_t g = p0 + (f - ne);
+                    uint32_t l = 0, h = nq;           // largest q with spre[q] <= g
+                    while (h - l > 1) { const uint32_t m = (l + h) >> 1; if (spre[m] <= g) l = m; else h = m; }
+                    const uint32_t ein = sinb[l] + (g - spre[l]);
+                    fl[u] = 4u;                       // potentiation event
+                    e[u] = a.in_pos[ein];
+                    x1[u] = a.in_src[ein];
                 }
             }
 #pragma unroll
-            for (uint32_t u = 0; u < kPlU; ++u)
-                if (e[u] != 0xFFFFFFFFu) {
-                    off[u] = a.ent[e[u]];
-                    wv[u] = (fl[u] & 2u) ? a.w[e[u]] : -1.0f;
+            for (uint32_t u = 0; u < kPlU; ++u)       // potentiation: second-level loads
+                if (fl[u] == 4u) {
+                    skip[u] = spiked_global(a, gbm, x1[u]);
+                    wv[u] = a.w[e[u]];
+                    xv[u] = xo[x1[u]];
                 }
 #pragma unroll
-            for (uint32_t u = 0; u < kPlU; ++u)
-                if (e[u] != 0xFFFFFFFFu) plastic_event(a, cnt, plo, phi, ys, e[u], off[u], fl[u], wv[u]);
+            for (uint32_t u = 0; u < kPlU; ++u) {
+                if (fl[u] == 0xFFFFFFFFu) continue;
+                if (fl[u] == 4u) {
+                    if (!skip[u]) {
+                        const float nw = __fadd_rn(wv[u], __fmul_rn(a.mc.Ap, xv[u]));
+                        a.w[e[u]] = nw < a.mc.wmax ? nw : a.mc.wmax;
+                    }
+                } else {
+                    plastic_deliver(a, sm.cnt, sm.plo, sm.phi, sm.ys, sm.tb, e[u], x1[u], fl[u], wv[u], xv[u], merged);
+                }
+            }
         }
+        if (n_sp == 0) break;
     }
     __syncthreads();
     if (marks) phase_mark(a, 4);
@@ -876,9 +946,8 @@ size_t tile_smem_bytes(uint32_t TW, uint32_t NR) {
 // ([TW] each), region prefix, scan tmp, staging.
 size_t plastic_smem_bytes(uint32_t TW, uint32_t NR) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
-    return ((size_t)4 * tw4 + ((NR + 1 + 3) & ~3u) + 32 + kStageWords) * 4 + 16;
+    return ((size_t)4 * tw4 + ((TW / 32 + 3) & ~3u) + ((NR + 1 + 3) & ~3u) + 32 + kStageWords) * 4 + 16;
 }
-struct PlasticSmem { uint32_t *cnt, *plo, *phi; float *ys; uint32_t *pref, *tmp, *stage; };
 __device__ __forceinline__ PlasticSmem carve_plastic(const SimArgs &a, uint32_t *smem) {
     PlasticSmem sm;
     const uint32_t tw4 = (a.TW + 3u) & ~3u;
@@ -886,7 +955,8 @@ __device__ __forceinline__ PlasticSmem carve_plastic(const SimArgs &a, uint32_t 
     sm.plo = smem + tw4;
     sm.phi = smem + 2 * tw4;
     sm.ys = reinterpret_cast<float *>(smem + 3 * tw4);
-    sm.pref = smem + 4 * tw4;
+    sm.tb = smem + 4 * tw4;
+    sm.pref = sm.tb + ((a.TW / 32 + 3) & ~3u);
     sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
     sm.stage = sm.tmp + 32;
     return sm;
@@ -952,7 +1022,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver_plastic(SimArgs a, uint32_t 
     const uint64_t t = *a.t0 + k;
     const uint32_t b = blockIdx.x;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.plo[x] = 0u; sm.phi[x] = 0u; }
-    const uint32_t d = deliver_tile_plastic(a, t, b, sm.cnt, sm.plo, sm.phi, sm.pref, sm.tmp, sm.stage, sm.ys);
+    const uint32_t d = deliver_tile_plastic(a, t, b, sm);
     plastic_flush(a, t, b, sm);
     store_delivered(a, b, d, sm.tmp);
 }
@@ -1003,7 +1073,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         phase_mark(a, 0);
         if (threadIdx.x == 0) s_count3 = 0;
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.plo[x] = 0u; sm.phi[x] = 0u; }
-        const uint32_t d = deliver_tile_plastic(a, t, b, sm.cnt, sm.plo, sm.phi, sm.pref, sm.tmp, sm.stage, sm.ys, true);
+        const uint32_t d = deliver_tile_plastic(a, t, b, sm, true);
         plastic_flush(a, t, b, sm);
         store_delivered(a, b, d, sm.tmp);
         __syncthreads();

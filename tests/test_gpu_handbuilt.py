@@ -93,7 +93,7 @@ def test_isi_constant_drive(S, kw):
 def test_coincidence_window(S, gap, fires, kw):
     """Reading R6: two 12 mV inputs into a neuron at rest fire it iff the gap <= 80 steps."""
     cfg = _cfg(W.BRUNEL, 2, 2, [W.Rule((0, 1), (1, 2), W.FIXED_PROB, 1.0)], _bp(JE=12.0))
-    got, _, _ = _run_both(S, cfg, gap + 5, lambda t: ([0], "replace") if t in (0, gap) else ([], "replace"), kw)
+    got, _, _ = _run_both(S, cfg, gap + 5, lambda t: ([0], "replace") if t in (0, gap) else None, kw)
     assert any(1 in s for s in got) == fires
 
 
