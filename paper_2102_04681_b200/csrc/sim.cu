@@ -844,7 +844,15 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
             np = (uint32_t)((uint64_t)ep * (blockIdx.x + 1) / gridDim.x) - p0;
         }
         if (tid == 0) delivered += ne;
-        const uint32_t total = ne + np;
+#ifdef SPICE_ABLATE_POT                               // diagnostics builds only (tools/phases.py)
+        np = 0;
+#endif
+#ifdef SPICE_ABLATE_DEL
+        const uint32_t ne_eff = 0;
+#else
+        const uint32_t ne_eff = ne;
+#endif
+        const uint32_t total = ne_eff + np;
         for (uint32_t f0 = tid; f0 < total; f0 += kBlock * kPlU) {
             uint32_t e[kPlU], x1[kPlU], fl[kPlU];
             float wv[kPlU], xv[kPlU];
@@ -853,7 +861,7 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
             for (uint32_t u = 0; u < kPlU; ++u) {     // indices (shared memory) + first loads
                 const uint32_t f = f0 + u * kBlock;
                 fl[u] = 0xFFFFFFFFu;                  // none
-                if (f < ne) {
+                if (f < ne_eff) {
                     uint32_t l = 0, h = nq;           // largest q with slen[q] <= f
                     while (h - l > 1) { const uint32_t m = (l + h) >> 1; if (slen[m] <= f) l = m; else h = m; }
                     e[u] = sst[l] + (f - slen[l]);
@@ -862,7 +870,7 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
                     x1[u] = a.ent[e[u]];
                     wv[u] = (fl[u] & 2u) ? a.w[e[u]] : -1.0f;
                 } else if (f < total) {
-                    const uint32_t g = p0 + (f - ne);
+                    const uint32_t g = p0 + (f - ne_eff);
                     uint32_t l = 0, h = nq;           // largest q with spre[q] <= g
                     while (h - l > 1) { const uint32_t m = (l + h) >> 1; if (spre[m] <= g) l = m; else h = m; }
                     const uint32_t ein = sinb[l] + (g - spre[l]);

@@ -6,7 +6,8 @@ import sys
 os.environ["SPICE_PHASES"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 # the phase clocks are compiled out of the product library: build a variant with them
-_VARIANT = "/tmp/libspice_phases.so"
+_EXTRA = [d for d in os.environ.get("SPICE_DEFINES", "").split(",") if d]
+_VARIANT = "/tmp/libspice_phases%s.so" % ("_" + "_".join(_EXTRA) if _EXTRA else "")
 if "SPICE_LIB" not in os.environ:
     import importlib.util  # noqa: E402
     _spec = importlib.util.spec_from_file_location(
@@ -14,7 +15,7 @@ if "SPICE_LIB" not in os.environ:
                                      "paper_2102_04681_b200", "build.py"))
     _B = importlib.util.module_from_spec(_spec)
     _spec.loader.exec_module(_B)                   # (not via the package: it loads the library)
-    _B.build(out=_VARIANT, defines=["SPICE_PHASES_BUILD=1"])
+    _B.build(out=_VARIANT, defines=["SPICE_PHASES_BUILD=1"] + _EXTRA)
     os.environ["SPICE_LIB"] = _VARIANT
 import numpy as np  # noqa: E402
 
