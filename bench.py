@@ -56,6 +56,11 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=1024)
     ap.add_argument("--e2e-chunk", type=int, default=32, help="steps per spice_step call in the e2e leg")
     ap.add_argument("--no-parity", action="store_true", help="skip the in-run oracle check (synth)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="G > 1 spike exchange: device-initiated stores into peer windows (default) "
+                         "or an NCCL all-gather inside the step graph")
+    ap.add_argument("--same-device", action="store_true",
+                    help="tests only: every rank on cuda:0 (host collectives over gloo)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--setup", action="store_true",
@@ -237,9 +242,14 @@ def main_spice(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2102_04681_b200 import build as B
     if local == 0:                                 # one build per node; the others wait
         B.build()
@@ -249,7 +259,8 @@ def main_spice(args):
 
     cfg, wl = workload(args.workload, world, args.scaling)
     nccl_id = None
-    if world > 1:
+    peer = world > 1 and args.exchange == "peer"
+    if world > 1 and not peer:
         obj = [S.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
@@ -257,7 +268,12 @@ def main_spice(args):
     t0 = time.perf_counter()
     net = S.Network(cfg, rank=rank, world_size=world, device=local, nccl_id=nccl_id,
                     record_steps=record, global_atomics=args.global_atomics,
-                    tile_width=args.tile_width, ctas_per_tile=args.ctas_per_tile, unfused=args.unfused)
+                    tile_width=args.tile_width, ctas_per_tile=args.ctas_per_tile, unfused=args.unfused,
+                    exchange=S.EXCHANGE_PEER if peer else S.EXCHANGE_NCCL)
+    if peer:                                       # map every rank's receive window
+        handles = [None] * world
+        dist.all_gather_object(handles, net.peer_handle())
+        net.peer_connect(handles)
     setup_s = time.perf_counter() - t0
     info = net.info()
 
@@ -270,7 +286,7 @@ def main_spice(args):
     def allreduce(x, op):
         if world == 1:
             return x
-        t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([float(x)], dtype=torch.float64, device="cpu" if args.same_device else "cuda")
         dist.all_reduce(t, op=op)
         return t.item()
 
@@ -387,7 +403,10 @@ def main_spice(args):
                    "synapses_rank0": info["n_synapses"], "spikes_per_step": fired / args.steps,
                    "events_per_step": events / args.steps,
                    "parallelism": f"model-parallel strided neuron slices x{world}",
-                   "exchange": "NCCL all-gather of spike bitmaps in the step graph" if world > 1 else None,
+                   "exchange": (None if world == 1 else
+                                "device-initiated: update kernel stores bitmap words into every rank's window, "
+                                "flag release/acquire kernels (no host round trip)" if peer else
+                                "NCCL all-gather of spike bitmaps in the step graph"),
                    "delivery": delivery,
                    "l2": "no flush: synapse stream per step >> 126 MB L2 is read from 12 GB/GPU",
                    "setup_s": setup_s},

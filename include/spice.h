@@ -306,6 +306,23 @@ SPICE_API spice_status spice_exchange_end_fused(spice_net *net);
  * (both handles on the same device; ordered after src's update; returns when done). */
 SPICE_API spice_status spice_exchange_put(spice_net *dst, spice_net *src);
 
+/* PEER exchange (spice_config.exchange = SPICE_EXCHANGE_PEER, world_size > 1): the
+ * device-initiated spike synchronisation (§III-D/E, "the
+ * spike synchronization time is entirely dominated by CUDA API overhead").  Every rank owns a
+ * receive window of 2 x G x W words (step parity x rank x bitmap word) plus G arrival flags;
+ * the neuron-update kernel stores its bitmap words straight into all G windows (NVLink /
+ * NVSwitch stores through CUDA IPC mappings, or plain stores on the same GPU), a one-thread
+ * kernel then releases this rank's flag for the step in every window, and before
+ * bitmap->list each rank's one-thread wait kernel acquires all G flags.  No host round trip
+ * and no library call per step.  Setup: create every rank, get each rank's 128-byte handle
+ * with spice_peer_handle, all-gather them (rank order) with any host transport, and pass
+ * the G x 128 bytes to spice_peer_connect, which maps the peers' windows and captures the
+ * step graphs; spice_step returns ESTATE until then.  Ranks of one process may share a GPU
+ * (the handle carries the process ID; same-process windows are used directly).  A peer
+ * that stalls > 20 s makes the next synchronising call return SPICE_ENCCL. */
+SPICE_API spice_status spice_peer_handle(spice_net *net, void *out128);
+SPICE_API spice_status spice_peer_connect(spice_net *net, const void *handles);
+
 /* ------------------- static partition (host-only, no GPU needed) -------------- */
 /* PAPER.md §III-F P:376 strided slices, Listing 1 P:496 (reading R1). */
 SPICE_API uint32_t spice_partition_owner(uint64_t j, uint32_t world_size, uint32_t slice_width);

@@ -2,6 +2,7 @@
 // include/spice.h.  Host-side runtime of the B200 Spice hot path.
 #include <dlfcn.h>
 #include <nccl.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -145,6 +146,13 @@ struct spice_net {
     void *alloc_ctx = nullptr;
     bool poisoned = false;
     bool external = false;
+    // PEER exchange: receive window (cudaMalloc: IPC-exportable), the G windows' addresses
+    // (device array), the mappings opened here, and the device error flag of the wait kernel
+    bool peer = false, connected = true;
+    uint32_t *win = nullptr;
+    uint32_t **peers_dev = nullptr;
+    std::vector<void *> opened;
+    uint32_t *xerr = nullptr;
     // geometry
     uint64_t n_own = 0, n_own_max = 0;
     uint32_t W = 0, TW = 32, NT = 1, C = 1, TWs = 32;
@@ -341,26 +349,47 @@ spice_status enqueue_steps(spice_net *n, uint32_t steps, cudaStream_t s) {
         CU(n, launch_update(a, 0, s));
         for (uint32_t k = 0; k + 1 < steps; ++k) CU(n, launch_fused(a, k, s));   // deliver(k)+update(k+1)
         CU(n, launch_deliver(a, steps - 1, false, n->n_sm, s));
-    } else if (n->G > 1 && n->fused && !n->global_atomics) {
-        // G > 1, padded layout: update(0), then per step all-gather(t) -> bitmap->list +
-        // descriptors(t) -> fused deliver(t)+update(t+1); the last step delivers unfused
-        CU(n, launch_update(a, 0, s));
-        for (uint32_t k = 0; k < steps; ++k) {
-            ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, s);
-            if (r != ncclSuccess) return fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
-            CU(n, launch_bitmap_to_list(a, k, s));
-            if (k + 1 < steps) CU(n, launch_fused(a, k, s));
-            else CU(n, launch_deliver(a, k, false, n->n_sm, s));
-        }
     } else {
-        for (uint32_t k = 0; k < steps; ++k) {
-            CU(n, launch_update(a, k, s));
-            if (n->G > 1) {
+        // G > 1: the exchange of step k's bitmaps (NCCL all-gather, or the PEER flags wait:
+        // the bitmap words were stored into every window by the update) and bitmap->list
+        const bool peer = n->peer;
+        auto xchg = [&](uint32_t k) -> spice_status {
+            if (peer) CU(n, launch_peer_wait(a, k, s));
+            else {
                 ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, s);
                 if (r != ncclSuccess) return fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
-                CU(n, launch_bitmap_to_list(a, k, s));
             }
-            CU(n, launch_deliver(a, k, n->global_atomics, n->n_sm, s));
+            CU(n, launch_bitmap_to_list(a, k, s));
+            return SPICE_OK;
+        };
+        auto publish = [&](uint32_t k) -> spice_status {   // after the update of step k (PEER)
+            if (peer) CU(n, launch_peer_signal(a, k, s));
+            return SPICE_OK;
+        };
+        spice_status st;
+        if (n->G > 1 && n->fused && !n->global_atomics) {
+            // padded layout: update(0), then per step exchange(t) -> bitmap->list + descriptors(t)
+            // -> fused deliver(t)+update(t+1); the last step delivers unfused
+            CU(n, launch_update(a, 0, s));
+            if ((st = publish(0))) return st;
+            for (uint32_t k = 0; k < steps; ++k) {
+                if ((st = xchg(k))) return st;
+                if (k + 1 < steps) {
+                    CU(n, launch_fused(a, k, s));
+                    if ((st = publish(k + 1))) return st;
+                } else {
+                    CU(n, launch_deliver(a, k, false, n->n_sm, s));
+                }
+            }
+        } else {
+            for (uint32_t k = 0; k < steps; ++k) {
+                CU(n, launch_update(a, k, s));
+                if (n->G > 1) {
+                    if ((st = publish(k))) return st;
+                    if ((st = xchg(k))) return st;
+                }
+                CU(n, launch_deliver(a, k, n->global_atomics, n->n_sm, s));
+            }
         }
     }
     CU(n, launch_advance(n->t0, steps, s));
@@ -384,6 +413,8 @@ void destroy(spice_net *n) {
     if (!n) return;
     if (n->stream) cudaStreamSynchronize(n->stream);
     for (cudaGraphExec_t &g : n->graphs) if (g) cudaGraphExecDestroy(g);
+    for (void *p : n->opened) cudaIpcCloseMemHandle(p);
+    if (n->win) cudaFree(n->win);
     if (n->comm) nccl().CommDestroy(n->comm);
     for (void *p : n->allocs) release(n, p);
     n->allocs.clear();
@@ -573,8 +604,11 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     n->prm.assign(c->model_params, c->model_params + c->n_model_params);
     n->rules.assign(c->rules, c->rules + c->n_rules);
     auto bail = [&](spice_status s) { destroy(n); return s; };
-    if (n->G > 1 && !n->external && !c->nccl_unique_id)
-        return bail(fail(n, SPICE_EINVAL, "world_size > 1 needs nccl_unique_id or EXTERNAL_EXCHANGE"));
+    if (c->exchange != SPICE_EXCHANGE_NCCL && c->exchange != SPICE_EXCHANGE_PEER)
+        return bail(fail(n, SPICE_EINVAL, "unknown exchange %u", c->exchange));
+    n->peer = n->G > 1 && !n->external && c->exchange == SPICE_EXCHANGE_PEER;
+    if (n->G > 1 && !n->external && !n->peer && !c->nccl_unique_id)
+        return bail(fail(n, SPICE_EINVAL, "world_size > 1 needs nccl_unique_id, SPICE_EXCHANGE_PEER or EXTERNAL_EXCHANGE"));
     {
         cudaError_t e = cudaSetDevice(n->device);
         if (e) return bail(fail(n, SPICE_ECUDA, "cudaSetDevice(%d): %s", n->device, cudaGetErrorString(e)));
@@ -648,7 +682,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (n->model == SPICE_BRUNEL_PLUS && plastic_smem_bytes(n->TW, n->NR) > smem_max)
         return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for the Brunel+ tile kernels", n->TW));
     // ---- NCCL communicator ----
-    if (n->G > 1 && !n->external) {
+    if (n->G > 1 && !n->external && !n->peer) {
         if (!nccl().ok) return bail(fail(n, SPICE_ENCCL, "libnccl.so.2 not found (set SPICE_NCCL_LIB)"));
         ncclUniqueId id;
         memcpy(&id, c->nccl_unique_id, sizeof id);
@@ -786,7 +820,22 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // the caller's stream may still be running work of its own: everything the library
     // enqueued on it so far (memsets, generator) is done; capture never touches it
     CU(n, cudaStreamSynchronize(s));
-    if (!n->external)
+    if (n->peer) {
+        // receive window: 2 parities x G x W bitmap words + G u64 flags; device memory from
+        // cudaMalloc (exportable through CUDA IPC), released in destroy
+        const size_t wb = (2ull * n->G * n->W + 2ull * n->G + 2) * 4;
+        cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&n->win), wb);
+        if (e != cudaSuccess) { cudaGetLastError(); return bail(fail(n, SPICE_ENOMEM, "cudaMalloc of the %zu-byte peer window failed", wb)); }
+        CU(n, cudaMemset(n->win, 0, wb));
+        if ((st = dalloc_t(n, &n->peers_dev, n->G, "peer window table"))) return bail(st);
+        if ((st = dalloc_t(n, &n->xerr, 1, "exchange error flag"))) return bail(st);
+        CU(n, cudaMemset(n->xerr, 0, 4));
+        n->args.gather = n->win;
+        n->args.peers = n->peers_dev;
+        n->args.xerr = n->xerr;
+        n->connected = false;                              // graphs are captured by spice_peer_connect
+    }
+    if (!n->external && !n->peer)
         for (uint32_t k = 0; k < spice_net::kGraphLevels; ++k)
             if ((st = capture_graph(n, 1u << k, &n->graphs[k]))) return bail(st);
     n->create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_create).count();
@@ -804,6 +853,7 @@ spice_status spice_setup_times(spice_net *n, double *gen_ms, double *create_ms) 
 spice_status spice_step(spice_net *n, uint64_t steps) {
     CHECK_NET(n);
     if (n->external) return fail(n, SPICE_ESTATE, "external-exchange networks step via spice_exchange_begin/end");
+    if (!n->connected) return fail(n, SPICE_ESTATE, "PEER exchange: call spice_peer_connect first");
     while (steps) {                                        // largest graph first
         uint32_t k = spice_net::kGraphLevels - 1;
         while ((1ull << k) > steps) --k;
@@ -811,6 +861,70 @@ spice_status spice_step(spice_net *n, uint64_t steps) {
         steps -= 1ull << k;
         n->t_host += 1ull << k;
     }
+    return SPICE_OK;
+}
+
+namespace {
+struct PeerBlob {                 // spice_peer_handle's 128 bytes
+    cudaIpcMemHandle_t ipc;       // 64
+    uint64_t pid;
+    uint64_t ptr;                 // the window's address in the exporting process
+    int32_t device;
+    uint32_t magic, rank, G, W, pad[7];
+};
+static_assert(sizeof(PeerBlob) == 128, "peer handle size");
+constexpr uint32_t kPeerMagic = 0x45435053u;   // "SPCE"
+
+// PEER exchange errors surface at the next host synchronisation
+spice_status check_xerr(spice_net *n) {
+    if (!n->xerr) return SPICE_OK;
+    uint32_t e = 0;
+    CU(n, cudaMemcpy(&e, n->xerr, 4, cudaMemcpyDeviceToHost));
+    if (e) return fail(n, SPICE_ENCCL, "PEER exchange: rank %u's bitmap did not arrive within 20 s", e - 1);
+    return SPICE_OK;
+}
+}  // namespace
+
+spice_status spice_peer_handle(spice_net *n, void *out128) {
+    CHECK_NET(n);
+    if (!n->peer || !out128) return fail(n, SPICE_EINVAL, "not a PEER-exchange network (or null output)");
+    PeerBlob b{};
+    CU(n, cudaIpcGetMemHandle(&b.ipc, n->win));
+    b.pid = (uint64_t)getpid();
+    b.ptr = (uint64_t)(uintptr_t)n->win;
+    b.device = n->device;
+    b.magic = kPeerMagic;
+    b.rank = n->rank;
+    b.G = n->G;
+    b.W = n->W;
+    memcpy(out128, &b, sizeof b);
+    return SPICE_OK;
+}
+
+spice_status spice_peer_connect(spice_net *n, const void *handles) {
+    CHECK_NET(n);
+    if (!n->peer || !handles) return fail(n, SPICE_EINVAL, "not a PEER-exchange network (or null handles)");
+    if (n->connected) return fail(n, SPICE_ESTATE, "already connected");
+    std::vector<uint32_t *> ptrs(n->G, nullptr);
+    for (uint32_t r = 0; r < n->G; ++r) {
+        PeerBlob b;
+        memcpy(&b, static_cast<const char *>(handles) + 128ull * r, sizeof b);
+        if (b.magic != kPeerMagic || b.rank != r || b.G != n->G || b.W != n->W)
+            return fail(n, SPICE_EINVAL, "peer handle %u is not rank %u of this %u-rank network", r, r, n->G);
+        if (r == n->rank) { ptrs[r] = n->win; continue; }
+        if (b.pid == (uint64_t)getpid()) { ptrs[r] = reinterpret_cast<uint32_t *>(b.ptr); continue; }   // same process
+        void *p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, b.ipc, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return fail(n, SPICE_ECUDA, "cudaIpcOpenMemHandle(rank %u): %s", r, cudaGetErrorString(e));
+        n->opened.push_back(p);
+        ptrs[r] = static_cast<uint32_t *>(p);
+    }
+    CU(n, cudaMemcpy(n->peers_dev, ptrs.data(), n->G * sizeof(uint32_t *), cudaMemcpyHostToDevice));
+    for (uint32_t k = 0; k < spice_net::kGraphLevels; ++k) {
+        spice_status st = capture_graph(n, 1u << k, &n->graphs[k]);
+        if (st) return st;
+    }
+    n->connected = true;
     return SPICE_OK;
 }
 
@@ -883,6 +997,7 @@ spice_status spice_read_spikes(spice_net *n, uint64_t t_begin, uint64_t t_end, u
         t += run;
     }
     CU(n, cudaStreamSynchronize(n->stream));
+    if (spice_status xs = check_xerr(n)) return xs;
     std::vector<std::vector<uint32_t>> &per = n->hdec;
     const uint64_t tot = decode_steps(n->hbm, nsteps, words, n->G, n->W, n->S, per);
     if (total) *total = tot;
@@ -1117,7 +1232,7 @@ void *spice_stream(spice_net *n) { return n ? (void *)n->stream : nullptr; }
 spice_status spice_sync(spice_net *n) {
     CHECK_NET(n);
     CU(n, cudaStreamSynchronize(n->stream));
-    return SPICE_OK;
+    return check_xerr(n);
 }
 
 spice_status spice_info(spice_net *n, uint64_t *n_owned, uint64_t *n_syn, uint32_t *n_tiles,
@@ -1134,7 +1249,8 @@ spice_status spice_info(spice_net *n, uint64_t *n_owned, uint64_t *n_syn, uint32
 
 spice_status spice_profile(spice_net *n, uint64_t steps, double *ms, uint32_t cap, uint32_t *nk) {
     CHECK_NET(n);
-    if (n->external) return fail(n, SPICE_ESTATE, "profiling needs an NCCL or single-GPU network");
+    if (n->external) return fail(n, SPICE_ESTATE, "profiling needs an NCCL, PEER or single-GPU network");
+    if (!n->connected) return fail(n, SPICE_ESTATE, "PEER exchange: call spice_peer_connect first");
     if (!ms || cap < 4) return fail(n, SPICE_EINVAL, "need room for 4 timings");
     cudaStream_t s = n->stream;
     const SimArgs &a = n->args;
@@ -1155,17 +1271,28 @@ spice_status spice_profile(spice_net *n, uint64_t steps, double *ms, uint32_t ca
         cnt[slot] += 1;
         return SPICE_OK;
     };
+    // G > 1 exchange pieces: publish = this rank's arrival flags after an update (PEER);
+    // gather = NCCL all-gather or waiting for every rank's flags (PEER), then bitmap->list
+    auto publish = [&](uint32_t k) -> spice_status {
+        if (n->peer) CU(n, launch_peer_signal(a, k, s));
+        return SPICE_OK;
+    };
+    auto gather = [&]() -> spice_status {
+        if (n->peer) CU(n, launch_peer_wait(a, 0, s));
+        else {
+            ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, s);
+            if (r != ncclSuccess) return fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
+        }
+        CU(n, launch_bitmap_to_list(a, 0, s));
+        return SPICE_OK;
+    };
     // (1) unfused steps: update, [exchange], deliver
     for (uint64_t q = 0; q < steps; ++q) {
         spice_status st = timed(0, [&]() -> spice_status { CU(n, launch_update(a, 0, s)); return SPICE_OK; });
         if (st) return st;
         if (n->G > 1) {
-            st = timed(3, [&]() -> spice_status {
-                ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, s);
-                if (r != ncclSuccess) return fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
-                CU(n, launch_bitmap_to_list(a, 0, s));
-                return SPICE_OK;
-            });
+            if ((st = publish(0))) return st;
+            st = timed(3, gather);
             if (st) return st;
         }
         st = timed(1, [&]() -> spice_status { CU(n, launch_deliver(a, 0, n->global_atomics, n->n_sm, s)); return SPICE_OK; });
@@ -1198,22 +1325,18 @@ spice_status spice_profile(spice_net *n, uint64_t steps, double *ms, uint32_t ca
     // (2') G > 1: update(0), then all-gather + bitmap->list (exchange) and the fused kernel
     if (n->G > 1 && !n->external && n->fused && !n->global_atomics && steps > 0) {
         CU(n, launch_update(a, 0, s));
+        spice_status st0 = publish(0);
+        if (st0) return st0;
         for (uint64_t q = 0; q < steps; ++q) {
-            spice_status st = timed(3, [&]() -> spice_status {
-                ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, s);
-                if (r != ncclSuccess) return fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
-                CU(n, launch_bitmap_to_list(a, 0, s));
-                return SPICE_OK;
-            });
+            spice_status st = timed(3, gather);
             if (st) return st;
             st = timed(2, [&]() -> spice_status { CU(n, launch_fused(a, 0, s)); return SPICE_OK; });
             if (st) return st;
+            if ((st = publish(1))) return st;                // (step t + 1's bitmap, before the advance)
             CU(n, launch_advance(n->t0, 1, s));
             n->t_host += 1;
         }
-        ncclResult_t r = nccl().AllGather(n->sendbuf, n->gather, n->W, ncclUint32, n->comm, s);
-        if (r != ncclSuccess) return fail(n, SPICE_ENCCL, "ncclAllGather: %s", nccl().GetErrorString(r));
-        CU(n, launch_bitmap_to_list(a, 0, s));
+        if ((st0 = gather())) return st0;
         CU(n, launch_deliver(a, 0, false, n->n_sm, s));
         CU(n, launch_advance(n->t0, 1, s));
         n->t_host += 1;
@@ -1292,8 +1415,9 @@ uint64_t spice_launches(spice_net *n, uint64_t steps) {
 uint32_t spice_kernels_per_step(spice_net *n) {
     if (!n) return 0;
     if (n->G == 1 && n->fused && !n->global_atomics) return 1u;   // fused deliver(t)+update(t+1)
-    if (n->G > 1 && n->fused && !n->global_atomics) return 2u;    // bitmap_to_list, fused (+ NCCL's)
-    return n->G == 1 ? 2u : 3u;   // update, [bitmap_to_list], deliver (+ NCCL's own kernel)
+    const uint32_t px = n->peer ? 2u : 0u;                        // PEER: flag signal + wait kernels
+    if (n->G > 1 && n->fused && !n->global_atomics) return 2u + px;   // bitmap_to_list, fused (+ NCCL's)
+    return n->G == 1 ? 2u : 3u + px;   // update, [bitmap_to_list], deliver (+ NCCL's own kernel)
 }
 
 spice_status spice_free(spice_net *n) {

@@ -419,7 +419,12 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
         w |= __shfl_xor_sync(0xFFFFFFFFu, w, 2);
         w |= __shfl_xor_sync(0xFFFFFFFFu, w, 4);
         if ((lane & 7u) == 0 && x4 < span) {
-            bm[(lo + x4) >> 5] = w;
+            if (a.peers) {                                // PEER exchange: straight into every
+                const uint64_t o = ((uint64_t)(t & 1) * a.G + a.rank) * a.W + ((lo + x4) >> 5);
+                for (uint32_t r = 0; r < a.G; ++r) a.peers[r][o] = w;   // rank's window (NVLink stores)
+            } else {
+                bm[(lo + x4) >> 5] = w;
+            }
             if (bm_s) bm_s[x4 >> 5] = w;                  // (k_small: the step's bitmap in smem)
         }
         // append spikes to this tile's list region (warp-aggregated smem counter)
@@ -1305,7 +1310,7 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
     for (uint32_t q0 = 0; q0 < kB2LWords; q0 += kBlock) {
         const uint32_t idx = r * kB2LWords + q0 + threadIdx.x;
         const bool in = q0 + threadIdx.x < kB2LWords && idx < nw;
-        const uint32_t word = in ? a.gather[idx] : 0u;
+        const uint32_t word = in ? a.gather[(a.peers ? (uint64_t)par * nw : 0ull) + idx] : 0u;
         if (in) a.record[mod32(t, a.record_steps) * (uint64_t)nw + idx] = word;
         const uint32_t cnt = __popc(word), incl = warp_incl_scan(cnt);
         const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
@@ -1340,6 +1345,51 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
 }
 
 __global__ void k_advance(uint64_t *t0, uint32_t steps) { *t0 += steps; }
+
+// PEER exchange (device-initiated): after the kernel that
+// stored this rank's bitmap of step t into every rank's receive window, one thread
+// publishes "step t arrived" in every window's flag of this rank (system-scope release;
+// the kernel boundary has completed the bitmap stores).  The receiving side's k_peer_wait
+// spins (acquire) until all G flags show step t, so the spike union of step t is in its
+// window before bitmap->list reads it.  A peer that does not arrive within ~20 s sets
+// xerr instead of hanging the GPU (the host reports it as an exchange error).
+__device__ __forceinline__ unsigned long long *peer_flags(const SimArgs &a, uint32_t *win) {
+    return reinterpret_cast<unsigned long long *>(win + 2ull * a.G * a.W);
+}
+__global__ void k_peer_signal(SimArgs a, uint32_t k) {
+    const uint64_t t = *a.t0 + k;
+    asm volatile("fence.sc.sys;" ::: "memory");
+    for (uint32_t r = 0; r < a.G; ++r) {
+        unsigned long long *f = peer_flags(a, a.peers[r]) + a.rank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(f), "l"((unsigned long long)(t + 1)) : "memory");
+    }
+}
+__global__ void k_peer_wait(SimArgs a, uint32_t k) {
+    const uint64_t t = *a.t0 + k;
+    unsigned long long *f = peer_flags(a, a.gather);
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    for (uint32_t r = 0; r < a.G; ++r) {
+        while (true) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f + r) : "memory");
+            if (v >= t + 1) break;
+            unsigned long long now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (now - t_start > 20000000000ull) { *a.xerr = 1u + r; return; }
+            __nanosleep(200);
+        }
+    }
+    asm volatile("fence.sc.sys;" ::: "memory");
+}
+cudaError_t launch_peer_signal(const SimArgs &a, uint32_t k, cudaStream_t s) {
+    k_peer_signal<<<1, 1, 0, s>>>(a, k);
+    return cudaGetLastError();
+}
+cudaError_t launch_peer_wait(const SimArgs &a, uint32_t k, cudaStream_t s) {
+    k_peer_wait<<<1, 1, 0, s>>>(a, k);
+    return cudaGetLastError();
+}
 
 // ------------------------------------------------------------------ launchers
 template <typename K>

@@ -125,8 +125,12 @@ struct SimArgs {
     uint64_t dstride;        // descriptor slots per (parity, tile) list (>= owned neurons)
     uint32_t *dcount;        // [3] descriptors per list of step t at dcount[t % 3]
     uint32_t *record;        // record_steps * G * W words
-    uint32_t *sendbuf;       // W words (G > 1)
-    uint32_t *gather;        // G * W words (G > 1)
+    uint32_t *sendbuf;       // W words (G > 1, NCCL exchange)
+    uint32_t *gather;        // G * W words (G > 1); PEER exchange: this rank's receive window,
+                             // 2 step-parity halves of G * W words, then G u64 arrival flags
+    uint32_t *const *peers;  // PEER exchange: device array of the G ranks' receive windows
+                             // (this rank's own at index rank; CUDA IPC mappings of the others)
+    uint32_t *xerr;          // PEER exchange: set when a peer's flag did not arrive in time
     unsigned long long *fired_cta;      // [NT]   per-CTA counters (no shared atomics)
     unsigned long long *delivered_cta;  // [NT*C]
     // Brunel+ (model 3): per-synapse weights aligned with ent, fixed-point plastic input

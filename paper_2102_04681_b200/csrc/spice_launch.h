@@ -16,6 +16,8 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
 cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s);
+cudaError_t launch_peer_signal(const SimArgs &a, uint32_t k, cudaStream_t s);
+cudaError_t launch_peer_wait(const SimArgs &a, uint32_t k, cudaStream_t s);
 size_t small_smem_bytes(uint32_t tile_width, uint32_t model);
 cudaError_t launch_small(const SimArgs &a, uint32_t k0, uint32_t nsteps, cudaStream_t s);
 

@@ -96,6 +96,8 @@ def lib():
         "spice_exchange_end": (st, [vp]),
         "spice_exchange_end_fused": (st, [vp]),
         "spice_exchange_put": (st, [vp, vp]),
+        "spice_peer_handle": (st, [vp, vp]),
+        "spice_peer_connect": (st, [vp, vp]),
         "spice_partition_owner": (u32, [u64, u32, u32]),
         "spice_partition_local_to_global": (u64, [u64, u32, u32, u32]),
         "spice_partition_owned_count": (u64, [u64, u32, u32, u32]),
@@ -361,3 +363,16 @@ class Network:
 
     def exchange_put_from(self, src: "Network") -> None:
         _check(lib().spice_exchange_put(self.h, src.h))
+
+    # PEER exchange (device-initiated bitmap stores into every rank's window) --------
+    def peer_handle(self) -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().spice_peer_handle(self.h, buf))
+        return buf.raw
+
+    def peer_connect(self, handles: Sequence[bytes]) -> None:
+        """handles: the G ranks' peer_handle() bytes in rank order."""
+        blob = b"".join(handles)
+        assert len(blob) == 128 * self.world_size
+        buf = C.create_string_buffer(blob, len(blob))
+        _check(lib().spice_peer_connect(self.h, buf))
