@@ -84,7 +84,10 @@ typedef struct {
     uint32_t kind;                 /* SPICE_FIXED_PROB | SPICE_FIXED_INDEGREE */
     uint32_t k;                    /* in-degree for FIXED_INDEGREE */
     uint32_t plastic;              /* 1: STDP synapses (Brunel+ E->E only) */
-    uint32_t reserved;
+    uint16_t delay_min, delay_max; /* per-synapse delays (reading R19): synapse
+                                      s->j of the rule has delay dmin + floor(x (dmax-dmin+1)
+                                      / 2^32), x = Philox(ctr = (s, j>>2, rule, 6))[j&3];
+                                      delay_min = 0: the network's delay_steps */
     double   p;                    /* probability for FIXED_PROB */
 } spice_rule;
 

@@ -41,7 +41,7 @@ class _Rule(C.Structure):
     _fields_ = [("src_begin", C.c_uint32), ("src_end", C.c_uint32),
                 ("dst_begin", C.c_uint32), ("dst_end", C.c_uint32),
                 ("kind", C.c_uint32), ("k", C.c_uint32), ("plastic", C.c_uint32),
-                ("reserved", C.c_uint32), ("p", C.c_double)]
+                ("delay_min", C.c_uint16), ("delay_max", C.c_uint16), ("p", C.c_double)]
 
 
 _LIBS = {}
@@ -83,6 +83,8 @@ def lib(precision: str = "mirror32"):
     L.orc_synth_fired.argtypes = [u32, dbl, u64, u64, vp, u64]
     L.orc_synth_acc.restype = u64
     L.orc_synth_acc.argtypes = [C.POINTER(_Rule), u32, u64, dbl, u32, u64, u32]
+    L.orc_delays.argtypes = [vp, vp]
+    L.orc_ring_slots.restype = u32; L.orc_ring_slots.argtypes = [vp]
     L.orc_set_input.argtypes = [vp, u32, vp]
     L.orc_set_time.argtypes = [vp, u64]
     _LIBS[tag] = L
@@ -106,7 +108,8 @@ def poisson_table(lam: float) -> np.ndarray:
 def _rules(cfg):
     rules = (_Rule * max(1, len(cfg.rules)))()
     for i, r in enumerate(cfg.rules):
-        rules[i] = _Rule(r.src[0], r.src[1], r.dst[0], r.dst[1], r.kind, r.k, 1 if r.plastic else 0, 0, float(r.p))
+        rules[i] = _Rule(r.src[0], r.src[1], r.dst[0], r.dst[1], r.kind, r.k, 1 if r.plastic else 0,
+                         r.delay_min, r.delay_max, float(r.p))
     return rules
 
 
@@ -167,7 +170,7 @@ class OracleNet:
         rules = (_Rule * max(1, len(cfg.rules)))()
         for i, r in enumerate(cfg.rules):
             rules[i] = _Rule(r.src[0], r.src[1], r.dst[0], r.dst[1], r.kind, r.k,
-                             1 if r.plastic else 0, 0, float(r.p))
+                             1 if r.plastic else 0, r.delay_min, r.delay_max, float(r.p))
         prm = (C.c_double * max(1, len(cfg.params)))(*cfg.params)
         g, G, S = part if part else (0, 1, 1)
         self.h = self.L.orc_create(cfg.model, cfg.n, cfg.n_exc, rules, len(cfg.rules),
@@ -194,6 +197,16 @@ class OracleNet:
         tg = np.zeros(max(1, self.nnz), dtype=np.uint32)
         self.L.orc_targets(self.h, tg.ctypes.data)
         return rp, tg[: self.nnz]
+
+    def delays(self) -> np.ndarray:
+        """Per-synapse delays in CSR order (reading R19)."""
+        d = np.zeros(max(1, self.nnz), dtype=np.uint16)
+        self.L.orc_delays(self.h, d.ctypes.data)
+        return d[: self.nnz]
+
+    @property
+    def ring_slots(self) -> int:
+        return self.L.orc_ring_slots(self.h)
 
     def plastic_flags(self) -> np.ndarray:
         f = np.zeros(max(1, self.nnz), dtype=np.uint8)

@@ -50,7 +50,7 @@ typedef ORC_REAL real;
 enum { ORC_VOGELS = 1, ORC_BRUNEL = 2, ORC_BRUNEL_PLUS = 3, ORC_SYNTH = 4 };
 enum { ORC_FIXED_PROB = 0, ORC_FIXED_INDEGREE = 1 };
 /* Philox counter word 3 stream tags (reading R9 / SURVEY App. B) */
-enum { TAG_CONN = 1, TAG_INDEG = 2, TAG_INIT = 3, TAG_EXT = 4, TAG_FIRE = 5 };
+enum { TAG_CONN = 1, TAG_INDEG = 2, TAG_INIT = 3, TAG_EXT = 4, TAG_FIRE = 5, TAG_DELAY = 6 };
 
 /* ------------------------------------------------------------------------- */
 /* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11 "Parallel random numbers:  */
@@ -125,7 +125,8 @@ EXPORT uint64_t orc_local_to_global(uint64_t i, uint32_t g, uint32_t G, uint32_t
 /* ------------------------------------------------------------------------- */
 typedef struct {
     uint32_t src_begin, src_end, dst_begin, dst_end;
-    uint32_t kind, k, plastic, reserved;
+    uint32_t kind, k, plastic;
+    uint16_t delay_min, delay_max;    /* per-synapse delays (reading R19); 0 = network delay */
     double p;
 } orc_rule;
 
@@ -140,6 +141,7 @@ typedef struct {
     uint64_t *row_ptr;
     uint32_t *tgt;
     uint8_t *plastic;                 /* per edge */
+    uint16_t *dly;                    /* per edge: synaptic delay in steps (reading R19) */
     real *w;                          /* per edge (Brunel+ plastic edges) */
     uint64_t nnz;
     /* CSC index of plastic edges (for eager potentiation, R13) */
@@ -237,6 +239,25 @@ static int cmp_u32v(const void *a, const void *b)
     return (x > y) - (x < y);
 }
 
+/* Per-synapse delay (reading R19, "per-synapse delays"): a rule with delay range
+ * [dmin, dmax] gives synapse s -> j the delay dmin + floor(x (dmax - dmin + 1) / 2^32),
+ * x = Philox(ctr=(s, j>>2, r, TAG_DELAY))[j&3]; a rule without a range (delay_min = 0)
+ * uses the network delay.  Multapses of one pair share the delay. */
+static uint32_t rule_dmin(const orc_rule *R, uint32_t net_delay) { return R->delay_min ? R->delay_min : net_delay; }
+static uint32_t rule_dmax(const orc_rule *R, uint32_t net_delay)
+{
+    uint32_t lo = rule_dmin(R, net_delay);
+    return R->delay_min && R->delay_max > lo ? R->delay_max : lo;
+}
+static uint32_t edge_delay(uint32_t key0, uint32_t key1, const orc_rule *R, uint32_t r, uint32_t net_delay,
+                           uint64_t s, uint64_t j)
+{
+    uint32_t lo = rule_dmin(R, net_delay), hi = rule_dmax(R, net_delay);
+    if (hi == lo) return lo;
+    uint32_t x = philox_word((uint32_t)s, (uint32_t)(j >> 2), r, TAG_DELAY, key0, key1, (unsigned)(j & 3));
+    return lo + (uint32_t)(((uint64_t)x * (uint64_t)(hi - lo + 1)) >> 32);
+}
+
 /* Sampled row: the sorted targets of source s under all rules (brute force over all
  * targets; fixed in-degree rules scan every target's draws), restricted to targets
  * owned by rank pg of pG with slice width pS.  Returns the row length (writes at most cap). */
@@ -313,6 +334,10 @@ EXPORT orc_net *orc_create(uint32_t model, uint32_t n, uint32_t n_exc,
     if (n == 0 || delay == 0 || n_params > 32 || (pG > 1 && (pS == 0 || pg >= pG))) return NULL;
     orc_net *N = xcalloc(1, sizeof *N);
     N->model = model; N->n = n; N->n_exc = n_exc; N->delay = delay; N->D = delay + 1;
+    for (uint32_t r = 0; r < n_rules; r++) {
+        uint32_t hi = rule_dmax(&rules[r], delay);
+        if (hi + 1 > N->D) N->D = hi + 1;   /* the ring holds the longest delay */
+    }
     N->key0 = (uint32_t)seed; N->key1 = (uint32_t)(seed >> 32);
     N->dt = dt_ms; N->activity = activity;
     for (uint32_t i = 0; i < n_params; i++) N->prm[i] = params[i];
@@ -348,6 +373,21 @@ EXPORT orc_net *orc_create(uint32_t model, uint32_t n, uint32_t n_exc,
         for (uint64_t q = b; q < e; q++) { N->tgt[q] = tmp[q - b].t; N->plastic[q] = (uint8_t)tmp[q - b].pl; }
         free(tmp);
     }
+    /* per-edge delays: the rule of (s, j) is unique (rules of one source have disjoint
+     * destination ranges) */
+    N->dly = xcalloc(N->nnz, sizeof(uint16_t));
+    for (uint32_t s = 0; s < n; s++)
+        for (uint64_t e = N->row_ptr[s]; e < N->row_ptr[s + 1]; e++) {
+            uint32_t j = N->tgt[e];
+            N->dly[e] = (uint16_t)delay;
+            for (uint32_t r = 0; r < n_rules; r++) {
+                const orc_rule *R = &N->rules[r];
+                if (s >= R->src_begin && s < R->src_end && j >= R->dst_begin && j < R->dst_end) {
+                    N->dly[e] = (uint16_t)edge_delay(N->key0, N->key1, R, r, delay, s, j);
+                    break;
+                }
+            }
+        }
 
     /* ---- derived scalars: computed in double from the inputs, rounded once ---- */
     const double *P = N->prm;
@@ -417,7 +457,7 @@ EXPORT orc_net *orc_create(uint32_t model, uint32_t n, uint32_t n_exc,
 EXPORT void orc_free(orc_net *N)
 {
     if (!N) return;
-    free(N->rules); free(N->row_ptr); free(N->tgt); free(N->plastic); free(N->w);
+    free(N->rules); free(N->row_ptr); free(N->tgt); free(N->plastic); free(N->w); free(N->dly);
     free(N->in_ptr); free(N->in_edge); free(N->edge_src);
     free(N->v); free(N->ge); free(N->gi); free(N->xtr); free(N->ytr); free(N->ref); free(N->acc);
     free(N->ring); free(N->pring); free(N->sp); free(N->sp_off); free(N->delivered); free(N->force_bits);
@@ -549,16 +589,16 @@ EXPORT int orc_step(orc_net *N, uint64_t n_steps)
                 }
             }
         }
-        /* (4) deliver S_t row by row into I[(t + delay) mod D] */
-        uint32_t *dslot = N->ring + (size_t)((t + N->delay) % D) * n;
-        int64_t *dpslot = N->pring + (size_t)((t + N->delay) % D) * n;
+        /* (4) deliver S_t row by row into I[(t + d_e) mod D], d_e the synapse's delay
+         * (per-synapse delays P:485, reading R19) */
         uint64_t events = 0;
         for (uint64_t q = s_begin; q < s_end; q++) {
             uint32_t s = N->sp[q];
             uint32_t qs = q_of(N, s);
             for (uint64_t e = N->row_ptr[s]; e < N->row_ptr[s + 1]; e++) {
-                if (N->model == ORC_BRUNEL_PLUS && N->plastic[e]) dpslot[N->tgt[e]] += wq(N->w[e]);
-                else dslot[N->tgt[e]] += qs;
+                size_t slot = (size_t)((t + N->dly[e]) % D) * n;
+                if (N->model == ORC_BRUNEL_PLUS && N->plastic[e]) N->pring[slot + N->tgt[e]] += wq(N->w[e]);
+                else N->ring[slot + N->tgt[e]] += qs;
                 events++;
             }
         }
@@ -585,6 +625,8 @@ EXPORT uint64_t orc_time(const orc_net *N) { return N->t; }
 EXPORT void orc_row_ptr(const orc_net *N, uint64_t *out) { memcpy(out, N->row_ptr, ((size_t)N->n + 1) * sizeof(uint64_t)); }
 EXPORT void orc_targets(const orc_net *N, uint32_t *out) { memcpy(out, N->tgt, N->nnz * sizeof(uint32_t)); }
 EXPORT void orc_plastic_flags(const orc_net *N, uint8_t *out) { memcpy(out, N->plastic, N->nnz); }
+EXPORT void orc_delays(const orc_net *N, uint16_t *out) { memcpy(out, N->dly, N->nnz * sizeof(uint16_t)); }
+EXPORT uint32_t orc_ring_slots(const orc_net *N) { return N->D; }
 EXPORT int orc_weights(const orc_net *N, real *out) { if (!N->w) return -1; memcpy(out, N->w, N->nnz * sizeof(real)); return 0; }
 EXPORT uint64_t orc_spike_count_total(const orc_net *N) { return N->sp_len; }
 EXPORT void orc_spike_offsets(const orc_net *N, uint64_t *out) { memcpy(out, N->sp_off, (N->t + 1) * sizeof(uint64_t)); }
@@ -677,24 +719,36 @@ EXPORT uint64_t orc_synth_fired(uint32_t n, double activity, uint64_t seed, uint
     return c;
 }
 
-/* Synth accumulator of target j after T steps with delay d (no teacher forcing):
- * acc_j = sum over in-synapses (s -> j), with multiplicity, of the number of steps
- * t < T - d at which s fired (a spike of step t reaches the update of step t + d). */
+/* Synth accumulator of target j after T steps (no teacher forcing): acc_j = sum over
+ * in-synapses (s -> j), with multiplicity, of the number of steps t with t + d_sj < T at
+ * which s fired (a spike of step t reaches the update of step t + d_sj; d_sj the
+ * synapse's delay, the network delay d for rules without a delay range). */
+static uint64_t spikes_before(uint32_t key0, uint32_t key1, uint64_t thr, uint32_t s, uint64_t T, uint32_t d)
+{
+    uint64_t c = 0;
+    for (uint64_t t = 0; t + d < T; t++)
+        c += (uint64_t)philox_word(s >> 2, (uint32_t)t, 0, TAG_FIRE, key0, key1, s & 3) < thr;
+    return c;
+}
 EXPORT uint64_t orc_synth_acc(const orc_rule *rules, uint32_t n_rules, uint64_t seed, double activity,
                               uint32_t j, uint64_t T, uint32_t d)
 {
     uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
     uint64_t thr = prob_threshold(activity), acc = 0;
-    uint64_t n = orc_col(rules, n_rules, seed, j, NULL, 0);
-    uint32_t *src = malloc((n ? n : 1) * sizeof(uint32_t));
-    orc_col(rules, n_rules, seed, j, src, n);
-    for (uint64_t q = 0; q < n; q++) {
-        uint32_t s = src[q];
-        for (uint64_t t = 0; t + d < T; t++) {
-            uint32_t x = philox_word(s >> 2, (uint32_t)t, 0, TAG_FIRE, key0, key1, s & 3);
-            acc += (uint64_t)x < thr;
+    for (uint32_t r = 0; r < n_rules; r++) {
+        const orc_rule *R = &rules[r];
+        if (j < R->dst_begin || j >= R->dst_end) continue;
+        if (R->kind == ORC_FIXED_PROB) {
+            uint64_t pthr = prob_threshold(R->p);
+            for (uint64_t s = R->src_begin; s < R->src_end; s++)
+                if (prob_edge(key0, key1, r, pthr, s, j))
+                    acc += spikes_before(key0, key1, thr, (uint32_t)s, T, edge_delay(key0, key1, R, r, d, s, j));
+        } else {
+            for (uint32_t k = 0; k < R->k; k++) {
+                uint64_t s = indeg_source(key0, key1, r, R, j, k);
+                acc += spikes_before(key0, key1, thr, (uint32_t)s, T, edge_delay(key0, key1, R, r, d, s, j));
+            }
         }
     }
-    free(src);
     return acc;
 }

@@ -32,7 +32,7 @@ class Rule(C.Structure):
     _fields_ = [("src_begin", C.c_uint32), ("src_end", C.c_uint32),
                 ("dst_begin", C.c_uint32), ("dst_end", C.c_uint32),
                 ("kind", C.c_uint32), ("k", C.c_uint32), ("plastic", C.c_uint32),
-                ("reserved", C.c_uint32), ("p", C.c_double)]
+                ("delay_min", C.c_uint16), ("delay_max", C.c_uint16), ("p", C.c_double)]
 
 
 class Config(C.Structure):
@@ -169,7 +169,8 @@ class Network:
         self._rules = (Rule * max(1, len(cfg.rules)))()
         for q, r in enumerate(cfg.rules):
             self._rules[q] = Rule(r.src[0], r.src[1], r.dst[0], r.dst[1], r.kind, r.k,
-                                  1 if r.plastic else 0, 0, float(r.p))
+                                  1 if r.plastic else 0, getattr(r, "delay_min", 0),
+                                  getattr(r, "delay_max", 0), float(r.p))
         self._params = (C.c_double * max(1, len(cfg.params)))(*cfg.params)
         self._nccl = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         flags = (FLAG_EXTERNAL_EXCHANGE if external_exchange else 0) | \

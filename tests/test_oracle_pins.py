@@ -581,3 +581,83 @@ def test_synth_checkers_match_simulation():
         acc = net.state(O.F_ACC)
         for j in range(0, cfg.n, 97):
             assert O.synth_acc(cfg, j, T) == int(acc[j])
+
+
+# ------------------------------------------------ per-synapse delays (reading R19)
+def test_per_synapse_delay_chain():
+    """Reading R19 (P:485 per-synapse delays): A -> B with delay 2, B -> C with delay 5
+    (rule delay ranges), the network default 1 unused: A forced at t0 fires B at t0 + 2
+    and C at t0 + 7 (the single-delay chain of reading R2 generalised)."""
+    rules = [W.Rule((0, 1), (1, 2), W.FIXED_PROB, 1.0, delay_min=2, delay_max=2),
+             W.Rule((1, 2), (2, 3), W.FIXED_PROB, 1.0, delay_min=5, delay_max=5)]
+    cfg = _cfg(W.BRUNEL, 3, 3, rules, _brunel_params(JE=25.0, vlo=0.0, vhi=0.0), delay=1)
+    net = O.OracleNet(cfg)
+    assert net.ring_slots == 6
+    t0 = 4
+    for t in range(t0 + 10):
+        if t == t0:
+            net.force_next([0], "replace")
+        net.step(1)
+    times = {i: [t for t, s in enumerate(net.spikes()) if i in s] for i in range(3)}
+    assert times == {0: [t0], 1: [t0 + 2], 2: [t0 + 7]}
+
+
+def test_per_synapse_delays_uniform_and_default():
+    """Delays of a ranged rule are uniform on [dmin, dmax] (chi-square over 4e4
+    synapses); a rule without a range uses the network delay."""
+    n = 400
+    rules = [W.Rule((0, 320), (0, n), W.FIXED_PROB, 0.3, delay_min=3, delay_max=10),
+             W.Rule((320, n), (0, n), W.FIXED_PROB, 0.3)]
+    cfg = _cfg(W.BRUNEL, n, 320, rules, _brunel_params(), delay=2, seed=9)
+    net = O.OracleNet(cfg)
+    rp, tg = net.csr()
+    d = net.delays().astype(np.int64)
+    src = np.repeat(np.arange(n), np.diff(rp.astype(np.int64)))
+    exc, inh = d[src < 320], d[src >= 320]
+    assert np.all(inh == 2) and exc.min() == 3 and exc.max() == 10
+    obs = np.bincount(exc - 3, minlength=8)
+    assert st.chisquare(obs).pvalue > 1e-4
+    assert net.ring_slots == 11
+
+
+def test_per_synapse_delivery_is_per_delay_spmv():
+    """Delivery with per-synapse delays ("transmit 1-step old spikes via the first
+    adjacency list, 2-steps old spikes via the second ... "): one forced spike set at step
+    0 lands, for every delay d, in the slot of step d as A_d^T 1[S_0] (packed receptors),
+    A_d the adjacency restricted to synapses of delay d."""
+    n = 600
+    rules = [W.Rule((0, 480), (0, n), W.FIXED_PROB, 0.1, delay_min=1, delay_max=6),
+             W.Rule((480, n), (0, n), W.FIXED_PROB, 0.1, delay_min=2, delay_max=4)]
+    cfg = _cfg(W.BRUNEL, n, 480, rules, _brunel_params(theta=1e9), delay=1, seed=12)
+    net = O.OracleNet(cfg)
+    rp, tg = net.csr()
+    d = net.delays().astype(np.int64)
+    rows = np.repeat(np.arange(n), np.diff(rp.astype(np.int64)))
+    rng = np.random.default_rng(5)
+    ids = np.sort(rng.choice(n, 150, replace=False))
+    net.force_next(ids, "replace")
+    net.step(1)
+    x = np.zeros(n, dtype=np.int64)
+    x[ids] = 1
+    q = np.where(rows < 480, 1, 65536)
+    for dd in range(1, 7):
+        sel = d == dd
+        A = sp.csr_matrix(((q * x[rows])[sel], (rows[sel], tg[sel].astype(np.int64))), shape=(n, n))
+        want = np.asarray(A.sum(axis=0)).ravel()
+        got, _ = net.input(dd - 1)
+        assert np.array_equal(got.astype(np.int64), want), dd
+
+
+def test_synth_checkers_with_per_synapse_delays():
+    """orc_synth_acc honours per-synapse delays: equal to the simulated accumulators."""
+    base = W.synth(2000, 19, 0.02, seed=41)
+    cfg = W.NetConfig("sd", W.SYNTH, 2000, 2000,
+                      (W.Rule((0, 2000), (0, 2000), W.FIXED_INDEGREE, k=19, delay_min=1, delay_max=5),),
+                      0.1, 1, 41, 0.02, ())
+    net = O.OracleNet(cfg)
+    T = 40
+    net.step(T)
+    acc = net.state(O.F_ACC)
+    for j in range(0, 2000, 83):
+        assert O.synth_acc(cfg, j, T) == int(acc[j])
+    assert base.n == cfg.n

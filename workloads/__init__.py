@@ -35,6 +35,10 @@ class Rule:
     p: float = 0.0
     k: int = 0
     plastic: bool = False
+    # per-synapse delays in steps (reading R19): each synapse of the
+    # rule draws a delay uniformly from [delay_min, delay_max]; 0 = the network delay
+    delay_min: int = 0
+    delay_max: int = 0
 
 
 @dataclass(frozen=True)
