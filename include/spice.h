@@ -198,6 +198,11 @@ SPICE_API spice_status spice_read_connectivity(spice_net *net, uint32_t row_begi
                                      uint32_t *tgt_global, uint64_t cap,
                                      uint64_t *row_offsets, uint64_t *total);
 
+/* Per-synapse delays in steps (reading R19) of this rank's synapses in the order of
+ * spice_read_connectivity for rows [row_begin, row_end).  ETRUNC as above. */
+SPICE_API spice_status spice_read_delays(spice_net *net, uint32_t row_begin, uint32_t row_end,
+                                         uint8_t *delays, uint64_t cap, uint64_t *total);
+
 /* Neuron state (the SoA neuron pool of P:151 §III-A) of the owned neurons in local order
  * (Listing 1; n must equal the owned count, host buffer caller-owned):
  * 0 v (f32), 1 ge (f32), 2 gi (f32), 3 refractory counter (u32), 4 synth accumulator

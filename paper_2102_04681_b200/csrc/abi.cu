@@ -162,6 +162,8 @@ struct spice_net {
     bool pad8 = false;       // segments padded to 8-entry windows (window-stream delivery)
     uint32_t eshift = 0;     // entries hold (tile offset << eshift); 2 when padded
     uint32_t *deg = nullptr; // pad8: true out-degree of every source on this rank
+    bool mixed_delays = false;   // synapses of more than one delay (reading R19)
+    uint8_t *dly = nullptr;      // per-entry delay (mixed delays only), aligned with ent
     double mean_seg = 0;
     double gen_ms = 0, create_ms = 0;   // setup: generator kernels (device), create (host wall)
     bool small = false;                 // one-CTA persistent step kernel (k_small)
@@ -299,6 +301,7 @@ spice_status validate(const spice_config *c) {
     if (c->model == SPICE_SYNTH && !(c->activity >= 0 && c->activity <= 1))
         return fail(nullptr, SPICE_EINVAL, "activity outside [0,1]");
     if (c->n_rules && !c->rules) return fail(nullptr, SPICE_EINVAL, "rules is NULL");
+    if (c->n_rules > 16) return fail(nullptr, SPICE_EINVAL, "at most 16 rules");
     for (uint32_t r = 0; r < c->n_rules; ++r) {
         const spice_rule &R = c->rules[r];
         if (R.src_begin > R.src_end || R.src_end > c->n_neurons || R.dst_begin > R.dst_end || R.dst_end > c->n_neurons)
@@ -307,6 +310,8 @@ spice_status validate(const spice_config *c) {
         if (R.kind != SPICE_FIXED_PROB && R.kind != SPICE_FIXED_INDEGREE) return fail(nullptr, SPICE_EINVAL, "rule %u: unknown kind", r);
         if (R.plastic && c->model != SPICE_BRUNEL_PLUS) return fail(nullptr, SPICE_EINVAL, "rule %u: plastic synapses need model BRUNEL_PLUS", r);
         if (R.plastic && ++nplastic > kMaxPlasticRules) return fail(nullptr, SPICE_EINVAL, "at most %d plastic rules", kMaxPlasticRules);
+        if (R.delay_min && (R.delay_max > 255 || (R.delay_max && R.delay_max < R.delay_min)))
+            return fail(nullptr, SPICE_EINVAL, "rule %u: delay range [%u, %u] (1 <= min <= max <= 255)", r, R.delay_min, R.delay_max);
         for (uint32_t q = 0; q < r; ++q) {
             const spice_rule &Q = c->rules[q];
             const bool src_overlap = R.src_begin < Q.src_end && Q.src_begin < R.src_end;
@@ -594,6 +599,23 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     spice_net *n = new spice_net();
     n->model = c->model; n->N = c->n_neurons; n->n_exc = c->n_exc; n->delay = c->delay_steps;
     n->D = c->delay_steps + 1; n->rank = c->rank; n->G = c->world_size;
+    // per-synapse delays (reading R19): the fast path keeps the minimum delay of all rules;
+    // synapses with longer delays carry a delay byte; the ring spans the longest delay
+    {
+        uint32_t dmin = ~0u, dmax = 0;
+        for (uint32_t r = 0; r < c->n_rules; ++r) {
+            const spice_rule &R = c->rules[r];
+            if (R.src_begin >= R.src_end || R.dst_begin >= R.dst_end) continue;
+            const uint32_t lo = R.delay_min ? R.delay_min : c->delay_steps;
+            const uint32_t hi = R.delay_min && R.delay_max > lo ? R.delay_max : lo;
+            dmin = std::min(dmin, lo);
+            dmax = std::max(dmax, hi);
+        }
+        if (dmax == 0) dmin = dmax = c->delay_steps;        // no synapses
+        n->mixed_delays = dmin != dmax;
+        n->delay = dmin;
+        n->D = dmax + 1;
+    }
     n->S = c->slice_width ? c->slice_width : spice_default_slice_width(c->n_neurons, c->world_size);
     n->flags = c->flags; n->R = c->record_steps; n->dt = c->dt_ms; n->activity = c->activity;
     // Brunel+ reads step t's bitmap while the same launch writes step t + 1's: two slots
@@ -648,7 +670,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     {
         const uint64_t tw = (n->n_own + 31) / 32 * 32;
         n->small = n->G == 1 && n->pad8 && !c->tile_width && !c->ctas_per_tile && n->C == 1 &&
-                   c->delay_steps == 1 && (n->model == SPICE_VOGELS || n->model == SPICE_BRUNEL || n->model == SPICE_SYNTH) &&
+                   n->delay == 1 && !n->mixed_delays && (n->model == SPICE_VOGELS || n->model == SPICE_BRUNEL || n->model == SPICE_SYNTH) &&
                    !(n->flags & (SPICE_FLAG_GLOBAL_ATOMICS | SPICE_FLAG_EXTERNAL_EXCHANGE | SPICE_FLAG_UNFUSED)) &&
                    tw >= 32 && tw <= kMaxPadTileWord && small_smem_bytes((uint32_t)tw, n->model) <= 227 * 1024 - 2048 &&
                    !getenv("SPICE_NOSMALL");
@@ -691,6 +713,25 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     }
     // ---- connectivity (a0') ----
     if ((st = generate(n))) return bail(st);
+    if (n->mixed_delays) {
+        DelayRules dr{};
+        for (uint32_t r = 0; r < c->n_rules; ++r) {
+            const spice_rule &R = c->rules[r];
+            dr.box[dr.n][0] = R.src_begin; dr.box[dr.n][1] = R.src_end;
+            dr.box[dr.n][2] = R.dst_begin; dr.box[dr.n][3] = R.dst_end;
+            dr.lo[dr.n] = R.delay_min ? R.delay_min : c->delay_steps;
+            dr.hi[dr.n] = R.delay_min && R.delay_max > dr.lo[dr.n] ? R.delay_max : dr.lo[dr.n];
+            dr.index[dr.n] = r;
+            ++dr.n;
+        }
+        GenGeom gd{};
+        gd.N = n->N; gd.n_own = (uint32_t)n->n_own; gd.rank = n->rank; gd.G = n->G; gd.S = n->S;
+        gd.TW = n->TW; gd.NT = n->NT; gd.key0 = (uint32_t)n->seed; gd.key1 = (uint32_t)(n->seed >> 32);
+        gd.eshift = n->eshift;
+        if ((st = dalloc_t(n, &n->dly, (size_t)n->nnz + 16, "synapse delays"))) return bail(st);
+        CU(n, cudaMemsetAsync(n->dly, (int)n->delay, (size_t)n->nnz + 16, n->stream));
+        CU(n, gen_delays(gd, dr, n->delay, n->row_ptr, n->bnd, n->ent, n->dly, n->stream));
+    }
     // ---- state, ring, spike buffers (state padded to NT*TW for 16-byte vector access) ----
     const uint64_t no = n->ring_stride;
     const uint64_t nctas = (uint64_t)n->NT * n->C;
@@ -794,7 +835,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (n->G > 1 && !n->desc) n->fused = false;           // G > 1: fused only on the padded layout
     // ---- kernel arguments ----
     SimArgs &a = n->args;
-    a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D;
+    a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D; a.dly = n->dly;
     a.rank = n->rank; a.G = n->G; a.S = n->S; a.n_own = (uint32_t)n->n_own; a.W = n->W;
     a.TW = n->TW; a.NT = n->NT; a.C = n->C; a.TWs = n->TWs; a.ring_stride = n->ring_stride; a.record_steps = n->R;
     if (getenv("SPICE_PHASES") && atoi(getenv("SPICE_PHASES"))) {     // diagnostics only
@@ -1108,6 +1149,37 @@ spice_status spice_read_connectivity(spice_net *n, uint32_t row_begin, uint32_t 
                                          (unsigned long long)(o - off[q]), (unsigned long long)(off[q + 1] - off[q]));
     }
     if (row_offsets) row_offsets[nr] = tot;
+    return SPICE_OK;
+}
+
+spice_status spice_read_delays(spice_net *n, uint32_t row_begin, uint32_t row_end, uint8_t *out,
+                               uint64_t cap, uint64_t *total) {
+    CHECK_NET(n);
+    if (row_begin > row_end || row_end > n->N) return fail(n, SPICE_EINVAL, "rows outside [0, N)");
+    CU(n, cudaStreamSynchronize(n->stream));
+    const uint32_t nr = row_end - row_begin;
+    std::vector<uint64_t> rp(nr + 1);
+    CU(n, cudaMemcpy(rp.data(), n->row_ptr + row_begin, (nr + 1) * 8ull, cudaMemcpyDeviceToHost));
+    const uint64_t stored = rp[nr] - rp[0];
+    std::vector<uint32_t> bd((uint64_t)nr * (n->NT + 1));
+    std::vector<uint16_t> en(stored ? stored : 1);
+    std::vector<uint8_t> dl(stored ? stored : 1, (uint8_t)n->delay);
+    if (nr) CU(n, cudaMemcpy(bd.data(), n->bnd + (uint64_t)row_begin * (n->NT + 1), bd.size() * 4, cudaMemcpyDeviceToHost));
+    if (stored) CU(n, cudaMemcpy(en.data(), n->ent + rp[0], stored * 2, cudaMemcpyDeviceToHost));
+    if (stored && n->dly) CU(n, cudaMemcpy(dl.data(), n->dly + rp[0], stored, cudaMemcpyDeviceToHost));
+    uint64_t o = 0;                                       // connectivity order, sentinels removed
+    for (uint32_t q = 0; q < nr; ++q) {
+        const uint32_t *B = bd.data() + (uint64_t)q * (n->NT + 1);
+        for (uint32_t b = 0; b < n->NT; ++b)
+            for (uint32_t e = B[b]; e < B[b + 1]; ++e) {
+                const uint64_t k = rp[q] - rp[0] + e;
+                if (((uint32_t)en[k] >> n->eshift) >= n->TW) continue;
+                if (out && o < cap) out[o] = dl[k];
+                ++o;
+            }
+    }
+    if (total) *total = o;
+    if (o > cap || (!out && o)) return fail(n, SPICE_ETRUNC, "need %llu delays", (unsigned long long)o);
     return SPICE_OK;
 }
 

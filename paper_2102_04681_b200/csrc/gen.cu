@@ -482,6 +482,42 @@ cudaError_t gen_plastic_fill(const GenGeom &g, const PlasticBoxes &pb, const uin
     return cudaGetLastError();
 }
 
+// ---- per-synapse delays (reading R19) ----
+__global__ void __launch_bounds__(256) delays_kernel(GenGeom g, DelayRules dr, uint32_t dmin, const uint64_t *row_ptr,
+                                                     const uint32_t *bnd, const uint16_t *ent, uint8_t *dly) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * 8;
+    for (uint64_t q = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); q < (uint64_t)g.N * g.NT; q += nwarps) {
+        const uint32_t s = (uint32_t)(q / g.NT), b = (uint32_t)(q % g.NT);
+        const uint32_t *bp = bnd + (uint64_t)s * (g.NT + 1) + b;
+        const uint64_t st = row_ptr[s] + bp[0];
+        const uint32_t len = bp[1] - bp[0];
+        for (uint32_t e = lane; e < len; e += 32) {
+            const uint32_t off = ent[st + e] >> g.eshift;
+            uint32_t d = dmin;                                  // (padding sentinels: the fast path)
+            if (off < g.TW) {
+                const uint32_t j = (uint32_t)local_to_global((uint64_t)b * g.TW + off, g.rank, g.G, g.S);
+                for (uint32_t r = 0; r < dr.n; ++r)
+                    if (s >= dr.box[r][0] && s < dr.box[r][1] && j >= dr.box[r][2] && j < dr.box[r][3]) {
+                        d = dr.lo[r];
+                        if (dr.hi[r] > dr.lo[r]) {
+                            const uint4 x = philox4x32_10(make_uint4(s, j >> 2, dr.index[r], kTagDelay), g.key0, g.key1);
+                            d += (uint32_t)(((uint64_t)word_of(x, j & 3) * (dr.hi[r] - dr.lo[r] + 1)) >> 32);
+                        }
+                        break;
+                    }
+            }
+            dly[st + e] = (uint8_t)d;
+        }
+    }
+}
+
+cudaError_t gen_delays(const GenGeom &g, const DelayRules &dr, uint32_t dmin, const uint64_t *row_ptr,
+                       const uint32_t *bnd, const uint16_t *ent, uint8_t *dly, cudaStream_t s) {
+    delays_kernel<<<grid_for((uint64_t)g.N * g.NT, 8), 256, 0, s>>>(g, dr, dmin, row_ptr, bnd, ent, dly);
+    return cudaGetLastError();
+}
+
 cudaError_t gen_init_uniform(const GenGeom &g, uint32_t field, float lo, float hi, float *out,
                              cudaStream_t s) {
     if (g.n_own == 0) return cudaSuccess;

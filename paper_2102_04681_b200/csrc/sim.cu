@@ -401,6 +401,11 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                         cv.x += v.x; cv.y += v.y; cv.z += v.z; cv.w += v.w;
                     }
                 }
+                if (a.dly) {                              // longer-delay arrivals of earlier steps
+                    const uint4 rv = *reinterpret_cast<const uint4 *>(ring_slot + x4);
+                    *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
+                    cv.x += rv.x; cv.y += rv.y; cv.z += rv.z; cv.w += rv.w;
+                }
                 c[0] = cv.x; c[1] = cv.y; c[2] = cv.z; c[3] = cv.w;
             } else {
                 const uint4 cv = *reinterpret_cast<const uint4 *>(ring_slot + x4);
@@ -530,7 +535,28 @@ __device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v,
 // the ring 64 entries per iteration with lane L taking entries L and L + 32 (consecutive
 // windows of a segment sit in one load instruction and coalesce into one L1 line lookup),
 // the next iteration's two window loads in flight while the current windows are reduced.
+// Mixed per-synapse delays (reading R19): the 8 entries of a window with their delay bytes;
+// minimum-delay events go to the tile counters (shared memory), longer ones straight into
+// ring slot (t + d) mod D (global red: they are read by the update of step t + d).
 template <bool WORD>
+__device__ __forceinline__ void accumulate_window_dly(const SimArgs &a, uint32_t cnt_s, const uint4 v, const uint2 dd,
+                                                      uint32_t q, uint32_t tD, uint64_t tile_base) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint32_t raw = (w[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+        const uint32_t d = ((u < 4 ? dd.x : dd.y) >> (8 * (u & 3))) & 0xFFu;
+        if (d == a.delay) {
+            asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(cnt_s + (WORD ? raw << 2 : raw)), "r"(q) : "memory");
+        } else {
+            uint32_t sl = tD + d;
+            if (sl >= a.D) sl -= a.D;
+            atomicAdd(a.ring + (uint64_t)sl * a.ring_stride + tile_base + (WORD ? raw : raw >> 2), q);
+        }
+    }
+}
+
+template <bool WORD, bool DLY = false>
 __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
                                                   uint32_t *cnt, uint32_t *ring_base, bool marks = false,
                                                   uint32_t pre_total = 0xFFFFFFFFu) {
@@ -592,26 +618,37 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
         if (e == NONE) return make_uint4(0, 0, 0, 0);
         return ld_stream_v4(a.ent + 8ull * (e & 0x7FFFFFFFu));
     };
+    auto load_dly = [&](uint32_t e) -> uint2 {
+        if (!DLY || e == NONE) return make_uint2(0, 0);
+        return *reinterpret_cast<const uint2 *>(a.dly + 8ull * (e & 0x7FFFFFFFu));
+    };
+    const uint32_t tD = DLY ? (uint32_t)mod32(t, a.D) : 0u;
+    const uint64_t tile_base = (uint64_t)b * a.TW;
     constexpr uint32_t RW = SPICE_RW;                  // windows per lane per iteration
     fill(32u * RW);
     uint32_t e[RW];
     uint4 v[RW];
+    uint2 dd[RW];
 #pragma unroll
-    for (uint32_t r = 0; r < RW; ++r) { e[r] = entry(head + 32u * r + lane); v[r] = load_win(e[r]); }
+    for (uint32_t r = 0; r < RW; ++r) { e[r] = entry(head + 32u * r + lane); v[r] = load_win(e[r]); dd[r] = load_dly(e[r]); }
     head = min(head + 32u * RW, tail);
     while (__any_sync(FULL, e[0] != NONE)) {
         __syncwarp();
         fill(32u * RW);
         uint32_t x[RW];
         uint4 nv[RW];
+        uint2 nd[RW];
 #pragma unroll
-        for (uint32_t r = 0; r < RW; ++r) { x[r] = entry(head + 32u * r + lane); nv[r] = load_win(x[r]); }
+        for (uint32_t r = 0; r < RW; ++r) { x[r] = entry(head + 32u * r + lane); nv[r] = load_win(x[r]); nd[r] = load_dly(x[r]); }
         head = min(head + 32u * RW, tail);
 #pragma unroll
         for (uint32_t r = 0; r < RW; ++r)
-            if (e[r] != NONE) accumulate_window<WORD>(cnt_s, v[r], (e[r] >> 31) ? 65536u : 1u);
+            if (e[r] != NONE) {
+                if (DLY) accumulate_window_dly<WORD>(a, cnt_s, v[r], dd[r], (e[r] >> 31) ? 65536u : 1u, tD, tile_base);
+                else accumulate_window<WORD>(cnt_s, v[r], (e[r] >> 31) ? 65536u : 1u);
+            }
 #pragma unroll
-        for (uint32_t r = 0; r < RW; ++r) { e[r] = x[r]; v[r] = nv[r]; }
+        for (uint32_t r = 0; r < RW; ++r) { e[r] = x[r]; v[r] = nv[r]; dd[r] = nd[r]; }
     }
     if (marks) phase_mark(a, 4);
     __syncthreads();
@@ -766,7 +803,17 @@ constexpr uint32_t kPlU = 4;                          // events in flight per th
 
 __device__ __forceinline__ void plastic_deliver(const SimArgs &a, uint32_t *cnt, uint32_t *plo, uint32_t *phi,
                                                 const float *ys, const uint32_t *tb, uint32_t e, uint32_t off,
-                                                uint32_t fl, float wv, float xpre, bool pot_first) {
+                                                uint32_t fl, float wv, float xpre, bool pot_first,
+                                                uint32_t tD, uint64_t tile_base) {
+    uint64_t gslot = ~0ull;                          // longer per-synapse delay: ring slot t + d
+    if (a.dly) {
+        const uint32_t d = a.dly[e];
+        if (d != a.delay) {
+            uint32_t sl = tD + d;
+            if (sl >= a.D) sl -= a.D;
+            gslot = (uint64_t)sl * a.ring_stride + tile_base + off;
+        }
+    }
     if (wv >= 0.0f) {
         if (pot_first && ((tb[off >> 5] >> (off & 31)) & 1u)) {   // post spiked at t as well: (i) first
             const float pw = __fadd_rn(wv, __fmul_rn(a.mc.Ap, xpre));
@@ -776,12 +823,17 @@ __device__ __forceinline__ void plastic_deliver(const SimArgs &a, uint32_t *cnt,
         nw = nw > 0.0f ? nw : 0.0f;
         a.w[e] = nw;
         const uint64_t q = (uint64_t)__double2ll_rn((double)nw * 4294967296.0);   // (iii)
+        if (gslot != ~0ull) {
+            atomicAdd(reinterpret_cast<unsigned long long *>(a.pring + gslot), (unsigned long long)q);
+            return;
+        }
         const uint32_t lo = (uint32_t)q, hi = (uint32_t)(q >> 32);
         const uint32_t old = atomicAdd(&plo[off], lo);
         const uint32_t carry = old + lo < old ? 1u : 0u;
         if (hi + carry) atomicAdd(&phi[off], hi + carry);
     } else {
-        atomicAdd(&cnt[off], (fl & 1u) ? 65536u : 1u);
+        if (gslot != ~0ull) atomicAdd(a.ring + gslot, (fl & 1u) ? 65536u : 1u);
+        else atomicAdd(&cnt[off], (fl & 1u) ? 65536u : 1u);
     }
 }
 
@@ -809,6 +861,7 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
     }
     if (marks) phase_mark(a, 2);
     const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
+    const uint32_t tD = a.dly ? (uint32_t)mod32(t, a.D) : 0u;
     uint32_t *sst = stage, *slen = stage + kPlSeg, *sfl = stage + 2 * kPlSeg + 1;
     float *sx = reinterpret_cast<float *>(stage + 3 * kPlSeg + 1);
     uint32_t *spre = stage + 4 * kPlSeg + 1, *sinb = stage + 5 * kPlSeg + 2;
@@ -900,7 +953,8 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
                         a.w[e[u]] = nw < a.mc.wmax ? nw : a.mc.wmax;
                     }
                 } else {
-                    plastic_deliver(a, sm.cnt, sm.plo, sm.phi, sm.ys, sm.tb, e[u], x1[u], fl[u], wv[u], xv[u], merged);
+                    plastic_deliver(a, sm.cnt, sm.plo, sm.phi, sm.ys, sm.tb, e[u], x1[u], fl[u], wv[u], xv[u], merged,
+                                    tD, (uint64_t)b * a.TW);
                 }
             }
         }
@@ -917,8 +971,13 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
 __device__ __forceinline__ void deliver_padded(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
                                                uint32_t *cnt, uint32_t *big, bool marks = false,
                                                uint32_t pre_total = 0xFFFFFFFFu) {
-    if (a.eshift) deliver_tile_ring<false>(a, t, b, c, cnt, big, marks, pre_total);
-    else deliver_tile_ring<true>(a, t, b, c, cnt, big, marks, pre_total);
+    if (a.dly) {
+        if (a.eshift) deliver_tile_ring<false, true>(a, t, b, c, cnt, big, marks, pre_total);
+        else deliver_tile_ring<true, true>(a, t, b, c, cnt, big, marks, pre_total);
+    } else {
+        if (a.eshift) deliver_tile_ring<false>(a, t, b, c, cnt, big, marks, pre_total);
+        else deliver_tile_ring<true>(a, t, b, c, cnt, big, marks, pre_total);
+    }
 }
 
 __device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot, uint32_t d, uint32_t *s_tmp) {
@@ -1074,7 +1133,8 @@ __device__ __forceinline__ void cluster_wait() {
 }
 
 // Fused kernel: for MODEL != 3 the second parameter V selects the padded entry format
-// (1: counter indices, cluster tiles; 0: byte offsets); Brunel+ has one variant (V = 0).
+// (bit 0 = 1: counter indices, cluster tiles; 0: byte offsets) and bit 1 the mixed
+// per-synapse delay variant; Brunel+ has one variant (V = 0).
 template <int MODEL, int V>
 __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
     if constexpr (MODEL == 3) {                             // Brunel+ (delay >= 1 via the rings)
@@ -1122,7 +1182,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             *reinterpret_cast<uint4 *>(sm.cnt + x) = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
         phase_mark(a, 1);
-        deliver_tile_ring<V == 1>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
+        deliver_tile_ring<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
         uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice
         const uint32_t lo = b * a.TWs;
         constexpr bool DESC = true;
@@ -1139,8 +1199,14 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             if (a.C > 1) cluster_reduce_slice(a, sm.cnt, c);   // slice summed in place
             phase_mark(a, 6);
             uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + lo;
-            for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u)
-                *reinterpret_cast<uint4 *>(dst + x) = *reinterpret_cast<const uint4 *>(cnt + x);
+            for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u) {
+                uint4 o = *reinterpret_cast<const uint4 *>(cnt + x);
+                if (V & 2) {                                  // the slot may hold longer-delay arrivals
+                    const uint4 r = *reinterpret_cast<const uint4 *>(dst + x);
+                    o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+                }
+                *reinterpret_cast<uint4 *>(dst + x) = o;
+            }
             update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, a.G == 1, &s_count, sm.stage, nullptr, true,
                                      kMaxCluster, sm.stage + kStageWords);
             if (a.C > 1) cluster_wait();                     // partners done reading this CTA's counters
@@ -1290,7 +1356,11 @@ __global__ void __launch_bounds__(kBlock) k_global_atomics(SimArgs a, uint32_t k
         uint32_t *tile = slot + (uint64_t)b * a.TW;
         for (uint32_t e = lane; e < len; e += 32) {
             const uint32_t x = (uint32_t)a.ent[st + e] >> a.eshift;
-            if (x < a.TW) atomicAdd(tile + x, qv);       // skip padding sentinels
+            if (x >= a.TW) continue;                     // skip padding sentinels
+            if (a.dly && a.dly[st + e] != a.delay)       // longer per-synapse delay (reading R19)
+                atomicAdd(a.ring + mod32(t + a.dly[st + e], a.D) * a.ring_stride + (uint64_t)b * a.TW + x, qv);
+            else
+                atomicAdd(tile + x, qv);
         }
         if (lane == 0 && !a.deg) delivered += len;
     }
@@ -1404,9 +1474,9 @@ cudaError_t prepare_kernels(const SimArgs &a) {
 #define ALLOW(kern, b) if (!e) e = allow_smem(kern, b)
     ALLOW(k_update<1>, ub); ALLOW(k_update<2>, ub); ALLOW(k_update<3>, ub); ALLOW(k_update<4>, ub);
     ALLOW(k_deliver, bytes);
-    ALLOW((k_fused<1, 0>), bytes); ALLOW((k_fused<1, 1>), bytes);
-    ALLOW((k_fused<2, 0>), bytes); ALLOW((k_fused<2, 1>), bytes);
-    ALLOW((k_fused<4, 0>), bytes); ALLOW((k_fused<4, 1>), bytes);
+    ALLOW((k_fused<1, 0>), bytes); ALLOW((k_fused<1, 1>), bytes); ALLOW((k_fused<1, 2>), bytes); ALLOW((k_fused<1, 3>), bytes);
+    ALLOW((k_fused<2, 0>), bytes); ALLOW((k_fused<2, 1>), bytes); ALLOW((k_fused<2, 2>), bytes); ALLOW((k_fused<2, 3>), bytes);
+    ALLOW((k_fused<4, 0>), bytes); ALLOW((k_fused<4, 1>), bytes); ALLOW((k_fused<4, 2>), bytes); ALLOW((k_fused<4, 3>), bytes);
     ALLOW(k_global_atomics, tile_smem_bytes(0, a.NR));
     {
         const size_t sb = small_smem_bytes(a.TW, a.model);
@@ -1481,8 +1551,13 @@ static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) 
     if constexpr (M == 3) {                               // Brunel+ (C = 1)
         k_fused<M, 0><<<a.NT, kBlock, bytes, s>>>(a, k);
     } else {
-        if (a.eshift) fused_v<M, 0>(a, k, bytes, s);       // byte-offset entries
-        else fused_v<M, 1>(a, k, bytes, s);                // counter-index entries
+        if (a.dly) {                                       // mixed per-synapse delays
+            if (a.eshift) fused_v<M, 2>(a, k, bytes, s);
+            else fused_v<M, 3>(a, k, bytes, s);
+        } else {
+            if (a.eshift) fused_v<M, 0>(a, k, bytes, s);   // byte-offset entries
+            else fused_v<M, 1>(a, k, bytes, s);            // counter-index entries
+        }
     }
 }
 

@@ -9,7 +9,7 @@
 namespace spice {
 
 // Philox counter word 3 stream tags (reading R9).
-enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFire = 5 };
+enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFire = 5, kTagDelay = 6 };
 
 #ifndef SPICE_KBLOCK
 #define SPICE_KBLOCK 1024
@@ -113,6 +113,10 @@ struct SimArgs {
     float *v, *ge, *gi;
     uint32_t *ref, *acc;
     uint32_t *ring;          // D * ring_stride packed receptor counts
+    const uint8_t *dly;      // mixed per-synapse delays (reading R19): delay of every stored
+                             // entry, aligned with ent; nullptr = every synapse has `delay`.
+                             // `delay` is then the minimum delay (the shared-memory path);
+                             // longer-delay events go to ring slot t + d with global atomics
     // spikes
     uint32_t *sl_ids;        // 2 * NR * RS
     uint64_t *sl_rows;       // 2 * NR * RS row starts of the listed spikes

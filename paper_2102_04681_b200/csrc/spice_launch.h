@@ -65,6 +65,15 @@ cudaError_t gen_plastic_count(const GenGeom &g, const PlasticBoxes &pb, const ui
 cudaError_t gen_plastic_fill(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
                              const uint32_t *bnd, const uint16_t *ent, uint32_t *tmp_cnt,
                              const uint64_t *in_ptr, uint32_t *in_pos, uint32_t *in_src, cudaStream_t s);
+// Per-synapse delays (reading R19): every stored entry (padding sentinels: dmin) gets the
+// delay of its (source, target) pair under the rule that contains it.
+struct DelayRules {
+    uint32_t n;
+    uint32_t box[16][4];          // src_begin, src_end, dst_begin, dst_end
+    uint32_t lo[16], hi[16], index[16];
+};
+cudaError_t gen_delays(const GenGeom &g, const DelayRules &dr, uint32_t dmin, const uint64_t *row_ptr,
+                       const uint32_t *bnd, const uint16_t *ent, uint8_t *dly, cudaStream_t s);
 // Initial state (reading R15).
 cudaError_t gen_init_uniform(const GenGeom &g, uint32_t field, float lo, float hi, float *out,
                              cudaStream_t s);

@@ -79,6 +79,7 @@ def lib():
         "spice_write_state": (st, [vp, u32, vp, u64]),
         "spice_read_input": (st, [vp, u32, vp, vp, u64]),
         "spice_read_weights": (st, [vp, u32, u32, vp, u64, C.POINTER(u64)]),
+        "spice_read_delays": (st, [vp, u32, u32, vp, u64, C.POINTER(u64)]),
         "spice_force_spikes": (st, [vp, vp, u64, i32]),
         "spice_stats": (st, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
         "spice_stream": (vp, [vp]),
@@ -276,6 +277,18 @@ class Network:
         w = np.zeros(max(1, total.value), dtype=np.float32)
         _check(L.spice_read_weights(self.h, row_begin, row_end, w.ctypes.data, w.size, C.byref(total)))
         return w[: total.value]
+
+    def delays(self, row_begin: int = 0, row_end: Optional[int] = None) -> np.ndarray:
+        """Per-synapse delays (steps) in the order of :meth:`connectivity`."""
+        L = lib()
+        row_end = self.n if row_end is None else row_end
+        total = C.c_uint64(0)
+        st = L.spice_read_delays(self.h, row_begin, row_end, None, 0, C.byref(total))
+        if st not in (OK, ETRUNC):
+            _check(st)
+        d = np.zeros(max(1, total.value), dtype=np.uint8)
+        _check(L.spice_read_delays(self.h, row_begin, row_end, d.ctypes.data, d.size, C.byref(total)))
+        return d[: total.value]
 
     def state(self, field: int) -> np.ndarray:
         dt = np.uint32 if field in (FIELD_REF, FIELD_ACC) else np.float32
