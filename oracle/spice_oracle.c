@@ -333,10 +333,16 @@ EXPORT orc_net *orc_create(uint32_t model, uint32_t n, uint32_t n_exc,
 {
     if (n == 0 || delay == 0 || n_params > 32 || (pG > 1 && (pS == 0 || pg >= pG))) return NULL;
     orc_net *N = xcalloc(1, sizeof *N);
-    N->model = model; N->n = n; N->n_exc = n_exc; N->delay = delay; N->D = delay + 1;
-    for (uint32_t r = 0; r < n_rules; r++) {
-        uint32_t hi = rule_dmax(&rules[r], delay);
-        if (hi + 1 > N->D) N->D = hi + 1;   /* the ring holds the longest delay */
+    N->model = model; N->n = n; N->n_exc = n_exc; N->delay = delay;
+    {   /* the ring holds the longest delay of any synapse (reading R19): max rule delay + 1,
+         * the network delay + 1 when there are no synapses */
+        uint32_t dmax = 0;
+        for (uint32_t r = 0; r < n_rules; r++)
+            if (rules[r].src_begin < rules[r].src_end && rules[r].dst_begin < rules[r].dst_end) {
+                uint32_t hi = rule_dmax(&rules[r], delay);
+                if (hi > dmax) dmax = hi;
+            }
+        N->D = (dmax ? dmax : delay) + 1;
     }
     N->key0 = (uint32_t)seed; N->key1 = (uint32_t)(seed >> 32);
     N->dt = dt_ms; N->activity = activity;
