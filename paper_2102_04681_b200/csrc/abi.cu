@@ -498,8 +498,8 @@ spice_status generate(spice_net *n) {
     if (n->pad8 && (st = dalloc_t(n, &n->deg, n->N, "out-degrees"))) return st;
     CU(n, gen_scan(g, n->bnd, n->row_ptr, &nnz, n->deg, n->stream));
     n->nnz = nnz;
-    if (n->pad8 && nnz / 8 >= (1ull << 31) - 1)
-        return fail(n, SPICE_EINVAL, "%llu synapse windows per rank exceed the 32-bit window index", (unsigned long long)(nnz / 8));
+    if (n->pad8 && nnz / kWin >= (1ull << 31) - 1)
+        return fail(n, SPICE_EINVAL, "%llu synapse windows per rank exceed the 32-bit window index", (unsigned long long)(nnz / kWin));
     if ((st = dalloc_t(n, &n->ent_alloc, (size_t)nnz + 2 * kEntPad, "synapse entries"))) return st;
     n->ent = n->ent_alloc + kEntPad;
     CU(n, cudaMemsetAsync(n->ent_alloc, 0, ((size_t)nnz + 2 * kEntPad) * 2, n->stream));
@@ -835,6 +835,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (n->G > 1 && !n->desc) n->fused = false;           // G > 1: fused only on the padded layout
     // ---- kernel arguments ----
     SimArgs &a = n->args;
+    a.pdl = getenv("SPICE_NO_PDL") ? 0u : 1u;             // (A/B switch for measurements)
     a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D; a.dly = n->dly;
     a.rank = n->rank; a.G = n->G; a.S = n->S; a.n_own = (uint32_t)n->n_own; a.W = n->W;
     a.TW = n->TW; a.NT = n->NT; a.C = n->C; a.TWs = n->TWs; a.ring_stride = n->ring_stride; a.record_steps = n->R;

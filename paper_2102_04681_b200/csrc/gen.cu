@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256) row_prefix_kernel(GenGeom g, uint32_t *cn
         for (uint32_t b0 = 0; b0 < g.NT; b0 += 32) {
             const uint32_t b = b0 + lane;
             const uint32_t c = b < g.NT ? row[b] : 0u;
-            const uint32_t cp = g.pad8 ? (c + 7u) & ~7u : c;
+            const uint32_t cp = g.pad8 ? (c + kWin - 1u) & ~(kWin - 1u) : c;
             const uint32_t incl = warp_incl_scan_g(cp, lane);
             if (b < g.NT) row[b] = carry + incl - cp;
             carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) pad_segments_kernel(GenGeom g, const uint
         const uint64_t base = row_ptr[s] + bnd[seg];
         const uint32_t padded = bnd[seg + 1] - bnd[seg];
         for (uint32_t e = cursor[seg]; e < padded; ++e)
-            ent[base + e] = (uint16_t)((g.TW + (((base + e) >> 3) & 63u)) << g.eshift);
+            ent[base + e] = (uint16_t)((g.TW + (((base + e) >> kWinShift) & 63u)) << g.eshift);
     }
 }
 

@@ -105,7 +105,11 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, const StatePtrs &s
     if (forced) fbits = (a.force_bits[i0 >> 5] >> (i0 & 31)) & 0xFu;
     uint32_t spk = 0;
     if (MODEL == 4) {                                   // Synth (reading R12)
+#ifndef SPICE_ABLATE_PHILOX
         const uint4 x = philox4x32_10(make_uint4(j0 >> 2, (uint32_t)t, 0u, kTagFire), a.key0, a.key1);
+#else
+        const uint4 x = make_uint4(j0 * 0x9E3779B9u, (uint32_t)t * 0x85EBCA6Bu, j0 ^ (uint32_t)t, j0 + (uint32_t)t);
+#endif
         if (!acc_done) {                                // (else applied by update_tile's batched pass)
             uint4 acc = *reinterpret_cast<const uint4 *>(sp.acc + li);
             acc.x += c[0]; acc.y += c[1]; acc.z += c[2]; acc.w += c[3];
@@ -312,13 +316,13 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
         for (uint32_t j0 = 0; j0 < nq; j0 += 32) {          // lane = spike; per-spike values hoisted
             const uint32_t ql = j0 + lane;
             if (ql < nq) {                                   // padded: rs, lo, hi multiples of 8
-                const uint32_t rs8 = (uint32_t)(srow[ql] >> 3);
+                const uint32_t rsw = (uint32_t)(srow[ql] >> kWinShift);
                 const uint32_t ih = region[q0 + ql] >= a.n_exc ? 0x80000000u : 0u;
                 const uint32_t *row = stage + ql * rs4 + (uint32_t)(((uint64_t)region[q0 + ql] * rowlen) & 3u);
                 uint2 *dst = reinterpret_cast<uint2 *>(a.desc + (uint64_t)par * a.NT * a.dstride + s_off + q0 + ql);
                 for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
                     const uint32_t lo = row[bb], hi = row[bb + 1];
-                    dst[(uint64_t)bb * a.dstride] = make_uint2(rs8 + (lo >> 3), ((hi - lo) >> 3) | ih);
+                    dst[(uint64_t)bb * a.dstride] = make_uint2(rsw + (lo >> kWinShift), ((hi - lo) >> kWinShift) | ih);
                 }
             }
         }
@@ -387,7 +391,11 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
             }
             if (cnt) {
                 uint4 cv = *reinterpret_cast<const uint4 *>(cnt + x4);
+#ifndef SPICE_ABLATE_PEER
                 if (cl_c < kMaxCluster) {
+#else
+                if (false) {
+#endif
                     const uint32_t la = (uint32_t)__cvta_generic_to_shared(cnt + x4);
 #pragma unroll 1
                     for (uint32_t k = 1; k < a.C; ++k) {
@@ -414,7 +422,9 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
             }
             if (acc_pf) {                                  // (update4 then skips its own RMW)
                 acc_cur.x += c[0]; acc_cur.y += c[1]; acc_cur.z += c[2]; acc_cur.w += c[3];
+#ifndef SPICE_ABLATE_ACC
                 *reinterpret_cast<uint4 *>(a.acc + lo + x4) = acc_cur;
+#endif
             }
             nib = update4<MODEL>(a, sp, t, lo + x4, c, pin, ptab, acc_done || acc_pf, forced);
         }
@@ -535,7 +545,9 @@ __device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v,
 // the ring 64 entries per iteration with lane L taking entries L and L + 32 (consecutive
 // windows of a segment sit in one load instruction and coalesce into one L1 line lookup),
 // the next iteration's two window loads in flight while the current windows are reduced.
-// Mixed per-synapse delays (reading R19): the 8 entries of a window with their delay bytes;
+struct Win { uint4 a, b; };                          // one 32-byte delivery window (kWin entries)
+
+// Mixed per-synapse delays (reading R19): 8 entries of a window with their delay bytes;
 // minimum-delay events go to the tile counters (shared memory), longer ones straight into
 // ring slot (t + d) mod D (global red: they are read by the update of step t + d).
 template <bool WORD>
@@ -614,21 +626,22 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
         __syncwarp();
     };
     auto entry = [&](uint32_t x) -> uint32_t { return x < tail ? ring[x & (kRing - 1)] : NONE; };
-    auto load_win = [&](uint32_t e) -> uint4 {
-        if (e == NONE) return make_uint4(0, 0, 0, 0);
-        return ld_stream_v4(a.ent + 8ull * (e & 0x7FFFFFFFu));
+    auto load_win = [&](uint32_t e) -> Win {
+        if (e == NONE) return Win{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+        const uint16_t *p = a.ent + (uint64_t)kWin * (e & 0x7FFFFFFFu);
+        return Win{ld_stream_v4(p), ld_stream_v4(p + 8)};
     };
-    auto load_dly = [&](uint32_t e) -> uint2 {
-        if (!DLY || e == NONE) return make_uint2(0, 0);
-        return *reinterpret_cast<const uint2 *>(a.dly + 8ull * (e & 0x7FFFFFFFu));
+    auto load_dly = [&](uint32_t e) -> uint4 {
+        if (!DLY || e == NONE) return make_uint4(0, 0, 0, 0);
+        return *reinterpret_cast<const uint4 *>(a.dly + (uint64_t)kWin * (e & 0x7FFFFFFFu));
     };
     const uint32_t tD = DLY ? (uint32_t)mod32(t, a.D) : 0u;
     const uint64_t tile_base = (uint64_t)b * a.TW;
     constexpr uint32_t RW = SPICE_RW;                  // windows per lane per iteration
     fill(32u * RW);
     uint32_t e[RW];
-    uint4 v[RW];
-    uint2 dd[RW];
+    Win v[RW];
+    uint4 dd[RW];
 #pragma unroll
     for (uint32_t r = 0; r < RW; ++r) { e[r] = entry(head + 32u * r + lane); v[r] = load_win(e[r]); dd[r] = load_dly(e[r]); }
     head = min(head + 32u * RW, tail);
@@ -636,16 +649,22 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
         __syncwarp();
         fill(32u * RW);
         uint32_t x[RW];
-        uint4 nv[RW];
-        uint2 nd[RW];
+        Win nv[RW];
+        uint4 nd[RW];
 #pragma unroll
         for (uint32_t r = 0; r < RW; ++r) { x[r] = entry(head + 32u * r + lane); nv[r] = load_win(x[r]); nd[r] = load_dly(x[r]); }
         head = min(head + 32u * RW, tail);
 #pragma unroll
         for (uint32_t r = 0; r < RW; ++r)
             if (e[r] != NONE) {
-                if (DLY) accumulate_window_dly<WORD>(a, cnt_s, v[r], dd[r], (e[r] >> 31) ? 65536u : 1u, tD, tile_base);
-                else accumulate_window<WORD>(cnt_s, v[r], (e[r] >> 31) ? 65536u : 1u);
+                const uint32_t q = (e[r] >> 31) ? 65536u : 1u;
+                if (DLY) {
+                    accumulate_window_dly<WORD>(a, cnt_s, v[r].a, make_uint2(dd[r].x, dd[r].y), q, tD, tile_base);
+                    accumulate_window_dly<WORD>(a, cnt_s, v[r].b, make_uint2(dd[r].z, dd[r].w), q, tD, tile_base);
+                } else {
+                    accumulate_window<WORD>(cnt_s, v[r].a, q);
+                    accumulate_window<WORD>(cnt_s, v[r].b, q);
+                }
             }
 #pragma unroll
         for (uint32_t r = 0; r < RW; ++r) { e[r] = x[r]; v[r] = nv[r]; dd[r] = nd[r]; }
@@ -1163,10 +1182,12 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         // tile bt = blockIdx.x / C; with C > 1 this CTA is rank c of the tile's cluster
         const uint32_t bt = b / a.C, c = b % a.C;
         phase_mark(a, 0);
+        // Programmatic dependent launch: the next step's kernel may be scheduled as soon as
+        // every CTA of this one runs; it zeroes its counters and prefetches its state while
+        // this one finishes, then waits (griddepcontrol.wait) for this grid's completion
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         // (G > 1: the update of t+1 only writes the send bitmap; the lists and descriptors of
         //  the gathered spikes come from bitmap->list)
-        // thread 0: the step's descriptor count, loaded before the counters are zeroed
-        const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t % 3] : 0xFFFFFFFFu;
         if (threadIdx.x == 0) {   // this slice's neuron state (+ input slot t+1) -> L2 while delivering
             const uint32_t lo0 = b * a.TWs, nb = a.TWs * 4u;
             const void *arr[5] = {MODEL == 4 ? (const void *)(a.acc + lo0) : (const void *)(a.v + lo0),
@@ -1180,6 +1201,9 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         }
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)      // TW is a multiple of 32
             *reinterpret_cast<uint4 *>(sm.cnt + x) = make_uint4(0u, 0u, 0u, 0u);
+        asm volatile("griddepcontrol.wait;" ::: "memory");          // the previous step is complete
+        // thread 0: the step's descriptor count
+        const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t % 3] : 0xFFFFFFFFu;
         __syncthreads();
         phase_mark(a, 1);
         deliver_tile_ring<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
@@ -1256,8 +1280,8 @@ __global__ void __launch_bounds__(kBlock) k_small(SimArgs a, uint32_t k0, uint32
     if (rows)                                               // sources' windows, staged once
         for (uint32_t x = tid; x < a.n_own; x += kBlock) {
             const uint64_t rs = a.row_ptr[x];
-            rw0[x] = (uint32_t)((rs + a.bnd[2u * x]) >> 3);
-            rw1[x] = (uint32_t)((rs + a.bnd[2u * x + 1u]) >> 3);
+            rw0[x] = (uint32_t)((rs + a.bnd[2u * x]) >> kWinShift);
+            rw1[x] = (uint32_t)((rs + a.bnd[2u * x + 1u]) >> kWinShift);
             rdg[x] = a.deg[x];
         }
     const uint64_t t0 = *a.t0 + k0;
@@ -1292,13 +1316,13 @@ __global__ void __launch_bounds__(kBlock) k_small(SimArgs a, uint32_t k0, uint32
                 if (rows) { w0 = rw0[sidx]; w1 = rw1[sidx]; }
                 else {
                     const uint64_t rs = a.row_ptr[sidx];
-                    w0 = (uint32_t)((rs + a.bnd[2u * sidx]) >> 3); w1 = (uint32_t)((rs + a.bnd[2u * sidx + 1u]) >> 3);
+                    w0 = (uint32_t)((rs + a.bnd[2u * sidx]) >> kWinShift); w1 = (uint32_t)((rs + a.bnd[2u * sidx + 1u]) >> kWinShift);
                 }
                 const uint32_t qv = sidx >= a.n_exc ? 65536u : 1u;
                 for (uint32_t w = w0 + lane; w < w1; w += 32) {
-                    const uint4 v = ent4[w];
-                    if (a.eshift) accumulate_window<false>(cnt_s, v, qv);
-                    else accumulate_window<true>(cnt_s, v, qv);
+                    const uint4 v0 = ent4[2u * w], v1 = ent4[2u * w + 1u];
+                    if (a.eshift) { accumulate_window<false>(cnt_s, v0, qv); accumulate_window<false>(cnt_s, v1, qv); }
+                    else { accumulate_window<true>(cnt_s, v0, qv); accumulate_window<true>(cnt_s, v1, qv); }
                 }
                 if (lane == 0) deliv += rows ? rdg[sidx] : a.deg[sidx];
             }
@@ -1522,28 +1546,30 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
     return cudaGetLastError();
 }
 
-// C > 1: the C CTAs of a tile are launched as one thread-block cluster.
+// The fused step kernel: C > 1 launches the C CTAs of a tile as one thread-block cluster;
+// every launch may start early (programmatic dependent launch, see k_fused).
 template <typename K>
-static void launch_cluster(K kern, const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
+static void launch_step_kernel(K kern, const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.NT * a.C);
     cfg.blockDim = dim3(kBlock);
     cfg.dynamicSmemBytes = bytes;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = a.C;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = a.C;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = a.C > 1 ? 2 : 1;
     cudaLaunchKernelEx(&cfg, kern, a, k);
 }
 
 template <int M, int V>
 static void fused_v(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
-    if (a.C > 1) launch_cluster(k_fused<M, V>, a, k, bytes, s);
-    else k_fused<M, V><<<a.NT, kBlock, bytes, s>>>(a, k);
+    launch_step_kernel(k_fused<M, V>, a, k, bytes, s);
 }
 
 template <int M>

@@ -21,7 +21,7 @@ enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFi
 #define SPICE_ACC_PREFETCH 1    // synth update: accumulators loaded one loop iteration ahead
 #endif
 #ifndef SPICE_RW
-#define SPICE_RW 2              // ring delivery: 16-byte windows per lane per iteration
+#define SPICE_RW 1              // ring delivery: 32-byte windows per lane per iteration
 #endif
 constexpr int kBlock = SPICE_KBLOCK;  // threads per tile CTA (update / deliver / fused)
 constexpr int kStageWords = 12288;     // bnd rows staged per descriptor-transposition pass
@@ -29,6 +29,10 @@ constexpr uint32_t kMaxTileWidth = 49152;   // u32 counters per tile <= 192 KiB 
 constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
 constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list region
 constexpr int kEntPad = 64;           // u16 padding before/after the entry array
+// Padded layout: every (row, tile) segment is a whole number of delivery windows of
+// kWin u16 entries (32 bytes, one DRAM sector), starting at a window boundary.
+constexpr uint32_t kWinShift = 4;
+constexpr uint32_t kWin = 1u << kWinShift;
 constexpr uint32_t kDummy = 64;       // dummy counters past the tile (padding sentinels)
 constexpr uint32_t kPtabSmem = 128;   // Poisson inversion table entries staged in smem
 constexpr uint32_t kMaxPadTile = 16320;   // padded layout, byte-offset entries: (TW + kDummy) * 4 fits a u16
@@ -97,6 +101,7 @@ struct SimArgs {
                              // across the cluster through distributed shared memory
     uint64_t ring_stride;    // NT * TW
     uint32_t record_steps;
+    uint32_t pdl;            // 1: fused step kernels use programmatic dependent launch
     uint32_t key0, key1;
     uint32_t NR, RS;         // spike-list regions
     unsigned long long *ptimes;   // diagnostics (SPICE_PHASES=1): per CTA [16] phase clocks
