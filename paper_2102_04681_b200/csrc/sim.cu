@@ -545,7 +545,106 @@ __device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v,
 // the ring 64 entries per iteration with lane L taking entries L and L + 32 (consecutive
 // windows of a segment sit in one load instruction and coalesce into one L1 line lookup),
 // the next iteration's two window loads in flight while the current windows are reduced.
-struct Win { uint4 a, b; };                          // one 32-byte delivery window (kWin entries)
+// ------------------------------------------------------- synth step, G = 1 (fast path)
+// The synth drive is input-independent (reading R12: neuron j fires at step t iff
+// Philox(j>>2, t, 0, 5)[j&3] < floor(a 2^32)), so the fused kernel of step t computes
+// the spikes of step t + 1 in its prologue -- while the previous step's grid drains
+// (programmatic dependent launch) -- and stages them as a slice bitmap and spike list in
+// shared memory; right after the grid dependency it L2-prefetches nothing and writes the
+// step's descriptors (production, one pass), then delivers step t, and the update of step
+// t + 1 reduces to the accumulator: acc += this step's input.  Every output (record
+// bitmap, spike lists, descriptors, counters) is the one the general update writes.
+__device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32_t b, uint32_t lo, uint32_t width,
+                                           uint32_t *sfire, uint32_t *sid_s, uint32_t *s_count) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;
+    const uint32_t par = (uint32_t)(t1 & 1);
+    uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
+    const int forced = a.force_ctl[0] == t1 ? (int)a.force_ctl[1] : 0;
+    for (uint32_t x0 = 0; x0 < span; x0 += 4u * kBlock) {
+        if (x0 + 4u * (tid & ~31u) >= span) continue;            // whole warp past the slice
+        const uint32_t x4 = x0 + 4u * tid;
+        uint32_t nib = 0;
+        if (x4 < span && lo + x4 < a.n_own) {
+            const uint32_t j0 = lo + x4;                           // G = 1: local = global
+            const uint4 x = philox4x32_10(make_uint4(j0 >> 2, (uint32_t)t1, 0u, kTagFire), a.key0, a.key1);
+            const uint64_t thr = a.mc.thr_fire;
+            nib = ((uint64_t)x.x < thr ? 1u : 0u) | ((uint64_t)x.y < thr ? 2u : 0u) |
+                  ((uint64_t)x.z < thr ? 4u : 0u) | ((uint64_t)x.w < thr ? 8u : 0u);
+            if (forced) {
+                const uint32_t fb = (a.force_bits[j0 >> 5] >> (j0 & 31)) & 0xFu;
+                nib = forced == 1 ? fb : (nib | fb);
+            }
+            uint32_t valid = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) valid |= (j0 + e < a.n_own ? 1u : 0u) << e;
+            nib &= valid;
+        }
+        uint32_t w = nib << (4u * (lane & 7u));
+        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 1);
+        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 2);
+        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 4);
+        if ((lane & 7u) == 0 && x4 < span) sfire[x4 >> 5] = w;
+        const uint32_t nsp = __popc(nib);
+        const uint32_t incl = warp_incl_scan(nsp);
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        if (tot) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(s_count, tot);
+            base = __shfl_sync(0xFFFFFFFFu, base, 0);
+            uint32_t pos = base + incl - nsp;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if ((nib >> e) & 1u) {
+                    region[pos] = lo + x4 + e;
+                    if (pos < kSidCap) sid_s[pos] = lo + x4 + e;
+                    ++pos;
+                }
+        }
+    }
+}
+
+// acc += input of step t1 for the owned neurons [lo, lo + width): the tile counters (plus
+// the C - 1 peers' partial counts through distributed shared memory, plus longer-delay ring
+// arrivals) or, cnt == nullptr, the ring slot of t1 (read and cleared).
+__device__ __forceinline__ void synth_accumulate(const SimArgs &a, uint64_t t1, uint32_t lo, uint32_t width,
+                                                 const uint32_t *cnt, uint32_t cl_c) {
+    uint32_t *ring_slot = a.ring + mod32(t1, a.D) * a.ring_stride + lo;
+    const uint32_t span = min(width, a.n_own > lo ? a.n_own - lo : 0u);
+    for (uint32_t x4 = 4u * threadIdx.x; x4 < span; x4 += 4u * kBlock) {
+        uint4 acc = *reinterpret_cast<const uint4 *>(a.acc + lo + x4);
+        uint4 cv;
+        if (cnt) {
+            cv = *reinterpret_cast<const uint4 *>(cnt + x4);
+            if (cl_c < kMaxCluster) {
+                const uint32_t la = (uint32_t)__cvta_generic_to_shared(cnt + x4);
+#pragma unroll 1
+                for (uint32_t k = 1; k < a.C; ++k) {
+                    uint32_t peer = cl_c + k;
+                    if (peer >= a.C) peer -= a.C;
+                    uint32_t ra;
+                    uint4 v;
+                    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(peer));
+                    asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(ra));
+                    cv.x += v.x; cv.y += v.y; cv.z += v.z; cv.w += v.w;
+                }
+            }
+            if (a.dly) {
+                const uint4 rv = *reinterpret_cast<const uint4 *>(ring_slot + x4);
+                *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
+                cv.x += rv.x; cv.y += rv.y; cv.z += rv.z; cv.w += rv.w;
+            }
+        } else {
+            cv = *reinterpret_cast<const uint4 *>(ring_slot + x4);
+            *reinterpret_cast<uint4 *>(ring_slot + x4) = make_uint4(0, 0, 0, 0);
+        }
+        acc.x += cv.x; acc.y += cv.y; acc.z += cv.z; acc.w += cv.w;
+        *reinterpret_cast<uint4 *>(a.acc + lo + x4) = acc;
+    }
+}
+
+struct Win { uint4 a, b; };                          // one delivery window (kWin entries; b: kWin = 16)
 
 // Mixed per-synapse delays (reading R19): 8 entries of a window with their delay bytes;
 // minimum-delay events go to the tile counters (shared memory), longer ones straight into
@@ -627,13 +726,19 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
     };
     auto entry = [&](uint32_t x) -> uint32_t { return x < tail ? ring[x & (kRing - 1)] : NONE; };
     auto load_win = [&](uint32_t e) -> Win {
-        if (e == NONE) return Win{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+        Win w;
+        if (e == NONE) { w.a = make_uint4(0, 0, 0, 0); if constexpr (kWin == 16) w.b = w.a; return w; }
         const uint16_t *p = a.ent + (uint64_t)kWin * (e & 0x7FFFFFFFu);
-        return Win{ld_stream_v4(p), ld_stream_v4(p + 8)};
+        w.a = ld_stream_v4(p);
+        if constexpr (kWin == 16) w.b = ld_stream_v4(p + 8);
+        return w;
     };
     auto load_dly = [&](uint32_t e) -> uint4 {
         if (!DLY || e == NONE) return make_uint4(0, 0, 0, 0);
-        return *reinterpret_cast<const uint4 *>(a.dly + (uint64_t)kWin * (e & 0x7FFFFFFFu));
+        const uint8_t *p = a.dly + (uint64_t)kWin * (e & 0x7FFFFFFFu);
+        if constexpr (kWin == 16) return *reinterpret_cast<const uint4 *>(p);
+        const uint2 d = *reinterpret_cast<const uint2 *>(p);
+        return make_uint4(d.x, d.y, 0u, 0u);
     };
     const uint32_t tD = DLY ? (uint32_t)mod32(t, a.D) : 0u;
     const uint64_t tile_base = (uint64_t)b * a.TW;
@@ -660,10 +765,11 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
                 const uint32_t q = (e[r] >> 31) ? 65536u : 1u;
                 if (DLY) {
                     accumulate_window_dly<WORD>(a, cnt_s, v[r].a, make_uint2(dd[r].x, dd[r].y), q, tD, tile_base);
-                    accumulate_window_dly<WORD>(a, cnt_s, v[r].b, make_uint2(dd[r].z, dd[r].w), q, tD, tile_base);
+                    if constexpr (kWin == 16)
+                        accumulate_window_dly<WORD>(a, cnt_s, v[r].b, make_uint2(dd[r].z, dd[r].w), q, tD, tile_base);
                 } else {
                     accumulate_window<WORD>(cnt_s, v[r].a, q);
-                    accumulate_window<WORD>(cnt_s, v[r].b, q);
+                    if constexpr (kWin == 16) accumulate_window<WORD>(cnt_s, v[r].b, q);
                 }
             }
 #pragma unroll
@@ -1201,22 +1307,56 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         }
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)      // TW is a multiple of 32
             *reinterpret_cast<uint4 *>(sm.cnt + x) = make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t lo = b * a.TWs;
+        // synth, G = 1: the spikes of step t + 1 before the grid dependency (see synth_fire)
+        constexpr uint32_t kFireWords = 1536;
+        __shared__ uint32_t s_fire[MODEL == 4 ? kFireWords : 1];
+        const bool syn = MODEL == 4 && a.G == 1 && a.TWs <= 32u * kFireWords;
+        uint32_t *sid_s = sm.stage + kStageWords;
+        if (syn) {
+            synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count);
+            __syncthreads();
+            const uint32_t n = s_count;                     // L2 prefetch of the spiking rows'
+            for (uint32_t q = threadIdx.x; q < min(n, kSidCap); q += kBlock) {   // segment bounds
+                const uint64_t r0 = (uint64_t)sid_s[q] * (a.NT + 1u);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                             :: "l"(a.bnd + (r0 & ~3ull)), "r"((((uint32_t)(r0 & 3u) + a.NT + 1u) * 4u + 15u) & ~15u) : "memory");
+            }
+        }
         asm volatile("griddepcontrol.wait;" ::: "memory");          // the previous step is complete
         // thread 0: the step's descriptor count
         const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t % 3] : 0xFFFFFFFFu;
         __syncthreads();
         phase_mark(a, 1);
+        if (syn) {                                           // step t + 1's record, counters, descriptors
+            const uint32_t n = s_count;
+            const uint64_t t1 = t + 1;
+            uint32_t *bm = a.record + mod32(t1, a.record_steps) * (uint64_t)a.W;
+            const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
+            for (uint32_t x = threadIdx.x; x < nwd; x += kBlock) bm[(lo >> 5) + x] = s_fire[x];
+            const uint32_t par1 = (uint32_t)(t1 & 1);
+            if (threadIdx.x == 0) {
+                a.sl_counts[par1 * a.NR + b] = n;
+                if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
+            }
+            uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
+            uint64_t *region_rows = a.sl_rows + ((uint64_t)par1 * a.NR + b) * a.RS;
+            const uint64_t dsum = write_descriptors(a, t1, b, n, region, region_rows, sm.stage, true, sid_s);
+            if (threadIdx.x == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
+            phase_mark(a, 9);
+        }
         deliver_tile_ring<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
         uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice
-        const uint32_t lo = b * a.TWs;
         constexpr bool DESC = true;
         if (a.delay == 1) {
             // C > 1: the update sums the C partial slices itself (peers read after one cluster
             // barrier; a second one at exit keeps every CTA's counters alive until then)
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
             phase_mark(a, 6);
-            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, a.G == 1, &s_count, sm.stage, nullptr, true,
-                                     a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
+            if (syn) synth_accumulate(a, t + 1, lo, a.TWs, cnt, a.C > 1 ? c : kMaxCluster);
+            else
+                update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, a.G == 1, &s_count, sm.stage, nullptr, true,
+                                         a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
             // (an arrive right after the update loop, waited at exit, measured 0.5 us slower)
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         } else {
@@ -1231,8 +1371,13 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
                 }
                 *reinterpret_cast<uint4 *>(dst + x) = o;
             }
-            update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, a.G == 1, &s_count, sm.stage, nullptr, true,
-                                     kMaxCluster, sm.stage + kStageWords);
+            if (syn) {
+                __syncthreads();                             // (the slot's ring writes above)
+                synth_accumulate(a, t + 1, lo, a.TWs, nullptr, kMaxCluster);
+            } else {
+                update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, a.G == 1, &s_count, sm.stage, nullptr, true,
+                                         kMaxCluster, sm.stage + kStageWords);
+            }
             if (a.C > 1) cluster_wait();                     // partners done reading this CTA's counters
         }
         phase_mark(a, 12);
@@ -1320,9 +1465,11 @@ __global__ void __launch_bounds__(kBlock) k_small(SimArgs a, uint32_t k0, uint32
                 }
                 const uint32_t qv = sidx >= a.n_exc ? 65536u : 1u;
                 for (uint32_t w = w0 + lane; w < w1; w += 32) {
-                    const uint4 v0 = ent4[2u * w], v1 = ent4[2u * w + 1u];
-                    if (a.eshift) { accumulate_window<false>(cnt_s, v0, qv); accumulate_window<false>(cnt_s, v1, qv); }
-                    else { accumulate_window<true>(cnt_s, v0, qv); accumulate_window<true>(cnt_s, v1, qv); }
+                    for (uint32_t h = 0; h < kWin / 8; ++h) {
+                        const uint4 v0 = ent4[(kWin / 8) * w + h];
+                        if (a.eshift) accumulate_window<false>(cnt_s, v0, qv);
+                        else accumulate_window<true>(cnt_s, v0, qv);
+                    }
                 }
                 if (lane == 0) deliv += rows ? rdg[sidx] : a.deg[sidx];
             }

@@ -21,7 +21,7 @@ enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFi
 #define SPICE_ACC_PREFETCH 1    // synth update: accumulators loaded one loop iteration ahead
 #endif
 #ifndef SPICE_RW
-#define SPICE_RW 1              // ring delivery: 32-byte windows per lane per iteration
+#define SPICE_RW (SPICE_WIN_SHIFT == 3 ? 2 : 1)   // ring delivery: windows per lane per iteration
 #endif
 constexpr int kBlock = SPICE_KBLOCK;  // threads per tile CTA (update / deliver / fused)
 constexpr int kStageWords = 12288;     // bnd rows staged per descriptor-transposition pass
@@ -30,8 +30,13 @@ constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
 constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list region
 constexpr int kEntPad = 64;           // u16 padding before/after the entry array
 // Padded layout: every (row, tile) segment is a whole number of delivery windows of
-// kWin u16 entries (32 bytes, one DRAM sector), starting at a window boundary.
-constexpr uint32_t kWinShift = 4;
+// kWin u16 entries, starting at a window boundary.  16-byte windows (kWinShift = 3)
+// measured faster than sector-sized 32-byte windows (kWinShift = 4: +12 % padding
+// atomics, synth delivery 12.3 -> 14.5 us, DESIGN.md delivery log).
+#ifndef SPICE_WIN_SHIFT
+#define SPICE_WIN_SHIFT 3
+#endif
+constexpr uint32_t kWinShift = SPICE_WIN_SHIFT;
 constexpr uint32_t kWin = 1u << kWinShift;
 constexpr uint32_t kDummy = 64;       // dummy counters past the tile (padding sentinels)
 constexpr uint32_t kPtabSmem = 128;   // Poisson inversion table entries staged in smem
