@@ -177,6 +177,7 @@ struct spice_net {
     } slot[2];
     std::vector<std::vector<uint32_t>> hdec;   // decoded per-step lists (reused)
     uint32_t NR = 1, RS = 32;    // spike-list regions
+    uint32_t prod_words = 0;     // synth fast path: producer-warp shared memory (words)
     unsigned long long *ptimes = nullptr;   // SPICE_PHASES diagnostics
     bool fused = true, global_atomics = false;
     // device memory
@@ -699,8 +700,10 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (n->G == 1) { n->NR = n->NT * n->C; n->RS = n->TWs; }
     else { n->NR = (uint32_t)(((uint64_t)n->G * n->W + kB2LWords - 1) / kB2LWords); n->RS = kB2LWords * 32; }
     if (n->NR > kMaxRegions) return bail(fail(n, SPICE_EINVAL, "%u spike-list regions > %u: use a wider tile_width", n->NR, kMaxRegions));
-    const size_t smem_max = 227 * 1024 - 2048;             // dynamic; static shared variables need the rest
-    if (n->pad8 && tile_smem_bytes(n->TW, n->NR) > smem_max) return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for shared memory", n->TW));
+    const size_t smem_max = 227 * 1024 - 2048 - 6 * 1024;  // dynamic; static shared variables need the rest
+    if (n->model == SPICE_SYNTH && n->G == 1 && n->pad8 && tile_smem_bytes(n->TW, n->NR, kSynthProdWordsHost) <= smem_max)
+        n->prod_words = kSynthProdWordsHost;
+    if (n->pad8 && tile_smem_bytes(n->TW, n->NR, n->prod_words) > smem_max) return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for shared memory", n->TW));
     if (n->model == SPICE_BRUNEL_PLUS && plastic_smem_bytes(n->TW, n->NR) > smem_max)
         return bail(fail(n, SPICE_EINVAL, "tile_width %u too wide for the Brunel+ tile kernels", n->TW));
     // ---- NCCL communicator ----
@@ -839,6 +842,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.model = n->model; a.N = n->N; a.n_exc = n->n_exc; a.delay = n->delay; a.D = n->D; a.dly = n->dly;
     a.rank = n->rank; a.G = n->G; a.S = n->S; a.n_own = (uint32_t)n->n_own; a.W = n->W;
     a.TW = n->TW; a.NT = n->NT; a.C = n->C; a.TWs = n->TWs; a.ring_stride = n->ring_stride; a.record_steps = n->R;
+    a.prod_words = n->prod_words;
     if (getenv("SPICE_PHASES") && atoi(getenv("SPICE_PHASES"))) {     // diagnostics only
         if ((st = dalloc_t(n, &n->ptimes, (size_t)n->NT * n->C * 16, "phase clocks"))) return bail(st);
         CU(n, cudaMemset(n->ptimes, 0, (size_t)n->NT * n->C * 16 * 8));

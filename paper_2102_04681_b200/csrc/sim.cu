@@ -238,6 +238,7 @@ struct DeliverSmem {
     uint32_t *stage;   // [kStageWords] bnd-row staging of the update phase (aliases dsm)
     uint32_t *pref;    // [NR + 1] region prefix
     uint32_t *tmp;     // [32]
+    uint32_t *prod;    // [prod_words]
 };
 
 __device__ __forceinline__ uint32_t region_of(const uint32_t *pref, uint32_t nr, uint32_t p) {
@@ -255,6 +256,8 @@ constexpr uint32_t kRing = 512;                        // ring entries per warp 
 // spike IDs of the update kept in shared memory for the descriptor pass: the words of the
 // delivery area past the descriptor staging (kStageWords) and before the end of the rings
 constexpr uint32_t kSidCap = (kBlock / 32) * kRing - kStageWords;
+// synth fast path: shared-memory area of the producer warps (spike IDs, then row staging)
+constexpr uint32_t kSynthSid = 2048;
 
 // Descriptor transposition (G = 1, padded layout): for the n spikes of region b (this
 // tile's spikes), one pass loads every spike's bnd row (a warp per spike, coalesced),
@@ -273,11 +276,20 @@ __device__ __forceinline__ DescStage desc_stage(const SimArgs &a) {
     d.CH = max(1u, (uint32_t)kStageWords / (d.rs4 + 3u));
     return d;
 }
+// SUB: run by the pth threads ptid = 0 .. pth - 1 of a producer warp group (named barrier 1)
+// while the other warps of the CTA deliver (synth fast path); sid_cap: the capacity of sid_s.
+template <bool SUB = false>
 __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t t, uint32_t b, uint32_t n,
                                   const uint32_t *region, uint64_t *region_rows, uint32_t *stage,
-                                  bool marks = false, const uint32_t *sid_s = nullptr) {
-    if (sid_s && n <= kSidCap) region = sid_s;          // the spike IDs' shared-memory copy
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                  bool marks = false, const uint32_t *sid_s = nullptr,
+                                  uint32_t ptid = threadIdx.x, uint32_t pth = kBlock, uint32_t sid_cap = kSidCap,
+                                  uint32_t stage_words = kStageWords) {
+    auto barrier = [&]() {
+        if constexpr (SUB) asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
+        else __syncthreads();
+    };
+    if (sid_s && n <= sid_cap) region = sid_s;          // the spike IDs' shared-memory copy
+    const uint32_t lane = ptid & 31, warp = ptid >> 5, nwp = pth / 32;
     const uint32_t par = (uint32_t)(t & 1);
     // dense per-tile lists: this CTA's n descriptors go to [off, off + n) of every
     // destination tile's list of step t (one atomic on the step's counter)
@@ -285,18 +297,19 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
     //  its copies; the pass's closing barrier orders it before the descriptor writes)
     __shared__ uint32_t s_off;
     uint32_t off_reg = 0;
-    if (threadIdx.x == 0 && n) off_reg = atomicAdd(&a.dcount[t % 3], n);
+    if (ptid == 0 && n) off_reg = atomicAdd(&a.dcount[t % 3], n);
     const DescStage ds = desc_stage(a);
-    const uint32_t rowlen = ds.rowlen, rs4 = ds.rs4, CH = ds.CH;
+    const uint32_t rowlen = ds.rowlen, rs4 = ds.rs4;
+    const uint32_t CH = SUB ? max(1u, stage_words / (rs4 + 3u)) : ds.CH;
     uint64_t *srow = reinterpret_cast<uint64_t *>(stage + CH * rs4);
     uint32_t *sdeg = reinterpret_cast<uint32_t *>(srow + CH);
     const uint4 *bnd4 = reinterpret_cast<const uint4 *>(a.bnd);
     uint64_t dsum = 0;
     for (uint32_t q0 = 0; q0 < n; q0 += CH) {
         const uint32_t nq = min(CH, n - q0);
-        __syncthreads();
+        barrier();
         // every load of the pass in flight at once (cp.async, no register round trips)
-        for (uint32_t ql = warp; ql < nq; ql += kBlock / 32) {            // one warp per spike row
+        for (uint32_t ql = warp; ql < nq; ql += nwp) {                    // one warp per spike row
             const uint32_t s = region[q0 + ql];
             const uint64_t g0 = (uint64_t)s * rowlen;
             const uint64_t k0 = g0 >> 2, nk = ((g0 + rowlen - 1) >> 2) - k0 + 1;
@@ -307,9 +320,9 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(sdeg + ql)), "l"(a.deg + s) : "memory");
             }
         }
-        if (threadIdx.x == 0 && q0 == 0) s_off = off_reg;
+        if (ptid == 0 && q0 == 0) s_off = off_reg;
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
+        barrier();
         if (marks) phase_mark(a, 10);
         if (warp == 0)
             for (uint32_t ql = lane; ql < nq; ql += 32) { region_rows[q0 + ql] = srow[ql]; dsum += sdeg[ql]; }
@@ -320,7 +333,7 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
                 const uint32_t ih = region[q0 + ql] >= a.n_exc ? 0x80000000u : 0u;
                 const uint32_t *row = stage + ql * rs4 + (uint32_t)(((uint64_t)region[q0 + ql] * rowlen) & 3u);
                 uint2 *dst = reinterpret_cast<uint2 *>(a.desc + (uint64_t)par * a.NT * a.dstride + s_off + q0 + ql);
-                for (uint32_t bb = warp; bb < a.NT; bb += kBlock / 32) {
+                for (uint32_t bb = warp; bb < a.NT; bb += nwp) {
                     const uint32_t lo = row[bb], hi = row[bb + 1];
                     dst[(uint64_t)bb * a.dstride] = make_uint2(rsw + (lo >> kWinShift), ((hi - lo) >> kWinShift) | ih);
                 }
@@ -329,7 +342,7 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xFFFFFFFFu, dsum, o);
-    __syncthreads();
+    barrier();
     return dsum;                                       // valid in warp 0
 }
 
@@ -555,7 +568,7 @@ __device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v,
 // t + 1 reduces to the accumulator: acc += this step's input.  Every output (record
 // bitmap, spike lists, descriptors, counters) is the one the general update writes.
 __device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32_t b, uint32_t lo, uint32_t width,
-                                           uint32_t *sfire, uint32_t *sid_s, uint32_t *s_count) {
+                                           uint32_t *sfire, uint32_t *sid_s, uint32_t *s_count, uint32_t sid_cap) {
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;
     const uint32_t par = (uint32_t)(t1 & 1);
@@ -597,7 +610,7 @@ __device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32
             for (int e = 0; e < 4; ++e)
                 if ((nib >> e) & 1u) {
                     region[pos] = lo + x4 + e;
-                    if (pos < kSidCap) sid_s[pos] = lo + x4 + e;
+                    if (pos < sid_cap) sid_s[pos] = lo + x4 + e;
                     ++pos;
                 }
         }
@@ -611,6 +624,37 @@ __device__ __forceinline__ void synth_accumulate(const SimArgs &a, uint64_t t1, 
                                                  const uint32_t *cnt, uint32_t cl_c) {
     uint32_t *ring_slot = a.ring + mod32(t1, a.D) * a.ring_stride + lo;
     const uint32_t span = min(width, a.n_own > lo ? a.n_own - lo : 0u);
+    if (cnt && !a.dly && (cl_c >= kMaxCluster || a.C == 2) && span <= 4u * kBlock * 3u) {
+        // common case: every load of the thread's <= 3 groups in flight before any add
+        uint4 acc[3], cv[3], pv[3];
+        const uint32_t peer = cl_c < kMaxCluster ? cl_c ^ 1u : 0u;
+#pragma unroll
+        for (int it = 0; it < 3; ++it) {
+            const uint32_t x4 = 4u * threadIdx.x + (uint32_t)it * 4u * kBlock;
+            if (x4 < span) {
+                acc[it] = *reinterpret_cast<const uint4 *>(a.acc + lo + x4);
+                cv[it] = *reinterpret_cast<const uint4 *>(cnt + x4);
+                pv[it] = make_uint4(0u, 0u, 0u, 0u);
+                if (cl_c < kMaxCluster) {
+                    uint32_t ra;
+                    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"((uint32_t)__cvta_generic_to_shared(cnt + x4)), "r"(peer));
+                    asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(pv[it].x), "=r"(pv[it].y), "=r"(pv[it].z), "=r"(pv[it].w) : "r"(ra));
+                }
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < 3; ++it) {
+            const uint32_t x4 = 4u * threadIdx.x + (uint32_t)it * 4u * kBlock;
+            if (x4 < span) {
+                uint4 o = acc[it];
+                o.x += cv[it].x + pv[it].x; o.y += cv[it].y + pv[it].y;
+                o.z += cv[it].z + pv[it].z; o.w += cv[it].w + pv[it].w;
+                *reinterpret_cast<uint4 *>(a.acc + lo + x4) = o;
+            }
+        }
+        return;
+    }
     for (uint32_t x4 = 4u * threadIdx.x; x4 < span; x4 += 4u * kBlock) {
         uint4 acc = *reinterpret_cast<const uint4 *>(a.acc + lo + x4);
         uint4 cv;
@@ -667,24 +711,30 @@ __device__ __forceinline__ void accumulate_window_dly(const SimArgs &a, uint32_t
     }
 }
 
-template <bool WORD, bool DLY = false>
-__device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
-                                                  uint32_t *cnt, uint32_t *ring_base, bool marks = false,
-                                                  uint32_t pre_total = 0xFFFFFFFFu) {
-    constexpr uint32_t NW = kBlock / 32;
-    constexpr uint32_t NONE = 0xFFFFFFFFu;
-    constexpr uint32_t FULL = 0xFFFFFFFFu;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t par = (uint32_t)(t & 1);
-    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
+// The step's descriptor count of tile list t (thread 0 may pass it preloaded) and the
+// reset of the counter step t + 2's producers use; block-wide.
+__device__ __forceinline__ uint32_t delivery_count(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+                                                   uint32_t pre_total) {
     __shared__ uint32_t s_total;
-    if (tid == 0) {
-        s_total = pre_total != 0xFFFFFFFFu ? pre_total : a.dcount[t % 3];   // (preloaded by thread 0)
+    if (threadIdx.x == 0) {
+        s_total = pre_total != 0xFFFFFFFFu ? pre_total : a.dcount[t % 3];
         if (b == 0 && c == 0) a.dcount[(t + 2) % 3] = 0u;     // next user: step t + 2's producers
     }
     __syncthreads();
-    if (marks) phase_mark(a, 2);
-    const uint32_t n_sp = s_total;
+    return s_total;
+}
+
+// The per-warp part of ring delivery: warp `warp` of NW delivering warps takes its share
+// of the tile list's n_sp visits (no block-wide barriers inside).
+template <bool WORD, bool DLY = false>
+__device__ __forceinline__ void deliver_ring_core(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+                                                  uint32_t *cnt, uint32_t *ring_base, uint32_t n_sp,
+                                                  uint32_t warp, uint32_t NW) {
+    constexpr uint32_t NONE = 0xFFFFFFFFu;
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
     const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
     const uint32_t v0 = (uint32_t)((uint64_t)my * warp / NW), v1 = (uint32_t)((uint64_t)my * (warp + 1) / NW);
     const uint64_t *dlist = a.desc + ((uint64_t)par * a.NT + b) * a.dstride + c;   // visit v -> dlist[v * C]
@@ -693,7 +743,6 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
         const uint32_t v = vb + lane;
         return v < v1 ? dlist[(uint64_t)v * a.C] : 0ull;
     };
-    if (marks) phase_mark(a, 3);
     uint32_t gnext = v0;
     uint64_t dn = dload(v0);
     uint32_t w0 = 0, nw = 0, inh = 0, pre = 0, T = 0, c0 = 0;   // current group, c0 = expanded
@@ -775,6 +824,15 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
 #pragma unroll
         for (uint32_t r = 0; r < RW; ++r) { e[r] = x[r]; v[r] = nv[r]; dd[r] = nd[r]; }
     }
+}
+
+template <bool WORD, bool DLY = false>
+__device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, uint32_t b, uint32_t c,
+                                                  uint32_t *cnt, uint32_t *ring_base, bool marks = false,
+                                                  uint32_t pre_total = 0xFFFFFFFFu) {
+    const uint32_t n_sp = delivery_count(a, t, b, c, pre_total);
+    if (marks) phase_mark(a, 2);
+    deliver_ring_core<WORD, DLY>(a, t, b, c, cnt, ring_base, n_sp, threadIdx.x >> 5, kBlock / 32);
     if (marks) phase_mark(a, 4);
     __syncthreads();
     if (marks) phase_mark(a, 5);
@@ -1119,6 +1177,7 @@ __device__ __forceinline__ void store_delivered(const SimArgs &a, uint32_t slot,
 }
 
 // Delivery shared memory: cnt [TW + kDummy] | big [max(kStageWords, rings)] | pref | tmp
+// | prod [a.prod_words] (synth fast path: spike IDs + descriptor staging of the producer warps)
 __host__ __device__ constexpr uint32_t big_words() {
     return (uint32_t)kStageWords > (kBlock / 32) * kRing ? (uint32_t)kStageWords : (kBlock / 32) * kRing;
 }
@@ -1131,12 +1190,13 @@ __device__ __forceinline__ DeliverSmem carve(const SimArgs &a, uint32_t *smem) {
     smem += big_words();
     sm.pref = smem;
     sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
+    sm.prod = sm.tmp + 36;                              // 16-byte aligned (tmp is 32 + 4 words)
     return sm;
 }
 
-size_t tile_smem_bytes(uint32_t TW, uint32_t NR) {
+size_t tile_smem_bytes(uint32_t TW, uint32_t NR, uint32_t prod_words) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
-    return ((size_t)tw4 + kDummy + big_words() + ((NR + 1 + 3) & ~3u) + 32 + 4) * 4;
+    return ((size_t)tw4 + kDummy + big_words() + ((NR + 1 + 3) & ~3u) + 32 + 4 + prod_words) * 4;
 }
 
 // Brunel+ tile kernels: counters, plastic fixed-point low / high words, post traces y
@@ -1311,13 +1371,13 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         // synth, G = 1: the spikes of step t + 1 before the grid dependency (see synth_fire)
         constexpr uint32_t kFireWords = 1536;
         __shared__ uint32_t s_fire[MODEL == 4 ? kFireWords : 1];
-        const bool syn = MODEL == 4 && a.G == 1 && a.TWs <= 32u * kFireWords;
-        uint32_t *sid_s = sm.stage + kStageWords;
+        const bool syn = MODEL == 4 && a.G == 1 && a.TWs <= 32u * kFireWords && a.prod_words > kSynthSid;
+        uint32_t *sid_s = syn ? sm.prod : sm.stage + kStageWords;
         if (syn) {
-            synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count);
+            synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid);
             __syncthreads();
             const uint32_t n = s_count;                     // L2 prefetch of the spiking rows'
-            for (uint32_t q = threadIdx.x; q < min(n, kSidCap); q += kBlock) {   // segment bounds
+            for (uint32_t q = threadIdx.x; q < min(n, kSynthSid); q += kBlock) {   // segment bounds
                 const uint64_t r0 = (uint64_t)sid_s[q] * (a.NT + 1u);
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
                              :: "l"(a.bnd + (r0 & ~3ull)), "r"((((uint32_t)(r0 & 3u) + a.NT + 1u) * 4u + 15u) & ~15u) : "memory");
@@ -1328,24 +1388,38 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t % 3] : 0xFFFFFFFFu;
         __syncthreads();
         phase_mark(a, 1);
-        if (syn) {                                           // step t + 1's record, counters, descriptors
-            const uint32_t n = s_count;
-            const uint64_t t1 = t + 1;
-            uint32_t *bm = a.record + mod32(t1, a.record_steps) * (uint64_t)a.W;
-            const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
-            for (uint32_t x = threadIdx.x; x < nwd; x += kBlock) bm[(lo >> 5) + x] = s_fire[x];
-            const uint32_t par1 = (uint32_t)(t1 & 1);
-            if (threadIdx.x == 0) {
-                a.sl_counts[par1 * a.NR + b] = n;
-                if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
+        if (syn) {
+            // warp-specialised: the last kProdWarps warps publish step t + 1 (record bitmap,
+            // counters, descriptors) while the others deliver step t
+            constexpr uint32_t kProdWarps = 2, NWD = kBlock / 32 - kProdWarps;
+            const uint32_t n_sp = delivery_count(a, t, bt, c, pre_total);
+            const uint32_t warp = threadIdx.x >> 5;
+            if (warp < NWD) {
+                deliver_ring_core<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, n_sp, warp, NWD);
+            } else {
+                const uint32_t ptid = threadIdx.x - NWD * 32, pth = kProdWarps * 32;
+                const uint32_t n = s_count;
+                const uint64_t t1 = t + 1;
+                uint32_t *bm = a.record + mod32(t1, a.record_steps) * (uint64_t)a.W;
+                const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
+                for (uint32_t x = ptid; x < nwd; x += pth) bm[(lo >> 5) + x] = s_fire[x];
+                const uint32_t par1 = (uint32_t)(t1 & 1);
+                if (ptid == 0) {
+                    a.sl_counts[par1 * a.NR + b] = n;
+                    if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
+                }
+                uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
+                uint64_t *region_rows = a.sl_rows + ((uint64_t)par1 * a.NR + b) * a.RS;
+                const uint64_t dsum = write_descriptors<true>(a, t1, b, n, region, region_rows, sm.prod + kSynthSid,
+                                                              false, sid_s, ptid, pth, kSynthSid,
+                                                              a.prod_words - kSynthSid);
+                if (ptid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
             }
-            uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
-            uint64_t *region_rows = a.sl_rows + ((uint64_t)par1 * a.NR + b) * a.RS;
-            const uint64_t dsum = write_descriptors(a, t1, b, n, region, region_rows, sm.stage, true, sid_s);
-            if (threadIdx.x == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
-            phase_mark(a, 9);
+            __syncthreads();
+            phase_mark(a, 5);
+        } else {
+            deliver_tile_ring<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
         }
-        deliver_tile_ring<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
         uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice
         constexpr bool DESC = true;
         if (a.delay == 1) {
@@ -1639,7 +1713,7 @@ static cudaError_t allow_smem(K kern, size_t bytes) {
 }
 
 cudaError_t prepare_kernels(const SimArgs &a) {
-    const size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    const size_t bytes = tile_smem_bytes(a.TW, a.NR, a.prod_words);
     const size_t ub = (size_t)kStageWords * 4;
     cudaError_t e = cudaSuccess;
 #define ALLOW(kern, b) if (!e) e = allow_smem(kern, b)
@@ -1648,7 +1722,7 @@ cudaError_t prepare_kernels(const SimArgs &a) {
     ALLOW((k_fused<1, 0>), bytes); ALLOW((k_fused<1, 1>), bytes); ALLOW((k_fused<1, 2>), bytes); ALLOW((k_fused<1, 3>), bytes);
     ALLOW((k_fused<2, 0>), bytes); ALLOW((k_fused<2, 1>), bytes); ALLOW((k_fused<2, 2>), bytes); ALLOW((k_fused<2, 3>), bytes);
     ALLOW((k_fused<4, 0>), bytes); ALLOW((k_fused<4, 1>), bytes); ALLOW((k_fused<4, 2>), bytes); ALLOW((k_fused<4, 3>), bytes);
-    ALLOW(k_global_atomics, tile_smem_bytes(0, a.NR));
+    ALLOW(k_global_atomics, tile_smem_bytes(0, a.NR, 0));
     {
         const size_t sb = small_smem_bytes(a.TW, a.model);
         if (sb <= kSmallSmemMax) {
@@ -1679,7 +1753,7 @@ cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s) {
 
 cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, int n_sm, cudaStream_t s) {
     if (global_atomics) {
-        const size_t bytes = tile_smem_bytes(0, a.NR);
+        const size_t bytes = tile_smem_bytes(0, a.NR, 0);
         k_global_atomics<<<min((uint32_t)(n_sm * 4), a.NT * a.C), kBlock, bytes, s>>>(a, k);
         return cudaGetLastError();
     }
@@ -1689,7 +1763,7 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
         return cudaGetLastError();
     }
     if (!a.desc) return cudaErrorInvalidValue;             // padded layout only
-    k_deliver<<<a.NT * a.C, kBlock, tile_smem_bytes(a.TW, a.NR), s>>>(a, k);
+    k_deliver<<<a.NT * a.C, kBlock, tile_smem_bytes(a.TW, a.NR, a.prod_words), s>>>(a, k);
     return cudaGetLastError();
 }
 
@@ -1736,7 +1810,7 @@ static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) 
 
 cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
     if (a.model != 3 && !a.desc) return cudaErrorInvalidValue;
-    const size_t bytes = tile_smem_bytes(a.TW, a.NR);
+    const size_t bytes = tile_smem_bytes(a.TW, a.NR, a.prod_words);
     switch (a.model) {
     case 1: fused_m<1>(a, k, bytes, s); break;
     case 2: fused_m<2>(a, k, bytes, s); break;

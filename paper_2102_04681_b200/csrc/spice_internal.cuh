@@ -107,6 +107,7 @@ struct SimArgs {
     uint64_t ring_stride;    // NT * TW
     uint32_t record_steps;
     uint32_t pdl;            // 1: fused step kernels use programmatic dependent launch
+    uint32_t prod_words;     // synth fast path (G = 1): producer-warp shared-memory words
     uint32_t key0, key1;
     uint32_t NR, RS;         // spike-list regions
     unsigned long long *ptimes;   // diagnostics (SPICE_PHASES=1): per CTA [16] phase clocks

@@ -8,7 +8,8 @@
 namespace spice {
 
 // ---- step kernels (sim.cu) ----
-size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions);
+size_t tile_smem_bytes(uint32_t tile_width, uint32_t n_regions, uint32_t prod_words);
+constexpr uint32_t kSynthProdWordsHost = 8192;   // (== kSynthProdWords in sim.cu)
 size_t plastic_smem_bytes(uint32_t tile_width, uint32_t n_regions);
 cudaError_t prepare_kernels(const SimArgs &a);
 cudaError_t launch_update(const SimArgs &a, uint32_t k, cudaStream_t s);
