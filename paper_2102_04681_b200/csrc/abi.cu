@@ -830,7 +830,9 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (n->pad8 && !n->global_atomics) {
         // a tile's list holds every spike of the step: the rank's own (G = 1) or all N (G > 1)
         const uint64_t dstride = ((n->G == 1 ? n->n_own : (uint64_t)n->N) + 1) & ~1ull;
-        if ((st = dalloc_t(n, &n->desc, 2ull * n->NT * dstride, "segment descriptors"))) return bail(st);
+        // three step buffers: the producers of step t + 1 (synth fast path: in the prologue
+        // of the kernel delivering t, which may overlap the kernel delivering t - 1)
+        if ((st = dalloc_t(n, &n->desc, 3ull * n->NT * dstride, "segment descriptors"))) return bail(st);
         if ((st = dalloc_t(n, &n->dcount, 4, "descriptor counters"))) return bail(st);
         CU(n, cudaMemset(n->dcount, 0, 16));
     }

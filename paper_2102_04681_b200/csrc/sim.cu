@@ -210,11 +210,11 @@ __device__ __forceinline__ uint32_t update4(const SimArgs &a, const StatePtrs &s
 // clock offset of phase boundary `slot` from the kernel start into ptimes[cta*16 + slot];
 // slot 13 counts launches, 14/15 hold %globaltimer at start/end of the last launch.
 __device__ __forceinline__ long long &phase_c0() { __shared__ long long c0; return c0; }
-__device__ __forceinline__ void phase_mark(const SimArgs &a, int slot) {
+__device__ __forceinline__ void phase_mark(const SimArgs &a, int slot, uint32_t who = 0) {
 #if !SPICE_PHASES_BUILD
-    (void)a; (void)slot;   // compiled out: even predicated-off marks cost issue slots (ncu r01u)
+    (void)a; (void)slot; (void)who;   // compiled out: even predicated-off marks cost issue slots (ncu r01u)
 #else
-    if (a.ptimes && threadIdx.x == 0) {
+    if (a.ptimes && threadIdx.x == who) {
         unsigned long long *p = a.ptimes + blockIdx.x * 16u;
         if (slot == 0) {
             phase_c0() = clock64();
@@ -290,14 +290,15 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
     };
     if (sid_s && n <= sid_cap) region = sid_s;          // the spike IDs' shared-memory copy
     const uint32_t lane = ptid & 31, warp = ptid >> 5, nwp = pth / 32;
-    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t dbuf = (uint32_t)mod32(t, 3);        // descriptor lists: 3 buffers by step
     // dense per-tile lists: this CTA's n descriptors go to [off, off + n) of every
     // destination tile's list of step t (one atomic on the step's counter)
     // (the reservation's latency overlaps the row loads: thread 0 publishes it after issuing
     //  its copies; the pass's closing barrier orders it before the descriptor writes)
     __shared__ uint32_t s_off;
     uint32_t off_reg = 0;
-    if (ptid == 0 && n) off_reg = atomicAdd(&a.dcount[t % 3], n);
+    if (ptid == 0 && n) off_reg = atomicAdd(&a.dcount[t & 3u], n);
+    if (marks) phase_mark(a, 11, threadIdx.x - ptid);
     const DescStage ds = desc_stage(a);
     const uint32_t rowlen = ds.rowlen, rs4 = ds.rs4;
     const uint32_t CH = SUB ? max(1u, stage_words / (rs4 + 3u)) : ds.CH;
@@ -323,7 +324,7 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
         if (ptid == 0 && q0 == 0) s_off = off_reg;
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         barrier();
-        if (marks) phase_mark(a, 10);
+        if (marks) phase_mark(a, 10, threadIdx.x - ptid);
         if (warp == 0)
             for (uint32_t ql = lane; ql < nq; ql += 32) { region_rows[q0 + ql] = srow[ql]; dsum += sdeg[ql]; }
         for (uint32_t j0 = 0; j0 < nq; j0 += 32) {          // lane = spike; per-spike values hoisted
@@ -332,7 +333,7 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
                 const uint32_t rsw = (uint32_t)(srow[ql] >> kWinShift);
                 const uint32_t ih = region[q0 + ql] >= a.n_exc ? 0x80000000u : 0u;
                 const uint32_t *row = stage + ql * rs4 + (uint32_t)(((uint64_t)region[q0 + ql] * rowlen) & 3u);
-                uint2 *dst = reinterpret_cast<uint2 *>(a.desc + (uint64_t)par * a.NT * a.dstride + s_off + q0 + ql);
+                uint2 *dst = reinterpret_cast<uint2 *>(a.desc + (uint64_t)dbuf * a.NT * a.dstride + s_off + q0 + ql);
                 for (uint32_t bb = warp; bb < a.NT; bb += nwp) {
                     const uint32_t lo = row[bb], hi = row[bb + 1];
                     dst[(uint64_t)bb * a.dstride] = make_uint2(rsw + (lo >> kWinShift), ((hi - lo) >> kWinShift) | ih);
@@ -717,8 +718,11 @@ __device__ __forceinline__ uint32_t delivery_count(const SimArgs &a, uint64_t t,
                                                    uint32_t pre_total) {
     __shared__ uint32_t s_total;
     if (threadIdx.x == 0) {
-        s_total = pre_total != 0xFFFFFFFFu ? pre_total : a.dcount[t % 3];
-        if (b == 0 && c == 0) a.dcount[(t + 2) % 3] = 0u;     // next user: step t + 2's producers
+        s_total = pre_total != 0xFFFFFFFFu ? pre_total : a.dcount[t & 3u];
+        if (b == 0 && c == 0) {                     // next user: step t + 3's producers, which
+            a.dcount[(t + 3) & 3u] = 0u;            // run in the prologue of the kernel after next
+            __threadfence();
+        }
     }
     __syncthreads();
     return s_total;
@@ -737,7 +741,7 @@ __device__ __forceinline__ void deliver_ring_core(const SimArgs &a, uint64_t t, 
     const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
     const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
     const uint32_t v0 = (uint32_t)((uint64_t)my * warp / NW), v1 = (uint32_t)((uint64_t)my * (warp + 1) / NW);
-    const uint64_t *dlist = a.desc + ((uint64_t)par * a.NT + b) * a.dstride + c;   // visit v -> dlist[v * C]
+    const uint64_t *dlist = a.desc + ((uint64_t)mod32(t, 3) * a.NT + b) * a.dstride + c;   // visit v -> dlist[v * C]
     uint32_t *ring = ring_base + warp * kRing;
     auto dload = [&](uint32_t vb) -> uint64_t {
         const uint32_t v = vb + lane;
@@ -1374,52 +1378,35 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         const bool syn = MODEL == 4 && a.G == 1 && a.TWs <= 32u * kFireWords && a.prod_words > kSynthSid;
         uint32_t *sid_s = syn ? sm.prod : sm.stage + kStageWords;
         if (syn) {
+            // step t + 1's spikes, record bitmap, counters and descriptors, all before the grid
+            // dependency: they touch only step t + 1's buffers (record slot, list parity,
+            // descriptor buffer (t + 1) mod 3, counter (t + 1) mod 4), none of which the
+            // previous kernel (delivering t - 1, publishing t) reads or writes
             synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid);
             __syncthreads();
-            const uint32_t n = s_count;                     // L2 prefetch of the spiking rows'
-            for (uint32_t q = threadIdx.x; q < min(n, kSynthSid); q += kBlock) {   // segment bounds
-                const uint64_t r0 = (uint64_t)sid_s[q] * (a.NT + 1u);
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                             :: "l"(a.bnd + (r0 & ~3ull)), "r"((((uint32_t)(r0 & 3u) + a.NT + 1u) * 4u + 15u) & ~15u) : "memory");
+            const uint32_t n = s_count;
+            const uint64_t t1 = t + 1;
+            uint32_t *bm = a.record + mod32(t1, a.record_steps) * (uint64_t)a.W;
+            const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
+            for (uint32_t x = threadIdx.x; x < nwd; x += kBlock) bm[(lo >> 5) + x] = s_fire[x];
+            const uint32_t par1 = (uint32_t)(t1 & 1);
+            if (threadIdx.x == 0) {
+                a.sl_counts[par1 * a.NR + b] = n;
+                if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
             }
+            uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
+            uint64_t *region_rows = a.sl_rows + ((uint64_t)par1 * a.NR + b) * a.RS;
+            const uint64_t dsum = write_descriptors(a, t1, b, n, region, region_rows, sm.stage, true, sid_s,
+                                                    threadIdx.x, kBlock, kSynthSid);
+            if (threadIdx.x == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
+            phase_mark(a, 9);
         }
         asm volatile("griddepcontrol.wait;" ::: "memory");          // the previous step is complete
         // thread 0: the step's descriptor count
-        const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t % 3] : 0xFFFFFFFFu;
+        const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t & 3u] : 0xFFFFFFFFu;
         __syncthreads();
         phase_mark(a, 1);
-        if (syn) {
-            // warp-specialised: the last kProdWarps warps publish step t + 1 (record bitmap,
-            // counters, descriptors) while the others deliver step t
-            constexpr uint32_t kProdWarps = 2, NWD = kBlock / 32 - kProdWarps;
-            const uint32_t n_sp = delivery_count(a, t, bt, c, pre_total);
-            const uint32_t warp = threadIdx.x >> 5;
-            if (warp < NWD) {
-                deliver_ring_core<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, n_sp, warp, NWD);
-            } else {
-                const uint32_t ptid = threadIdx.x - NWD * 32, pth = kProdWarps * 32;
-                const uint32_t n = s_count;
-                const uint64_t t1 = t + 1;
-                uint32_t *bm = a.record + mod32(t1, a.record_steps) * (uint64_t)a.W;
-                const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
-                for (uint32_t x = ptid; x < nwd; x += pth) bm[(lo >> 5) + x] = s_fire[x];
-                const uint32_t par1 = (uint32_t)(t1 & 1);
-                if (ptid == 0) {
-                    a.sl_counts[par1 * a.NR + b] = n;
-                    if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
-                }
-                uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
-                uint64_t *region_rows = a.sl_rows + ((uint64_t)par1 * a.NR + b) * a.RS;
-                const uint64_t dsum = write_descriptors<true>(a, t1, b, n, region, region_rows, sm.prod + kSynthSid,
-                                                              false, sid_s, ptid, pth, kSynthSid,
-                                                              a.prod_words - kSynthSid);
-                if (ptid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
-            }
-            __syncthreads();
-            phase_mark(a, 5);
-        } else {
-            deliver_tile_ring<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
-        }
+        deliver_tile_ring<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
         uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice
         constexpr bool DESC = true;
         if (a.delay == 1) {

@@ -20,6 +20,9 @@ enum : uint32_t { kTagConn = 1, kTagIndeg = 2, kTagInit = 3, kTagExt = 4, kTagFi
 #ifndef SPICE_ACC_PREFETCH
 #define SPICE_ACC_PREFETCH 1    // synth update: accumulators loaded one loop iteration ahead
 #endif
+#ifndef SPICE_PROD_WARPS
+#define SPICE_PROD_WARPS 2      // synth fast path: producer warps beside the delivering warps
+#endif
 #ifndef SPICE_RW
 #define SPICE_RW (SPICE_WIN_SHIFT == 3 ? 2 : 1)   // ring delivery: windows per lane per iteration
 #endif
@@ -133,12 +136,12 @@ struct SimArgs {
     uint64_t *sl_rows;       // 2 * NR * RS row starts of the listed spikes
     uint32_t *sl_counts;     // 2 * NR
     // G = 1 (padded layout): per-step segment descriptors, written transposed by the
-    // updating CTAs into one dense list per destination tile: desc[(par*NT + b)*dstride + i]
+    // updating CTAs into one dense list per destination tile: desc[((t mod 3)*NT + b)*dstride + i]
     // = first 16-byte window (bits 0-31) | window count (32-62) | inh (63) of the i-th
     // spike of the step restricted to tile b (list order = producer arrival order)
     uint64_t *desc;
     uint64_t dstride;        // descriptor slots per (parity, tile) list (>= owned neurons)
-    uint32_t *dcount;        // [3] descriptors per list of step t at dcount[t % 3]
+    uint32_t *dcount;        // [4] descriptors per list of step t at dcount[t % 4]
     uint32_t *record;        // record_steps * G * W words
     uint32_t *sendbuf;       // W words (G > 1, NCCL exchange)
     uint32_t *gather;        // G * W words (G > 1); PEER exchange: this rank's receive window,
