@@ -622,16 +622,17 @@ __device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32
 // the C - 1 peers' partial counts through distributed shared memory, plus longer-delay ring
 // arrivals) or, cnt == nullptr, the ring slot of t1 (read and cleared).
 __device__ __forceinline__ void synth_accumulate(const SimArgs &a, uint64_t t1, uint32_t lo, uint32_t width,
-                                                 const uint32_t *cnt, uint32_t cl_c) {
+                                                 const uint32_t *cnt, uint32_t cl_c,
+                                                 uint32_t tid = threadIdx.x, uint32_t nth = kBlock) {
     uint32_t *ring_slot = a.ring + mod32(t1, a.D) * a.ring_stride + lo;
     const uint32_t span = min(width, a.n_own > lo ? a.n_own - lo : 0u);
-    if (cnt && !a.dly && (cl_c >= kMaxCluster || a.C == 2) && span <= 4u * kBlock * 3u) {
-        // common case: every load of the thread's <= 3 groups in flight before any add
-        uint4 acc[3], cv[3], pv[3];
+    if (cnt && !a.dly && (cl_c >= kMaxCluster || a.C == 2) && span <= 4u * nth * 4u) {
+        // common case: every load of the thread's <= 4 groups in flight before any add
+        uint4 acc[4], cv[4], pv[4];
         const uint32_t peer = cl_c < kMaxCluster ? cl_c ^ 1u : 0u;
 #pragma unroll
-        for (int it = 0; it < 3; ++it) {
-            const uint32_t x4 = 4u * threadIdx.x + (uint32_t)it * 4u * kBlock;
+        for (int it = 0; it < 4; ++it) {
+            const uint32_t x4 = 4u * tid + (uint32_t)it * 4u * nth;
             if (x4 < span) {
                 acc[it] = *reinterpret_cast<const uint4 *>(a.acc + lo + x4);
                 cv[it] = *reinterpret_cast<const uint4 *>(cnt + x4);
@@ -645,8 +646,8 @@ __device__ __forceinline__ void synth_accumulate(const SimArgs &a, uint64_t t1, 
             }
         }
 #pragma unroll
-        for (int it = 0; it < 3; ++it) {
-            const uint32_t x4 = 4u * threadIdx.x + (uint32_t)it * 4u * kBlock;
+        for (int it = 0; it < 4; ++it) {
+            const uint32_t x4 = 4u * tid + (uint32_t)it * 4u * nth;
             if (x4 < span) {
                 uint4 o = acc[it];
                 o.x += cv[it].x + pv[it].x; o.y += cv[it].y + pv[it].y;
@@ -656,7 +657,7 @@ __device__ __forceinline__ void synth_accumulate(const SimArgs &a, uint64_t t1, 
         }
         return;
     }
-    for (uint32_t x4 = 4u * threadIdx.x; x4 < span; x4 += 4u * kBlock) {
+    for (uint32_t x4 = 4u * tid; x4 < span; x4 += 4u * nth) {
         uint4 acc = *reinterpret_cast<const uint4 *>(a.acc + lo + x4);
         uint4 cv;
         if (cnt) {
@@ -687,6 +688,51 @@ __device__ __forceinline__ void synth_accumulate(const SimArgs &a, uint64_t t1, 
         acc.x += cv.x; acc.y += cv.y; acc.z += cv.z; acc.w += cv.w;
         *reinterpret_cast<uint4 *>(a.acc + lo + x4) = acc;
     }
+}
+
+// The end of a synth fast-path step: warps [0, kAccWarps) add the step's input to the
+// accumulators while the other warps publish step t + 1 (record bitmap, spike list and
+// counts, descriptors of its spiking rows) -- after delivery, when the memory system is
+// quiet, and off the accumulators' critical path.
+constexpr uint32_t kAccWarps = 24;
+__device__ __forceinline__ void synth_publish_and_accumulate(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo,
+                                                             const uint32_t *cnt, uint32_t cl_c, const uint32_t *s_fire,
+                                                             const uint32_t *sid_s, uint32_t n, uint32_t *stage,
+                                                             uint32_t stage_words) {
+    const uint32_t warp = threadIdx.x >> 5;
+    if (warp < kAccWarps) {
+        synth_accumulate(a, t + 1, lo, a.TWs, cnt, cl_c, threadIdx.x, kAccWarps * 32);
+    } else {
+        const uint32_t ptid = threadIdx.x - kAccWarps * 32, pth = kBlock - kAccWarps * 32;
+        const uint64_t t1 = t + 1;
+        const uint32_t par1 = (uint32_t)(t1 & 1);
+        uint32_t *bm = a.record + mod32(t1, a.record_steps) * (uint64_t)a.W;
+        const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
+        uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
+        uint64_t *region_rows = a.sl_rows + ((uint64_t)par1 * a.NR + b) * a.RS;
+        for (uint32_t x = ptid; x < nwd; x += pth) bm[(lo >> 5) + x] = s_fire[x];
+        if (n <= kSynthSid) {
+            for (uint32_t q = ptid; q < n; q += pth) region[q] = sid_s[q];
+        } else {                                     // (more spikes than the shared list holds)
+            __shared__ uint32_t s_pos;
+            if (ptid == 0) s_pos = 0;
+            asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
+            for (uint32_t x = ptid; x < nwd; x += pth) {
+                uint32_t w = s_fire[x];
+                uint32_t p = w ? atomicAdd(&s_pos, __popc(w)) : 0u;
+                while (w) { region[p++] = lo + 32u * x + (uint32_t)(__ffs(w) - 1); w &= w - 1u; }
+            }
+        }
+        if (ptid == 0) {
+            a.sl_counts[par1 * a.NR + b] = n;
+            if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
+        }
+        asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");   // (region complete)
+        const uint64_t dsum = write_descriptors<true>(a, t1, b, n, region, region_rows, stage, false, sid_s,
+                                                      ptid, pth, kSynthSid, stage_words);
+        if (ptid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
+    }
+    __syncthreads();
 }
 
 struct Win { uint4 a, b; };                          // one delivery window (kWin entries; b: kWin = 16)
@@ -1352,10 +1398,11 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         // tile bt = blockIdx.x / C; with C > 1 this CTA is rank c of the tile's cluster
         const uint32_t bt = b / a.C, c = b % a.C;
         phase_mark(a, 0);
-        // Programmatic dependent launch: the next step's kernel may be scheduled as soon as
-        // every CTA of this one runs; it zeroes its counters and prefetches its state while
-        // this one finishes, then waits (griddepcontrol.wait) for this grid's completion
-        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        // Programmatic dependent launch: the next step's kernel may be scheduled once every
+        // CTA of this one has passed its own grid dependency (launch_dependents after
+        // griddepcontrol.wait below, so at most two step kernels ever overlap); it zeroes its
+        // counters and computes what needs no input while this one finishes, then waits
+        // (griddepcontrol.wait) for this grid's completion
         // (G > 1: the update of t+1 only writes the send bitmap; the lists and descriptors of
         //  the gathered spikes come from bitmap->list)
         if (threadIdx.x == 0) {   // this slice's neuron state (+ input slot t+1) -> L2 while delivering
@@ -1377,31 +1424,9 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         __shared__ uint32_t s_fire[MODEL == 4 ? kFireWords : 1];
         const bool syn = MODEL == 4 && a.G == 1 && a.TWs <= 32u * kFireWords && a.prod_words > kSynthSid;
         uint32_t *sid_s = syn ? sm.prod : sm.stage + kStageWords;
-        if (syn) {
-            // step t + 1's spikes, record bitmap, counters and descriptors, all before the grid
-            // dependency: they touch only step t + 1's buffers (record slot, list parity,
-            // descriptor buffer (t + 1) mod 3, counter (t + 1) mod 4), none of which the
-            // previous kernel (delivering t - 1, publishing t) reads or writes
-            synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid);
-            __syncthreads();
-            const uint32_t n = s_count;
-            const uint64_t t1 = t + 1;
-            uint32_t *bm = a.record + mod32(t1, a.record_steps) * (uint64_t)a.W;
-            const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
-            for (uint32_t x = threadIdx.x; x < nwd; x += kBlock) bm[(lo >> 5) + x] = s_fire[x];
-            const uint32_t par1 = (uint32_t)(t1 & 1);
-            if (threadIdx.x == 0) {
-                a.sl_counts[par1 * a.NR + b] = n;
-                if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
-            }
-            uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
-            uint64_t *region_rows = a.sl_rows + ((uint64_t)par1 * a.NR + b) * a.RS;
-            const uint64_t dsum = write_descriptors(a, t1, b, n, region, region_rows, sm.stage, true, sid_s,
-                                                    threadIdx.x, kBlock, kSynthSid);
-            if (threadIdx.x == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
-            phase_mark(a, 9);
-        }
+        if (syn) synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid);   // shared memory only
         asm volatile("griddepcontrol.wait;" ::: "memory");          // the previous step is complete
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         // thread 0: the step's descriptor count
         const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t & 3u] : 0xFFFFFFFFu;
         __syncthreads();
@@ -1414,7 +1439,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             // barrier; a second one at exit keeps every CTA's counters alive until then)
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
             phase_mark(a, 6);
-            if (syn) synth_accumulate(a, t + 1, lo, a.TWs, cnt, a.C > 1 ? c : kMaxCluster);
+            if (syn) synth_publish_and_accumulate(a, t, b, lo, cnt, a.C > 1 ? c : kMaxCluster, s_fire, sid_s, s_count,
+                                                  sm.prod + kSynthSid, a.prod_words - kSynthSid);
             else
                 update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, a.G == 1, &s_count, sm.stage, nullptr, true,
                                          a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
@@ -1434,7 +1460,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             }
             if (syn) {
                 __syncthreads();                             // (the slot's ring writes above)
-                synth_accumulate(a, t + 1, lo, a.TWs, nullptr, kMaxCluster);
+                synth_publish_and_accumulate(a, t, b, lo, nullptr, kMaxCluster, s_fire, sid_s, s_count,
+                                             sm.prod + kSynthSid, a.prod_words - kSynthSid);
             } else {
                 update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, a.G == 1, &s_count, sm.stage, nullptr, true,
                                          kMaxCluster, sm.stage + kStageWords);
