@@ -690,6 +690,74 @@ __device__ __forceinline__ void synth_accumulate(const SimArgs &a, uint64_t t1, 
     }
 }
 
+// Synth fast path, producer warps: in the prologue (the spike IDs of step t + 1 are known,
+// the descriptor buffer and counter of t + 1 are free: the kernels that used them finished
+// before this one could launch) reserve the step's slots in the dense per-tile lists and
+// start the cp.async copies of the spiking rows' segment bounds, row starts and out-degrees;
+// they land while the CTA delivers.  Only when the rows fit one staging pass (else the
+// general write_descriptors runs at the end).
+struct SynthStage { uint32_t rs4, CH; };
+__device__ __forceinline__ SynthStage synth_stage(const SimArgs &a, uint32_t stage_words) {
+    const DescStage ds = desc_stage(a);
+    return SynthStage{ds.rs4, max(1u, stage_words / (ds.rs4 + 3u))};
+}
+__device__ __forceinline__ void synth_rows_prefetch(const SimArgs &a, uint64_t t1, uint32_t n, const uint32_t *sid_s,
+                                                    uint32_t *stage, uint32_t stage_words, uint32_t ptid, uint32_t pth,
+                                                    uint32_t *s_off) {
+    const SynthStage ss = synth_stage(a, stage_words);
+    if (n == 0 || n > ss.CH || n > kSynthSid) return;
+    const uint32_t lane = ptid & 31, warp = ptid >> 5, nwp = pth / 32, rowlen = a.NT + 1u;
+    if (ptid == 0) *s_off = atomicAdd(&a.dcount[t1 & 3u], n);
+    uint64_t *srow = reinterpret_cast<uint64_t *>(stage + ss.CH * ss.rs4);
+    uint32_t *sdeg = reinterpret_cast<uint32_t *>(srow + ss.CH);
+    const uint4 *bnd4 = reinterpret_cast<const uint4 *>(a.bnd);
+    for (uint32_t ql = warp; ql < n; ql += nwp) {
+        const uint32_t sj = sid_s[ql];
+        const uint64_t g0 = (uint64_t)sj * rowlen;
+        const uint64_t k0 = g0 >> 2, nk = ((g0 + rowlen - 1) >> 2) - k0 + 1;
+        for (uint32_t kk = lane; kk < nk; kk += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" :: "r"(smem_u32(stage + ql * ss.rs4 + 4u * kk)), "l"(bnd4 + k0 + kk) : "memory");
+        if (lane == 0) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(srow + ql)), "l"(a.row_ptr + sj) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(sdeg + ql)), "l"(a.deg + sj) : "memory");
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+// ... and at the end of the step: wait for the copies, write the descriptors.  Returns the
+// spikes' delivered-event count (valid in producer warp 0).
+__device__ __forceinline__ uint64_t synth_descriptors(const SimArgs &a, uint64_t t1, uint32_t n, const uint32_t *sid_s,
+                                                      uint64_t *region_rows, uint32_t *stage, uint32_t stage_words,
+                                                      uint32_t ptid, uint32_t pth, uint32_t off) {
+    const SynthStage ss = synth_stage(a, stage_words);
+    const uint32_t lane = ptid & 31, warp = ptid >> 5, nwp = pth / 32, rowlen = a.NT + 1u;
+    uint64_t *srow = reinterpret_cast<uint64_t *>(stage + ss.CH * ss.rs4);
+    uint32_t *sdeg = reinterpret_cast<uint32_t *>(srow + ss.CH);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
+    uint64_t dsum = 0;
+    if (warp == 0)
+        for (uint32_t ql = lane; ql < n; ql += 32) { region_rows[ql] = srow[ql]; dsum += sdeg[ql]; }
+    const uint32_t dbuf = (uint32_t)mod32(t1, 3);
+    for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+        const uint32_t ql = j0 + lane;
+        if (ql < n) {
+            const uint32_t rsw = (uint32_t)(srow[ql] >> kWinShift);
+            const uint32_t sj = sid_s[ql];
+            const uint32_t ih = sj >= a.n_exc ? 0x80000000u : 0u;
+            const uint32_t *row = stage + ql * ss.rs4 + (uint32_t)(((uint64_t)sj * rowlen) & 3u);
+            uint2 *dst = reinterpret_cast<uint2 *>(a.desc + (uint64_t)dbuf * a.NT * a.dstride + off + ql);
+            for (uint32_t bb = warp; bb < a.NT; bb += nwp) {
+                const uint32_t lo = row[bb], hi = row[bb + 1];
+                dst[(uint64_t)bb * a.dstride] = make_uint2(rsw + (lo >> kWinShift), ((hi - lo) >> kWinShift) | ih);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xFFFFFFFFu, dsum, o);
+    return dsum;
+}
+
 // The end of a synth fast-path step: warps [0, kAccWarps) add the step's input to the
 // accumulators while the other warps publish step t + 1 (record bitmap, spike list and
 // counts, descriptors of its spiking rows) -- after delivery, when the memory system is
@@ -698,10 +766,11 @@ constexpr uint32_t kAccWarps = 24;
 __device__ __forceinline__ void synth_publish_and_accumulate(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo,
                                                              const uint32_t *cnt, uint32_t cl_c, const uint32_t *s_fire,
                                                              const uint32_t *sid_s, uint32_t n, uint32_t *stage,
-                                                             uint32_t stage_words) {
+                                                             uint32_t stage_words, uint32_t s_off) {
     const uint32_t warp = threadIdx.x >> 5;
     if (warp < kAccWarps) {
         synth_accumulate(a, t + 1, lo, a.TWs, cnt, cl_c, threadIdx.x, kAccWarps * 32);
+        phase_mark(a, 7);
     } else {
         const uint32_t ptid = threadIdx.x - kAccWarps * 32, pth = kBlock - kAccWarps * 32;
         const uint64_t t1 = t + 1;
@@ -728,9 +797,13 @@ __device__ __forceinline__ void synth_publish_and_accumulate(const SimArgs &a, u
             if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
         }
         asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");   // (region complete)
-        const uint64_t dsum = write_descriptors<true>(a, t1, b, n, region, region_rows, stage, false, sid_s,
-                                                      ptid, pth, kSynthSid, stage_words);
+        phase_mark(a, 8, kAccWarps * 32);
+        const bool staged = n > 0 && n <= synth_stage(a, stage_words).CH && n <= kSynthSid;   // (synth_rows_prefetch)
+        const uint64_t dsum = staged ? synth_descriptors(a, t1, n, sid_s, region_rows, stage, stage_words, ptid, pth, s_off)
+                                     : write_descriptors<true>(a, t1, b, n, region, region_rows, stage, true, sid_s,
+                                                               ptid, pth, kSynthSid, stage_words);
         if (ptid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
+        phase_mark(a, 9, kAccWarps * 32);
     }
     __syncthreads();
 }
@@ -1424,7 +1497,14 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         __shared__ uint32_t s_fire[MODEL == 4 ? kFireWords : 1];
         const bool syn = MODEL == 4 && a.G == 1 && a.TWs <= 32u * kFireWords && a.prod_words > kSynthSid;
         uint32_t *sid_s = syn ? sm.prod : sm.stage + kStageWords;
-        if (syn) synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid);   // shared memory only
+        __shared__ uint32_t s_off;
+        if (syn) {                                           // (shared memory and async copies only)
+            synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid);
+            __syncthreads();
+            if ((threadIdx.x >> 5) >= kAccWarps)
+                synth_rows_prefetch(a, t + 1, s_count, sid_s, sm.prod + kSynthSid, a.prod_words - kSynthSid,
+                                    threadIdx.x - kAccWarps * 32, kBlock - kAccWarps * 32, &s_off);
+        }
         asm volatile("griddepcontrol.wait;" ::: "memory");          // the previous step is complete
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         // thread 0: the step's descriptor count
@@ -1440,7 +1520,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
             phase_mark(a, 6);
             if (syn) synth_publish_and_accumulate(a, t, b, lo, cnt, a.C > 1 ? c : kMaxCluster, s_fire, sid_s, s_count,
-                                                  sm.prod + kSynthSid, a.prod_words - kSynthSid);
+                                                  sm.prod + kSynthSid, a.prod_words - kSynthSid, s_off);
             else
                 update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, a.G == 1, &s_count, sm.stage, nullptr, true,
                                          a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
@@ -1461,7 +1541,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             if (syn) {
                 __syncthreads();                             // (the slot's ring writes above)
                 synth_publish_and_accumulate(a, t, b, lo, nullptr, kMaxCluster, s_fire, sid_s, s_count,
-                                             sm.prod + kSynthSid, a.prod_words - kSynthSid);
+                                             sm.prod + kSynthSid, a.prod_words - kSynthSid, s_off);
             } else {
                 update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, a.G == 1, &s_count, sm.stage, nullptr, true,
                                          kMaxCluster, sm.stage + kStageWords);
