@@ -40,6 +40,7 @@
 #include <string.h>
 #include <math.h>
 
+#define ORC_TRACE_LEN 8192    /* closed-form trace table length (reading R13) */
 #ifndef ORC_REAL
 #define ORC_REAL float
 #endif
@@ -149,12 +150,18 @@ typedef struct {
     uint64_t *in_edge;
     uint32_t *edge_src;
     /* state (SoA) */
-    real *v, *ge, *gi, *xtr, *ytr;
+    real *v, *ge, *gi;
+    /* STDP traces in event-driven closed form (reading R13): per neuron the step of its last
+     * spike (-1 none) and the pre / post trace values just after it, cx = X(ts) + 1,
+     * cy = Y(ts) + 1; X(t) = cx P+[t - ts], Y(t) = cy P-[t - ts] */
+    int64_t *ts;
+    real *cx, *cy;
+    real *pp, *pm;                    /* P+[k] = exp(-k dt / tau+), P-[k], k < ORC_TRACE_LEN */
     uint32_t *ref, *acc;
     uint32_t *ring;                   /* D x n packed receptor counts (R10) */
     int64_t *pring;                   /* D x n plastic fixed-point sums (R10) */
     /* derived scalars */
-    real h, ke, ki, dge, dgi, JE, JI, ap, am, Ap, Am, wmax;
+    real h, ke, ki, dge, dgi, JE, JI, Ap, Am, wmax;
     real EL, Vt, Vr, Ee, Ei, theta;
     uint32_t R;
     uint64_t thr_fire;
@@ -409,7 +416,6 @@ EXPORT orc_net *orc_create(uint32_t model, uint32_t n, uint32_t n_exc,
         N->ptab_len = orc_poisson_table(P[7], N->ptab, 256);
         if (N->ptab_len == 0) { orc_free(N); return NULL; }
         if (model == ORC_BRUNEL_PLUS) {
-            N->ap = (real)exp(-dt_ms / P[10]); N->am = (real)exp(-dt_ms / P[11]);
             N->Ap = (real)P[12]; N->Am = (real)P[13]; N->wmax = (real)P[14];
         }
     } else if (model == ORC_SYNTH) {
@@ -418,7 +424,15 @@ EXPORT orc_net *orc_create(uint32_t model, uint32_t n, uint32_t n_exc,
 
     /* ---- state (SoA) ---- */
     N->v = xcalloc(n, sizeof(real)); N->ge = xcalloc(n, sizeof(real)); N->gi = xcalloc(n, sizeof(real));
-    N->xtr = xcalloc(n, sizeof(real)); N->ytr = xcalloc(n, sizeof(real));
+    N->ts = xcalloc(n, sizeof(int64_t));
+    for (uint32_t j = 0; j < n; j++) N->ts[j] = -1;
+    N->cx = xcalloc(n, sizeof(real)); N->cy = xcalloc(n, sizeof(real));
+    N->pp = xcalloc(ORC_TRACE_LEN, sizeof(real)); N->pm = xcalloc(ORC_TRACE_LEN, sizeof(real));
+    if (model == ORC_BRUNEL_PLUS)
+        for (uint32_t k = 0; k < ORC_TRACE_LEN; k++) {
+            N->pp[k] = (real)exp(-(double)k * dt_ms / P[10]);
+            N->pm[k] = (real)exp(-(double)k * dt_ms / P[11]);
+        }
     N->ref = xcalloc(n, sizeof(uint32_t)); N->acc = xcalloc(n, sizeof(uint32_t));
     N->ring = xcalloc((size_t)N->D * n, sizeof(uint32_t));
     N->pring = xcalloc((size_t)N->D * n, sizeof(int64_t));
@@ -465,7 +479,8 @@ EXPORT void orc_free(orc_net *N)
     if (!N) return;
     free(N->rules); free(N->row_ptr); free(N->tgt); free(N->plastic); free(N->w); free(N->dly);
     free(N->in_ptr); free(N->in_edge); free(N->edge_src);
-    free(N->v); free(N->ge); free(N->gi); free(N->xtr); free(N->ytr); free(N->ref); free(N->acc);
+    free(N->v); free(N->ge); free(N->gi); free(N->ts); free(N->cx); free(N->cy); free(N->pp); free(N->pm);
+    free(N->ref); free(N->acc);
     free(N->ring); free(N->pring); free(N->sp); free(N->sp_off); free(N->delivered); free(N->force_bits);
     free(N);
 }
@@ -546,6 +561,18 @@ static int update_neuron(orc_net *N, uint32_t j, uint64_t t, uint32_t c, int64_t
     return spiked;
 }
 
+/* Event-driven trace evaluation (reading R13): X_j(t) = cx_j P+[t - ts_j] for t > ts_j
+ * (one rounded product; P+[k] = exp(-k dt/tau+) computed in double, rounded once; 0 for
+ * k >= ORC_TRACE_LEN, where it is below 2^-24 of any trace); 0 before the first spike.
+ * The value excludes a spike at t itself (it is the sum over spikes t' < t). */
+static real trace_at(const orc_net *N, const real *c, const real *tab, uint32_t j, uint64_t t)
+{
+    if (N->ts[j] < 0) return (real)0;
+    uint64_t k = t - (uint64_t)N->ts[j];
+    if (k >= ORC_TRACE_LEN) return (real)0;
+    return c[j] * tab[k];
+}
+
 /* Fixed-point quantisation of a plastic weight (reading R10): rint(w 2^32). */
 static int64_t wq(real w) { return (int64_t)llrint((double)w * 4294967296.0); }
 
@@ -580,7 +607,7 @@ EXPORT int orc_step(orc_net *N, uint64_t n_steps)
                 uint32_t i = N->sp[q];
                 for (uint64_t a = N->in_ptr[i]; a < N->in_ptr[i + 1]; a++) {
                     uint64_t e = N->in_edge[a];
-                    real inc = N->Ap * N->xtr[N->edge_src[e]];
+                    real inc = N->Ap * trace_at(N, N->cx, N->pp, N->edge_src[e], t);
                     real w = N->w[e] + inc;
                     N->w[e] = w < N->wmax ? w : N->wmax;
                 }
@@ -589,7 +616,7 @@ EXPORT int orc_step(orc_net *N, uint64_t n_steps)
                 uint32_t j = N->sp[q];
                 for (uint64_t e = N->row_ptr[j]; e < N->row_ptr[j + 1]; e++) {
                     if (!N->plastic[e]) continue;
-                    real dec = N->Am * N->ytr[N->tgt[e]];
+                    real dec = N->Am * trace_at(N, N->cy, N->pm, N->tgt[e], t);
                     real w = N->w[e] - dec;
                     N->w[e] = w > (real)0 ? w : (real)0;
                 }
@@ -609,13 +636,13 @@ EXPORT int orc_step(orc_net *N, uint64_t n_steps)
             }
         }
         N->delivered[t] = events;
-        /* traces for the next step: x(t+1) = a (x(t) + [spiked at t]) (R13) */
+        /* traces: a spike at t restarts both closed forms from their value at t plus one (R13) */
         if (N->model == ORC_BRUNEL_PLUS) {
             for (uint32_t j = 0; j < n; j++) {
-                real xs = N->xtr[j] + (real)spk[j];
-                N->xtr[j] = N->ap * xs;
-                real ys = N->ytr[j] + (real)spk[j];
-                N->ytr[j] = N->am * ys;
+                if (!spk[j]) continue;
+                real xs = trace_at(N, N->cx, N->pp, j, t) + (real)1;
+                real ys = trace_at(N, N->cy, N->pm, j, t) + (real)1;
+                N->cx[j] = xs; N->cy[j] = ys; N->ts[j] = (int64_t)t;
             }
         }
         N->t = t + 1;
@@ -650,8 +677,8 @@ EXPORT int orc_get_state(const orc_net *N, uint32_t field, void *out)
     case 2: memcpy(out, N->gi, n * sizeof(real)); return 0;
     case 3: memcpy(out, N->ref, n * sizeof(uint32_t)); return 0;
     case 4: memcpy(out, N->acc, n * sizeof(uint32_t)); return 0;
-    case 5: memcpy(out, N->xtr, n * sizeof(real)); return 0;
-    case 6: memcpy(out, N->ytr, n * sizeof(real)); return 0;
+    case 5: for (size_t j = 0; j < n; j++) ((real *)out)[j] = trace_at(N, N->cx, N->pp, (uint32_t)j, N->t); return 0;
+    case 6: for (size_t j = 0; j < n; j++) ((real *)out)[j] = trace_at(N, N->cy, N->pm, (uint32_t)j, N->t); return 0;
     }
     return -1;
 }

@@ -661,3 +661,43 @@ def test_synth_checkers_with_per_synapse_delays():
     for j in range(0, 2000, 83):
         assert O.synth_acc(cfg, j, T) == int(acc[j])
     assert base.n == cfg.n
+
+
+# ------------------------------------------ event-driven STDP traces (reading R13)
+def test_stdp_traces_closed_form():
+    """Reading R13 (event-driven traces): after spikes at steps t_k the pre and post traces at
+    step T are X(T) = sum_{t_k < T} exp(-(T - t_k) dt / tau+) and Y(T) likewise with tau-
+    (ref64 within 1e-12; a spike at T itself is not yet counted)."""
+    prm = _brunel_params(JE=0.0, vlo=0.0, vhi=0.0) + (20.0, 35.0, 0.01, 0.0105, 1.0, 0.5)
+    cfg = _cfg(W.BRUNEL_PLUS, 2, 2, [W.Rule((0, 1), (1, 2), W.FIXED_PROB, 1.0, plastic=True)], prm)
+    net = O.OracleNet(cfg, "ref64")
+    times = [3, 4, 17, 60, 61, 200]
+    for t in range(260):
+        net.force_next([0] if t in times else [], "replace")
+        net.step(1)
+        T = t + 1
+        if T in (4, 18, 61, 150, 201, 260):
+            past = [tk for tk in times if tk < T]
+            for f, tau in ((O.F_XTR, 20.0), (O.F_YTR, 35.0)):
+                want = sum(np.exp(-(T - tk) * 0.1 / tau) for tk in past)
+                assert abs(net.state(f)[0] - want) < 1e-12, (T, f)
+            assert net.state(O.F_XTR)[1] == 0.0
+
+
+def test_stdp_cumulative_pair_sum():
+    """Pair STDP over spike trains (reading R13, no clamping): the final weight is
+    w0 + sum_post A+ X_pre(t_post) - sum_pre A- Y_post(t_pre), with the traces' closed
+    forms, potentiation before depression at equal steps (ref64 within 1e-12)."""
+    ap, am = 0.002, 0.0021
+    prm = _brunel_params(JE=0.0, vlo=0.0, vhi=0.0) + (20.0, 20.0, ap, am, 10.0, 0.5)
+    cfg = _cfg(W.BRUNEL_PLUS, 2, 2, [W.Rule((0, 1), (1, 2), W.FIXED_PROB, 1.0, plastic=True)], prm)
+    net = O.OracleNet(cfg, "ref64")
+    pre, post = [5, 30, 31, 90, 140], [10, 31, 32, 100, 141, 160]
+    for t in range(200):
+        ids = ([0] if t in pre else []) + ([1] if t in post else [])
+        net.force_next(ids, "replace")
+        net.step(1)
+    a = np.exp(-0.1 / 20.0)
+    tr = lambda ts, T: sum(a ** (T - x) for x in ts if x < T)
+    want = 0.5 + sum(ap * tr(pre, tp) for tp in post) - sum(am * tr(post, tq) for tq in pre)
+    assert abs(net.weights()[0] - want) < 1e-12
