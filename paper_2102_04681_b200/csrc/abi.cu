@@ -199,11 +199,11 @@ struct spice_net {
     uint64_t *force_ctl = nullptr;
     uint64_t *ptab = nullptr;
     // Brunel+
-    float *w = nullptr, *xtr = nullptr, *ytr = nullptr;
+    float *w = nullptr;
+    uint32_t *pre_ts = nullptr, *post = nullptr, *post_mask = nullptr;   // event-driven STDP state
+    float *pre_c = nullptr, *tab_p = nullptr, *tab_m = nullptr;
+    std::vector<float> htab_p, htab_m;     // host copies (trace read-out)
     long long *pring = nullptr;
-    uint64_t *in_ptr = nullptr;
-    uint32_t *in_pos = nullptr, *in_src = nullptr;
-    uint64_t n_plastic = 0;
     ModelConst mc{};
     SimArgs args{};
     // host progress
@@ -781,26 +781,39 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         GenGeom g2{};
         g2.N = n->N; g2.n_own = (uint32_t)n->n_own; g2.rank = n->rank; g2.G = n->G; g2.S = n->S;
         g2.TW = n->TW; g2.NT = n->NT; g2.key0 = (uint32_t)n->seed; g2.key1 = (uint32_t)(n->seed >> 32);
-        uint32_t *tmp = nullptr;
         if (n->nnz >= (1ull << 32))
-            return bail(fail(n, SPICE_EINVAL, "Brunel+ slices hold < 2^32 synapses per rank (32-bit in-synapse index); got %llu",
+            return bail(fail(n, SPICE_EINVAL, "Brunel+ slices hold < 2^32 synapses per rank (32-bit entry starts); got %llu",
                              (unsigned long long)n->nnz));
+        if (n->N / 1024 + 1 > 1486)                        // (flush-row list of one step, sim.cu kPlFlush)
+            return bail(fail(n, SPICE_EINVAL, "Brunel+ supports up to 1.5M neurons"));
         if ((st = dalloc_t(n, &n->w, n->nnz + 8, "plastic weights"))) return bail(st);
         if ((st = dalloc_t(n, &n->pring, (size_t)n->D * n->ring_stride, "plastic input ring"))) return bail(st);
-        if ((st = dalloc_t(n, &n->xtr, 2ull * n->N, "pre traces"))) return bail(st);
-        if ((st = dalloc_t(n, &n->ytr, no, "post traces"))) return bail(st);
-        if ((st = dalloc_t(n, &n->in_ptr, n->n_own + 1, "in-synapse index"))) return bail(st);
-        if ((st = dalloc_t(n, &tmp, std::max<uint64_t>(n->n_own, 1), "in-degree counts"))) return bail(st);
+        if ((st = dalloc_t(n, &n->pre_ts, 2ull * n->N, "pre spike steps"))) return bail(st);
+        if ((st = dalloc_t(n, &n->pre_c, 2ull * n->N, "pre traces"))) return bail(st);
+        if ((st = dalloc_t(n, &n->post, 2ull * 4 * no, "post spike history"))) return bail(st);
+        if ((st = dalloc_t(n, &n->post_mask, 64ull * no, "post spike bit rings"))) return bail(st);
+        if ((st = dalloc_t(n, &n->tab_p, 8192, "pre trace table"))) return bail(st);
+        if ((st = dalloc_t(n, &n->tab_m, 8192, "post trace table"))) return bail(st);
         CU(n, cudaMemsetAsync(n->pring, 0, (size_t)n->D * n->ring_stride * 8, s));
-        CU(n, cudaMemsetAsync(n->xtr, 0, 2ull * n->N * 4, s));
-        CU(n, cudaMemsetAsync(n->ytr, 0, no * 4, s));
-        CU(n, gen_plastic_count(g2, pbx, n->row_ptr, n->bnd, n->ent, n->w, (float)n->prm[15], tmp, n->in_ptr,
-                                &n->n_plastic, s));
-        if ((st = dalloc_t(n, &n->in_pos, std::max<uint64_t>(n->n_plastic, 1), "in-synapse positions"))) return bail(st);
-        if ((st = dalloc_t(n, &n->in_src, std::max<uint64_t>(n->n_plastic, 1), "in-synapse sources"))) return bail(st);
-        CU(n, gen_plastic_fill(g2, pbx, n->row_ptr, n->bnd, n->ent, tmp, n->in_ptr, n->in_pos, n->in_src, s));
+        CU(n, cudaMemsetAsync(n->pre_ts, 0xFF, 2ull * n->N * 4, s));          // no spike yet
+        CU(n, cudaMemsetAsync(n->pre_c, 0, 2ull * n->N * 4, s));
+        {
+            std::vector<uint32_t> init(4 * no);
+            for (uint64_t i = 0; i < no; ++i) { init[4 * i] = init[4 * i + 1] = init[4 * i + 2] = 0xFFFFFFFFu; init[4 * i + 3] = 0u; }
+            CU(n, cudaMemcpy(n->post, init.data(), init.size() * 4, cudaMemcpyHostToDevice));
+            CU(n, cudaMemcpy(n->post + 4 * no, init.data(), init.size() * 4, cudaMemcpyHostToDevice));
+        }
+        CU(n, cudaMemsetAsync(n->post_mask, 0, 64ull * no * 4, s));
+        // closed-form trace tables (reading R13): exp(-k dt / tau) in double, rounded once
+        n->htab_p.resize(8192); n->htab_m.resize(8192);
+        for (uint32_t k = 0; k < 8192; ++k) {
+            n->htab_p[k] = (float)std::exp(-(double)k * n->dt / n->prm[10]);
+            n->htab_m[k] = (float)std::exp(-(double)k * n->dt / n->prm[11]);
+        }
+        CU(n, cudaMemcpy(n->tab_p, n->htab_p.data(), 8192 * 4, cudaMemcpyHostToDevice));
+        CU(n, cudaMemcpy(n->tab_m, n->htab_m.data(), 8192 * 4, cudaMemcpyHostToDevice));
+        CU(n, gen_plastic_weights(g2, pbx, n->row_ptr, n->bnd, n->ent, n->w, (float)n->prm[15], s));
         CU(n, cudaStreamSynchronize(s));
-        dfree(n, tmp);
     }
     build_model_const(n);
     GenGeom g{};
@@ -860,8 +873,9 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.record = n->record; a.sendbuf = n->sendbuf;
     a.gather = n->gather; a.fired_cta = n->fired_cta; a.delivered_cta = n->delivered_cta;
     a.t0 = n->t0; a.force_bits = n->force_bits; a.force_ctl = n->force_ctl;
-    a.w = n->w; a.pring = n->pring; a.xtr = n->xtr; a.ytr = n->ytr;
-    a.in_ptr = n->in_ptr; a.in_pos = n->in_pos; a.in_src = n->in_src;
+    a.w = n->w; a.pring = n->pring;
+    a.pre_ts = n->pre_ts; a.pre_c = n->pre_c; a.post = n->post; a.post_mask = n->post_mask;
+    a.tab_p = n->tab_p; a.tab_m = n->tab_m;
     a.npl = pbx.n;
     memcpy(a.pl, pbx.box, sizeof a.pl);
     CU(n, prepare_kernels(a));
@@ -1198,8 +1212,8 @@ static spice_status field_ptr(spice_net *n, uint32_t field, void **p) {
     case SPICE_FIELD_GI: *p = n->gi; break;
     case SPICE_FIELD_REF: *p = n->model != SPICE_SYNTH ? n->ref : nullptr; break;
     case SPICE_FIELD_ACC: *p = n->acc; break;
-    case SPICE_FIELD_XTR: *p = n->xtr; break;
-    case SPICE_FIELD_YTR: *p = n->ytr; break;
+    case SPICE_FIELD_XTR: *p = n->pre_c; break;
+    case SPICE_FIELD_YTR: *p = n->post; break;
     default: break;
     }
     if (!*p) return fail(n, SPICE_EINVAL, "field %u not present for model %u", field, n->model);
@@ -1213,10 +1227,33 @@ spice_status spice_read_state(spice_net *n, uint32_t field, void *out, uint64_t 
     if (st) return st;
     if (count != n->n_own) return fail(n, SPICE_EINVAL, "n = %llu, owned = %llu", (unsigned long long)count, (unsigned long long)n->n_own);
     CU(n, cudaStreamSynchronize(n->stream));
-    if (field == SPICE_FIELD_XTR) {           // global pre traces of the current parity
-        std::vector<float> x(n->N);
-        CU(n, cudaMemcpy(x.data(), n->xtr + (n->t_host & 1) * (uint64_t)n->N, n->N * 4ull, cudaMemcpyDeviceToHost));
-        for (uint64_t i = 0; i < count; ++i) ((float *)out)[i] = x[local_to_global(i, n->rank, n->G, n->S)];
+    // traces in event-driven form (reading R13): X(t) = c P[t - ts], evaluated here at
+    // t = steps done with the device's operation (one rounded float product)
+    auto tr = [&](float c, uint32_t ts, const std::vector<float> &tab) -> float {
+        if (ts == 0xFFFFFFFFu) return 0.0f;
+        const uint64_t k = n->t_host - ts;
+        return k < tab.size() ? c * tab[k] : 0.0f;
+    };
+    if (field == SPICE_FIELD_XTR) {           // pre traces of the owned neurons (global arrays)
+        const uint64_t par = n->t_host & 1;
+        std::vector<float> c(n->N);
+        std::vector<uint32_t> ts(n->N);
+        CU(n, cudaMemcpy(c.data(), n->pre_c + par * n->N, n->N * 4ull, cudaMemcpyDeviceToHost));
+        CU(n, cudaMemcpy(ts.data(), n->pre_ts + par * n->N, n->N * 4ull, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < count; ++i) {
+            const uint64_t j = local_to_global(i, n->rank, n->G, n->S);
+            ((float *)out)[i] = tr(c[j], ts[j], n->htab_p);
+        }
+        return SPICE_OK;
+    }
+    if (field == SPICE_FIELD_YTR) {           // post traces (post history, parity of t)
+        std::vector<uint32_t> h(4 * count);
+        if (count) CU(n, cudaMemcpy(h.data(), n->post + (n->t_host & 1) * 4 * n->ring_stride, count * 16, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < count; ++i) {
+            float c;
+            memcpy(&c, &h[4 * i + 3], 4);
+            ((float *)out)[i] = tr(c, h[4 * i], n->htab_m);
+        }
         return SPICE_OK;
     }
     if (count) CU(n, cudaMemcpy(out, p, count * 4, cudaMemcpyDeviceToHost));
@@ -1230,14 +1267,8 @@ spice_status spice_write_state(spice_net *n, uint32_t field, const void *in, uin
     if (st) return st;
     if (count != n->n_own) return fail(n, SPICE_EINVAL, "n = %llu, owned = %llu", (unsigned long long)count, (unsigned long long)n->n_own);
     CU(n, cudaStreamSynchronize(n->stream));
-    if (field == SPICE_FIELD_XTR) {           // global pre traces of the current parity (mirrors read)
-        float *dst = n->xtr + (n->t_host & 1) * (uint64_t)n->N;
-        std::vector<float> x(n->N);
-        CU(n, cudaMemcpy(x.data(), dst, n->N * 4ull, cudaMemcpyDeviceToHost));
-        for (uint64_t i = 0; i < count; ++i) x[local_to_global(i, n->rank, n->G, n->S)] = ((const float *)in)[i];
-        CU(n, cudaMemcpy(dst, x.data(), n->N * 4ull, cudaMemcpyHostToDevice));
-        return SPICE_OK;
-    }
+    if (field == SPICE_FIELD_XTR || field == SPICE_FIELD_YTR)
+        return fail(n, SPICE_EINVAL, "STDP traces are event-driven state (last spike step + value): read-only");
     if (count) CU(n, cudaMemcpy(p, in, count * 4, cudaMemcpyHostToDevice));
     return SPICE_OK;
 }
@@ -1268,8 +1299,17 @@ spice_status spice_read_weights(spice_net *n, uint32_t row_begin, uint32_t row_e
     const uint64_t tot = rp[1] - rp[0];
     if (total) *total = tot;
     if (tot > cap || (!w && tot)) return fail(n, SPICE_ETRUNC, "need %llu weights", (unsigned long long)tot);
-    if (tot) CU(n, cudaMemcpy(w, n->w + rp[0], tot * 4, cudaMemcpyDeviceToHost));
-    for (uint64_t q = 0; q < tot; ++q) if (w[q] < 0.0f) w[q] = 0.0f;   // static synapses' sentinel
+    if (tot) {
+        // the eager rule's weights: stored weights plus the rows' pending (lazy) potentiations
+        float *dv = nullptr;
+        spice_status st2 = dalloc_t(n, &dv, tot, "weight read-out");
+        if (st2) return st2;
+        CU(n, launch_settle_weights(n->args, n->t_host, row_begin, row_end, dv, n->stream));
+        CU(n, cudaMemcpyAsync(w, dv, tot * 4, cudaMemcpyDeviceToHost, n->stream));
+        CU(n, cudaStreamSynchronize(n->stream));
+        dfree(n, dv);
+        n->device_bytes -= tot * 4;
+    }
     return SPICE_OK;
 }
 

@@ -424,14 +424,9 @@ __device__ __forceinline__ bool is_plastic(const PlasticBoxes &pb, uint32_t s, u
         if (s >= pb.box[q][0] && s < pb.box[q][1] && j >= pb.box[q][2] && j < pb.box[q][3]) return true;
     return false;
 }
-// MODE 0: weights (w0 on plastic synapses, 0 elsewhere) and in-degree counts;
-// MODE 1: fill the in-synapse index (absolute entry, source) through per-target cursors.
-template <int MODE>
-__global__ void __launch_bounds__(256) plastic_kernel(GenGeom g, PlasticBoxes pb, const uint64_t *row_ptr,
-                                                      const uint32_t *bnd, const uint16_t *ent, float *w,
-                                                      float w0, uint32_t *cnt_or_cursor,
-                                                      const uint64_t *in_ptr, uint32_t *in_pos,
-                                                      uint32_t *in_src) {
+__global__ void __launch_bounds__(256) plastic_weights_kernel(GenGeom g, PlasticBoxes pb, const uint64_t *row_ptr,
+                                                              const uint32_t *bnd, const uint16_t *ent, float *w,
+                                                              float w0) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t)gridDim.x * 8;
     for (uint64_t q = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); q < (uint64_t)g.N * g.NT; q += nwarps) {
@@ -441,44 +436,14 @@ __global__ void __launch_bounds__(256) plastic_kernel(GenGeom g, PlasticBoxes pb
         const uint32_t len = bp[1] - bp[0];
         for (uint32_t e = lane; e < len; e += 32) {
             const uint32_t il = b * g.TW + (ent[st + e] >> g.eshift);
-            const bool pl = is_plastic(pb, s, (uint32_t)local_to_global(il, g.rank, g.G, g.S));
-            if (MODE == 0) {
-                w[st + e] = pl ? w0 : -1.0f;         // static synapses: negative sentinel
-                if (pl) atomicAdd(&cnt_or_cursor[il], 1u);
-            } else if (pl) {
-                const uint64_t k = in_ptr[il] + atomicAdd(&cnt_or_cursor[il], 1u);
-                in_pos[k] = (uint32_t)(st + e);
-                in_src[k] = s;
-            }
+            w[st + e] = is_plastic(pb, s, (uint32_t)local_to_global(il, g.rank, g.G, g.S)) ? w0 : -1.0f;
         }
     }
 }
-__global__ void u32_to_u64(const uint32_t *in, uint64_t n, uint64_t *out) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        out[i] = in[i];
-}
 
-cudaError_t gen_plastic_count(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
-                              const uint32_t *bnd, const uint16_t *ent, float *w, float w0,
-                              uint32_t *tmp_cnt, uint64_t *in_ptr, uint64_t *n_plastic, cudaStream_t s) {
-    cudaError_t e;
-    const uint64_t pairs = (uint64_t)g.N * g.NT;
-    if ((e = cudaMemsetAsync(tmp_cnt, 0, (size_t)g.n_own * 4, s))) return e;
-    plastic_kernel<0><<<grid_for(pairs, 8), 256, 0, s>>>(g, pb, row_ptr, bnd, ent, w, w0, tmp_cnt, nullptr, nullptr, nullptr);
-    u32_to_u64<<<grid_for(g.n_own, 256), 256, 0, s>>>(tmp_cnt, g.n_own, in_ptr);
-    if ((e = cudaGetLastError())) return e;
-    if ((e = gen_scan_u64(in_ptr, g.n_own, s))) return e;
-    if ((e = cudaMemcpyAsync(n_plastic, in_ptr + g.n_own, 8, cudaMemcpyDeviceToHost, s))) return e;
-    return cudaStreamSynchronize(s);
-}
-
-cudaError_t gen_plastic_fill(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
-                             const uint32_t *bnd, const uint16_t *ent, uint32_t *tmp_cnt,
-                             const uint64_t *in_ptr, uint32_t *in_pos, uint32_t *in_src, cudaStream_t s) {
-    cudaError_t e;
-    const uint64_t pairs = (uint64_t)g.N * g.NT;
-    if ((e = cudaMemsetAsync(tmp_cnt, 0, (size_t)g.n_own * 4, s))) return e;
-    plastic_kernel<1><<<grid_for(pairs, 8), 256, 0, s>>>(g, pb, row_ptr, bnd, ent, nullptr, 0.0f, tmp_cnt, in_ptr, in_pos, in_src);
+cudaError_t gen_plastic_weights(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
+                                const uint32_t *bnd, const uint16_t *ent, float *w, float w0, cudaStream_t s) {
+    plastic_weights_kernel<<<grid_for((uint64_t)g.N * g.NT, 8), 256, 0, s>>>(g, pb, row_ptr, bnd, ent, w, w0);
     return cudaGetLastError();
 }
 

@@ -23,6 +23,8 @@
 // Floating point: every operation of the neuron update is an explicit round-to-nearest
 // intrinsic in the order fixed by DESIGN.md readings R3-R5 (no contraction), so results
 // are bit-identical to the fp32 oracle.
+#include <algorithm>
+
 #include "spice_internal.cuh"
 #include "spice_launch.h"
 
@@ -354,6 +356,8 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
 // DESC = true: compile only the padded-layout descriptor path (the fused G = 1 kernel's
 // variants), keeping the inlined code on the hot path small (instruction-fetch stalls were
 // the largest stall class of the fused kernel, ncu r01u).
+__device__ __forceinline__ void post_state_update(const SimArgs &a, uint64_t t, uint32_t i0, uint32_t nib);   // (Brunel+)
+
 template <int MODEL, bool DESC = false>
 __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                             const uint32_t *cnt, bool write_list, uint32_t *s_count, uint32_t *stage,
@@ -441,6 +445,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
 #endif
             }
             nib = update4<MODEL>(a, sp, t, lo + x4, c, pin, ptab, acc_done || acc_pf, forced);
+            if constexpr (MODEL == 3) post_state_update(a, t, lo + x4, nib);
         }
         // 8 lanes x 4 bits -> one 32-neuron bitmap word
         uint32_t w = nib << (4u * (lane & 7u));
@@ -856,7 +861,6 @@ __device__ __forceinline__ void deliver_ring_core(const SimArgs &a, uint64_t t, 
     constexpr uint32_t NONE = 0xFFFFFFFFu;
     constexpr uint32_t FULL = 0xFFFFFFFFu;
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t par = (uint32_t)(t & 1);
     const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
     const uint32_t my = n_sp > c ? (n_sp - c + a.C - 1u) / a.C : 0u;
     const uint32_t v0 = (uint32_t)((uint64_t)my * warp / NW), v1 = (uint32_t)((uint64_t)my * (warp + 1) / NW);
@@ -962,12 +966,24 @@ __device__ __forceinline__ void deliver_tile_ring(const SimArgs &a, uint64_t t, 
 }
 
 // ------------------------------------------------------------- Brunel+ STDP
-// Reading R13 (eager, in the oracle's order): (i) every post spike i of this tile at step
-// t potentiates its plastic in-synapses w += A+ x_pre(t) (clamped at w_max); (ii) the
-// delivery walk depresses every plastic synapse of a spiking pre w -= A- y_post(t)
-// (clamped at 0) and then delivers w as int64 fixed point rint(w 2^32) (reading R10);
-// (iii) traces advance x(t+1) = a+ (x(t) + s(t)), y likewise.  Every synapse touched by
-// CTA b has its target in tile b, so no two CTAs write the same weight.
+// Reading R13 with event-driven traces: every neuron keeps the step ts of its last spike and
+// the trace values just after it (pre: cx = X(ts) + 1 for all N sources, post: cy for the
+// owned targets), a trace is read as c P[t - ts].  The eager rule -- (i) every post spike at
+// t_p potentiates w += A+ X_pre(t_p) (clamp w_max), (ii) every pre spike at t depresses
+// w -= A- Y_post(t) (clamp 0), (iii) w is delivered -- is evaluated LAZILY on the synapse
+// stream (north star: "STDP weight updates run on the same synapse stream"): a row is
+// processed when its source spikes (potentiation by the post spikes since the row's last
+// processing, then depression and delivery) and, so that the post-spike history stays
+// bounded, at a fixed flush step every kFlush steps (potentiation only).  Between two
+// processings of a row nothing else touches its weights, so every weight sees exactly the
+// eager sequence of fp32 operations: GPU == oracle bit for bit.  Post-spike history per
+// owned neuron: its last three spike steps (in the post state) and a 2048-step bit ring.
+// Every synapse touched by CTA b has its target in tile b: no two CTAs write one weight.
+constexpr uint32_t kTraceLen = 8192;      // closed-form trace table (== ORC_TRACE_LEN)
+constexpr uint32_t kFlush = 1024;         // row flush period (steps)
+constexpr uint32_t kHistWords = 64;       // post-spike bit ring: 2048 steps per neuron
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
 __device__ __forceinline__ const uint32_t *step_bitmap(const SimArgs &a, uint64_t t) {
     return a.record + mod32(t, a.record_steps) * (uint64_t)a.G * a.W + (uint64_t)a.rank * a.W;
 }
@@ -977,108 +993,6 @@ __device__ __forceinline__ bool plastic_src(const SimArgs &a, uint32_t s) {
         if (s >= a.pl[q][0] && s < a.pl[q][1]) return true;
     return false;
 }
-__device__ __forceinline__ bool plastic_edge(const SimArgs &a, uint32_t s, uint32_t j) {
-    for (uint32_t q = 0; q < a.npl; ++q)
-        if (s >= a.pl[q][0] && s < a.pl[q][1] && j >= a.pl[q][2] && j < a.pl[q][3]) return true;
-    return false;
-}
-
-// (i) potentiation.  The tile's post spikes of step t are gathered into a shared list
-// with the start of their in-synapse index ranges and an exclusive prefix of their
-// in-degrees; the flat (spike, in-synapse) index space is then spread over all threads,
-// U independent synapses per thread with every load issued before the stores (a synapse
-// is touched at most once per step, so the read-modify-writes never conflict).  Falls
-// back to one warp per bitmap word when the list does not fit the staging area.
-__device__ __forceinline__ void potentiate_tile(const SimArgs &a, uint64_t t, uint32_t b,
-                                                uint32_t *stage, uint32_t *tmp) {
-    constexpr int U = 4;
-    const uint32_t *bm = step_bitmap(a, t);
-    const float *x = a.xtr + (t & 1) * (uint64_t)a.N;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t lo = b * a.TW, hi = min(lo + a.TW, a.n_own);
-    const uint32_t cap = ((uint32_t)kStageWords - 2u) / 4u;
-    uint64_t *base = reinterpret_cast<uint64_t *>(stage);      // [cap] in-synapse range starts
-    uint32_t *pre = stage + 2 * cap;                            // [cap + 1] in-degree prefix
-    __shared__ uint32_t s_np;
-    if (tid == 0) s_np = 0;
-    __syncthreads();
-    for (uint32_t wi = lo / 32 + tid; wi < (hi + 31) / 32; wi += kBlock) {
-        uint32_t word = bm[wi];
-        while (word) {
-            const uint32_t i = wi * 32 + __ffs(word) - 1;
-            word &= word - 1;
-            const uint32_t k = atomicAdd(&s_np, 1u);
-            if (k < cap) { base[k] = a.in_ptr[i]; pre[k] = (uint32_t)(a.in_ptr[i + 1] - a.in_ptr[i]); }
-        }
-    }
-    __syncthreads();
-    const uint32_t np = s_np;
-    if (np == 0) return;
-    if (np <= cap) {
-        block_exclusive_scan(pre, np, tmp);
-        const uint32_t total = pre[np];
-        for (uint32_t f0 = tid; f0 < total; f0 += kBlock * U) {
-            uint32_t pos[U];
-            uint32_t src[U];
-            bool ok[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t f = f0 + u * kBlock;
-                ok[u] = f < total;
-                if (ok[u]) {
-                    uint32_t l = 0, h = np;                     // largest k with pre[k] <= f
-                    while (h - l > 1) { const uint32_t m = (l + h) >> 1; if (pre[m] <= f) l = m; else h = m; }
-                    const uint64_t e = base[l] + (f - pre[l]);
-                    pos[u] = a.in_pos[e];
-                    src[u] = a.in_src[e];
-                }
-            }
-            float wv[U], xv[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) if (ok[u]) { wv[u] = a.w[pos[u]]; xv[u] = x[src[u]]; }
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (ok[u]) {
-                    const float nw = __fadd_rn(wv[u], __fmul_rn(a.mc.Ap, xv[u]));
-                    a.w[pos[u]] = nw < a.mc.wmax ? nw : a.mc.wmax;
-                }
-        }
-        return;                                              // (the caller's barrier orders (i) before (ii))
-    }
-    for (uint32_t wi = lo / 32 + warp; wi < (hi + 31) / 32; wi += kBlock / 32) {
-        uint32_t word = bm[wi];
-        while (word) {
-            const uint32_t i = wi * 32 + __ffs(word) - 1;
-            word &= word - 1;
-            for (uint64_t e = a.in_ptr[i] + lane; e < a.in_ptr[i + 1]; e += 32) {
-                const uint32_t pos = a.in_pos[e];
-                const float wv = __fadd_rn(a.w[pos], __fmul_rn(a.mc.Ap, x[a.in_src[e]]));
-                a.w[pos] = wv < a.mc.wmax ? wv : a.mc.wmax;
-            }
-        }
-    }
-}
-
-__device__ __forceinline__ void stdp_traces(const SimArgs &a, uint64_t t, uint32_t b) {
-    const uint32_t *bm = step_bitmap(a, t);
-    const uint32_t lo = b * a.TW, hi = min(lo + a.TW, a.n_own);
-    for (uint32_t i = lo + threadIdx.x; i < hi; i += kBlock) {
-        const float sp = (bm[i >> 5] >> (i & 31)) & 1u ? 1.0f : 0.0f;
-        a.ytr[i] = __fmul_rn(a.mc.am, __fadd_rn(a.ytr[i], sp));
-    }
-    // pre traces of every global source: CTA b advances slice b of [0, N)
-    const float *xo = a.xtr + (t & 1) * (uint64_t)a.N;
-    float *xn = a.xtr + ((t + 1) & 1) * (uint64_t)a.N;
-    const uint32_t per = (a.N + a.NT * a.C - 1) / (a.NT * a.C);
-    const uint32_t j0 = blockIdx.x * per, j1 = min(a.N, j0 + per);
-    const uint32_t *gbm = a.record + mod32(t, a.record_steps) * (uint64_t)a.G * a.W;
-    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kBlock) {
-        const uint32_t r = (j / a.S) % a.G;
-        const uint32_t il = (j / a.S / a.G) * a.S + j % a.S;
-        const float sp = (gbm[(uint64_t)r * a.W + (il >> 5)] >> (il & 31)) & 1u ? 1.0f : 0.0f;
-        xn[j] = __fmul_rn(a.mc.ap, __fadd_rn(xo[j], sp));
-    }
-}
 
 // Global spike bit of source j in the gathered bitmaps of step t (Listing 1 inverse).
 __device__ __forceinline__ bool spiked_global(const SimArgs &a, const uint32_t *gbm, uint32_t j) {
@@ -1087,29 +1001,106 @@ __device__ __forceinline__ bool spiked_global(const SimArgs &a, const uint32_t *
     return (gbm[(uint64_t)r * a.W + (il >> 5)] >> (il & 31)) & 1u;
 }
 
-// (i)-(iii) of a step for tile b as ONE flattened event space spread over all threads:
-//   delivery events: every (segment, entry) of the step's spiking rows into tile b.
-//     Consecutive events of a segment are consecutive threads (entry and weight loads
-//     coalesce).  A plastic synapse (weight >= 0; static ones hold the sentinel -1) whose
-//     post neuron also spiked at t is first potentiated (w = min(w_max, w + A+ x_pre(t))),
-//     then depressed (w = max(0, w - A- y_post(t))), stored and delivered as fixed point
-//     rint(w 2^32), summed exactly in two u32 shared words (low word with carry detection
-//     from the returned old value: native 32-bit shared atomics, no 64-bit CAS loop);
-//     static synapses add their packed receptor count.
-//   potentiation events: CTA b's equal share of the step's global (post spike, plastic
-//     in-synapse) space, so a tile with many post spikes does not stall the step.  The
-//     in-synapses whose pre neuron also spiked at t are skipped here (their delivery
-//     event potentiates them first), so the two event sets touch disjoint weights and
-//     need no ordering: every weight sees exactly the eager oracle's operations in its
-//     order (reading R13).
-// Segments are staged kPlSeg spikes per pass; a step with more spikes than one pass holds
-// falls back to tile-local potentiation (potentiate_tile) before the delivery passes.
-constexpr uint32_t kPlSeg = 1900;                     // spikes staged per pass (6 words each)
-constexpr uint32_t kPlU = 4;                          // events in flight per thread
+// c P[t - ts]: one rounded product (0 before the first spike and past the table)
+__device__ __forceinline__ float trace_val(float c, uint32_t ts, uint64_t t, const float *tab) {
+    if (ts == kNone) return 0.0f;
+    const uint64_t k = t - ts;
+    return k < kTraceLen ? __fmul_rn(c, tab[k]) : 0.0f;
+}
+
+// The step of row j's last processing before step t: its last spike (< t) or its last
+// flush step (< t, steps congruent to j mod kFlush); -1 before any.
+__device__ __forceinline__ int64_t row_tproc(uint32_t j, uint64_t t, uint32_t ts_j) {
+    int64_t tp = ts_j == kNone ? -1 : (int64_t)ts_j;
+    const uint64_t ph = j % kFlush;
+    if (t >= 1 && t - 1 >= ph) {
+        const int64_t f = (int64_t)(t - 1) - (int64_t)((t - 1 - ph) % kFlush);
+        if (f > tp) tp = f;
+    }
+    return tp;
+}
+
+// One potentiation at post spike step tp with the row's pre state (ts_j, cx_j).
+__device__ __forceinline__ float potentiate_at(const SimArgs &a, float w, uint64_t tp, uint32_t ts_j, float cx_j) {
+    const float x = trace_val(cx_j, ts_j, tp, a.tab_p);
+    const float nw = __fadd_rn(w, __fmul_rn(a.mc.Ap, x));
+    return nw < a.mc.wmax ? nw : a.mc.wmax;
+}
+
+// Lazy potentiation of one synapse: the post neuron's spikes in (tproc, t], in time order.
+// pl = its last three spike steps up to and including t (most recent first, kNone = none);
+// older ones come from its bit ring `mask` (only when all three are inside the window).
+__device__ __forceinline__ float potentiate_lazy(const SimArgs &a, float w, int64_t tproc, uint32_t ts_j, float cx_j,
+                                                 uint32_t p1, uint32_t p2, uint32_t p3, const uint32_t *mask) {
+    if (ts_j == kNone || p1 == kNone || (int64_t)p1 <= tproc) return w;     // X = 0 / no post spike
+    if (p3 != kNone && (int64_t)p3 > tproc) {
+        for (uint64_t s = (uint64_t)(tproc + 1); s < p3;) {                  // spikes before p3
+            const uint32_t wi = (uint32_t)((s >> 5) % kHistWords);
+            const uint32_t b0 = (uint32_t)(s & 31u);
+            const uint64_t wend = (s | 31u) + 1;                             // first step of the next word
+            const uint32_t nb = (uint32_t)((wend < p3 ? wend : (uint64_t)p3) - s);   // bits b0 .. b0 + nb - 1
+            uint32_t bits = mask[wi] >> b0;
+            if (nb < 32) bits &= (1u << nb) - 1u;
+            while (bits) {
+                const uint32_t k = __ffs(bits) - 1;
+                bits &= bits - 1u;
+                w = potentiate_at(a, w, s + k, ts_j, cx_j);
+            }
+            s = wend;
+        }
+    }
+    if (p3 != kNone && (int64_t)p3 > tproc) w = potentiate_at(a, w, p3, ts_j, cx_j);
+    if (p2 != kNone && (int64_t)p2 > tproc) w = potentiate_at(a, w, p2, ts_j, cx_j);
+    return potentiate_at(a, w, p1, ts_j, cx_j);
+}
+
+// Pre state of every global source for step t + 1 (CTA slices of [0, N)): a source that
+// spiked at t restarts its trace, cx = X(t) + 1 (the oracle's event-driven update).
+__device__ __forceinline__ void pre_state_pass(const SimArgs &a, uint64_t t) {
+    const uint32_t *gbm = a.record + mod32(t, a.record_steps) * (uint64_t)a.G * a.W;
+    const uint32_t *ots = a.pre_ts + (t & 1) * (uint64_t)a.N;
+    const float *oc = a.pre_c + (t & 1) * (uint64_t)a.N;
+    uint32_t *nts = a.pre_ts + ((t + 1) & 1) * (uint64_t)a.N;
+    float *nc = a.pre_c + ((t + 1) & 1) * (uint64_t)a.N;
+    const uint32_t per = (a.N + gridDim.x - 1) / gridDim.x;
+    const uint32_t j0 = blockIdx.x * per, j1 = min(a.N, j0 + per);
+    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kBlock) {
+        uint32_t ts = ots[j];
+        float c = oc[j];
+        if (spiked_global(a, gbm, j)) {
+            c = __fadd_rn(trace_val(c, ts, t, a.tab_p), 1.0f);
+            ts = (uint32_t)t;
+        }
+        nts[j] = ts;
+        nc[j] = c;
+    }
+}
+
+// Post state of the owned neurons [i0, i0 + 4) at their update of step t (spike nibble):
+// last three spike steps and cy, double-buffered by step parity; the bit ring word of t is
+// rewritten at every 32-step boundary and or-ed on a spike.
+__device__ __forceinline__ void post_state_update(const SimArgs &a, uint64_t t, uint32_t i0, uint32_t nib) {
+    const uint4 *o = reinterpret_cast<const uint4 *>(a.post) + (t & 1) * a.ring_stride + i0;
+    uint4 *n = reinterpret_cast<uint4 *>(a.post) + ((t + 1) & 1) * a.ring_stride + i0;
+    const uint32_t wi = (uint32_t)((t >> 5) % kHistWords), bit = (uint32_t)(t & 31u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (i0 + e >= a.n_own) break;
+        uint4 st = o[e];
+        const bool s = (nib >> e) & 1u;
+        if (s) {
+            const float y = trace_val(__uint_as_float(st.w), st.x, t, a.tab_m);
+            st = make_uint4((uint32_t)t, st.x, st.y, __float_as_uint(__fadd_rn(y, 1.0f)));
+        }
+        n[e] = st;
+        uint32_t *m = a.post_mask + (uint64_t)(i0 + e) * kHistWords + wi;
+        if (bit == 0) *m = s ? 1u : 0u;
+        else if (s) *m |= 1u << bit;
+    }
+}
 
 __device__ __forceinline__ void plastic_deliver(const SimArgs &a, uint32_t *cnt, uint32_t *plo, uint32_t *phi,
-                                                const float *ys, const uint32_t *tb, uint32_t e, uint32_t off,
-                                                uint32_t fl, float wv, float xpre, bool pot_first,
+                                                const float *ys, uint32_t e, uint32_t off, uint32_t fl, float wv,
                                                 uint32_t tD, uint64_t tile_base) {
     uint64_t gslot = ~0ull;                          // longer per-synapse delay: ring slot t + d
     if (a.dly) {
@@ -1121,10 +1112,6 @@ __device__ __forceinline__ void plastic_deliver(const SimArgs &a, uint32_t *cnt,
         }
     }
     if (wv >= 0.0f) {
-        if (pot_first && ((tb[off >> 5] >> (off & 31)) & 1u)) {   // post spiked at t as well: (i) first
-            const float pw = __fadd_rn(wv, __fmul_rn(a.mc.Ap, xpre));
-            wv = pw < a.mc.wmax ? pw : a.mc.wmax;
-        }
         float nw = __fsub_rn(wv, __fmul_rn(a.mc.Am, ys[off]));     // (ii)
         nw = nw > 0.0f ? nw : 0.0f;
         a.w[e] = nw;
@@ -1143,7 +1130,24 @@ __device__ __forceinline__ void plastic_deliver(const SimArgs &a, uint32_t *cnt,
     }
 }
 
-struct PlasticSmem { uint32_t *cnt, *plo, *phi; float *ys; uint32_t *tb, *pref, *tmp, *stage; };
+struct PlasticSmem {
+    uint32_t *cnt, *plo, *phi;     // [TW] counters, fixed-point low / high words
+    float *ys;                     // [TW] Y(t) of the tile's neurons
+    uint32_t *p1, *p2, *p3;        // [TW] their last three spike steps up to t
+    uint32_t *pref, *tmp, *stage;
+};
+
+// (i)-(iii) of step t for tile b, one flattened event space over all threads: the
+// (segment, entry) pairs of the step's spiking rows and of its flush rows into tile b.
+// Consecutive events of a segment are consecutive threads (entry and weight loads coalesce).
+// Plastic synapses (weight >= 0; static ones hold the sentinel -1): lazy potentiation, then
+// on spike rows depression, store and delivery as fixed point rint(w 2^32) summed exactly in
+// two u32 shared words (low word with carry detection: native 32-bit shared atomics); on
+// flush rows the potentiated weight is stored.  Static synapses of spike rows add their
+// packed receptor count.
+constexpr uint32_t kPlSeg = 1800;                     // segments staged per pass (6 words each)
+constexpr uint32_t kPlFlush = kStageWords - 6 * kPlSeg - 2;   // flush-row list capacity
+constexpr uint32_t kPlU = 4;                          // events in flight per thread
 
 __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b,
                                                          const PlasticSmem &sm, bool marks = false) {
@@ -1152,125 +1156,170 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
     uint32_t *pref = sm.pref, *tmp = sm.tmp, *stage = sm.stage;
     const uint32_t *bm = step_bitmap(a, t);
     const uint32_t *gbm = a.record + mod32(t, a.record_steps) * (uint64_t)a.G * a.W;
-    const float *xo = a.xtr + (t & 1) * (uint64_t)a.N;
+    const uint32_t *pts = a.pre_ts + (t & 1) * (uint64_t)a.N;
+    const float *pc = a.pre_c + (t & 1) * (uint64_t)a.N;
+    const uint64_t tile_base = (uint64_t)b * a.TW;
     for (uint32_t r = tid; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
-    // the tile's post traces y and post spike bits of step t
-    for (uint32_t x = tid; x < a.TW; x += kBlock) sm.ys[x] = b * a.TW + x < a.n_own ? a.ytr[b * a.TW + x] : 0.0f;
-    for (uint32_t x = tid; x < a.TW / 32; x += kBlock) sm.tb[x] = b * a.TW + 32 * x < a.n_own ? bm[b * a.TW / 32 + x] : 0u;
-    __syncthreads();
-    block_exclusive_scan(pref, a.NR, tmp);
-    const uint32_t n_sp = pref[a.NR];
-    const bool merged = n_sp <= kPlSeg;
-    if (!merged) {                                    // (i) tile-local, before every delivery pass
-        potentiate_tile(a, t, b, stage, tmp);
-        __syncthreads();
+    // the tile's post neurons before step t's spikes (post state parity t) plus their spike at t
+    const uint4 *post = reinterpret_cast<const uint4 *>(a.post) + (t & 1) * a.ring_stride + tile_base;
+    for (uint32_t x = tid; x < a.TW; x += kBlock) {
+        float y = 0.0f;
+        uint32_t q1 = kNone, q2 = kNone, q3 = kNone;
+        if (tile_base + x < a.n_own) {
+            const uint4 st = post[x];
+            y = trace_val(__uint_as_float(st.w), st.x, t, a.tab_m);
+            const uint32_t i = (uint32_t)tile_base + x;
+            if ((bm[i >> 5] >> (i & 31)) & 1u) { q1 = (uint32_t)t; q2 = st.x; q3 = st.y; }
+            else { q1 = st.x; q2 = st.y; q3 = st.z; }
+        }
+        sm.ys[x] = y; sm.p1[x] = q1; sm.p2[x] = q2; sm.p3[x] = q3;
     }
+    // flush rows of step t: plastic sources j = t mod kFlush + k kFlush that do not spike at t
+    __shared__ uint32_t s_nfl;
+    if (tid == 0) s_nfl = 0;
+    uint32_t *flist = stage + 6 * kPlSeg + 2;
+    __syncthreads();
+    {
+        const uint32_t ph = (uint32_t)(t % kFlush);
+        const uint32_t ncand = ph < a.N ? (a.N - ph + kFlush - 1) / kFlush : 0u;
+        for (uint32_t k = tid; k < ncand; k += kBlock) {
+            const uint32_t j = ph + k * kFlush;
+            if (plastic_src(a, j) && !spiked_global(a, gbm, j)) {
+                const uint32_t pos = atomicAdd(&s_nfl, 1u);
+                if (pos < kPlFlush) flist[pos] = j;
+            }
+        }
+    }
+    block_exclusive_scan(pref, a.NR, tmp);       // (its barriers also publish flist)
     if (marks) phase_mark(a, 2);
+    const uint32_t n_sp = pref[a.NR];
+    const uint32_t n_fl = min(s_nfl, kPlFlush);
+    const uint32_t nseg = n_sp + n_fl;
     const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
     const uint32_t tD = a.dly ? (uint32_t)mod32(t, a.D) : 0u;
     uint32_t *sst = stage, *slen = stage + kPlSeg, *sfl = stage + 2 * kPlSeg + 1;
     float *sx = reinterpret_cast<float *>(stage + 3 * kPlSeg + 1);
-    uint32_t *spre = stage + 4 * kPlSeg + 1, *sinb = stage + 5 * kPlSeg + 2;
+    uint32_t *sts = stage + 4 * kPlSeg + 1;
+    int32_t *stp = reinterpret_cast<int32_t *>(stage + 5 * kPlSeg + 1);
     uint32_t delivered = 0;
-    for (uint32_t q0 = 0; q0 < max(n_sp, 1u); q0 += kPlSeg) {
-        const uint32_t nq = min(kPlSeg, n_sp - q0);
+    for (uint32_t q0 = 0; q0 < nseg; q0 += kPlSeg) {
+        const uint32_t nq = min(kPlSeg, nseg - q0);
         __syncthreads();                          // previous pass done with the staging
         for (uint32_t q = tid; q < nq; q += kBlock) {
             const uint32_t p = q0 + q;
-            const uint32_t r = region_of(pref, a.NR, p);
-            const uint64_t slot = lbase + (uint64_t)r * a.RS + (p - pref[r]);
-            const uint32_t s = a.sl_ids[slot];
+            uint32_t s;
+            uint64_t rs;
+            uint32_t fl;
+            if (p < n_sp) {                       // spike row
+                const uint32_t r = region_of(pref, a.NR, p);
+                const uint64_t slot = lbase + (uint64_t)r * a.RS + (p - pref[r]);
+                s = a.sl_ids[slot];
+                rs = a.sl_rows[slot];
+                fl = 0u;
+            } else {                              // flush row
+                s = flist[p - n_sp];
+                rs = a.row_ptr[s];
+                fl = 4u;
+            }
             const uint32_t *bp = a.bnd + (uint64_t)s * (a.NT + 1u) + b;
             const uint32_t lo = bp[0], hi = bp[1];
             const bool pls = plastic_src(a, s);
-            sst[q] = (uint32_t)(a.sl_rows[slot] + lo);
+            sst[q] = (uint32_t)(rs + lo);
             slen[q] = hi - lo;
-            sfl[q] = (s >= a.n_exc ? 1u : 0u) | (pls ? 2u : 0u);
-            sx[q] = pls ? xo[s] : 0.0f;
-            uint32_t indeg = 0, inb = 0;
-            if (merged && (a.G == 1 || (s / a.S) % a.G == a.rank)) {     // owned post neuron
-                const uint32_t li = a.G == 1 ? s : (s / a.S / a.G) * a.S + s % a.S;
-                inb = (uint32_t)a.in_ptr[li];
-                indeg = (uint32_t)a.in_ptr[li + 1] - inb;
-            }
-            spre[q] = indeg;
-            sinb[q] = inb;
+            sfl[q] = fl | (s >= a.n_exc ? 1u : 0u) | (pls ? 2u : 0u);
+            const uint32_t ts_j = pls ? pts[s] : kNone;
+            sts[q] = ts_j;
+            sx[q] = pls ? pc[s] : 0.0f;
+            stp[q] = (int32_t)row_tproc(s, t, ts_j);
         }
         __syncthreads();
-        block_exclusive_scan(slen, nq, tmp);      // slen -> delivery-event prefix
-        if (merged) block_exclusive_scan(spre, nq, tmp);    // spre -> potentiation-event prefix
+        block_exclusive_scan(slen, nq, tmp);      // slen -> event prefix
         if (marks) phase_mark(a, 3);
         const uint32_t ne = slen[nq];
-        uint32_t p0 = 0, np = 0;
-        if (merged) {                             // this CTA's share of the step's potentiation
-            const uint32_t ep = spre[nq];
-            p0 = (uint32_t)((uint64_t)ep * blockIdx.x / gridDim.x);
-            np = (uint32_t)((uint64_t)ep * (blockIdx.x + 1) / gridDim.x) - p0;
-        }
-        if (tid == 0) delivered += ne;
-#ifdef SPICE_ABLATE_POT                               // diagnostics builds only (tools/phases.py)
-        np = 0;
-#endif
-#ifdef SPICE_ABLATE_DEL
-        const uint32_t ne_eff = 0;
-#else
-        const uint32_t ne_eff = ne;
-#endif
-        const uint32_t total = ne_eff + np;
-        for (uint32_t f0 = tid; f0 < total; f0 += kBlock * kPlU) {
-            uint32_t e[kPlU], x1[kPlU], fl[kPlU];
-            float wv[kPlU], xv[kPlU];
-            bool skip[kPlU];
+        for (uint32_t f0 = tid; f0 < ne; f0 += kBlock * kPlU) {
+            uint32_t e[kPlU], off[kPlU], l[kPlU];
+            float wv[kPlU];
 #pragma unroll
-            for (uint32_t u = 0; u < kPlU; ++u) {     // indices (shared memory) + first loads
+            for (uint32_t u = 0; u < kPlU; ++u) {     // indices (shared memory) + loads
                 const uint32_t f = f0 + u * kBlock;
-                fl[u] = 0xFFFFFFFFu;                  // none
-                if (f < ne_eff) {
-                    uint32_t l = 0, h = nq;           // largest q with slen[q] <= f
-                    while (h - l > 1) { const uint32_t m = (l + h) >> 1; if (slen[m] <= f) l = m; else h = m; }
-                    e[u] = sst[l] + (f - slen[l]);
-                    fl[u] = sfl[l];
-                    xv[u] = sx[l];
-                    x1[u] = a.ent[e[u]];
-                    wv[u] = (fl[u] & 2u) ? a.w[e[u]] : -1.0f;
-                } else if (f < total) {
-                    const uint32_t g = p0 + (f - ne_eff);
-                    uint32_t l = 0, h = nq;           // largest q with spre[q] <= g
-                    while (h - l > 1) { const uint32_t m = (l + h) >> 1; if (spre[m] <= g) l = m; else h = m; }
-                    const uint32_t ein = sinb[l] + (g - spre[l]);
-                    fl[u] = 4u;                       // potentiation event
-                    e[u] = a.in_pos[ein];
-                    x1[u] = a.in_src[ein];
+                l[u] = kNone;
+                if (f < ne) {
+                    uint32_t lo = 0, h = nq;          // largest q with slen[q] <= f
+                    while (h - lo > 1) { const uint32_t m = (lo + h) >> 1; if (slen[m] <= f) lo = m; else h = m; }
+                    l[u] = lo;
+                    e[u] = sst[lo] + (f - slen[lo]);
+                    off[u] = a.ent[e[u]];
+                    wv[u] = (sfl[lo] & 2u) ? a.w[e[u]] : -1.0f;
                 }
             }
-#pragma unroll
-            for (uint32_t u = 0; u < kPlU; ++u)       // potentiation: second-level loads
-                if (fl[u] == 4u) {
-                    skip[u] = spiked_global(a, gbm, x1[u]);
-                    wv[u] = a.w[e[u]];
-                    xv[u] = xo[x1[u]];
-                }
 #pragma unroll
             for (uint32_t u = 0; u < kPlU; ++u) {
-                if (fl[u] == 0xFFFFFFFFu) continue;
-                if (fl[u] == 4u) {
-                    if (!skip[u]) {
-                        const float nw = __fadd_rn(wv[u], __fmul_rn(a.mc.Ap, xv[u]));
-                        a.w[e[u]] = nw < a.mc.wmax ? nw : a.mc.wmax;
-                    }
+                if (l[u] == kNone) continue;
+                const uint32_t fl = sfl[l[u]];
+                float w = wv[u];
+                if (w >= 0.0f)                        // (i), lazily: post spikes since the last processing
+                    w = potentiate_lazy(a, w, stp[l[u]], sts[l[u]], sx[l[u]], sm.p1[off[u]], sm.p2[off[u]],
+                                        sm.p3[off[u]], a.post_mask + (tile_base + off[u]) * kHistWords);
+                if (fl & 4u) {                        // flush row: potentiation only
+                    if (w >= 0.0f && w != wv[u]) a.w[e[u]] = w;
                 } else {
-                    plastic_deliver(a, sm.cnt, sm.plo, sm.phi, sm.ys, sm.tb, e[u], x1[u], fl[u], wv[u], xv[u], merged,
-                                    tD, (uint64_t)b * a.TW);
+                    plastic_deliver(a, sm.cnt, sm.plo, sm.phi, sm.ys, e[u], off[u], fl, w, tD, tile_base);
                 }
             }
         }
-        if (n_sp == 0) break;
+        // delivered events: the spike rows' entries of this pass
+        if (tid == 0) {
+            const uint32_t sp_end = n_sp > q0 ? min(nq, n_sp - q0) : 0u;
+            delivered += slen[sp_end];
+        }
     }
     __syncthreads();
     if (marks) phase_mark(a, 4);
-    stdp_traces(a, t, b);
+    pre_state_pass(a, t);
     if (marks) phase_mark(a, 5);
     return delivered;
+}
+
+// Weights as the eager rule has them after the steps done (t_now = steps completed): the
+// stored weight plus the row's pending potentiations (post spikes since its last
+// processing), for the entries of rows [row_lo, row_hi) in storage order; static synapses
+// read 0.  The stored state is left untouched (the lazy schedule stays the same).
+__global__ void __launch_bounds__(256) k_settle_weights(SimArgs a, uint64_t t_now, uint32_t row_lo, uint32_t row_hi,
+                                                        float *out) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * 8;
+    const uint32_t *pts = a.pre_ts + (t_now & 1) * (uint64_t)a.N;
+    const float *pc = a.pre_c + (t_now & 1) * (uint64_t)a.N;
+    const uint4 *post = reinterpret_cast<const uint4 *>(a.post) + (t_now & 1) * a.ring_stride;
+    const uint64_t base0 = a.row_ptr[row_lo];
+    for (uint64_t q = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); q < (uint64_t)(row_hi - row_lo) * a.NT; q += nwarps) {
+        const uint32_t s = row_lo + (uint32_t)(q / a.NT), b = (uint32_t)(q % a.NT);
+        const uint32_t *bp = a.bnd + (uint64_t)s * (a.NT + 1) + b;
+        const uint64_t st = a.row_ptr[s] + bp[0];
+        const uint32_t len = bp[1] - bp[0];
+        const bool pls = plastic_src(a, s);
+        const uint32_t ts_j = pls ? pts[s] : kNone;
+        const float cx = pls ? pc[s] : 0.0f;
+        const int64_t tproc = row_tproc(s, t_now, ts_j);
+        for (uint32_t e = lane; e < len; e += 32) {
+            float w = a.w[st + e];
+            if (w >= 0.0f) {
+                const uint32_t il = b * a.TW + a.ent[st + e];
+                const uint4 ps = post[il];
+                w = potentiate_lazy(a, w, tproc, ts_j, cx, ps.x, ps.y, ps.z, a.post_mask + (uint64_t)il * kHistWords);
+            } else {
+                w = 0.0f;
+            }
+            out[st + e - base0] = w;
+        }
+    }
+}
+cudaError_t launch_settle_weights(const SimArgs &a, uint64_t t_now, uint32_t row_lo, uint32_t row_hi, float *out,
+                                  cudaStream_t s) {
+    const uint64_t work = (uint64_t)(row_hi - row_lo) * a.NT;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((work + 7) / 8, 148ull * 16);
+    if (grid) k_settle_weights<<<grid, 256, 0, s>>>(a, t_now, row_lo, row_hi, out);
+    return cudaGetLastError();
 }
 
 // Padded-layout delivery of tile b (CTA c of C): byte-offset or counter-index entries.
@@ -1326,7 +1375,7 @@ size_t tile_smem_bytes(uint32_t TW, uint32_t NR, uint32_t prod_words) {
 // ([TW] each), region prefix, scan tmp, staging.
 size_t plastic_smem_bytes(uint32_t TW, uint32_t NR) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
-    return ((size_t)4 * tw4 + ((TW / 32 + 3) & ~3u) + ((NR + 1 + 3) & ~3u) + 32 + kStageWords) * 4 + 16;
+    return ((size_t)7 * tw4 + ((NR + 1 + 3) & ~3u) + 32 + kStageWords) * 4 + 16;
 }
 __device__ __forceinline__ PlasticSmem carve_plastic(const SimArgs &a, uint32_t *smem) {
     PlasticSmem sm;
@@ -1335,8 +1384,10 @@ __device__ __forceinline__ PlasticSmem carve_plastic(const SimArgs &a, uint32_t 
     sm.plo = smem + tw4;
     sm.phi = smem + 2 * tw4;
     sm.ys = reinterpret_cast<float *>(smem + 3 * tw4);
-    sm.tb = smem + 4 * tw4;
-    sm.pref = sm.tb + ((a.TW / 32 + 3) & ~3u);
+    sm.p1 = smem + 4 * tw4;
+    sm.p2 = smem + 5 * tw4;
+    sm.p3 = smem + 6 * tw4;
+    sm.pref = smem + 7 * tw4;
     sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
     sm.stage = sm.tmp + 32;
     return sm;

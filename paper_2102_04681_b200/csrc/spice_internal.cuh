@@ -156,11 +156,13 @@ struct SimArgs {
     // y for owned neurons, and per-target in-synapse index (absolute entry, source).
     float *w;
     long long *pring;        // D * ring_stride, rint(w 2^32) sums
-    float *xtr;              // 2 * N
-    float *ytr;              // ring_stride
-    const uint64_t *in_ptr;  // [n_own + 1]
-    const uint32_t *in_pos;  // entry index of each plastic in-synapse (nnz < 2^32 for Brunel+)
-    const uint32_t *in_src;
+    // event-driven STDP state (reading R13), double-buffered by step parity:
+    uint32_t *pre_ts;        // [2][N] step of every source's last spike (~0 = none)
+    float *pre_c;            // [2][N] its pre trace just after that spike, X(ts) + 1
+    uint32_t *post;          // [2][ring_stride] uint4 per owned neuron: last three spike
+                             // steps (most recent first) and cy = Y(ts) + 1 (float bits)
+    uint32_t *post_mask;     // [ring_stride][64] post-spike bit ring (2048 steps)
+    const float *tab_p, *tab_m;   // [8192] exp(-k dt / tau+-), rounded once
     uint32_t npl;                                  // plastic boxes (src x dst ranges)
     uint32_t pl[kMaxPlasticRules][4];
     const uint64_t *t0;      // step index of the first step of this graph replay

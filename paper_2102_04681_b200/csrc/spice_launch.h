@@ -17,6 +17,8 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
 cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s);
+cudaError_t launch_settle_weights(const SimArgs &a, uint64_t t_now, uint32_t row_lo, uint32_t row_hi, float *out,
+                                  cudaStream_t s);
 cudaError_t launch_peer_signal(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_peer_wait(const SimArgs &a, uint32_t k, cudaStream_t s);
 size_t small_smem_bytes(uint32_t tile_width, uint32_t model);
@@ -58,14 +60,9 @@ struct PlasticBoxes {
     uint32_t n;
     uint32_t box[kMaxPlasticRules][4];
 };
-// Weights (w0 on plastic synapses), per-target plastic in-degrees -> in_ptr (exclusive
-// prefix, in_ptr[n_own] = *n_plastic; synchronises), then the in-synapse index itself.
-cudaError_t gen_plastic_count(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
-                              const uint32_t *bnd, const uint16_t *ent, float *w, float w0,
-                              uint32_t *tmp_cnt, uint64_t *in_ptr, uint64_t *n_plastic, cudaStream_t s);
-cudaError_t gen_plastic_fill(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
-                             const uint32_t *bnd, const uint16_t *ent, uint32_t *tmp_cnt,
-                             const uint64_t *in_ptr, uint32_t *in_pos, uint32_t *in_src, cudaStream_t s);
+// Weights: w0 on plastic synapses, the sentinel -1 on static ones.
+cudaError_t gen_plastic_weights(const GenGeom &g, const PlasticBoxes &pb, const uint64_t *row_ptr,
+                                const uint32_t *bnd, const uint16_t *ent, float *w, float w0, cudaStream_t s);
 // Per-synapse delays (reading R19): every stored entry (padding sentinels: dmin) gets the
 // delay of its (source, target) pair under the rule that contains it.
 struct DelayRules {

@@ -116,8 +116,9 @@ def test_user_stream_and_torch_allocator(S):
 
 
 def test_write_state_round_trip(S):
-    """spice_write_state mirrors spice_read_state for every field, including the
-    double-buffered, globally indexed pre traces at an odd step."""
+    """spice_write_state mirrors spice_read_state for every writable field, at an even and
+    an odd step; the STDP traces are event-driven state (reading R13) and reject writes
+    (the old trace write was wrong at odd steps)."""
     cfg = W.brunel_plus(2001, 0.1, seed=5)
     with S.Network(cfg, world_size=2, rank=1, external_exchange=True, tile_width=256) as net:
         rng = np.random.default_rng(0)
@@ -125,10 +126,13 @@ def test_write_state_round_trip(S):
             if t:
                 net.exchange_begin()            # one step; rank 0's bitmap stays all-zero
                 net.exchange_end()
-            for f in (S.FIELD_V, S.FIELD_XTR, S.FIELD_YTR):
-                x = rng.random(net.n_owned).astype(np.float32)
-                net.write_state(f, x)
-                assert np.array_equal(net.state(f), x), (t, f)
+            x = rng.random(net.n_owned).astype(np.float32)
+            net.write_state(S.FIELD_V, x)
+            assert np.array_equal(net.state(S.FIELD_V), x), t
+            for f in (S.FIELD_XTR, S.FIELD_YTR):          # event-driven traces: read-only
+                net.state(f)
+                with pytest.raises(S.SpiceError):
+                    net.write_state(f, x)
             r = rng.integers(0, 5, net.n_owned).astype(np.uint32)
             net.write_state(S.FIELD_REF, r)
             assert np.array_equal(net.state(S.FIELD_REF), r)
