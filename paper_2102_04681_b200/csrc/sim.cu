@@ -358,13 +358,21 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
 // the largest stall class of the fused kernel, ncu r01u).
 __device__ __forceinline__ void post_state_update(const SimArgs &a, uint64_t t, uint32_t i0, uint32_t nib);   // (Brunel+)
 
-template <int MODEL, bool DESC = false>
+// SUB: run by the pth threads ptid = 0 .. pth - 1 of a warp group (named barrier 1) while
+// the CTA's other warps deliver the current step (delay >= 2: the update of t + 1 does not
+// depend on the delivery of t -- the timestep grouping of P:290 inside one kernel).
+template <int MODEL, bool DESC = false, bool SUB = false>
 __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                             const uint32_t *cnt, bool write_list, uint32_t *s_count, uint32_t *stage,
                             const StatePtrs *staged = nullptr, bool marks = false,
-                            uint32_t cl_c = kMaxCluster, uint32_t *sid_s = nullptr, uint32_t *bm_s = nullptr) {
+                            uint32_t cl_c = kMaxCluster, uint32_t *sid_s = nullptr, uint32_t *bm_s = nullptr,
+                            uint32_t ptid = threadIdx.x, uint32_t pth = kBlock) {
+    auto sync = [&]() {
+        if constexpr (SUB) asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
+        else __syncthreads();
+    };
     const StatePtrs sp = staged ? *staged : global_state(a);
-    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    const uint32_t tid = ptid, lane = tid & 31;
     const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;   // bitmap coverage
     const uint32_t par = (uint32_t)(t & 1);
     uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
@@ -376,9 +384,9 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     __shared__ uint64_t s_ptab[kPtabSmem];
     const uint64_t *ptab = a.mc.ptab;
     if ((MODEL == 2 || MODEL == 3) && a.mc.ptab_len <= kPtabSmem) {
-        for (uint32_t x = tid; x < a.mc.ptab_len; x += kBlock) s_ptab[x] = a.mc.ptab[x];
+        for (uint32_t x = tid; x < a.mc.ptab_len; x += pth) s_ptab[x] = a.mc.ptab[x];
         ptab = s_ptab;
-        __syncthreads();
+        sync();
     }
     const bool acc_done = false;
     const int forced = a.force_ctl[0] == t ? (int)a.force_ctl[1] : 0;   // once per CTA, not per neuron
@@ -389,14 +397,14 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     uint4 acc_next = make_uint4(0u, 0u, 0u, 0u);
     if (acc_pf && 4u * tid < span && lo + 4u * tid < a.n_own)
         acc_next = *reinterpret_cast<const uint4 *>(a.acc + lo + 4u * tid);
-    for (uint32_t x0 = 0; x0 < span; x0 += 4u * kBlock) {      // uniform trip count per CTA
+    for (uint32_t x0 = 0; x0 < span; x0 += 4u * pth) {         // uniform trip count per CTA
         if (x0 + 4u * (tid & ~31u) >= span) continue;             // whole warp past the slice
         const uint32_t x4 = x0 + 4u * tid;
         uint32_t nib = 0;
         const bool act = x4 < span && lo + x4 < a.n_own;
         uint4 acc_cur = acc_next;
         if (acc_pf) {
-            const uint32_t xn = x4 + 4u * kBlock;
+            const uint32_t xn = x4 + 4u * pth;
             if (xn < span && lo + xn < a.n_own) acc_next = *reinterpret_cast<const uint4 *>(a.acc + lo + xn);
         }
         if (act) {
@@ -482,11 +490,11 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
             }
         }
     }
-    __syncthreads();
+    sync();
     if (marks) phase_mark(a, 7);
     if (staged) {                                          // staged state -> global (coalesced)
         const uint32_t nw = width / 4;
-        for (uint32_t x = tid; x < nw; x += kBlock) {
+        for (uint32_t x = tid; x < nw; x += pth) {
             const uint32_t g = lo + 4 * x;
             if (MODEL == 4) reinterpret_cast<uint4 *>(a.acc + g)[0] = reinterpret_cast<const uint4 *>(sp.acc)[x];
             if (MODEL != 4) reinterpret_cast<float4 *>(a.v + g)[0] = reinterpret_cast<const float4 *>(sp.v)[x];
@@ -494,16 +502,16 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
             if (MODEL == 1) reinterpret_cast<float4 *>(a.ge + g)[0] = reinterpret_cast<const float4 *>(sp.ge)[x];
             if (MODEL == 1) reinterpret_cast<float4 *>(a.gi + g)[0] = reinterpret_cast<const float4 *>(sp.gi)[x];
         }
-        __syncthreads();
+        sync();
     }
     const uint32_t n_tile = *s_count;
     if (tid == 0) {
         if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
         if (n_tile) atomicAdd(&a.fired_cta[b], (unsigned long long)n_tile);   // RED: no load on the path
     }
-    if (!DESC && write_list && !a.desc) {        // row starts of the spikes, all at once
-        uint32_t dsum = 0;                                // (the descriptor pass loads them itself)
-        for (uint32_t q = tid; q < n_tile; q += kBlock) {
+    if (!DESC && write_list && !a.desc && MODEL != 3) {   // row starts of the spikes, all at once
+        uint32_t dsum = 0;                                // (the descriptor pass loads them itself;
+        for (uint32_t q = tid; q < n_tile; q += pth) {    //  Brunel+ staging loads row_ptr itself)
             const uint32_t s = region[q];
             region_rows[q] = a.row_ptr[s];
             if (a.deg) dsum += a.deg[s];
@@ -513,16 +521,26 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
             for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xFFFFFFFFu, dsum, o);
             if (lane == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
         }
-        __syncthreads();
+        sync();
     }
     if (marks) phase_mark(a, 8);
     if (write_list && (DESC || a.desc)) {                 // padded layout: delivered events (out-degrees)
-        const uint64_t dsum = write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
+        uint64_t dsum;
+        if constexpr (SUB) dsum = write_descriptors<true>(a, t, b, n_tile, region, region_rows, stage, false, sid_s,
+                                                          ptid, pth);
+        else dsum = write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
         if (tid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
     }
     if (marks) phase_mark(a, 9);
-    __syncthreads();
+    sync();
     if (tid == 0) *s_count = 0;
+}
+
+template <int MODEL>
+__device__ __forceinline__ void update_tile_sub(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
+                                                uint32_t *s_count, uint32_t *stage, uint32_t ptid, uint32_t pth) {
+    update_tile<MODEL, false, true>(a, t, b, lo, width, nullptr, true, s_count, stage, nullptr, false, kMaxCluster,
+                                    nullptr, nullptr, ptid, pth);
 }
 
 // Eight unconditional shared-memory reductions of one padded 16-byte window (sentinel
@@ -1149,8 +1167,16 @@ constexpr uint32_t kPlSeg = 1800;                     // segments staged per pas
 constexpr uint32_t kPlFlush = kStageWords - 6 * kPlSeg - 2;   // flush-row list capacity
 constexpr uint32_t kPlU = 4;                          // events in flight per thread
 
+// upd_count != nullptr (fused kernel, delay >= 2, one staging pass): the last kUpdWarps warps
+// run the update of step t + 1 meanwhile (it reads input slot t + 1, complete since delay >= 2,
+// and post state parity t + 1, already staged) and *upd_done is set.
+constexpr uint32_t kUpdWarps = 8;
+template <int MODEL>
+__device__ __forceinline__ void update_tile_sub(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
+                                                uint32_t *s_count, uint32_t *stage, uint32_t ptid, uint32_t pth);
 __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b,
-                                                         const PlasticSmem &sm, bool marks = false) {
+                                                         const PlasticSmem &sm, bool marks = false,
+                                                         uint32_t *upd_count = nullptr, bool *upd_done = nullptr) {
     const uint32_t tid = threadIdx.x;
     const uint32_t par = (uint32_t)(t & 1);
     uint32_t *pref = sm.pref, *tmp = sm.tmp, *stage = sm.stage;
@@ -1214,13 +1240,12 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
                 const uint32_t r = region_of(pref, a.NR, p);
                 const uint64_t slot = lbase + (uint64_t)r * a.RS + (p - pref[r]);
                 s = a.sl_ids[slot];
-                rs = a.sl_rows[slot];
                 fl = 0u;
             } else {                              // flush row
                 s = flist[p - n_sp];
-                rs = a.row_ptr[s];
                 fl = 4u;
             }
+            rs = a.row_ptr[s];
             const uint32_t *bp = a.bnd + (uint64_t)s * (a.NT + 1u) + b;
             const uint32_t lo = bp[0], hi = bp[1];
             const bool pls = plastic_src(a, s);
@@ -1236,12 +1261,24 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
         block_exclusive_scan(slen, nq, tmp);      // slen -> event prefix
         if (marks) phase_mark(a, 3);
         const uint32_t ne = slen[nq];
-        for (uint32_t f0 = tid; f0 < ne; f0 += kBlock * kPlU) {
+        // (fused, delay >= 2, single pass) the update of t + 1 on the last kUpdWarps warps
+        const bool ovl = upd_count && a.delay >= 2 && nseg <= kPlSeg;
+        uint32_t etid = tid, eth = kBlock;
+        if (ovl) {
+            eth = kBlock - kUpdWarps * 32;
+            if (tid >= eth) {
+                update_tile_sub<3>(a, t + 1, b, b * a.TW, a.TW, upd_count, sm.stage + kStageWords - 64,
+                                   tid - eth, kUpdWarps * 32);
+                *upd_done = true;
+                continue;                         // (nseg <= kPlSeg: this was the only pass)
+            }
+        }
+        for (uint32_t f0 = etid; f0 < ne; f0 += eth * kPlU) {
             uint32_t e[kPlU], off[kPlU], l[kPlU];
             float wv[kPlU];
 #pragma unroll
             for (uint32_t u = 0; u < kPlU; ++u) {     // indices (shared memory) + loads
-                const uint32_t f = f0 + u * kBlock;
+                const uint32_t f = f0 + u * eth;
                 l[u] = kNone;
                 if (f < ne) {
                     uint32_t lo = 0, h = nq;          // largest q with slen[q] <= f
@@ -1505,12 +1542,16 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         phase_mark(a, 0);
         if (threadIdx.x == 0) s_count3 = 0;
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.plo[x] = 0u; sm.phi[x] = 0u; }
-        const uint32_t d = deliver_tile_plastic(a, t, b, sm, true);
+        __shared__ bool s_upd;
+        if (threadIdx.x == 0) s_upd = false;
+        __syncthreads();
+        const uint32_t d = deliver_tile_plastic(a, t, b, sm, true, &s_count3, &s_upd);
         plastic_flush(a, t, b, sm);
         store_delivered(a, b, d, sm.tmp);
         __syncthreads();
         phase_mark(a, 6);
-        update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count3, sm.stage, nullptr, true);
+        if (!s_upd)
+            update_tile<MODEL>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count3, sm.stage, nullptr, true);
         phase_mark(a, 12);
     } else {                                                 // padded layout (G = 1)
         extern __shared__ __align__(16) uint32_t smem[];
