@@ -366,7 +366,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
                             const uint32_t *cnt, bool write_list, uint32_t *s_count, uint32_t *stage,
                             const StatePtrs *staged = nullptr, bool marks = false,
                             uint32_t cl_c = kMaxCluster, uint32_t *sid_s = nullptr, uint32_t *bm_s = nullptr,
-                            uint32_t ptid = threadIdx.x, uint32_t pth = kBlock) {
+                            uint32_t ptid = threadIdx.x, uint32_t pth = kBlock, uint32_t stage_words = kStageWords) {
     auto sync = [&]() {
         if constexpr (SUB) asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
         else __syncthreads();
@@ -527,7 +527,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     if (write_list && (DESC || a.desc)) {                 // padded layout: delivered events (out-degrees)
         uint64_t dsum;
         if constexpr (SUB) dsum = write_descriptors<true>(a, t, b, n_tile, region, region_rows, stage, false, sid_s,
-                                                          ptid, pth);
+                                                          ptid, pth, kSidCap, stage_words);
         else dsum = write_descriptors(a, t, b, n_tile, region, region_rows, stage, marks, sid_s);
         if (tid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
     }
@@ -1165,7 +1165,10 @@ struct PlasticSmem {
 // packed receptor count.
 constexpr uint32_t kPlSeg = 1800;                     // segments staged per pass (6 words each)
 constexpr uint32_t kPlFlush = kStageWords - 6 * kPlSeg - 2;   // flush-row list capacity
-constexpr uint32_t kPlU = 4;                          // events in flight per thread
+#ifndef SPICE_PL_U
+#define SPICE_PL_U 2
+#endif
+constexpr uint32_t kPlU = SPICE_PL_U;                 // events in flight per thread
 
 // upd_count != nullptr (fused kernel, delay >= 2, one staging pass): the last kUpdWarps warps
 // run the update of step t + 1 meanwhile (it reads input slot t + 1, complete since delay >= 2,
@@ -1544,6 +1547,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.plo[x] = 0u; sm.phi[x] = 0u; }
         __shared__ bool s_upd;
         if (threadIdx.x == 0) s_upd = false;
+        asm volatile("griddepcontrol.wait;" ::: "memory");          // (programmatic dependent launch)
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         __syncthreads();
         const uint32_t d = deliver_tile_plastic(a, t, b, sm, true, &s_count3, &s_upd);
         plastic_flush(a, t, b, sm);
@@ -1590,6 +1595,9 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         const bool syn = MODEL == 4 && a.G == 1 && a.TWs <= 32u * kFireWords && a.prod_words > kSynthSid;
         uint32_t *sid_s = syn ? sm.prod : sm.stage + kStageWords;
         __shared__ uint32_t s_off;
+        // delay >= 2, one CTA per tile: the update of t + 1 runs on the last kUpdWarps warps
+        // while the others deliver t (its input slot t + 1 is complete; P:290 timestep grouping)
+        const bool ovl = !syn && a.delay >= 2 && a.C == 1;
         if (syn) {                                           // (shared memory and async copies only)
             synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid);
             __syncthreads();
@@ -1603,7 +1611,21 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t & 3u] : 0xFFFFFFFFu;
         __syncthreads();
         phase_mark(a, 1);
-        deliver_tile_ring<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
+        if (ovl) {
+            constexpr uint32_t NWD = kBlock / 32 - kUpdWarps;
+            const uint32_t n_sp = delivery_count(a, t, bt, c, pre_total);
+            const uint32_t warp = threadIdx.x >> 5;
+            if (warp < NWD) {
+                deliver_ring_core<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, n_sp, warp, NWD);
+            } else {
+                update_tile<MODEL, true, true>(a, t + 1, b, b * a.TWs, a.TWs, nullptr, a.G == 1, &s_count,
+                                               sm.stage + NWD * kRing, nullptr, false, kMaxCluster, nullptr, nullptr,
+                                               threadIdx.x - NWD * 32, kUpdWarps * 32, kUpdWarps * kRing);
+            }
+            __syncthreads();
+        } else {
+            deliver_tile_ring<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, true, pre_total);
+        }
         uint32_t *cnt = sm.cnt + c * a.TWs;                  // this CTA's slice
         constexpr bool DESC = true;
         if (a.delay == 1) {
@@ -1634,6 +1656,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
                 __syncthreads();                             // (the slot's ring writes above)
                 synth_publish_and_accumulate(a, t, b, lo, nullptr, kMaxCluster, s_fire, sid_s, s_count,
                                              sm.prod + kSynthSid, a.prod_words - kSynthSid, s_off);
+            } else if (ovl) {
+                // (the update of t + 1 ran during the delivery)
             } else {
                 update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, a.G == 1, &s_count, sm.stage, nullptr, true,
                                          kMaxCluster, sm.stage + kStageWords);
@@ -1982,7 +2006,7 @@ static void fused_v(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) 
 template <int M>
 static void fused_m(const SimArgs &a, uint32_t k, size_t bytes, cudaStream_t s) {
     if constexpr (M == 3) {                               // Brunel+ (C = 1)
-        k_fused<M, 0><<<a.NT, kBlock, bytes, s>>>(a, k);
+        launch_step_kernel(k_fused<M, 0>, a, k, bytes, s);
     } else {
         if (a.dly) {                                       // mixed per-synapse delays
             if (a.eshift) fused_v<M, 2>(a, k, bytes, s);
