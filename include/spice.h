@@ -64,6 +64,11 @@ enum { SPICE_FIXED_PROB = 0, SPICE_FIXED_INDEGREE = 1 };
                                               warps and global atomics (A/B baseline) */
 #define SPICE_FLAG_UNFUSED           0x4u  /* G = 1: separate update and delivery kernels
                                               instead of the fused deliver(t)+update(t+1) */
+#define SPICE_FLAG_PROCEDURAL        0x10u /* procedural connectivity (PAPER.md:506
+                                              [Knight2021]): no adjacency is stored, each tile
+                                              regenerates its row segments of every spike from
+                                              the FIXED_PROB Philox predicate; Vogels / Brunel /
+                                              Synth-with-FIXED_PROB rules only */
 #define SPICE_FLAG_USER_STREAM       0x8u  /* enqueue on spice_config.stream (may be the
                                               legacy default stream 0) instead of a
                                               library-owned non-blocking stream */

@@ -163,6 +163,7 @@ struct spice_net {
     uint32_t eshift = 0;     // entries hold (tile offset << eshift); 2 when padded
     uint32_t *deg = nullptr; // pad8: true out-degree of every source on this rank
     bool mixed_delays = false;   // synapses of more than one delay (reading R19)
+    bool procedural = false;     // SPICE_FLAG_PROCEDURAL: rows regenerated per spike, none stored
     uint8_t *dly = nullptr;      // per-entry delay (mixed delays only), aligned with ent
     double mean_seg = 0;
     double gen_ms = 0, create_ms = 0;   // setup: generator kernels (device), create (host wall)
@@ -660,10 +661,21 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // (multiples of 32); CTA x updates slice x.  On the fused G = 1 path the C CTAs form a
     // thread-block cluster that reduces the tile's counters through distributed shared memory.
     // (G > 1: the bitmap->list kernel writes the descriptors of the gathered spikes)
-    n->pad8 = n->model != SPICE_BRUNEL_PLUS;
+    n->procedural = (n->flags & SPICE_FLAG_PROCEDURAL) != 0;
+    if (n->procedural) {
+        if (n->model == SPICE_BRUNEL_PLUS)
+            return bail(fail(n, SPICE_EINVAL, "procedural connectivity needs stored weights for STDP (Brunel+)"));
+        if (n->flags & (SPICE_FLAG_GLOBAL_ATOMICS | SPICE_FLAG_EXTERNAL_EXCHANGE))
+            return bail(fail(n, SPICE_EINVAL, "procedural connectivity: no global-atomics or external-exchange mode"));
+        for (const spice_rule &R : n->rules)
+            if (R.kind != SPICE_FIXED_PROB)
+                return bail(fail(n, SPICE_EINVAL, "procedural connectivity regenerates FIXED_PROB rules only"));
+        if (n->rules.size() > 16) return bail(fail(n, SPICE_EINVAL, "procedural connectivity: at most 16 rules"));
+    }
+    n->pad8 = n->model != SPICE_BRUNEL_PLUS && !n->procedural;
     // auto: 2-CTA cluster tiles for large padded networks (half the spike x tile visits per
     // CTA; measured -4 % step time on synth 3e9, DESIGN.md delivery log), else one CTA per tile
-    n->C = c->ctas_per_tile ? c->ctas_per_tile
+    n->C = n->procedural ? 1u : c->ctas_per_tile ? c->ctas_per_tile
          : (n->pad8 && !c->tile_width && n->n_own >= (uint64_t)n->n_sm * 4096u ? 2u : 1u);
     if (n->C > kMaxCluster) return bail(fail(n, SPICE_EINVAL, "ctas_per_tile %u > %u", n->C, kMaxCluster));
     // small networks: one tile of all owned neurons, one CTA runs whole graph chunks
@@ -715,8 +727,10 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
         if (r != ncclSuccess) return bail(fail(n, SPICE_ENCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r)));
     }
     // ---- connectivity (a0') ----
-    if ((st = generate(n))) return bail(st);
-    if (n->mixed_delays) {
+    if (!n->procedural) {
+        if ((st = generate(n))) return bail(st);
+    }
+    if (n->mixed_delays && !n->procedural) {
         DelayRules dr{};
         for (uint32_t r = 0; r < c->n_rules; ++r) {
             const spice_rule &R = c->rules[r];
@@ -851,6 +865,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     }
     if (n->C > 1 && !n->desc) n->fused = false;           // cluster tiles: descriptor path only
     if (n->G > 1 && !n->desc) n->fused = false;           // G > 1: fused only on the padded layout
+    if (n->procedural) n->fused = false;                   // update + procedural delivery per step
     // ---- kernel arguments ----
     SimArgs &a = n->args;
     a.pdl = getenv("SPICE_NO_PDL") ? 0u : 1u;             // (A/B switch for measurements)
@@ -877,8 +892,42 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.pre_ts = n->pre_ts; a.pre_c = n->pre_c; a.post = n->post; a.post_mask = n->post_mask;
     a.tab_p = n->tab_p; a.tab_m = n->tab_m;
     a.npl = pbx.n;
+    if (n->procedural) {
+        for (uint32_t r = 0; r < n->rules.size(); ++r) {
+            const spice_rule &R = n->rules[r];
+            const uint64_t thr = prob_threshold(R.p);
+            const uint32_t lo = R.delay_min ? R.delay_min : n->delay, hi = R.delay_min && R.delay_max > lo ? R.delay_max : lo;
+            uint32_t *P = a.proc[a.nproc++];
+            P[0] = R.src_begin; P[1] = R.src_end; P[2] = R.dst_begin; P[3] = R.dst_end;
+            P[4] = (uint32_t)thr; P[5] = (uint32_t)(thr >> 32); P[6] = r;
+            P[7] = lo | (hi << 16);
+        }
+    }
     memcpy(a.pl, pbx.box, sizeof a.pl);
     CU(n, prepare_kernels(a));
+    if (n->procedural) {            // exact synapse count and receptor-packing check (nothing stored)
+        unsigned long long *cnt = nullptr;
+        uint32_t *tc = nullptr, *mx = nullptr;
+        if ((st = dalloc_t(n, &cnt, 1, "synapse count"))) return bail(st);
+        if ((st = dalloc_t(n, &tc, 2 * std::max<uint64_t>(n->n_own, 1), "in-degree counts"))) return bail(st);
+        if ((st = dalloc_t(n, &mx, 2, "in-degree max"))) return bail(st);
+        CU(n, cudaMemsetAsync(cnt, 0, 8, s));
+        CU(n, cudaMemsetAsync(tc, 0, 2 * std::max<uint64_t>(n->n_own, 1) * 4, s));
+        CU(n, cudaMemsetAsync(mx, 0, 8, s));
+        CU(n, launch_count_proc(a, cnt, tc, s));
+        max_halves_kernel<<<n->n_sm * 4, 256, 0, s>>>(tc, 2 * n->n_own, mx);
+        uint32_t h[2] = {0, 0};
+        unsigned long long hc = 0;
+        CU(n, cudaMemcpyAsync(&hc, cnt, 8, cudaMemcpyDeviceToHost, s));
+        CU(n, cudaMemcpyAsync(h, mx, 8, cudaMemcpyDeviceToHost, s));
+        CU(n, cudaStreamSynchronize(s));
+        n->n_syn = hc;
+        const uint64_t fb = 3ull * 8 + 2 * std::max<uint64_t>(n->n_own, 1) * 4;
+        dfree(n, cnt); dfree(n, tc); dfree(n, mx);
+        n->device_bytes -= fb;
+        if (h[0] >= 65535u || h[1] > 0u)                   // (plain counts: any high half is >= 65536)
+            return bail(fail(n, SPICE_EINVAL, "a target has >= 65535 in-synapses of one receptor type; packed counts could overflow"));
+    }
     // the caller's stream may still be running work of its own: everything the library
     // enqueued on it so far (memsets, generator) is done; capture never touches it
     CU(n, cudaStreamSynchronize(s));
@@ -1132,10 +1181,65 @@ spice_status spice_spikes_collect(spice_net *n, uint32_t slot, uint32_t *ids, ui
     return SPICE_OK;
 }
 
+namespace {
+// Philox4x32-10 on the host (the same published algorithm as the device's, for regenerating
+// procedural rows in the read-out hooks)
+void philox_host(const uint32_t ctr[4], uint32_t k0, uint32_t k1, uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n1 = (uint32_t)p1;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1, n3 = (uint32_t)p0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+// Row s of a procedural network on this rank: (global target, delay) pairs, ascending.
+void procedural_row(const spice_net *n, uint32_t s, std::vector<std::pair<uint32_t, uint8_t>> &row) {
+    row.clear();
+    const uint32_t k0 = (uint32_t)n->seed, k1 = (uint32_t)(n->seed >> 32);
+    for (uint64_t i = 0; i < n->n_own; ++i) {
+        const uint32_t j = (uint32_t)local_to_global(i, n->rank, n->G, n->S);
+        for (uint32_t r = 0; r < n->rules.size(); ++r) {
+            const spice_rule &R = n->rules[r];
+            if (s < R.src_begin || s >= R.src_end || j < R.dst_begin || j >= R.dst_end) continue;
+            const uint32_t ctr[4] = {s, j >> 2, r, kTagConn};
+            uint32_t o[4];
+            philox_host(ctr, k0, k1, o);
+            if ((uint64_t)o[j & 3] >= prob_threshold(R.p)) continue;
+            const uint32_t lo = R.delay_min ? R.delay_min : n->delay;
+            const uint32_t hi = R.delay_min && R.delay_max > lo ? R.delay_max : lo;
+            uint32_t d = lo;
+            if (hi > lo) {
+                const uint32_t cd[4] = {s, j >> 2, r, kTagDelay};
+                philox_host(cd, k0, k1, o);
+                d += (uint32_t)(((uint64_t)o[j & 3] * (hi - lo + 1)) >> 32);
+            }
+            row.emplace_back(j, (uint8_t)d);
+        }
+    }
+    std::sort(row.begin(), row.end());
+}
+}  // namespace
+
 spice_status spice_read_connectivity(spice_net *n, uint32_t row_begin, uint32_t row_end, uint32_t *tgt,
                                      uint64_t cap, uint64_t *row_offsets, uint64_t *total) {
     CHECK_NET(n);
     if (row_begin > row_end || row_end > n->N) return fail(n, SPICE_EINVAL, "rows outside [0, N)");
+    if (n->procedural) {                       // regenerated (the device stores no rows)
+        std::vector<std::pair<uint32_t, uint8_t>> row;
+        uint64_t o = 0;
+        for (uint32_t q = row_begin; q < row_end; ++q) {
+            procedural_row(n, q, row);
+            if (row_offsets) row_offsets[q - row_begin] = o;
+            for (auto &e : row) { if (tgt && o < cap) tgt[o] = e.first; ++o; }
+        }
+        if (row_offsets) row_offsets[row_end - row_begin] = o;
+        if (total) *total = o;
+        if (o > cap || (!tgt && o)) return fail(n, SPICE_ETRUNC, "need %llu targets", (unsigned long long)o);
+        return SPICE_OK;
+    }
     CU(n, cudaStreamSynchronize(n->stream));
     const uint32_t nr = row_end - row_begin;
     std::vector<uint64_t> rp(nr + 1);
@@ -1177,6 +1281,17 @@ spice_status spice_read_delays(spice_net *n, uint32_t row_begin, uint32_t row_en
                                uint64_t cap, uint64_t *total) {
     CHECK_NET(n);
     if (row_begin > row_end || row_end > n->N) return fail(n, SPICE_EINVAL, "rows outside [0, N)");
+    if (n->procedural) {
+        std::vector<std::pair<uint32_t, uint8_t>> row;
+        uint64_t o = 0;
+        for (uint32_t q = row_begin; q < row_end; ++q) {
+            procedural_row(n, q, row);
+            for (auto &e : row) { if (out && o < cap) out[o] = e.second; ++o; }
+        }
+        if (total) *total = o;
+        if (o > cap || (!out && o)) return fail(n, SPICE_ETRUNC, "need %llu delays", (unsigned long long)o);
+        return SPICE_OK;
+    }
     CU(n, cudaStreamSynchronize(n->stream));
     const uint32_t nr = row_end - row_begin;
     std::vector<uint64_t> rp(nr + 1);

@@ -509,7 +509,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
         if (write_list) a.sl_counts[par * a.NR + b] = n_tile;
         if (n_tile) atomicAdd(&a.fired_cta[b], (unsigned long long)n_tile);   // RED: no load on the path
     }
-    if (!DESC && write_list && !a.desc && MODEL != 3) {   // row starts of the spikes, all at once
+    if (!DESC && write_list && !a.desc && MODEL != 3 && a.row_ptr) {   // row starts of the spikes, all at once
         uint32_t dsum = 0;                                // (the descriptor pass loads them itself;
         for (uint32_t q = tid; q < n_tile; q += pth) {    //  Brunel+ staging loads row_ptr itself)
             const uint32_t s = region[q];
@@ -1783,6 +1783,101 @@ cudaError_t launch_small(const SimArgs &a, uint32_t k0, uint32_t nsteps, cudaStr
     return cudaGetLastError();
 }
 
+// Procedural connectivity ("only store the parameters used to
+// create the network and then generate adjacency data on the fly" [Knight2021]): no rows are
+// stored; the CTA of tile b regenerates, for every spike s of step t, its row segment into
+// the tile from the same Philox predicate the generator uses (FIXED_PROB rules: edge s -> j
+// iff Philox(s, j>>2, rule, 1)[j&3] < floor(p 2^32), reading R9), one Philox call per spike and
+// 4-target block, flattened over all threads, and accumulates the hits' packed receptor
+// counts in shared memory (per-synapse delays: minimum delay there, longer delays into ring
+// slot t + d).  Memory: O(neurons) instead of O(synapses); the work is one Philox call per
+// 4 candidate pairs instead of 2 bytes per synapse.
+__global__ void __launch_bounds__(kBlock) k_deliver_proc(SimArgs a, uint32_t k) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t *cnt = smem;                                   // [TW]
+    uint32_t *pref = smem + ((a.TW + 3u) & ~3u), *tmp = pref + ((a.NR + 1 + 3) & ~3u);
+    const uint64_t t = *a.t0 + k;
+    const uint32_t par = (uint32_t)(t & 1), b = blockIdx.x;
+    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) cnt[x] = 0u;
+    for (uint32_t r = threadIdx.x; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
+    __syncthreads();
+    block_exclusive_scan(pref, a.NR, tmp);
+    const uint32_t n_sp = pref[a.NR];
+    const uint32_t lo = b * a.TW, width = min(a.TW, a.n_own - lo), nblk = (width + 3u) / 4u;
+    const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
+    const uint32_t tD = a.dly ? (uint32_t)mod32(t, a.D) : 0u;
+    uint32_t hits = 0;
+    const uint64_t total = (uint64_t)n_sp * nblk;
+    for (uint64_t f = threadIdx.x; f < total; f += kBlock) {
+        const uint32_t p = (uint32_t)(f / nblk), q4 = (uint32_t)(f % nblk);
+        const uint32_t r = region_of(pref, a.NR, p);
+        const uint32_t s = a.sl_ids[lbase + (uint64_t)r * a.RS + (p - pref[r])];
+        const uint32_t i0 = lo + 4u * q4;                   // 4 consecutive owned targets
+        const uint32_t j0 = a.G == 1 ? i0 : (uint32_t)local_to_global(i0, a.rank, a.G, a.S);
+        const uint32_t qv = s >= a.n_exc ? 65536u : 1u;
+        for (uint32_t rr = 0; rr < a.nproc; ++rr) {
+            const uint32_t *R = a.proc[rr];                 // src_b, src_e, dst_b, dst_e, thr lo, thr hi, index, dmin | dmax << 16
+            if (s < R[0] || s >= R[1] || j0 + 3u < R[2] || j0 >= R[3]) continue;
+            const uint64_t thr = ((uint64_t)R[5] << 32) | R[4];
+            const uint4 x = philox4x32_10(make_uint4(s, j0 >> 2, R[6], kTagConn), a.key0, a.key1);
+#pragma unroll
+            for (uint32_t e = 0; e < 4; ++e) {
+                const uint32_t j = j0 + e;
+                if (i0 + e >= lo + width || j < R[2] || j >= R[3] || (uint64_t)word_of(x, e) >= thr) continue;
+                ++hits;
+                const uint32_t off = i0 + e - lo;
+                const uint32_t dlo = R[7] & 0xFFFFu, dhi = R[7] >> 16;
+                uint32_t d = dlo;
+                if (dhi > dlo) {                            // per-synapse delay (reading R19)
+                    const uint4 y = philox4x32_10(make_uint4(s, j >> 2, R[6], kTagDelay), a.key0, a.key1);
+                    d += (uint32_t)(((uint64_t)word_of(y, j & 3) * (dhi - dlo + 1)) >> 32);
+                }
+                if (d == a.delay) atomicAdd(&cnt[off], qv);
+                else {
+                    uint32_t sl = tD + d;
+                    if (sl >= a.D) sl -= a.D;
+                    atomicAdd(a.ring + (uint64_t)sl * a.ring_stride + lo + off, qv);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + lo;
+    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) dst[x] += cnt[x];
+    store_delivered(a, b, hits, tmp);
+}
+
+// Synapses of this rank under the procedural rules (count only; nothing is stored), and the
+// per-target excitatory / inhibitory in-degrees tc[2 i], tc[2 i + 1] (packing check).
+__global__ void k_count_proc(SimArgs a, unsigned long long *out, uint32_t *tc) {
+    unsigned long long c = 0;
+    const uint64_t nblk = (a.n_own + 3u) / 4u;
+    const uint64_t total = (uint64_t)a.N * nblk;
+    for (uint64_t f = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = (uint32_t)(f / nblk), i0 = 4u * (uint32_t)(f % nblk);
+        const uint32_t j0 = a.G == 1 ? i0 : (uint32_t)local_to_global(i0, a.rank, a.G, a.S);
+        for (uint32_t rr = 0; rr < a.nproc; ++rr) {
+            const uint32_t *R = a.proc[rr];
+            if (s < R[0] || s >= R[1] || j0 + 3u < R[2] || j0 >= R[3]) continue;
+            const uint64_t thr = ((uint64_t)R[5] << 32) | R[4];
+            const uint4 x = philox4x32_10(make_uint4(s, j0 >> 2, R[6], kTagConn), a.key0, a.key1);
+            for (uint32_t e = 0; e < 4; ++e) {
+                const uint32_t j = j0 + e;
+                if (i0 + e < a.n_own && j >= R[2] && j < R[3] && (uint64_t)word_of(x, e) < thr) {
+                    ++c;
+                    atomicAdd(&tc[2u * (i0 + e) + (s >= a.n_exc ? 1u : 0u)], 1u);
+                }
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+cudaError_t launch_count_proc(const SimArgs &a, unsigned long long *out, uint32_t *tc, cudaStream_t s) {
+    k_count_proc<<<148 * 8, 256, 0, s>>>(a, out, tc);
+    return cudaGetLastError();
+}
+
 // Paper-style baseline: warp w delivers spike (w mod |S|) to tile (w / |S|), column-wise
 // (P:200), with one global atomic per event.
 __global__ void __launch_bounds__(kBlock) k_global_atomics(SimArgs a, uint32_t k) {
@@ -1851,7 +1946,7 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
                 bits &= bits - 1;
                 const uint32_t j = (uint32_t)local_to_global((uint64_t)wl * 32 + bit, rk, a.G, a.S);
                 region[pos] = j;
-                region_rows[pos] = a.row_ptr[j];
+                if (a.row_ptr) region_rows[pos] = a.row_ptr[j];   // (procedural networks store no rows)
                 ++pos;
             }
         }
@@ -1940,6 +2035,7 @@ cudaError_t prepare_kernels(const SimArgs &a) {
         }
     }
     ALLOW(k_b2l, ub);
+    if (a.nproc) ALLOW(k_deliver_proc, (((a.TW + 3u) & ~3u) + ((a.NR + 1 + 3) & ~3u) + 36) * 4);
     if (a.model == 3) {
         const size_t pb = plastic_smem_bytes(a.TW, a.NR);
         ALLOW(k_deliver_plastic, pb);
@@ -1970,6 +2066,10 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
     if (a.model == 3) {
         const size_t pb = plastic_smem_bytes(a.TW, a.NR);
         k_deliver_plastic<<<a.NT, kBlock, pb, s>>>(a, k);
+        return cudaGetLastError();
+    }
+    if (a.nproc) {                                         // procedural connectivity
+        k_deliver_proc<<<a.NT, kBlock, (((a.TW + 3u) & ~3u) + ((a.NR + 1 + 3) & ~3u) + 36) * 4, s>>>(a, k);
         return cudaGetLastError();
     }
     if (!a.desc) return cudaErrorInvalidValue;             // padded layout only

@@ -163,6 +163,8 @@ struct SimArgs {
                              // steps (most recent first) and cy = Y(ts) + 1 (float bits)
     uint32_t *post_mask;     // [ring_stride][64] post-spike bit ring (2048 steps)
     const float *tab_p, *tab_m;   // [8192] exp(-k dt / tau+-), rounded once
+    uint32_t nproc;          // procedural connectivity (NEXT-4): rules regenerated per spike
+    uint32_t proc[16][8];    // src_b, src_e, dst_b, dst_e, thr lo, thr hi, rule index, dmin | dmax << 16
     uint32_t npl;                                  // plastic boxes (src x dst ranges)
     uint32_t pl[kMaxPlasticRules][4];
     const uint64_t *t0;      // step index of the first step of this graph replay

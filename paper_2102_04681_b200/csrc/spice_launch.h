@@ -17,6 +17,7 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
 cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s);
+cudaError_t launch_count_proc(const SimArgs &a, unsigned long long *out, uint32_t *tc, cudaStream_t s);
 cudaError_t launch_settle_weights(const SimArgs &a, uint64_t t_now, uint32_t row_lo, uint32_t row_hi, float *out,
                                   cudaStream_t s);
 cudaError_t launch_peer_signal(const SimArgs &a, uint32_t k, cudaStream_t s);

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("SPICE_LIB") or os.path.join(_PKG, "libspice.so")
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ERANGE, ETRUNC, ESTATE = range(8)
 VOGELS, BRUNEL, BRUNEL_PLUS, SYNTH = 1, 2, 3, 4
-FLAG_EXTERNAL_EXCHANGE, FLAG_GLOBAL_ATOMICS, FLAG_UNFUSED, FLAG_USER_STREAM = 0x1, 0x2, 0x4, 0x8
+FLAG_EXTERNAL_EXCHANGE, FLAG_GLOBAL_ATOMICS, FLAG_UNFUSED, FLAG_USER_STREAM, FLAG_PROCEDURAL = 0x1, 0x2, 0x4, 0x8, 0x10
 EXCHANGE_NCCL, EXCHANGE_PEER = 0, 1
 FIELD_V, FIELD_GE, FIELD_GI, FIELD_REF, FIELD_ACC, FIELD_XTR, FIELD_YTR = range(7)
 ABI_VERSION = 2
@@ -161,7 +161,7 @@ class Network:
                  external_exchange: bool = False, global_atomics: bool = False,
                  tile_width: int = 0, ctas_per_tile: int = 0, unfused: bool = False,
                  exchange: int = EXCHANGE_NCCL, stream: Optional[int] = None,
-                 allocator=None):
+                 allocator=None, procedural: bool = False):
         """``stream``: a cudaStream_t handle (int, e.g. ``torch.cuda.current_stream().cuda_stream``)
         to enqueue on instead of a library-owned stream.  ``allocator``: a pair of callables
         ``(alloc(nbytes) -> device pointer int, free(pointer))`` (e.g. torch's caching
@@ -176,7 +176,7 @@ class Network:
         self._nccl = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         flags = (FLAG_EXTERNAL_EXCHANGE if external_exchange else 0) | \
                 (FLAG_GLOBAL_ATOMICS if global_atomics else 0) | (FLAG_UNFUSED if unfused else 0) | \
-                (FLAG_USER_STREAM if stream is not None else 0)
+                (FLAG_USER_STREAM if stream is not None else 0) | (FLAG_PROCEDURAL if procedural else 0)
         self._alloc_cbs = None
         if allocator is not None:
             alloc_fn, free_fn = allocator
