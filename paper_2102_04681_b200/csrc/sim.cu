@@ -1805,7 +1805,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver_proc(SimArgs a, uint32_t k) 
     const uint32_t n_sp = pref[a.NR];
     const uint32_t lo = b * a.TW, width = min(a.TW, a.n_own - lo), nblk = (width + 3u) / 4u;
     const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
-    const uint32_t tD = a.dly ? (uint32_t)mod32(t, a.D) : 0u;
+    const uint32_t tD = (uint32_t)mod32(t, a.D);
     uint32_t hits = 0;
     const uint64_t total = (uint64_t)n_sp * nblk;
     for (uint64_t f = threadIdx.x; f < total; f += kBlock) {
