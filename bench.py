@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--tile-width", type=int, default=0)
     ap.add_argument("--ctas-per-tile", type=int, default=0)
     ap.add_argument("--global-atomics", action="store_true", help="paper-style delivery (A/B)")
+    ap.add_argument("--procedural", action="store_true",
+                    help="procedural connectivity (NEXT-4): rows regenerated per spike, none stored (A/B)")
     ap.add_argument("--unfused", action="store_true",
                     help="separate update and delivery launches per step (the G > 1 kernel sequence, A/B)")
     ap.add_argument("--profile-steps", type=int, default=200)
@@ -269,7 +271,7 @@ def main_spice(args):
     net = S.Network(cfg, rank=rank, world_size=world, device=local, nccl_id=nccl_id,
                     record_steps=record, global_atomics=args.global_atomics,
                     tile_width=args.tile_width, ctas_per_tile=args.ctas_per_tile, unfused=args.unfused,
-                    exchange=S.EXCHANGE_PEER if peer else S.EXCHANGE_NCCL)
+                    exchange=S.EXCHANGE_PEER if peer else S.EXCHANGE_NCCL, procedural=args.procedural)
     if peer:                                       # map every rank's receive window
         handles = [None] * world
         dist.all_gather_object(handles, net.peer_handle())
@@ -385,7 +387,9 @@ def main_spice(args):
         cpu = {"value": eps, "unit": "events/s", "cores": 1, "kind": "oracle",
                "sample": f"{desc}; {done} steps in {el:.1f} s, single thread"}
 
-    delivery = ("global-atomics (paper-style A/B)" if args.global_atomics else
+    delivery = ("procedural: row segments regenerated per spike and tile from Philox, no adjacency stored"
+                if args.procedural else
+                "global-atomics (paper-style A/B)" if args.global_atomics else
                 f"one CTA, {info['tile_width']} targets in smem, 32 steps per launch" if small else
                 f"tiled smem, {info['n_tiles']} tiles x {info['tile_width']} targets, {info['ctas_per_tile']} CTA/tile")
     traffic, traffic_src = ncu_traffic(wl, delivery) if fused else (None, None)
