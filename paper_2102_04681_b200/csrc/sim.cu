@@ -67,6 +67,16 @@ __device__ __forceinline__ void block_exclusive_scan(uint32_t *arr, uint32_t n, 
 __device__ __forceinline__ uint64_t mod32(uint64_t t, uint32_t m) {
     return (t >> 32) ? t % m : (uint64_t)((uint32_t)t % m);
 }
+// t mod m with the host-computed M = floor((2^64 - 1) / m) + 1: for 32-bit t the remainder
+// is the high word of (M t mod 2^64) m (exact for every 32-bit t and m; Lemire, Kaser and
+// Kurz 2019, "Faster remainder by direct computation") -- two multiplies instead of the
+// ~20-instruction reciprocal sequence of a runtime-divisor remainder
+__device__ __forceinline__ uint64_t modm(uint64_t t, uint32_t m, uint64_t M) {
+    if (t >> 32) return t % m;
+    return __umul64hi(M * (uint32_t)t, m);
+}
+#define modD(a, t) modm((t), (a).D, (a).mD)
+#define modR(a, t) modm((t), (a).record_steps, (a).mR)
 
 __device__ __forceinline__ uint4 ld_stream_v4(const uint16_t *p) {
     uint4 v;
@@ -377,8 +387,8 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     const uint32_t par = (uint32_t)(t & 1);
     uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
     uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + b) * a.RS;
-    uint32_t *bm = a.G == 1 ? a.record + mod32(t, a.record_steps) * (uint64_t)a.W : a.sendbuf;
-    uint32_t *ring_slot = a.ring + mod32(t, a.D) * a.ring_stride + lo;
+    uint32_t *bm = a.G == 1 ? a.record + modR(a, t) * (uint64_t)a.W : a.sendbuf;
+    uint32_t *ring_slot = a.ring + modD(a, t) * a.ring_stride + lo;
     // Brunel drive: the Poisson inversion table in shared memory (the walk is a chain of
     // dependent loads per neuron)
     __shared__ uint64_t s_ptab[kPtabSmem];
@@ -411,7 +421,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
             uint32_t c[4];
             long long pin[4] = {0, 0, 0, 0};
             if (MODEL == 3) {
-                long long *ps = a.pring + mod32(t, a.D) * a.ring_stride + lo + x4;
+                long long *ps = a.pring + modD(a, t) * a.ring_stride + lo + x4;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) { pin[e] = ps[e]; ps[e] = 0; }
             }
@@ -647,7 +657,7 @@ __device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32
 __device__ __forceinline__ void synth_accumulate(const SimArgs &a, uint64_t t1, uint32_t lo, uint32_t width,
                                                  const uint32_t *cnt, uint32_t cl_c,
                                                  uint32_t tid = threadIdx.x, uint32_t nth = kBlock) {
-    uint32_t *ring_slot = a.ring + mod32(t1, a.D) * a.ring_stride + lo;
+    uint32_t *ring_slot = a.ring + modD(a, t1) * a.ring_stride + lo;
     const uint32_t span = min(width, a.n_own > lo ? a.n_own - lo : 0u);
     if (cnt && !a.dly && (cl_c >= kMaxCluster || a.C == 2) && span <= 4u * nth * 4u) {
         // common case: every load of the thread's <= 4 groups in flight before any add
@@ -798,7 +808,7 @@ __device__ __forceinline__ void synth_publish_and_accumulate(const SimArgs &a, u
         const uint32_t ptid = threadIdx.x - kAccWarps * 32, pth = kBlock - kAccWarps * 32;
         const uint64_t t1 = t + 1;
         const uint32_t par1 = (uint32_t)(t1 & 1);
-        uint32_t *bm = a.record + mod32(t1, a.record_steps) * (uint64_t)a.W;
+        uint32_t *bm = a.record + modR(a, t1) * (uint64_t)a.W;
         const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
         uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
         uint64_t *region_rows = a.sl_rows + ((uint64_t)par1 * a.NR + b) * a.RS;
@@ -934,7 +944,7 @@ __device__ __forceinline__ void deliver_ring_core(const SimArgs &a, uint64_t t, 
         const uint2 d = *reinterpret_cast<const uint2 *>(p);
         return make_uint4(d.x, d.y, 0u, 0u);
     };
-    const uint32_t tD = DLY ? (uint32_t)mod32(t, a.D) : 0u;
+    const uint32_t tD = DLY ? (uint32_t)modD(a, t) : 0u;
     const uint64_t tile_base = (uint64_t)b * a.TW;
     constexpr uint32_t RW = SPICE_RW;                  // windows per lane per iteration
     fill(32u * RW);
@@ -1003,7 +1013,7 @@ constexpr uint32_t kHistWords = 64;       // post-spike bit ring: 2048 steps per
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 __device__ __forceinline__ const uint32_t *step_bitmap(const SimArgs &a, uint64_t t) {
-    return a.record + mod32(t, a.record_steps) * (uint64_t)a.G * a.W + (uint64_t)a.rank * a.W;
+    return a.record + modR(a, t) * (uint64_t)a.G * a.W + (uint64_t)a.rank * a.W;
 }
 
 __device__ __forceinline__ bool plastic_src(const SimArgs &a, uint32_t s) {
@@ -1039,8 +1049,10 @@ __device__ __forceinline__ int64_t row_tproc(uint32_t j, uint64_t t, uint32_t ts
 }
 
 // One potentiation at post spike step tp with the row's pre state (ts_j, cx_j).
-__device__ __forceinline__ float potentiate_at(const SimArgs &a, float w, uint64_t tp, uint32_t ts_j, float cx_j) {
-    const float x = trace_val(cx_j, ts_j, tp, a.tab_p);
+// (tabp: the X table, a shared-memory copy on the delivery path)
+__device__ __forceinline__ float potentiate_at(const SimArgs &a, const float *tabp, float w, uint64_t tp,
+                                               uint32_t ts_j, float cx_j) {
+    const float x = trace_val(cx_j, ts_j, tp, tabp);
     const float nw = __fadd_rn(w, __fmul_rn(a.mc.Ap, x));
     return nw < a.mc.wmax ? nw : a.mc.wmax;
 }
@@ -1048,10 +1060,15 @@ __device__ __forceinline__ float potentiate_at(const SimArgs &a, float w, uint64
 // Lazy potentiation of one synapse: the post neuron's spikes in (tproc, t], in time order.
 // pl = its last three spike steps up to and including t (most recent first, kNone = none);
 // older ones come from its bit ring `mask` (only when all three are inside the window).
-__device__ __forceinline__ float potentiate_lazy(const SimArgs &a, float w, int64_t tproc, uint32_t ts_j, float cx_j,
+__device__ __forceinline__ float potentiate_lazy(const SimArgs &a, const float *tabp, float w, int64_t tproc,
+                                                 uint32_t ts_j, float cx_j,
                                                  uint32_t p1, uint32_t p2, uint32_t p3, const uint32_t *mask) {
     if (ts_j == kNone || p1 == kNone || (int64_t)p1 <= tproc) return w;     // X = 0 / no post spike
+#ifndef SPICE_ABLATE_MASK
     if (p3 != kNone && (int64_t)p3 > tproc) {
+#else
+    if (false) {
+#endif
         for (uint64_t s = (uint64_t)(tproc + 1); s < p3;) {                  // spikes before p3
             const uint32_t wi = (uint32_t)((s >> 5) % kHistWords);
             const uint32_t b0 = (uint32_t)(s & 31u);
@@ -1062,31 +1079,32 @@ __device__ __forceinline__ float potentiate_lazy(const SimArgs &a, float w, int6
             while (bits) {
                 const uint32_t k = __ffs(bits) - 1;
                 bits &= bits - 1u;
-                w = potentiate_at(a, w, s + k, ts_j, cx_j);
+                w = potentiate_at(a, tabp, w, s + k, ts_j, cx_j);
             }
             s = wend;
         }
     }
-    if (p3 != kNone && (int64_t)p3 > tproc) w = potentiate_at(a, w, p3, ts_j, cx_j);
-    if (p2 != kNone && (int64_t)p2 > tproc) w = potentiate_at(a, w, p2, ts_j, cx_j);
-    return potentiate_at(a, w, p1, ts_j, cx_j);
+    if (p3 != kNone && (int64_t)p3 > tproc) w = potentiate_at(a, tabp, w, p3, ts_j, cx_j);
+    if (p2 != kNone && (int64_t)p2 > tproc) w = potentiate_at(a, tabp, w, p2, ts_j, cx_j);
+    return potentiate_at(a, tabp, w, p1, ts_j, cx_j);
 }
 
 // Pre state of every global source for step t + 1 (CTA slices of [0, N)): a source that
 // spiked at t restarts its trace, cx = X(t) + 1 (the oracle's event-driven update).
-__device__ __forceinline__ void pre_state_pass(const SimArgs &a, uint64_t t) {
-    const uint32_t *gbm = a.record + mod32(t, a.record_steps) * (uint64_t)a.G * a.W;
+__device__ __forceinline__ void pre_state_pass(const SimArgs &a, uint64_t t, const float *tabp,
+                                               uint32_t ptid = threadIdx.x, uint32_t pth = kBlock) {
+    const uint32_t *gbm = a.record + modR(a, t) * (uint64_t)a.G * a.W;
     const uint32_t *ots = a.pre_ts + (t & 1) * (uint64_t)a.N;
     const float *oc = a.pre_c + (t & 1) * (uint64_t)a.N;
     uint32_t *nts = a.pre_ts + ((t + 1) & 1) * (uint64_t)a.N;
     float *nc = a.pre_c + ((t + 1) & 1) * (uint64_t)a.N;
     const uint32_t per = (a.N + gridDim.x - 1) / gridDim.x;
     const uint32_t j0 = blockIdx.x * per, j1 = min(a.N, j0 + per);
-    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kBlock) {
+    for (uint32_t j = j0 + ptid; j < j1; j += pth) {
         uint32_t ts = ots[j];
         float c = oc[j];
         if (spiked_global(a, gbm, j)) {
-            c = __fadd_rn(trace_val(c, ts, t, a.tab_p), 1.0f);
+            c = __fadd_rn(trace_val(c, ts, t, tabp), 1.0f);
             ts = (uint32_t)t;
         }
         nts[j] = ts;
@@ -1153,6 +1171,9 @@ struct PlasticSmem {
     float *ys;                     // [TW] Y(t) of the tile's neurons
     uint32_t *p1, *p2, *p3;        // [TW] their last three spike steps up to t
     uint32_t *pref, *tmp, *stage;
+    float *tabp;                   // [kTraceLen] the X trace table (constant: loaded before the
+                                   // dependent-launch wait)
+    uint32_t *cst;                 // [kPlChunks + 1] first segment of each 32-event chunk
 };
 
 // (i)-(iii) of step t for tile b, one flattened event space over all threads: the
@@ -1169,6 +1190,7 @@ constexpr uint32_t kPlFlush = kStageWords - 6 * kPlSeg - 2;   // flush-row list 
 #define SPICE_PL_U 2
 #endif
 constexpr uint32_t kPlU = SPICE_PL_U;                 // events in flight per thread
+constexpr uint32_t kPlChunks = 4096;                  // chunk-start table: passes of <= 2^17 events
 
 // upd_count != nullptr (fused kernel, delay >= 2, one staging pass): the last kUpdWarps warps
 // run the update of step t + 1 meanwhile (it reads input slot t + 1, complete since delay >= 2,
@@ -1184,7 +1206,7 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
     const uint32_t par = (uint32_t)(t & 1);
     uint32_t *pref = sm.pref, *tmp = sm.tmp, *stage = sm.stage;
     const uint32_t *bm = step_bitmap(a, t);
-    const uint32_t *gbm = a.record + mod32(t, a.record_steps) * (uint64_t)a.G * a.W;
+    const uint32_t *gbm = a.record + modR(a, t) * (uint64_t)a.G * a.W;
     const uint32_t *pts = a.pre_ts + (t & 1) * (uint64_t)a.N;
     const float *pc = a.pre_c + (t & 1) * (uint64_t)a.N;
     const uint64_t tile_base = (uint64_t)b * a.TW;
@@ -1225,7 +1247,7 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
     const uint32_t n_fl = min(s_nfl, kPlFlush);
     const uint32_t nseg = n_sp + n_fl;
     const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
-    const uint32_t tD = a.dly ? (uint32_t)mod32(t, a.D) : 0u;
+    const uint32_t tD = a.dly ? (uint32_t)modD(a, t) : 0u;
     uint32_t *sst = stage, *slen = stage + kPlSeg, *sfl = stage + 2 * kPlSeg + 1;
     float *sx = reinterpret_cast<float *>(stage + 3 * kPlSeg + 1);
     uint32_t *sts = stage + 4 * kPlSeg + 1;
@@ -1262,8 +1284,20 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
         }
         __syncthreads();
         block_exclusive_scan(slen, nq, tmp);      // slen -> event prefix
-        if (marks) phase_mark(a, 3);
         const uint32_t ne = slen[nq];
+        // first segment of every 32-event chunk (one search per chunk instead of per event;
+        // an event walks forward from its chunk's start over the few boundaries inside it)
+        const bool chunked = ne <= 32u * kPlChunks;
+        if (chunked) {
+            for (uint32_t c = tid; c < (ne + 31u) / 32u; c += kBlock) {
+                const uint32_t f = c * 32u;
+                uint32_t lo = 0, h = nq;
+                while (h - lo > 1) { const uint32_t m = (lo + h) >> 1; if (slen[m] <= f) lo = m; else h = m; }
+                sm.cst[c] = lo;
+            }
+            __syncthreads();
+        }
+        if (marks) phase_mark(a, 3);
         // (fused, delay >= 2, single pass) the update of t + 1 on the last kUpdWarps warps
         const bool ovl = upd_count && a.delay >= 2 && nseg <= kPlSeg;
         uint32_t etid = tid, eth = kBlock;
@@ -1272,7 +1306,11 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
             if (tid >= eth) {
                 update_tile_sub<3>(a, t + 1, b, b * a.TW, a.TW, upd_count, sm.stage + kStageWords - 64,
                                    tid - eth, kUpdWarps * 32);
+                // then the pre state for t + 1 (independent of the delivery: it writes the
+                // other parity and reads step t's spikes)
+                pre_state_pass(a, t, sm.tabp, tid - eth, kUpdWarps * 32);
                 *upd_done = true;
+                if (marks) phase_mark(a, 8, eth);
                 continue;                         // (nseg <= kPlSeg: this was the only pass)
             }
         }
@@ -1284,8 +1322,15 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
                 const uint32_t f = f0 + u * eth;
                 l[u] = kNone;
                 if (f < ne) {
-                    uint32_t lo = 0, h = nq;          // largest q with slen[q] <= f
-                    while (h - lo > 1) { const uint32_t m = (lo + h) >> 1; if (slen[m] <= f) lo = m; else h = m; }
+                    uint32_t lo;                      // largest q with slen[q] <= f (slen[nq] = ne > f)
+                    if (chunked) {
+                        lo = sm.cst[f >> 5];
+                        while (slen[lo + 1] <= f) ++lo;
+                    } else {
+                        lo = 0;
+                        uint32_t h = nq;
+                        while (h - lo > 1) { const uint32_t m = (lo + h) >> 1; if (slen[m] <= f) lo = m; else h = m; }
+                    }
                     l[u] = lo;
                     e[u] = sst[lo] + (f - slen[lo]);
                     off[u] = a.ent[e[u]];
@@ -1297,16 +1342,25 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
                 if (l[u] == kNone) continue;
                 const uint32_t fl = sfl[l[u]];
                 float w = wv[u];
+#ifndef SPICE_ABLATE_POT
                 if (w >= 0.0f)                        // (i), lazily: post spikes since the last processing
-                    w = potentiate_lazy(a, w, stp[l[u]], sts[l[u]], sx[l[u]], sm.p1[off[u]], sm.p2[off[u]],
+#else
+                if (false)
+#endif
+                    w = potentiate_lazy(a, sm.tabp, w, stp[l[u]], sts[l[u]], sx[l[u]], sm.p1[off[u]], sm.p2[off[u]],
                                         sm.p3[off[u]], a.post_mask + (tile_base + off[u]) * kHistWords);
                 if (fl & 4u) {                        // flush row: potentiation only
                     if (w >= 0.0f && w != wv[u]) a.w[e[u]] = w;
                 } else {
+#ifndef SPICE_ABLATE_DEL
                     plastic_deliver(a, sm.cnt, sm.plo, sm.phi, sm.ys, e[u], off[u], fl, w, tD, tile_base);
+#else
+                    if (w == 12345.0f) a.w[e[u]] = w;
+#endif
                 }
             }
         }
+        if (marks) phase_mark(a, 7);
         // delivered events: the spike rows' entries of this pass
         if (tid == 0) {
             const uint32_t sp_end = n_sp > q0 ? min(nq, n_sp - q0) : 0u;
@@ -1315,7 +1369,7 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
     }
     __syncthreads();
     if (marks) phase_mark(a, 4);
-    pre_state_pass(a, t);
+    if (!(upd_done && *upd_done)) pre_state_pass(a, t, sm.tabp);
     if (marks) phase_mark(a, 5);
     return delivered;
 }
@@ -1346,7 +1400,7 @@ __global__ void __launch_bounds__(256) k_settle_weights(SimArgs a, uint64_t t_no
             if (w >= 0.0f) {
                 const uint32_t il = b * a.TW + a.ent[st + e];
                 const uint4 ps = post[il];
-                w = potentiate_lazy(a, w, tproc, ts_j, cx, ps.x, ps.y, ps.z, a.post_mask + (uint64_t)il * kHistWords);
+                w = potentiate_lazy(a, a.tab_p, w, tproc, ts_j, cx, ps.x, ps.y, ps.z, a.post_mask + (uint64_t)il * kHistWords);
             } else {
                 w = 0.0f;
             }
@@ -1415,7 +1469,7 @@ size_t tile_smem_bytes(uint32_t TW, uint32_t NR, uint32_t prod_words) {
 // ([TW] each), region prefix, scan tmp, staging.
 size_t plastic_smem_bytes(uint32_t TW, uint32_t NR) {
     const uint32_t tw4 = (TW + 3u) & ~3u;
-    return ((size_t)7 * tw4 + ((NR + 1 + 3) & ~3u) + 32 + kStageWords) * 4 + 16;
+    return ((size_t)7 * tw4 + ((NR + 1 + 3) & ~3u) + 32 + kStageWords + kTraceLen + kPlChunks + 4) * 4 + 16;
 }
 __device__ __forceinline__ PlasticSmem carve_plastic(const SimArgs &a, uint32_t *smem) {
     PlasticSmem sm;
@@ -1430,14 +1484,30 @@ __device__ __forceinline__ PlasticSmem carve_plastic(const SimArgs &a, uint32_t 
     sm.pref = smem + 7 * tw4;
     sm.tmp = sm.pref + ((a.NR + 1 + 3) & ~3u);
     sm.stage = sm.tmp + 32;
+    sm.tabp = reinterpret_cast<float *>(sm.stage + kStageWords);
+    sm.cst = sm.stage + kStageWords + kTraceLen;
     return sm;
+}
+__device__ __forceinline__ void load_trace_table(const SimArgs &a, const PlasticSmem &sm) {
+    const float4 *src = reinterpret_cast<const float4 *>(a.tab_p);
+    float4 *dst = reinterpret_cast<float4 *>(sm.tabp);
+    for (uint32_t x = threadIdx.x; x < kTraceLen / 4; x += kBlock) dst[x] = src[x];
 }
 // the tile's delivered step: counters -> ring slot t + delay, fixed-point sums -> plastic ring
 __device__ __forceinline__ void plastic_flush(const SimArgs &a, uint64_t t, uint32_t b, const PlasticSmem &sm) {
-    const uint64_t base = mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
-    for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
-        a.ring[base + x] += sm.cnt[x];
-        a.pring[base + x] += (long long)(((uint64_t)sm.phi[x] << 32) | sm.plo[x]);
+    const uint64_t base = modD(a, t + a.delay) * a.ring_stride + (uint64_t)b * a.TW;
+    // slot t + delay was consumed (zeroed) by the update of step t + delay - D < t; only
+    // longer per-synapse delays of earlier steps add into it, else this is its sole writer
+    if (a.dly) {
+        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
+            a.ring[base + x] += sm.cnt[x];
+            a.pring[base + x] += (long long)(((uint64_t)sm.phi[x] << 32) | sm.plo[x]);
+        }
+    } else {
+        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
+            a.ring[base + x] = sm.cnt[x];
+            a.pring[base + x] = (long long)(((uint64_t)sm.phi[x] << 32) | sm.plo[x]);
+        }
     }
 }
 
@@ -1462,7 +1532,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver(SimArgs a, uint32_t k) {
     __syncthreads();
     deliver_padded(a, t, b, c, sm.cnt, sm.stage);
     const uint32_t d = 0;                                // (counted from out-degrees by the producers)
-    uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + (uint64_t)b * a.TW;
+    uint32_t *dst = a.ring + modD(a, t + a.delay) * a.ring_stride + (uint64_t)b * a.TW;
     if (a.C == 1u) {
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u) {
             uint4 o = *reinterpret_cast<uint4 *>(dst + x);
@@ -1493,6 +1563,8 @@ __global__ void __launch_bounds__(kBlock) k_deliver_plastic(SimArgs a, uint32_t 
     const uint64_t t = *a.t0 + k;
     const uint32_t b = blockIdx.x;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.plo[x] = 0u; sm.phi[x] = 0u; }
+    load_trace_table(a, sm);
+    __syncthreads();
     const uint32_t d = deliver_tile_plastic(a, t, b, sm);
     plastic_flush(a, t, b, sm);
     store_delivered(a, b, d, sm.tmp);
@@ -1545,6 +1617,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         phase_mark(a, 0);
         if (threadIdx.x == 0) s_count3 = 0;
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.plo[x] = 0u; sm.phi[x] = 0u; }
+        load_trace_table(a, sm);                            // (constant: before the dependent-launch wait)
         __shared__ bool s_upd;
         if (threadIdx.x == 0) s_upd = false;
         asm volatile("griddepcontrol.wait;" ::: "memory");          // (programmatic dependent launch)
@@ -1581,7 +1654,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
                                   MODEL == 4 ? nullptr : (const void *)(a.ref + lo0),
                                   MODEL == 1 ? (const void *)(a.ge + lo0) : nullptr,
                                   MODEL == 1 ? (const void *)(a.gi + lo0) : nullptr,
-                                  a.delay > 1 ? (const void *)(a.ring + mod32(t + 1, a.D) * a.ring_stride + lo0) : nullptr};
+                                  a.delay > 1 ? (const void *)(a.ring + modD(a, t + 1) * a.ring_stride + lo0) : nullptr};
 #pragma unroll
             for (int q = 0; q < 5; ++q)
                 if (arr[q]) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(arr[q]), "r"(nb) : "memory");
@@ -1643,7 +1716,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         } else {
             if (a.C > 1) cluster_reduce_slice(a, sm.cnt, c);   // slice summed in place
             phase_mark(a, 6);
-            uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + lo;
+            uint32_t *dst = a.ring + modD(a, t + a.delay) * a.ring_stride + lo;
             for (uint32_t x = threadIdx.x * 4u; x < a.TWs; x += kBlock * 4u) {
                 uint4 o = *reinterpret_cast<const uint4 *>(cnt + x);
                 if (V & 2) {                                  // the slot may hold longer-delay arrivals
@@ -1714,7 +1787,7 @@ __global__ void __launch_bounds__(kBlock) k_small(SimArgs a, uint32_t k0, uint32
             rdg[x] = a.deg[x];
         }
     const uint64_t t0 = *a.t0 + k0;
-    uint32_t *slot0 = a.ring + mod32(t0, a.D) * a.ring_stride;
+    uint32_t *slot0 = a.ring + modD(a, t0) * a.ring_stride;
     for (uint32_t x = tid * 4u; x < TW; x += kBlock * 4u) {    // stage state + step t0's inputs
         if (MODEL == 4) *reinterpret_cast<uint4 *>(sp.acc + x) = *reinterpret_cast<const uint4 *>(a.acc + x);
         if (MODEL != 4) *reinterpret_cast<float4 *>(sp.v + x) = *reinterpret_cast<const float4 *>(a.v + x);
@@ -1761,7 +1834,7 @@ __global__ void __launch_bounds__(kBlock) k_small(SimArgs a, uint32_t k0, uint32
         __syncthreads();
     }
     // step t0 + nsteps's inputs -> its ring slot (added: the slot is otherwise empty)
-    uint32_t *slot1 = a.ring + mod32(t0 + nsteps, a.D) * a.ring_stride;
+    uint32_t *slot1 = a.ring + modD(a, t0 + nsteps) * a.ring_stride;
     for (uint32_t x = tid * 4u; x < TW; x += kBlock * 4u) {
         uint4 o = *reinterpret_cast<uint4 *>(slot1 + x);
         o.x += cnt[x]; o.y += cnt[x + 1]; o.z += cnt[x + 2]; o.w += cnt[x + 3];
@@ -1805,7 +1878,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver_proc(SimArgs a, uint32_t k) 
     const uint32_t n_sp = pref[a.NR];
     const uint32_t lo = b * a.TW, width = min(a.TW, a.n_own - lo), nblk = (width + 3u) / 4u;
     const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
-    const uint32_t tD = (uint32_t)mod32(t, a.D);
+    const uint32_t tD = (uint32_t)modD(a, t);
     uint32_t hits = 0;
     const uint64_t total = (uint64_t)n_sp * nblk;
     for (uint64_t f = threadIdx.x; f < total; f += kBlock) {
@@ -1842,7 +1915,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver_proc(SimArgs a, uint32_t k) 
         }
     }
     __syncthreads();
-    uint32_t *dst = a.ring + mod32(t + a.delay, a.D) * a.ring_stride + lo;
+    uint32_t *dst = a.ring + modD(a, t + a.delay) * a.ring_stride + lo;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) dst[x] += cnt[x];
     store_delivered(a, b, hits, tmp);
 }
@@ -1891,7 +1964,7 @@ __global__ void __launch_bounds__(kBlock) k_global_atomics(SimArgs a, uint32_t k
     const uint32_t n_sp = pref[a.NR];
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t)gridDim.x * (kBlock / 32);
-    uint32_t *slot = a.ring + mod32(t + a.delay, a.D) * a.ring_stride;
+    uint32_t *slot = a.ring + modD(a, t + a.delay) * a.ring_stride;
     const uint64_t lbase = (uint64_t)par * a.NR * a.RS;
     uint32_t delivered = 0;
     for (uint64_t w = (uint64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); w < (uint64_t)a.NT * n_sp; w += nwarps) {
@@ -1908,7 +1981,7 @@ __global__ void __launch_bounds__(kBlock) k_global_atomics(SimArgs a, uint32_t k
             const uint32_t x = (uint32_t)a.ent[st + e] >> a.eshift;
             if (x >= a.TW) continue;                     // skip padding sentinels
             if (a.dly && a.dly[st + e] != a.delay)       // longer per-synapse delay (reading R19)
-                atomicAdd(a.ring + mod32(t + a.dly[st + e], a.D) * a.ring_stride + (uint64_t)b * a.TW + x, qv);
+                atomicAdd(a.ring + modD(a, t + a.dly[st + e]) * a.ring_stride + (uint64_t)b * a.TW + x, qv);
             else
                 atomicAdd(tile + x, qv);
         }
@@ -1931,7 +2004,7 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
         const uint32_t idx = r * kB2LWords + q0 + threadIdx.x;
         const bool in = q0 + threadIdx.x < kB2LWords && idx < nw;
         const uint32_t word = in ? a.gather[(a.peers ? (uint64_t)par * nw : 0ull) + idx] : 0u;
-        if (in) a.record[mod32(t, a.record_steps) * (uint64_t)nw + idx] = word;
+        if (in) a.record[modR(a, t) * (uint64_t)nw + idx] = word;
         const uint32_t cnt = __popc(word), incl = warp_incl_scan(cnt);
         const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
         uint32_t base = 0;

@@ -109,6 +109,7 @@ struct SimArgs {
                              // across the cluster through distributed shared memory
     uint64_t ring_stride;    // NT * TW
     uint32_t record_steps;
+    uint64_t mD, mR;         // fast remainders mod D / record_steps: floor((2^64 - 1) / m) + 1
     uint32_t pdl;            // 1: fused step kernels use programmatic dependent launch
     uint32_t prod_words;     // synth fast path (G = 1): producer-warp shared-memory words
     uint32_t key0, key1;
