@@ -5,6 +5,9 @@ outputs the oracle can compute one by one (R17):
   row; one full-size step replayed by the oracle from the GPU's state and inputs
   (update bit-exact for all 100K neurons); the input ring after delivery equals the sum of
   the oracle's rows of that step's spiking sources (every target).
+* Brunel+ 50K (250M synapses, 200M plastic): the whole network free-runs bit-exact
+  against the oracle past one full flush period of the lazy STDP rows (reading R13):
+  every spike, every weight, membrane potentials, traces and the input rings.
 * Synth 3e9 synapses (one B200): every neuron's spike train bit-exact (the oracle
   simulates the synth drive for all 1.39M neurons); the accumulators of sampled targets
   equal the spike counts of the oracle's column (in-degree sources) of that target.
@@ -103,3 +106,35 @@ def test_synth3b_spikes_and_sampled_accumulators(S):
     assert st["fired"] == sum(len(s) for s in want)
     # every delivered event is one (spike, synapse) pair: K per target on average
     assert abs(st["delivered"] / max(1, sum(len(s) for s in want)) - cfg.rules[0].k) < 0.02 * cfg.rules[0].k
+
+
+def test_brunelplus50k_full_size_free_run(S):
+    """Brunel+ at BASELINE configs[2]'s full size in bench.py's launch configuration: the
+    oracle simulates the same 250M-synapse network (~40 ms per step on one host core) for
+    1100 steps, past the 1024-step flush period, so every plastic row has been processed
+    lazily (spike or flush) at least once; all state is compared bit-exact."""
+    cfg = W.brunel_plus(50_000)
+    T = 1100
+    o = O.OracleNet(cfg)
+    o.step(T)
+    want = o.spikes()
+    with S.Network(cfg, record_steps=T) as net:
+        assert net.info()["n_synapses"] == o.nnz
+        net.step(T)
+        got = net.read_spikes(0, T)
+        bad = [t for t in range(T) if not np.array_equal(got[t], want[t])]
+        assert not bad, f"first mismatching step {bad[0]}"
+        assert sum(len(x) for x in want) > 100 * T
+        w_gpu, w_orc = net.weights(), o.weights()
+        moved = np.count_nonzero(w_orc[o.plastic_flags() == 1] != np.float32(cfg.params[15]))
+        assert moved > 0
+        assert np.array_equal(w_gpu, w_orc), np.flatnonzero(w_gpu != w_orc)[:10]
+        del w_gpu, w_orc
+        assert np.array_equal(net.state(S.FIELD_V), o.state(O.F_V))
+        assert np.array_equal(net.state(S.FIELD_XTR), o.state(O.F_XTR))
+        assert np.array_equal(net.state(S.FIELD_YTR), o.state(O.F_YTR))
+        for rel in range(cfg.delay + 1):
+            c1, p1 = net.input(rel)
+            c2, p2 = o.input(rel)
+            assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
+        assert net.stats()["delivered"] == int(o.delivered().sum())
