@@ -319,6 +319,18 @@ SPICE_API spice_status spice_exchange_end_fused(spice_net *net);
  * (both handles on the same device; ordered after src's update; returns when done). */
 SPICE_API spice_status spice_exchange_put(spice_net *dst, spice_net *src);
 
+/* External exchange over the caller's own transport (MPI, a custom NVLink kernel, ...;
+ * P:287-290 §III-D/E: every rank needs every rank's spikes of the step).  get_send copies
+ * this rank's send buffer (words_per_rank u32 words: the step's spike bitmap, valid after
+ * spice_exchange_begin or spice_exchange_end_fused) to `out`; set_recv fills rank r's
+ * receive segment (words_per_rank words) from `words`.  on_device != 0: device pointers on
+ * the network's device, the copy is enqueued on the network's stream (asynchronous, stream
+ * ordered, capturable); 0: host memory, the call returns when the copy is done.  The caller
+ * owns both buffers; bits past rank r's owned neurons are ignored.  SPICE_EINVAL for a null pointer or rank >= world_size, SPICE_ESTATE
+ * for a network without SPICE_FLAG_EXTERNAL_EXCHANGE. */
+SPICE_API spice_status spice_exchange_get_send(spice_net *net, uint32_t *out, int on_device);
+SPICE_API spice_status spice_exchange_set_recv(spice_net *net, uint32_t rank, const uint32_t *words, int on_device);
+
 /* PEER exchange (spice_config.exchange = SPICE_EXCHANGE_PEER, world_size > 1): the
  * device-initiated spike synchronisation (§III-D/E, "the
  * spike synchronization time is entirely dominated by CUDA API overhead").  Every rank owns a

@@ -674,9 +674,11 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     }
     n->pad8 = n->model != SPICE_BRUNEL_PLUS && !n->procedural;
     // auto: 2-CTA cluster tiles for large padded networks (half the spike x tile visits per
-    // CTA; measured -4 % step time on synth 3e9, DESIGN.md delivery log), else one CTA per tile
+    // CTA; measured -4 % step time on synth 3e9, DESIGN.md delivery log; at G > 1 the rows
+    // are G times shorter and the threshold is halved: -26 % on the G = 8 weak-scaling slice,
+    // tools/g_proxy.py), else one CTA per tile
     n->C = n->procedural ? 1u : c->ctas_per_tile ? c->ctas_per_tile
-         : (n->pad8 && !c->tile_width && n->n_own >= (uint64_t)n->n_sm * 4096u ? 2u : 1u);
+         : (n->pad8 && !c->tile_width && n->n_own >= (uint64_t)n->n_sm * (n->G > 1 ? 2048u : 4096u) ? 2u : 1u);
     if (n->C > kMaxCluster) return bail(fail(n, SPICE_EINVAL, "ctas_per_tile %u > %u", n->C, kMaxCluster));
     // small networks: one tile of all owned neurons, one CTA runs whole graph chunks
     // (k_small); auto only, SPICE_NOSMALL=1 disables (A/B)
@@ -710,7 +712,13 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // spike-list regions: one per CTA slice (G = 1, written by the slice's update) or one per
     // kB2LWords gathered bitmap words (G > 1, written by bitmap->list)
     if (n->G == 1) { n->NR = n->NT * n->C; n->RS = n->TWs; }
-    else { n->NR = (uint32_t)(((uint64_t)n->G * n->W + kB2LWords - 1) / kB2LWords); n->RS = kB2LWords * 32; }
+    else {      // about one region per SM: bitmap->list (and its descriptor writes) in one wave
+        const uint64_t gw = (uint64_t)n->G * n->W;
+        uint64_t bw = (gw + n->n_sm - 1) / n->n_sm;
+        bw = std::max<uint64_t>(kB2LWords, (bw + 31) / 32 * 32);
+        n->NR = (uint32_t)((gw + bw - 1) / bw);
+        n->RS = (uint32_t)(bw * 32);
+    }
     if (n->NR > kMaxRegions) return bail(fail(n, SPICE_EINVAL, "%u spike-list regions > %u: use a wider tile_width", n->NR, kMaxRegions));
     const size_t smem_max = 227 * 1024 - 2048 - 6 * 1024;  // dynamic; static shared variables need the rest
     if (n->model == SPICE_SYNTH && n->G == 1 && n->pad8 && tile_smem_bytes(n->TW, n->NR, kSynthProdWordsHost) <= smem_max)
@@ -1057,6 +1065,35 @@ spice_status spice_exchange_put(spice_net *dst, spice_net *src) {
                             cudaMemcpyDeviceToDevice, dst->stream));
     // test hook: complete the copy so src may overwrite its send buffer next step
     CU(dst, cudaStreamSynchronize(dst->stream));
+    return SPICE_OK;
+}
+
+spice_status spice_exchange_get_send(spice_net *n, uint32_t *out, int on_device) {
+    CHECK_NET(n);
+    if (!n->external) return fail(n, SPICE_ESTATE, "not an external-exchange network");
+    if (!out) return fail(n, SPICE_EINVAL, "null buffer");
+    const size_t bytes = (size_t)n->W * 4;
+    if (on_device) {
+        CU(n, cudaMemcpyAsync(out, n->sendbuf, bytes, cudaMemcpyDeviceToDevice, n->stream));
+    } else {
+        CU(n, cudaMemcpyAsync(out, n->sendbuf, bytes, cudaMemcpyDeviceToHost, n->stream));
+        CU(n, cudaStreamSynchronize(n->stream));
+    }
+    return SPICE_OK;
+}
+
+spice_status spice_exchange_set_recv(spice_net *n, uint32_t rank, const uint32_t *words, int on_device) {
+    CHECK_NET(n);
+    if (!n->external) return fail(n, SPICE_ESTATE, "not an external-exchange network");
+    if (!words || rank >= n->G) return fail(n, SPICE_EINVAL, "null buffer or rank out of range");
+    const size_t bytes = (size_t)n->W * 4;
+    uint32_t *dst = n->gather + (uint64_t)rank * n->W;
+    if (on_device) {
+        CU(n, cudaMemcpyAsync(dst, words, bytes, cudaMemcpyDeviceToDevice, n->stream));
+    } else {
+        CU(n, cudaMemcpyAsync(dst, words, bytes, cudaMemcpyHostToDevice, n->stream));
+        CU(n, cudaStreamSynchronize(n->stream));
+    }
     return SPICE_OK;
 }
 

@@ -2000,10 +2000,15 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
     __syncthreads();
     uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + r) * a.RS;
     uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + r) * a.RS;
-    for (uint32_t q0 = 0; q0 < kB2LWords; q0 += kBlock) {
-        const uint32_t idx = r * kB2LWords + q0 + threadIdx.x;
-        const bool in = q0 + threadIdx.x < kB2LWords && idx < nw;
-        const uint32_t word = in ? a.gather[(a.peers ? (uint64_t)par * nw : 0ull) + idx] : 0u;
+    const uint32_t bw = a.RS / 32;                      // bitmap words of this region
+    for (uint32_t q0 = 0; q0 < bw; q0 += kBlock) {
+        const uint32_t idx = r * bw + q0 + threadIdx.x;
+        const bool in = q0 + threadIdx.x < bw && idx < nw;
+        uint32_t word = in ? a.gather[(a.peers ? (uint64_t)par * nw : 0ull) + idx] : 0u;
+        if (word) {               // bits past the rank's owned neurons (global ID >= N) are ignored
+            const uint64_t j0 = local_to_global((uint64_t)(idx % a.W) * 32, idx / a.W, a.G, a.S);
+            word = j0 >= a.N ? 0u : (a.N - j0 >= 32 ? word : word & ((1u << (a.N - j0)) - 1u));
+        }
         if (in) a.record[modR(a, t) * (uint64_t)nw + idx] = word;
         const uint32_t cnt = __popc(word), incl = warp_incl_scan(cnt);
         const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);

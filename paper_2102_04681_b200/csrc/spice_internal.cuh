@@ -30,7 +30,7 @@ constexpr int kBlock = SPICE_KBLOCK;  // threads per tile CTA (update / deliver 
 constexpr int kStageWords = 12288;     // bnd rows staged per descriptor-transposition pass
 constexpr uint32_t kMaxTileWidth = 49152;   // u32 counters per tile <= 192 KiB smem
 constexpr uint32_t kMaxRegions = 4096;      // spike-list regions per step
-constexpr uint32_t kB2LWords = 256;         // bitmap words per bitmap->list region
+constexpr uint32_t kB2LWords = 256;         // minimum bitmap words per bitmap->list region
 constexpr int kEntPad = 64;           // u16 padding before/after the entry array
 // Padded layout: every (row, tile) segment is a whole number of delivery windows of
 // kWin u16 entries, starting at a window boundary.  16-byte windows (kWinShift = 3)

@@ -97,6 +97,8 @@ def lib():
         "spice_exchange_end": (st, [vp]),
         "spice_exchange_end_fused": (st, [vp]),
         "spice_exchange_put": (st, [vp, vp]),
+        "spice_exchange_get_send": (st, [vp, vp, i32]),
+        "spice_exchange_set_recv": (st, [vp, u32, vp, i32]),
         "spice_peer_handle": (st, [vp, vp]),
         "spice_peer_connect": (st, [vp, vp]),
         "spice_partition_owner": (u32, [u64, u32, u32]),
@@ -110,6 +112,15 @@ def lib():
         f.restype, f.argtypes = res, args
     _lib = L
     return L
+
+
+def _ptr(buf) -> int:
+    """Address of a numpy array, a torch tensor or a raw integer pointer."""
+    if isinstance(buf, int):
+        return buf
+    if isinstance(buf, np.ndarray):
+        return buf.ctypes.data
+    return buf.data_ptr()
 
 
 def _check(status: int) -> None:
@@ -198,6 +209,9 @@ class Network:
         info = self.info()
         self.n_owned = info["n_owned"]
         self.slice_width = slice_width or default_slice_width(cfg.n, world_size)
+        # u32 words of one rank's spike bitmap in the exchange buffers
+        self.words_per_rank = (max(partition_owned_count(cfg.n, r, world_size, self.slice_width)
+                                   for r in range(world_size)) + 31) // 32
 
     # lifecycle ---------------------------------------------------------------
     def free(self) -> None:
@@ -377,6 +391,16 @@ class Network:
 
     def exchange_put_from(self, src: "Network") -> None:
         _check(lib().spice_exchange_put(self.h, src.h))
+
+    def exchange_get_send(self, out, on_device: bool = False):
+        """This rank's send bitmap -> `out` (numpy uint32[words_per_rank], or a device
+        pointer / torch tensor with on_device=True)."""
+        _check(lib().spice_exchange_get_send(self.h, _ptr(out), 1 if on_device else 0))
+        return out
+
+    def exchange_set_recv(self, rank: int, words, on_device: bool = False) -> None:
+        """Fill rank `rank`'s receive segment from `words` (host array or device pointer)."""
+        _check(lib().spice_exchange_set_recv(self.h, rank, _ptr(words), 1 if on_device else 0))
 
     # PEER exchange (device-initiated bitmap stores into every rank's window) --------
     def peer_handle(self) -> bytes:

@@ -141,3 +141,39 @@ def test_bench_two_ranks_peer_parity(S):
     assert line["n_gpus"] == 2 and line["scaling"] == "strong"
     assert line["parity"]["ok"] is True and line["parity"]["ranks"] == 2
     assert line["config"]["exchange"].startswith("device-initiated")
+
+
+def test_external_exchange_over_host_buffers(S):
+    """spice_exchange_get_send / _set_recv: G = 3 virtual ranks whose bitmaps travel through
+    host memory (a caller-owned transport) on the fused G > 1 sequence; spike trains equal
+    the G = 1 oracle's."""
+    cfg, T, G = W.synth(5003, 31, 0.05, seed=23), 40, 3
+    o = O.OracleNet(cfg)
+    o.step(T)
+    want = o.spikes()
+    nets = [S.Network(cfg, rank=g, world_size=G, external_exchange=True, record_steps=T)
+            for g in range(G)]
+    try:
+        Wd = nets[0].words_per_rank
+        bufs = [np.zeros(Wd, dtype=np.uint32) for _ in range(G)]
+        for n in nets:
+            n.exchange_begin()
+        for t in range(T):
+            for g, n in enumerate(nets):
+                n.exchange_get_send(bufs[g])
+            for n in nets:
+                for g in range(G):
+                    n.exchange_set_recv(g, bufs[g])
+            for n in nets:
+                if t < T - 1:
+                    n.exchange_end_fused()
+                else:
+                    n.exchange_end()
+        for n in nets:
+            got = n.read_spikes(0, T)
+            assert all(np.array_equal(a, b) for a, b in zip(got, want))
+        with pytest.raises(S.SpiceError):
+            nets[0].exchange_set_recv(G, bufs[0])
+    finally:
+        for n in nets:
+            n.free()
