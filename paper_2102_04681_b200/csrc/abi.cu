@@ -881,6 +881,15 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.rank = n->rank; a.G = n->G; a.S = n->S; a.n_own = (uint32_t)n->n_own; a.W = n->W;
     a.TW = n->TW; a.NT = n->NT; a.C = n->C; a.TWs = n->TWs; a.ring_stride = n->ring_stride; a.record_steps = n->R;
     a.mD = ~0ull / a.D + 1; a.mR = ~0ull / a.record_steps + 1;
+    if (n->model == SPICE_BRUNEL_PLUS) {
+        // every plastic weight stays in [0, max(w0, w_max)] (clamped potentiation, depression
+        // floored at 0), so q = rint(w 2^32) <= qmax; a target receives at most N events per
+        // step: the split sums cannot wrap when N (2^16 - 1) < 2^32 and N (qmax >> 16) < 2^32
+        const double wtop = std::max(n->prm.size() > 15 ? n->prm[15] : 0.0, n->prm.size() > 14 ? n->prm[14] : 0.0);
+        const double qmax = std::ceil(std::max(wtop, 0.0) * 4294967296.0);
+        a.pl_split = (uint64_t)n->N * 65535ull < (1ull << 32) && qmax < 9.0e15 &&
+                     (double)n->N * std::floor(qmax / 65536.0) < 4294967296.0 ? 1u : 0u;
+    }
     a.prod_words = n->prod_words;
     if (getenv("SPICE_PHASES") && atoi(getenv("SPICE_PHASES"))) {     // diagnostics only
         if ((st = dalloc_t(n, &n->ptimes, (size_t)n->NT * n->C * 16, "phase clocks"))) return bail(st);

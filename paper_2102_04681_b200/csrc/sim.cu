@@ -1151,9 +1151,16 @@ __device__ __forceinline__ void plastic_deliver(const SimArgs &a, uint32_t *cnt,
         float nw = __fsub_rn(wv, __fmul_rn(a.mc.Am, ys[off]));     // (ii)
         nw = nw > 0.0f ? nw : 0.0f;
         a.w[e] = nw;
-        const uint64_t q = (uint64_t)__double2ll_rn((double)nw * 4294967296.0);   // (iii)
+        // (iii) rint(w 2^32): w 2^32 is exact in fp32 (a power-of-two scaling), so the fp32
+        // round-to-nearest-even conversion equals the fp64 one
+        const uint64_t q = (uint64_t)__float2ll_rn(nw * 4294967296.0f);
         if (gslot != ~0ull) {
             atomicAdd(reinterpret_cast<unsigned long long *>(a.pring + gslot), (unsigned long long)q);
+            return;
+        }
+        if (a.pl_split) {                            // fire-and-forget: no returned value
+            atomicAdd(&plo[off], (uint32_t)q & 0xFFFFu);
+            atomicAdd(&phi[off], (uint32_t)(q >> 16));
             return;
         }
         const uint32_t lo = (uint32_t)q, hi = (uint32_t)(q >> 32);
@@ -1185,7 +1192,8 @@ struct PlasticSmem {
 // flush rows the potentiated weight is stored.  Static synapses of spike rows add their
 // packed receptor count.
 constexpr uint32_t kPlSeg = 1800;                     // segments staged per pass (6 words each)
-constexpr uint32_t kPlFlush = kStageWords - 6 * kPlSeg - 2;   // flush-row list capacity
+// flush-row list capacity (the stage's last 64 words are the overlapped update's scratch)
+constexpr uint32_t kPlFlush = kStageWords - 6 * kPlSeg - 2 - 64;
 #ifndef SPICE_PL_U
 #define SPICE_PL_U 2
 #endif
@@ -1498,15 +1506,16 @@ __device__ __forceinline__ void plastic_flush(const SimArgs &a, uint64_t t, uint
     const uint64_t base = modD(a, t + a.delay) * a.ring_stride + (uint64_t)b * a.TW;
     // slot t + delay was consumed (zeroed) by the update of step t + delay - D < t; only
     // longer per-synapse delays of earlier steps add into it, else this is its sole writer
+    const uint32_t sh = a.pl_split ? 16u : 32u;
     if (a.dly) {
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
             a.ring[base + x] += sm.cnt[x];
-            a.pring[base + x] += (long long)(((uint64_t)sm.phi[x] << 32) | sm.plo[x]);
+            a.pring[base + x] += (long long)(((uint64_t)sm.phi[x] << sh) + sm.plo[x]);
         }
     } else {
         for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) {
             a.ring[base + x] = sm.cnt[x];
-            a.pring[base + x] = (long long)(((uint64_t)sm.phi[x] << 32) | sm.plo[x]);
+            a.pring[base + x] = (long long)(((uint64_t)sm.phi[x] << sh) + sm.plo[x]);
         }
     }
 }

@@ -111,6 +111,9 @@ struct SimArgs {
     uint32_t record_steps;
     uint64_t mD, mR;         // fast remainders mod D / record_steps: floor((2^64 - 1) / m) + 1
     uint32_t pdl;            // 1: fused step kernels use programmatic dependent launch
+    uint32_t pl_split;       // Brunel+: plastic fixed point q summed as (q mod 2^16) and
+                             // (q >> 16) in two u32 words (no carry round trip; abi.cu proves
+                             // neither sum can wrap), else low word + carry into the high word
     uint32_t prod_words;     // synth fast path (G = 1): producer-warp shared-memory words
     uint32_t key0, key1;
     uint32_t NR, RS;         // spike-list regions
