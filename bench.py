@@ -369,6 +369,9 @@ def main_spice(args):
     e2e_s = allreduce(e2e_s, MAX)
     e2e_events = events / args.steps * nchunks * K     # same per-step work
     e2e_value = e2e_events / e2e_s
+    compacted = K * G * ((words + 31) // 32) >= (1 << 16)
+    if compacted:   # device-compacted read-out: counts + the IDs guess (1.25 x the last chunk + 4096)
+        d2h = int(4 + 4 * (1.25 * got_spikes / (nchunks * K) + 4096 / K))
 
     parity = None
     if not args.no_parity:
@@ -424,8 +427,12 @@ def main_spice(args):
                      "kernel_ms": prof},
         "e2e": {"value": e2e_value, "unit": "events/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": d2h, "steps": nchunks * K, "spikes_read": got_spikes,
-                "note": f"spice_step({K}) + spice_spikes_prefetch of those steps' bitmaps to pinned host memory, "
-                        f"decoded by spice_spikes_collect while the next chunk runs (double-buffered)"},
+                "note": (f"spice_step({K}) + spice_spikes_prefetch of those steps: bitmaps compacted into "
+                         f"ascending spike IDs on the device, counts and IDs copied to pinned host memory, "
+                         f"spice_spikes_collect fills the caller's arrays while the next chunk runs (double-buffered)"
+                         if compacted else
+                         f"spice_step({K}) + spice_spikes_prefetch of those steps' bitmaps to pinned host memory, "
+                         f"decoded by spice_spikes_collect while the next chunk runs (double-buffered)")},
         "gpu_launches": launches,
         "clocks": ck,
         "parity": parity,

@@ -180,10 +180,15 @@ SPICE_API spice_status spice_free(spice_net *net);
 
 /* Double-buffered spike read-out for streaming runs (same data and ordering as
  * spice_read_spikes).  prefetch enqueues, on the library stream after the steps already
- * enqueued, an asynchronous copy of the recorded bitmaps of steps [t_begin, t_end) into
- * library-owned pinned host slot `slot` (0 or 1) and returns without waiting; collect
- * waits for that slot's copy only (an event, not a stream sync, so later enqueued steps
- * keep running) and decodes it into ids / offsets as spice_read_spikes does.  ERANGE as
+ * enqueued, the compaction of the recorded bitmaps of steps [t_begin, t_end) into per-step
+ * ascending global IDs on the device (two kernels) and an asynchronous copy of the counts
+ * and of the IDs (up to 1.25x the slot's previous total) into library-owned pinned host slot
+ * `slot` (0 or 1), and returns without waiting; collect waits for that slot's copy only (an
+ * event, not a stream sync, so later enqueued steps keep running), fetches any IDs beyond
+ * the guess on a private copy stream, and fills ids / offsets as spice_read_spikes does
+ * (ETRUNC with *total set when cap is too small; the slot stays full).  Device buffers of
+ * (t_end - t_begin) x n_neurons IDs per slot are allocated on first use.  Chunks of fewer
+ * than 2^16 bitmap words are copied as bitmaps and decoded on the host.  ERANGE as
  * spice_read_spikes (t_end may exceed the steps enqueued so far by 0); ESTATE when collect
  * names an empty slot. */
 SPICE_API spice_status spice_spikes_prefetch(spice_net *net, uint64_t t_begin, uint64_t t_end,

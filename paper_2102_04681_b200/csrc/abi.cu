@@ -171,11 +171,14 @@ struct spice_net {
     uint32_t *hbm = nullptr;            // pinned host staging of recorded bitmaps (read_spikes)
     uint64_t hbm_words = 0;
     struct Slot {                       // double-buffered read-out (spikes_prefetch/collect)
-        uint32_t *h = nullptr;
+        uint32_t *h = nullptr;          // pinned: the chunk's packed IDs
         uint64_t words = 0, t_begin = 0, t_end = 0;
-        bool full = false;
+        uint32_t *d_ids = nullptr, *d_cnt = nullptr, *h_cnt = nullptr;   // device IDs / counts, pinned counts
+        uint64_t dcap = 0, ccap = 0, copied = 0, guess = 0;
+        bool full = false, compact = false;
         cudaEvent_t done = nullptr;
     } slot[2];
+    cudaStream_t xfer = nullptr;        // read-out: copies that must not queue behind later steps
     std::vector<std::vector<uint32_t>> hdec;   // decoded per-step lists (reused)
     uint32_t NR = 1, RS = 32;    // spike-list regions
     uint32_t prod_words = 0;     // synth fast path: producer-warp shared memory (words)
@@ -429,8 +432,10 @@ void destroy(spice_net *n) {
     if (n->hbm) cudaFreeHost(n->hbm);
     for (auto &sl : n->slot) {
         if (sl.h) cudaFreeHost(sl.h);
+        if (sl.h_cnt) cudaFreeHost(sl.h_cnt);
         if (sl.done) cudaEventDestroy(sl.done);
     }
+    if (n->xfer) cudaStreamDestroy(n->xfer);
     if (n->stream && n->own_stream) cudaStreamDestroy(n->stream);
     if (n->cap_stream) cudaStreamDestroy(n->cap_stream);
     delete n;
@@ -1180,27 +1185,69 @@ spice_status spice_spikes_prefetch(spice_net *n, uint64_t t_begin, uint64_t t_en
                     (unsigned long long)(n->t_host > n->R ? n->t_host - n->R : 0), (unsigned long long)n->t_host);
     spice_net::Slot &sl = n->slot[slot];
     if (sl.full) CU(n, cudaEventSynchronize(sl.done));    // (an uncollected earlier copy)
-    const uint64_t words = (uint64_t)n->G * n->W, need = std::max<uint64_t>((t_end - t_begin) * words, 1);
-    if (sl.words < need) {
+    const uint64_t words = (uint64_t)n->G * n->W, nsteps = t_end - t_begin;
+    if (!sl.done) CU(n, cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    sl.t_begin = t_begin;
+    sl.t_end = t_end;
+    sl.compact = nsteps * words >= (1u << 16);
+    if (!sl.compact) {         // small bitmaps: copy them as they are, collect decodes on the host
+        const uint64_t need = std::max<uint64_t>(nsteps * words, 1);
+        if (sl.words < need) {
+            if (sl.h) cudaFreeHost(sl.h);
+            sl.h = nullptr;
+            sl.words = 0;
+            CU(n, cudaMallocHost(reinterpret_cast<void **>(&sl.h), need * 4));
+            sl.words = need;
+        }
+        for (uint64_t t = t_begin; t < t_end;) {        // one copy per contiguous run of ring slots
+            const uint64_t rs = t % n->R;
+            const uint64_t run = std::min<uint64_t>(t_end - t, n->R - rs);
+            CU(n, cudaMemcpyAsync(sl.h + (t - t_begin) * words, n->record + rs * words, run * words * 4,
+                                  cudaMemcpyDeviceToHost, n->stream));
+            t += run;
+        }
+        CU(n, cudaEventRecord(sl.done, n->stream));
+        sl.full = true;
+        return SPICE_OK;
+    }
+    // the chunk's bitmaps are compacted on the device into per-step counts and packed
+    // ascending IDs; the counts and a guess of the IDs (1.25x the previous chunk's total)
+    // are copied now, collect fetches any remainder
+    const uint64_t worst = std::max<uint64_t>(nsteps * n->N, 1);
+    spice_status st;
+    if (sl.dcap < worst) {
+        dfree(n, sl.d_ids);
+        sl.d_ids = nullptr;
+        sl.dcap = 0;
+        if ((st = dalloc_t(n, &sl.d_ids, worst, "read-out IDs"))) return st;
+        sl.dcap = worst;
+    }
+    if (sl.ccap < nsteps + 1) {
+        dfree(n, sl.d_cnt);
+        sl.d_cnt = nullptr;
+        if (sl.h_cnt) cudaFreeHost(sl.h_cnt);
+        sl.h_cnt = nullptr;
+        sl.ccap = 0;
+        if ((st = dalloc_t(n, &sl.d_cnt, nsteps + 1, "read-out counts"))) return st;
+        CU(n, cudaMallocHost(reinterpret_cast<void **>(&sl.h_cnt), (nsteps + 1) * 4));
+        sl.ccap = nsteps + 1;
+    }
+    if (!sl.guess) sl.guess = nsteps * std::max<uint64_t>(1024, n->N / 32);
+    const uint64_t guess = std::min<uint64_t>(sl.guess, worst);
+    if (sl.words < guess) {
         if (sl.h) cudaFreeHost(sl.h);
         sl.h = nullptr;
         sl.words = 0;
-        CU(n, cudaMallocHost(reinterpret_cast<void **>(&sl.h), need * 4));
-        sl.words = need;
+        CU(n, cudaMallocHost(reinterpret_cast<void **>(&sl.h), guess * 4));
+        sl.words = guess;
     }
-    if (!sl.done) CU(n, cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
-    // steps enqueued before this call are recorded by the time the copy runs (stream order);
-    // a run that wraps the ring needs one copy per contiguous run of slots
-    for (uint64_t t = t_begin; t < t_end;) {
-        const uint64_t rs = t % n->R;
-        const uint64_t run = std::min<uint64_t>(t_end - t, n->R - rs);
-        CU(n, cudaMemcpyAsync(sl.h + (t - t_begin) * words, n->record + rs * words, run * words * 4,
-                              cudaMemcpyDeviceToHost, n->stream));
-        t += run;
-    }
+    // steps enqueued before this call are recorded by the time the kernels run (stream order)
+    CU(n, launch_compact(n->record, n->R, words, t_begin, (uint32_t)nsteps, n->G, n->W, n->S, n->N, sl.d_cnt,
+                         sl.d_ids, n->stream));
+    CU(n, cudaMemcpyAsync(sl.h_cnt, sl.d_cnt, nsteps * 4, cudaMemcpyDeviceToHost, n->stream));
+    CU(n, cudaMemcpyAsync(sl.h, sl.d_ids, guess * 4, cudaMemcpyDeviceToHost, n->stream));
     CU(n, cudaEventRecord(sl.done, n->stream));
-    sl.t_begin = t_begin;
-    sl.t_end = t_end;
+    sl.copied = guess;
     sl.full = true;
     return SPICE_OK;
 }
@@ -1212,18 +1259,50 @@ spice_status spice_spikes_collect(spice_net *n, uint32_t slot, uint32_t *ids, ui
     spice_net::Slot &sl = n->slot[slot];
     if (!sl.full) return fail(n, SPICE_ESTATE, "slot %u holds no prefetched steps", slot);
     CU(n, cudaEventSynchronize(sl.done));
-    const uint64_t words = (uint64_t)n->G * n->W, nsteps = sl.t_end - sl.t_begin;
-    std::vector<std::vector<uint32_t>> &per = n->hdec;
-    const uint64_t tot = decode_steps(sl.h, nsteps, words, n->G, n->W, n->S, per);
+    const uint64_t nsteps = sl.t_end - sl.t_begin;
+    if (!sl.compact) {
+        const uint64_t words = (uint64_t)n->G * n->W;
+        std::vector<std::vector<uint32_t>> &per = n->hdec;
+        const uint64_t tot = decode_steps(sl.h, nsteps, words, n->G, n->W, n->S, per);
+        if (total) *total = tot;
+        if (tot > cap || (!ids && tot)) return fail(n, SPICE_ETRUNC, "need %llu ids", (unsigned long long)tot);
+        uint64_t o = 0;
+        for (uint64_t q = 0; q < nsteps; ++q) {
+            if (offsets) offsets[q] = o;
+            if (!per[q].empty()) memcpy(ids + o, per[q].data(), per[q].size() * 4);
+            o += per[q].size();
+        }
+        if (offsets) offsets[nsteps] = o;
+        sl.full = false;
+        return SPICE_OK;
+    }
+    uint64_t tot = 0;
+    for (uint64_t q = 0; q < nsteps; ++q) tot += sl.h_cnt[q];
     if (total) *total = tot;
     if (tot > cap || (!ids && tot)) return fail(n, SPICE_ETRUNC, "need %llu ids", (unsigned long long)tot);
+    if (tot > sl.copied) {                               // more than the guess: the rest now
+        if (sl.words < tot) {
+            uint32_t *h2 = nullptr;
+            CU(n, cudaMallocHost(reinterpret_cast<void **>(&h2), tot * 4));
+            memcpy(h2, sl.h, sl.copied * 4);
+            cudaFreeHost(sl.h);
+            sl.h = h2;
+            sl.words = tot;
+        }
+        if (!n->xfer) CU(n, cudaStreamCreateWithFlags(&n->xfer, cudaStreamNonBlocking));
+        CU(n, cudaMemcpyAsync(sl.h + sl.copied, sl.d_ids + sl.copied, (tot - sl.copied) * 4,
+                              cudaMemcpyDeviceToHost, n->xfer));
+        CU(n, cudaStreamSynchronize(n->xfer));
+        sl.copied = tot;
+    }
+    sl.guess = tot + tot / 4 + 4096;
     uint64_t o = 0;
     for (uint64_t q = 0; q < nsteps; ++q) {
         if (offsets) offsets[q] = o;
-        if (!per[q].empty()) memcpy(ids + o, per[q].data(), per[q].size() * 4);
-        o += per[q].size();
+        o += sl.h_cnt[q];
     }
     if (offsets) offsets[nsteps] = o;
+    if (tot) memcpy(ids, sl.h, tot * 4);
     sl.full = false;
     return SPICE_OK;
 }

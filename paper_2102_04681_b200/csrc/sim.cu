@@ -2223,6 +2223,89 @@ cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s) 
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------- read-out compaction
+// Recorded steps [t_begin, t_begin + nsteps) of the bitmap ring (words = G W per step) ->
+// per-step global spike IDs, ascending, packed step after step (spice_spikes_prefetch: only
+// the IDs cross the host link, not the bitmaps).  Global word gw (IDs 32 gw .. 32 gw + 31)
+// lies in global slice gw / (S / 32) = (local slice) G + rank (the partition).
+__device__ __forceinline__ uint32_t global_word(const uint32_t *bm, uint32_t gw, uint32_t G, uint32_t W,
+                                                uint32_t spw, uint32_t N) {
+    const uint32_t sl = gw / spw, rk = sl % G, lw = (sl / G) * spw + gw % spw;
+    uint32_t w = lw < W ? bm[(uint64_t)rk * W + lw] : 0u;
+    const uint32_t rem = N - 32u * gw;                       // (gw < ceil(N / 32))
+    if (rem < 32u) w &= (1u << rem) - 1u;
+    return w;
+}
+// CTA q: the spike count of step t_begin + q -> counts[q]
+__global__ void __launch_bounds__(1024) k_compact_count(const uint32_t *record, uint32_t R, uint64_t words,
+                                                        uint64_t t_begin, uint32_t G, uint32_t W, uint32_t S,
+                                                        uint32_t N, uint32_t *counts) {
+    __shared__ uint32_t s_part[32];
+    const uint32_t *bm = record + ((t_begin + blockIdx.x) % R) * words;
+    const uint32_t GW = (N + 31u) / 32u, spw = S / 32u;
+    uint32_t c = 0;
+    for (uint32_t gw = threadIdx.x; gw < GW; gw += blockDim.x) c += __popc(global_word(bm, gw, G, W, spw, N));
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if ((threadIdx.x & 31u) == 0) s_part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        uint32_t v = threadIdx.x < blockDim.x / 32 ? s_part[threadIdx.x] : 0u;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (threadIdx.x == 0) counts[blockIdx.x] = v;
+    }
+}
+// CTA q: the IDs of step t_begin + q at ids[sum of counts[0 .. q)], ascending; warp w takes a
+// contiguous run of global words (its base: a scan of the warps' counts)
+__global__ void __launch_bounds__(1024) k_compact_ids(const uint32_t *record, uint32_t R, uint64_t words,
+                                                      uint64_t t_begin, uint32_t G, uint32_t W, uint32_t S,
+                                                      uint32_t N, const uint32_t *counts, uint32_t *ids) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint64_t s_base;
+    const uint32_t *bm = record + ((t_begin + blockIdx.x) % R) * words;
+    const uint32_t GW = (N + 31u) / 32u, spw = S / 32u;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x / 32;
+    const uint32_t chunk = (GW + nwarps * 32u - 1) / (nwarps * 32u) * 32u;
+    const uint32_t g0 = min(GW, warp * chunk), g1 = min(GW, g0 + chunk);
+    if (threadIdx.x == 0) {
+        uint64_t b = 0;
+        for (uint32_t q = 0; q < blockIdx.x; ++q) b += counts[q];
+        s_base = b;
+    }
+    uint32_t c = 0;
+    for (uint32_t gw = g0 + lane; gw < g1; gw += 32u) c += __popc(global_word(bm, gw, G, W, spw, N));
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if (lane == 0) s_warp[warp] = c;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t v = lane < nwarps ? s_warp[lane] : 0u;
+        const uint32_t incl = warp_incl_scan(v);
+        s_warp[lane] = incl - v;
+    }
+    __syncthreads();
+    uint32_t *out = ids + s_base + s_warp[warp];
+    uint32_t run = 0;
+    for (uint32_t i = g0; i < g1; i += 32u) {                 // (warp-uniform trips)
+        const uint32_t gw = i + lane;
+        uint32_t w = gw < g1 ? global_word(bm, gw, G, W, spw, N) : 0u;
+        const uint32_t cnt = __popc(w), incl = warp_incl_scan(cnt);
+        uint32_t pos = run + incl - cnt;
+        while (w) {
+            const uint32_t bit = __ffs(w) - 1;
+            w &= w - 1;
+            out[pos++] = 32u * gw + bit;
+        }
+        run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+}
+cudaError_t launch_compact(const uint32_t *record, uint32_t R, uint64_t words, uint64_t t_begin, uint32_t nsteps,
+                           uint32_t G, uint32_t W, uint32_t S, uint32_t N, uint32_t *counts, uint32_t *ids,
+                           cudaStream_t s) {
+    if (!nsteps) return cudaSuccess;
+    k_compact_count<<<nsteps, 1024, 0, s>>>(record, R, words, t_begin, G, W, S, N, counts);
+    k_compact_ids<<<nsteps, 1024, 0, s>>>(record, R, words, t_begin, G, W, S, N, counts, ids);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s) {
     k_advance<<<1, 1, 0, s>>>(t0, steps);
     return cudaGetLastError();

@@ -17,6 +17,10 @@ cudaError_t launch_deliver(const SimArgs &a, uint32_t k, bool global_atomics, in
 cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s);
+// Recorded bitmaps of nsteps steps -> counts[nsteps] and the packed ascending global IDs.
+cudaError_t launch_compact(const uint32_t *record, uint32_t R, uint64_t words, uint64_t t_begin, uint32_t nsteps,
+                           uint32_t G, uint32_t W, uint32_t S, uint32_t N, uint32_t *counts, uint32_t *ids,
+                           cudaStream_t s);
 cudaError_t launch_count_proc(const SimArgs &a, unsigned long long *out, uint32_t *tc, cudaStream_t s);
 cudaError_t launch_settle_weights(const SimArgs &a, uint64_t t_now, uint32_t row_lo, uint32_t row_hi, float *out,
                                   cudaStream_t s);

@@ -162,3 +162,34 @@ def test_read_spikes_into_matches_oracle(S):
             net.step(1)
             k = net.read_spikes_into(t, t + 1, ids, offs)
             assert np.array_equal(ids[:k], want[t]), t
+
+
+def test_prefetch_collect_beyond_the_guess(S):
+    """Device-compacted read-out (chunks of >= 2^16 bitmap words): a chunk with far more
+    spikes than the slot's previous chunk (forced bursts) makes collect fetch the IDs past the
+    speculative copy; ETRUNC keeps the slot for a larger buffer."""
+    cfg, K = W.synth(200_000, 31, 0.002, seed=4), 12
+    rng = np.random.default_rng(5)
+    o = O.OracleNet(cfg)
+    ids = np.zeros(cfg.n * K, dtype=np.uint32)
+    offs = np.zeros(K + 1, dtype=np.uint64)
+    with S.Network(cfg, record_steps=32, tile_width=1024) as net:
+        for c in range(4):
+            for q in range(K):
+                if c == 2 and q % 2 == 0:
+                    f = np.sort(rng.choice(cfg.n, 150_000, replace=False)).astype(np.uint32)
+                    o.force_next(f, "add")
+                    net.force_next(f, "add")
+                o.step(1)
+                net.step(1)
+            net.spikes_prefetch(c * K, (c + 1) * K, c & 1)
+            if c == 2:
+                small = np.zeros(10, dtype=np.uint32)
+                with pytest.raises(S.SpiceError):
+                    net.spikes_collect_into(c & 1, small, offs)
+            n = net.spikes_collect_into(c & 1, ids, offs)
+            want = o.spikes()[c * K:(c + 1) * K]
+            assert n == sum(len(w) for w in want)
+            for q in range(K):
+                assert np.array_equal(ids[int(offs[q]):int(offs[q + 1])], want[q]), (c, q)
+        assert max(len(x) for x in o.spikes()) >= 150_000
