@@ -177,3 +177,37 @@ def test_external_exchange_over_host_buffers(S):
     finally:
         for n in nets:
             n.free()
+
+
+def test_compacted_readout_over_ranks(S):
+    """Device read-out compaction at G = 2 (global IDs interleaved across the ranks' slices,
+    ascending): spice_spikes_prefetch / _collect equal the host decode of spice_read_spikes and
+    the G = 1 oracle's spike trains."""
+    cfg, T, K, G = W.synth(200_000, 31, 0.004, seed=9), 24, 12, 2
+    o = O.OracleNet(cfg)
+    o.step(T)
+    want = o.spikes()
+    nets = [S.Network(cfg, rank=g, world_size=G, slice_width=64, external_exchange=True, record_steps=T)
+            for g in range(G)]
+    try:
+        for _ in range(T):
+            for n in nets:
+                n.exchange_begin()
+            for d in nets:
+                for s in nets:
+                    d.exchange_put_from(s)
+            for n in nets:
+                n.exchange_end()
+        ids = np.zeros(cfg.n * K, dtype=np.uint32)
+        offs = np.zeros(K + 1, dtype=np.uint64)
+        for n in nets:
+            assert K * G * n.words_per_rank >= 1 << 16           # the compacted path
+            for c in range(T // K):
+                n.spikes_prefetch(c * K, (c + 1) * K, c & 1)
+                n.spikes_collect_into(c & 1, ids, offs)
+                for q in range(K):
+                    assert np.array_equal(ids[int(offs[q]):int(offs[q + 1])], want[c * K + q]), (c, q)
+            assert all(np.array_equal(a, b) for a, b in zip(n.read_spikes(0, T), want))
+    finally:
+        for n in nets:
+            n.free()
