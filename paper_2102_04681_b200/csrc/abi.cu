@@ -175,8 +175,8 @@ struct spice_net {
         uint64_t words = 0, t_begin = 0, t_end = 0;
         uint32_t *d_ids = nullptr, *d_cnt = nullptr, *h_cnt = nullptr;   // device IDs / counts, pinned counts
         uint64_t dcap = 0, ccap = 0, copied = 0, guess = 0;
-        bool full = false, compact = false;
-        cudaEvent_t done = nullptr;
+        bool full = false, compact = false, guarded = false;
+        cudaEvent_t done = nullptr, ready = nullptr;
     } slot[2];
     cudaStream_t xfer = nullptr;        // read-out: copies that must not queue behind later steps
     std::vector<std::vector<uint32_t>> hdec;   // decoded per-step lists (reused)
@@ -422,6 +422,7 @@ spice_status capture_graph(spice_net *n, uint32_t steps, cudaGraphExec_t *out) {
 void destroy(spice_net *n) {
     if (!n) return;
     if (n->stream) cudaStreamSynchronize(n->stream);
+    if (n->xfer) cudaStreamSynchronize(n->xfer);
     for (cudaGraphExec_t &g : n->graphs) if (g) cudaGraphExecDestroy(g);
     for (void *p : n->opened) cudaIpcCloseMemHandle(p);
     if (n->win) cudaFree(n->win);
@@ -434,6 +435,7 @@ void destroy(spice_net *n) {
         if (sl.h) cudaFreeHost(sl.h);
         if (sl.h_cnt) cudaFreeHost(sl.h_cnt);
         if (sl.done) cudaEventDestroy(sl.done);
+        if (sl.ready) cudaEventDestroy(sl.ready);
     }
     if (n->xfer) cudaStreamDestroy(n->xfer);
     if (n->stream && n->own_stream) cudaStreamDestroy(n->stream);
@@ -984,10 +986,22 @@ spice_status spice_setup_times(spice_net *n, double *gen_ms, double *create_ms) 
     return SPICE_OK;
 }
 
+// A compacted read-out still pending on the read-out stream holds ring slots
+// [t_begin, t_end) until done: steps from t_begin + R on (which overwrite them) wait for it.
+spice_status guard_readout(spice_net *n, uint64_t steps) {
+    for (auto &sl : n->slot)
+        if (sl.full && sl.compact && !sl.guarded && n->t_host + steps > sl.t_begin + n->R) {
+            CU(n, cudaStreamWaitEvent(n->stream, sl.done, 0));
+            sl.guarded = true;
+        }
+    return SPICE_OK;
+}
+
 spice_status spice_step(spice_net *n, uint64_t steps) {
     CHECK_NET(n);
     if (n->external) return fail(n, SPICE_ESTATE, "external-exchange networks step via spice_exchange_begin/end");
     if (!n->connected) return fail(n, SPICE_ESTATE, "PEER exchange: call spice_peer_connect first");
+    if (spice_status st = guard_readout(n, steps)) return st;
     while (steps) {                                        // largest graph first
         uint32_t k = spice_net::kGraphLevels - 1;
         while ((1ull << k) > steps) --k;
@@ -1065,6 +1079,7 @@ spice_status spice_peer_connect(spice_net *n, const void *handles) {
 spice_status spice_exchange_begin(spice_net *n) {
     CHECK_NET(n);
     if (!n->external) return fail(n, SPICE_ESTATE, "not an external-exchange network");
+    if (spice_status st = guard_readout(n, 2)) return st;
     CU(n, launch_update(n->args, 0, n->stream));
     CU(n, cudaEventRecord(n->ev, n->stream));
     return SPICE_OK;
@@ -1114,6 +1129,7 @@ spice_status spice_exchange_set_recv(spice_net *n, uint32_t rank, const uint32_t
 spice_status spice_exchange_end(spice_net *n) {
     CHECK_NET(n);
     if (!n->external) return fail(n, SPICE_ESTATE, "not an external-exchange network");
+    if (spice_status st = guard_readout(n, 2)) return st;
     if (n->G > 1) CU(n, launch_bitmap_to_list(n->args, 0, n->stream));
     CU(n, launch_deliver(n->args, 0, n->global_atomics, n->n_sm, n->stream));
     CU(n, launch_advance(n->t0, 1, n->stream));
@@ -1125,6 +1141,7 @@ spice_status spice_exchange_end(spice_net *n) {
 spice_status spice_exchange_end_fused(spice_net *n) {
     CHECK_NET(n);
     if (!n->external) return fail(n, SPICE_ESTATE, "not an external-exchange network");
+    if (spice_status st = guard_readout(n, 2)) return st;
     if (!n->fused || n->global_atomics || n->G == 1) return fail(n, SPICE_ESTATE, "no fused G > 1 path on this network");
     CU(n, launch_bitmap_to_list(n->args, 0, n->stream));
     CU(n, launch_fused(n->args, 0, n->stream));        // deliver(t) + update(t+1): next bitmap
@@ -1241,13 +1258,20 @@ spice_status spice_spikes_prefetch(spice_net *n, uint64_t t_begin, uint64_t t_en
         CU(n, cudaMallocHost(reinterpret_cast<void **>(&sl.h), guess * 4));
         sl.words = guess;
     }
-    // steps enqueued before this call are recorded by the time the kernels run (stream order)
+    // on the read-out stream, after the steps enqueued so far (an event), concurrently with
+    // the steps enqueued later; a step that would overwrite these ring slots (t_begin + R
+    // onwards) waits for it (guard_readout)
+    if (!n->xfer) CU(n, cudaStreamCreateWithFlags(&n->xfer, cudaStreamNonBlocking));
+    if (!sl.ready) CU(n, cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+    CU(n, cudaEventRecord(sl.ready, n->stream));
+    CU(n, cudaStreamWaitEvent(n->xfer, sl.ready, 0));
     CU(n, launch_compact(n->record, n->R, words, t_begin, (uint32_t)nsteps, n->G, n->W, n->S, n->N, sl.d_cnt,
-                         sl.d_ids, n->stream));
-    CU(n, cudaMemcpyAsync(sl.h_cnt, sl.d_cnt, nsteps * 4, cudaMemcpyDeviceToHost, n->stream));
-    CU(n, cudaMemcpyAsync(sl.h, sl.d_ids, guess * 4, cudaMemcpyDeviceToHost, n->stream));
-    CU(n, cudaEventRecord(sl.done, n->stream));
+                         sl.d_ids, n->xfer));
+    CU(n, cudaMemcpyAsync(sl.h_cnt, sl.d_cnt, nsteps * 4, cudaMemcpyDeviceToHost, n->xfer));
+    CU(n, cudaMemcpyAsync(sl.h, sl.d_ids, guess * 4, cudaMemcpyDeviceToHost, n->xfer));
+    CU(n, cudaEventRecord(sl.done, n->xfer));
     sl.copied = guess;
+    sl.guarded = false;
     sl.full = true;
     return SPICE_OK;
 }
