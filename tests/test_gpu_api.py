@@ -193,3 +193,25 @@ def test_prefetch_collect_beyond_the_guess(S):
             for q in range(K):
                 assert np.array_equal(ids[int(offs[q]):int(offs[q + 1])], want[q]), (c, q)
         assert max(len(x) for x in o.spikes()) >= 150_000
+
+
+def test_compacted_readout_guards_its_ring_slots(S):
+    """The compacted read-out runs on its own stream; with a ring barely larger than a chunk
+    the next chunk's steps overwrite its slots and must wait for it (spice_step's guard)."""
+    cfg, T, K = W.synth(200_000, 31, 0.002, seed=6), 48, 12
+    o = O.OracleNet(cfg)
+    o.step(T)
+    want = o.spikes()
+    ids = np.zeros(cfg.n * K, dtype=np.uint32)
+    offs = np.zeros(K + 1, dtype=np.uint64)
+    got = []
+    with S.Network(cfg, record_steps=16, tile_width=4096) as net:
+        for c in range(T // K):
+            net.step(K)
+            net.spikes_prefetch(c * K, (c + 1) * K, c & 1)
+            if c:
+                net.spikes_collect_into((c - 1) & 1, ids, offs)
+                got += [ids[int(offs[q]):int(offs[q + 1])].copy() for q in range(K)]
+        net.spikes_collect_into((T // K - 1) & 1, ids, offs)
+        got += [ids[int(offs[q]):int(offs[q + 1])].copy() for q in range(K)]
+    assert all(np.array_equal(g, w) for g, w in zip(got, want))
