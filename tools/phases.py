@@ -48,3 +48,6 @@ for s, nm in NAMES.items():
 st, en = gl[:, 14].astype(np.int64), gl[:, 15].astype(np.int64)
 print(f"  last launch: CTA start spread {(st.max() - st.min()) / 1e3:.2f} us, end spread {(en.max() - en.min()) / 1e3:.2f} us, "
       f"first start -> last end {(en.max() - st.min()) / 1e3:.2f} us")
+if os.environ.get("PHASES_DUMP"):
+    np.savez(os.environ["PHASES_DUMP"], p=p, gl=gl.astype(np.int64), mhz=mhz)
+    print("  per-CTA phase clocks saved to", os.environ["PHASES_DUMP"])
