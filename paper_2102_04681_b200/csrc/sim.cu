@@ -595,20 +595,23 @@ __device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v,
 // ------------------------------------------------------- synth step, G = 1 (fast path)
 // The synth drive is input-independent (reading R12: neuron j fires at step t iff
 // Philox(j>>2, t, 0, 5)[j&3] < floor(a 2^32)), so the fused kernel of step t computes
-// the spikes of step t + 1 in its prologue -- while the previous step's grid drains
-// (programmatic dependent launch) -- and stages them as a slice bitmap and spike list in
-// shared memory; right after the grid dependency it L2-prefetches nothing and writes the
-// step's descriptors (production, one pass), then delivers step t, and the update of step
+// the spikes of step t + 1 on kFireWarps warps WHILE the other warps deliver step t (the
+// draws are ALU work, the delivery is memory-bound), stages them as a slice bitmap and
+// spike list in shared memory and starts the copies of their rows' segment bounds; at the
+// end it publishes them (record bitmap, spike list, descriptors) and the update of step
 // t + 1 reduces to the accumulator: acc += this step's input.  Every output (record
 // bitmap, spike lists, descriptors, counters) is the one the general update writes.
+// (Measured: in the prologue, before the grid dependency, the draws were on the step's
+// critical path -- the CTA whose SM frees last pays them: 3.7 us of a 24.7 us step.)
 __device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32_t b, uint32_t lo, uint32_t width,
-                                           uint32_t *sfire, uint32_t *sid_s, uint32_t *s_count, uint32_t sid_cap) {
-    const uint32_t tid = threadIdx.x, lane = tid & 31;
+                                           uint32_t *sfire, uint32_t *sid_s, uint32_t *s_count, uint32_t sid_cap,
+                                           uint32_t tid = threadIdx.x, uint32_t nth = kBlock) {
+    const uint32_t lane = tid & 31;
     const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;
     const uint32_t par = (uint32_t)(t1 & 1);
     uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
     const int forced = a.force_ctl[0] == t1 ? (int)a.force_ctl[1] : 0;
-    for (uint32_t x0 = 0; x0 < span; x0 += 4u * kBlock) {
+    for (uint32_t x0 = 0; x0 < span; x0 += 4u * nth) {
         if (x0 + 4u * (tid & ~31u) >= span) continue;            // whole warp past the slice
         const uint32_t x4 = x0 + 4u * tid;
         uint32_t nib = 0;
@@ -796,6 +799,10 @@ __device__ __forceinline__ uint64_t synth_descriptors(const SimArgs &a, uint64_t
 // counts, descriptors of its spiking rows) -- after delivery, when the memory system is
 // quiet, and off the accumulators' critical path.
 constexpr uint32_t kAccWarps = 24;
+#ifndef SPICE_FIRE_WARPS
+#define SPICE_FIRE_WARPS 8
+#endif
+constexpr uint32_t kFireWarps = SPICE_FIRE_WARPS;   // synth: warps computing the next step's spikes during delivery
 __device__ __forceinline__ void synth_publish_and_accumulate(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo,
                                                              const uint32_t *cnt, uint32_t cl_c, const uint32_t *s_fire,
                                                              const uint32_t *sid_s, uint32_t n, uint32_t *stage,
@@ -1671,7 +1678,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)      // TW is a multiple of 32
             *reinterpret_cast<uint4 *>(sm.cnt + x) = make_uint4(0u, 0u, 0u, 0u);
         const uint32_t lo = b * a.TWs;
-        // synth, G = 1: the spikes of step t + 1 before the grid dependency (see synth_fire)
+        // synth, G = 1: the spikes of step t + 1, computed during the delivery of t (synth_fire)
         constexpr uint32_t kFireWords = 1536;
         __shared__ uint32_t s_fire[MODEL == 4 ? kFireWords : 1];
         const bool syn = MODEL == 4 && a.G == 1 && a.TWs <= 32u * kFireWords && a.prod_words > kSynthSid;
@@ -1680,20 +1687,34 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         // delay >= 2, one CTA per tile: the update of t + 1 runs on the last kUpdWarps warps
         // while the others deliver t (its input slot t + 1 is complete; P:290 timestep grouping)
         const bool ovl = !syn && a.delay >= 2 && a.C == 1;
-        if (syn) {                                           // (shared memory and async copies only)
-            synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid);
-            __syncthreads();
-            if ((threadIdx.x >> 5) >= kAccWarps)
-                synth_rows_prefetch(a, t + 1, s_count, sid_s, sm.prod + kSynthSid, a.prod_words - kSynthSid,
-                                    threadIdx.x - kAccWarps * 32, kBlock - kAccWarps * 32, &s_off);
-        }
+        phase_mark(a, 10);                                   // (diagnostics: counters zeroed)
         asm volatile("griddepcontrol.wait;" ::: "memory");          // the previous step is complete
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         // thread 0: the step's descriptor count
         const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t & 3u] : 0xFFFFFFFFu;
         __syncthreads();
         phase_mark(a, 1);
-        if (ovl) {
+        if (syn) {
+            // synth: the spikes of step t + 1 (input-independent Philox draws, ~2.7 us of ALU
+            // work per CTA) on the last kFireWarps warps while the others deliver t -- off the
+            // step's critical path (in the prologue, the CTA that starts last paid them)
+            constexpr uint32_t NWD = kBlock / 32 - kFireWarps;
+            const uint32_t n_sp = delivery_count(a, t, bt, c, pre_total);
+            const uint32_t warp = threadIdx.x >> 5;
+            if (warp < NWD) {
+                deliver_ring_core<(V & 1) != 0, (V & 2) != 0>(a, t, bt, c, sm.cnt, sm.stage, n_sp, warp, NWD);
+            } else {
+                const uint32_t ptid = threadIdx.x - NWD * 32, pth = kFireWarps * 32;
+                synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid, ptid, pth);
+                asm volatile("bar.sync 2, %0;" :: "r"(pth) : "memory");
+                phase_mark(a, 11, NWD * 32);                 // (diagnostics: spikes of t + 1)
+                synth_rows_prefetch(a, t + 1, s_count, sid_s, sm.prod + kSynthSid, a.prod_words - kSynthSid,
+                                    ptid, pth, &s_off);
+            }
+            phase_mark(a, 4);
+            __syncthreads();
+            phase_mark(a, 5);
+        } else if (ovl) {
             constexpr uint32_t NWD = kBlock / 32 - kUpdWarps;
             const uint32_t n_sp = delivery_count(a, t, bt, c, pre_total);
             const uint32_t warp = threadIdx.x >> 5;

@@ -24,7 +24,7 @@ from paper_2102_04681_b200 import spice as S  # noqa: E402
 
 NAMES = {1: "counters zeroed", 2: "region prefix", 3: "descriptors staged", 4: "warp0 delivered",
          5: "delivery barrier", 6: "cluster reduce", 7: "update loop", 8: "spike rows",
-         10: "(prod) rows loaded", 11: "(prod) reserved", 9: "descriptors written", 12: "end"}
+         10: "(pro) zeroed / rows", 11: "(pro) fired / reserved", 9: "descriptors written", 12: "end"}
 which = sys.argv[1] if len(sys.argv) > 1 else "synth"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
 ctas = int(sys.argv[3]) if len(sys.argv) > 3 else 0
