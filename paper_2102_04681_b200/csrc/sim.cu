@@ -794,58 +794,47 @@ __device__ __forceinline__ uint64_t synth_descriptors(const SimArgs &a, uint64_t
     return dsum;
 }
 
-// The end of a synth fast-path step: warps [0, kAccWarps) add the step's input to the
-// accumulators while the other warps publish step t + 1 (record bitmap, spike list and
-// counts, descriptors of its spiking rows) -- after delivery, when the memory system is
-// quiet, and off the accumulators' critical path.
-constexpr uint32_t kAccWarps = 24;
 #ifndef SPICE_FIRE_WARPS
 #define SPICE_FIRE_WARPS 8
 #endif
-constexpr uint32_t kFireWarps = SPICE_FIRE_WARPS;   // synth: warps computing the next step's spikes during delivery
-__device__ __forceinline__ void synth_publish_and_accumulate(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo,
-                                                             const uint32_t *cnt, uint32_t cl_c, const uint32_t *s_fire,
-                                                             const uint32_t *sid_s, uint32_t n, uint32_t *stage,
-                                                             uint32_t stage_words, uint32_t s_off) {
-    const uint32_t warp = threadIdx.x >> 5;
-    if (warp < kAccWarps) {
-        synth_accumulate(a, t + 1, lo, a.TWs, cnt, cl_c, threadIdx.x, kAccWarps * 32);
-        phase_mark(a, 7);
-    } else {
-        const uint32_t ptid = threadIdx.x - kAccWarps * 32, pth = kBlock - kAccWarps * 32;
-        const uint64_t t1 = t + 1;
-        const uint32_t par1 = (uint32_t)(t1 & 1);
-        uint32_t *bm = a.record + modR(a, t1) * (uint64_t)a.W;
-        const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
-        uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
-        uint64_t *region_rows = a.sl_rows + ((uint64_t)par1 * a.NR + b) * a.RS;
-        for (uint32_t x = ptid; x < nwd; x += pth) bm[(lo >> 5) + x] = s_fire[x];
-        if (n <= kSynthSid) {
-            for (uint32_t q = ptid; q < n; q += pth) region[q] = sid_s[q];
-        } else {                                     // (more spikes than the shared list holds)
-            __shared__ uint32_t s_pos;
-            if (ptid == 0) s_pos = 0;
-            asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
-            for (uint32_t x = ptid; x < nwd; x += pth) {
-                uint32_t w = s_fire[x];
-                uint32_t p = w ? atomicAdd(&s_pos, __popc(w)) : 0u;
-                while (w) { region[p++] = lo + 32u * x + (uint32_t)(__ffs(w) - 1); w &= w - 1u; }
-            }
+constexpr uint32_t kFireWarps = SPICE_FIRE_WARPS;   // synth: warps drawing + publishing step t + 1 during delivery
+
+// Publication of step t + 1 by the fire warps (ptid < pth), right after they drew its
+// spikes -- still during the delivery of step t: record bitmap, spike list and count, and
+// the descriptors of its spiking rows (into descriptor buffer (t + 1) mod 3, which no
+// kernel reads before the delivery of t + 1; the list slots were reserved by
+// synth_rows_prefetch).  The end of the step is then only the accumulator update.
+__device__ __forceinline__ void synth_publish(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo,
+                                             const uint32_t *s_fire, const uint32_t *sid_s, uint32_t n,
+                                             uint32_t *stage, uint32_t stage_words, uint32_t s_off,
+                                             uint32_t ptid, uint32_t pth) {
+    const uint64_t t1 = t + 1;
+    const uint32_t par1 = (uint32_t)(t1 & 1);
+    uint32_t *bm = a.record + modR(a, t1) * (uint64_t)a.W;
+    const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
+    uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
+    uint64_t *region_rows = a.sl_rows + ((uint64_t)par1 * a.NR + b) * a.RS;
+    for (uint32_t x = ptid; x < nwd; x += pth) bm[(lo >> 5) + x] = s_fire[x];
+    if (n > kSynthSid) {                             // (more spikes than the shared list holds:
+        __shared__ uint32_t s_pos;                   //  synth_fire listed only the first ones)
+        if (ptid == 0) s_pos = 0;
+        asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
+        for (uint32_t x = ptid; x < nwd; x += pth) {
+            uint32_t w = s_fire[x];
+            uint32_t p = w ? atomicAdd(&s_pos, __popc(w)) : 0u;
+            while (w) { region[p++] = lo + 32u * x + (uint32_t)(__ffs(w) - 1); w &= w - 1u; }
         }
-        if (ptid == 0) {
-            a.sl_counts[par1 * a.NR + b] = n;
-            if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
-        }
-        asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");   // (region complete)
-        phase_mark(a, 8, kAccWarps * 32);
-        const bool staged = n > 0 && n <= synth_stage(a, stage_words).CH && n <= kSynthSid;   // (synth_rows_prefetch)
-        const uint64_t dsum = staged ? synth_descriptors(a, t1, n, sid_s, region_rows, stage, stage_words, ptid, pth, s_off)
-                                     : write_descriptors<true>(a, t1, b, n, region, region_rows, stage, true, sid_s,
-                                                               ptid, pth, kSynthSid, stage_words);
-        if (ptid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
-        phase_mark(a, 9, kAccWarps * 32);
     }
-    __syncthreads();
+    if (ptid == 0) {
+        a.sl_counts[par1 * a.NR + b] = n;
+        if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
+    }
+    asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");   // (region complete)
+    const bool staged = n > 0 && n <= synth_stage(a, stage_words).CH && n <= kSynthSid;   // (synth_rows_prefetch)
+    const uint64_t dsum = staged ? synth_descriptors(a, t1, n, sid_s, region_rows, stage, stage_words, ptid, pth, s_off)
+                                 : write_descriptors<true>(a, t1, b, n, region, region_rows, stage, true, sid_s,
+                                                           ptid, pth, kSynthSid, stage_words);
+    if (ptid == 0 && dsum) atomicAdd(&a.delivered_cta[b], (unsigned long long)dsum);
 }
 
 struct Win { uint4 a, b; };                          // one delivery window (kWin entries; b: kWin = 16)
@@ -1706,10 +1695,14 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             } else {
                 const uint32_t ptid = threadIdx.x - NWD * 32, pth = kFireWarps * 32;
                 synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid, ptid, pth);
-                asm volatile("bar.sync 2, %0;" :: "r"(pth) : "memory");
+                asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
                 phase_mark(a, 11, NWD * 32);                 // (diagnostics: spikes of t + 1)
                 synth_rows_prefetch(a, t + 1, s_count, sid_s, sm.prod + kSynthSid, a.prod_words - kSynthSid,
                                     ptid, pth, &s_off);
+                asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");   // (s_off)
+                synth_publish(a, t, b, lo, s_fire, sid_s, s_count, sm.prod + kSynthSid, a.prod_words - kSynthSid,
+                              s_off, ptid, pth);
+                phase_mark(a, 9, NWD * 32);                  // (diagnostics: step t + 1 published)
             }
             phase_mark(a, 4);
             __syncthreads();
@@ -1736,8 +1729,11 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             // barrier; a second one at exit keeps every CTA's counters alive until then)
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
             phase_mark(a, 6);
-            if (syn) synth_publish_and_accumulate(a, t, b, lo, cnt, a.C > 1 ? c : kMaxCluster, s_fire, sid_s, s_count,
-                                                  sm.prod + kSynthSid, a.prod_words - kSynthSid, s_off);
+            if (syn) {
+                synth_accumulate(a, t + 1, lo, a.TWs, cnt, a.C > 1 ? c : kMaxCluster);
+                phase_mark(a, 7);
+                __syncthreads();
+            }
             else
                 update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, a.G == 1, &s_count, sm.stage, nullptr, true,
                                          a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
@@ -1757,8 +1753,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             }
             if (syn) {
                 __syncthreads();                             // (the slot's ring writes above)
-                synth_publish_and_accumulate(a, t, b, lo, nullptr, kMaxCluster, s_fire, sid_s, s_count,
-                                             sm.prod + kSynthSid, a.prod_words - kSynthSid, s_off);
+                synth_accumulate(a, t + 1, lo, a.TWs, nullptr, kMaxCluster);
+                __syncthreads();
             } else if (ovl) {
                 // (the update of t + 1 ran during the delivery)
             } else {
