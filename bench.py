@@ -330,7 +330,10 @@ def main_spice(args):
     peak, peak_src = hbm_peak()
     fused = prof["fused"] > 0
     small = net.launches(32) == 2                  # one-CTA persistent kernel (small networks)
+    persistent = net.launches(32) == 4             # persistent synth kernel: one launch per replay
     kern = ("k_small (whole steps, one CTA, 32 per launch)" if small else
+            "k_synth_run (persistent: the steps of a replay in one launch, deliver t + publish t+1 "
+            "per step, grid barrier between steps; time per step)" if persistent else
             "k_fused (deliver t + update t+1)") if fused else ("k_global_atomics" if args.global_atomics else "k_deliver")
     # spice_step runs the fused kernel back to back inside captured graphs: the in-graph
     # timing is the kernel as the timed region ran it (the individually launched timing

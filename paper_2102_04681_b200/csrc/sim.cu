@@ -630,19 +630,32 @@ __device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32
             for (int e = 0; e < 4; ++e) valid |= (j0 + e < a.n_own ? 1u : 0u) << e;
             nib &= valid;
         }
-        uint32_t w = nib << (4u * (lane & 7u));
-        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 1);
-        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 2);
-        w |= __shfl_xor_sync(0xFFFFFFFFu, w, 4);
-        if ((lane & 7u) == 0 && x4 < span) sfire[x4 >> 5] = w;
-        const uint32_t nsp = __popc(nib);
-        const uint32_t incl = warp_incl_scan(nsp);
-        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        // bitmap words and list positions from four ballots (bit e of every lane's nibble):
+        // no shuffles -- the fire warps run beside the delivery, whose shared-memory atomics
+        // keep the MIO queue (shuffles, shared memory) busy
+        uint32_t m[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) m[e] = __ballot_sync(0xFFFFFFFFu, (nib >> e) & 1u);
+        if (lane < 4) {                              // word `lane` of the warp's 128 neurons:
+            uint32_t w = 0;                          // lanes 8 lane .. 8 lane + 7, bit 4 L' + e
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                uint32_t x = (m[e] >> (8u * lane)) & 0xFFu;                 // spread 8 bits to 4i
+                x = (x | (x << 12)) & 0x000F000Fu;
+                x = (x | (x << 6)) & 0x03030303u;
+                x = (x | (x << 3)) & 0x11111111u;
+                w |= x << e;
+            }
+            const uint32_t xw = x0 + 4u * (tid & ~31u) + 32u * lane;
+            if (xw < span) sfire[xw >> 5] = w;
+        }
+        const uint32_t lt = (1u << lane) - 1u;
+        const uint32_t tot = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
         if (tot) {
             uint32_t base = 0;
             if (lane == 0) base = atomicAdd(s_count, tot);
             base = __shfl_sync(0xFFFFFFFFu, base, 0);
-            uint32_t pos = base + incl - nsp;
+            uint32_t pos = base + __popc(m[0] & lt) + __popc(m[1] & lt) + __popc(m[2] & lt) + __popc(m[3] & lt);
 #pragma unroll
             for (int e = 0; e < 4; ++e)
                 if ((nib >> e) & 1u) {
@@ -1767,6 +1780,101 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
     }
 }
 
+// ------------------------------------------------- synth, persistent (G = 1, delay 1)
+// In-kernel grid barrier (all CTAs co-resident: cooperative launch).  Barrier i of a launch
+// counts arrivals in slot i mod 4 (thread 0 of every CTA: fence + release add, then an
+// acquire spin until all gridDim.x arrived); CTA 0 clears slot (i + 2) mod 4 once past
+// barrier i (its last users passed barrier i - 2 before anyone could arrive at i - 1),
+// k_advance clears all four after the launch.  A barrier not complete within ~10 s (a CTA
+// that never got scheduled) sets gbar[4] and every CTA falls through the remaining
+// barriers: the host reports an error instead of hanging the GPU.
+__device__ __forceinline__ void grid_arrive(const SimArgs &a, uint32_t i) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(a.gbar + (i & 3u)) : "memory");
+    }
+}
+__device__ __forceinline__ void grid_wait(const SimArgs &a, uint32_t i) {
+    if (threadIdx.x == 0) {
+        const uint32_t *slot = a.gbar + (i & 3u);
+        unsigned long long t_start;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        for (uint32_t spin = 0;; ++spin) {
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(slot) : "memory");
+            if (v >= gridDim.x) break;
+            if ((spin & 255u) == 255u) {
+                if (*(volatile uint32_t *)(a.gbar + 4)) break;
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                if (now - t_start > 10000000000ull) { atomicExch(a.gbar + 4, 1u); break; }
+            }
+        }
+        __threadfence();
+        if (blockIdx.x == 0) a.gbar[(i + 2u) & 3u] = 0u;
+    }
+    __syncthreads();
+}
+
+// nsteps consecutive synth steps k .. k + nsteps - 1 in ONE launch (each: deliver t + the
+// update of t + 1).  The synth update of t + 1 is acc += input(t + 1) and the drive does not
+// depend on the input (reading R12), so the tile counters are not cleared between
+// steps: they keep the running sum of the launch's inputs in shared memory (u32, wrapping
+// exactly like acc) and are folded into acc once, at the end of the launch -- the per-step
+// counter clearing, cluster reduction and accumulator pass (~4.5 us of a 21.5 us step in
+// the one-kernel-per-step form) disappear, as does the kernel boundary.  Per step: the
+// delivery warps deliver t while the fire warps draw, list and publish the spikes of t + 1
+// (descriptor buffer (t + 1) mod 3), then a grid barrier.  Outputs per step (record bitmap,
+// spike lists, descriptors, fired / delivered counts) are those of k_fused; acc equals
+// k_fused's after the launch.
+template <int V>
+__global__ void __launch_bounds__(kBlock) k_synth_run(SimArgs a, uint32_t k, uint32_t nsteps) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    DeliverSmem sm = carve(a, smem);
+    __shared__ uint32_t s_count, s_off;
+    constexpr uint32_t kFireWords = 1536;
+    __shared__ uint32_t s_fire[kFireWords];
+    const uint32_t b = blockIdx.x, bt = b / a.C, c = b % a.C, lo = b * a.TWs;
+    uint32_t *sid_s = sm.prod;
+    constexpr uint32_t NWD = kBlock / 32 - kFireWarps;
+    const uint32_t warp = threadIdx.x >> 5;
+    for (uint32_t x = threadIdx.x * 4u; x < a.TW; x += kBlock * 4u)      // TW is a multiple of 32
+        *reinterpret_cast<uint4 *>(sm.cnt + x) = make_uint4(0u, 0u, 0u, 0u);
+    asm volatile("griddepcontrol.wait;" ::: "memory");          // the replay's first update is complete
+    for (uint32_t i = 0; i < nsteps; ++i) {
+        const uint64_t t = *a.t0 + k + i;
+        if (i) grid_wait(a, i - 1);
+        phase_mark(a, 0);
+        const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t & 3u] : 0xFFFFFFFFu;
+        if (threadIdx.x == 0) s_count = 0;
+        const uint32_t n_sp = delivery_count(a, t, bt, c, pre_total);   // (block-wide)
+        phase_mark(a, 1);
+        if (warp < NWD) {
+            deliver_ring_core<(V & 1) != 0, false>(a, t, bt, c, sm.cnt, sm.stage, n_sp, warp, NWD);
+        } else {
+            const uint32_t ptid = threadIdx.x - NWD * 32, pth = kFireWarps * 32;
+            synth_fire(a, t + 1, b, lo, a.TWs, s_fire, sid_s, &s_count, kSynthSid, ptid, pth);
+            asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
+            phase_mark(a, 11, NWD * 32);
+            synth_rows_prefetch(a, t + 1, s_count, sid_s, sm.prod + kSynthSid, a.prod_words - kSynthSid,
+                                ptid, pth, &s_off);
+            asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");   // (s_off)
+            synth_publish(a, t, b, lo, s_fire, sid_s, s_count, sm.prod + kSynthSid, a.prod_words - kSynthSid,
+                          s_off, ptid, pth);
+            phase_mark(a, 9, NWD * 32);
+        }
+        phase_mark(a, 4);
+        __syncthreads();
+        phase_mark(a, 12);
+        if (i + 1 < nsteps) grid_arrive(a, i);
+    }
+    // fold the launch's input sums into acc (C > 1: this CTA's slice of all C partial tiles)
+    if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    synth_accumulate(a, *a.t0 + k + nsteps, lo, a.TWs, sm.cnt + c * a.TWs, a.C > 1 ? c : kMaxCluster);
+    if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // Small networks (G = 1, delay 1, one tile of all owned neurons, fits shared memory): one
 // CTA runs nsteps whole steps per launch.  Neuron state and the input counters live in
 // shared memory for the launch; a step is update(t) (the shared update code: bitmap into
@@ -2068,7 +2176,10 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
     }
 }
 
-__global__ void k_advance(uint64_t *t0, uint32_t steps) { *t0 += steps; }
+__global__ void k_advance(uint64_t *t0, uint32_t steps, uint32_t *gbar) {
+    *t0 += steps;
+    if (gbar) { gbar[0] = 0u; gbar[1] = 0u; gbar[2] = 0u; gbar[3] = 0u; }   // (persistent launches)
+}
 
 // PEER exchange (device-initiated): after the kernel that
 // stored this rank's bitmap of step t into every rank's receive window, one thread
@@ -2235,6 +2346,72 @@ cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// The persistent synth kernel (k_synth_run): cooperative launch (every CTA co-resident,
+// which its grid barrier needs; the launch fails instead of deadlocking otherwise).
+static cudaLaunchConfig_t synth_run_config(const SimArgs &a, cudaStream_t s, cudaLaunchAttribute *at, bool coop) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.NT * a.C);
+    cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = tile_smem_bytes(a.TW, a.NR, a.prod_words);
+    cfg.stream = s;
+    uint32_t na = 0;
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+    ++na;
+    if (a.C > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = a.C;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (coop) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cfg;
+}
+
+bool synth_run_supported(const SimArgs &a, int n_sm) {
+    if (a.model != 4 || a.G != 1 || a.delay != 1 || a.dly || !a.desc || a.prod_words <= kSynthSid ||
+        a.TWs > 32u * 1536u || a.C > kMaxCluster)
+        return false;
+    auto kern = a.eshift ? k_synth_run<0> : k_synth_run<1>;
+    const size_t bytes = tile_smem_bytes(a.TW, a.NR, a.prod_words);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    uint64_t resident = 0;
+    if (a.C > 1) {
+        cudaLaunchAttribute at[3];
+        cudaLaunchConfig_t cfg = synth_run_config(a, nullptr, at, false);
+        cfg.attrs = at + 1;                               // (cluster dimension only)
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) { cudaGetLastError(); return false; }
+        resident = (uint64_t)ncl * a.C;
+    } else {
+        int per = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kBlock, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
+        resident = (uint64_t)per * n_sm;
+    }
+    return resident >= (uint64_t)a.NT * a.C;
+}
+
+cudaError_t launch_synth_run(const SimArgs &a, uint32_t k, uint32_t nsteps, cudaStream_t s) {
+    if (nsteps == 0) return cudaSuccess;
+    if (!a.gbar) return cudaErrorInvalidValue;
+    cudaLaunchAttribute at[3];
+    cudaLaunchConfig_t cfg = synth_run_config(a, s, at, true);
+    const cudaError_t e = a.eshift ? cudaLaunchKernelEx(&cfg, k_synth_run<0>, a, k, nsteps)
+                                   : cudaLaunchKernelEx(&cfg, k_synth_run<1>, a, k, nsteps);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s) {
     k_b2l<<<a.NR, kBlock, a.desc ? (size_t)kStageWords * 4 : 0, s>>>(a, k);
     return cudaGetLastError();
@@ -2323,8 +2500,8 @@ cudaError_t launch_compact(const uint32_t *record, uint32_t R, uint64_t words, u
     return cudaGetLastError();
 }
 
-cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s) {
-    k_advance<<<1, 1, 0, s>>>(t0, steps);
+cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s, uint32_t *gbar) {
+    k_advance<<<1, 1, 0, s>>>(t0, steps, gbar);
     return cudaGetLastError();
 }
 
