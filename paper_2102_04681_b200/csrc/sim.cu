@@ -880,10 +880,8 @@ __device__ __forceinline__ uint32_t delivery_count(const SimArgs &a, uint64_t t,
     __shared__ uint32_t s_total;
     if (threadIdx.x == 0) {
         s_total = pre_total != 0xFFFFFFFFu ? pre_total : a.dcount[t & 3u];
-        if (b == 0 && c == 0) {                     // next user: step t + 3's producers, which
-            a.dcount[(t + 3) & 3u] = 0u;            // run in the prologue of the kernel after next
-            __threadfence();
-        }
+        if (b == 0 && c == 0)                       // next user: step t + 3's producers (two
+            a.dcount[(t + 3) & 3u] = 0u;            // kernel boundaries / grid barriers later)
     }
     __syncthreads();
     return s_total;
@@ -1782,19 +1780,12 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
 
 // ------------------------------------------------- synth, persistent (G = 1, delay 1)
 // In-kernel grid barrier (all CTAs co-resident: cooperative launch).  Barrier i of a launch
-// counts arrivals in slot i mod 4 (thread 0 of every CTA: fence + release add, then an
-// acquire spin until all gridDim.x arrived); CTA 0 clears slot (i + 2) mod 4 once past
+// counts arrivals in slot i mod 4 (one thread of every CTA: a gpu-scope release add, then
+// an acquire spin until all gridDim.x arrived); CTA 0 clears slot (i + 2) mod 4 once past
 // barrier i (its last users passed barrier i - 2 before anyone could arrive at i - 1),
 // k_advance clears all four after the launch.  A barrier not complete within ~10 s (a CTA
 // that never got scheduled) sets gbar[4] and every CTA falls through the remaining
 // barriers: the host reports an error instead of hanging the GPU.
-__device__ __forceinline__ void grid_arrive(const SimArgs &a, uint32_t i) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(a.gbar + (i & 3u)) : "memory");
-    }
-}
 __device__ __forceinline__ void grid_wait(const SimArgs &a, uint32_t i) {
     if (threadIdx.x == 0) {
         const uint32_t *slot = a.gbar + (i & 3u);
@@ -1825,7 +1816,12 @@ __device__ __forceinline__ void grid_wait(const SimArgs &a, uint32_t i) {
 // counter clearing, cluster reduction and accumulator pass (~4.5 us of a 21.5 us step in
 // the one-kernel-per-step form) disappear, as does the kernel boundary.  Per step: the
 // delivery warps deliver t while the fire warps draw, list and publish the spikes of t + 1
-// (descriptor buffer (t + 1) mod 3), then a grid barrier.  Outputs per step (record bitmap,
+// (descriptor buffer (t + 1) mod 3) and then arrive at the step's grid barrier ("all CTAs
+// published t + 1"), which every CTA waits for before step t + 1: a CTA's delivery of t
+// overlaps the other CTAs' barrier traffic.  Why that is enough: the delivery of t + 1 reads
+// only the descriptors of t + 1 and the CTA's own counters; descriptor buffer (t + 2) mod 3,
+// written in step t + 1, was last read by the deliveries of t - 1, which every CTA finished
+// before it could publish t + 1.  Outputs per step (record bitmap,
 // spike lists, descriptors, fired / delivered counts) are those of k_fused; acc equals
 // k_fused's after the launch.
 template <int V>
@@ -1862,12 +1858,17 @@ __global__ void __launch_bounds__(kBlock) k_synth_run(SimArgs a, uint32_t k, uin
             asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");   // (s_off)
             synth_publish(a, t, b, lo, s_fire, sid_s, s_count, sm.prod + kSynthSid, a.prod_words - kSynthSid,
                           s_off, ptid, pth);
+            // barrier i = "every CTA has published step t + 1": the fire warps arrive right
+            // away; this CTA's delivery warps finish step t meanwhile (the next delivery needs
+            // only the descriptors of t + 1 and this CTA's own counters, never cleared here)
+            asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
+            if (ptid == 0 && i + 1 < nsteps)
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(a.gbar + (i & 3u)) : "memory");
             phase_mark(a, 9, NWD * 32);
         }
         phase_mark(a, 4);
         __syncthreads();
         phase_mark(a, 12);
-        if (i + 1 < nsteps) grid_arrive(a, i);
     }
     // fold the launch's input sums into acc (C > 1: this CTA's slice of all C partial tiles)
     if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
