@@ -332,8 +332,8 @@ def main_spice(args):
     small = net.launches(32) == 2                  # one-CTA persistent kernel (small networks)
     persistent = net.launches(32) == 4             # persistent synth kernel: one launch per replay
     kern = ("k_small (whole steps, one CTA, 32 per launch)" if small else
-            "k_synth_run (persistent: the steps of a replay in one launch, deliver t + publish t+1 "
-            "per step, grid barrier between steps; time per step)" if persistent else
+            "persistent step kernel (k_synth_run: the steps of a replay in one launch, "
+            "deliver t + update/publish t+1 per step, grid barrier between steps; time per step)" if persistent else
             "k_fused (deliver t + update t+1)") if fused else ("k_global_atomics" if args.global_atomics else "k_deliver")
     # spice_step runs the fused kernel back to back inside captured graphs: the in-graph
     # timing is the kernel as the timed region ran it (the individually launched timing

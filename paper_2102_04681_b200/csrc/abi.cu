@@ -153,7 +153,7 @@ struct spice_net {
     uint32_t **peers_dev = nullptr;
     std::vector<void *> opened;
     uint32_t *xerr = nullptr;
-    uint32_t *gbar = nullptr;           // persistent synth kernel: grid-barrier slots + timeout flag
+    uint32_t *gbar = nullptr;           // persistent step kernel: grid-barrier slots + timeout flag
     // geometry
     uint64_t n_own = 0, n_own_max = 0;
     uint32_t W = 0, TW = 32, NT = 1, C = 1, TWs = 32;
@@ -358,7 +358,7 @@ spice_status enqueue_steps(spice_net *n, uint32_t steps, cudaStream_t s) {
         CU(n, launch_small(a, 0, steps, s));
     } else if (n->G == 1 && n->fused && !n->global_atomics) {
         CU(n, launch_update(a, 0, s));
-        if (a.persist) CU(n, launch_synth_run(a, 0, steps - 1, s));          // one persistent launch
+        if (a.persist) CU(n, launch_run(a, 0, steps - 1, s));          // one persistent launch
         else for (uint32_t k = 0; k + 1 < steps; ++k) CU(n, launch_fused(a, k, s));   // deliver(k)+update(k+1)
         CU(n, launch_deliver(a, steps - 1, false, n->n_sm, s));
     } else {
@@ -932,10 +932,10 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     }
     memcpy(a.pl, pbx.box, sizeof a.pl);
     CU(n, prepare_kernels(a));
-    // synth (G = 1, delay 1): the steps of a graph replay in one persistent launch
+    // G = 1 synth with delay 1: the steps of a graph replay in one persistent launch
     // (SPICE_NO_PERSIST=1: one fused kernel per step, the A/B baseline)
     if (n->G == 1 && n->fused && !n->global_atomics && !n->small && !n->procedural && !getenv("SPICE_NO_PERSIST") &&
-        synth_run_supported(a, n->n_sm)) {
+        run_supported(a, n->n_sm)) {
         if ((st = dalloc_t(n, &n->gbar, 5, "grid barrier"))) return bail(st);
         CU(n, cudaMemset(n->gbar, 0, 20));
         a.gbar = n->gbar;
@@ -1750,7 +1750,7 @@ spice_status spice_profile(spice_net *n, uint64_t steps, double *ms, uint32_t ca
         cudaGraphExec_t ge = nullptr;
         CU(n, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         if (n->small) launch_small(a, 0, kProf, s);       // (per step: the chunk's time / kProf)
-        else if (a.persist) launch_synth_run(a, 0, kProf, s);   // (persistent: the launch's time / kProf)
+        else if (a.persist) launch_run(a, 0, kProf, s);   // (persistent: the launch's time / kProf)
         else for (uint32_t k = 0; k < kProf; ++k) launch_fused(a, k, s);
         launch_advance(n->t0, kProf, s, n->gbar);
         CU(n, cudaStreamEndCapture(s, &g));
@@ -1802,7 +1802,7 @@ uint64_t spice_launches(spice_net *n, uint64_t steps) {
         while ((1ull << k) > steps) --k;
         const uint64_t m = 1ull << k;
         if (n->small) total += 2;                          // k_small + k_advance per replay
-        else if (n->args.persist) total += m > 1 ? 4 : 3;  // update, persistent synth steps, deliver, advance
+        else if (n->args.persist) total += m > 1 ? 4 : 3;  // update, persistent steps, deliver, advance
         else {
             // + one k_advance per replay; the fused sequences open with an update (G = 1 and
             // G > 1) and close with a plain delivery

@@ -1202,7 +1202,7 @@ constexpr uint32_t kPlSeg = 1800;                     // segments staged per pas
 // flush-row list capacity (the stage's last 64 words are the overlapped update's scratch)
 constexpr uint32_t kPlFlush = kStageWords - 6 * kPlSeg - 2 - 64;
 #ifndef SPICE_PL_U
-#define SPICE_PL_U 2
+#define SPICE_PL_U 3
 #endif
 constexpr uint32_t kPlU = SPICE_PL_U;                 // events in flight per thread
 constexpr uint32_t kPlChunks = 4096;                  // chunk-start table: passes of <= 2^17 events
@@ -2347,9 +2347,9 @@ cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// The persistent synth kernel (k_synth_run): cooperative launch (every CTA co-resident,
-// which its grid barrier needs; the launch fails instead of deadlocking otherwise).
-static cudaLaunchConfig_t synth_run_config(const SimArgs &a, cudaStream_t s, cudaLaunchAttribute *at, bool coop) {
+// The persistent step kernel (k_synth_run): cooperative launch (every CTA
+// co-resident, which their grid barrier needs; the launch fails instead of deadlocking).
+static cudaLaunchConfig_t run_config(const SimArgs &a, cudaStream_t s, cudaLaunchAttribute *at, bool coop) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.NT * a.C);
     cfg.blockDim = dim3(kBlock);
@@ -2376,11 +2376,25 @@ static cudaLaunchConfig_t synth_run_config(const SimArgs &a, cudaStream_t s, cud
     return cfg;
 }
 
-bool synth_run_supported(const SimArgs &a, int n_sm) {
-    if (a.model != 4 || a.G != 1 || a.delay != 1 || a.dly || !a.desc || a.prod_words <= kSynthSid ||
-        a.TWs > 32u * 1536u || a.C > kMaxCluster)
-        return false;
-    auto kern = a.eshift ? k_synth_run<0> : k_synth_run<1>;
+// The persistent kernel of this configuration (nullptr: none): synth with delay 1, G = 1,
+// padded layout.
+typedef void (*RunKernel)(SimArgs, uint32_t, uint32_t);
+static RunKernel run_kernel(const SimArgs &a) {
+    if (a.G != 1 || !a.desc) return nullptr;
+    if (a.model == 4) {
+        if (a.delay != 1 || a.dly || a.prod_words <= kSynthSid || a.TWs > 32u * 1536u || a.C > kMaxCluster)
+            return nullptr;
+        return a.eshift ? k_synth_run<0> : k_synth_run<1>;
+    }
+    // (Vogels / Brunel with delay >= 2 in the same persistent form -- update warps publishing
+    //  t + 1 while the others deliver t -- measured 9.6-9.9 vs 9.4 us/step for Brunel 100K:
+    //  there the update of t + 1, not the kernel boundary, is the critical path; not kept)
+    return nullptr;
+}
+
+bool run_supported(const SimArgs &a, int n_sm) {
+    const RunKernel kern = run_kernel(a);
+    if (!kern) return false;
     const size_t bytes = tile_smem_bytes(a.TW, a.NR, a.prod_words);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
         cudaGetLastError();
@@ -2389,7 +2403,7 @@ bool synth_run_supported(const SimArgs &a, int n_sm) {
     uint64_t resident = 0;
     if (a.C > 1) {
         cudaLaunchAttribute at[3];
-        cudaLaunchConfig_t cfg = synth_run_config(a, nullptr, at, false);
+        cudaLaunchConfig_t cfg = run_config(a, nullptr, at, false);
         cfg.attrs = at + 1;                               // (cluster dimension only)
         cfg.numAttrs = 1;
         int ncl = 0;
@@ -2403,13 +2417,13 @@ bool synth_run_supported(const SimArgs &a, int n_sm) {
     return resident >= (uint64_t)a.NT * a.C;
 }
 
-cudaError_t launch_synth_run(const SimArgs &a, uint32_t k, uint32_t nsteps, cudaStream_t s) {
+cudaError_t launch_run(const SimArgs &a, uint32_t k, uint32_t nsteps, cudaStream_t s) {
     if (nsteps == 0) return cudaSuccess;
-    if (!a.gbar) return cudaErrorInvalidValue;
+    const RunKernel kern = run_kernel(a);
+    if (!a.gbar || !kern) return cudaErrorInvalidValue;
     cudaLaunchAttribute at[3];
-    cudaLaunchConfig_t cfg = synth_run_config(a, s, at, true);
-    const cudaError_t e = a.eshift ? cudaLaunchKernelEx(&cfg, k_synth_run<0>, a, k, nsteps)
-                                   : cudaLaunchKernelEx(&cfg, k_synth_run<1>, a, k, nsteps);
+    cudaLaunchConfig_t cfg = run_config(a, s, at, true);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, k, nsteps);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 

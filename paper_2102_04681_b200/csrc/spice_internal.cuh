@@ -111,7 +111,7 @@ struct SimArgs {
     uint32_t record_steps;
     uint64_t mD, mR;         // fast remainders mod D / record_steps: floor((2^64 - 1) / m) + 1
     uint32_t pdl;            // 1: fused step kernels use programmatic dependent launch
-    uint32_t persist;        // 1: synth steps of a replay in one persistent launch (k_synth_run)
+    uint32_t persist;        // 1: the steps of a replay in one persistent launch (k_synth_run)
     uint32_t *gbar;          // [5] its grid-barrier arrival slots (barrier i of a launch: slot
                              // i mod 4; zero between launches) and a timeout flag
     uint32_t pl_split;       // Brunel+: plastic fixed point q summed as (q mod 2^16) and

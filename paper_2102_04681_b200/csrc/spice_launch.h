@@ -18,11 +18,11 @@ cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s);
 cudaError_t launch_bitmap_to_list(const SimArgs &a, uint32_t k, cudaStream_t s);
 // *t0 += steps; gbar != nullptr: clear the persistent kernel's grid-barrier slots
 cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s, uint32_t *gbar = nullptr);
-// Persistent synth steps (G = 1, delay 1, no per-synapse delays): k .. k + nsteps - 1 in one
-// cooperative launch (a.gbar: grid-barrier slots); supported = configuration fits and the
-// whole grid can be co-resident.
-bool synth_run_supported(const SimArgs &a, int n_sm);
-cudaError_t launch_synth_run(const SimArgs &a, uint32_t k, uint32_t nsteps, cudaStream_t s);
+// Persistent steps (G = 1, synth with delay 1): k .. k + nsteps - 1 in one cooperative
+// launch (a.gbar: grid-barrier slots);
+// supported = the configuration has such a kernel and its whole grid can be co-resident.
+bool run_supported(const SimArgs &a, int n_sm);
+cudaError_t launch_run(const SimArgs &a, uint32_t k, uint32_t nsteps, cudaStream_t s);
 // Recorded bitmaps of nsteps steps -> counts[nsteps] and the packed ascending global IDs.
 cudaError_t launch_compact(const uint32_t *record, uint32_t R, uint64_t words, uint64_t t_begin, uint32_t nsteps,
                            uint32_t G, uint32_t W, uint32_t S, uint32_t N, uint32_t *counts, uint32_t *ids,
