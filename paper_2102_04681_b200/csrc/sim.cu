@@ -1211,6 +1211,10 @@ constexpr uint32_t kPlChunks = 4096;                  // chunk-start table: pass
 // run the update of step t + 1 meanwhile (it reads input slot t + 1, complete since delay >= 2,
 // and post state parity t + 1, already staged) and *upd_done is set.
 constexpr uint32_t kUpdWarps = 8;
+#ifndef SPICE_OVL_UPD_WARPS
+#define SPICE_OVL_UPD_WARPS 8
+#endif
+constexpr uint32_t kOvlUpdWarps = SPICE_OVL_UPD_WARPS;   // Vogels / Brunel delay >= 2: update warps beside the delivery
 template <int MODEL>
 __device__ __forceinline__ void update_tile_sub(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                                                 uint32_t *s_count, uint32_t *stage, uint32_t ptid, uint32_t pth);
@@ -1719,7 +1723,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             __syncthreads();
             phase_mark(a, 5);
         } else if (ovl) {
-            constexpr uint32_t NWD = kBlock / 32 - kUpdWarps;
+            constexpr uint32_t NWD = kBlock / 32 - kOvlUpdWarps;
             const uint32_t n_sp = delivery_count(a, t, bt, c, pre_total);
             const uint32_t warp = threadIdx.x >> 5;
             if (warp < NWD) {
@@ -1727,7 +1731,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             } else {
                 update_tile<MODEL, true, true>(a, t + 1, b, b * a.TWs, a.TWs, nullptr, a.G == 1, &s_count,
                                                sm.stage + NWD * kRing, nullptr, false, kMaxCluster, nullptr, nullptr,
-                                               threadIdx.x - NWD * 32, kUpdWarps * 32, kUpdWarps * kRing);
+                                               threadIdx.x - NWD * 32, kOvlUpdWarps * 32, kOvlUpdWarps * kRing);
             }
             __syncthreads();
         } else {
