@@ -105,7 +105,8 @@ def ncu_traffic(workload_name: str, delivery: str):
             e = json.load(f)[workload_name]
         if e["delivery"] != delivery:
             return None, None
-        return float(e["dram_bytes_read"] + e["dram_bytes_write"]), e["capture"]
+        # a persistent launch runs several steps: traffic per step, like `achieved`
+        return float(e["dram_bytes_read"] + e["dram_bytes_write"]) / float(e.get("steps_per_launch", 1)), e["capture"]
     except Exception:
         return None, None
 
