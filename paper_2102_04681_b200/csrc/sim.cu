@@ -2425,8 +2425,13 @@ cudaError_t launch_run(const SimArgs &a, uint32_t k, uint32_t nsteps, cudaStream
     if (nsteps == 0) return cudaSuccess;
     const RunKernel kern = run_kernel(a);
     if (!a.gbar || !kern) return cudaErrorInvalidValue;
+    // cooperative: the launch fails unless every CTA can be co-resident (co-residency was also
+    // checked at creation).  SPICE_NO_COOP=1 drops the attribute for profilers that cannot
+    // replay cooperative cluster launches (ncu 2025.2 reports them as empty grids); the grid
+    // barrier's timeout flag still guards against a CTA that never gets an SM.
+    static const bool coop = getenv("SPICE_NO_COOP") == nullptr;
     cudaLaunchAttribute at[3];
-    cudaLaunchConfig_t cfg = run_config(a, s, at, true);
+    cudaLaunchConfig_t cfg = run_config(a, s, at, coop);
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, k, nsteps);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
