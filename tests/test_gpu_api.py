@@ -219,3 +219,33 @@ def test_compacted_readout_guards_its_ring_slots(S):
         net.spikes_collect_into((T // K - 1) & 1, ids, offs)
         got += [ids[int(offs[q]):int(offs[q + 1])].copy() for q in range(K)]
     assert all(np.array_equal(g, w) for g, w in zip(got, want))
+
+
+@pytest.mark.parametrize("kw", [dict(tile_width=4096), dict(tile_width=20480, ctas_per_tile=2)])
+def test_persistent_synth_kernel_matches_per_step_kernels_and_oracle(S, kw):
+    """The persistent synth kernel (k_synth_run: one launch per graph replay, in-kernel grid
+    barrier, tile counters folded into acc once per launch) against one fused kernel per step
+    (SPICE_NO_PERSIST=1, read when a network is created) and the oracle: spike lists, the
+    accumulators and the delivered/fired counts, over replays of 1 .. 256 steps."""
+    import os
+    cfg, T = W.synth(40000, 31, 0.005, seed=12), 300        # 256 + 32 + 8 + 4: every replay size
+    o = O.OracleNet(cfg)
+    o.step(T)
+    want = o.spikes()
+    out = {}
+    for persist in (True, False):
+        if not persist:
+            os.environ["SPICE_NO_PERSIST"] = "1"
+        try:
+            with S.Network(cfg, record_steps=T, **kw) as net:
+                assert (net.launches(32) == 4) == persist          # one persistent launch per replay
+                net.step(T)
+                out[persist] = (net.read_spikes(0, T), net.state(S.FIELD_ACC), net.stats())
+        finally:
+            os.environ.pop("SPICE_NO_PERSIST", None)
+    for persist, (spk, acc, st) in out.items():
+        bad = [t for t in range(T) if not np.array_equal(spk[t], want[t])]
+        assert not bad, f"persist={persist}: first mismatching step {bad[0]}"
+        assert np.array_equal(acc, o.state(O.F_ACC)), f"persist={persist}: accumulators"
+        assert st["fired"] == sum(len(s) for s in want)
+        assert st["delivered"] == int(o.delivered().sum())
