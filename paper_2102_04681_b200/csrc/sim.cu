@@ -371,12 +371,22 @@ __device__ __forceinline__ void post_state_update(const SimArgs &a, uint64_t t, 
 // SUB: run by the pth threads ptid = 0 .. pth - 1 of a warp group (named barrier 1) while
 // the CTA's other warps deliver the current step (delay >= 2: the update of t + 1 does not
 // depend on the delivery of t -- the timestep grouping of P:290 inside one kernel).
+// Brunel drive: the Poisson inversion table in shared memory (one instance per kernel)
+__device__ __forceinline__ uint64_t *ptab_smem() { __shared__ uint64_t s_ptab[kPtabSmem]; return s_ptab; }
+// ... staged by the whole CTA (a step kernel's prologue: the table is constant)
+__device__ __forceinline__ bool stage_ptab(const SimArgs &a) {
+    if (a.mc.ptab_len > kPtabSmem) return false;
+    for (uint32_t x = threadIdx.x; x < a.mc.ptab_len; x += kBlock) ptab_smem()[x] = a.mc.ptab[x];
+    return true;
+}
+
 template <int MODEL, bool DESC = false, bool SUB = false>
 __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                             const uint32_t *cnt, bool write_list, uint32_t *s_count, uint32_t *stage,
                             const StatePtrs *staged = nullptr, bool marks = false,
                             uint32_t cl_c = kMaxCluster, uint32_t *sid_s = nullptr, uint32_t *bm_s = nullptr,
-                            uint32_t ptid = threadIdx.x, uint32_t pth = kBlock, uint32_t stage_words = kStageWords) {
+                            uint32_t ptid = threadIdx.x, uint32_t pth = kBlock, uint32_t stage_words = kStageWords,
+                            bool ptab_staged = false) {
     auto sync = [&]() {
         if constexpr (SUB) asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
         else __syncthreads();
@@ -390,13 +400,14 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     uint32_t *bm = a.G == 1 ? a.record + modR(a, t) * (uint64_t)a.W : a.sendbuf;
     uint32_t *ring_slot = a.ring + modD(a, t) * a.ring_stride + lo;
     // Brunel drive: the Poisson inversion table in shared memory (the walk is a chain of
-    // dependent loads per neuron)
-    __shared__ uint64_t s_ptab[kPtabSmem];
+    // dependent loads per neuron); ptab_staged: the kernel's prologue copied it already
     const uint64_t *ptab = a.mc.ptab;
     if ((MODEL == 2 || MODEL == 3) && a.mc.ptab_len <= kPtabSmem) {
-        for (uint32_t x = tid; x < a.mc.ptab_len; x += pth) s_ptab[x] = a.mc.ptab[x];
-        ptab = s_ptab;
-        sync();
+        if (!ptab_staged) {
+            for (uint32_t x = tid; x < a.mc.ptab_len; x += pth) ptab_smem()[x] = a.mc.ptab[x];
+            sync();
+        }
+        ptab = ptab_smem();
     }
     const bool acc_done = false;
     const int forced = a.force_ctl[0] == t ? (int)a.force_ctl[1] : 0;   // once per CTA, not per neuron
@@ -1691,6 +1702,9 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
         // delay >= 2, one CTA per tile: the update of t + 1 runs on the last kUpdWarps warps
         // while the others deliver t (its input slot t + 1 is complete; P:290 timestep grouping)
         const bool ovl = !syn && a.delay >= 2 && a.C == 1;
+        // Brunel: the drive's inversion table is constant -- into shared memory before the
+        // grid dependency instead of at the start of the update (one round trip off its path)
+        const bool pstaged = MODEL == 2 && stage_ptab(a);
         phase_mark(a, 10);                                   // (diagnostics: counters zeroed)
         asm volatile("griddepcontrol.wait;" ::: "memory");          // the previous step is complete
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1731,7 +1745,7 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             } else {
                 update_tile<MODEL, true, true>(a, t + 1, b, b * a.TWs, a.TWs, nullptr, a.G == 1, &s_count,
                                                sm.stage + NWD * kRing, nullptr, false, kMaxCluster, nullptr, nullptr,
-                                               threadIdx.x - NWD * 32, kOvlUpdWarps * 32, kOvlUpdWarps * kRing);
+                                               threadIdx.x - NWD * 32, kOvlUpdWarps * 32, kOvlUpdWarps * kRing, pstaged);
             }
             __syncthreads();
         } else {
@@ -1751,7 +1765,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
             }
             else
                 update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, cnt, a.G == 1, &s_count, sm.stage, nullptr, true,
-                                         a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords);
+                                         a.C > 1 ? c : kMaxCluster, sm.stage + kStageWords, nullptr, threadIdx.x, kBlock,
+                                         kStageWords, pstaged);
             // (an arrive right after the update loop, waited at exit, measured 0.5 us slower)
             if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         } else {
@@ -1774,7 +1789,8 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
                 // (the update of t + 1 ran during the delivery)
             } else {
                 update_tile<MODEL, DESC>(a, t + 1, b, lo, a.TWs, nullptr, a.G == 1, &s_count, sm.stage, nullptr, true,
-                                         kMaxCluster, sm.stage + kStageWords);
+                                         kMaxCluster, sm.stage + kStageWords, nullptr, threadIdx.x, kBlock, kStageWords,
+                                         pstaged);
             }
             if (a.C > 1) cluster_wait();                     // partners done reading this CTA's counters
         }
