@@ -56,7 +56,8 @@ def parse_args():
                     help="separate update and delivery launches per step (the G > 1 kernel sequence, A/B)")
     ap.add_argument("--profile-steps", type=int, default=200)
     ap.add_argument("--e2e-steps", type=int, default=1024)
-    ap.add_argument("--e2e-chunk", type=int, default=32, help="steps per spice_step call in the e2e leg")
+    ap.add_argument("--e2e-chunk", type=int, default=128,
+                    help="steps per spice_step call in the e2e leg (every step's spikes are read back, chunk by chunk)")
     ap.add_argument("--no-parity", action="store_true", help="skip the in-run oracle check (synth)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="G > 1 spike exchange: device-initiated stores into peer windows (default) "
