@@ -49,6 +49,7 @@ def test_ncu_traffic_lookup():
     with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
         rec = json.load(f)["synth_3e9_synapses_per_gpu"]
     t, src = bench.ncu_traffic("synth_3e9_synapses_per_gpu", rec["delivery"])
-    assert t == rec["dram_bytes_read"] + rec["dram_bytes_write"] and src
+    # per step, like roofline.achieved: a persistent launch covers steps_per_launch steps
+    assert t == (rec["dram_bytes_read"] + rec["dram_bytes_write"]) / rec.get("steps_per_launch", 1) and src
     assert bench.ncu_traffic("synth_3e9_synapses_per_gpu", "another geometry") == (None, None)
     assert bench.ncu_traffic("no_such_workload", rec["delivery"]) == (None, None)
