@@ -767,7 +767,6 @@ __device__ __forceinline__ void synth_rows_prefetch(const SimArgs &a, uint64_t t
     const SynthStage ss = synth_stage(a, stage_words);
     if (n == 0 || n > ss.CH || n > kSynthSid) return;
     const uint32_t lane = ptid & 31, warp = ptid >> 5, nwp = pth / 32, rowlen = a.NT + 1u;
-    if (ptid == 0) *s_off = atomicAdd(&a.dcount[t1 & 3u], n);
     uint64_t *srow = reinterpret_cast<uint64_t *>(stage + ss.CH * ss.rs4);
     uint32_t *sdeg = reinterpret_cast<uint32_t *>(srow + ss.CH);
     const uint4 *bnd4 = reinterpret_cast<const uint4 *>(a.bnd);
@@ -783,6 +782,8 @@ __device__ __forceinline__ void synth_rows_prefetch(const SimArgs &a, uint64_t t
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
+    // the list reservation last: its round trip stalls only the reserving warp, after its copies
+    if (ptid == pth - 32) *s_off = atomicAdd(&a.dcount[t1 & 3u], n);
 }
 // ... and at the end of the step: wait for the copies, write the descriptors.  Returns the
 // spikes' delivered-event count (valid in producer warp 0).
@@ -795,6 +796,7 @@ __device__ __forceinline__ uint64_t synth_descriptors(const SimArgs &a, uint64_t
     uint32_t *sdeg = reinterpret_cast<uint32_t *>(srow + ss.CH);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
+    phase_mark(a, 6, threadIdx.x - ptid);            // (diagnostics: rows staged)
     uint64_t dsum = 0;
     if (warp == 0)
         for (uint32_t ql = lane; ql < n; ql += 32) { region_rows[ql] = srow[ql]; dsum += sdeg[ql]; }
@@ -813,6 +815,7 @@ __device__ __forceinline__ uint64_t synth_descriptors(const SimArgs &a, uint64_t
             }
         }
     }
+    phase_mark(a, 7, threadIdx.x - ptid);            // (diagnostics: descriptors issued)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xFFFFFFFFu, dsum, o);
     return dsum;
@@ -854,6 +857,7 @@ __device__ __forceinline__ void synth_publish(const SimArgs &a, uint64_t t, uint
         if (n) atomicAdd(&a.fired_cta[b], (unsigned long long)n);
     }
     asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");   // (region complete)
+    phase_mark(a, 5, threadIdx.x - ptid);            // (diagnostics: bitmap + list published)
     const bool staged = n > 0 && n <= synth_stage(a, stage_words).CH && n <= kSynthSid;   // (synth_rows_prefetch)
     const uint64_t dsum = staged ? synth_descriptors(a, t1, n, sid_s, region_rows, stage, stage_words, ptid, pth, s_off)
                                  : write_descriptors<true>(a, t1, b, n, region, region_rows, stage, true, sid_s,
@@ -1875,13 +1879,16 @@ __global__ void __launch_bounds__(kBlock) k_synth_run(SimArgs a, uint32_t k, uin
             phase_mark(a, 11, NWD * 32);
             synth_rows_prefetch(a, t + 1, s_count, sid_s, sm.prod + kSynthSid, a.prod_words - kSynthSid,
                                 ptid, pth, &s_off);
+            phase_mark(a, 2, NWD * 32);
             asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");   // (s_off)
+            phase_mark(a, 3, NWD * 32);
             synth_publish(a, t, b, lo, s_fire, sid_s, s_count, sm.prod + kSynthSid, a.prod_words - kSynthSid,
                           s_off, ptid, pth);
             // barrier i = "every CTA has published step t + 1": the fire warps arrive right
             // away; this CTA's delivery warps finish step t meanwhile (the next delivery needs
             // only the descriptors of t + 1 and this CTA's own counters, never cleared here)
             asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
+            phase_mark(a, 8, NWD * 32);
             if (ptid == 0 && i + 1 < nsteps)
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(a.gbar + (i & 3u)) : "memory");
             phase_mark(a, 9, NWD * 32);

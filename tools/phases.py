@@ -22,8 +22,8 @@ import numpy as np  # noqa: E402
 import bench  # noqa: E402
 from paper_2102_04681_b200 import spice as S  # noqa: E402
 
-NAMES = {1: "counters zeroed", 2: "region prefix", 3: "descriptors staged", 4: "warp0 delivered",
-         5: "delivery barrier", 6: "cluster reduce", 7: "update loop", 8: "spike rows",
+NAMES = {1: "counters zeroed", 2: "region prefix / rows issued", 3: "staged / s_off", 4: "warp0 delivered",
+         5: "barrier / list published", 6: "cluster reduce / rows landed", 7: "update loop / desc issued", 8: "spike rows / publ. bar",
          10: "(pro) zeroed / rows", 11: "(pro) fired / reserved", 9: "descriptors written", 12: "end"}
 which = sys.argv[1] if len(sys.argv) > 1 else "synth"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
