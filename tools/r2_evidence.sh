@@ -14,9 +14,10 @@ for w in brunel100k brunelplus50k vogels4000 synth250m; do
   timeout 400 python bench.py --workload $w --steps 5000 --warmup 100 > gpurun_out/bench_${TAG}_$w.json 2> gpurun_out/bench_${TAG}_$w.err
 done
 timeout 400 python bench.py --setup > gpurun_out/setup_$TAG.json 2> gpurun_out/setup_$TAG.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 64 --warmup 5 --profile-steps 4 --e2e-steps 64 --no-cpu-baseline --no-parity > /dev/null 2>&1
-# synth: the persistent kernel; launch 2 is the timed region's spice_step(32): 31 steps in one launch
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_synth_run" -s 1 -c 1 -o gpurun_out/prof_${TAG}_synth python bench.py --workload synth --steps 32 --warmup 5 --profile-steps 2 --e2e-steps 32 --no-cpu-baseline --no-parity > /dev/null 2>&1
+SPICE_NO_COOP=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 64 --warmup 5 --profile-steps 4 --e2e-steps 64 --no-cpu-baseline --no-parity > /dev/null 2>&1
+# synth: the persistent kernel (ncu cannot replay cooperative cluster launches: SPICE_NO_COOP=1);
+# launch 2 is the timed region's spice_step(32): 31 steps in one launch
+SPICE_NO_COOP=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_synth_run" -s 1 -c 1 -o gpurun_out/prof_${TAG}_synth python bench.py --workload synth --steps 32 --warmup 5 --profile-steps 2 --e2e-steps 32 --no-cpu-baseline --no-parity > /dev/null 2>&1
 for w in brunel100k brunelplus50k; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_fused" -s 40 -c 1 -o gpurun_out/prof_${TAG}_$w python bench.py --workload $w --steps 64 --warmup 5 --profile-steps 2 --e2e-steps 32 --no-cpu-baseline --no-parity > /dev/null 2>&1
 done
