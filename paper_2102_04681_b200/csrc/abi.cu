@@ -908,7 +908,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     a.key0 = (uint32_t)n->seed; a.key1 = (uint32_t)(n->seed >> 32);
     a.NR = n->NR; a.RS = n->RS;
     a.mc = n->mc;
-    a.row_ptr = n->row_ptr; a.bnd = n->bnd; a.ent = n->ent; a.deg = n->deg; a.eshift = n->eshift;
+    a.row_ptr = n->row_ptr; a.bnd = n->bnd; a.ent = n->ent; a.deg = n->deg; a.eshift = n->eshift; a.nnz = n->nnz;
     a.v = n->v; a.ge = n->ge; a.gi = n->gi; a.ref = n->ref; a.acc = n->acc; a.ring = n->ring;
     a.sl_ids = n->sl_ids; a.sl_rows = n->sl_rows; a.sl_counts = n->sl_counts; a.desc = n->desc;
     a.dstride = ((n->G == 1 ? n->n_own : (uint64_t)n->N) + 1) & ~1ull; a.dcount = n->dcount;

@@ -336,6 +336,7 @@ __device__ __forceinline__ uint64_t write_descriptors(const SimArgs &a, uint64_t
         if (ptid == 0 && q0 == 0) s_off = off_reg;
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         barrier();
+        SPICE_CHECK((uint64_t)s_off + n <= a.dstride);
         if (marks) phase_mark(a, 10, threadIdx.x - ptid);
         if (warp == 0)
             for (uint32_t ql = lane; ql < nq; ql += 32) { region_rows[q0 + ql] = srow[ql]; dsum += sdeg[ql]; }
@@ -568,6 +569,18 @@ __device__ __forceinline__ void update_tile_sub(const SimArgs &a, uint64_t t, ui
 // entries land in the dummy counters past the tile).  Padded entries are byte offsets
 // (tiles up to kMaxPadTile) or, WORD = true, counter indices (cluster tiles up to
 // kMaxPadTileWord).
+// (debug builds: every entry, padding sentinels included, addresses a counter of the tile
+//  or one of its dummies)
+template <bool WORD>
+__device__ __forceinline__ void check_window(const uint4 v, uint32_t tw) {
+#if SPICE_CHECKS
+    const uint32_t lim = WORD ? tw + kDummy : (tw + kDummy) * 4u;
+    const uint32_t w8[4] = {v.x, v.y, v.z, v.w};
+    for (int u = 0; u < 8; ++u) SPICE_CHECK(((w8[u >> 1] >> (16 * (u & 1))) & 0xFFFFu) < lim);
+#else
+    (void)v; (void)tw;
+#endif
+}
 template <bool WORD = false>
 __device__ __forceinline__ void accumulate_window(uint32_t cnt_s, const uint4 v, uint32_t q) {
     uint32_t a0, a1, a2, a3, a4, a5, a6, a7;
@@ -670,6 +683,7 @@ __device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32
 #pragma unroll
             for (int e = 0; e < 4; ++e)
                 if ((nib >> e) & 1u) {
+                    SPICE_CHECK(pos < a.RS);             // (the region holds the CTA's slice)
                     region[pos] = lo + x4 + e;
                     if (pos < sid_cap) sid_s[pos] = lo + x4 + e;
                     ++pos;
@@ -801,6 +815,7 @@ __device__ __forceinline__ uint64_t synth_descriptors(const SimArgs &a, uint64_t
     if (warp == 0)
         for (uint32_t ql = lane; ql < n; ql += 32) { region_rows[ql] = srow[ql]; dsum += sdeg[ql]; }
     const uint32_t dbuf = (uint32_t)mod32(t1, 3);
+    SPICE_CHECK((uint64_t)off + n <= a.dstride);
     for (uint32_t j0 = 0; j0 < n; j0 += 32) {
         const uint32_t ql = j0 + lane;
         if (ql < n) {
@@ -916,6 +931,7 @@ __device__ __forceinline__ void deliver_ring_core(const SimArgs &a, uint64_t t, 
     const uint32_t v0 = (uint32_t)((uint64_t)my * warp / NW), v1 = (uint32_t)((uint64_t)my * (warp + 1) / NW);
     const uint64_t *dlist = a.desc + ((uint64_t)mod32(t, 3) * a.NT + b) * a.dstride + c;   // visit v -> dlist[v * C]
     uint32_t *ring = ring_base + warp * kRing;
+    SPICE_CHECK((uint64_t)my * a.C <= a.dstride);     // (the step's list fits its buffer)
     auto dload = [&](uint32_t vb) -> uint64_t {
         const uint32_t v = vb + lane;
         return v < v1 ? dlist[(uint64_t)v * a.C] : 0ull;
@@ -954,6 +970,7 @@ __device__ __forceinline__ void deliver_ring_core(const SimArgs &a, uint64_t t, 
     auto load_win = [&](uint32_t e) -> Win {
         Win w;
         if (e == NONE) { w.a = make_uint4(0, 0, 0, 0); if constexpr (kWin == 16) w.b = w.a; return w; }
+        SPICE_CHECK((uint64_t)kWin * ((e & 0x7FFFFFFFu) + 1u) <= a.nnz);
         const uint16_t *p = a.ent + (uint64_t)kWin * (e & 0x7FFFFFFFu);
         w.a = ld_stream_v4(p);
         if constexpr (kWin == 16) w.b = ld_stream_v4(p + 8);
@@ -994,6 +1011,7 @@ __device__ __forceinline__ void deliver_ring_core(const SimArgs &a, uint64_t t, 
                     if constexpr (kWin == 16)
                         accumulate_window_dly<WORD>(a, cnt_s, v[r].b, make_uint2(dd[r].z, dd[r].w), q, tD, tile_base);
                 } else {
+                    check_window<WORD>(v[r].a, a.TW);
                     accumulate_window<WORD>(cnt_s, v[r].a, q);
                     if constexpr (kWin == 16) accumulate_window<WORD>(cnt_s, v[r].b, q);
                 }
@@ -1367,7 +1385,9 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
                     }
                     l[u] = lo;
                     e[u] = sst[lo] + (f - slen[lo]);
+                    SPICE_CHECK(e[u] < a.nnz);
                     off[u] = a.ent[e[u]];
+                    SPICE_CHECK(off[u] < a.TW);
                     wv[u] = (sfl[lo] & 2u) ? a.w[e[u]] : -1.0f;
                 }
             }

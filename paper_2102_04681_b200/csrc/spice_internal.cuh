@@ -47,6 +47,15 @@ constexpr uint32_t kMaxPadTile = 16320;   // padded layout, byte-offset entries:
 constexpr uint32_t kMaxPadTileWord = 65472;   // padded layout, word-offset entries: TW + kDummy fits a u16
 constexpr uint32_t kMaxCluster = 8;       // CTAs per tile cluster (portable cluster size)
 
+// Device-side bounds checks of the hot kernels' indices (debug builds only: -DSPICE_CHECKS=1,
+// tools/checked_run.py; compute-sanitizer is not available on the GPU pool).  A violated
+// check traps: the launch fails with an illegal-instruction error naming no data.
+#if SPICE_CHECKS
+#define SPICE_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define SPICE_CHECK(cond) do { } while (0)
+#endif
+
 // Philox4x32-10 (Salmon et al., SC'11).  Multipliers 0xD2511F53 / 0xCD9E8D57, Weyl
 // key increments 0x9E3779B9 / 0xBB67AE85; 10 rounds.
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
@@ -111,6 +120,7 @@ struct SimArgs {
     uint32_t record_steps;
     uint64_t mD, mR;         // fast remainders mod D / record_steps: floor((2^64 - 1) / m) + 1
     uint32_t pdl;            // 1: fused step kernels use programmatic dependent launch
+    uint64_t nnz;            // stored entries (incl. padding sentinels): bounds of ent / w / dly
     uint32_t persist;        // 1: the steps of a replay in one persistent launch (k_synth_run)
     uint32_t *gbar;          // [5] its grid-barrier arrival slots (barrier i of a launch: slot
                              // i mod 4; zero between launches) and a timeout flag
