@@ -20,4 +20,14 @@ if __name__ == "__main__":
     lib = B.build(out="/tmp/libspice_checks.so", defines=["SPICE_CHECKS=1"])
     env = dict(os.environ, SPICE_LIB=lib)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize.py")] + sys.argv[1:], env=env)
-    sys.exit(r.returncode)
+    rc = r.returncode
+    if not sys.argv[1:]:    # and the full-size workloads in the bench's launch configuration
+        for w in ("synth", "brunel100k", "brunelplus50k"):
+            b = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", w, "--steps", "300",
+                                "--warmup", "5", "--profile-steps", "2", "--e2e-steps", "128", "--no-cpu-baseline"],
+                               env=env, capture_output=True, text=True)
+            line = (b.stdout.strip().splitlines() or ["(none)"])[-1]
+            print(f"bench {w} with bounds checks: rc {b.returncode}, "
+                  f"parity {line.split('\"parity\": ')[1][:30] if '\"parity\": ' in line else '?'}", flush=True)
+            rc = rc or b.returncode
+    sys.exit(rc)
