@@ -770,9 +770,10 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     const uint64_t no = n->ring_stride;
     const uint64_t nctas = (uint64_t)n->NT * n->C;
     if ((st = dalloc_t(n, &n->ring, (size_t)n->D * n->ring_stride, "input ring"))) return bail(st);
-    if ((st = dalloc_t(n, &n->sl_ids, 2ull * n->NR * n->RS, "spike lists"))) return bail(st);
-    if ((st = dalloc_t(n, &n->sl_rows, 2ull * n->NR * n->RS, "spike list rows"))) return bail(st);
-    if ((st = dalloc_t(n, &n->sl_counts, 2ull * n->NR, "spike list counts"))) return bail(st);
+    // (three copies by step mod 3: sim.cu lslot)
+    if ((st = dalloc_t(n, &n->sl_ids, 3ull * n->NR * n->RS, "spike lists"))) return bail(st);
+    if ((st = dalloc_t(n, &n->sl_rows, 3ull * n->NR * n->RS, "spike list rows"))) return bail(st);
+    if ((st = dalloc_t(n, &n->sl_counts, 3ull * n->NR, "spike list counts"))) return bail(st);
 
     if ((st = dalloc_t(n, &n->record, (size_t)n->R * n->G * n->W, "spike record"))) return bail(st);
     if ((st = dalloc_t(n, &n->sendbuf, std::max<uint32_t>(n->W, 1), "send bitmap"))) return bail(st);
@@ -791,7 +792,7 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     if (n->model == SPICE_SYNTH && (st = dalloc_t(n, &n->acc, no, "acc"))) return bail(st);
     cudaStream_t s = n->stream;
     CU(n, cudaMemsetAsync(n->ring, 0, (size_t)n->D * n->ring_stride * 4, s));
-    CU(n, cudaMemsetAsync(n->sl_counts, 0, 2ull * n->NR * 4, s));
+    CU(n, cudaMemsetAsync(n->sl_counts, 0, 3ull * n->NR * 4, s));
     CU(n, cudaMemsetAsync(n->sendbuf, 0, std::max<uint32_t>(n->W, 1) * 4, s));   // words past the last tile stay 0
     CU(n, cudaMemsetAsync(n->gather, 0, (size_t)n->G * std::max<uint32_t>(n->W, 1) * 4, s));
     CU(n, cudaMemsetAsync(n->record, 0, (size_t)n->R * n->G * n->W * 4, s));
@@ -819,15 +820,15 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
             return bail(fail(n, SPICE_EINVAL, "Brunel+ supports up to 1.5M neurons"));
         if ((st = dalloc_t(n, &n->w, n->nnz + 8, "plastic weights"))) return bail(st);
         if ((st = dalloc_t(n, &n->pring, (size_t)n->D * n->ring_stride, "plastic input ring"))) return bail(st);
-        if ((st = dalloc_t(n, &n->pre_ts, 2ull * n->N, "pre spike steps"))) return bail(st);
-        if ((st = dalloc_t(n, &n->pre_c, 2ull * n->N, "pre traces"))) return bail(st);
+        if ((st = dalloc_t(n, &n->pre_ts, 3ull * n->N, "pre spike steps"))) return bail(st);   // (by step mod 3)
+        if ((st = dalloc_t(n, &n->pre_c, 3ull * n->N, "pre traces"))) return bail(st);
         if ((st = dalloc_t(n, &n->post, 2ull * 4 * no, "post spike history"))) return bail(st);
         if ((st = dalloc_t(n, &n->post_mask, 64ull * no, "post spike bit rings"))) return bail(st);
         if ((st = dalloc_t(n, &n->tab_p, 8192, "pre trace table"))) return bail(st);
         if ((st = dalloc_t(n, &n->tab_m, 8192, "post trace table"))) return bail(st);
         CU(n, cudaMemsetAsync(n->pring, 0, (size_t)n->D * n->ring_stride * 8, s));
-        CU(n, cudaMemsetAsync(n->pre_ts, 0xFF, 2ull * n->N * 4, s));          // no spike yet
-        CU(n, cudaMemsetAsync(n->pre_c, 0, 2ull * n->N * 4, s));
+        CU(n, cudaMemsetAsync(n->pre_ts, 0xFF, 3ull * n->N * 4, s));          // no spike yet
+        CU(n, cudaMemsetAsync(n->pre_c, 0, 3ull * n->N * 4, s));
         {
             std::vector<uint32_t> init(4 * no);
             for (uint64_t i = 0; i < no; ++i) { init[4 * i] = init[4 * i + 1] = init[4 * i + 2] = 0xFFFFFFFFu; init[4 * i + 3] = 0u; }
@@ -1515,7 +1516,7 @@ spice_status spice_read_state(spice_net *n, uint32_t field, void *out, uint64_t 
         return k < tab.size() ? c * tab[k] : 0.0f;
     };
     if (field == SPICE_FIELD_XTR) {           // pre traces of the owned neurons (global arrays)
-        const uint64_t par = n->t_host & 1;
+        const uint64_t par = n->t_host % 3;             // (pre state copies by step mod 3)
         std::vector<float> c(n->N);
         std::vector<uint32_t> ts(n->N);
         CU(n, cudaMemcpy(c.data(), n->pre_c + par * n->N, n->N * 4ull, cudaMemcpyDeviceToHost));

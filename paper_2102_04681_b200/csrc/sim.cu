@@ -67,6 +67,10 @@ __device__ __forceinline__ void block_exclusive_scan(uint32_t *arr, uint32_t n, 
 __device__ __forceinline__ uint64_t mod32(uint64_t t, uint32_t m) {
     return (t >> 32) ? t % m : (uint64_t)((uint32_t)t % m);
 }
+// Step-indexed buffers that CTAs of different steps may touch at once (spike lists, the
+// Brunel+ pre state): three copies by t mod 3, so that a CTA one step ahead (the persistent
+// kernels' split barrier) never writes the copy a slower CTA still reads
+__device__ __forceinline__ uint32_t lslot(uint64_t t) { return (uint32_t)mod32(t, 3); }
 // t mod m with the host-computed M = floor((2^64 - 1) / m) + 1: for 32-bit t the remainder
 // is the high word of (M t mod 2^64) m (exact for every 32-bit t and m; Lemire, Kaser and
 // Kurz 2019, "Faster remainder by direct computation") -- two multiplies instead of the
@@ -395,7 +399,7 @@ __device__ __forceinline__ void update_tile(const SimArgs &a, uint64_t t, uint32
     const StatePtrs sp = staged ? *staged : global_state(a);
     const uint32_t tid = ptid, lane = tid & 31;
     const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;   // bitmap coverage
-    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t par = lslot(t);
     uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
     uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + b) * a.RS;
     uint32_t *bm = a.G == 1 ? a.record + modR(a, t) * (uint64_t)a.W : a.sendbuf;
@@ -632,7 +636,7 @@ __device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32
                                            uint32_t tid = threadIdx.x, uint32_t nth = kBlock) {
     const uint32_t lane = tid & 31;
     const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;
-    const uint32_t par = (uint32_t)(t1 & 1);
+    const uint32_t par = lslot(t1);
     uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
     const int forced = a.force_ctl[0] == t1 ? (int)a.force_ctl[1] : 0;
     for (uint32_t x0 = 0; x0 < span; x0 += 4u * nth) {
@@ -851,7 +855,7 @@ __device__ __forceinline__ void synth_publish(const SimArgs &a, uint64_t t, uint
                                              uint32_t *stage, uint32_t stage_words, uint32_t s_off,
                                              uint32_t ptid, uint32_t pth) {
     const uint64_t t1 = t + 1;
-    const uint32_t par1 = (uint32_t)(t1 & 1);
+    const uint32_t par1 = lslot(t1);
     uint32_t *bm = a.record + modR(a, t1) * (uint64_t)a.W;
     const uint32_t nwd = (min(a.TWs, a.W * 32u > lo ? a.W * 32u - lo : 0u) + 31u) / 32u;
     uint32_t *region = a.sl_ids + ((uint64_t)par1 * a.NR + b) * a.RS;
@@ -1134,10 +1138,10 @@ __device__ __forceinline__ float potentiate_lazy(const SimArgs &a, const float *
 __device__ __forceinline__ void pre_state_pass(const SimArgs &a, uint64_t t, const float *tabp,
                                                uint32_t ptid = threadIdx.x, uint32_t pth = kBlock) {
     const uint32_t *gbm = a.record + modR(a, t) * (uint64_t)a.G * a.W;
-    const uint32_t *ots = a.pre_ts + (t & 1) * (uint64_t)a.N;
-    const float *oc = a.pre_c + (t & 1) * (uint64_t)a.N;
-    uint32_t *nts = a.pre_ts + ((t + 1) & 1) * (uint64_t)a.N;
-    float *nc = a.pre_c + ((t + 1) & 1) * (uint64_t)a.N;
+    const uint32_t *ots = a.pre_ts + lslot(t) * (uint64_t)a.N;
+    const float *oc = a.pre_c + lslot(t) * (uint64_t)a.N;
+    uint32_t *nts = a.pre_ts + lslot(t + 1) * (uint64_t)a.N;
+    float *nc = a.pre_c + lslot(t + 1) * (uint64_t)a.N;
     const uint32_t per = (a.N + gridDim.x - 1) / gridDim.x;
     const uint32_t j0 = blockIdx.x * per, j1 = min(a.N, j0 + per);
     for (uint32_t j = j0 + ptid; j < j1; j += pth) {
@@ -1255,12 +1259,12 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
                                                          const PlasticSmem &sm, bool marks = false,
                                                          uint32_t *upd_count = nullptr, bool *upd_done = nullptr) {
     const uint32_t tid = threadIdx.x;
-    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t par = lslot(t);
     uint32_t *pref = sm.pref, *tmp = sm.tmp, *stage = sm.stage;
     const uint32_t *bm = step_bitmap(a, t);
     const uint32_t *gbm = a.record + modR(a, t) * (uint64_t)a.G * a.W;
-    const uint32_t *pts = a.pre_ts + (t & 1) * (uint64_t)a.N;
-    const float *pc = a.pre_c + (t & 1) * (uint64_t)a.N;
+    const uint32_t *pts = a.pre_ts + lslot(t) * (uint64_t)a.N;
+    const float *pc = a.pre_c + lslot(t) * (uint64_t)a.N;
     const uint64_t tile_base = (uint64_t)b * a.TW;
     for (uint32_t r = tid; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
     // the tile's post neurons before step t's spikes (post state parity t) plus their spike at t
@@ -1436,8 +1440,8 @@ __global__ void __launch_bounds__(256) k_settle_weights(SimArgs a, uint64_t t_no
                                                         float *out) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t)gridDim.x * 8;
-    const uint32_t *pts = a.pre_ts + (t_now & 1) * (uint64_t)a.N;
-    const float *pc = a.pre_c + (t_now & 1) * (uint64_t)a.N;
+    const uint32_t *pts = a.pre_ts + lslot(t_now) * (uint64_t)a.N;
+    const float *pc = a.pre_c + lslot(t_now) * (uint64_t)a.N;
     const uint4 *post = reinterpret_cast<const uint4 *>(a.post) + (t_now & 1) * a.ring_stride;
     const uint64_t base0 = a.row_ptr[row_lo];
     for (uint64_t q = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); q < (uint64_t)(row_hi - row_lo) * a.NT; q += nwarps) {
@@ -2052,7 +2056,7 @@ __global__ void __launch_bounds__(kBlock) k_deliver_proc(SimArgs a, uint32_t k) 
     uint32_t *cnt = smem;                                   // [TW]
     uint32_t *pref = smem + ((a.TW + 3u) & ~3u), *tmp = pref + ((a.NR + 1 + 3) & ~3u);
     const uint64_t t = *a.t0 + k;
-    const uint32_t par = (uint32_t)(t & 1), b = blockIdx.x;
+    const uint32_t par = lslot(t), b = blockIdx.x;
     for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) cnt[x] = 0u;
     for (uint32_t r = threadIdx.x; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
     __syncthreads();
@@ -2139,7 +2143,7 @@ __global__ void __launch_bounds__(kBlock) k_global_atomics(SimArgs a, uint32_t k
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t *pref = smem, *tmp = smem + ((a.NR + 1 + 3) & ~3u);
     const uint64_t t = *a.t0 + k;
-    const uint32_t par = (uint32_t)(t & 1);
+    const uint32_t par = lslot(t);
     for (uint32_t r = threadIdx.x; r < a.NR; r += kBlock) pref[r] = a.sl_counts[par * a.NR + r];
     __syncthreads();
     block_exclusive_scan(pref, a.NR, tmp);
@@ -2180,8 +2184,9 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
     const uint32_t nw = a.G * a.W, r = blockIdx.x;
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
-    uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + r) * a.RS;
-    uint64_t *region_rows = a.sl_rows + ((uint64_t)par * a.NR + r) * a.RS;
+    const uint32_t ls = lslot(t);                         // (list copy; par: the PEER window parity)
+    uint32_t *region = a.sl_ids + ((uint64_t)ls * a.NR + r) * a.RS;
+    uint64_t *region_rows = a.sl_rows + ((uint64_t)ls * a.NR + r) * a.RS;
     const uint32_t bw = a.RS / 32;                      // bitmap words of this region
     for (uint32_t q0 = 0; q0 < bw; q0 += kBlock) {
         const uint32_t idx = r * bw + q0 + threadIdx.x;
@@ -2213,7 +2218,7 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
     }
     __syncthreads();
     const uint32_t n = s_count;
-    if (threadIdx.x == 0) a.sl_counts[par * a.NR + r] = n;
+    if (threadIdx.x == 0) a.sl_counts[ls * a.NR + r] = n;
     if (a.desc) {
         // padded layout (G > 1): the region's spikes -> transposed segment descriptors of
         // every local tile, as the G = 1 update writes them for its own spikes; the

@@ -149,8 +149,8 @@ struct SimArgs {
                              // `delay` is then the minimum delay (the shared-memory path);
                              // longer-delay events go to ring slot t + d with global atomics
     // spikes
-    uint32_t *sl_ids;        // 2 * NR * RS
-    uint64_t *sl_rows;       // 2 * NR * RS row starts of the listed spikes
+    uint32_t *sl_ids;        // 3 * NR * RS (copy t mod 3)
+    uint64_t *sl_rows;       // 3 * NR * RS row starts of the listed spikes
     uint32_t *sl_counts;     // 2 * NR
     // G = 1 (padded layout): per-step segment descriptors, written transposed by the
     // updating CTAs into one dense list per destination tile: desc[((t mod 3)*NT + b)*dstride + i]
@@ -174,8 +174,8 @@ struct SimArgs {
     float *w;
     long long *pring;        // D * ring_stride, rint(w 2^32) sums
     // event-driven STDP state (reading R13), double-buffered by step parity:
-    uint32_t *pre_ts;        // [2][N] step of every source's last spike (~0 = none)
-    float *pre_c;            // [2][N] its pre trace just after that spike, X(ts) + 1
+    uint32_t *pre_ts;        // [3][N] step of every source's last spike (~0 = none), copy t mod 3
+    float *pre_c;            // [3][N] its pre trace just after that spike, X(ts) + 1
     uint32_t *post;          // [2][ring_stride] uint4 per owned neuron: last three spike
                              // steps (most recent first) and cy = Y(ts) + 1 (float bits)
     uint32_t *post_mask;     // [ring_stride][64] post-spike bit ring (2048 steps)
