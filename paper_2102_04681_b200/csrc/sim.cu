@@ -70,7 +70,11 @@ __device__ __forceinline__ uint64_t mod32(uint64_t t, uint32_t m) {
 // Step-indexed buffers that CTAs of different steps may touch at once (spike lists, the
 // Brunel+ pre state): three copies by t mod 3, so that a CTA one step ahead (the persistent
 // kernels' split barrier) never writes the copy a slower CTA still reads
-__device__ __forceinline__ uint32_t lslot(uint64_t t) { return (uint32_t)mod32(t, 3); }
+__device__ __forceinline__ uint32_t lslot(uint64_t t) {   // t mod 3 (2^32 = 1 mod 3: fold the halves)
+    const uint64_t x = (t >> 32) + (t & 0xFFFFFFFFull);
+    const uint32_t y = (uint32_t)(x >> 32) + (uint32_t)x;      // (no wrap: x < 2^33)
+    return y % 3u;
+}
 // t mod m with the host-computed M = floor((2^64 - 1) / m) + 1: for 32-bit t the remainder
 // is the high word of (M t mod 2^64) m (exact for every 32-bit t and m; Lemire, Kaser and
 // Kurz 2019, "Faster remainder by direct computation") -- two multiplies instead of the
@@ -1255,9 +1259,12 @@ constexpr uint32_t kOvlUpdWarps = SPICE_OVL_UPD_WARPS;   // Vogels / Brunel dela
 template <int MODEL>
 __device__ __forceinline__ void update_tile_sub(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                                                 uint32_t *s_count, uint32_t *stage, uint32_t ptid, uint32_t pth);
+// arrive != kNone (persistent kernel): once the overlapped update of t + 1 and the pre state
+// for t + 1 are written, the update warps arrive at grid barrier `arrive` ("t + 1 published")
 __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b,
                                                          const PlasticSmem &sm, bool marks = false,
-                                                         uint32_t *upd_count = nullptr, bool *upd_done = nullptr) {
+                                                         uint32_t *upd_count = nullptr, bool *upd_done = nullptr,
+                                                         uint32_t arrive = 0xFFFFFFFFu) {
     const uint32_t tid = threadIdx.x;
     const uint32_t par = lslot(t);
     uint32_t *pref = sm.pref, *tmp = sm.tmp, *stage = sm.stage;
@@ -1366,6 +1373,11 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
                 // other parity and reads step t's spikes)
                 pre_state_pass(a, t, sm.tabp, tid - eth, kUpdWarps * 32);
                 *upd_done = true;
+                if (arrive != kNone) {
+                    asm volatile("bar.sync 1, %0;" :: "r"(kUpdWarps * 32) : "memory");
+                    if (tid == eth)
+                        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(a.gbar + (arrive & 3u)) : "memory");
+                }
                 if (marks) phase_mark(a, 8, eth);
                 continue;                         // (nseg <= kPlSeg: this was the only pass)
             }
@@ -1927,6 +1939,46 @@ __global__ void __launch_bounds__(kBlock) k_synth_run(SimArgs a, uint32_t k, uin
     if (a.C > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// ------------------------------------------------ Brunel+, persistent (G = 1)
+// The steps of a replay in one launch: per step the delivery of t (lazy STDP on the synapse
+// stream) with the update of t + 1 and the pre-state pass on 8 warps beside it (k_fused<3>);
+// the barrier is "every CTA has published t + 1" (its spikes, lists and pre state): the
+// update warps arrive as soon as they are done, the delivery of t finishes meanwhile.  The
+// next delivery reads the spike lists and pre state of t + 1 (copies (t + 1) mod 3) and this
+// CTA's own tile state; the copies a CTA one step ahead writes, (t + 2) mod 3, are not the
+// ones a slower CTA still reads (t mod 3).  A step whose segments need more than one staging
+// pass runs the update after the delivery (k_fused's order) and arrives at its end.
+__global__ void __launch_bounds__(kBlock) k_plastic_run(SimArgs a, uint32_t k, uint32_t nsteps) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    PlasticSmem sm = carve_plastic(a, smem);
+    __shared__ uint32_t s_count3;
+    __shared__ bool s_upd;
+    const uint32_t b = blockIdx.x;
+    load_trace_table(a, sm);                                // (constant: before the dependent-launch wait)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (uint32_t i = 0; i < nsteps; ++i) {
+        const uint64_t t = *a.t0 + k + i;
+        if (i) grid_wait(a, i - 1);
+        phase_mark(a, 0);
+        if (threadIdx.x == 0) { s_count3 = 0; s_upd = false; }
+        for (uint32_t x = threadIdx.x; x < a.TW; x += kBlock) { sm.cnt[x] = 0u; sm.plo[x] = 0u; sm.phi[x] = 0u; }
+        __syncthreads();
+        phase_mark(a, 1);
+        const uint32_t arrive = i + 1 < nsteps ? i : kNone;
+        const uint32_t d = deliver_tile_plastic(a, t, b, sm, true, &s_count3, &s_upd, arrive);
+        plastic_flush(a, t, b, sm);
+        store_delivered(a, b, d, sm.tmp);
+        __syncthreads();
+        phase_mark(a, 6);
+        if (!s_upd) {
+            update_tile<3>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count3, sm.stage, nullptr, true);
+            if (arrive != kNone && threadIdx.x == 0)
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(a.gbar + (arrive & 3u)) : "memory");
+        }
+        phase_mark(a, 12);
+    }
+}
+
 // Small networks (G = 1, delay 1, one tile of all owned neurons, fits shared memory): one
 // CTA runs nsteps whole steps per launch.  Neuron state and the input counters live in
 // shared memory for the launch; a step is update(t) (the shared update code: bitmap into
@@ -2401,11 +2453,14 @@ cudaError_t launch_fused(const SimArgs &a, uint32_t k, cudaStream_t s) {
 
 // The persistent step kernel (k_synth_run): cooperative launch (every CTA
 // co-resident, which their grid barrier needs; the launch fails instead of deadlocking).
+static size_t run_smem(const SimArgs &a) {
+    return a.model == 3 ? plastic_smem_bytes(a.TW, a.NR) : tile_smem_bytes(a.TW, a.NR, a.prod_words);
+}
 static cudaLaunchConfig_t run_config(const SimArgs &a, cudaStream_t s, cudaLaunchAttribute *at, bool coop) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.NT * a.C);
     cfg.blockDim = dim3(kBlock);
-    cfg.dynamicSmemBytes = tile_smem_bytes(a.TW, a.NR, a.prod_words);
+    cfg.dynamicSmemBytes = run_smem(a);
     cfg.stream = s;
     uint32_t na = 0;
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -2428,11 +2483,13 @@ static cudaLaunchConfig_t run_config(const SimArgs &a, cudaStream_t s, cudaLaunc
     return cfg;
 }
 
-// The persistent kernel of this configuration (nullptr: none): synth with delay 1, G = 1,
-// padded layout.
+// The persistent kernel of this configuration (nullptr: none), G = 1: synth with delay 1
+// (padded layout), Brunel+.
 typedef void (*RunKernel)(SimArgs, uint32_t, uint32_t);
 static RunKernel run_kernel(const SimArgs &a) {
-    if (a.G != 1 || !a.desc) return nullptr;
+    if (a.G != 1) return nullptr;
+    if (a.model == 3 && a.C == 1) return k_plastic_run;  // Brunel+ (delay >= 1 via the rings)
+    if (!a.desc) return nullptr;
     if (a.model == 4) {
         if (a.delay != 1 || a.dly || a.prod_words <= kSynthSid || a.TWs > 32u * 1536u || a.C > kMaxCluster)
             return nullptr;
@@ -2447,7 +2504,7 @@ static RunKernel run_kernel(const SimArgs &a) {
 bool run_supported(const SimArgs &a, int n_sm) {
     const RunKernel kern = run_kernel(a);
     if (!kern) return false;
-    const size_t bytes = tile_smem_bytes(a.TW, a.NR, a.prod_words);
+    const size_t bytes = run_smem(a);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
         cudaGetLastError();
         return false;
