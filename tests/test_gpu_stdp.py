@@ -135,3 +135,35 @@ def test_brunel_plus_teacher_forced_bursts(S):
             c1, p1 = net.input(rel)
             c2, p2 = o.input(rel)
             assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
+
+
+def test_brunel_plus_persistent_kernel_matches_per_step_kernels(S):
+    """The persistent Brunel+ kernel (k_plastic_run: one launch per graph replay, the update
+    warps arrive at the grid barrier once t + 1 is published, spike lists and pre state in
+    copies t mod 3) against one k_fused<3> per step (SPICE_NO_PERSIST=1, read when a network
+    is created): spikes, weights, traces, inputs bit-identical, over replays of 1 .. 256 steps
+    (300 = 256 + 32 + 8 + 4)."""
+    import os
+    cfg, kw, T = _stronger_stdp(W.brunel_plus(3000, 0.1, seed=21)), dict(tile_width=128), 300
+    out = {}
+    for persist in (True, False):
+        if not persist:
+            os.environ["SPICE_NO_PERSIST"] = "1"
+        try:
+            with S.Network(cfg, record_steps=T, **kw) as net:
+                assert (net.launches(32) == 4) == persist          # one persistent launch per replay
+                net.step(T)
+                out[persist] = (net.read_spikes(0, T), net.weights(), net.state(S.FIELD_V),
+                                net.state(S.FIELD_XTR), net.state(S.FIELD_YTR), net.input(0), net.stats())
+        finally:
+            os.environ.pop("SPICE_NO_PERSIST", None)
+    a, b = out[True], out[False]
+    assert all(np.array_equal(a[0][t], b[0][t]) for t in range(T))
+    for x, y in zip(a[1:5], b[1:5]):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a[5][0], b[5][0]) and np.array_equal(a[5][1], b[5][1])
+    assert a[6]["delivered"] == b[6]["delivered"] and a[6]["fired"] == b[6]["fired"]
+    o = O.OracleNet(cfg)
+    o.step(T)
+    assert np.array_equal(a[1], o.weights())
+    assert all(np.array_equal(a[0][t], s) for t, s in enumerate(o.spikes()))
