@@ -236,12 +236,14 @@ __device__ __forceinline__ void phase_mark(const SimArgs &a, int slot, uint32_t 
 #else
     if (a.ptimes && threadIdx.x == who) {
         unsigned long long *p = a.ptimes + blockIdx.x * 16u;
+        // (fire-and-forget reductions: a load-add-store would stall the marking thread for
+        //  a global round trip and distort the next interval)
         if (slot == 0) {
             phase_c0() = clock64();
             unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-            p[14] = g; p[13] += 1;
+            p[14] = g; atomicAdd(p + 13, 1ull);
         } else {
-            p[slot] += (unsigned long long)(clock64() - phase_c0());
+            atomicAdd(p + slot, (unsigned long long)(clock64() - phase_c0()));
             if (slot == 12) { unsigned long long g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); p[15] = g; }
         }
     }
