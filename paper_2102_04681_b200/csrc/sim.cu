@@ -1253,7 +1253,10 @@ constexpr uint32_t kPlChunks = 4096;                  // chunk-start table: pass
 // upd_count != nullptr (fused kernel, delay >= 2, one staging pass): the last kUpdWarps warps
 // run the update of step t + 1 meanwhile (it reads input slot t + 1, complete since delay >= 2,
 // and post state parity t + 1, already staged) and *upd_done is set.
-constexpr uint32_t kUpdWarps = 8;
+#ifndef SPICE_PL_UPD_WARPS
+#define SPICE_PL_UPD_WARPS 4
+#endif
+constexpr uint32_t kUpdWarps = SPICE_PL_UPD_WARPS;   // Brunel+: update warps beside the event warps
 #ifndef SPICE_OVL_UPD_WARPS
 #define SPICE_OVL_UPD_WARPS 8
 #endif
