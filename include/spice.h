@@ -157,8 +157,12 @@ SPICE_API spice_status spice_create_network(const spice_config *cfg, spice_net *
  * slot (t + delay) mod D ("delivered to all neighbors in said row"); Brunel+ applies
  * STDP on the same synapse stream (reading R13).  n_steps is decomposed into
  * replays of captured step graphs of 2^k steps (k <= 8); inside a replay every step but
- * the first is one fused kernel (delivery of t + update of t + 1).  No host round trip;
- * n_steps = 0 is a no-op.  ESTATE on a poisoned or external-exchange handle. */
+ * the first is one fused kernel (delivery of t + update of t + 1) -- for synth (delay 1)
+ * and Brunel+ at G = 1 all of them run in ONE persistent cooperative launch with an
+ * in-kernel grid barrier per step (set SPICE_NO_PERSIST=1 at create time for one kernel
+ * per step).  No host round trip; n_steps = 0 is a no-op.  ESTATE on a poisoned or
+ * external-exchange handle; a grid barrier that does not complete within 10 s (a CTA
+ * never scheduled) is reported as ECUDA by the next synchronising call instead of hanging. */
 SPICE_API spice_status spice_step(spice_net *net, uint64_t n_steps);
 
 /* Copy the spikes of steps [t_begin, t_end) to the host (synchronises the stream): the
@@ -274,8 +278,9 @@ SPICE_API spice_status spice_setup_times(spice_net *net, double *gen_ms, double 
  * on the library stream; writes the average device time per launch in ms:
  * [0] neuron update kernel, [1] delivery kernel, [2] fused deliver(t)+update(t+1) kernel
  * (G = 1; 0 otherwise), [3] exchange (NCCL all-gather + bitmap->list; G > 1), and, when
- * cap >= 5, [4] the fused kernel inside a captured graph of 32 back-to-back launches (the
- * configuration spice_step runs; G = 1, 0 otherwise), timed over n_steps / 32 replays.
+ * cap >= 5, [4] the fused kernel inside a captured graph of 32 back-to-back launches, or
+ * one persistent launch of 32 steps, per step (the configuration spice_step runs; G = 1,
+ * 0 otherwise), timed over n_steps / 32 replays.
  * *n_kernels = entries written (cap >= 4).  Advances the network.  Synchronises. */
 SPICE_API spice_status spice_profile(spice_net *net, uint64_t n_steps, double *ms_per_kernel,
                                      uint32_t cap, uint32_t *n_kernels);
