@@ -18,8 +18,8 @@ SPICE_NO_COOP=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control
 # synth: the persistent kernel (ncu cannot replay cooperative cluster launches: SPICE_NO_COOP=1);
 # launch 2 is the timed region's spice_step(32): 31 steps in one launch
 SPICE_NO_COOP=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_synth_run" -s 1 -c 1 -o gpurun_out/prof_${TAG}_synth python bench.py --workload synth --steps 32 --warmup 5 --profile-steps 2 --e2e-steps 32 --no-cpu-baseline --no-parity > /dev/null 2>&1
-for w in brunel100k brunelplus50k; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_fused" -s 40 -c 1 -o gpurun_out/prof_${TAG}_$w python bench.py --workload $w --steps 64 --warmup 5 --profile-steps 2 --e2e-steps 32 --no-cpu-baseline --no-parity > /dev/null 2>&1
-done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_fused" -s 40 -c 1 -o gpurun_out/prof_${TAG}_brunel100k python bench.py --workload brunel100k --steps 64 --warmup 5 --profile-steps 2 --e2e-steps 32 --no-cpu-baseline --no-parity > /dev/null 2>&1
+# Brunel+: the persistent kernel (launch 2: the timed spice_step(32), 31 steps)
+SPICE_NO_COOP=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_plastic_run" -s 1 -c 1 -o gpurun_out/prof_${TAG}_brunelplus50k python bench.py --workload brunelplus50k --steps 32 --warmup 5 --profile-steps 2 --e2e-steps 32 --no-cpu-baseline --no-parity > /dev/null 2>&1
 WORKLOADS="synth brunel100k brunelplus50k" bash tools/r2_diag.sh > gpurun_out/diag_$TAG.txt 2>&1
 ls gpurun_out | grep $TAG
