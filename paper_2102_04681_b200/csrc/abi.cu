@@ -699,8 +699,25 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
                    tw >= 32 && tw <= kMaxPadTileWord && small_smem_bytes((uint32_t)tw, n->model) <= 227 * 1024 - 2048 &&
                    !getenv("SPICE_NOSMALL");
     }
+    // G > 1 (rows G times shorter: more, shorter segments per spike): 4-CTA cluster tiles,
+    // as many as are co-resident (one wave), when a tile's counters fit shared memory --
+    // half the spike x tile visits of 2-CTA tiles (tools/g_proxy.py, G = 8 rank slice of
+    // the 24e9 network: 53.5 -> 40.9 us/step; G = 4 42.6 -> 36.4; G = 2 35.4 -> 33.2)
+    if (!n->small && !c->tile_width && !c->ctas_per_tile && n->pad8 && n->G > 1 && n->C == 2) {
+        const uint32_t ncl = max_active_clusters(4);
+        if (ncl) {
+            const uint64_t tw4 = ((n->n_own + ncl - 1) / ncl + 127) / 128 * 128;
+            const size_t smem_cap = 227 * 1024 - 2048 - 6 * 1024;
+            if (tw4 <= kMaxPadTileWord && tile_smem_bytes((uint32_t)tw4, 1024, 0) <= smem_cap) {
+                n->C = 4;
+                n->TW = (uint32_t)tw4;
+            }
+        }
+    }
     if (n->small) {
         n->TW = (uint32_t)((n->n_own + 31) / 32 * 32);
+    } else if (n->C == 4 && !c->tile_width && !c->ctas_per_tile && n->G > 1 && n->pad8) {
+        // (set above)
     } else if (c->tile_width) {
         const uint32_t q = 32u * n->C;
         n->TW = (c->tile_width + q - 1) / q * q;

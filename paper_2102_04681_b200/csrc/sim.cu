@@ -2506,6 +2506,30 @@ static RunKernel run_kernel(const SimArgs &a) {
     return nullptr;
 }
 
+// Thread-block clusters of C one-CTA-per-SM step kernels that can be resident at once (the
+// GPC layout decides: 148 CTAs in 2-clusters but 132 in 4-clusters on a B200).
+uint32_t max_active_clusters(uint32_t C) {
+    const size_t bytes = 200 * 1024;                      // (forces one CTA per SM)
+    if (cudaFuncSetAttribute(k_fused<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C * 64);
+    cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = bytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, k_fused<4, 1>, &cfg) != cudaSuccess) { cudaGetLastError(); return 0; }
+    return (uint32_t)ncl;
+}
+
 bool run_supported(const SimArgs &a, int n_sm) {
     const RunKernel kern = run_kernel(a);
     if (!kern) return false;

@@ -22,6 +22,8 @@ cudaError_t launch_advance(uint64_t *t0, uint32_t steps, cudaStream_t s, uint32_
 // launch (a.gbar: grid-barrier slots);
 // supported = the configuration has such a kernel and its whole grid can be co-resident.
 bool run_supported(const SimArgs &a, int n_sm);
+// Clusters of C one-CTA-per-SM step kernels resident at once (0 if unknown).
+uint32_t max_active_clusters(uint32_t C);
 cudaError_t launch_run(const SimArgs &a, uint32_t k, uint32_t nsteps, cudaStream_t s);
 // Recorded bitmaps of nsteps steps -> counts[nsteps] and the packed ascending global IDs.
 cudaError_t launch_compact(const uint32_t *record, uint32_t R, uint64_t words, uint64_t t_begin, uint32_t nsteps,
