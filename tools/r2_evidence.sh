@@ -22,4 +22,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_f
 # Brunel+: the persistent kernel (launch 2: the timed spice_step(32), 31 steps)
 SPICE_NO_COOP=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_plastic_run" -s 1 -c 1 -o gpurun_out/prof_${TAG}_brunelplus50k python bench.py --workload brunelplus50k --steps 32 --warmup 5 --profile-steps 2 --e2e-steps 32 --no-cpu-baseline --no-parity > /dev/null 2>&1
 WORKLOADS="synth brunel100k brunelplus50k" bash tools/r2_diag.sh > gpurun_out/diag_$TAG.txt 2>&1
+for g in 2 4 8; do timeout 300 python tools/g_proxy.py $g 2>&1 | tail -1; done > gpurun_out/gproxy_$TAG.txt
+timeout 1100 python tools/checked_run.py > gpurun_out/checked_$TAG.txt 2>&1
 ls gpurun_out | grep $TAG
