@@ -847,7 +847,7 @@ __device__ __forceinline__ uint64_t synth_descriptors(const SimArgs &a, uint64_t
 }
 
 #ifndef SPICE_FIRE_WARPS
-#define SPICE_FIRE_WARPS 8
+#define SPICE_FIRE_WARPS 9
 #endif
 constexpr uint32_t kFireWarps = SPICE_FIRE_WARPS;   // synth: warps drawing + publishing step t + 1 during delivery
 
