@@ -1245,7 +1245,7 @@ constexpr uint32_t kPlSeg = 1800;                     // segments staged per pas
 // flush-row list capacity (the stage's last 64 words are the overlapped update's scratch)
 constexpr uint32_t kPlFlush = kStageWords - 6 * kPlSeg - 2 - 64;
 #ifndef SPICE_PL_U
-#define SPICE_PL_U 3
+#define SPICE_PL_U 2
 #endif
 constexpr uint32_t kPlU = SPICE_PL_U;                 // events in flight per thread
 constexpr uint32_t kPlChunks = 4096;                  // chunk-start table: passes of <= 2^17 events
