@@ -1258,7 +1258,7 @@ constexpr uint32_t kPlChunks = 4096;                  // chunk-start table: pass
 #endif
 constexpr uint32_t kUpdWarps = SPICE_PL_UPD_WARPS;   // Brunel+: update warps beside the event warps
 #ifndef SPICE_OVL_UPD_WARPS
-#define SPICE_OVL_UPD_WARPS 8
+#define SPICE_OVL_UPD_WARPS 12
 #endif
 constexpr uint32_t kOvlUpdWarps = SPICE_OVL_UPD_WARPS;   // Vogels / Brunel delay >= 2: update warps beside the delivery
 template <int MODEL>
