@@ -138,3 +138,45 @@ def test_brunelplus50k_full_size_free_run(S):
             c2, p2 = o.input(rel)
             assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
         assert net.stats()["delivered"] == int(o.delivered().sum())
+
+
+def test_synth_g2_rank_slices_with_auto_cluster4_tiles(S):
+    """The weak-scaling configuration at G = 2 (1,961,161 neurons, K = 3059, 3.0e9 synapses
+    per rank) as two rank slices in one process, stepped through the G > 1 kernel sequence
+    (exchange, bitmap->list + descriptors, fused delivery + update): the auto geometry must
+    pick 4-CTA cluster tiles (abi.cu), and the union of the ranks' spikes and
+    sampled accumulators must equal the oracle's (the definition: Bernoulli drive, column
+    sums over the in-synapses)."""
+    cfg, G, Sw, T = W.synth_weak(2), 2, 32, 30
+    nets = [S.Network(cfg, rank=g, world_size=G, slice_width=Sw, external_exchange=True, record_steps=T)
+            for g in range(G)]
+    try:
+        for n in nets:
+            assert n.info()["ctas_per_tile"] == 4
+        for n in nets:
+            n.exchange_begin()
+        for t in range(T):
+            for d in nets:
+                for s in nets:
+                    d.exchange_put_from(s)
+            for n in nets:
+                n.exchange_end_fused() if t + 1 < T else n.exchange_end()
+        got = [n.read_spikes(0, T) for n in nets]
+        accs = [n.state(S.FIELD_ACC) for n in nets]
+    finally:
+        for n in nets:
+            n.free()
+    o = O.OracleNet(dataclasses.replace(cfg, rules=()))
+    o.step(T)
+    want = o.spikes()
+    for g in range(G):
+        assert all(np.array_equal(a, b) for a, b in zip(got[g], want)), g
+    counts = np.zeros(cfg.n, dtype=np.int64)
+    for s in want[:T - cfg.delay]:
+        counts[s] += 1
+    rng = np.random.default_rng(5)
+    for g in range(G):
+        for i in list(rng.choice(len(accs[g]), 12, replace=False)) + [0, len(accs[g]) - 1]:
+            j = S.partition_local_to_global(int(i), g, G, Sw)
+            src = O.col(cfg, int(j))
+            assert accs[g][int(i)] == counts[src.astype(np.int64)].sum(), (g, i, j)
