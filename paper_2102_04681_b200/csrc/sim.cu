@@ -642,8 +642,6 @@ __device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32
                                            uint32_t tid = threadIdx.x, uint32_t nth = kBlock) {
     const uint32_t lane = tid & 31;
     const uint32_t span = lo < a.W * 32u ? min(width, a.W * 32u - lo) : 0u;
-    const uint32_t par = lslot(t1);
-    uint32_t *region = a.sl_ids + ((uint64_t)par * a.NR + b) * a.RS;
     const int forced = a.force_ctl[0] == t1 ? (int)a.force_ctl[1] : 0;
     for (uint32_t x0 = 0; x0 < span; x0 += 4u * nth) {
         if (x0 + 4u * (tid & ~31u) >= span) continue;            // whole warp past the slice
@@ -692,11 +690,9 @@ __device__ __forceinline__ void synth_fire(const SimArgs &a, uint64_t t1, uint32
             uint32_t pos = base + __popc(m[0] & lt) + __popc(m[1] & lt) + __popc(m[2] & lt) + __popc(m[3] & lt);
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-                if ((nib >> e) & 1u) {
-                    SPICE_CHECK(pos < a.RS);             // (the region holds the CTA's slice)
-                    region[pos] = lo + x4 + e;
-                    if (pos < sid_cap) sid_s[pos] = lo + x4 + e;
-                    ++pos;
+                if ((nib >> e) & 1u) {                   // (shared list only: the global
+                    if (pos < sid_cap) sid_s[pos] = lo + x4 + e;   //  region is written by synth_publish
+                    ++pos;                               //  when the list overflows, else unused)
                 }
         }
     }
