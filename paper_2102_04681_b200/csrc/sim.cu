@@ -818,8 +818,9 @@ __device__ __forceinline__ uint64_t synth_descriptors(const SimArgs &a, uint64_t
     asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
     phase_mark(a, 6, threadIdx.x - ptid);            // (diagnostics: rows staged)
     uint64_t dsum = 0;
-    if (warp == 0)
-        for (uint32_t ql = lane; ql < n; ql += 32) { region_rows[ql] = srow[ql]; dsum += sdeg[ql]; }
+    if (warp == 0)                                   // (the list's row starts are not needed on
+        for (uint32_t ql = lane; ql < n; ql += 32) dsum += sdeg[ql];   //  the descriptor path)
+    (void)region_rows;
     const uint32_t dbuf = (uint32_t)mod32(t1, 3);
     SPICE_CHECK((uint64_t)off + n <= a.dstride);
     for (uint32_t j0 = 0; j0 < n; j0 += 32) {
