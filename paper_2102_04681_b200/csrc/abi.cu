@@ -954,8 +954,8 @@ spice_status spice_create_network(const spice_config *c, spice_net **out) {
     // (SPICE_NO_PERSIST=1: one fused kernel per step, the A/B baseline)
     if (n->G == 1 && n->fused && !n->global_atomics && !n->small && !n->procedural && !getenv("SPICE_NO_PERSIST") &&
         run_supported(a, n->n_sm)) {
-        if ((st = dalloc_t(n, &n->gbar, 5, "grid barrier"))) return bail(st);
-        CU(n, cudaMemset(n->gbar, 0, 20));
+        if ((st = dalloc_t(n, &n->gbar, 10, "grid barrier"))) return bail(st);   // 4 x u64 slots + flag
+        CU(n, cudaMemset(n->gbar, 0, 40));
         a.gbar = n->gbar;
         a.persist = 1;
     }
@@ -1056,7 +1056,7 @@ constexpr uint32_t kPeerMagic = 0x45435053u;   // "SPCE"
 spice_status check_xerr(spice_net *n) {
     uint32_t e = 0;
     if (n->gbar) {                                 // (and the persistent kernel's grid barrier)
-        CU(n, cudaMemcpy(&e, n->gbar + 4, 4, cudaMemcpyDeviceToHost));
+        CU(n, cudaMemcpy(&e, n->gbar + 8, 4, cudaMemcpyDeviceToHost));
         if (e) return fail(n, SPICE_ECUDA, "persistent step kernel: a grid barrier did not complete within 10 s");
     }
     if (!n->xerr) return SPICE_OK;

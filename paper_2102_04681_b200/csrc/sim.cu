@@ -1261,6 +1261,7 @@ constexpr uint32_t kOvlUpdWarps = SPICE_OVL_UPD_WARPS;   // Vogels / Brunel dela
 template <int MODEL>
 __device__ __forceinline__ void update_tile_sub(const SimArgs &a, uint64_t t, uint32_t b, uint32_t lo, uint32_t width,
                                                 uint32_t *s_count, uint32_t *stage, uint32_t ptid, uint32_t pth);
+__device__ __forceinline__ void grid_arrive_add(const SimArgs &a, uint32_t i, uint32_t payload);   // (below)
 // arrive != kNone (persistent kernel): once the overlapped update of t + 1 and the pre state
 // for t + 1 are written, the update warps arrive at grid barrier `arrive` ("t + 1 published")
 __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint64_t t, uint32_t b,
@@ -1378,7 +1379,7 @@ __device__ __forceinline__ uint32_t deliver_tile_plastic(const SimArgs &a, uint6
                 if (arrive != kNone) {
                     asm volatile("bar.sync 1, %0;" :: "r"(kUpdWarps * 32) : "memory");
                     if (tid == eth)
-                        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(a.gbar + (arrive & 3u)) : "memory");
+                        grid_arrive_add(a, arrive, 0u);
                 }
                 if (marks) phase_mark(a, 8, eth);
                 continue;                         // (nseg <= kPlSeg: this was the only pass)
@@ -1846,28 +1847,40 @@ __global__ void __launch_bounds__(kBlock) k_fused(SimArgs a, uint32_t k) {
 // an acquire spin until all gridDim.x arrived); CTA 0 clears slot (i + 2) mod 4 once past
 // barrier i (its last users passed barrier i - 2 before anyone could arrive at i - 1),
 // k_advance clears all four after the launch.  A barrier not complete within ~10 s (a CTA
-// that never got scheduled) sets gbar[4] and every CTA falls through the remaining
+// that never got scheduled) sets gbar[8] and every CTA falls through the remaining
 // barriers: the host reports an error instead of hanging the GPU.
-__device__ __forceinline__ void grid_wait(const SimArgs &a, uint32_t i) {
+// (slot i: a 64-bit word at gbar + 2 (i mod 4) -- arrivals in the low half, a payload the
+//  arrivals add in the high half: the synth kernel's descriptor count of the next step)
+__device__ __forceinline__ unsigned long long *gbar_slot(const SimArgs &a, uint32_t i) {
+    return reinterpret_cast<unsigned long long *>(a.gbar) + (i & 3u);
+}
+__device__ __forceinline__ void grid_arrive_add(const SimArgs &a, uint32_t i, uint32_t payload) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;"
+                 :: "l"(gbar_slot(a, i)), "l"(((unsigned long long)payload << 32) | 1ull) : "memory");
+}
+// Thread 0 waits; returns the payload sum (valid in thread 0).
+__device__ __forceinline__ uint32_t grid_wait(const SimArgs &a, uint32_t i) {
+    uint32_t payload = 0;
     if (threadIdx.x == 0) {
-        const uint32_t *slot = a.gbar + (i & 3u);
+        const unsigned long long *slot = gbar_slot(a, i);
         unsigned long long t_start;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         for (uint32_t spin = 0;; ++spin) {
-            uint32_t v;
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(slot) : "memory");
-            if (v >= gridDim.x) break;
+            unsigned long long v;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(slot) : "memory");
+            if ((uint32_t)v >= gridDim.x) { payload = (uint32_t)(v >> 32); break; }
             if ((spin & 255u) == 255u) {
-                if (*(volatile uint32_t *)(a.gbar + 4)) break;
+                if (*(volatile uint32_t *)(a.gbar + 8)) break;
                 unsigned long long now;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-                if (now - t_start > 10000000000ull) { atomicExch(a.gbar + 4, 1u); break; }
+                if (now - t_start > 10000000000ull) { atomicExch(a.gbar + 8, 1u); break; }
             }
         }
-        __threadfence();
-        if (blockIdx.x == 0) a.gbar[(i + 2u) & 3u] = 0u;
+        __threadfence();                              // (also drops stale L1 lines of this SM)
+        if (blockIdx.x == 0) *gbar_slot(a, i + 2u) = 0ull;
     }
     __syncthreads();
+    return payload;
 }
 
 // nsteps consecutive synth steps k .. k + nsteps - 1 in ONE launch (each: deliver t + the
@@ -1902,9 +1915,11 @@ __global__ void __launch_bounds__(kBlock) k_synth_run(SimArgs a, uint32_t k, uin
     asm volatile("griddepcontrol.wait;" ::: "memory");          // the replay's first update is complete
     for (uint32_t i = 0; i < nsteps; ++i) {
         const uint64_t t = *a.t0 + k + i;
-        if (i) grid_wait(a, i - 1);
+        // the step's descriptor count: the barrier word's payload (no extra round trip), or,
+        // for the launch's first step (published by k_update), the step counter
+        const uint32_t wsum = i ? grid_wait(a, i - 1) : 0u;
         phase_mark(a, 0);
-        const uint32_t pre_total = threadIdx.x == 0 ? a.dcount[t & 3u] : 0xFFFFFFFFu;
+        const uint32_t pre_total = threadIdx.x == 0 ? (i ? wsum : a.dcount[t & 3u]) : 0xFFFFFFFFu;
         if (threadIdx.x == 0) s_count = 0;
         const uint32_t n_sp = delivery_count(a, t, bt, c, pre_total);   // (block-wide)
         phase_mark(a, 1);
@@ -1927,8 +1942,8 @@ __global__ void __launch_bounds__(kBlock) k_synth_run(SimArgs a, uint32_t k, uin
             // only the descriptors of t + 1 and this CTA's own counters, never cleared here)
             asm volatile("bar.sync 1, %0;" :: "r"(pth) : "memory");
             phase_mark(a, 8, NWD * 32);
-            if (ptid == 0 && i + 1 < nsteps)
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(a.gbar + (i & 3u)) : "memory");
+            if (ptid == 0 && i + 1 < nsteps)            // (+ this CTA's descriptors of t + 1)
+                grid_arrive_add(a, i, s_count);
             phase_mark(a, 9, NWD * 32);
         }
         phase_mark(a, 4);
@@ -1975,7 +1990,7 @@ __global__ void __launch_bounds__(kBlock) k_plastic_run(SimArgs a, uint32_t k, u
         if (!s_upd) {
             update_tile<3>(a, t + 1, b, b * a.TW, a.TW, nullptr, true, &s_count3, sm.stage, nullptr, true);
             if (arrive != kNone && threadIdx.x == 0)
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(a.gbar + (arrive & 3u)) : "memory");
+                grid_arrive_add(a, arrive, 0u);
         }
         phase_mark(a, 12);
     }
@@ -2285,7 +2300,8 @@ __global__ void __launch_bounds__(kBlock) k_b2l(SimArgs a, uint32_t k) {
 
 __global__ void k_advance(uint64_t *t0, uint32_t steps, uint32_t *gbar) {
     *t0 += steps;
-    if (gbar) { gbar[0] = 0u; gbar[1] = 0u; gbar[2] = 0u; gbar[3] = 0u; }   // (persistent launches)
+    if (gbar)                                        // (persistent launches: four 64-bit slots)
+        for (int q = 0; q < 8; ++q) gbar[q] = 0u;
 }
 
 // PEER exchange (device-initiated): after the kernel that

@@ -122,8 +122,9 @@ struct SimArgs {
     uint32_t pdl;            // 1: fused step kernels use programmatic dependent launch
     uint64_t nnz;            // stored entries (incl. padding sentinels): bounds of ent / w / dly
     uint32_t persist;        // 1: the steps of a replay in one persistent launch (k_synth_run)
-    uint32_t *gbar;          // [5] its grid-barrier arrival slots (barrier i of a launch: slot
-                             // i mod 4; zero between launches) and a timeout flag
+    uint32_t *gbar;          // [10] its grid-barrier slots (barrier i of a launch: 64-bit word
+                             // i mod 4, arrivals low / payload high; zero between launches)
+                             // and a timeout flag at [8]
     uint32_t pl_split;       // Brunel+: plastic fixed point q summed as (q mod 2^16) and
                              // (q >> 16) in two u32 words (no carry round trip; abi.cu proves
                              // neither sum can wrap), else low word + carry into the high word
